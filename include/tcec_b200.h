@@ -1,0 +1,188 @@
+/*
+ * tcec_b200.h -- C-ABI boundary of the B200-native TCEC tensor-network path.
+ *
+ * One shared library, paper_2303_08989_b200/libtcec_b200.so (sm_100a CUDA
+ * kernels + the C++ host orchestration), exports exactly these symbols.  They
+ * replace the reference mpsgemm entry points (/root/reference/proj/include/
+ * mpsgemm/*.hpp) for the north-star path; each declaration cites the interface
+ * it replaces.  Plain pointers and sizes only: "device" buffers are CUDA device
+ * pointers (e.g. from torch or cudaMalloc); "host" buffers are ordinary memory.
+ * Complex data is interleaved (re, im) float32, row-major, exactly the layout
+ * of Matrix<std::complex<float>> (matrix.hpp:11-35) and Tensor (tensor.hpp:16-53).
+ *
+ * Errors: every function returns a tcec_status (0 = OK).  The codes map 1:1
+ * onto the reference exception taxonomy (common.hpp:9-41) and
+ * tcec_last_error() returns the message (same prefixes as the reference).
+ * There is no CPU fallback: on a machine without an sm_100 GPU every compute
+ * entry point fails with TCEC_ERR_CUDA.
+ *
+ * Threading: a handle owns its stream, workspace and decision buffers; use one
+ * handle per host thread (reference functions are reentrant, precsel.hpp:105-123).
+ */
+#ifndef TCEC_B200_H
+#define TCEC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------- status */
+typedef enum {
+    TCEC_OK = 0,
+    TCEC_ERR_SHAPE_MISMATCH = 1,      /* ShapeMismatch        common.hpp:10 */
+    TCEC_ERR_ZERO_REFERENCE = 2,      /* ZeroReference        common.hpp:13 */
+    TCEC_ERR_SCALE_OVERFLOW = 3,      /* ScaleOverflow        common.hpp:18 */
+    TCEC_ERR_INVALID_PERMUTATION = 4, /* InvalidPermutation   common.hpp:23 */
+    TCEC_ERR_EXTENT_MISMATCH = 5,     /* ExtentMismatch       common.hpp:26 */
+    TCEC_ERR_INVALID_PATH = 6,        /* InvalidPath          common.hpp:29 */
+    TCEC_ERR_DISCONNECTED = 7,        /* DisconnectedNetwork  common.hpp:32 */
+    TCEC_ERR_INVALID_ARGUMENT = 8,    /* std::invalid_argument (gemm.cpp:19, k_tile < 1) */
+    TCEC_ERR_LOGIC = 9,               /* std::logic_error (precsel.cpp:117-118) */
+    TCEC_ERR_CUDA = 10,               /* device / driver failure (no fallback) */
+    TCEC_ERR_TOO_MANY_QUBITS = 11     /* TooManyQubits        common.hpp:39 */
+} tcec_status;
+
+typedef struct tcec_handle_s* tcec_handle;
+
+/* message of the last failure on this thread ("" if none) */
+const char* tcec_last_error(void);
+/* library build string (arch, kernel variants) */
+const char* tcec_version(void);
+
+/* create a handle bound to a CUDA device; it owns a non-blocking stream */
+int tcec_create(int device, tcec_handle* out);
+int tcec_destroy(tcec_handle h);
+/* run subsequent work on a caller stream (cudaStream_t; NULL = the handle's own) */
+int tcec_set_stream(tcec_handle h, void* stream);
+void* tcec_get_stream(tcec_handle h);
+int tcec_synchronize(tcec_handle h);
+/* RN flush interval of the TCEC main term in k-blocks of 64 (f16) / 32 (tf32)
+ * elements; 0 = accumulate the whole K inside the tensor core.  This is the
+ * device counterpart of TilingConfig::k_tile (gemm.hpp:28-30). */
+int tcec_set_flush_kblocks(tcec_handle h, int kblocks);
+int tcec_get_flush_kblocks(tcec_handle h);
+
+/* ------------------------------------------------ format emulation (device)
+ * KernelTable entries, kernels.hpp:20-63; bit-identical to the reference
+ * scalar table.  fmt: 0 = FP16, 1 = TF32 (lowprec.hpp:15); rounding: 0 = RN,
+ * 1 = RZ (lowprec.hpp:13).  *overflow (host, may be NULL) is OR-accumulated. */
+int tcec_quantize_buf(tcec_handle h, const float* src, float* dst, int64_t n, int fmt,
+                      int rounding, int* overflow);
+int tcec_split_buf(tcec_handle h, const float* src, float* hi, float* lo, int64_t n, int fmt,
+                   int* overflow);
+int tcec_scale_buf(tcec_handle h, const float* src, float* dst, int64_t n, int scale_exp);
+int tcec_add_buf(tcec_handle h, const float* a, const float* b, float* dst, int64_t n);
+int tcec_sub_buf(tcec_handle h, const float* a, const float* b, float* dst, int64_t n);
+
+/* ------------------------------------------------- precision selection */
+/* ExpStats, precsel.hpp:18-36 (e_max_valid == 0 <=> std::nullopt) */
+typedef struct {
+    uint64_t n1, n2;
+    int32_t e_max;
+    int32_t e_max_valid;
+    uint64_t n_nonzero, n_total;
+    int32_t stage2_evaluated;
+    int32_t pad_;
+} tcec_exp_stats_t;
+
+/* exp_stats (precsel.hpp:68) when staged == 0, exp_stats_staged (precsel.hpp:70)
+ * when staged != 0; x is a device rows x cols complex matrix */
+int tcec_exp_stats(tcec_handle h, const void* x, int64_t rows, int64_t cols, int target_max_exponent,
+                   int staged, double t, tcec_exp_stats_t* out);
+double tcec_r1(const tcec_exp_stats_t* s); /* precsel.hpp:27-30 */
+double tcec_r2(const tcec_exp_stats_t* s); /* precsel.hpp:32-35 */
+/* matrix_tolerance, precsel.hpp:74; *level = ToleranceLevel (0 tf32_only,
+ * 1 fp16_scaled_ok, 2 fp16_ok); TCEC_ERR_LOGIC when stage 2 was needed but skipped */
+int tcec_matrix_tolerance(const tcec_exp_stats_t* s, double t, int target_max_exponent, int* level);
+/* select_mode, precsel.hpp:76-77; kind = ComputeKind (0 FP16TCEC, 1 FP16TCEC_SCALED,
+ * 2 TF32TCEC, 3 FP32_BASELINE) */
+int tcec_select_mode(int level_a, int e_max_valid_a, int e_max_a, int level_b, int e_max_valid_b,
+                     int e_max_b, int target_max_exponent, int* kind, int* scale_a, int* scale_b);
+/* scale_matrix_inplace (precsel.hpp:82-85) on n components; ScaleOverflow when
+ * a result leaves the finite range (check != 0) -- descale_output uses check = 0 */
+int tcec_scale_components(tcec_handle h, float* x, int64_t n, int scale_exp, int check);
+
+/* ------------------------------------------------------------- CGEMM */
+/* GemmMode, gemm.hpp:19 */
+enum { TCEC_FP32_REF = 0, TCEC_FP64_ORACLE = 1, TCEC_TF32_TC = 2, TCEC_FP16_TC = 3,
+       TCEC_TF32_TCEC = 4, TCEC_FP16_TCEC = 5 };
+/* ForcedMode, precsel.hpp:128-136 (force = -1: automatic selection) */
+enum { TCEC_FORCE_NONE = -1, TCEC_FORCE_FP32_REF = 0, TCEC_FORCE_FP64_ORACLE = 1,
+       TCEC_FORCE_TF32_TC = 2, TCEC_FORCE_FP16_TC = 3, TCEC_FORCE_TF32_TCEC = 4,
+       TCEC_FORCE_FP16_TCEC = 5, TCEC_FORCE_FP16_TCEC_SCALED = 6 };
+
+/* cgemm, cgemm.hpp:17-18 -- device a (m x k), b (k x n), c (m x n) complex.
+ * FP32_REF and FP64_ORACLE are bit-identical to the reference; the tensor-core
+ * modes are within the FP32-level tolerance. */
+int tcec_cgemm(tcec_handle h, const void* a, const void* b, void* c, int64_t m, int64_t n,
+               int64_t k, int mode, int k_tile, int* overflow);
+
+/* SelectionPolicy + TilingConfig + ForcedMode = DispatchConfig, precsel.hpp:60-65,140-144 */
+typedef struct {
+    double threshold_t;
+    int64_t size_auto;
+    int64_t size_tf32;
+    int32_t target_max_exponent;
+    int32_t k_tile;
+    int32_t force;
+    int32_t pad_;
+} tcec_dispatch_config_t;
+
+/* DispatchResult + DecisionRecord, precsel.hpp:92-101,146-151 */
+typedef struct {
+    int32_t kind, scale_a, scale_b, overflow;
+    int32_t has_stats, pad_;
+    tcec_exp_stats_t stats_a, stats_b;
+    char line[160]; /* DecisionRecord::to_line(), precsel.cpp:185-205 */
+} tcec_dispatch_result_t;
+
+void tcec_default_config(tcec_dispatch_config_t* cfg);
+/* dispatch_cgemm, precsel.hpp:153-156 -- device buffers; the statistics and the
+ * decision are computed on the device; *res (host) is filled after the call
+ * completes (the call synchronizes the handle stream). */
+int tcec_dispatch_cgemm(tcec_handle h, const void* a, const void* b, void* c, int64_t m, int64_t n,
+                        int64_t k, const tcec_dispatch_config_t* cfg, tcec_dispatch_result_t* res);
+/* same with HOST buffers: H2D copy of A and B, dispatch, D2H copy of C */
+int tcec_dispatch_cgemm_host(tcec_handle h, const void* a, const void* b, void* c, int64_t m,
+                             int64_t n, int64_t k, const tcec_dispatch_config_t* cfg,
+                             tcec_dispatch_result_t* res);
+
+/* ------------------------------------------------------------ permute */
+/* permute, tensor.hpp:56-105: dst = src transposed so that new axis a is old
+ * axis axis_of[a]; old_dims are the source extents; complex elements; device */
+int tcec_permute(tcec_handle h, const void* src, void* dst, int rank, const int64_t* old_dims,
+                 const int* axis_of);
+
+/* ------------------------------------------------ network contraction */
+typedef struct tcec_network_s* tcec_network;
+
+/* TensorNetwork (network.hpp:17-19) with integer labels.  Node i has ranks[i]
+ * axes whose labels/dims are the next ranks[i] entries of labels/dims. */
+int tcec_network_create(tcec_handle h, int n_nodes, const int* ranks, const int* labels,
+                        const int64_t* dims, tcec_network* out);
+int tcec_network_destroy(tcec_network net);
+/* copy node data (host, complex, row-major in label order) */
+int tcec_network_set_node(tcec_network net, int node, const void* host_data);
+/* greedy_path, network.hpp:49 -- writes 2 * (n_nodes - 1) ints */
+int tcec_network_greedy_path(tcec_network net, int* steps);
+/* contract_network, network.hpp:37-38 -- path as (a, b) id pairs in SSA
+ * numbering (network.hpp:22-26).  The result tensor (host) has the labels
+ * written to out_labels (may be NULL) and rank to *out_rank.  When log_lines is
+ * non-NULL the decision-log lines ('\n'-separated) are written there. */
+int tcec_contract_network(tcec_network net, const int* steps, int n_steps,
+                          const tcec_dispatch_config_t* cfg, void* out_host, int64_t out_capacity,
+                          int* out_rank, int* out_labels, char* log_lines, int64_t log_capacity);
+/* amplitude batch (qcircuit.hpp:49-52 over many bitstrings): the network's
+ * closing selector nodes (one per entry of sel_nodes) are replaced per
+ * bitstring; the same plan is replayed; out_host gets one complex per string */
+int tcec_contract_selector_batch(tcec_network net, const int* steps, int n_steps,
+                                 const tcec_dispatch_config_t* cfg, int n_sel, const int* sel_nodes,
+                                 int n_strings, const uint8_t* bits, void* out_host);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TCEC_B200_H */

@@ -1,0 +1,254 @@
+"""Python host mirror of the reference mpsgemm API over the C-ABI.
+
+Names, argument meaning and error behaviour follow /root/reference/proj/include/
+mpsgemm/*.hpp so the parity tests read like the reference's own tests.  Device
+data lives in torch CUDA tensors (torch is plumbing here: allocation, streams,
+H2D/D2H); every computation runs in libtcec_b200.so.
+
+    h = Handle()                     # one handle per thread (owns stream + workspace)
+    c, res = h.dispatch_cgemm(a, b, DispatchConfig(...))   # precsel.hpp:153-156
+    c, ovf = h.cgemm(a, b, "FP16TCEC")                     # cgemm.hpp:17-18
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import DispatchConfig as _CConfig
+from ._lib import DispatchResult, ExpStats, check
+
+GEMM_MODES = {"FP32_REF": 0, "FP64_ORACLE": 1, "TF32TC": 2, "FP16TC": 3, "TF32TCEC": 4,
+              "FP16TCEC": 5}
+FORCED_MODES = {"FP32_REF": 0, "FP64_ORACLE": 1, "TF32TC": 2, "FP16TC": 3, "TF32TCEC": 4,
+                "FP16TCEC": 5, "FP16TCEC_SCALED": 6}
+KINDS = ["FP16TCEC", "FP16TCEC_SCALED", "TF32TCEC", "FP32_BASELINE"]
+LEVELS = ["tf32_only", "fp16_scaled_ok", "fp16_ok"]
+
+
+@dataclass
+class SelectionPolicy:
+    """precsel.hpp:60-65"""
+    threshold_t: float = 0.0
+    size_auto: int = 2048
+    size_tf32: int = 512
+    target_max_exponent: int = 14
+
+
+def make_config(policy: SelectionPolicy | None = None, k_tile: int = 16,
+                force: str | int | None = None) -> _CConfig:
+    """DispatchConfig{policy, tiling, force} (precsel.hpp:140-144)."""
+    p = policy or SelectionPolicy()
+    f = -1 if force is None else (FORCED_MODES[force] if isinstance(force, str) else int(force))
+    return _CConfig(float(p.threshold_t), int(p.size_auto), int(p.size_tf32),
+                    int(p.target_max_exponent), int(k_tile), f, 0)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _ptr(t) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr())
+
+
+class Handle:
+    """tcec_handle: stream, workspace and device decision buffers of one thread."""
+
+    def __init__(self, device: int = 0, stream=None):
+        self.lib = _lib.load()
+        self.device = device
+        h = C.c_void_p()
+        check(self.lib.tcec_create(device, C.byref(h)))
+        self.h = h
+        if stream is not None:
+            self.set_stream(stream)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.tcec_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------- control
+    def set_stream(self, stream) -> None:
+        ptr = stream if isinstance(stream, int) else (stream.cuda_stream if stream is not None else 0)
+        check(self.lib.tcec_set_stream(self.h, C.c_void_p(ptr)))
+
+    @property
+    def stream_ptr(self) -> int:
+        return self.lib.tcec_get_stream(self.h) or 0
+
+    def synchronize(self) -> None:
+        check(self.lib.tcec_synchronize(self.h))
+
+    @property
+    def flush_kblocks(self) -> int:
+        return self.lib.tcec_get_flush_kblocks(self.h)
+
+    @flush_kblocks.setter
+    def flush_kblocks(self, v: int) -> None:
+        check(self.lib.tcec_set_flush_kblocks(self.h, int(v)))
+
+    # ------------------------------------------------------ KernelTable level
+    def _out_like(self, x):
+        return _torch().empty_like(x)
+
+    def quantize_buf(self, x, fmt: int, rounding: int = 0):
+        y = self._out_like(x)
+        ovf = C.c_int(0)
+        check(self.lib.tcec_quantize_buf(self.h, _ptr(x), _ptr(y), x.numel(), fmt, rounding,
+                                         C.byref(ovf)))
+        return y, bool(ovf.value)
+
+    def split_buf(self, x, fmt: int):
+        hi, lo = self._out_like(x), self._out_like(x)
+        ovf = C.c_int(0)
+        check(self.lib.tcec_split_buf(self.h, _ptr(x), _ptr(hi), _ptr(lo), x.numel(), fmt,
+                                      C.byref(ovf)))
+        return hi, lo, bool(ovf.value)
+
+    def scale_buf(self, x, scale_exp: int):
+        y = self._out_like(x)
+        check(self.lib.tcec_scale_buf(self.h, _ptr(x), _ptr(y), x.numel(), int(scale_exp)))
+        return y
+
+    def add_buf(self, a, b):
+        y = self._out_like(a)
+        check(self.lib.tcec_add_buf(self.h, _ptr(a), _ptr(b), _ptr(y), a.numel()))
+        return y
+
+    def sub_buf(self, a, b):
+        y = self._out_like(a)
+        check(self.lib.tcec_sub_buf(self.h, _ptr(a), _ptr(b), _ptr(y), a.numel()))
+        return y
+
+    # ------------------------------------------------------------- precsel
+    def exp_stats(self, m, target_max_exponent: int = 14) -> ExpStats:
+        """exp_stats (precsel.hpp:68): both stages unconditionally."""
+        out = ExpStats()
+        rows, cols = (m.shape if m.dim() == 2 else (1, m.numel()))
+        check(self.lib.tcec_exp_stats(self.h, _ptr(m), rows, cols, target_max_exponent, 0, 0.0,
+                                      C.byref(out)))
+        return out
+
+    def exp_stats_staged(self, m, target_max_exponent: int, t: float) -> ExpStats:
+        """exp_stats_staged (precsel.hpp:70)."""
+        out = ExpStats()
+        rows, cols = (m.shape if m.dim() == 2 else (1, m.numel()))
+        check(self.lib.tcec_exp_stats(self.h, _ptr(m), rows, cols, target_max_exponent, 1,
+                                      float(t), C.byref(out)))
+        return out
+
+    def scale_matrix_inplace(self, m, scale_exp: int) -> None:
+        """scale_matrix_inplace (precsel.hpp:82): ScaleOverflow on nonfinite."""
+        x = m.view(_torch().float32)
+        check(self.lib.tcec_scale_components(self.h, _ptr(x), x.numel(), int(scale_exp), 1))
+
+    def scale_matrix(self, m, scale_exp: int):
+        out = m.clone()
+        self.scale_matrix_inplace(out, scale_exp)
+        return out
+
+    def descale_output_inplace(self, c, scale_exp_a: int, scale_exp_b: int) -> None:
+        """descale_output_inplace (precsel.hpp:88): no overflow check."""
+        x = c.view(_torch().float32)
+        check(self.lib.tcec_scale_components(self.h, _ptr(x), x.numel(),
+                                             -(int(scale_exp_a) + int(scale_exp_b)), 0))
+
+    # --------------------------------------------------------------- CGEMM
+    def _shapes(self, a, b):
+        if a.dim() != 2 or b.dim() != 2:
+            raise _lib.ShapeMismatch(1, "operands must be matrices")
+        m, k = a.shape
+        k2, n = b.shape
+        if k != k2:
+            raise _lib.ShapeMismatch(1, "cgemm: inner dimensions differ")
+        return m, n, k
+
+    def cgemm(self, a, b, mode: str | int, k_tile: int = 16, out=None):
+        """cgemm (cgemm.hpp:17-18); returns (C, overflow)."""
+        m, n, k = self._shapes(a, b)
+        c = out if out is not None else _torch().empty((m, n), dtype=_torch().complex64,
+                                                       device=a.device)
+        md = GEMM_MODES[mode] if isinstance(mode, str) else int(mode)
+        ovf = C.c_int(0)
+        check(self.lib.tcec_cgemm(self.h, _ptr(a), _ptr(b), _ptr(c), m, n, k, md, int(k_tile),
+                                  C.byref(ovf)))
+        return c, bool(ovf.value)
+
+    def cgemm_batched(self, pairs, mode, k_tile: int = 16):
+        """cgemm_batched (cgemm.hpp:21-23): errors carry the batch index."""
+        out = []
+        for i, (a, b) in enumerate(pairs):
+            try:
+                out.append(self.cgemm(a, b, mode, k_tile)[0])
+            except _lib.ShapeMismatch as e:
+                raise _lib.ShapeMismatch(1, f"batch entry {i}: {e.msg}") from None
+        return out
+
+    def dispatch_cgemm(self, a, b, config: _CConfig | SelectionPolicy | None = None, out=None):
+        """dispatch_cgemm (precsel.hpp:153-156); returns (C, DispatchResult)."""
+        if config is None or isinstance(config, SelectionPolicy):
+            config = make_config(config)
+        m, n, k = self._shapes(a, b)
+        c = out if out is not None else _torch().empty((m, n), dtype=_torch().complex64,
+                                                       device=a.device)
+        res = DispatchResult()
+        check(self.lib.tcec_dispatch_cgemm(self.h, _ptr(a), _ptr(b), _ptr(c), m, n, k,
+                                           C.byref(config), C.byref(res)))
+        return c, res
+
+    def dispatch_cgemm_host(self, a: np.ndarray, b: np.ndarray, config=None, out=None):
+        """The same with HOST numpy buffers (H2D / D2H inside the call)."""
+        if config is None or isinstance(config, SelectionPolicy):
+            config = make_config(config)
+        a = np.ascontiguousarray(a, dtype=np.complex64)
+        b = np.ascontiguousarray(b, dtype=np.complex64)
+        m, k = a.shape
+        n = b.shape[1]
+        c = out if out is not None else np.empty((m, n), dtype=np.complex64)
+        res = DispatchResult()
+        check(self.lib.tcec_dispatch_cgemm_host(self.h, a.ctypes.data_as(C.c_void_p),
+                                                b.ctypes.data_as(C.c_void_p),
+                                                c.ctypes.data_as(C.c_void_p), m, n, k,
+                                                C.byref(config), C.byref(res)))
+        return c, res
+
+    # ------------------------------------------------------------- permute
+    def permute(self, t, axis_of):
+        """permute (tensor.hpp:56-57): new axis a is old axis axis_of[a]."""
+        r = t.dim()
+        if len(axis_of) != r:
+            raise _lib.InvalidPermutation(4, "permutation has wrong length")
+        out = _torch().empty(tuple(t.shape[a] for a in axis_of), dtype=t.dtype, device=t.device)
+        dims = (C.c_int64 * max(r, 1))(*t.shape)
+        ax = (C.c_int * max(r, 1))(*axis_of)
+        check(self.lib.tcec_permute(self.h, _ptr(t), _ptr(out), r, dims, ax))
+        return out
+
+
+def matrix_tolerance(stats: ExpStats, t: float, target_max_exponent: int = 14) -> int:
+    """matrix_tolerance (precsel.hpp:74): returns the ToleranceLevel index."""
+    lib = _lib.load()
+    lvl = C.c_int(0)
+    check(lib.tcec_matrix_tolerance(C.byref(stats), float(t), target_max_exponent, C.byref(lvl)))
+    return lvl.value
+
+
+def select_mode(level_a: int, e_max_a, level_b: int, e_max_b, target_max_exponent: int = 14):
+    """select_mode (precsel.hpp:76-77): returns (kind name, scale_a, scale_b)."""
+    lib = _lib.load()
+    k, sa, sb = C.c_int(0), C.c_int(0), C.c_int(0)
+    check(lib.tcec_select_mode(level_a, e_max_a is not None, e_max_a or 0, level_b,
+                               e_max_b is not None, e_max_b or 0, target_max_exponent,
+                               C.byref(k), C.byref(sa), C.byref(sb)))
+    return KINDS[k.value], sa.value, sb.value

@@ -1,0 +1,620 @@
+// C-ABI core: handles, errors, the KernelTable entry points, exponent
+// statistics / selection, and the CGEMM dispatcher (host orchestration of the
+// device pipeline).  Mirrors reference precsel.cpp:225-322 (dispatch_cgemm),
+// cgemm.cpp:25-46 (cgemm) and gemm.cpp:60-125 (mode switch).
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/tcec_b200.h"
+#include "tcec_handle.h"
+
+namespace tcec {
+
+thread_local std::string g_last_error;
+
+int set_error(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int cuda_error(cudaError_t e, const char* what) {
+    return set_error(TCEC_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------ shared helpers
+
+void stats_from_dev(const DevStats& d, int64_t n_total, tcec_exp_stats_t* s) {
+    std::memset(s, 0, sizeof(*s));
+    s->n1 = d.n1;
+    s->n2 = d.n2;
+    s->e_max_valid = d.max_bits != 0;
+    s->e_max = d.max_bits ? exponent_of_bits_host(d.max_bits) : 0;
+    s->n_nonzero = d.n_nonzero;
+    s->n_total = uint64_t(n_total);
+    s->stage2_evaluated = d.stage2_evaluated;
+}
+
+static double r1_of(const tcec_exp_stats_t* s) {
+    return s->n_nonzero ? double(s->n_nonzero - s->n1) / double(s->n_nonzero) : 0.0;
+}
+static double r2_of(const tcec_exp_stats_t* s) {
+    return s->n_nonzero ? double(s->n_nonzero - s->n2) / double(s->n_nonzero) : 0.0;
+}
+
+const char* kind_name(int kind) {
+    switch (kind) {  // precsel.cpp:63-71
+    case kKindFp16: return "FP16TCEC";
+    case kKindFp16Scaled: return "FP16TCEC_SCALED";
+    case kKindTf32: return "TF32TCEC";
+    default: return "FP32_BASELINE";
+    }
+}
+
+const char* forced_name(int f) {  // precsel.cpp:73-84
+    static const char* names[] = {"FP32_REF", "FP64_ORACLE", "TF32TC", "FP16TC",
+                                  "TF32TCEC", "FP16TCEC",    "FP16TCEC_SCALED"};
+    return (f >= 0 && f <= 6) ? names[f] : "?";
+}
+
+// DecisionRecord::to_line, precsel.cpp:185-205
+void format_line(char* out, size_t cap, int64_t m, int64_t n, int64_t k, const char* label,
+                 int sa, int sb, const tcec_exp_stats_t* a, const tcec_exp_stats_t* b, bool has) {
+    auto ratio = [&](char* buf, size_t c, const tcec_exp_stats_t* s, bool second) {
+        if (!has || (second && !s->stage2_evaluated))
+            std::snprintf(buf, c, "-");
+        else
+            std::snprintf(buf, c, "%.9g", second ? r2_of(s) : r1_of(s));
+    };
+    auto emax = [&](char* buf, size_t c, const tcec_exp_stats_t* s) {
+        if (!has || !s->e_max_valid)
+            std::snprintf(buf, c, "-");
+        else
+            std::snprintf(buf, c, "%d", s->e_max);
+    };
+    char r1a[32], r2a[32], r1b[32], r2b[32], ea[16], eb[16];
+    ratio(r1a, sizeof r1a, a, false);
+    ratio(r2a, sizeof r2a, a, true);
+    ratio(r1b, sizeof r1b, b, false);
+    ratio(r2b, sizeof r2b, b, true);
+    emax(ea, sizeof ea, a);
+    emax(eb, sizeof eb, b);
+    std::snprintf(out, cap, "%lld,%lld,%lld,%s,%d,%d,%s,%s,%s,%s,%s,%s", (long long)m,
+                  (long long)n, (long long)k, label, sa, sb, r1a, r2a, r1b, r2b, ea, eb);
+}
+
+static inline int64_t round_up(int64_t x, int64_t q) { return (x + q - 1) / q * q; }
+
+// Host-side plan of one dispatched CGEMM (precsel.cpp:225-306 control flow)
+DispatchPlan plan_dispatch(int64_t m, int64_t n, int64_t k, const tcec_dispatch_config_t& cfg) {
+    DispatchPlan p;
+    const int64_t mn = std::min(std::min(m, n), k);
+    p.forced = cfg.force;
+    if (cfg.force >= 0) {
+        p.label = forced_name(cfg.force);
+        switch (cfg.force) {
+        case TCEC_FORCE_FP32_REF: p.tier = kTierFp32; p.kind = kKindFp32; break;
+        case TCEC_FORCE_FP64_ORACLE: p.tier = kTierFp64; p.kind = kKindFp32; break;
+        case TCEC_FORCE_TF32_TC: p.tier = kTierTc; p.kind = kKindTf32; p.corrected = 0; break;
+        case TCEC_FORCE_FP16_TC: p.tier = kTierTc; p.kind = kKindFp16; p.corrected = 0; break;
+        case TCEC_FORCE_TF32_TCEC: p.tier = kTierTc; p.kind = kKindTf32; break;
+        case TCEC_FORCE_FP16_TCEC: p.tier = kTierTc; p.kind = kKindFp16; break;
+        case TCEC_FORCE_FP16_TCEC_SCALED:
+            p.tier = kTierTc;
+            p.kind = -1;  // scales from statistics (precsel.cpp:264-271)
+            p.stats = true;
+            p.forced_scaled = true;
+            p.kind_known = kKindFp16Scaled;
+            break;
+        default: p.tier = kTierInvalid; break;
+        }
+    } else if (mn >= cfg.size_auto) {
+        p.tier = kTierTc;
+        p.kind = -1;  // decided on the device
+        p.stats = true;
+    } else if (mn >= cfg.size_tf32) {
+        p.tier = kTierTc;
+        p.kind = kKindTf32;
+        p.label = kind_name(kKindTf32);
+    } else {
+        p.tier = kTierFp32;
+        p.kind = kKindFp32;
+        p.label = kind_name(kKindFp32);
+    }
+    if (p.kind >= 0 && p.tier == kTierTc) p.kind_known = p.kind;
+    if (p.tier == kTierFp32 || p.tier == kTierFp64) p.kind_known = kKindFp32;
+    p.kp = round_up(2 * k, 64);
+    return p;
+}
+
+size_t plan_workspace(const DispatchPlan& p, int64_t m, int64_t n) {
+    if (p.tier != kTierTc) return 0;
+    const int elem = (p.kind == kKindFp16 || p.forced_scaled) ? 2 : 4;  // auto: sized for tf32
+    const size_t a = size_t(m) * p.kp * elem, b = size_t(2 * n) * p.kp * elem;
+    return 2 * round_up(int64_t(a), 1024) + 2 * round_up(int64_t(b), 1024);
+}
+
+// Launch the device pipeline of one dispatch (no host synchronization).
+int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t m, int64_t n,
+                    int64_t k, const tcec_dispatch_config_t& cfg, const DispatchPlan& p,
+                    DevDecision* d, void* ws) {
+    cudaStream_t s = h.stream;
+    if (p.tier == kTierInvalid) return set_error(TCEC_ERR_INVALID_ARGUMENT, "unknown forced mode");
+    if (p.tier == kTierTc && cfg.k_tile < 1)
+        return set_error(TCEC_ERR_INVALID_ARGUMENT, "k_tile must be >= 1");
+    cudaMemsetAsync(d, 0, sizeof(DevDecision), s);
+    if (p.stats) {
+        launch_stats1(a, 2 * m * k, b, 2 * k * n, d, s);
+        const double t = p.forced_scaled ? 1.0 : cfg.threshold_t;
+        launch_stats2(a, 2 * m * k, b, 2 * k * n, d, t, cfg.target_max_exponent, 0, s);
+        launch_select(d, cfg.threshold_t, cfg.target_max_exponent, p.forced_scaled ? 1 : 0, s);
+    }
+    if (m == 0 || n == 0) return TCEC_OK;
+    if (k == 0) {
+        // every mode yields +0 (the reference chains start at 0.0f)
+        cudaMemsetAsync(c, 0, size_t(m) * n * 8, s);
+        return TCEC_OK;
+    }
+    switch (p.tier) {
+    case kTierFp32:
+        launch_cgemm_fp32_ref(reinterpret_cast<const float2*>(a), reinterpret_cast<const float2*>(b),
+                              reinterpret_cast<float2*>(c), m, n, k, s);
+        return TCEC_OK;
+    case kTierFp64:
+        launch_cgemm_fp64(reinterpret_cast<const float2*>(a), reinterpret_cast<const float2*>(b),
+                          reinterpret_cast<float2*>(c), m, n, k, s);
+        return TCEC_OK;
+    default: break;
+    }
+    // tensor-core tier: operand preparation + tcgen05 GEMM(s)
+    const int elem = (p.kind == kKindFp16 || p.forced_scaled) ? 2 : 4;
+    const size_t abytes = round_up(int64_t(size_t(m) * p.kp * elem), 1024);
+    const size_t bbytes = round_up(int64_t(size_t(2 * n) * p.kp * elem), 1024);
+    uint8_t* w = static_cast<uint8_t*>(ws);
+    void* ahi = w;
+    void* alo = w + abytes;
+    void* bhi = w + 2 * abytes;
+    void* blo = w + 2 * abytes + bbytes;
+    launch_prep_a(a, m, k, p.kp, ahi, alo, d, p.kind, p.corrected, s);
+    launch_prep_b(b, k, n, p.kp, bhi, blo, d, p.kind, p.corrected, s);
+    TcecGemmArgs g{};
+    g.a_hi = ahi;
+    g.a_lo = alo;
+    g.b_hi = bhi;
+    g.b_lo = blo;
+    g.c = c;
+    g.m = m;
+    g.n2 = 2 * n;
+    g.kp = p.kp;
+    g.d = d;
+    g.kind_fixed = p.kind;
+    g.corrected = p.corrected;
+    g.flush_kblocks = p.corrected ? h.flush_kblocks : 0;
+    const bool want16 = p.kind < 0 || p.kind == kKindFp16 || p.kind == kKindFp16Scaled;
+    const bool want32 = (p.kind < 0 && !p.forced_scaled) || p.kind == kKindTf32;
+    if (want16) {
+        g.fmt = kFp16;
+        const int e = launch_tcec_gemm(g, s);
+        if (e) return cuda_error(cudaError_t(e), "tcec_gemm f16");
+    }
+    if (want32) {
+        g.fmt = kTf32;
+        const int e = launch_tcec_gemm(g, s);
+        if (e) return cuda_error(cudaError_t(e), "tcec_gemm tf32");
+    }
+    return TCEC_OK;
+}
+
+// Fill a host result from the (already copied back) device decision.
+int finish_dispatch(const DispatchPlan& p, const DevDecision& dd, int64_t m, int64_t n, int64_t k,
+                    tcec_dispatch_result_t* res) {
+    std::memset(res, 0, sizeof(*res));
+    if (p.stats) {
+        res->has_stats = 1;
+        stats_from_dev(dd.st[0], 2 * m * k, &res->stats_a);
+        stats_from_dev(dd.st[1], 2 * k * n, &res->stats_b);
+    }
+    int kind = p.stats ? dd.kind : p.kind_known;
+    if (p.forced >= 0) {
+        // forced-mode decisions, precsel.cpp:238-272
+        static const int forced_kind[] = {kKindFp32, kKindFp32, kKindTf32, kKindFp16,
+                                          kKindTf32, kKindFp16, kKindFp16Scaled};
+        kind = forced_kind[p.forced];
+    }
+    if (kind < 0)
+        return set_error(TCEC_ERR_LOGIC, "matrix_tolerance: stage-2 statistics required but skipped");
+    res->kind = kind;
+    if (kind == kKindFp16Scaled) {
+        res->scale_a = dd.scale_a;
+        res->scale_b = dd.scale_b;
+    }
+    res->overflow = dd.overflow ? 1 : 0;
+    const char* label = p.forced >= 0 ? forced_name(p.forced) : kind_name(kind);
+    format_line(res->line, sizeof res->line, m, n, k, label, res->scale_a, res->scale_b,
+                &res->stats_a, &res->stats_b, res->has_stats != 0);
+    if (dd.scale_overflow)
+        return set_error(TCEC_ERR_SCALE_OVERFLOW, "scaled component left the f32 range");
+    return TCEC_OK;
+}
+
+}  // namespace tcec
+
+using namespace tcec;
+
+void* tcec_handle_s::workspace(size_t bytes) {
+    if (bytes <= ws_bytes) return ws;
+    cudaStreamSynchronize(stream);
+    if (ws) cudaFree(ws);
+    ws = nullptr;
+    ws_bytes = 0;
+    size_t want = bytes + bytes / 4 + (1u << 20);
+    if (cudaMalloc(&ws, want) != cudaSuccess) {
+        cudaGetLastError();
+        if (cudaMalloc(&ws, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        want = bytes;
+    }
+    ws_bytes = want;
+    return ws;
+}
+
+tcec::DevDecision* tcec_handle_s::decisions(int slots) {
+    if (slots <= dec_slots) return dec;
+    cudaStreamSynchronize(stream);
+    if (dec) cudaFree(dec);
+    if (dec_host) cudaFreeHost(dec_host);
+    dec = nullptr;
+    dec_host = nullptr;
+    dec_slots = 0;
+    const int want = slots < 16 ? 16 : slots;
+    if (cudaMalloc(&dec, sizeof(tcec::DevDecision) * want) != cudaSuccess) return nullptr;
+    if (cudaMallocHost(&dec_host, sizeof(tcec::DevDecision) * want) != cudaSuccess) return nullptr;
+    dec_slots = want;
+    return dec;
+}
+
+tcec_handle_s::~tcec_handle_s() {
+    if (ws) cudaFree(ws);
+    if (dec) cudaFree(dec);
+    if (dec_host) cudaFreeHost(dec_host);
+    if (scratch_host) cudaFreeHost(scratch_host);
+    if (own_stream) cudaStreamDestroy(own_stream);
+}
+
+
+#define CHECK_HANDLE(h)                                                         \
+    do {                                                                        \
+        if (!(h)) return set_error(TCEC_ERR_INVALID_ARGUMENT, "null handle");   \
+        cudaSetDevice((h)->device);                                             \
+    } while (0)
+
+#define CUDA_TRY(expr)                                                          \
+    do {                                                                        \
+        cudaError_t e_ = (expr);                                                \
+        if (e_ != cudaSuccess) return cuda_error(e_, #expr);                    \
+    } while (0)
+
+extern "C" {
+
+const char* tcec_last_error(void) { return g_last_error.c_str(); }
+
+const char* tcec_version(void) {
+    return "tcec_b200 sm_100a: tcgen05 TCEC CGEMM (f16/tf32, TMEM main+corr, RN flush), "
+           "device-side precision selection, bit-exact SIMT FP32/FP64 tiers";
+}
+
+int tcec_create(int device, tcec_handle* out) {
+    if (!out) return set_error(TCEC_ERR_INVALID_ARGUMENT, "null output");
+    *out = nullptr;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return set_error(TCEC_ERR_CUDA, "no CUDA device (the TCEC path has no CPU fallback)");
+    }
+    if (device < 0 || device >= count) return set_error(TCEC_ERR_INVALID_ARGUMENT, "bad device");
+    cudaDeviceProp prop{};
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return set_error(TCEC_ERR_CUDA, std::string("sm_100 required, found ") + prop.name);
+    CUDA_TRY(cudaSetDevice(device));
+    auto* h = new tcec_handle_s();
+    h->device = device;
+    h->sm_count = prop.multiProcessorCount;
+    if (cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete h;
+        return set_error(TCEC_ERR_CUDA, "stream creation failed");
+    }
+    h->stream = h->own_stream;
+    if (!h->decisions(64)) {
+        delete h;
+        return set_error(TCEC_ERR_CUDA, "decision buffer allocation failed");
+    }
+    if (cudaMallocHost(&h->scratch_host, 4096) != cudaSuccess) {
+        delete h;
+        return set_error(TCEC_ERR_CUDA, "pinned scratch allocation failed");
+    }
+    *out = h;
+    return TCEC_OK;
+}
+
+int tcec_destroy(tcec_handle h) {
+    if (!h) return TCEC_OK;
+    cudaSetDevice(h->device);
+    cudaStreamSynchronize(h->stream);
+    delete h;
+    return TCEC_OK;
+}
+
+int tcec_set_stream(tcec_handle h, void* stream) {
+    CHECK_HANDLE(h);
+    h->stream = stream ? static_cast<cudaStream_t>(stream) : h->own_stream;
+    return TCEC_OK;
+}
+
+void* tcec_get_stream(tcec_handle h) { return h ? static_cast<void*>(h->stream) : nullptr; }
+
+int tcec_synchronize(tcec_handle h) {
+    CHECK_HANDLE(h);
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    return TCEC_OK;
+}
+
+int tcec_set_flush_kblocks(tcec_handle h, int kblocks) {
+    CHECK_HANDLE(h);
+    if (kblocks < 0) return set_error(TCEC_ERR_INVALID_ARGUMENT, "flush interval must be >= 0");
+    h->flush_kblocks = kblocks;
+    return TCEC_OK;
+}
+
+int tcec_get_flush_kblocks(tcec_handle h) { return h ? h->flush_kblocks : -1; }
+
+// ------------------------------------------------------------ KernelTable
+
+static int read_flag(tcec_handle h, unsigned* dflag, int* out) {
+    unsigned* hf = static_cast<unsigned*>(h->scratch_host);
+    CUDA_TRY(cudaMemcpyAsync(hf, dflag, sizeof(unsigned), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (out && *hf) *out = 1;
+    return TCEC_OK;
+}
+
+int tcec_quantize_buf(tcec_handle h, const float* src, float* dst, int64_t n, int fmt,
+                      int rounding, int* overflow) {
+    CHECK_HANDLE(h);
+    if (fmt < 0 || fmt > 1 || rounding < 0 || rounding > 1)
+        return set_error(TCEC_ERR_INVALID_ARGUMENT, "bad format or rounding");
+    DevDecision* d = h->dec;
+    CUDA_TRY(cudaMemsetAsync(&d->overflow, 0, sizeof(unsigned), h->stream));
+    launch_quantize(src, dst, n, fmt, rounding, &d->overflow, h->stream);
+    CUDA_TRY(cudaGetLastError());
+    return read_flag(h, &d->overflow, overflow);
+}
+
+int tcec_split_buf(tcec_handle h, const float* src, float* hi, float* lo, int64_t n, int fmt,
+                   int* overflow) {
+    CHECK_HANDLE(h);
+    if (fmt < 0 || fmt > 1) return set_error(TCEC_ERR_INVALID_ARGUMENT, "bad format");
+    DevDecision* d = h->dec;
+    CUDA_TRY(cudaMemsetAsync(&d->overflow, 0, sizeof(unsigned), h->stream));
+    launch_split_flat(src, hi, lo, n, fmt, &d->overflow, h->stream);
+    CUDA_TRY(cudaGetLastError());
+    return read_flag(h, &d->overflow, overflow);
+}
+
+int tcec_scale_buf(tcec_handle h, const float* src, float* dst, int64_t n, int scale_exp) {
+    CHECK_HANDLE(h);
+    launch_scale(src, dst, n, scale_exp, nullptr, h->stream);
+    CUDA_TRY(cudaGetLastError());
+    return TCEC_OK;
+}
+
+int tcec_add_buf(tcec_handle h, const float* a, const float* b, float* dst, int64_t n) {
+    CHECK_HANDLE(h);
+    launch_add_sub(a, b, dst, n, 0, h->stream);
+    CUDA_TRY(cudaGetLastError());
+    return TCEC_OK;
+}
+
+int tcec_sub_buf(tcec_handle h, const float* a, const float* b, float* dst, int64_t n) {
+    CHECK_HANDLE(h);
+    launch_add_sub(a, b, dst, n, 1, h->stream);
+    CUDA_TRY(cudaGetLastError());
+    return TCEC_OK;
+}
+
+int tcec_scale_components(tcec_handle h, float* x, int64_t n, int scale_exp, int check) {
+    CHECK_HANDLE(h);
+    DevDecision* d = h->dec;
+    CUDA_TRY(cudaMemsetAsync(&d->scale_overflow, 0, sizeof(unsigned), h->stream));
+    launch_scale(x, x, n, scale_exp, check ? &d->scale_overflow : nullptr, h->stream);
+    CUDA_TRY(cudaGetLastError());
+    if (!check) return TCEC_OK;
+    int bad = 0;
+    const int rc = read_flag(h, &d->scale_overflow, &bad);
+    if (rc) return rc;
+    if (bad) return set_error(TCEC_ERR_SCALE_OVERFLOW, "scaled component left the f32 range");
+    return TCEC_OK;
+}
+
+// ------------------------------------------------------ statistics / selection
+
+int tcec_exp_stats(tcec_handle h, const void* x, int64_t rows, int64_t cols, int target,
+                   int staged, double t, tcec_exp_stats_t* out) {
+    CHECK_HANDLE(h);
+    if (!out) return set_error(TCEC_ERR_INVALID_ARGUMENT, "null output");
+    DevDecision* d = h->dec;
+    const int64_t n = 2 * rows * cols;
+    const float* p = static_cast<const float*>(x);
+    CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(DevDecision), h->stream));
+    launch_stats1(p, n, nullptr, 0, d, h->stream);
+    launch_stats2(p, n, nullptr, 0, d, t, target, staged ? 0 : 1, h->stream);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(h->dec_host, d, sizeof(DevDecision), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    DevStats st = h->dec_host->st[0];
+    // finalize exactly as precsel.cpp:95-104
+    tcec_exp_stats_t s;
+    stats_from_dev(st, n, &s);
+    bool pass = true;
+    if (s.n_nonzero != 0) {
+        const double r1 = r1_of(&s);
+        pass = !(r1 > t) && (!s.e_max_valid || s.e_max <= target);
+    }
+    if (staged && pass) {
+        s.n2 = s.n1;
+        s.stage2_evaluated = 0;
+    } else {
+        s.stage2_evaluated = 1;
+        if (!s.e_max_valid) s.n2 = 0;
+    }
+    *out = s;
+    return TCEC_OK;
+}
+
+double tcec_r1(const tcec_exp_stats_t* s) { return r1_of(s); }
+double tcec_r2(const tcec_exp_stats_t* s) { return r2_of(s); }
+
+int tcec_matrix_tolerance(const tcec_exp_stats_t* s, double t, int target, int* level) {
+    // precsel.cpp:106-121
+    if (!s || !level) return set_error(TCEC_ERR_INVALID_ARGUMENT, "null argument");
+    if (s->n_nonzero == 0) {
+        *level = 2;
+        return TCEC_OK;
+    }
+    const bool pass = !(r1_of(s) > t) && (!s->e_max_valid || s->e_max <= target);
+    if (pass) {
+        *level = 2;
+        return TCEC_OK;
+    }
+    if (!s->stage2_evaluated)
+        return set_error(TCEC_ERR_LOGIC, "matrix_tolerance: stage-2 statistics required but skipped");
+    *level = r2_of(s) <= t ? 1 : 0;
+    return TCEC_OK;
+}
+
+int tcec_select_mode(int la, int eva, int ea, int lb, int evb, int eb, int target, int* kind,
+                     int* sa, int* sb) {
+    // precsel.cpp:123-135
+    if (!kind || !sa || !sb) return set_error(TCEC_ERR_INVALID_ARGUMENT, "null argument");
+    *sa = *sb = 0;
+    if (la == 2 && lb == 2) {
+        *kind = kKindFp16;
+    } else if (la >= 1 && lb >= 1) {
+        *kind = kKindFp16Scaled;
+        *sa = eva ? target - ea : 0;
+        *sb = evb ? target - eb : 0;
+    } else {
+        *kind = kKindTf32;
+    }
+    return TCEC_OK;
+}
+
+// ------------------------------------------------------------------ CGEMM
+
+void tcec_default_config(tcec_dispatch_config_t* cfg) {
+    std::memset(cfg, 0, sizeof(*cfg));
+    cfg->threshold_t = 0.0;  // SelectionPolicy defaults, precsel.hpp:60-65
+    cfg->size_auto = 2048;
+    cfg->size_tf32 = 512;
+    cfg->target_max_exponent = 14;
+    cfg->k_tile = 16;        // TilingConfig, gemm.hpp:28-30
+    cfg->force = -1;
+}
+
+int tcec_cgemm(tcec_handle h, const void* a, const void* b, void* c, int64_t m, int64_t n,
+               int64_t k, int mode, int k_tile, int* overflow) {
+    CHECK_HANDLE(h);
+    static const int mode_to_force[] = {TCEC_FORCE_FP32_REF, TCEC_FORCE_FP64_ORACLE,
+                                        TCEC_FORCE_TF32_TC,  TCEC_FORCE_FP16_TC,
+                                        TCEC_FORCE_TF32_TCEC, TCEC_FORCE_FP16_TCEC};
+    if (mode < 0 || mode > 5) return set_error(TCEC_ERR_INVALID_ARGUMENT, "unknown GEMM mode");
+    tcec_dispatch_config_t cfg;
+    tcec_default_config(&cfg);
+    cfg.k_tile = k_tile;
+    cfg.force = mode_to_force[mode];
+    tcec_dispatch_result_t res;
+    const int rc = tcec_dispatch_cgemm(h, a, b, c, m, n, k, &cfg, &res);
+    if (rc == TCEC_OK && overflow && res.overflow) *overflow = 1;
+    return rc;
+}
+
+int tcec_dispatch_cgemm(tcec_handle h, const void* a, const void* b, void* c, int64_t m, int64_t n,
+                        int64_t k, const tcec_dispatch_config_t* cfg, tcec_dispatch_result_t* res) {
+    CHECK_HANDLE(h);
+    if (!cfg || !res) return set_error(TCEC_ERR_INVALID_ARGUMENT, "null argument");
+    if (m < 0 || n < 0 || k < 0) return set_error(TCEC_ERR_SHAPE_MISMATCH, "negative extent");
+    const DispatchPlan p = plan_dispatch(m, n, k, *cfg);
+    void* ws = nullptr;
+    const size_t wsb = plan_workspace(p, m, n);
+    if (wsb) {
+        ws = h->workspace(wsb);
+        if (!ws) return set_error(TCEC_ERR_CUDA, "workspace allocation failed");
+    }
+    DevDecision* d = h->dec;
+    int rc = launch_dispatch(*h, static_cast<const float*>(a), static_cast<const float*>(b),
+                             static_cast<float*>(c), m, n, k, *cfg, p, d, ws);
+    if (rc) return rc;
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(h->dec_host, d, sizeof(DevDecision), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    return finish_dispatch(p, *h->dec_host, m, n, k, res);
+}
+
+int tcec_dispatch_cgemm_host(tcec_handle h, const void* a, const void* b, void* c, int64_t m,
+                             int64_t n, int64_t k, const tcec_dispatch_config_t* cfg,
+                             tcec_dispatch_result_t* res) {
+    CHECK_HANDLE(h);
+    const size_t ab = size_t(m) * k * 8, bb = size_t(k) * n * 8, cb = size_t(m) * n * 8;
+    const size_t ra = size_t(round_up(int64_t(ab), 256)), rb = size_t(round_up(int64_t(bb), 256));
+    const size_t need = ra + rb + cb + 256;
+    if (h->io_bytes < need) {
+        cudaStreamSynchronize(h->stream);
+        if (h->io) cudaFree(h->io);
+        h->io = nullptr;
+        h->io_bytes = 0;
+        CUDA_TRY(cudaMalloc(&h->io, need));
+        h->io_bytes = need;
+    }
+    uint8_t* base = static_cast<uint8_t*>(h->io);
+    void* da = base;
+    void* db = base + ra;
+    void* dc = base + ra + rb;
+    CUDA_TRY(cudaMemcpyAsync(da, a, ab, cudaMemcpyHostToDevice, h->stream));
+    CUDA_TRY(cudaMemcpyAsync(db, b, bb, cudaMemcpyHostToDevice, h->stream));
+    const int rc = tcec_dispatch_cgemm(h, da, db, dc, m, n, k, cfg, res);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(c, dc, cb, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    return TCEC_OK;
+}
+
+// ---------------------------------------------------------------- permute
+
+int tcec_permute(tcec_handle h, const void* src, void* dst, int rank, const int64_t* old_dims,
+                 const int* axis_of) {
+    CHECK_HANDLE(h);
+    if (rank < 0 || rank > kMaxRank)
+        return set_error(TCEC_ERR_INVALID_PERMUTATION, "permutation has wrong length");
+    bool used[kMaxRank] = {false};
+    for (int a = 0; a < rank; ++a) {
+        const int o = axis_of[a];
+        if (o < 0 || o >= rank || used[o])
+            return set_error(TCEC_ERR_INVALID_PERMUTATION, "label not in tensor: axis " +
+                                                               std::to_string(o));
+        used[o] = true;
+        if (old_dims[a] < 1) return set_error(TCEC_ERR_SHAPE_MISMATCH, "tensor extents must be >= 1");
+    }
+    if (rank == 0) {
+        CUDA_TRY(cudaMemcpyAsync(dst, src, 8, cudaMemcpyDeviceToDevice, h->stream));
+        return TCEC_OK;
+    }
+    launch_permute(static_cast<const float2*>(src), static_cast<float2*>(dst), rank, old_dims,
+                   axis_of, h->stream);
+    CUDA_TRY(cudaGetLastError());
+    return TCEC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,642 @@
+// HBM-bound kernels of the TCEC path: format conversion, exponent statistics,
+// device-side precision selection, operand preparation (scale + split + complex
+// block expansion), the bit-exact SIMT GEMM tiers, and the TTGT permute.
+//
+// Reference mapping (KernelTable, proj/include/mpsgemm/kernels.hpp:20-63):
+//   quantize_buf / split_buf / scale_buf / add_buf / sub_buf -> *_kernel below
+//   abs_stats + count_abs_ge (stage1/stage2, precsel.cpp:23-45) -> stats1/stats2
+//   matrix_tolerance + select_mode (precsel.cpp:106-135)      -> select_kernel
+//   gemm_rows_rn (+ cgemm.cpp assembly)                        -> cgemm_fp32_ref_kernel
+//   gemm_rows_f64                                               -> cgemm_fp64_kernel
+//   permute (tensor.hpp:56-105)                                 -> permute_kernel
+#include "tcec_common.cuh"
+#include "tcec_internal.h"
+
+namespace tcec {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline int grid_for(int64_t work, int per_block, int max_blocks = 148 * 16) {
+    int64_t g = (work + per_block - 1) / per_block;
+    if (g < 1) g = 1;
+    if (g > max_blocks) g = max_blocks;
+    return int(g);
+}
+
+TCEC_DEV unsigned warp_or(unsigned v) { return __reduce_or_sync(0xFFFFFFFFu, v); }
+
+TCEC_DEV void flag_or(unsigned* flag, unsigned v) {
+    // one atomic per warp at most; the flag is an OR-accumulated out-parameter
+    const unsigned any = warp_or(v);
+    if (any && flag && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
+// ------------------------------------------------------------ elementwise
+
+__global__ void quantize_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t n,
+                                int fmt, int rz, unsigned* ovf) {
+    unsigned o = 0;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        dst[i] = quantize(src[i], fmt, rz != 0, o);
+    flag_or(ovf, o);
+}
+
+__global__ void split_flat_kernel(const float* __restrict__ src, float* __restrict__ hi,
+                                  float* __restrict__ lo, int64_t n, int fmt, unsigned* ovf) {
+    unsigned o = 0;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        float h, l;
+        if (fmt == kFp16)
+            split<kFp16>(src[i], h, l, o);
+        else
+            split<kTf32>(src[i], h, l, o);
+        hi[i] = h;
+        lo[i] = l;
+    }
+    flag_or(ovf, o);
+}
+
+__global__ void scale_kernel(const float* src, float* dst, int64_t n, double factor,
+                             unsigned* nonfinite) {
+    unsigned bad = 0;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const float v = scale_pow2(src[i], factor);
+        dst[i] = v;
+        bad |= isfinite(v) ? 0u : 1u;
+    }
+    flag_or(nonfinite, bad);
+}
+
+__global__ void add_sub_kernel(const float* a, const float* b, float* dst, int64_t n, int sub) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        dst[i] = sub ? __fsub_rn(a[i], b[i]) : __fadd_rn(a[i], b[i]);
+}
+
+// ------------------------------------------------------------- statistics
+
+// bits of |x|; "valid" = nonzero and not NaN, i.e. the reference's a > 0.0f
+TCEC_DEV bool valid_mag(uint32_t m) { return (m - 1u) < 0x7F800000u; }
+
+constexpr uint32_t kFp16MinNormalBits = 0x38800000u;  // 2^-14, precsel.cpp:21
+
+template <typename T>
+TCEC_DEV T block_sum(T v, T* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    T r = 0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < int(blockDim.x >> 5); ++i) r += red[i];
+    return r;
+}
+
+TCEC_DEV unsigned block_max(unsigned v, unsigned* red) {
+    v = __reduce_max_sync(0xFFFFFFFFu, v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    unsigned r = 0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < int(blockDim.x >> 5); ++i) r = max(r, red[i]);
+    return r;
+}
+
+// stage 1 (precsel.cpp:23-32 via abs_stats, kernels_scalar.cpp:50-65):
+// nonzero count, count of |x| >= 2^-14, max |x| -- one coalesced float4 sweep
+__global__ void __launch_bounds__(kThreads) stats1_kernel(const float* a, int64_t na,
+                                                          const float* b, int64_t nb,
+                                                          DevDecision* d) {
+    const float* x = blockIdx.y ? b : a;
+    const int64_t n = blockIdx.y ? nb : na;
+    if (x == nullptr || n == 0) return;
+    unsigned nz = 0, n1 = 0, mx = 0;
+    auto visit = [&](float v) {
+        const uint32_t m = __float_as_uint(v) & 0x7FFFFFFFu;
+        const bool ok = valid_mag(m);
+        nz += ok;
+        n1 += ok && m >= kFp16MinNormalBits;
+        mx = max(mx, ok ? m : 0u);
+    };
+    const int64_t tid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    int64_t head = 0;
+    if ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) {
+        const int64_t n4 = n / 4;
+        const float4* x4 = reinterpret_cast<const float4*>(x);
+        for (int64_t i = tid; i < n4; i += stride) {
+            const float4 v = __ldcs(x4 + i);
+            visit(v.x);
+            visit(v.y);
+            visit(v.z);
+            visit(v.w);
+        }
+        head = n4 * 4;
+    }
+    for (int64_t i = head + tid; i < n; i += stride) visit(x[i]);
+
+    __shared__ unsigned long long red64[kThreads / 32];
+    __shared__ unsigned red32[kThreads / 32];
+    const unsigned long long snz = block_sum<unsigned long long>(nz, red64);
+    const unsigned long long sn1 = block_sum<unsigned long long>(n1, red64);
+    const unsigned smx = block_max(mx, red32);
+    if (threadIdx.x == 0) {
+        DevStats& st = d->st[blockIdx.y];
+        if (snz) atomicAdd(&st.n_nonzero, snz);
+        if (sn1) atomicAdd(&st.n1, sn1);
+        if (smx) atomicMax(&st.max_bits, smx);
+    }
+}
+
+// stage1_passes (precsel.cpp:47-52); r1 in double exactly as precsel.hpp:27-30
+TCEC_DEV bool stage1_passes(unsigned long long nz, unsigned long long n1, unsigned max_bits,
+                            double t, int target) {
+    if (nz == 0) return true;
+    const double r1 = double(nz - n1) / double(nz);
+    if (r1 > t) return false;
+    return max_bits == 0 || exponent_of_bits(max_bits) <= target;
+}
+
+// stage 2 (precsel.cpp:34-45 via count_abs_ge): count of |x| >= 2^(e_max - target - 14)
+__global__ void __launch_bounds__(kThreads) stats2_kernel(const float* a, int64_t na,
+                                                          const float* b, int64_t nb,
+                                                          DevDecision* d, double t, int target,
+                                                          int always) {
+    const float* x = blockIdx.y ? b : a;
+    const int64_t n = blockIdx.y ? nb : na;
+    if (x == nullptr || n == 0) return;
+    const DevStats st = d->st[blockIdx.y];
+    if (!always && stage1_passes(st.n_nonzero, st.n1, st.max_bits, t, target)) return;
+    if (st.max_bits == 0) return;  // no e_max: n2 = 0
+    const int w = exponent_of_bits(st.max_bits) - (target + 14);
+    // ldexp(1.0f, w): a normal, a subnormal power of two, or 0 (all nonzero pass)
+    const uint32_t thr = w >= -126 ? uint32_t(w + 127) << 23 : (w >= -149 ? 1u << (w + 149) : 1u);
+    unsigned cnt = 0;
+    auto visit = [&](float v) {
+        const uint32_t m = __float_as_uint(v) & 0x7FFFFFFFu;
+        cnt += valid_mag(m) && m >= thr;
+    };
+    const int64_t tid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    int64_t head = 0;
+    if ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) {
+        const int64_t n4 = n / 4;
+        const float4* x4 = reinterpret_cast<const float4*>(x);
+        for (int64_t i = tid; i < n4; i += stride) {
+            const float4 v = __ldcs(x4 + i);
+            visit(v.x);
+            visit(v.y);
+            visit(v.z);
+            visit(v.w);
+        }
+        head = n4 * 4;
+    }
+    for (int64_t i = head + tid; i < n; i += stride) visit(x[i]);
+    __shared__ unsigned long long red64[kThreads / 32];
+    const unsigned long long s = block_sum<unsigned long long>(cnt, red64);
+    if (threadIdx.x == 0 && s) atomicAdd(&d->st[blockIdx.y].n2, s);
+}
+
+// finalize ExpStats, tolerance levels and the pair rule (precsel.cpp:95-135)
+__global__ void select_kernel(DevDecision* d, double t, int target, int forced_scaled,
+                              int stage2_always) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int level[2];
+    for (int op = 0; op < 2; ++op) {
+        DevStats& st = d->st[op];
+        st.e_max_valid = st.max_bits != 0;
+        st.e_max = st.e_max_valid ? exponent_of_bits(st.max_bits) : 0;
+        const double ts = forced_scaled ? 1.0 : t;
+        const bool pass = stage1_passes(st.n_nonzero, st.n1, st.max_bits, ts, target);
+        if (!stage2_always && pass) {
+            st.n2 = st.n1;  // lower bound, stage 2 skipped (precsel.cpp:97-101)
+            st.stage2_evaluated = 0;
+        } else {
+            st.stage2_evaluated = 1;  // n2 counted by stats2 (0 when no e_max)
+        }
+        // matrix_tolerance (precsel.cpp:106-121)
+        if (st.n_nonzero == 0 || stage1_passes(st.n_nonzero, st.n1, st.max_bits, t, target)) {
+            level[op] = 2;
+        } else if (!st.stage2_evaluated) {
+            level[op] = -1;
+        } else {
+            const double r2 = double(st.n_nonzero - st.n2) / double(st.n_nonzero);
+            level[op] = r2 <= t ? 1 : 0;
+        }
+    }
+    d->level_a = level[0];
+    d->level_b = level[1];
+    const int sa = d->st[0].e_max_valid ? target - d->st[0].e_max : 0;
+    const int sb = d->st[1].e_max_valid ? target - d->st[1].e_max : 0;
+    if (forced_scaled) {
+        d->kind = kKindFp16Scaled;
+        d->scale_a = sa;
+        d->scale_b = sb;
+        return;
+    }
+    if (level[0] < 0 || level[1] < 0) {
+        d->kind = -1;  // std::logic_error in matrix_tolerance
+        return;
+    }
+    if (level[0] == 2 && level[1] == 2) {
+        d->kind = kKindFp16;
+        d->scale_a = d->scale_b = 0;
+    } else if (level[0] >= 1 && level[1] >= 1) {
+        d->kind = kKindFp16Scaled;
+        d->scale_a = sa;
+        d->scale_b = sb;
+    } else {
+        d->kind = kKindTf32;
+        d->scale_a = d->scale_b = 0;
+    }
+}
+
+// --------------------------------------------------------- operand prep
+
+struct PrepMode {
+    int fmt;       // kFp16 / kTf32
+    int scale;     // power-of-two shift (FP16TCEC_SCALED)
+    bool active;   // false: this dispatch does not use tensor cores
+};
+
+TCEC_DEV PrepMode prep_mode(const DevDecision* d, int kind_fixed, bool is_b) {
+    const int kind = kind_fixed >= 0 ? kind_fixed : d->kind;
+    PrepMode p;
+    p.active = kind == kKindFp16 || kind == kKindFp16Scaled || kind == kKindTf32;
+    p.fmt = kind == kKindTf32 ? kTf32 : kFp16;
+    p.scale = kind == kKindFp16Scaled ? (is_b ? d->scale_b : d->scale_a) : 0;
+    return p;
+}
+
+// scale (optional) + split/quantize one component; returns hi, lo
+TCEC_DEV void convert(float x, const PrepMode& pm, double factor, bool corrected, float& hi,
+                      float& lo, unsigned& ovf, unsigned& bad) {
+    if (pm.scale != 0) {
+        x = scale_pow2(x, factor);
+        bad |= isfinite(x) ? 0u : 1u;
+    }
+    if (corrected) {
+        if (pm.fmt == kFp16)
+            split<kFp16>(x, hi, lo, ovf);
+        else
+            split<kTf32>(x, hi, lo, ovf);
+    } else {
+        hi = quantize(x, pm.fmt, false, ovf);
+        lo = 0.0f;
+    }
+}
+
+// A (m x k complex) -> K-major m x kp; each thread converts 8 consecutive
+// real components of one row (16 B of f16 or 32 B of tf32 per output plane)
+__global__ void __launch_bounds__(kThreads) prep_a_kernel(const float* __restrict__ a, int64_t m,
+                                                          int64_t k2, int64_t kp, void* hi_v,
+                                                          void* lo_v, const DevDecision* d,
+                                                          int kind_fixed, int corrected) {
+    const PrepMode pm = prep_mode(d, kind_fixed, false);
+    if (!pm.active) return;
+    const double factor = ldexp(1.0, pm.scale);
+    const int64_t chunks_per_row = kp / 8;
+    const int64_t total = m * chunks_per_row;
+    unsigned ovf = 0, bad = 0;
+    const bool vec = (k2 % 8) == 0 && (reinterpret_cast<uintptr_t>(a) & 15u) == 0;
+    for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < total;
+         c += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t row = c / chunks_per_row;
+        const int64_t col = (c - row * chunks_per_row) * 8;
+        float x[8];
+        if (vec && col < k2) {
+            const float4* p = reinterpret_cast<const float4*>(a + row * k2 + col);
+            const float4 v0 = __ldcs(p), v1 = __ldcs(p + 1);
+            x[0] = v0.x; x[1] = v0.y; x[2] = v0.z; x[3] = v0.w;
+            x[4] = v1.x; x[5] = v1.y; x[6] = v1.z; x[7] = v1.w;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) x[e] = (col + e < k2) ? a[row * k2 + col + e] : 0.0f;
+        }
+        float h[8], l[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) convert(x[e], pm, factor, corrected, h[e], l[e], ovf, bad);
+        if (pm.fmt == kFp16) {
+            __half2 hh[4], ll[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                hh[e] = __floats2half2_rn(h[2 * e], h[2 * e + 1]);  // exact: values are FP16
+                ll[e] = __floats2half2_rn(l[2 * e], l[2 * e + 1]);
+            }
+            __half* hp = static_cast<__half*>(hi_v) + row * kp + col;
+            *reinterpret_cast<uint4*>(hp) = *reinterpret_cast<uint4*>(hh);
+            if (corrected) {
+                __half* lp = static_cast<__half*>(lo_v) + row * kp + col;
+                *reinterpret_cast<uint4*>(lp) = *reinterpret_cast<uint4*>(ll);
+            }
+        } else {
+            float4* hp = reinterpret_cast<float4*>(static_cast<float*>(hi_v) + row * kp + col);
+            hp[0] = make_float4(h[0], h[1], h[2], h[3]);
+            hp[1] = make_float4(h[4], h[5], h[6], h[7]);
+            if (corrected) {
+                float4* lp = reinterpret_cast<float4*>(static_cast<float*>(lo_v) + row * kp + col);
+                lp[0] = make_float4(l[0], l[1], l[2], l[3]);
+                lp[1] = make_float4(l[4], l[5], l[6], l[7]);
+            }
+        }
+    }
+    DevDecision* dm = const_cast<DevDecision*>(d);
+    flag_or(&dm->overflow, ovf);
+    flag_or(&dm->scale_overflow, bad);
+}
+
+// B (k x n complex) -> B'^T (2n x kp, K-major) with the complex block expansion
+//   row 2j   : (Br, -Bi) at columns (2kk, 2kk+1)
+//   row 2j+1 : ( Bi,  Br)
+// via a 32x32 shared-memory transpose tile (coalesced reads along j, writes along kk)
+__global__ void __launch_bounds__(256) prep_b_kernel(const float2* __restrict__ b, int64_t k,
+                                                     int64_t n, int64_t kp, void* hi_v,
+                                                     void* lo_v, const DevDecision* d,
+                                                     int kind_fixed, int corrected) {
+    const PrepMode pm = prep_mode(d, kind_fixed, true);
+    if (!pm.active) return;
+    const double factor = ldexp(1.0, pm.scale);
+    __shared__ float2 tile[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    const int64_t j0 = int64_t(blockIdx.x) * 32, kk0 = int64_t(blockIdx.y) * 32;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int64_t kk = kk0 + ty + 8 * r, j = j0 + tx;
+        tile[ty + 8 * r][tx] = (kk < k && j < n) ? b[kk * n + j] : make_float2(0.0f, 0.0f);
+    }
+    __syncthreads();
+    unsigned ovf = 0, bad = 0;
+    const int64_t kk = kk0 + tx;
+    const int64_t col = 2 * kk;
+    const bool in_cols = col < kp;
+    for (int jj = ty; jj < 32; jj += 8) {
+        const int64_t j = j0 + jj;
+        if (j >= n || !in_cols) continue;
+        const float2 v = tile[tx][jj];
+        float rh, rl, ih, il;
+        convert(v.x, pm, factor, corrected, rh, rl, ovf, bad);
+        convert(v.y, pm, factor, corrected, ih, il, ovf, bad);
+        const int64_t r0 = (2 * j) * kp + col, r1 = (2 * j + 1) * kp + col;
+        if (pm.fmt == kFp16) {
+            __half* hp = static_cast<__half*>(hi_v);
+            *reinterpret_cast<__half2*>(hp + r0) = __floats2half2_rn(rh, -ih);
+            *reinterpret_cast<__half2*>(hp + r1) = __floats2half2_rn(ih, rh);
+            if (corrected) {
+                __half* lp = static_cast<__half*>(lo_v);
+                *reinterpret_cast<__half2*>(lp + r0) = __floats2half2_rn(rl, -il);
+                *reinterpret_cast<__half2*>(lp + r1) = __floats2half2_rn(il, rl);
+            }
+        } else {
+            float* hp = static_cast<float*>(hi_v);
+            *reinterpret_cast<float2*>(hp + r0) = make_float2(rh, -ih);
+            *reinterpret_cast<float2*>(hp + r1) = make_float2(ih, rh);
+            if (corrected) {
+                float* lp = static_cast<float*>(lo_v);
+                *reinterpret_cast<float2*>(lp + r0) = make_float2(rl, -il);
+                *reinterpret_cast<float2*>(lp + r1) = make_float2(il, rl);
+            }
+        }
+    }
+    DevDecision* dm = const_cast<DevDecision*>(d);
+    flag_or(&dm->overflow, ovf);
+    flag_or(&dm->scale_overflow, bad);
+}
+
+// ------------------------------------------------------------ SIMT GEMM
+
+// FP32_REF complex GEMM with the reference's exact arithmetic: four RN chains
+// P1=ReRe, P2=ImIm, P3=ReIm, P4=ImRe, each starting at +0 and accumulating
+// mul-then-add in ascending k (kernels_scalar.cpp:76-87, -ffp-contract=off),
+// then C = (P1 - P2, P3 + P4) in f32 RN (cgemm.cpp:38-44).
+constexpr int SB_M = 64, SB_N = 64, SB_K = 16;
+
+__global__ void __launch_bounds__(256) cgemm_fp32_ref_kernel(const float2* __restrict__ a,
+                                                             const float2* __restrict__ b,
+                                                             float2* __restrict__ c, int64_t m,
+                                                             int64_t n, int64_t k) {
+    __shared__ float sar[SB_K][SB_M], sai[SB_K][SB_M], sbr[SB_K][SB_N], sbi[SB_K][SB_N];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int64_t i0 = int64_t(blockIdx.y) * SB_M, j0 = int64_t(blockIdx.x) * SB_N;
+    float p1[4][4], p2[4][4], p3[4][4], p4[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) p1[i][j] = p2[i][j] = p3[i][j] = p4[i][j] = 0.0f;
+
+    for (int64_t k0 = 0; k0 < k; k0 += SB_K) {
+        // A tile: 64 rows x 16 k; B tile: 16 k x 64 cols (4 complex per thread)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int idx = threadIdx.x + 256 * r;
+            const int ar = idx / SB_K, ak = idx % SB_K;
+            const int64_t gi = i0 + ar, gk = k0 + ak;
+            const float2 va = (gi < m && gk < k) ? a[gi * k + gk] : make_float2(0.f, 0.f);
+            sar[ak][ar] = va.x;
+            sai[ak][ar] = va.y;
+            const int bk = idx / SB_N, bj = idx % SB_N;
+            const int64_t gk2 = k0 + bk, gj = j0 + bj;
+            const float2 vb = (gk2 < k && gj < n) ? b[gk2 * n + gj] : make_float2(0.f, 0.f);
+            sbr[bk][bj] = vb.x;
+            sbi[bk][bj] = vb.y;
+        }
+        __syncthreads();
+        const int kend = (k - k0) < SB_K ? int(k - k0) : SB_K;  // never add padding terms
+        for (int kk = 0; kk < kend; ++kk) {
+            float ar[4], ai[4], br[4], bi[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                ar[i] = sar[kk][ty + 16 * i];
+                ai[i] = sai[kk][ty + 16 * i];
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                br[j] = sbr[kk][tx + 16 * j];
+                bi[j] = sbi[kk][tx + 16 * j];
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    p1[i][j] = __fadd_rn(p1[i][j], __fmul_rn(ar[i], br[j]));
+                    p2[i][j] = __fadd_rn(p2[i][j], __fmul_rn(ai[i], bi[j]));
+                    p3[i][j] = __fadd_rn(p3[i][j], __fmul_rn(ar[i], bi[j]));
+                    p4[i][j] = __fadd_rn(p4[i][j], __fmul_rn(ai[i], br[j]));
+                }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t gi = i0 + ty + 16 * i, gj = j0 + tx + 16 * j;
+            if (gi < m && gj < n)
+                c[gi * n + gj] =
+                    make_float2(__fsub_rn(p1[i][j], p2[i][j]), __fadd_rn(p3[i][j], p4[i][j]));
+        }
+}
+
+// FP64_ORACLE tier: f64 chains (kernels_scalar.cpp:137-148), each product
+// rounded to f32 (gemm.cpp:111-117), then assembled in f32 (cgemm.cpp:38-44)
+__global__ void cgemm_fp64_kernel(const float2* __restrict__ a, const float2* __restrict__ b,
+                                  float2* __restrict__ c, int64_t m, int64_t n, int64_t k) {
+    const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    const int64_t i = blockIdx.y;
+    if (j >= n || i >= m) return;
+    double p1 = 0.0, p2 = 0.0, p3 = 0.0, p4 = 0.0;
+    for (int64_t kk = 0; kk < k; ++kk) {
+        const float2 va = a[i * k + kk], vb = b[kk * n + j];
+        const double ar = va.x, ai = va.y, br = vb.x, bi = vb.y;
+        p1 = __dadd_rn(p1, __dmul_rn(ar, br));
+        p2 = __dadd_rn(p2, __dmul_rn(ai, bi));
+        p3 = __dadd_rn(p3, __dmul_rn(ar, bi));
+        p4 = __dadd_rn(p4, __dmul_rn(ai, br));
+    }
+    c[i * n + j] = make_float2(__fsub_rn(__double2float_rn(p1), __double2float_rn(p2)),
+                               __fadd_rn(__double2float_rn(p3), __double2float_rn(p4)));
+}
+
+// --------------------------------------------------------------- permute
+
+struct PermDesc {
+    int rank;
+    int64_t total;
+    int64_t out_dim[kMaxRank];     // merged output dims (innermost last)
+    int64_t in_stride[kMaxRank];   // input stride of each output axis
+};
+
+// gather out[pos] = in[offset(pos)]; the output is written fully coalesced,
+// axes that stay adjacent are merged on the host so the innermost run is as
+// long as possible
+__global__ void __launch_bounds__(kThreads) permute_kernel(const float2* __restrict__ src,
+                                                           float2* __restrict__ dst,
+                                                           const PermDesc desc) {
+    for (int64_t pos = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; pos < desc.total;
+         pos += int64_t(gridDim.x) * blockDim.x) {
+        int64_t rem = pos, off = 0;
+        for (int a = desc.rank - 1; a >= 0; --a) {
+            const int64_t dim = desc.out_dim[a];
+            const int64_t q = rem / dim;
+            off += (rem - q * dim) * desc.in_stride[a];
+            rem = q;
+        }
+        dst[pos] = src[off];
+    }
+}
+
+}  // namespace
+
+// ================================================================ launchers
+
+void launch_quantize(const float* src, float* dst, int64_t n, int fmt, int rz, unsigned* d_ovf,
+                     cudaStream_t s) {
+    if (n <= 0) return;
+    quantize_kernel<<<grid_for(n, kThreads), kThreads, 0, s>>>(src, dst, n, fmt, rz, d_ovf);
+}
+
+void launch_split_flat(const float* src, float* hi, float* lo, int64_t n, int fmt, unsigned* d_ovf,
+                       cudaStream_t s) {
+    if (n <= 0) return;
+    split_flat_kernel<<<grid_for(n, kThreads), kThreads, 0, s>>>(src, hi, lo, n, fmt, d_ovf);
+}
+
+void launch_scale(const float* src, float* dst, int64_t n, int scale_exp, unsigned* d_nonfinite,
+                  cudaStream_t s) {
+    if (n <= 0) return;
+    scale_kernel<<<grid_for(n, kThreads), kThreads, 0, s>>>(src, dst, n, ldexp(1.0, scale_exp),
+                                                             d_nonfinite);
+}
+
+void launch_add_sub(const float* a, const float* b, float* dst, int64_t n, int sub,
+                    cudaStream_t s) {
+    if (n <= 0) return;
+    add_sub_kernel<<<grid_for(n, kThreads), kThreads, 0, s>>>(a, b, dst, n, sub);
+}
+
+void launch_stats1(const float* a, int64_t na, const float* b, int64_t nb, DevDecision* d,
+                   cudaStream_t s) {
+    const int64_t nmax = na > nb ? na : nb;
+    dim3 grid(grid_for(nmax / 4 + 1, kThreads, 148 * 8), 2);
+    stats1_kernel<<<grid, kThreads, 0, s>>>(a, na, b, nb, d);
+}
+
+void launch_stats2(const float* a, int64_t na, const float* b, int64_t nb, DevDecision* d,
+                   double t, int target, int always, cudaStream_t s) {
+    const int64_t nmax = na > nb ? na : nb;
+    dim3 grid(grid_for(nmax / 4 + 1, kThreads, 148 * 8), 2);
+    stats2_kernel<<<grid, kThreads, 0, s>>>(a, na, b, nb, d, t, target, always);
+}
+
+void launch_select(DevDecision* d, double t, int target, int forced_scaled, cudaStream_t s) {
+    select_kernel<<<1, 32, 0, s>>>(d, t, target, forced_scaled, 0);
+}
+
+void launch_prep_a(const float* a, int64_t m, int64_t k, int64_t kp, void* hi, void* lo,
+                   const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s) {
+    const int64_t total = m * (kp / 8);
+    if (total <= 0) return;
+    prep_a_kernel<<<grid_for(total, kThreads, 148 * 32), kThreads, 0, s>>>(
+        a, m, 2 * k, kp, hi, lo, d, kind_fixed, corrected);
+}
+
+void launch_prep_b(const float* b, int64_t k, int64_t n, int64_t kp, void* hi, void* lo,
+                   const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s) {
+    if (n <= 0 || kp <= 0) return;
+    dim3 grid(unsigned((n + 31) / 32), unsigned((kp / 2 + 31) / 32));
+    prep_b_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const float2*>(b), k, n, kp, hi, lo, d,
+                                       kind_fixed, corrected);
+}
+
+void launch_cgemm_fp32_ref(const float2* a, const float2* b, float2* c, int64_t m, int64_t n,
+                           int64_t k, cudaStream_t s) {
+    if (m <= 0 || n <= 0) return;
+    dim3 grid(unsigned((n + SB_N - 1) / SB_N), unsigned((m + SB_M - 1) / SB_M));
+    cgemm_fp32_ref_kernel<<<grid, 256, 0, s>>>(a, b, c, m, n, k);
+}
+
+void launch_cgemm_fp64(const float2* a, const float2* b, float2* c, int64_t m, int64_t n,
+                       int64_t k, cudaStream_t s) {
+    if (m <= 0 || n <= 0) return;
+    dim3 grid(unsigned((n + 127) / 128), unsigned(m));
+    cgemm_fp64_kernel<<<grid, 128, 0, s>>>(a, b, c, m, n, k);
+}
+
+void launch_permute(const float2* src, float2* dst, int rank, const int64_t* old_dims,
+                    const int* axis_of, cudaStream_t s) {
+    PermDesc desc{};
+    int64_t total = 1;
+    for (int a = 0; a < rank; ++a) total *= old_dims[a];
+    desc.total = total;
+    if (total == 0) return;
+    // old strides, then merge runs of output axes that are adjacent in the input
+    int64_t old_stride[kMaxRank];
+    if (rank > 0) old_stride[rank - 1] = 1;
+    for (int a = rank - 2; a >= 0; --a) old_stride[a] = old_stride[a + 1] * old_dims[a + 1];
+    int r = 0;
+    for (int a = 0; a < rank; ++a) {
+        const int64_t dim = old_dims[axis_of[a]];
+        if (dim == 1) continue;
+        const int64_t st = old_stride[axis_of[a]];
+        if (r > 0 && desc.in_stride[r - 1] == st * dim) {
+            desc.out_dim[r - 1] *= dim;
+            desc.in_stride[r - 1] = st;
+        } else {
+            desc.out_dim[r] = dim;
+            desc.in_stride[r] = st;
+            ++r;
+        }
+    }
+    desc.rank = r;
+    permute_kernel<<<grid_for(total, kThreads, 148 * 32), kThreads, 0, s>>>(src, dst, desc);
+}
+
+}  // namespace tcec

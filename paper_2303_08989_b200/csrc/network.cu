@@ -1,0 +1,579 @@
+// Device-resident TTGT tensor-network contraction.
+//
+// Host side mirrors reference network.cpp: split_pair / ttgt_contract
+// (:33-85), fold_path / contract_network (:149-177) and greedy_path
+// (:204-315) with integer labels.  The whole fold runs on one stream with no
+// host round trip: every step is (optional) permute(A) -> (optional)
+// permute(B) -> device-dispatched CGEMM into a stream-ordered allocation;
+// per-step decisions land in device decision slots and the decision log is
+// produced once at the end.  Replays over bitstrings reuse one captured CUDA
+// graph of the whole fold (the topology and path do not depend on the
+// bitstring, experiments.cpp:211-213).
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "tcec_handle.h"
+
+namespace tcec {
+
+struct NetNode {
+    std::vector<int> labels;
+    std::vector<int64_t> dims;
+    int64_t size() const {
+        int64_t s = 1;
+        for (auto d : dims) s *= d;
+        return s;
+    }
+};
+
+struct StepPlan {
+    int ia = 0, ib = 0;
+    int64_t m = 1, n = 1, k = 1;
+    bool perm_a = false, perm_b = false;
+    std::vector<int64_t> a_dims, b_dims;
+    std::vector<int> a_axis, b_axis;
+    int64_t a_size = 1, b_size = 1;
+    DispatchPlan dp;
+};
+
+struct FoldPlan {
+    std::vector<StepPlan> steps;
+    std::vector<int> out_labels;
+    std::vector<int64_t> out_dims;
+    size_t ws_bytes = 0;
+};
+
+static bool contains(const std::vector<int>& v, int x) {
+    return std::find(v.begin(), v.end(), x) != v.end();
+}
+
+}  // namespace tcec
+
+struct tcec_network_s {
+    tcec_handle h = nullptr;
+    std::vector<tcec::NetNode> nodes;
+    std::vector<int64_t> offset;     // element offset of node i in node_dev
+    int64_t total = 0;
+    void* node_dev = nullptr;        // all node data, contiguous
+    std::vector<float> host_stage;   // staged host copy (uploaded lazily)
+    bool dirty = true;
+    // cached graph of the last fold (plan signature -> exec)
+    std::string graph_key;
+    cudaGraphExec_t graph = nullptr;
+    void* result_dev = nullptr;      // stable home of the final tensor
+    int64_t result_size = 0;
+    ~tcec_network_s() {
+        if (graph) cudaGraphExecDestroy(graph);
+        if (node_dev) cudaFree(node_dev);
+        if (result_dev) cudaFree(result_dev);
+    }
+};
+
+namespace tcec {
+
+// validate_network, network.cpp:114-127
+static int validate(const tcec_network_s& net) {
+    std::map<int, std::vector<std::pair<int, int64_t>>> occ;
+    for (size_t i = 0; i < net.nodes.size(); ++i) {
+        const NetNode& nd = net.nodes[i];
+        if (nd.labels.size() != nd.dims.size())
+            return set_error(TCEC_ERR_SHAPE_MISMATCH, "tensor labels and dims differ in length");
+        for (auto d : nd.dims)
+            if (d < 1) return set_error(TCEC_ERR_SHAPE_MISMATCH, "tensor extents must be >= 1");
+        for (size_t a = 0; a < nd.labels.size(); ++a)
+            for (size_t b = a + 1; b < nd.labels.size(); ++b)
+                if (nd.labels[a] == nd.labels[b])
+                    return set_error(TCEC_ERR_SHAPE_MISMATCH, "tensor labels must be distinct");
+        for (size_t a = 0; a < nd.labels.size(); ++a)
+            occ[nd.labels[a]].emplace_back(int(i), nd.dims[a]);
+    }
+    for (const auto& [label, o] : occ) {
+        if (o.size() > 2)
+            return set_error(TCEC_ERR_SHAPE_MISMATCH,
+                             "label " + std::to_string(label) + " appears in more than two nodes");
+        if (o.size() == 2 && o[0].second != o[1].second)
+            return set_error(TCEC_ERR_EXTENT_MISMATCH,
+                             "label " + std::to_string(label) + " has mismatched extents");
+    }
+    return TCEC_OK;
+}
+
+// fold_path + ttgt_contract bookkeeping (network.cpp:33-85, :149-168)
+static int build_plan(const tcec_network_s& net, const int* steps, int n_steps,
+                      const tcec_dispatch_config_t& cfg, FoldPlan* out) {
+    if (net.nodes.empty()) return set_error(TCEC_ERR_INVALID_PATH, "empty network");
+    std::map<int, NetNode> live;
+    for (size_t i = 0; i < net.nodes.size(); ++i) live.emplace(int(i), net.nodes[i]);
+    int next_id = int(net.nodes.size());
+    FoldPlan plan;
+    for (int s = 0; s < n_steps; ++s) {
+        const int ia = steps[2 * s], ib = steps[2 * s + 1];
+        auto a_it = live.find(ia), b_it = live.find(ib);
+        if (ia == ib || a_it == live.end() || b_it == live.end())
+            return set_error(TCEC_ERR_INVALID_PATH, "step references a dead or unknown node");
+        const NetNode& A = a_it->second;
+        const NetNode& B = b_it->second;
+        // split_pair: free_a | shared (a's order) | free_b (b's order)
+        std::vector<int> free_a, shared, free_b;
+        std::vector<int64_t> fa_d, sh_d, fb_d;
+        for (size_t i = 0; i < A.labels.size(); ++i) {
+            const int l = A.labels[i];
+            auto pos = std::find(B.labels.begin(), B.labels.end(), l);
+            if (pos != B.labels.end()) {
+                const int64_t bd = B.dims[size_t(pos - B.labels.begin())];
+                if (bd != A.dims[i])
+                    return set_error(TCEC_ERR_EXTENT_MISMATCH,
+                                     "label " + std::to_string(l) + " has extents " +
+                                         std::to_string(A.dims[i]) + " and " + std::to_string(bd));
+                shared.push_back(l);
+                sh_d.push_back(A.dims[i]);
+            } else {
+                free_a.push_back(l);
+                fa_d.push_back(A.dims[i]);
+            }
+        }
+        for (size_t i = 0; i < B.labels.size(); ++i)
+            if (!contains(A.labels, B.labels[i])) {
+                free_b.push_back(B.labels[i]);
+                fb_d.push_back(B.dims[i]);
+            }
+        StepPlan sp;
+        sp.ia = ia;
+        sp.ib = ib;
+        sp.m = sp.n = sp.k = 1;
+        for (auto d : fa_d) sp.m *= d;
+        for (auto d : sh_d) sp.k *= d;
+        for (auto d : fb_d) sp.n *= d;
+        // permutations A -> (free_a | shared), B -> (shared | free_b)
+        std::vector<int> order_a = free_a;
+        order_a.insert(order_a.end(), shared.begin(), shared.end());
+        std::vector<int> order_b = shared;
+        order_b.insert(order_b.end(), free_b.begin(), free_b.end());
+        auto axes = [](const NetNode& t, const std::vector<int>& order, std::vector<int>* ax) {
+            bool identity = true;
+            for (size_t a = 0; a < order.size(); ++a) {
+                const int o = int(std::find(t.labels.begin(), t.labels.end(), order[a]) -
+                                  t.labels.begin());
+                ax->push_back(o);
+                identity = identity && o == int(a);
+            }
+            return !identity;
+        };
+        sp.perm_a = axes(A, order_a, &sp.a_axis);
+        sp.perm_b = axes(B, order_b, &sp.b_axis);
+        sp.a_dims = A.dims;
+        sp.b_dims = B.dims;
+        sp.a_size = A.size();
+        sp.b_size = B.size();
+        sp.dp = plan_dispatch(sp.m, sp.n, sp.k, cfg);
+        if (sp.dp.tier == kTierTc && cfg.k_tile < 1)
+            return set_error(TCEC_ERR_INVALID_ARGUMENT, "k_tile must be >= 1");
+        plan.ws_bytes = std::max(plan.ws_bytes, plan_workspace(sp.dp, sp.m, sp.n));
+        NetNode result;
+        result.labels = free_a;
+        result.labels.insert(result.labels.end(), free_b.begin(), free_b.end());
+        result.dims = fa_d;
+        result.dims.insert(result.dims.end(), fb_d.begin(), fb_d.end());
+        live.erase(ia);
+        live.erase(ib);
+        live.emplace(next_id++, std::move(result));
+        plan.steps.push_back(std::move(sp));
+    }
+    if (live.size() != 1) return set_error(TCEC_ERR_INVALID_PATH, "path leaves more than one node");
+    plan.out_labels = live.begin()->second.labels;
+    plan.out_dims = live.begin()->second.dims;
+    *out = std::move(plan);
+    return TCEC_OK;
+}
+
+static int upload(tcec_network_s& net) {
+    if (!net.dirty) return TCEC_OK;
+    Handle& h = *net.h;
+    if (!net.node_dev) {
+        const cudaError_t e = cudaMalloc(&net.node_dev, size_t(std::max<int64_t>(net.total, 1)) * 8);
+        if (e != cudaSuccess) return cuda_error(e, "node buffer");
+    }
+    const cudaError_t e = cudaMemcpyAsync(net.node_dev, net.host_stage.data(), size_t(net.total) * 8,
+                                          cudaMemcpyHostToDevice, h.stream);
+    if (e != cudaSuccess) return cuda_error(e, "node upload");
+    net.dirty = false;
+    return TCEC_OK;
+}
+
+// Enqueue the fold on the handle stream.  Intermediates are stream-ordered
+// allocations freed as soon as they are consumed; the final tensor is copied
+// into net.result_dev.
+static int enqueue_fold(tcec_network_s& net, const FoldPlan& plan, const tcec_dispatch_config_t& cfg,
+                        DevDecision* dec, void* ws) {
+    Handle& h = *net.h;
+    cudaStream_t s = h.stream;
+    std::map<int, std::pair<float2*, bool>> live;  // id -> (buffer, owned)
+    float2* base = static_cast<float2*>(net.node_dev);
+    for (size_t i = 0; i < net.nodes.size(); ++i) live[int(i)] = {base + net.offset[i], false};
+    int next_id = int(net.nodes.size());
+    for (size_t si = 0; si < plan.steps.size(); ++si) {
+        const StepPlan& sp = plan.steps[si];
+        auto [pa_src, own_a] = live[sp.ia];
+        auto [pb_src, own_b] = live[sp.ib];
+        float2* pa = pa_src;
+        float2* pb = pb_src;
+        cudaError_t e;
+        if (sp.perm_a) {
+            e = cudaMallocAsync(reinterpret_cast<void**>(&pa), size_t(sp.a_size) * 8, s);
+            if (e != cudaSuccess) return cuda_error(e, "permute buffer");
+            launch_permute(pa_src, pa, int(sp.a_dims.size()), sp.a_dims.data(), sp.a_axis.data(), s);
+        }
+        if (sp.perm_b) {
+            e = cudaMallocAsync(reinterpret_cast<void**>(&pb), size_t(sp.b_size) * 8, s);
+            if (e != cudaSuccess) return cuda_error(e, "permute buffer");
+            launch_permute(pb_src, pb, int(sp.b_dims.size()), sp.b_dims.data(), sp.b_axis.data(), s);
+        }
+        float2* pc = nullptr;
+        e = cudaMallocAsync(reinterpret_cast<void**>(&pc), size_t(std::max<int64_t>(sp.m * sp.n, 1)) * 8, s);
+        if (e != cudaSuccess) return cuda_error(e, "step output");
+        const int rc = launch_dispatch(h, reinterpret_cast<const float*>(pa),
+                                       reinterpret_cast<const float*>(pb),
+                                       reinterpret_cast<float*>(pc), sp.m, sp.n, sp.k, cfg, sp.dp,
+                                       dec + si, ws);
+        if (rc) return rc;
+        if (sp.perm_a) cudaFreeAsync(pa, s);
+        if (sp.perm_b) cudaFreeAsync(pb, s);
+        if (own_a) cudaFreeAsync(pa_src, s);
+        if (own_b) cudaFreeAsync(pb_src, s);
+        live.erase(sp.ia);
+        live.erase(sp.ib);
+        live[next_id++] = {pc, true};
+    }
+    auto [res, own] = live.begin()->second;
+    int64_t size = 1;
+    for (auto d : plan.out_dims) size *= d;
+    const cudaError_t e =
+        cudaMemcpyAsync(net.result_dev, res, size_t(size) * 8, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_error(e, "result copy");
+    if (own) cudaFreeAsync(res, s);
+    return TCEC_OK;
+}
+
+static int prepare(tcec_network_s& net, const int* steps, int n_steps,
+                   const tcec_dispatch_config_t& cfg, FoldPlan* plan, DevDecision** dec,
+                   void** ws) {
+    int rc = validate(net);
+    if (rc) return rc;
+    rc = build_plan(net, steps, n_steps, cfg, plan);
+    if (rc) return rc;
+    Handle& h = *net.h;
+    *dec = h.decisions(std::max(n_steps, 1));
+    if (!*dec) return set_error(TCEC_ERR_CUDA, "decision buffer allocation failed");
+    *ws = nullptr;
+    if (plan->ws_bytes) {
+        *ws = h.workspace(plan->ws_bytes);
+        if (!*ws) return set_error(TCEC_ERR_CUDA, "workspace allocation failed");
+    }
+    int64_t size = 1;
+    for (auto d : plan->out_dims) size *= d;
+    if (size > net.result_size) {
+        if (net.result_dev) cudaFree(net.result_dev);
+        const cudaError_t e = cudaMalloc(&net.result_dev, size_t(size) * 8);
+        if (e != cudaSuccess) return cuda_error(e, "result buffer");
+        net.result_size = size;
+        if (net.graph) {
+            cudaGraphExecDestroy(net.graph);
+            net.graph = nullptr;
+            net.graph_key.clear();
+        }
+    }
+    return upload(net);
+}
+
+static std::string plan_key(const int* steps, int n_steps, const tcec_dispatch_config_t& cfg,
+                            const Handle& h, const void* ws, const void* dec) {
+    std::string k(reinterpret_cast<const char*>(steps), size_t(n_steps) * 2 * sizeof(int));
+    k.append(reinterpret_cast<const char*>(&cfg), sizeof(cfg));
+    k.append(reinterpret_cast<const char*>(&h.flush_kblocks), sizeof(int));
+    k.append(reinterpret_cast<const char*>(&ws), sizeof(ws));
+    k.append(reinterpret_cast<const char*>(&dec), sizeof(dec));
+    return k;
+}
+
+// Run the fold, through a cached CUDA graph when possible.
+static int run_fold(tcec_network_s& net, const int* steps, int n_steps,
+                    const tcec_dispatch_config_t& cfg, const FoldPlan& plan, DevDecision* dec,
+                    void* ws, bool use_graph) {
+    Handle& h = *net.h;
+    if (!use_graph) return enqueue_fold(net, plan, cfg, dec, ws);
+    const std::string key = plan_key(steps, n_steps, cfg, h, ws, dec);
+    if (!net.graph || key != net.graph_key) {
+        if (net.graph) {
+            cudaGraphExecDestroy(net.graph);
+            net.graph = nullptr;
+        }
+        cudaGraph_t g = nullptr;
+        cudaError_t e = cudaStreamBeginCapture(h.stream, cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) return cuda_error(e, "graph capture");
+        const int rc = enqueue_fold(net, plan, cfg, dec, ws);
+        e = cudaStreamEndCapture(h.stream, &g);
+        if (rc) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        if (e != cudaSuccess) return cuda_error(e, "graph capture end");
+        e = cudaGraphInstantiate(&net.graph, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return cuda_error(e, "graph instantiate");
+        net.graph_key = key;
+    }
+    const cudaError_t e = cudaGraphLaunch(net.graph, h.stream);
+    if (e != cudaSuccess) return cuda_error(e, "graph launch");
+    return TCEC_OK;
+}
+
+// ------------------------------------------------------------- greedy path
+
+struct Summary {
+    int id;
+    std::vector<int> labels;
+    std::vector<int64_t> dims;
+};
+
+// greedy_simulate, network.cpp:204-298: repeatedly contract the adjacent pair
+// with the smallest result, ties to the lowest (id, id) pair; disconnected
+// components fall back to the smallest outer product
+static void greedy(std::vector<Summary> live, int next_id, std::vector<int>* steps) {
+    while (live.size() > 1) {
+        int64_t best = -1;
+        size_t ba = 0, bb = 0;
+        auto better = [&](int64_t size, size_t x, size_t y) {
+            const std::pair<int, int> ids = std::minmax(live[x].id, live[y].id);
+            if (best < 0) return true;
+            const std::pair<int, int> bids = std::minmax(live[ba].id, live[bb].id);
+            return size < best || (size == best && ids < bids);
+        };
+        for (size_t x = 0; x < live.size(); ++x)
+            for (size_t y = x + 1; y < live.size(); ++y) {
+                int64_t fx = 1, fy = 1;
+                bool adjacent = false;
+                for (size_t i = 0; i < live[x].labels.size(); ++i) {
+                    if (contains(live[y].labels, live[x].labels[i]))
+                        adjacent = true;
+                    else
+                        fx *= live[x].dims[i];
+                }
+                if (!adjacent) continue;
+                for (size_t i = 0; i < live[y].labels.size(); ++i)
+                    if (!contains(live[x].labels, live[y].labels[i])) fy *= live[y].dims[i];
+                if (better(fx * fy, x, y)) {
+                    best = fx * fy;
+                    ba = x;
+                    bb = y;
+                }
+            }
+        if (best < 0) {
+            for (size_t x = 0; x < live.size(); ++x)
+                for (size_t y = x + 1; y < live.size(); ++y) {
+                    int64_t size = 1;
+                    for (auto d : live[x].dims) size *= d;
+                    for (auto d : live[y].dims) size *= d;
+                    if (better(size, x, y)) {
+                        best = size;
+                        ba = x;
+                        bb = y;
+                    }
+                }
+        }
+        Summary& a = live[ba];
+        Summary& b = live[bb];
+        Summary merged;
+        merged.id = next_id++;
+        for (size_t i = 0; i < a.labels.size(); ++i)
+            if (!contains(b.labels, a.labels[i])) {
+                merged.labels.push_back(a.labels[i]);
+                merged.dims.push_back(a.dims[i]);
+            }
+        for (size_t i = 0; i < b.labels.size(); ++i)
+            if (!contains(a.labels, b.labels[i])) {
+                merged.labels.push_back(b.labels[i]);
+                merged.dims.push_back(b.dims[i]);
+            }
+        steps->push_back(std::min(a.id, b.id));
+        steps->push_back(std::max(a.id, b.id));
+        const size_t hi = std::max(ba, bb), lo = std::min(ba, bb);
+        live.erase(live.begin() + long(hi));
+        live.erase(live.begin() + long(lo));
+        live.push_back(std::move(merged));
+    }
+}
+
+__global__ void set_selectors_kernel(float2* node_base, const int64_t* sel_off, int n_sel,
+                                     const uint8_t* bits) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n_sel) return;
+    float2* p = node_base + sel_off[q];
+    const bool one = bits[q] != 0;
+    p[0] = make_float2(one ? 0.0f : 1.0f, 0.0f);
+    p[1] = make_float2(one ? 1.0f : 0.0f, 0.0f);
+}
+
+}  // namespace tcec
+
+using namespace tcec;
+
+extern "C" {
+
+int tcec_network_create(tcec_handle h, int n_nodes, const int* ranks, const int* labels,
+                        const int64_t* dims, tcec_network* out) {
+    if (!h || !out || n_nodes < 0) return set_error(TCEC_ERR_INVALID_ARGUMENT, "bad argument");
+    cudaSetDevice(h->device);
+    auto* net = new tcec_network_s();
+    net->h = h;
+    int64_t pos = 0, off = 0;
+    for (int i = 0; i < n_nodes; ++i) {
+        NetNode nd;
+        for (int a = 0; a < ranks[i]; ++a) {
+            nd.labels.push_back(labels[pos + a]);
+            nd.dims.push_back(dims[pos + a]);
+        }
+        pos += ranks[i];
+        net->offset.push_back(off);
+        off += nd.size();
+        net->nodes.push_back(std::move(nd));
+    }
+    net->total = off;
+    net->host_stage.assign(size_t(2 * std::max<int64_t>(off, 1)), 0.0f);
+    *out = net;
+    return TCEC_OK;
+}
+
+int tcec_network_destroy(tcec_network net) {
+    if (!net) return TCEC_OK;
+    cudaSetDevice(net->h->device);
+    cudaStreamSynchronize(net->h->stream);
+    delete net;
+    return TCEC_OK;
+}
+
+int tcec_network_set_node(tcec_network net, int node, const void* host_data) {
+    if (!net || node < 0 || node >= int(net->nodes.size()))
+        return set_error(TCEC_ERR_INVALID_ARGUMENT, "bad node index");
+    std::memcpy(net->host_stage.data() + 2 * net->offset[size_t(node)], host_data,
+                size_t(net->nodes[size_t(node)].size()) * 8);
+    net->dirty = true;
+    return TCEC_OK;
+}
+
+int tcec_network_greedy_path(tcec_network net, int* steps) {
+    if (!net) return set_error(TCEC_ERR_INVALID_ARGUMENT, "null network");
+    int rc = validate(*net);
+    if (rc) return rc;
+    if (net->nodes.empty()) return set_error(TCEC_ERR_INVALID_PATH, "empty network");
+    std::vector<Summary> live;
+    for (size_t i = 0; i < net->nodes.size(); ++i)
+        live.push_back({int(i), net->nodes[i].labels, net->nodes[i].dims});
+    std::vector<int> out;
+    greedy(std::move(live), int(net->nodes.size()), &out);
+    std::copy(out.begin(), out.end(), steps);
+    return TCEC_OK;
+}
+
+int tcec_contract_network(tcec_network net, const int* steps, int n_steps,
+                          const tcec_dispatch_config_t* cfg, void* out_host, int64_t out_capacity,
+                          int* out_rank, int* out_labels, char* log_lines, int64_t log_capacity) {
+    if (!net || !cfg) return set_error(TCEC_ERR_INVALID_ARGUMENT, "null argument");
+    Handle& h = *net->h;
+    cudaSetDevice(h.device);
+    FoldPlan plan;
+    DevDecision* dec = nullptr;
+    void* ws = nullptr;
+    int rc = prepare(*net, steps, n_steps, *cfg, &plan, &dec, &ws);
+    if (rc) return rc;
+    rc = run_fold(*net, steps, n_steps, *cfg, plan, dec, ws, false);
+    if (rc) return rc;
+    int64_t size = 1;
+    for (auto d : plan.out_dims) size *= d;
+    if (out_capacity < size) return set_error(TCEC_ERR_SHAPE_MISMATCH, "output buffer too small");
+    cudaError_t e = cudaMemcpyAsync(out_host, net->result_dev, size_t(size) * 8,
+                                    cudaMemcpyDeviceToHost, h.stream);
+    if (e != cudaSuccess) return cuda_error(e, "result download");
+    std::vector<DevDecision> dd(plan.steps.size());
+    if (!plan.steps.empty()) {
+        e = cudaMemcpyAsync(dd.data(), dec, sizeof(DevDecision) * dd.size(), cudaMemcpyDeviceToHost,
+                            h.stream);
+        if (e != cudaSuccess) return cuda_error(e, "decision download");
+    }
+    e = cudaStreamSynchronize(h.stream);
+    if (e != cudaSuccess) return cuda_error(e, "contract_network");
+    if (out_rank) *out_rank = int(plan.out_labels.size());
+    if (out_labels) std::copy(plan.out_labels.begin(), plan.out_labels.end(), out_labels);
+    std::string log;
+    for (size_t i = 0; i < plan.steps.size(); ++i) {
+        const StepPlan& sp = plan.steps[i];
+        tcec_dispatch_result_t res;
+        rc = finish_dispatch(sp.dp, dd[i], sp.m, sp.n, sp.k, &res);
+        if (rc) return rc;
+        log += res.line;
+        log += "\n";
+    }
+    if (log_lines && log_capacity > 0) {
+        const size_t nb = std::min(size_t(log_capacity - 1), log.size());
+        std::memcpy(log_lines, log.data(), nb);
+        log_lines[nb] = '\0';
+    }
+    return TCEC_OK;
+}
+
+int tcec_contract_selector_batch(tcec_network net, const int* steps, int n_steps,
+                                 const tcec_dispatch_config_t* cfg, int n_sel, const int* sel_nodes,
+                                 int n_strings, const uint8_t* bits, void* out_host) {
+    if (!net || !cfg) return set_error(TCEC_ERR_INVALID_ARGUMENT, "null argument");
+    Handle& h = *net->h;
+    cudaSetDevice(h.device);
+    for (int q = 0; q < n_sel; ++q) {
+        const int nd = sel_nodes[q];
+        if (nd < 0 || nd >= int(net->nodes.size()) || net->nodes[size_t(nd)].size() != 2)
+            return set_error(TCEC_ERR_SHAPE_MISMATCH, "selector nodes must be rank-1 of extent 2");
+    }
+    FoldPlan plan;
+    DevDecision* dec = nullptr;
+    void* ws = nullptr;
+    int rc = prepare(*net, steps, n_steps, *cfg, &plan, &dec, &ws);
+    if (rc) return rc;
+    int64_t size = 1;
+    for (auto d : plan.out_dims) size *= d;
+    if (size != 1) return set_error(TCEC_ERR_SHAPE_MISMATCH, "amplitude networks must close");
+    cudaStream_t s = h.stream;
+    int64_t* d_off = nullptr;
+    uint8_t* d_bits = nullptr;
+    float2* d_out = nullptr;
+    std::vector<int64_t> off(size_t(std::max(n_sel, 1)));
+    for (int q = 0; q < n_sel; ++q) off[size_t(q)] = net->offset[size_t(sel_nodes[q])];
+    const size_t nbits = size_t(n_sel) * size_t(n_strings);
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d_off), off.size() * 8, s);
+    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&d_bits), std::max<size_t>(nbits, 1), s);
+    if (e == cudaSuccess)
+        e = cudaMallocAsync(reinterpret_cast<void**>(&d_out), size_t(std::max(n_strings, 1)) * 8, s);
+    if (e != cudaSuccess) return cuda_error(e, "batch buffers");
+    cudaMemcpyAsync(d_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice, s);
+    if (nbits) cudaMemcpyAsync(d_bits, bits, nbits, cudaMemcpyHostToDevice, s);
+    for (int i = 0; i < n_strings; ++i) {
+        if (n_sel)
+            set_selectors_kernel<<<(n_sel + 127) / 128, 128, 0, s>>>(
+                static_cast<float2*>(net->node_dev), d_off, n_sel, d_bits + size_t(i) * n_sel);
+        rc = run_fold(*net, steps, n_steps, *cfg, plan, dec, ws, true);
+        if (rc) return rc;
+        cudaMemcpyAsync(d_out + i, net->result_dev, 8, cudaMemcpyDeviceToDevice, s);
+    }
+    e = cudaMemcpyAsync(out_host, d_out, size_t(n_strings) * 8, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_error(e, "batch download");
+    cudaFreeAsync(d_off, s);
+    cudaFreeAsync(d_bits, s);
+    cudaFreeAsync(d_out, s);
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_error(e, "selector batch");
+    // the host copy of the selector slots no longer matches the device
+    net->dirty = true;
+    return TCEC_OK;
+}
+
+}  // extern "C"

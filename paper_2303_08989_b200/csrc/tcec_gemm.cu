@@ -1,0 +1,313 @@
+// TCEC complex GEMM on sm_100a tensor cores (tcgen05 + TMA + TMEM).
+//
+// The complex product C = A B (A m x k, B k x n, interleaved c32) runs as ONE
+// real GEMM C' = A' B' with A' = A viewed as m x 2k (interleaved (re, im)
+// columns) and B' the 2k x 2n block expansion of B (prepared K-major by
+// prep_b_kernel), so C' is exactly the interleaved C.  Each real operand is
+// split into (hi, lo) in FP16 or TF32 (reference lowprec.hpp:84-88) and the
+// error-corrected product (reference gemm.cpp:92-106, kernels_scalar.cpp:102-135,
+// PAPER.md Eq. 2) is
+//
+//     C' = RN( main + corr * 2^-11 ),  main = Ah Bh,  corr = Al Bh + Ah Bl
+//
+// main and corr accumulate in separate TMEM accumulators.  Following the
+// paper's rounding-mode care ("FP32 SIMT cores for addition with
+// RN ... to avoid the RZ rounding inside Tensor Cores"), the main term can be
+// flushed every `flush_kblocks` k-blocks: the MMA warp ping-pongs the main
+// accumulator between two TMEM buffers and the epilogue warps fold each
+// finished partial into a register accumulator with __fadd_rn while the tensor
+// core fills the other buffer.  The correction term stays in TMEM for the whole
+// K (its error is scaled by 2^-11).  The epilogue applies the FP16TCEC_SCALED
+// descale 2^-(sa+sb) (precsel.cpp:171-174) and stores C.
+//
+// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator +
+// single-thread MMA issuer, warps 2..5 = epilogue (TMEM lane quadrant warp%4).
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "tcec_common.cuh"
+#include "tcec_internal.h"
+
+namespace tcec {
+
+namespace {
+
+constexpr int BM = 128;           // rows of C' per CTA (UMMA M)
+constexpr int BN = 128;           // columns of C' per CTA (UMMA N)
+constexpr int kStages = 3;
+constexpr int kTileBytes = 128 * 128;  // one operand tile: 128 rows x 128 B (swizzle-128B)
+constexpr int kThreadsGemm = 192;
+constexpr int kGroupM = 16;       // rasterization: CTAs of a wave share A/B panels in L2
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kColMain0 = 0, kColMain1 = 128, kColCorr = 256;
+
+template <int FMT>
+struct Traits {
+    static constexpr int kElem = FMT == kFp16 ? 2 : 4;
+    static constexpr int kBK = 128 / kElem;              // elements per 128-B row
+    static constexpr int kUK = FMT == kFp16 ? 16 : 8;    // K per tcgen05.mma
+    static constexpr int kKSteps = kBK / kUK;            // 4
+    static constexpr uint32_t kIdesc = umma_idesc<FMT, BM, BN>();
+};
+
+struct alignas(8) GemmSmemTail {
+    uint64_t full[kStages];
+    uint64_t empty[kStages];
+    uint64_t tfull[2];
+    uint64_t tempty[2];
+    uint32_t tmem_base;
+};
+
+constexpr size_t kSmemBytes = 1024 /*align slack*/ + size_t(kStages) * 4 * kTileBytes +
+                              sizeof(GemmSmemTail);
+
+template <int FMT>
+__global__ void __launch_bounds__(kThreadsGemm, 1)
+    tcec_gemm_kernel(const __grid_constant__ CUtensorMap map_ahi,
+                     const __grid_constant__ CUtensorMap map_alo,
+                     const __grid_constant__ CUtensorMap map_bhi,
+                     const __grid_constant__ CUtensorMap map_blo, float* __restrict__ c,
+                     int m, int n2, int kp, const DevDecision* __restrict__ dec, int kind_fixed,
+                     int corrected, int flush_kblocks) {
+    using T = Traits<FMT>;
+    // device-side mode selection: the kernel of the unselected format exits
+    // (the paper's "both kernels launched, one exits early")
+    const int kind = kind_fixed >= 0 ? kind_fixed : dec->kind;
+    const bool mine = FMT == kTf32 ? kind == kKindTf32 : (kind == kKindFp16 || kind == kKindFp16Scaled);
+    if (!mine) return;
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    GemmSmemTail* tail = reinterpret_cast<GemmSmemTail*>(smem + size_t(kStages) * 4 * kTileBytes);
+    auto tile = [&](int stage, int which) -> uint8_t* {
+        return smem + (size_t(stage) * 4 + which) * kTileBytes;
+    };
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    // grouped rasterization over (m_blk, n_blk)
+    const int tiles_m = (m + BM - 1) / BM, tiles_n = (n2 + BN - 1) / BN;
+    const int id = blockIdx.x;
+    const int group = kGroupM * tiles_n;
+    const int first_m = (id / group) * kGroupM;
+    const int gsize = min(tiles_m - first_m, kGroupM);
+    const int m_blk = first_m + (id % group) % gsize;
+    const int n_blk = (id % group) / gsize;
+    const int m0 = m_blk * BM, n0 = n_blk * BN;
+
+    const int nkb = kp / T::kBK;
+    const int F = flush_kblocks > 0 ? flush_kblocks : (nkb > 0 ? nkb : 1);
+    const int nchunks = (nkb + F - 1) / F;
+    const uint32_t stage_bytes = uint32_t(corrected ? 4 : 2) * kTileBytes;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&tail->full[s], 1);
+            mbar_init(&tail->empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tail->tfull[b], 1);
+            mbar_init(&tail->tempty[b], 4);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&map_ahi);
+        tma_prefetch(&map_bhi);
+        if (corrected) {
+            tma_prefetch(&map_alo);
+            tma_prefetch(&map_blo);
+        }
+    }
+    if (warp == 1) tmem_alloc<kTmemCols>(&tail->tmem_base);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tail->tmem_base;
+
+    if (warp == 0) {
+        // ---------------------------------------------------- TMA producer
+        if (lane == 0) {
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int s = kb % kStages;
+                const uint32_t ph = (kb / kStages) & 1;
+                mbar_wait(&tail->empty[s], ph ^ 1);
+                mbar_expect_tx(&tail->full[s], stage_bytes);
+                const int kx = kb * T::kBK;
+                tma_load_2d(tile(s, 0), &map_ahi, &tail->full[s], kx, m0);
+                tma_load_2d(tile(s, 2), &map_bhi, &tail->full[s], kx, n0);
+                if (corrected) {
+                    tma_load_2d(tile(s, 1), &map_alo, &tail->full[s], kx, m0);
+                    tma_load_2d(tile(s, 3), &map_blo, &tail->full[s], kx, n0);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int chunk = kb / F;
+                const int buf = chunk & 1;
+                const bool chunk_start = (kb % F) == 0;
+                if (chunk_start) {
+                    mbar_wait(&tail->tempty[buf], ((chunk >> 1) & 1) ^ 1);
+                    tc_fence_after();
+                }
+                const int s = kb % kStages;
+                mbar_wait(&tail->full[s], (kb / kStages) & 1);
+                tc_fence_after();
+                const uint64_t dah = umma_desc_k_sw128(tile(s, 0));
+                const uint64_t dal = umma_desc_k_sw128(tile(s, 1));
+                const uint64_t dbh = umma_desc_k_sw128(tile(s, 2));
+                const uint64_t dbl = umma_desc_k_sw128(tile(s, 3));
+                const uint32_t d_main = tmem + (buf ? kColMain1 : kColMain0);
+                const uint32_t d_corr = tmem + kColCorr;
+#pragma unroll
+                for (int ks = 0; ks < T::kKSteps; ++ks) {
+                    const uint64_t adv = uint64_t((ks * T::kUK * T::kElem) >> 4);
+                    const uint32_t acc_main = (!chunk_start || ks > 0) ? 1u : 0u;
+                    const uint32_t acc_corr = (kb > 0 || ks > 0) ? 1u : 0u;
+                    if (FMT == kFp16) {
+                        mma_f16(d_main, dah + adv, dbh + adv, T::kIdesc, acc_main);
+                        if (corrected) {
+                            mma_f16(d_corr, dal + adv, dbh + adv, T::kIdesc, acc_corr);
+                            mma_f16(d_corr, dah + adv, dbl + adv, T::kIdesc, 1u);
+                        }
+                    } else {
+                        mma_tf32(d_main, dah + adv, dbh + adv, T::kIdesc, acc_main);
+                        if (corrected) {
+                            mma_tf32(d_corr, dal + adv, dbh + adv, T::kIdesc, acc_corr);
+                            mma_tf32(d_corr, dah + adv, dbl + adv, T::kIdesc, 1u);
+                        }
+                    }
+                }
+                mma_commit(&tail->empty[s]);
+                if ((kb % F) == F - 1 || kb == nkb - 1) mma_commit(&tail->tfull[buf]);
+            }
+        }
+        __syncwarp();
+    } else {
+        // -------------------------------------------------------- epilogue
+        const int q = warp & 3;                 // TMEM lane quadrant of this warp
+        const int row = m0 + 32 * q + lane;
+        const uint32_t lane_base = tmem + (uint32_t(32 * q) << 16);
+        float acc[BN];
+#pragma unroll
+        for (int i = 0; i < BN; ++i) acc[i] = 0.0f;
+        for (int ch = 0; ch < nchunks; ++ch) {
+            const int buf = ch & 1;
+            mbar_wait(&tail->tfull[buf], (ch >> 1) & 1);
+            tc_fence_after();
+            const uint32_t col0 = buf ? kColMain1 : kColMain0;
+#pragma unroll
+            for (int cb = 0; cb < BN / 32; ++cb) {
+                float v[32];
+                tmem_ld32(lane_base + col0 + 32 * cb, v);
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    acc[32 * cb + i] = ch == 0 ? v[i] : __fadd_rn(acc[32 * cb + i], v[i]);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tail->tempty[buf]);
+        }
+        if (corrected && nkb > 0) {
+#pragma unroll
+            for (int cb = 0; cb < BN / 32; ++cb) {
+                float v[32];
+                tmem_ld32(lane_base + kColCorr + 32 * cb, v);
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    acc[32 * cb + i] = __fadd_rn(acc[32 * cb + i], __fmul_rn(v[i], 0x1.0p-11f));
+            }
+        }
+        const bool scaled = kind == kKindFp16Scaled && (dec->scale_a + dec->scale_b) != 0;
+        if (scaled) {
+            const double f = ldexp(1.0, -(dec->scale_a + dec->scale_b));
+#pragma unroll
+            for (int i = 0; i < BN; ++i) acc[i] = scale_pow2(acc[i], f);
+        }
+        if (row < m) {
+            float* crow = c + size_t(row) * n2 + n0;
+            if (n0 + BN <= n2) {
+#pragma unroll
+                for (int i = 0; i < BN; i += 2)
+                    *reinterpret_cast<float2*>(crow + i) = make_float2(acc[i], acc[i + 1]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < BN; ++i)
+                    if (n0 + i < n2) crow[i] = acc[i];
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<kTmemCols>(tmem);
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+bool get_encode() {
+    std::call_once(g_encode_once, [] {
+        cudaDriverEntryPointQueryResult q{};
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    });
+    return g_encode != nullptr;
+}
+
+// 2-D K-major operand: rows x kp elements, box = 128 rows x 128 B, swizzle 128B
+bool make_map(CUtensorMap* map, const void* base, int fmt, int64_t rows, int64_t kp) {
+    const int elem = fmt == kFp16 ? 2 : 4;
+    cuuint64_t dims[2] = {cuuint64_t(kp), cuuint64_t(rows)};
+    cuuint64_t strides[1] = {cuuint64_t(kp) * elem};
+    cuuint32_t box[2] = {cuuint32_t(128 / elem), 128u};
+    cuuint32_t estr[2] = {1u, 1u};
+    const CUresult r = g_encode(
+        map, fmt == kFp16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+        const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int FMT>
+int launch_fmt(const TcecGemmArgs& g, cudaStream_t s) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        const cudaError_t e = cudaFuncSetAttribute(
+            tcec_gemm_kernel<FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes));
+        if (e != cudaSuccess) return int(e);
+        attr_set = true;
+    }
+    CUtensorMap mah, mal, mbh, mbl;
+    const void* alo = g.corrected ? g.a_lo : g.a_hi;
+    const void* blo = g.corrected ? g.b_lo : g.b_hi;
+    if (!make_map(&mah, g.a_hi, FMT, g.m, g.kp) || !make_map(&mal, alo, FMT, g.m, g.kp) ||
+        !make_map(&mbh, g.b_hi, FMT, g.n2, g.kp) || !make_map(&mbl, blo, FMT, g.n2, g.kp))
+        return int(cudaErrorInvalidValue);
+    const int64_t tiles = ((g.m + BM - 1) / BM) * ((g.n2 + BN - 1) / BN);
+    tcec_gemm_kernel<FMT><<<unsigned(tiles), kThreadsGemm, kSmemBytes, s>>>(
+        mah, mal, mbh, mbl, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed, g.corrected,
+        g.flush_kblocks);
+    return int(cudaGetLastError());
+}
+
+}  // namespace
+
+int launch_tcec_gemm(const TcecGemmArgs& g, cudaStream_t s) {
+    if (!get_encode()) return int(cudaErrorNotSupported);
+    if (g.m <= 0 || g.n2 <= 0) return 0;
+    return g.fmt == kFp16 ? launch_fmt<kFp16>(g, s) : launch_fmt<kTf32>(g, s);
+}
+
+}  // namespace tcec

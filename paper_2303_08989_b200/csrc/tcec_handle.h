@@ -1,0 +1,67 @@
+// Handle + dispatch-plan internals shared by the C-ABI translation units.
+#pragma once
+
+#include <algorithm>
+#include <string>
+
+#include "../../include/tcec_b200.h"
+#include "tcec_common.cuh"
+#include "tcec_internal.h"
+
+struct tcec_handle_s {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    int flush_kblocks = 4;  // RN flush of the main term every 4 k-blocks (256 f16 / 128 tf32 K')
+    // operand workspace (split hi/lo planes), grown on demand
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
+    // device decisions (one slot per dispatched GEMM of a contraction)
+    tcec::DevDecision* dec = nullptr;
+    tcec::DevDecision* dec_host = nullptr;  // pinned mirror
+    int dec_slots = 0;
+    // device staging for the host-buffer entry points
+    void* io = nullptr;
+    size_t io_bytes = 0;
+    void* scratch_host = nullptr;  // pinned 4 KiB
+
+    void* workspace(size_t bytes);
+    tcec::DevDecision* decisions(int slots);
+    ~tcec_handle_s();
+};
+
+namespace tcec {
+
+using Handle = tcec_handle_s;
+
+int set_error(int code, const std::string& msg);
+int cuda_error(cudaError_t e, const char* what);
+
+enum Tier : int { kTierInvalid = -1, kTierFp32 = 0, kTierFp64 = 1, kTierTc = 2 };
+
+struct DispatchPlan {
+    int tier = kTierInvalid;
+    int kind = -1;          // host-known ComputeKind, -1 = decided on the device
+    int kind_known = -1;    // kind for reporting when the host knows it
+    int forced = -1;        // ForcedMode or -1
+    int corrected = 1;      // TCEC (1) or uncorrected TC ablation (0)
+    bool stats = false;     // statistics on the device
+    bool forced_scaled = false;
+    int64_t kp = 0;         // padded 2k
+    const char* label = "";
+};
+
+DispatchPlan plan_dispatch(int64_t m, int64_t n, int64_t k, const tcec_dispatch_config_t& cfg);
+size_t plan_workspace(const DispatchPlan& p, int64_t m, int64_t n);
+int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t m, int64_t n,
+                    int64_t k, const tcec_dispatch_config_t& cfg, const DispatchPlan& p,
+                    DevDecision* d, void* ws);
+int finish_dispatch(const DispatchPlan& p, const DevDecision& dd, int64_t m, int64_t n, int64_t k,
+                    tcec_dispatch_result_t* res);
+void format_line(char* out, size_t cap, int64_t m, int64_t n, int64_t k, const char* label, int sa,
+                 int sb, const tcec_exp_stats_t* a, const tcec_exp_stats_t* b, bool has);
+const char* kind_name(int kind);
+const char* forced_name(int f);
+
+}  // namespace tcec

@@ -1,0 +1,94 @@
+// Internal (host-side) declarations shared by the CUDA translation units and the
+// C-ABI layer.  Not part of the public boundary (that is include/tcec_b200.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tcec {
+
+// Device-resident decision of one dispatched CGEMM.  Written by the statistics
+// and selection kernels and read by the operand-preparation and GEMM kernels,
+// so an AUTO dispatch needs no host round trip (paper: the selector runs on
+// the device).  Mirrors ExpStats / ComputeMode
+// (reference precsel.hpp:18-55).
+struct DevStats {
+    unsigned long long n_nonzero, n1, n2, n_total;
+    unsigned int max_bits;      // max |x| bit pattern over nonzero, non-NaN components
+    int stage2_evaluated;
+    int e_max, e_max_valid;
+};
+
+struct DevDecision {
+    DevStats st[2];             // operand A, operand B
+    int kind;                   // ComputeKind (precsel.hpp:45)
+    int scale_a, scale_b;       // ComputeMode shifts
+    int level_a, level_b;       // ToleranceLevel, -1 = logic_error
+    unsigned int overflow;      // split/quantize saturation (DispatchResult::overflow)
+    unsigned int scale_overflow;  // ScaleOverflow (precsel.cpp:54-57)
+    int pad_;
+};
+
+enum Kind : int { kKindFp16 = 0, kKindFp16Scaled = 1, kKindTf32 = 2, kKindFp32 = 3 };
+
+// ----------------------------------------------------------- elementwise
+void launch_quantize(const float* src, float* dst, int64_t n, int fmt, int rz,
+                     unsigned* d_ovf, cudaStream_t s);
+void launch_split_flat(const float* src, float* hi, float* lo, int64_t n, int fmt,
+                       unsigned* d_ovf, cudaStream_t s);
+void launch_scale(const float* src, float* dst, int64_t n, int scale_exp, unsigned* d_nonfinite,
+                  cudaStream_t s);
+void launch_add_sub(const float* a, const float* b, float* dst, int64_t n, int sub, cudaStream_t s);
+
+// ------------------------------------------------------------- statistics
+// stage 1 over both operands (n_a / n_b real components; a null operand is skipped)
+void launch_stats1(const float* a, int64_t n_a, const float* b, int64_t n_b, DevDecision* d,
+                   cudaStream_t s);
+// stage 2; mode 0 = staged (skip when stage 1 passes for t), 1 = always
+void launch_stats2(const float* a, int64_t n_a, const float* b, int64_t n_b, DevDecision* d,
+                   double t, int target, int always, cudaStream_t s);
+// selection (precsel.cpp:106-135); forced_scaled = 1 for ForcedMode::fp16_tcec_scaled
+void launch_select(DevDecision* d, double t, int target, int forced_scaled, cudaStream_t s);
+
+// ------------------------------------------------------- operand layouts
+// A (m x k complex, interleaved) -> A' = m x Kp real, K-major, hi/lo in the
+// decided format (f16 or tf32-in-f32); padded columns are zero.
+// kind_fixed >= 0 overrides the device decision (forced / size-gated modes).
+void launch_prep_a(const float* a, int64_t m, int64_t k, int64_t kp, void* hi, void* lo,
+                   const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s);
+// B (k x n complex) -> B'^T = 2n x Kp real, K-major, with the complex block
+// expansion [[Br, Bi], [-Bi, Br]] so one real GEMM yields interleaved C.
+void launch_prep_b(const float* b, int64_t k, int64_t n, int64_t kp, void* hi, void* lo,
+                   const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s);
+
+// -------------------------------------------------------------- SIMT GEMM
+// FP32_REF complex GEMM, bit-identical to the reference schedule
+// (kernels_scalar.cpp:76-87 + cgemm.cpp:33-44).  Strided operand views allow
+// fused TTGT gathers: element (i, kk) of A is at a[ (row_off(i) + col_off(kk)) ]
+void launch_cgemm_fp32_ref(const float2* a, const float2* b, float2* c, int64_t m, int64_t n,
+                           int64_t k, cudaStream_t s);
+// FP64_ORACLE mode (gemm.cpp:68-74, :111-117)
+void launch_cgemm_fp64(const float2* a, const float2* b, float2* c, int64_t m, int64_t n,
+                       int64_t k, cudaStream_t s);
+
+// ---------------------------------------------------------------- permute
+constexpr int kMaxRank = 48;
+void launch_permute(const float2* src, float2* dst, int rank, const int64_t* old_dims,
+                    const int* axis_of, cudaStream_t s);
+
+// ------------------------------------------------------------ tcgen05 GEMM
+struct TcecGemmArgs {
+    const void* a_hi; const void* a_lo;   // m x kp
+    const void* b_hi; const void* b_lo;   // n2 x kp  (n2 = 2n)
+    float* c;                             // m x n2 (interleaved complex C)
+    int64_t m, n2, kp;
+    const DevDecision* d;                 // device decision (kind / shifts)
+    int kind_fixed;                       // >= 0: host-known kind; -1: read d->kind
+    int fmt;                              // 0 = f16 kernel, 1 = tf32 kernel
+    int corrected;                        // 1 = TCEC (3 products), 0 = TC ablation
+    int flush_kblocks;                    // RN flush interval of the main term, 0 = none
+};
+// returns a cudaError_t
+int launch_tcec_gemm(const TcecGemmArgs& args, cudaStream_t s);
+
+}  // namespace tcec
