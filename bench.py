@@ -1,0 +1,404 @@
+#!/usr/bin/env python
+"""bench.py -- TCEC CGEMM TFLOP/s (+ fidelity) on B200, BASELINE.json configs[1].
+
+Workload (one "step"): one AUTO-0 dispatch_cgemm (precsel.cpp:225-322 semantics:
+device exponent statistics -> selection -> scale+split -> tcgen05 TCEC CGEMM ->
+descale) of the top of the configs[1] sweep, m = n = k = 16384, uniform(-1,1)
+complex64 inputs (synthetic; the selector picks FP16TCEC_SCALED, s = 15).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+value   = useful 8mnk flops / device time (CUDA events on the handle stream), inputs
+          resident in HBM; N>1 runs N independent replicas (replicas only: the
+          standalone CGEMM does not shard) -> whole-job flops / max time.
+e2e     = the same through the host-buffer C-ABI entry point tcec_dispatch_cgemm_host
+          (H2D of A and B from pinned memory + dispatch + D2H of C inside the timed region).
+roofline= the dominant kernel (tcec_gemm_kernel<f16>), tensor-pipe flops 3 x 8mnk per
+          launch over its CUDA-event duration, against the measured dense bf16/fp16 peak.
+cpu_baseline / --impl reference = the reference's own kernels (oracle/_ref, the
+          unmodified mpsgemm sources) row-partitioned over all host threads on a bounded
+          row block of the same CGEMM.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_DEFAULT = 16384
+METRIC = "TCEC CGEMM TFLOP/s (useful 8mnk, AUTO-selected, m=n=k=16384)"
+PAPER_A100_FP16TCEC = 54.2  # BASELINE.md / PAPER.md:246, max measured FP16TCEC CGEMM on A100
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["bf16_tflops"], d["bf16_tflops_sustained"], d["hbm_gbs"], "measured"
+    return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        load = [s for s in sm if s > 0.5 * mx] if mx else sm
+        return {"sm_mhz": float(np.median(load)) if load else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------- CPU reference
+def cpu_reference_sample(a_host, b_host, budget_s=10.0, threads=None, min_rows=None):
+    """The reference's own kernels on a row block of the same CGEMM, all host
+    threads (row partitioning is allowed by kernels.hpp:16-19 and bit-identical).
+    Returns (tflops, rows, seconds, threads, kind)."""
+    import oracle as O
+    threads = threads or os.cpu_count() or 1
+    n = b_host.shape[1]
+    k = b_host.shape[0]
+    ref = O.reference()
+    m = a_host.shape[0]
+    if ref is not None:
+        lib = ref.lib
+        fn = lib.ref_cgemm_rows_threaded_timed
+        fn.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
+                       C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int,
+                       C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        kind = "reference"
+
+        def run(rows):
+            c = np.empty((rows, n), np.complex64)
+            prep, gemm = C.c_double(0), C.c_double(0)
+            fn(a_host.ctypes.data, b_host.ctypes.data, c.ctypes.data, m, n, k, 0, rows,
+               5, 16, threads, C.byref(prep), C.byref(gemm))  # GemmMode::fp16_tcec, k_tile 16
+            return prep.value, gemm.value
+    else:
+        o = O.oracle()
+        kind = "port"
+        threads = 1
+
+        def run(rows):
+            t0 = time.perf_counter()
+            o.cgemm(a_host[:rows], b_host, "FP16TCEC")
+            return 0.0, time.perf_counter() - t0
+    if min_rows is None:
+        _, g1 = run(max(1, threads))
+        per_row = g1 / max(1, threads)
+        rows = int(max(threads, min(m, budget_s / max(per_row, 1e-9))))
+        rows = max(threads, (rows // threads) * threads)
+    else:
+        rows = min_rows
+    prep, gemm = run(rows)
+    # the full CGEMM runs the O(n^2) preparation once and the row loop m/rows times
+    full_s = prep + gemm * m / rows
+    return 8.0 * m * n * k / full_s / 1e12, rows, prep + gemm, threads, kind, prep, gemm
+
+
+# ---------------------------------------------------------------- helpers
+def dist_setup(gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def host_inputs(n, seed):
+    import torch
+    g = np.random.default_rng(seed)
+    pin = torch.cuda.is_available()
+    a = torch.empty((n, n), dtype=torch.complex64, pin_memory=pin)
+    b = torch.empty((n, n), dtype=torch.complex64, pin_memory=pin)
+    for t in (a, b):
+        v = t.numpy().view(np.float32)
+        for r0 in range(0, n, 1024):
+            v[r0:r0 + 1024] = g.random((min(1024, n - r0), 2 * n), dtype=np.float32) * 2 - 1
+    return a, b
+
+
+# ------------------------------------------------------------------- arms
+def run_ours(args):
+    import torch
+    from paper_2303_08989_b200 import Handle, make_config
+    world, rank, local = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    n = args.n
+    h = Handle(local)
+    stream = torch.cuda.ExternalStream(h.stream_ptr, device=dev)
+    a_h, b_h = host_inputs(n, 1 + n + rank)
+    a = a_h.to(dev)
+    b = b_h.to(dev)
+    c = torch.empty((n, n), dtype=torch.complex64, device=dev)
+    cfg = make_config()  # AUTO-0, default SelectionPolicy (size_auto 2048 <= n)
+    flops = 8.0 * n * n * n
+
+    for _ in range(args.warmup):
+        _, res = h.dispatch_cgemm(a, b, cfg, out=c)
+    decision = res.line
+    kind = res.line.split(",")[3]
+
+    # ---- device-resident timed region
+    h.profile(True)
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            h.dispatch_cgemm(a, b, cfg, out=c)
+        e1.record(stream)
+        e1.synchronize()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / args.steps
+    stage, cnt = h.profile_read()
+    h.profile(False)
+    ms_max = max_over_ranks(ms, world)
+    gemm_ms = stage["gemm"] / max(cnt, 1)
+
+    # ---- end to end through the host-buffer C-ABI
+    a_np, b_np = a_h.numpy(), b_h.numpy()
+    c_h = torch.empty((n, n), dtype=torch.complex64, pin_memory=True)
+    c_np = c_h.numpy()
+    h.dispatch_cgemm_host(a_np, b_np, cfg, out=c_np)  # allocate staging once
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(args.steps):
+        h.dispatch_cgemm_host(a_np, b_np, cfg, out=c_np)
+    e1.record(stream)
+    e1.synchronize()
+    e2e_ms = max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3) / args.steps
+    e2e_ms = max_over_ranks(e2e_ms, world)
+
+    # ---- fidelity: sampled rows vs complex128, and the bit-exact FP32 tier on the same rows
+    rows = torch.from_numpy(np.random.default_rng(3).choice(n, 16, replace=False)).to(dev)
+    ref = a[rows].to(torch.complex128) @ b.to(torch.complex128)
+    err = float(torch.linalg.norm(c[rows].to(torch.complex128) - ref) / torch.linalg.norm(ref))
+    c32, _ = h.cgemm(a[rows].contiguous(), b, "FP32_REF")
+    err32 = float(torch.linalg.norm(c32.to(torch.complex128) - ref) / torch.linalg.norm(ref))
+    del ref
+
+    # ---- small sweep (configs[1] 1024..8192), AUTO and forced formats
+    sweep = {}
+    if args.sweep and rank == 0:
+        for sn in (1024, 2048, 4096, 8192):
+            sa = torch.rand(sn, sn, 2, device=dev).mul_(2).sub_(1).view(torch.complex64)[..., 0].contiguous()
+            sb = torch.rand(sn, sn, 2, device=dev).mul_(2).sub_(1).view(torch.complex64)[..., 0].contiguous()
+            sc = torch.empty(sn, sn, dtype=torch.complex64, device=dev)
+            row = {}
+            for label, sc_cfg in (("AUTO-0", make_config()), ("FP16TCEC", make_config(force="FP16TCEC")),
+                                  ("TF32TCEC", make_config(force="TF32TCEC")),
+                                  ("FP32_REF", make_config(force="FP32_REF"))):
+                reps = 2 if label == "FP32_REF" else 5
+                for _ in range(2):
+                    _, r = h.dispatch_cgemm(sa, sb, sc_cfg, out=sc)
+                torch.cuda.synchronize(dev)
+                e0.record(stream)
+                for _ in range(reps):
+                    h.dispatch_cgemm(sa, sb, sc_cfg, out=sc)
+                e1.record(stream)
+                e1.synchronize()
+                row[label] = round(8.0 * sn ** 3 / (e0.elapsed_time(e1) / reps * 1e-3) / 1e12, 2)
+                if label == "AUTO-0":
+                    row["AUTO-0 mode"] = r.line.split(",")[3]
+            sweep[str(sn)] = row
+            del sa, sb, sc
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        tf, r_rows, dt, thr, kindc, prep, gemm = cpu_reference_sample(a_np, b_np,
+                                                                     budget_s=args.cpu_budget)
+        cpu = {"value": round(tf, 6), "unit": "TFLOP/s", "cores": thr, "kind": kindc,
+               "sample": f"rows 0..{r_rows} of the same m=n=k={n} CGEMM with the reference's "
+                         f"FP16TCEC kernels on {thr} threads: operand prep {prep:.1f} s + row "
+                         f"GEMM {gemm:.1f} s, extrapolated to all {n} rows (prep once)"}
+
+    if rank == 0:
+        bpk, bps, hbm, src = peaks()
+        tensor_flops = 3.0 * flops  # hi*hi, lo*hi, hi*lo tensor-core products per launch
+        achieved = tensor_flops / (gemm_ms * 1e-3) / 1e12
+        peak = bps if kind != "TF32TCEC" else bps / 2
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp)).get(f"tcec_gemm_f16_n{n}")
+        value = world * flops / (ms_max * 1e-3) / 1e12
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 3),
+            "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": round(value / PAPER_A100_FP16TCEC, 2),
+            "baseline_ref": "54.2 TFLOP/s FP16TCEC CGEMM max on A100 (PAPER.md:246)",
+            "dtype": "c64 (FP32 via error-corrected FP16 tensor cores)",
+            "data": "synthetic uniform(-1,1) complex64 (numpy default_rng), resident in HBM",
+            "config": {"workload": f"configs[1] CGEMM sweep top: m=n=k={n}, AUTO-0 "
+                                   f"(default SelectionPolicy) -> {kind}",
+                       "decision": decision, "parallelism": f"replicas x{world}",
+                       "l2": "inputs (2 GiB per operand) exceed the 126 MB L2",
+                       "flush_kblocks": h.flush_kblocks},
+            "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "kernel": "tcec_gemm_kernel<f16>",
+                         "note": f"3 x 8mnk tensor-pipe flops per launch / CUDA-event time; "
+                                 f"peak = {src} dense bf16 sustained (fp16 = bf16 rate)"},
+            "stages_ms": {k2: round(v / max(cnt, 1), 3) for k2, v in stage.items()},
+            "fidelity": {"rel_err": err, "fp32_ref_rel_err": err32,
+                         "ratio_vs_fp32": round(err / err32, 3) if err32 else None,
+                         "sample": "16 random rows vs complex128"},
+            "e2e": {"value": round(world * flops / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
+                    "h2d_bytes_per_step": 2 * n * n * 8, "d2h_bytes_per_step": n * n * 8},
+            "gpu_launches": 7 * args.steps,
+            "clocks": clk.summary(),
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        if sweep:
+            line["sweep_tflops"] = sweep
+        print(json.dumps(line), flush=True)
+    h.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch  # noqa: F401  (pinned inputs share the generator with our arm)
+    n = args.n
+    a_h, b_h = host_inputs(n, 1 + n)
+    a_np, b_np = a_h.numpy(), b_h.numpy()
+    # calibrate the bounded per-step sample once, then warm up and time
+    _, rows, _, thr, kind, _, _ = cpu_reference_sample(a_np, b_np, budget_s=args.ref_step_s)
+    for _ in range(args.warmup):
+        cpu_reference_sample(a_np, b_np, min_rows=rows)
+    vals, wall = [], 0.0
+    for _ in range(args.steps):
+        tf, _, dt, _, _, _, _ = cpu_reference_sample(a_np, b_np, min_rows=rows)
+        vals.append(tf)
+        wall += dt
+    value = float(np.mean(vals))
+    ms = 8.0 * n * n * n / (value * 1e12) * 1e3  # full-CGEMM time implied by the sample
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "TFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c64 (FP32 via error-corrected FP16 emulation, reference CPU)",
+        "data": "synthetic uniform(-1,1) complex64",
+        "config": {"workload": f"configs[1] CGEMM sweep top: m=n=k={n}, AUTO-0 -> FP16TCEC_SCALED",
+                   "parallelism": "host threads"},
+        "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": thr, "kind": kind,
+                         "sample": f"{rows} rows of the m=n=k={n} CGEMM per step (FP16TCEC "
+                                   f"kernels of the unmodified reference, row-partitioned over "
+                                   f"{thr} threads; O(n^2) operand prep timed per step and "
+                                   f"amortized over the full {n} rows); {wall / args.steps:.1f} s "
+                                   f"wall per step"},
+        "e2e": {"value": round(value, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--n", type=int, default=N_DEFAULT)
+    p.add_argument("--no-sweep", dest="sweep", action="store_false")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-budget", type=float, default=12.0)
+    p.add_argument("--ref-step-s", type=float, default=8.0)
+    args = p.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

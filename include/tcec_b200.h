@@ -63,6 +63,13 @@ int tcec_synchronize(tcec_handle h);
  * device counterpart of TilingConfig::k_tile (gemm.hpp:28-30). */
 int tcec_set_flush_kblocks(tcec_handle h, int kblocks);
 int tcec_get_flush_kblocks(tcec_handle h);
+/* stage tracing (the device counterpart of DecisionRecord::wall_ms,
+ * precsel.hpp:92-101): when enabled, every synchronous tcec_dispatch_cgemm
+ * records CUDA events around (statistics + selection), (operand preparation)
+ * and (tensor-core / SIMT GEMM) on the handle stream; read returns the summed
+ * milliseconds of the three stages and the number of dispatches; enable resets. */
+int tcec_profile_enable(tcec_handle h, int on);
+int tcec_profile_read(tcec_handle h, double* stage_ms, int64_t* count);
 
 /* ------------------------------------------------ format emulation (device)
  * KernelTable entries, kernels.hpp:20-63; bit-identical to the reference

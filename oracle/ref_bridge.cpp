@@ -221,6 +221,29 @@ void ref_permute_c64(const float* src, float* dst, int rank, const std::int64_t*
     std::memcpy(dst, p.data.data(), sizeof(float) * 2 * p.data.size());
 }
 
+// experiments.cpp:27-31 random_uniform_matrix with Rng(seed)
+void ref_rng_uniform_c32(std::uint64_t seed, std::int64_t rows, std::int64_t cols, float* out) {
+    Rng rng(seed);
+    for (std::int64_t i = 0; i < rows * cols; ++i) {
+        const std::complex<float> v{rng.uniform_pm1f(), rng.uniform_pm1f()};
+        out[2 * i] = v.real();
+        out[2 * i + 1] = v.imag();
+    }
+}
+
+// raw engine outputs / gaussian draws for pinning the generator
+void ref_rng_stream(std::uint64_t seed, int kind, std::int64_t n, double* out) {
+    Rng rng(seed);
+    for (std::int64_t i = 0; i < n; ++i) {
+        switch (kind) {
+        case 0: out[i] = static_cast<double>(rng.next_u64() >> 11); break;
+        case 1: out[i] = static_cast<double>(rng.next_below(1000003)); break;
+        case 2: out[i] = rng.gaussian(1e-2); break;
+        default: out[i] = rng.uniform01(); break;
+        }
+    }
+}
+
 // ---------------------------------------------------------------- circuits
 
 // save_circuit / save_network text of rqc_rectangular + circuit_to_network;
@@ -313,9 +336,25 @@ int ref_rqc_amplitude_sv_oracle(int rows, int cols, int depth, std::uint64_t see
 // across host threads.  kernels.hpp:16-19 allows row partitioning (k order is
 // untouched), so the result is bit-identical to the single-threaded cgemm.
 // Computes output rows [row_begin, row_end) of C (m x n) into c (row-local).
+int ref_cgemm_rows_threaded_timed(const float* a, const float* b, float* c, std::int64_t m,
+                                  std::int64_t n, std::int64_t k, std::int64_t row_begin,
+                                  std::int64_t row_end, int mode, int k_tile, int n_threads,
+                                  double* prep_s, double* gemm_s);
+
 int ref_cgemm_rows_threaded(const float* a, const float* b, float* c, std::int64_t m,
                             std::int64_t n, std::int64_t k, std::int64_t row_begin,
                             std::int64_t row_end, int mode, int k_tile, int n_threads) {
+    return ref_cgemm_rows_threaded_timed(a, b, c, m, n, k, row_begin, row_end, mode, k_tile,
+                                         n_threads, nullptr, nullptr);
+}
+
+// Same, reporting the O(n^2) operand preparation (deinterleave + split/quantize of
+// the B planes and the A rows) and the O(rows n k) GEMM wall times separately.
+int ref_cgemm_rows_threaded_timed(const float* a, const float* b, float* c, std::int64_t m,
+                                  std::int64_t n, std::int64_t k, std::int64_t row_begin,
+                                  std::int64_t row_end, int mode, int k_tile, int n_threads,
+                                  double* prep_s, double* gemm_s) {
+    const auto t_start = std::chrono::steady_clock::now();
     const auto& kt = kernels::active_kernels();
     const std::int64_t rows = row_end - row_begin;
     (void)m;
@@ -353,6 +392,7 @@ int ref_cgemm_rows_threaded(const float* a, const float* b, float* c, std::int64
     conv(bre, brh, brl);
     conv(bim, bih, bil);
     std::vector<float> p(static_cast<std::size_t>(4 * rows * n));
+    const auto t_prep = std::chrono::steady_clock::now();
     float* p1 = p.data();
     float* p2 = p1 + rows * n;
     float* p3 = p2 + rows * n;
@@ -380,11 +420,16 @@ int ref_cgemm_rows_threaded(const float* a, const float* b, float* c, std::int64
         if (r1 > r0) pool.emplace_back(worker, r0, r1);
     }
     for (auto& th : pool) th.join();
+    const auto t_gemm = std::chrono::steady_clock::now();
     // complex assembly (cgemm.cpp:38-44)
     for (std::int64_t i = 0; i < rows * n; ++i) {
         c[2 * i] = p1[i] - p2[i];
         c[2 * i + 1] = p3[i] + p4[i];
     }
+    if (prep_s) prep_s[0] = std::chrono::duration<double>(t_prep - t_start).count();
+    if (gemm_s)
+        gemm_s[0] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_prep).count();
+    (void)t_gemm;
     return ovf ? 1 : 0;
 }
 

@@ -97,6 +97,7 @@ _lib = None
 def header_symbols() -> list[str]:
     """Every function the public header declares."""
     text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
     return sorted(set(re.findall(r"\b(tcec_[a-z0-9_]+)\s*\(", text)))
 
 
@@ -120,6 +121,8 @@ def load() -> C.CDLL:
         "tcec_synchronize": ([vp], i32),
         "tcec_set_flush_kblocks": ([vp, i32], i32),
         "tcec_get_flush_kblocks": ([vp], i32),
+        "tcec_profile_enable": ([vp, i32], i32),
+        "tcec_profile_read": ([vp, C.POINTER(dbl), C.POINTER(i64)], i32),
         "tcec_quantize_buf": ([vp, vp, vp, i64, i32, i32, ip], i32),
         "tcec_split_buf": ([vp, vp, vp, vp, i64, i32, ip], i32),
         "tcec_scale_buf": ([vp, vp, vp, i64, i32], i32),

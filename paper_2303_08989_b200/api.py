@@ -98,6 +98,17 @@ class Handle:
     def flush_kblocks(self, v: int) -> None:
         check(self.lib.tcec_set_flush_kblocks(self.h, int(v)))
 
+    def profile(self, on: bool = True) -> None:
+        """Enable (and reset) per-stage CUDA-event tracing of dispatches."""
+        check(self.lib.tcec_profile_enable(self.h, int(on)))
+
+    def profile_read(self):
+        """-> ({'stats': ms, 'prep': ms, 'gemm': ms}, n_dispatches)"""
+        arr = (C.c_double * 3)()
+        cnt = C.c_int64(0)
+        check(self.lib.tcec_profile_read(self.h, arr, C.byref(cnt)))
+        return {"stats": arr[0], "prep": arr[1], "gemm": arr[2]}, cnt.value
+
     # ------------------------------------------------------ KernelTable level
     def _out_like(self, x):
         return _torch().empty_like(x)

@@ -142,6 +142,8 @@ int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t
     if (p.tier == kTierInvalid) return set_error(TCEC_ERR_INVALID_ARGUMENT, "unknown forced mode");
     if (p.tier == kTierTc && cfg.k_tile < 1)
         return set_error(TCEC_ERR_INVALID_ARGUMENT, "k_tile must be >= 1");
+    const bool prof = h.prof && h.ev[0];
+    if (prof) cudaEventRecord(h.ev[0], s);
     cudaMemsetAsync(d, 0, sizeof(DevDecision), s);
     if (p.stats) {
         launch_stats1(a, 2 * m * k, b, 2 * k * n, d, s);
@@ -149,20 +151,30 @@ int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t
         launch_stats2(a, 2 * m * k, b, 2 * k * n, d, t, cfg.target_max_exponent, 0, s);
         launch_select(d, cfg.threshold_t, cfg.target_max_exponent, p.forced_scaled ? 1 : 0, s);
     }
-    if (m == 0 || n == 0) return TCEC_OK;
+    if (prof) cudaEventRecord(h.ev[1], s);
+    if (m == 0 || n == 0 || k == 0 || p.tier != kTierTc) {
+        if (prof) cudaEventRecord(h.ev[2], s);
+    }
+    if (m == 0 || n == 0) {
+        if (prof) cudaEventRecord(h.ev[3], s);
+        return TCEC_OK;
+    }
     if (k == 0) {
         // every mode yields +0 (the reference chains start at 0.0f)
         cudaMemsetAsync(c, 0, size_t(m) * n * 8, s);
+        if (prof) cudaEventRecord(h.ev[3], s);
         return TCEC_OK;
     }
     switch (p.tier) {
     case kTierFp32:
         launch_cgemm_fp32_ref(reinterpret_cast<const float2*>(a), reinterpret_cast<const float2*>(b),
                               reinterpret_cast<float2*>(c), m, n, k, s);
+        if (prof) cudaEventRecord(h.ev[3], s);
         return TCEC_OK;
     case kTierFp64:
         launch_cgemm_fp64(reinterpret_cast<const float2*>(a), reinterpret_cast<const float2*>(b),
                           reinterpret_cast<float2*>(c), m, n, k, s);
+        if (prof) cudaEventRecord(h.ev[3], s);
         return TCEC_OK;
     default: break;
     }
@@ -177,6 +189,7 @@ int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t
     void* blo = w + 2 * abytes + bbytes;
     launch_prep_a(a, m, k, p.kp, ahi, alo, d, p.kind, p.corrected, s);
     launch_prep_b(b, k, n, p.kp, bhi, blo, d, p.kind, p.corrected, s);
+    if (prof) cudaEventRecord(h.ev[2], s);
     TcecGemmArgs g{};
     g.a_hi = ahi;
     g.a_lo = alo;
@@ -202,6 +215,7 @@ int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t
         const int e = launch_tcec_gemm(g, s);
         if (e) return cuda_error(cudaError_t(e), "tcec_gemm tf32");
     }
+    if (prof) cudaEventRecord(h.ev[3], s);
     return TCEC_OK;
 }
 
@@ -281,6 +295,8 @@ tcec_handle_s::~tcec_handle_s() {
     if (dec_host) cudaFreeHost(dec_host);
     if (scratch_host) cudaFreeHost(scratch_host);
     if (own_stream) cudaStreamDestroy(own_stream);
+    for (auto& e : ev)
+        if (e) cudaEventDestroy(e);
 }
 
 
@@ -370,6 +386,23 @@ int tcec_set_flush_kblocks(tcec_handle h, int kblocks) {
 }
 
 int tcec_get_flush_kblocks(tcec_handle h) { return h ? h->flush_kblocks : -1; }
+
+int tcec_profile_enable(tcec_handle h, int on) {
+    CHECK_HANDLE(h);
+    if (on && !h->ev[0])
+        for (auto& e : h->ev) CUDA_TRY(cudaEventCreate(&e));
+    h->prof = on != 0;
+    h->prof_ms[0] = h->prof_ms[1] = h->prof_ms[2] = 0.0;
+    h->prof_count = 0;
+    return TCEC_OK;
+}
+
+int tcec_profile_read(tcec_handle h, double* stage_ms, int64_t* count) {
+    CHECK_HANDLE(h);
+    for (int i = 0; i < 3; ++i) stage_ms[i] = h->prof_ms[i];
+    if (count) *count = h->prof_count;
+    return TCEC_OK;
+}
 
 // ------------------------------------------------------------ KernelTable
 
@@ -560,6 +593,13 @@ int tcec_dispatch_cgemm(tcec_handle h, const void* a, const void* b, void* c, in
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(h->dec_host, d, sizeof(DevDecision), cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (h->prof && h->ev[0]) {
+        for (int i = 0; i < 3; ++i) {
+            float ms = 0.0f;
+            if (cudaEventElapsedTime(&ms, h->ev[i], h->ev[i + 1]) == cudaSuccess) h->prof_ms[i] += ms;
+        }
+        ++h->prof_count;
+    }
     return finish_dispatch(p, *h->dec_host, m, n, k, res);
 }
 

@@ -424,8 +424,9 @@ extern "C" {
 
 int tcec_network_create(tcec_handle h, int n_nodes, const int* ranks, const int* labels,
                         const int64_t* dims, tcec_network* out) {
-    if (!h || !out || n_nodes < 0) return set_error(TCEC_ERR_INVALID_ARGUMENT, "bad argument");
-    cudaSetDevice(h->device);
+    // h may be NULL for planning-only use (greedy_path); contraction needs a handle
+    if (!out || n_nodes < 0) return set_error(TCEC_ERR_INVALID_ARGUMENT, "bad argument");
+    if (h) cudaSetDevice(h->device);
     auto* net = new tcec_network_s();
     net->h = h;
     int64_t pos = 0, off = 0;
@@ -448,8 +449,10 @@ int tcec_network_create(tcec_handle h, int n_nodes, const int* ranks, const int*
 
 int tcec_network_destroy(tcec_network net) {
     if (!net) return TCEC_OK;
-    cudaSetDevice(net->h->device);
-    cudaStreamSynchronize(net->h->stream);
+    if (net->h) {
+        cudaSetDevice(net->h->device);
+        cudaStreamSynchronize(net->h->stream);
+    }
     delete net;
     return TCEC_OK;
 }
@@ -481,6 +484,7 @@ int tcec_contract_network(tcec_network net, const int* steps, int n_steps,
                           const tcec_dispatch_config_t* cfg, void* out_host, int64_t out_capacity,
                           int* out_rank, int* out_labels, char* log_lines, int64_t log_capacity) {
     if (!net || !cfg) return set_error(TCEC_ERR_INVALID_ARGUMENT, "null argument");
+    if (!net->h) return set_error(TCEC_ERR_CUDA, "network has no device handle");
     Handle& h = *net->h;
     cudaSetDevice(h.device);
     FoldPlan plan;
@@ -527,6 +531,7 @@ int tcec_contract_selector_batch(tcec_network net, const int* steps, int n_steps
                                  const tcec_dispatch_config_t* cfg, int n_sel, const int* sel_nodes,
                                  int n_strings, const uint8_t* bits, void* out_host) {
     if (!net || !cfg) return set_error(TCEC_ERR_INVALID_ARGUMENT, "null argument");
+    if (!net->h) return set_error(TCEC_ERR_CUDA, "network has no device handle");
     Handle& h = *net->h;
     cudaSetDevice(h.device);
     for (int q = 0; q < n_sel; ++q) {

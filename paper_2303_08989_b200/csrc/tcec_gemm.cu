@@ -37,10 +37,13 @@ constexpr int BM = 128;           // rows of C' per CTA (UMMA M)
 constexpr int BN = 128;           // columns of C' per CTA (UMMA N)
 constexpr int kStages = 3;
 constexpr int kTileBytes = 128 * 128;  // one operand tile: 128 rows x 128 B (swizzle-128B)
-constexpr int kThreadsGemm = 192;
+constexpr int kEpiWarps = 8;      // 2 warps per TMEM lane quadrant, 64 columns each
+constexpr int kThreadsGemm = 64 + 32 * kEpiWarps;
 constexpr int kGroupM = 16;       // rasterization: CTAs of a wave share A/B panels in L2
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kColMain0 = 0, kColMain1 = 128, kColCorr = 256;
+constexpr int kMainBufs = 3;      // ping-pong-pong main partials: cols 0, 128, 256
+constexpr uint32_t kColCorr = 384;
+constexpr int kCStride = BN + 4;  // padded smem row (floats) of the staged C tile
 
 template <int FMT>
 struct Traits {
@@ -54,13 +57,19 @@ struct Traits {
 struct alignas(8) GemmSmemTail {
     uint64_t full[kStages];
     uint64_t empty[kStages];
-    uint64_t tfull[2];
-    uint64_t tempty[2];
+    uint64_t tfull[kMainBufs];
+    uint64_t tempty[kMainBufs];
     uint32_t tmem_base;
 };
 
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + size_t(kStages) * 4 * kTileBytes +
                               sizeof(GemmSmemTail);
+static_assert(size_t(BM) * kCStride * 4 <= size_t(kStages) * 4 * kTileBytes,
+              "C staging tile must fit in the operand stages");
+
+TCEC_DEV void epi_bar_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+}
 
 template <int FMT>
 __global__ void __launch_bounds__(kThreadsGemm, 1)
@@ -107,9 +116,9 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
             mbar_init(&tail->full[s], 1);
             mbar_init(&tail->empty[s], 1);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < kMainBufs; ++b) {
             mbar_init(&tail->tfull[b], 1);
-            mbar_init(&tail->tempty[b], 4);
+            mbar_init(&tail->tempty[b], kEpiWarps);
         }
         fence_barrier_init();
     }
@@ -149,10 +158,10 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
         if (lane == 0) {
             for (int kb = 0; kb < nkb; ++kb) {
                 const int chunk = kb / F;
-                const int buf = chunk & 1;
+                const int buf = chunk % kMainBufs;
                 const bool chunk_start = (kb % F) == 0;
                 if (chunk_start) {
-                    mbar_wait(&tail->tempty[buf], ((chunk >> 1) & 1) ^ 1);
+                    mbar_wait(&tail->tempty[buf], ((chunk / kMainBufs) & 1) ^ 1);
                     tc_fence_after();
                 }
                 const int s = kb % kStages;
@@ -162,7 +171,7 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
                 const uint64_t dal = umma_desc_k_sw128(tile(s, 1));
                 const uint64_t dbh = umma_desc_k_sw128(tile(s, 2));
                 const uint64_t dbl = umma_desc_k_sw128(tile(s, 3));
-                const uint32_t d_main = tmem + (buf ? kColMain1 : kColMain0);
+                const uint32_t d_main = tmem + uint32_t(buf * BN);
                 const uint32_t d_corr = tmem + kColCorr;
 #pragma unroll
                 for (int ks = 0; ks < T::kKSteps; ++ks) {
@@ -190,21 +199,24 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
         __syncwarp();
     } else {
         // -------------------------------------------------------- epilogue
-        const int q = warp & 3;                 // TMEM lane quadrant of this warp
-        const int row = m0 + 32 * q + lane;
-        const uint32_t lane_base = tmem + (uint32_t(32 * q) << 16);
-        float acc[BN];
+        // warp w owns TMEM lanes 32*(w%4).. (the hardware quadrant rule) and
+        // the 64-column half (w-2)/4 of the tile
+        const int q = warp & 3;
+        const int half = (warp - 2) >> 2;
+        const int rloc = 32 * q + lane;
+        const uint32_t lane_base = tmem + (uint32_t(32 * q) << 16) + uint32_t(64 * half);
+        constexpr int kCols = BN / 2;
+        float acc[kCols];
 #pragma unroll
-        for (int i = 0; i < BN; ++i) acc[i] = 0.0f;
+        for (int i = 0; i < kCols; ++i) acc[i] = 0.0f;
         for (int ch = 0; ch < nchunks; ++ch) {
-            const int buf = ch & 1;
-            mbar_wait(&tail->tfull[buf], (ch >> 1) & 1);
+            const int buf = ch % kMainBufs;
+            mbar_wait(&tail->tfull[buf], (ch / kMainBufs) & 1);
             tc_fence_after();
-            const uint32_t col0 = buf ? kColMain1 : kColMain0;
 #pragma unroll
-            for (int cb = 0; cb < BN / 32; ++cb) {
+            for (int cb = 0; cb < kCols / 32; ++cb) {
                 float v[32];
-                tmem_ld32(lane_base + col0 + 32 * cb, v);
+                tmem_ld32(lane_base + uint32_t(buf * BN + 32 * cb), v);
 #pragma unroll
                 for (int i = 0; i < 32; ++i)
                     acc[32 * cb + i] = ch == 0 ? v[i] : __fadd_rn(acc[32 * cb + i], v[i]);
@@ -215,9 +227,9 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
         }
         if (corrected && nkb > 0) {
 #pragma unroll
-            for (int cb = 0; cb < BN / 32; ++cb) {
+            for (int cb = 0; cb < kCols / 32; ++cb) {
                 float v[32];
-                tmem_ld32(lane_base + kColCorr + 32 * cb, v);
+                tmem_ld32(lane_base + kColCorr + uint32_t(32 * cb), v);
 #pragma unroll
                 for (int i = 0; i < 32; ++i)
                     acc[32 * cb + i] = __fadd_rn(acc[32 * cb + i], __fmul_rn(v[i], 0x1.0p-11f));
@@ -227,18 +239,27 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
         if (scaled) {
             const double f = ldexp(1.0, -(dec->scale_a + dec->scale_b));
 #pragma unroll
-            for (int i = 0; i < BN; ++i) acc[i] = scale_pow2(acc[i], f);
+            for (int i = 0; i < kCols; ++i) acc[i] = scale_pow2(acc[i], f);
         }
-        if (row < m) {
-            float* crow = c + size_t(row) * n2 + n0;
-            if (n0 + BN <= n2) {
+        // stage the tile in the (now idle) operand smem, then store coalesced rows
+        float* ctile = reinterpret_cast<float*>(smem);
+        float* myrow = ctile + size_t(rloc) * kCStride + kCols * half;
 #pragma unroll
-                for (int i = 0; i < BN; i += 2)
-                    *reinterpret_cast<float2*>(crow + i) = make_float2(acc[i], acc[i + 1]);
+        for (int i = 0; i < kCols; i += 4)
+            *reinterpret_cast<float4*>(myrow + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+        epi_bar_sync();
+        const int ew = warp - 2;
+        const bool full_cols = n0 + BN <= n2 && (n2 & 3) == 0;
+        for (int r = ew; r < BM; r += kEpiWarps) {
+            const int grow = m0 + r;
+            if (grow >= m) break;
+            float* dst = c + size_t(grow) * n2 + n0;
+            const float* srow = ctile + size_t(r) * kCStride;
+            if (full_cols) {
+                reinterpret_cast<float4*>(dst)[lane] = reinterpret_cast<const float4*>(srow)[lane];
             } else {
-#pragma unroll
-                for (int i = 0; i < BN; ++i)
-                    if (n0 + i < n2) crow[i] = acc[i];
+                for (int i = lane; i < BN; i += 32)
+                    if (n0 + i < n2) dst[i] = srow[i];
             }
         }
     }

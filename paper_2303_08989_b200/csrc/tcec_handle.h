@@ -13,7 +13,7 @@ struct tcec_handle_s {
     int sm_count = 148;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
-    int flush_kblocks = 4;  // RN flush of the main term every 4 k-blocks (256 f16 / 128 tf32 K')
+    int flush_kblocks = 1;  // RN flush of the main term every k-block (64 f16 / 32 tf32 K')
     // operand workspace (split hi/lo planes), grown on demand
     void* ws = nullptr;
     size_t ws_bytes = 0;
@@ -25,6 +25,12 @@ struct tcec_handle_s {
     void* io = nullptr;
     size_t io_bytes = 0;
     void* scratch_host = nullptr;  // pinned 4 KiB
+    // stage profiling (tcec_profile_*): CUDA events around the stages of a
+    // dispatched CGEMM, accumulated after each synchronous dispatch
+    bool prof = false;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    double prof_ms[3] = {0.0, 0.0, 0.0};  // statistics+selection, operand prep, GEMM
+    int64_t prof_count = 0;
 
     void* workspace(size_t bytes);
     tcec::DevDecision* decisions(int slots);

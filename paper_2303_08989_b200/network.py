@@ -1,0 +1,159 @@
+"""Tensor-network contraction through the C-ABI (host mirror of network.hpp).
+
+    net = Network(handle, spec)                  # TensorNetwork (network.hpp:17-19)
+    path = net.greedy_path()                     # greedy_path (network.hpp:49)
+    t = net.contract(path, config)               # contract_network (network.hpp:37-38)
+    z = amplitude(handle, circuit, x, config)    # amplitude (qcircuit.hpp:49-52)
+
+String labels are mapped to integer ids at the boundary; the label order and
+the SSA node numbering of paths are the reference's.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import check
+from .api import Handle, SelectionPolicy, make_config
+from .circuits import Circuit, NetworkSpec, circuit_to_network
+
+
+@dataclass
+class Tensor:
+    """Tensor<std::complex<float>> (tensor.hpp:16-53)."""
+    labels: list
+    dims: list
+    data: np.ndarray  # complex64, row-major in label order
+
+
+def _cfg(config):
+    if config is None or isinstance(config, SelectionPolicy):
+        return make_config(config)
+    return config
+
+
+class Network:
+    def __init__(self, handle: Handle | None, spec: NetworkSpec):
+        """handle=None builds a planning-only network (greedy_path works without a GPU)."""
+        self.handle = handle
+        self.lib = handle.lib if handle is not None else _lib.load()
+        self.spec = spec
+        self.label_ids: dict[str, int] = {}
+        ranks, labels, dims = [], [], []
+        for ls, ds in zip(spec.labels, spec.dims):
+            ranks.append(len(ls))
+            for l, d in zip(ls, ds):
+                labels.append(self.label_ids.setdefault(l, len(self.label_ids)))
+                dims.append(int(d))
+        self.names = {v: k for k, v in self.label_ids.items()}
+        n = len(ranks)
+        r = (C.c_int * max(n, 1))(*ranks)
+        lab = (C.c_int * max(len(labels), 1))(*labels)
+        dm = (C.c_int64 * max(len(dims), 1))(*dims)
+        net = C.c_void_p()
+        check(self.lib.tcec_network_create(handle.h if handle is not None else None, n, r, lab,
+                                           dm, C.byref(net)))
+        self.net = net
+        for i, d in enumerate(spec.data):
+            self.set_node(i, d)
+
+    def close(self):
+        if getattr(self, "net", None):
+            self.lib.tcec_network_destroy(self.net)
+            self.net = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def n_nodes(self) -> int:
+        return len(self.spec.labels)
+
+    def set_node(self, i: int, data) -> None:
+        d = np.ascontiguousarray(data, dtype=np.complex64)
+        expect = int(np.prod(self.spec.dims[i])) if self.spec.dims[i] else 1
+        if d.size != expect:
+            raise _lib.ShapeMismatch(1, "tensor data length does not match dims")
+        check(self.lib.tcec_network_set_node(self.net, i, d.ctypes.data_as(C.c_void_p)))
+
+    def greedy_path(self):
+        n = self.n_nodes
+        buf = (C.c_int * max(2 * (n - 1), 1))()
+        check(self.lib.tcec_network_greedy_path(self.net, buf))
+        return [(buf[2 * i], buf[2 * i + 1]) for i in range(n - 1)]
+
+    def contract(self, path, config=None, want_log: bool = False):
+        """contract_network: returns Tensor (and the decision-log lines)."""
+        cfg = _cfg(config)
+        flat = [x for st in path for x in st]
+        steps = (C.c_int * max(len(flat), 1))(*flat)
+        cap = 1
+        # output size bound: product of all open-label dims
+        open_dims = {}
+        for ls, ds in zip(self.spec.labels, self.spec.dims):
+            for l, d in zip(ls, ds):
+                open_dims[l] = d if l not in open_dims else None
+        for d in open_dims.values():
+            if d is not None:
+                cap *= d
+        out = np.empty(max(cap, 1), dtype=np.complex64)
+        rank = C.c_int(0)
+        labels = (C.c_int * max(len(open_dims), 1))()
+        log = C.create_string_buffer(200 * (len(path) + 1)) if want_log else None
+        check(self.lib.tcec_contract_network(self.net, steps, len(path), C.byref(cfg),
+                                             out.ctypes.data_as(C.c_void_p), out.size,
+                                             C.byref(rank), labels, log,
+                                             len(log) if log is not None else 0))
+        names = [self.names[labels[i]] for i in range(rank.value)]
+        dims = []
+        for nm in names:
+            dims.append(next(d for ls, ds in zip(self.spec.labels, self.spec.dims)
+                             for l, d in zip(ls, ds) if l == nm))
+        size = int(np.prod(dims)) if dims else 1
+        t = Tensor(names, dims, out[:size].copy())
+        if want_log:
+            lines = [ln for ln in log.value.decode().split("\n") if ln]
+            return t, lines
+        return t
+
+    def selector_batch(self, path, bitstrings, config=None) -> np.ndarray:
+        """Amplitudes of many bitstrings over one plan / one captured graph."""
+        cfg = _cfg(config)
+        flat = [x for st in path for x in st]
+        steps = (C.c_int * max(len(flat), 1))(*flat)
+        sel = self.spec.selector_nodes
+        nsel = len(sel)
+        sel_arr = (C.c_int * max(nsel, 1))(*sel)
+        bits = np.ascontiguousarray(np.asarray(bitstrings, dtype=np.uint8).reshape(-1))
+        n = len(bitstrings)
+        out = np.empty(n, dtype=np.complex64)
+        check(self.lib.tcec_contract_selector_batch(
+            self.net, steps, len(path), C.byref(cfg), nsel, sel_arr, n,
+            bits.ctypes.data_as(C.POINTER(C.c_uint8)), out.ctypes.data_as(C.c_void_p)))
+        return out
+
+
+def contract_pair(handle: Handle, a: Tensor, b: Tensor, config=None) -> Tensor:
+    """contract_pair (network.hpp:29-32) as a two-node fold."""
+    spec = NetworkSpec(labels=[list(a.labels), list(b.labels)], dims=[list(a.dims), list(b.dims)],
+                       data=[a.data, b.data])
+    net = Network(handle, spec)
+    try:
+        return net.contract([(0, 1)], config)
+    finally:
+        net.close()
+
+
+def amplitude(handle: Handle, circuit: Circuit, x, config=None) -> np.complex64:
+    """amplitude (qcircuit.cpp:184-195): network -> greedy path -> contraction."""
+    net = Network(handle, circuit_to_network(circuit, x))
+    try:
+        return net.contract(net.greedy_path(), config).data[0]
+    finally:
+        net.close()

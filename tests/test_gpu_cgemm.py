@@ -1,0 +1,193 @@
+"""GPU CGEMM parity (reference test_gemm.cpp / test_cgemm.cpp).
+
+FP32_REF and FP64_ORACLE tiers are bit-identical to the reference schedule.
+The tensor-core modes (tcgen05) accumulate in hardware order, so they are
+checked against the f64 oracle with the reference's own acceptance bar:
+    rel_err(TCEC) <= 4 * rel_err(FP32_REF on CPU)  and  <= 5e-6   (test_cgemm.cpp:64-66)
+    rel_err(TC)   >= 10 * rel_err(TCEC)                             (test_gemm.cpp:98-101)
+plus size-independent properties at full benchmark sizes.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2303_08989_b200 import InvalidArgument, ShapeMismatch
+from tests.conftest import bits
+from tests.golden.recipes import matrix_recipe
+
+pytestmark = pytest.mark.gpu
+
+TOL_FACTOR = 4.0    # TCEC vs CPU FP32_REF error (test_cgemm.cpp:64-66)
+TOL_ABS = 5e-6
+
+
+def relerr(c, ref):
+    c = np.asarray(c, dtype=np.complex128)
+    return float(np.linalg.norm(c - ref) / np.linalg.norm(ref))
+
+
+SHAPES = [(1, 1, 1), (3, 5, 7), (8, 32, 16), (13, 37, 65), (16, 48, 33), (64, 64, 64),
+          (100, 1, 50), (1, 200, 3), (129, 65, 200), (300, 257, 31)]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_fp32_ref_and_fp64_tiers_bit_exact(handle, orc, dev, shape):
+    m, n, k = shape
+    a = matrix_recipe("uniform", m, k, 1000 + m)
+    b = matrix_recipe("uniform", k, n, 2000 + n)
+    ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    for mode in ("FP32_REF", "FP64_ORACLE"):
+        c, _ = handle.cgemm(ad, bd, mode)
+        cr, _ = orc.cgemm(a, b, mode)
+        assert np.array_equal(bits(c.cpu().numpy().view(np.float32)), bits(cr.view(np.float32))), mode
+
+
+def test_fp32_ref_golden(handle, golden, dev):
+    g = golden("cgemm.npz")
+    for (m, n, k) in SHAPES[:8]:
+        a = matrix_recipe("uniform", m, k, 1000 + m)
+        b = matrix_recipe("uniform", k, n, 2000 + n)
+        c, _ = handle.cgemm(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev), "FP32_REF")
+        assert np.array_equal(bits(c.cpu().numpy().view(np.float32)), g[f"{m}x{n}x{k}:FP32_REF"])
+
+
+@pytest.mark.parametrize("n", [256, 512, 1024, 2048])
+def test_tcec_accuracy_uniform(handle, orc, dev, n):
+    r = O.Rng(7 + n)
+    a, b = r.uniform_c32(n, n), r.uniform_c32(n, n)
+    ref = orc.cgemm_oracle(a, b)
+    err_ref = relerr(orc.cgemm(a, b, "FP32_REF")[0], ref) if n <= 1024 else None
+    ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    errs = {}
+    for mode in ("FP16TCEC", "TF32TCEC", "FP16TC", "TF32TC"):
+        c, ovf = handle.cgemm(ad, bd, mode)
+        assert not ovf
+        errs[mode] = relerr(c.cpu().numpy(), ref)
+    for mode in ("FP16TCEC", "TF32TCEC"):
+        assert 1e-8 <= errs[mode] <= TOL_ABS, (mode, errs)
+        if err_ref is not None:
+            assert errs[mode] <= TOL_FACTOR * err_ref, (mode, errs, err_ref)
+    assert errs["FP16TC"] >= 10 * errs["FP16TCEC"]
+    assert errs["TF32TC"] >= 10 * errs["TF32TCEC"]
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (3, 5, 7), (13, 37, 65), (129, 65, 200),
+                                   (300, 257, 31), (1000, 7, 333), (5, 1100, 77), (130, 130, 1100)])
+def test_tcec_ragged_shapes(handle, orc, dev, shape):
+    m, n, k = shape
+    a = matrix_recipe("uniform", m, k, 31 + m)
+    b = matrix_recipe("uniform", k, n, 37 + n)
+    ref = orc.cgemm_oracle(a, b)
+    err_ref = relerr(orc.cgemm(a, b, "FP32_REF")[0], ref)
+    ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    for mode in ("FP16TCEC", "TF32TCEC"):
+        c, _ = handle.cgemm(ad, bd, mode)
+        e = relerr(c.cpu().numpy(), ref)
+        assert e <= max(TOL_FACTOR * err_ref, 2e-7), (mode, e, err_ref)
+
+
+def test_exact_small_value_matrices_all_modes(handle, dev):
+    # test_gemm.cpp:166-181: {0, +-1/2, +-1} products are exact in every mode
+    g = np.random.default_rng(31)
+    vals = np.array([0.0, 0.5, -0.5, 1.0, -1.0], np.float32)
+    for _ in range(20):
+        a = (vals[g.integers(0, 5, (6, 9))] + 1j * vals[g.integers(0, 5, (6, 9))]).astype(np.complex64)
+        b = (vals[g.integers(0, 5, (9, 5))] + 1j * vals[g.integers(0, 5, (9, 5))]).astype(np.complex64)
+        want = a.astype(np.complex128) @ b.astype(np.complex128)
+        ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+        for mode in ("FP32_REF", "FP64_ORACLE", "TF32TC", "FP16TC", "TF32TCEC", "FP16TCEC"):
+            c, _ = handle.cgemm(ad, bd, mode)
+            assert np.array_equal(c.cpu().numpy().astype(np.complex128), want), mode
+
+
+def test_identity_operand_exact(handle, dev):
+    # B entries exact in 11 significand bits (test_gemm.cpp:43-60, :147-164)
+    g = np.random.default_rng(5)
+    bv = (g.integers(-1024, 1025, (48, 40, 2)).astype(np.float32) / 1024).view(np.complex64)[..., 0]
+    b = torch.from_numpy(np.ascontiguousarray(bv)).to(dev)
+    eye = torch.eye(48, dtype=torch.complex64, device=dev)
+    for mode in ("FP32_REF", "FP16TCEC", "TF32TCEC"):
+        c, _ = handle.cgemm(eye, b, mode)
+        assert torch.equal(c, b), mode
+
+
+def test_power_of_two_scaling_commutes(handle, dev):
+    # test_gemm.cpp:129-145 on the device: scaling A by 2^s scales C by 2^s exactly
+    a = matrix_recipe("banded", 96, 80, 23)
+    b = matrix_recipe("banded", 80, 112, 24)
+    ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    for mode in ("FP32_REF", "FP16TCEC", "TF32TCEC", "FP16TC", "TF32TC"):
+        c, _ = handle.cgemm(ad, bd, mode)
+        for s in (-3, -1, 1, 2, 5):
+            cs, _ = handle.cgemm(ad * (2.0 ** s), bd, mode)
+            assert torch.equal(cs, c * (2.0 ** s)), (mode, s)
+
+
+def test_determinism(handle, dev):
+    a = torch.from_numpy(matrix_recipe("uniform", 300, 200, 17)).to(dev)
+    b = torch.from_numpy(matrix_recipe("uniform", 200, 260, 18)).to(dev)
+    for mode in ("FP32_REF", "FP64_ORACLE", "TF32TC", "FP16TC", "TF32TCEC", "FP16TCEC"):
+        c1, _ = handle.cgemm(a, b, mode)
+        c2, _ = handle.cgemm(a, b, mode)
+        assert torch.equal(c1, c2), mode
+
+
+def test_flush_interval_is_accuracy_relevant(handle, orc, dev):
+    """Without the RN flush the tensor-core main term truncates (error grows
+    with k); the flush restores FP32-level accuracy."""
+    r = O.Rng(99)
+    a, b = r.uniform_c32(128, 4096), r.uniform_c32(4096, 128)
+    ref = orc.cgemm_oracle(a, b)
+    ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    keep = handle.flush_kblocks
+    try:
+        handle.flush_kblocks = 0
+        e0 = relerr(handle.cgemm(ad, bd, "FP16TCEC")[0].cpu().numpy(), ref)
+        handle.flush_kblocks = keep
+        e4 = relerr(handle.cgemm(ad, bd, "FP16TCEC")[0].cpu().numpy(), ref)
+    finally:
+        handle.flush_kblocks = keep
+    assert e4 < e0 / 2
+
+
+def test_overflow_flag(handle, dev):
+    a = torch.full((4, 4), 70000.0 + 0j, dtype=torch.complex64, device=dev)
+    b = torch.ones(4, 4, dtype=torch.complex64, device=dev)
+    assert handle.cgemm(a, b, "FP16TCEC")[1]
+    assert not handle.cgemm(a, b, "TF32TCEC")[1]
+
+
+def test_shape_and_tiling_errors(handle, dev):
+    a = torch.zeros(2, 3, dtype=torch.complex64, device=dev)
+    b = torch.zeros(2, 2, dtype=torch.complex64, device=dev)
+    with pytest.raises(ShapeMismatch):
+        handle.cgemm(a, b, "FP32_REF")
+    sq = torch.zeros(4, 4, dtype=torch.complex64, device=dev)
+    with pytest.raises(InvalidArgument):
+        handle.cgemm(sq, sq, "FP16TCEC", k_tile=0)
+    handle.cgemm(sq, sq, "FP32_REF", k_tile=0)  # the FP32 tier takes no tiling (gemm.cpp:60-66)
+
+
+def test_batched_reports_index(handle, dev):
+    ok = (torch.zeros(4, 4, dtype=torch.complex64, device=dev),) * 2
+    bad = (torch.zeros(4, 5, dtype=torch.complex64, device=dev),
+           torch.zeros(4, 4, dtype=torch.complex64, device=dev))
+    assert handle.cgemm_batched([], "FP32_REF") == []
+    with pytest.raises(ShapeMismatch, match="batch entry 1"):
+        handle.cgemm_batched([ok, bad], "FP32_REF")
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("n", [4096, 8192])
+def test_tcec_full_size_row_sampled(handle, dev, n):
+    """Benchmark sizes: rows sampled against an f64 product of those rows."""
+    ah = (np.random.default_rng(n).uniform(-1, 1, (n, n, 2)).astype(np.float32)).view(np.complex64)[..., 0]
+    bh = (np.random.default_rng(n + 1).uniform(-1, 1, (n, n, 2)).astype(np.float32)).view(np.complex64)[..., 0]
+    ad, bd = torch.from_numpy(ah).to(dev), torch.from_numpy(bh).to(dev)
+    rows = np.random.default_rng(3).choice(n, 16, replace=False)
+    ref = ah[rows].astype(np.complex128) @ bh.astype(np.complex128)
+    for mode in ("FP16TCEC", "TF32TCEC"):
+        c, _ = handle.cgemm(ad, bd, mode)
+        e = relerr(c[torch.from_numpy(rows).to(dev)].cpu().numpy(), ref)
+        assert e <= 2e-6, (mode, e)

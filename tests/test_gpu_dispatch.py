@@ -1,0 +1,154 @@
+"""Device-side precision selection + dispatch (reference test_precsel.cpp:242-349).
+
+The exponent statistics, tolerance levels, chosen mode, scale exponents and the
+decision-log line must be identical to the reference (golden + oracle); the
+FP32 tier output is bit-identical, the tensor-core tiers are within tolerance."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2303_08989_b200 import SelectionPolicy, make_config
+from tests.conftest import bits
+from tests.golden.recipes import matrix_recipe
+
+pytestmark = pytest.mark.gpu
+
+
+def relerr(c, ref):
+    return float(np.linalg.norm(np.asarray(c, np.complex128) - ref) / np.linalg.norm(ref))
+
+
+def _gpu_cfg(kw):
+    kw = dict(kw)
+    force = kw.pop("force", None)
+    pol = SelectionPolicy(**{k: v for k, v in kw.items()})
+    return make_config(pol, force=force)
+
+
+def test_dispatch_golden(handle, orc, golden, dev):
+    for d in golden("dispatch.json"):
+        a = matrix_recipe(d["a"], d["m"], d["k"], d["seed_a"])
+        b = matrix_recipe(d["b"], d["k"], d["n"], d["seed_b"])
+        c, res = handle.dispatch_cgemm(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev),
+                                       _gpu_cfg(d["cfg"]))
+        assert res.line == d["line"], (d["cfg"], res.line, d["line"])
+        assert (["FP16TCEC", "FP16TCEC_SCALED", "TF32TCEC", "FP32_BASELINE"][res.kind],
+                res.scale_a, res.scale_b) == (d["kind"], d["scale_a"], d["scale_b"])
+        assert bool(res.overflow) == bool(d["overflow"])
+        ch = c.cpu().numpy()
+        rc, co, _ = orc.dispatch_cgemm(a, b, O.make_config(**d["cfg"]))
+        if d["kind"] == "FP32_BASELINE" or d["cfg"].get("force") in ("FP32_REF", "FP64_ORACLE"):
+            assert np.array_equal(bits(ch.view(np.float32)), bits(co.view(np.float32)))
+        elif d["c_oracle"] is not None and "TC" not in str(d["cfg"].get("force", "")).replace("TCEC", ""):
+            ref = np.array(d["c_oracle"], np.float64).view(np.complex128).reshape(d["m"], d["n"])
+            assert relerr(ch, ref) <= max(4 * relerr(co, ref), 5e-7)
+
+
+def test_default_policy_routing(handle, dev):
+    # SPEC.md:596 acceptance 10 (shapes scaled to keep the test fast) + test_precsel.cpp:242-256
+    small = torch.from_numpy(matrix_recipe("uniform", 64, 64, 410)).to(dev)
+    _, r = handle.dispatch_cgemm(small, small)
+    assert r.line == "64,64,64,FP32_BASELINE,0,0,-,-,-,-,-,-" and not r.has_stats
+    mid = torch.from_numpy(matrix_recipe("uniform", 512, 512, 411)).to(dev)
+    _, r = handle.dispatch_cgemm(mid, mid)
+    assert r.line.startswith("512,512,512,TF32TCEC,0,0,-,-,-,-,-,-")
+    big = torch.from_numpy(matrix_recipe("uniform", 2048, 2048, 412)).to(dev)
+    _, r = handle.dispatch_cgemm(big, big)
+    assert r.has_stats and r.line.split(",")[3] in ("FP16TCEC_SCALED", "FP16TCEC")
+
+
+@pytest.mark.parametrize("recipe,t,want", [
+    ("banded", 0.0, "FP16TCEC"),
+    ("tiny20", 0.0, "FP16TCEC_SCALED"),
+    ("uniform", 0.0, "FP16TCEC_SCALED"),
+    ("uniform", 0.1, "FP16TCEC"),
+    ("type3", 0.0, "TF32TCEC"),
+    ("type3", 0.5, "FP16TCEC_SCALED"),
+])
+def test_auto_selection_outcomes(handle, orc, dev, recipe, t, want):
+    a = matrix_recipe(recipe, 96, 88, 71)
+    b = matrix_recipe("banded" if recipe == "type3" else recipe, 88, 80, 72)
+    cfg_kw = dict(threshold_t=t, size_auto=16, size_tf32=8)
+    c, res = handle.dispatch_cgemm(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev),
+                                   _gpu_cfg(cfg_kw))
+    rc, co, ro = orc.dispatch_cgemm(a, b, O.make_config(**cfg_kw))
+    assert res.line == ro.line.decode()
+    assert res.line.split(",")[3] == want
+    ref = orc.cgemm_oracle(a, b)
+    err_ref = relerr(orc.cgemm(a, b, "FP32_REF")[0], ref)
+    assert relerr(c.cpu().numpy(), ref) <= max(4 * err_ref, 5e-7)
+
+
+def test_scaled_fp16_stays_accurate_on_tiny_inputs(handle, orc, dev):
+    # test_precsel.cpp:278-289: e_max = -20 -> scale 34, error <= 1e-6
+    r = O.Rng(411)
+    a = (r.uniform_c32(16, 16) * np.float32(0.5) + np.complex64(1 + 1j)) * np.float32(2.0 ** -20)
+    b = (r.uniform_c32(16, 16) * np.float32(0.5) + np.complex64(1 + 1j)) * np.float32(2.0 ** -20)
+    c, res = handle.dispatch_cgemm(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev),
+                                   SelectionPolicy(size_auto=16, size_tf32=8))
+    assert res.line.split(",")[3] == "FP16TCEC_SCALED" and res.scale_a == 34
+    assert relerr(c.cpu().numpy(), orc.cgemm_oracle(a, b)) <= 1e-6
+
+
+def test_forced_fp16_underflows_on_type2_like_inputs(handle, orc, dev):
+    """SPEC.md:593 criterion 5: forced FP16TCEC on 1e-8-scale inputs loses the
+    result, the selector's scaled mode does not."""
+    a = matrix_recipe("uniform", 64, 64, 5) * np.float32(1e-8)
+    b = matrix_recipe("uniform", 64, 64, 6) * np.float32(1e-8)
+    ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    ref = orc.cgemm_oracle(a, b)
+    forced, _ = handle.cgemm(ad, bd, "FP16TCEC")
+    assert np.abs(forced.cpu().numpy()).max() < 1e-3 * np.abs(ref).max()
+    c, res = handle.dispatch_cgemm(ad, bd, SelectionPolicy(size_auto=16, size_tf32=8))
+    assert res.line.split(",")[3] == "FP16TCEC_SCALED"
+    assert relerr(c.cpu().numpy(), ref) < 1e-6
+
+
+def test_scaled_roundtrip_bit_exact(handle, dev):
+    # test_precsel.cpp:226-240: descale(cgemm(scale A, scale B)) == cgemm(A, B) bit for bit
+    g = np.random.default_rng(409)
+    def band(r, c):
+        v = (g.choice([-1.0, 1.0], (r, c, 2)) * (0.25 + 0.7 * g.random((r, c, 2)))).astype(np.float32)
+        return np.ascontiguousarray(v.view(np.complex64)[..., 0])
+    a, b = band(24, 16), band(16, 20)
+    ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    direct, _ = handle.cgemm(ad, bd, "FP16TCEC")
+    scaled, _ = handle.cgemm(handle.scale_matrix(ad, 3), handle.scale_matrix(bd, 5), "FP16TCEC")
+    handle.descale_output_inplace(scaled, 3, 5)
+    assert torch.equal(scaled, direct)
+
+
+def test_forced_modes(handle, orc, dev):
+    a = matrix_recipe("uniform", 8, 8, 412)
+    b = matrix_recipe("uniform", 8, 8, 413)
+    ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    for f in O.FORCED:
+        c, res = handle.dispatch_cgemm(ad, bd, make_config(force=f))
+        assert res.line.split(",")[3] == f
+        if f == "FP16TCEC_SCALED":
+            assert res.has_stats
+            assert relerr(c.cpu().numpy(), orc.cgemm_oracle(a, b)) <= 1e-5
+
+
+def test_host_buffer_entry_point(handle, orc):
+    a = matrix_recipe("uniform", 200, 150, 1)
+    b = matrix_recipe("uniform", 150, 120, 2)
+    c, res = handle.dispatch_cgemm_host(a, b, make_config(force="FP32_REF"))
+    co, _ = orc.cgemm(a, b, "FP32_REF")
+    assert np.array_equal(bits(c.view(np.float32)), bits(co.view(np.float32)))
+    c2, res2 = handle.dispatch_cgemm_host(a, b, SelectionPolicy(size_auto=64, size_tf32=32))
+    rc, _, ro = orc.dispatch_cgemm(a, b, O.make_config(size_auto=64, size_tf32=32))
+    assert res2.line == ro.line.decode()
+
+
+def test_empty_and_zero_operands(handle, dev):
+    z = torch.zeros(32, 32, dtype=torch.complex64, device=dev)
+    c, res = handle.dispatch_cgemm(z, z, SelectionPolicy(size_auto=16, size_tf32=8))
+    assert res.line == "32,32,32,FP16TCEC,0,0,0,-,0,-,-,-"
+    assert torch.count_nonzero(c) == 0
+    a = torch.zeros(5, 0, dtype=torch.complex64, device=dev)
+    b = torch.zeros(0, 7, dtype=torch.complex64, device=dev)
+    for mode in ("FP32_REF", "FP16TCEC", "TF32TCEC"):
+        c, _ = handle.cgemm(a, b, mode)
+        assert c.shape == (5, 7) and torch.count_nonzero(c) == 0

@@ -1,0 +1,150 @@
+"""Device-resident TTGT contraction and RCS amplitudes (reference
+test_tensor.cpp:77-174, test_qcircuit.cpp:221-241, test_experiments.cpp:72-96).
+
+FP32-tier contractions (every step of the 4x4 circuits under the default
+policy) are bit-identical to the reference amplitudes in tests/golden/rqc.json."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from oracle.network import amplitude_sv, contract_network as oracle_fold
+from paper_2303_08989_b200 import ExtentMismatch, InvalidPath, SelectionPolicy, make_config
+from paper_2303_08989_b200.circuits import (NetworkSpec, bitstrings_for, circuit_to_network,
+                                            rqc_rectangular)
+from paper_2303_08989_b200.network import Network, Tensor, amplitude, contract_pair
+from tests.conftest import bits
+from tests.golden.recipes import matrix_recipe
+
+pytestmark = pytest.mark.gpu
+
+BASELINE = make_config(force="FP32_REF")
+
+
+def _t(labels, dims, seed):
+    return Tensor(labels, dims, matrix_recipe("uniform", 1, int(np.prod(dims)), seed).reshape(-1))
+
+
+def test_contract_pair_basics(handle):
+    a = Tensor(["s"], [2], np.array([1, 0], np.complex64))
+    b = Tensor(["s"], [2], np.array([1, 1], np.complex64))
+    c = contract_pair(handle, a, b, BASELINE)
+    assert c.labels == [] and c.data[0] == 1
+    with pytest.raises(ExtentMismatch):
+        contract_pair(handle, Tensor(["s"], [2], np.zeros(2, np.complex64)),
+                      Tensor(["s"], [3], np.zeros(3, np.complex64)), BASELINE)
+    t = _t(["a", "b", "c"], [3, 4, 5], 1)
+    eye = Tensor(["c", "c2"], [5, 5], np.eye(5, dtype=np.complex64).reshape(-1))
+    r = contract_pair(handle, t, eye, BASELINE)
+    assert r.labels == ["a", "b", "c2"] and np.array_equal(bits(r.data.view(np.float32)),
+                                                           bits(t.data.view(np.float32)))
+    x, y = _t(["x"], [3], 2), _t(["y"], [2], 3)
+    r = contract_pair(handle, x, y, BASELINE)
+    assert r.dims == [3, 2]
+    assert np.allclose(r.data.reshape(3, 2), np.outer(x.data, y.data), atol=1e-7)
+
+
+@pytest.mark.parametrize("mode", ["FP32_REF", "TF32TCEC", "FP16TCEC"])
+def test_contract_pair_random_vs_einsum(handle, mode):
+    g = np.random.default_rng(2)
+    for it in range(10):
+        a = _t(["i", "j", "k"], [4, 4, 4], 100 + it)
+        b = _t(["k", "l", "m"], [4, 4, 4], 200 + it)
+        want = np.einsum("ijk,klm->ijlm", a.data.reshape(4, 4, 4).astype(np.complex128),
+                         b.data.reshape(4, 4, 4).astype(np.complex128))
+        got = contract_pair(handle, a, b, make_config(force=mode))
+        assert got.labels == ["i", "j", "l", "m"]
+        err = np.linalg.norm(got.data - want.reshape(-1)) / np.linalg.norm(want)
+        assert err <= 1e-6, (mode, err)
+
+
+def test_contraction_matches_oracle_fold_bit_exact_fp32_tier(handle):
+    """Every FP32-tier step is bit-identical, so the whole fold is."""
+    spec = NetworkSpec(labels=[["a", "b", "c"], ["c", "d"], ["d", "e", "a"], ["b", "e"]],
+                       dims=[[3, 4, 5], [5, 6], [6, 2, 3], [4, 2]],
+                       data=[matrix_recipe("uniform", 1, n, 40 + i).reshape(-1)
+                             for i, n in enumerate((60, 30, 36, 8))])
+    net = Network(handle, spec)
+    for path in ([(0, 1), (2, 4), (3, 5)], [(2, 3), (0, 4), (1, 5)], [(0, 3), (1, 2), (4, 5)]):
+        got, lines = net.contract(path, BASELINE, want_log=True)
+        _, _, want, want_lines = oracle_fold(spec, path, O.make_config(force="FP32_REF"))
+        assert np.array_equal(bits(got.data.view(np.float32)), bits(want.view(np.float32)))
+        assert lines == want_lines
+
+
+def test_path_errors(handle):
+    spec = NetworkSpec(labels=[["a"], ["a", "b"], ["b"]], dims=[[2], [2, 2], [2]],
+                       data=[np.ones(2, np.complex64), np.ones(4, np.complex64), np.ones(2, np.complex64)])
+    net = Network(handle, spec)
+    with pytest.raises(InvalidPath):
+        net.contract([(0, 0)], BASELINE)
+    with pytest.raises(InvalidPath):
+        net.contract([(0, 1)], BASELINE)  # leaves two nodes
+    with pytest.raises(InvalidPath):
+        net.contract([(0, 1), (0, 2)], BASELINE)  # dead node
+
+
+@pytest.mark.parametrize("case", [0, 1, 2, 3])
+def test_rqc_amplitudes_bit_exact_vs_reference(handle, golden, case):
+    rq = golden("rqc.json")[case]
+    c = rqc_rectangular(rq["rows"], rq["cols"], rq["depth"], rq["seed"])
+    path = [tuple(s) for s in rq["path"]]
+    for row in rq["amplitudes"]:
+        net = Network(handle, circuit_to_network(c, row["x"]))
+        assert [list(s) for s in net.greedy_path()] == rq["path"]
+        for label, cfg in (("BASELINE", BASELINE), ("AUTO-0", make_config())):
+            z = net.contract(path, cfg).data[0]
+            assert bits(np.array([z.real, z.imag], np.float32)).tolist() == row[label], label
+        net.close()
+
+
+@pytest.mark.parametrize("case", [1, 2, 3])
+def test_rqc_tensor_core_modes_accuracy(handle, golden, case):
+    """TCEC modes vs the f64 state vector: median error <= 1e-4,
+    within 4x of the CPU BASELINE median; FP16TC markedly worse."""
+    rq = golden("rqc.json")[case]
+    c = rqc_rectangular(rq["rows"], rq["cols"], rq["depth"], rq["seed"])
+    path = [tuple(s) for s in rq["path"]]
+    errs = {m: [] for m in ("FP16TCEC", "TF32TCEC", "FP16TC", "AUTO-lowered")}
+    base = []
+    for row in rq["amplitudes"]:
+        ref = complex(*row["sv_oracle"])
+        net = Network(handle, circuit_to_network(c, row["x"]))
+        for m in ("FP16TCEC", "TF32TCEC", "FP16TC"):
+            z = complex(net.contract(path, make_config(force=m)).data[0])
+            errs[m].append(abs(z - ref) / abs(ref))
+        z, lines = net.contract(path, make_config(SelectionPolicy(size_auto=4, size_tf32=2)),
+                                want_log=True)
+        errs["AUTO-lowered"].append(abs(complex(z.data[0]) - ref) / abs(ref))
+        if row is rq["amplitudes"][0]:
+            assert lines == row["log_lowered"]
+        bz = np.array(row["BASELINE"], np.uint32).view(np.float32)
+        base.append(abs(complex(bz[0], bz[1]) - ref) / abs(ref))
+        net.close()
+    med = {k: float(np.median(v)) for k, v in errs.items()}
+    mb = float(np.median(base))
+    for m in ("FP16TCEC", "TF32TCEC", "AUTO-lowered"):
+        assert med[m] <= 1e-4 and med[m] <= max(4 * mb, 1e-6), (m, med, mb)
+
+
+def test_selector_batch_equals_single_amplitudes(handle, golden):
+    rq = golden("rqc.json")[2]  # 4x4, depth 1+8+1
+    c = rqc_rectangular(rq["rows"], rq["cols"], rq["depth"], rq["seed"])
+    xs = [row["x"] for row in rq["amplitudes"]]
+    net = Network(handle, circuit_to_network(c, xs[0]))
+    path = [tuple(s) for s in rq["path"]]
+    for cfg, label in ((BASELINE, "BASELINE"), (make_config(), "AUTO-0")):
+        amps = net.selector_batch(path, xs, cfg)
+        for z, row in zip(amps, rq["amplitudes"]):
+            assert bits(np.array([z.real, z.imag], np.float32)).tolist() == row[label]
+    net.close()
+
+
+def test_amplitude_api_and_statevector(handle):
+    c = rqc_rectangular(2, 3, 6, 21)
+    g = np.random.default_rng(99)
+    for _ in range(6):
+        x = [int(v) for v in g.integers(0, 2, 6)]
+        got = complex(amplitude(handle, c, x, SelectionPolicy()))
+        want = amplitude_sv(c, x)
+        assert abs(got - want) <= 1e-5 * abs(want)
