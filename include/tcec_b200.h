@@ -187,6 +187,14 @@ int tcec_contract_network(tcec_network net, const int* steps, int n_steps,
 int tcec_contract_selector_batch(tcec_network net, const int* steps, int n_steps,
                                  const tcec_dispatch_config_t* cfg, int n_sel, const int* sel_nodes,
                                  int n_strings, const uint8_t* bits, void* out_host);
+/* general form of the batch: run r replaces the data of the n_var nodes
+ * var_nodes[] with the r-th block of var_data (host; the nodes' complex data
+ * concatenated in var_nodes order) and replays the same plan.  Used for the
+ * slices of a sliced contraction (every slice has the same
+ * path, only the sliced nodes' data differ).  out_host: n_runs complex values. */
+int tcec_contract_node_batch(tcec_network net, const int* steps, int n_steps,
+                             const tcec_dispatch_config_t* cfg, int n_var, const int* var_nodes,
+                             int n_runs, const void* var_data, void* out_host);
 
 #ifdef __cplusplus
 }

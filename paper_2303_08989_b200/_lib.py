@@ -149,6 +149,8 @@ def load() -> C.CDLL:
                                    C.c_char_p, i64], i32),
         "tcec_contract_selector_batch": ([vp, ip, i32, C.POINTER(DispatchConfig), i32, ip, i32,
                                           C.POINTER(C.c_uint8), vp], i32),
+        "tcec_contract_node_batch": ([vp, ip, i32, C.POINTER(DispatchConfig), i32, ip, i32, vp,
+                                      vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name, None)

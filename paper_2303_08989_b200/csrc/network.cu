@@ -406,6 +406,16 @@ static void greedy(std::vector<Summary> live, int next_id, std::vector<int>* ste
     }
 }
 
+// scatter one run's variable-node data (concatenated, node order) into the
+// contiguous node buffer; seg[i] = {dst offset, src offset, count} in elements
+__global__ void scatter_nodes_kernel(float2* node_base, const float2* src, const int64_t* seg,
+                                     int n_seg) {
+    for (int s = blockIdx.x; s < n_seg; s += gridDim.x) {
+        const int64_t dst = seg[3 * s], off = seg[3 * s + 1], cnt = seg[3 * s + 2];
+        for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) node_base[dst + i] = src[off + i];
+    }
+}
+
 __global__ void set_selectors_kernel(float2* node_base, const int64_t* sel_off, int n_sel,
                                      const uint8_t* bits) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
@@ -578,6 +588,65 @@ int tcec_contract_selector_batch(tcec_network net, const int* steps, int n_steps
     if (e != cudaSuccess) return cuda_error(e, "selector batch");
     // the host copy of the selector slots no longer matches the device
     net->dirty = true;
+    return TCEC_OK;
+}
+
+int tcec_contract_node_batch(tcec_network net, const int* steps, int n_steps,
+                             const tcec_dispatch_config_t* cfg, int n_var, const int* var_nodes,
+                             int n_runs, const void* var_data, void* out_host) {
+    if (!net || !cfg) return set_error(TCEC_ERR_INVALID_ARGUMENT, "null argument");
+    if (!net->h) return set_error(TCEC_ERR_CUDA, "network has no device handle");
+    Handle& h = *net->h;
+    cudaSetDevice(h.device);
+    std::vector<int64_t> seg;
+    int64_t per_run = 0;
+    for (int i = 0; i < n_var; ++i) {
+        const int nd = var_nodes[i];
+        if (nd < 0 || nd >= int(net->nodes.size()))
+            return set_error(TCEC_ERR_INVALID_ARGUMENT, "bad variable node index");
+        const int64_t cnt = net->nodes[size_t(nd)].size();
+        seg.push_back(net->offset[size_t(nd)]);
+        seg.push_back(per_run);
+        seg.push_back(cnt);
+        per_run += cnt;
+    }
+    FoldPlan plan;
+    DevDecision* dec = nullptr;
+    void* ws = nullptr;
+    int rc = prepare(*net, steps, n_steps, *cfg, &plan, &dec, &ws);
+    if (rc) return rc;
+    int64_t size = 1;
+    for (auto d : plan.out_dims) size *= d;
+    if (size != 1) return set_error(TCEC_ERR_SHAPE_MISMATCH, "batched networks must close");
+    cudaStream_t s = h.stream;
+    int64_t* d_seg = nullptr;
+    float2* d_var = nullptr;
+    float2* d_out = nullptr;
+    const size_t var_bytes = size_t(std::max<int64_t>(per_run * n_runs, 1)) * 8;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d_seg), std::max<size_t>(seg.size(), 1) * 8, s);
+    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&d_var), var_bytes, s);
+    if (e == cudaSuccess)
+        e = cudaMallocAsync(reinterpret_cast<void**>(&d_out), size_t(std::max(n_runs, 1)) * 8, s);
+    if (e != cudaSuccess) return cuda_error(e, "batch buffers");
+    if (!seg.empty()) cudaMemcpyAsync(d_seg, seg.data(), seg.size() * 8, cudaMemcpyHostToDevice, s);
+    if (per_run * n_runs > 0)
+        cudaMemcpyAsync(d_var, var_data, size_t(per_run * n_runs) * 8, cudaMemcpyHostToDevice, s);
+    for (int r = 0; r < n_runs; ++r) {
+        if (n_var)
+            scatter_nodes_kernel<<<std::min(n_var, 1024), 64, 0, s>>>(
+                static_cast<float2*>(net->node_dev), d_var + size_t(r) * size_t(per_run), d_seg, n_var);
+        rc = run_fold(*net, steps, n_steps, *cfg, plan, dec, ws, true);
+        if (rc) return rc;
+        cudaMemcpyAsync(d_out + r, net->result_dev, 8, cudaMemcpyDeviceToDevice, s);
+    }
+    e = cudaMemcpyAsync(out_host, d_out, size_t(n_runs) * 8, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_error(e, "batch download");
+    cudaFreeAsync(d_seg, s);
+    cudaFreeAsync(d_var, s);
+    cudaFreeAsync(d_out, s);
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_error(e, "node batch");
+    net->dirty = true;  // device node data now holds the last run
     return TCEC_OK;
 }
 

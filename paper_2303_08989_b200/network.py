@@ -139,6 +139,24 @@ class Network:
         return out
 
 
+    def node_batch(self, path, var_nodes, runs, config=None) -> np.ndarray:
+        """Closed-network values of many runs that differ only in the data of
+        `var_nodes`; runs[r][i] is the data of var_nodes[i] in run r."""
+        cfg = _cfg(config)
+        flat = [x for st in path for x in st]
+        steps = (C.c_int * max(len(flat), 1))(*flat)
+        nv = len(var_nodes)
+        vn = (C.c_int * max(nv, 1))(*var_nodes)
+        blocks = [np.ascontiguousarray(np.asarray(d, dtype=np.complex64).reshape(-1))
+                  for run in runs for d in run]
+        data = np.concatenate(blocks) if blocks else np.zeros(1, np.complex64)
+        out = np.empty(max(len(runs), 1), dtype=np.complex64)
+        check(self.lib.tcec_contract_node_batch(self.net, steps, len(path), C.byref(cfg), nv, vn,
+                                                len(runs), data.ctypes.data_as(C.c_void_p),
+                                                out.ctypes.data_as(C.c_void_p)))
+        return out[:len(runs)]
+
+
 def contract_pair(handle: Handle, a: Tensor, b: Tensor, config=None) -> Tensor:
     """contract_pair (network.hpp:29-32) as a two-node fold."""
     spec = NetworkSpec(labels=[list(a.labels), list(b.labels)], dims=[list(a.dims), list(b.dims)],
