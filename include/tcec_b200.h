@@ -63,6 +63,9 @@ int tcec_synchronize(tcec_handle h);
  * device counterpart of TilingConfig::k_tile (gemm.hpp:28-30). */
 int tcec_set_flush_kblocks(tcec_handle h, int kblocks);
 int tcec_get_flush_kblocks(tcec_handle h);
+/* tensor-core kernel variant: 1 = CTA pair (cta_group::2, 256 x 128 tiles,
+ * default), 0 = single CTA (128 x 128 tiles) */
+int tcec_set_gemm_variant(tcec_handle h, int variant);
 /* stage tracing (the device counterpart of DecisionRecord::wall_ms,
  * precsel.hpp:92-101): when enabled, every synchronous tcec_dispatch_cgemm
  * records CUDA events around (statistics + selection), (operand preparation)

@@ -98,6 +98,10 @@ class Handle:
     def flush_kblocks(self, v: int) -> None:
         check(self.lib.tcec_set_flush_kblocks(self.h, int(v)))
 
+    def set_gemm_variant(self, pair: bool) -> None:
+        """1 = CTA-pair (cta_group::2) TCEC kernel, 0 = single-CTA kernel."""
+        check(self.lib.tcec_set_gemm_variant(self.h, int(pair)))
+
     def profile(self, on: bool = True) -> None:
         """Enable (and reset) per-stage CUDA-event tracing of dispatches."""
         check(self.lib.tcec_profile_enable(self.h, int(on)))

@@ -182,6 +182,84 @@ TCEC_DEV void mma_commit(uint64_t* bar) {
         : "memory");
 }
 
+// ---------------------------------------------------- CTA pair (cta_group::2)
+TCEC_DEV uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+TCEC_DEV void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n"
+                 "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// address of the same shared-memory object in CTA `rank` of the cluster
+TCEC_DEV uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+
+TCEC_DEV void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+                 : "memory");
+}
+
+// TMA into this CTA's smem whose transaction bytes land on the pair leader's
+// mbarrier (peer bit cleared, cute SM100_TMA_2SM_LOAD_2D)
+TCEC_DEV void tma_load_2d_pair(void* smem_dst, const void* tmap, uint64_t* bar, int x, int y) {
+    const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(mbar), "r"(x), "r"(y)
+        : "memory");
+}
+
+template <uint32_t kCols>
+TCEC_DEV void tmem_alloc_pair(uint32_t* smem_slot) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(smem_slot)),
+                 "n"(kCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+
+template <uint32_t kCols>
+TCEC_DEV void tmem_dealloc_pair(uint32_t taddr) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols)
+                 : "memory");
+}
+
+TCEC_DEV void mma2_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                       uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+TCEC_DEV void mma2_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                        uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// commit of the pair leader's MMAs, arriving on the barrier at the same smem
+// offset in every CTA of `mask`
+TCEC_DEV void mma_commit_pair(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+
 // 32 lanes x 32 consecutive 32-bit columns; thread t of the warp receives
 // lane (32*(warp%4) + t), columns [col, col+32)
 TCEC_DEV void tmem_ld32(uint32_t taddr, float (&v)[32]) {
@@ -215,7 +293,7 @@ TCEC_DEV uint64_t umma_desc_k_sw128(const void* smem_tile) {
 // instruction descriptor (mma_sm100_desc.hpp InstrDescriptor): D f32 @4,
 // A/B format @7/@10 (F16 = 0, TF32 = 2), K-major A/B, N>>3 @17, M>>4 @24
 template <int FMT, int M, int N>
-constexpr uint32_t umma_idesc() {
+__host__ __device__ constexpr uint32_t umma_idesc() {
     constexpr uint32_t ab = FMT == kFp16 ? 0u : 2u;
     return (1u << 4) | (ab << 7) | (ab << 10) | (uint32_t(N >> 3) << 17) |
            (uint32_t(M >> 4) << 24);

@@ -54,13 +54,15 @@ struct Traits {
     static constexpr uint32_t kIdesc = umma_idesc<FMT, BM, BN>();
 };
 
-struct alignas(8) GemmSmemTail {
-    uint64_t full[kStages];
-    uint64_t empty[kStages];
+template <int kS>
+struct alignas(8) SmemTailT {
+    uint64_t full[kS];
+    uint64_t empty[kS];
     uint64_t tfull[kMainBufs];
     uint64_t tempty[kMainBufs];
     uint32_t tmem_base;
 };
+using GemmSmemTail = SmemTailT<kStages>;
 
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + size_t(kStages) * 4 * kTileBytes +
                               sizeof(GemmSmemTail);
@@ -271,6 +273,225 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
     }
 }
 
+// ===================================================================== CTA pair
+// cta_group::2 variant: a cluster of 2 CTAs computes a 256 x 128 tile of C'
+// with UMMA M = 256.  Each CTA stages its own 128 rows of A and 64 of the 128
+// B rows (48 KB per k-block instead of 64 KB for the same MACs per SM), the
+// leader issues the MMAs for both and multicasts its commits; each CTA drains
+// its own 128 TMEM lanes.  4 smem stages.
+constexpr int kPairStages = 4;
+constexpr int kPairATile = 128 * 128;   // 128 rows x 128 B
+constexpr int kPairBTile = 64 * 128;    // 64 rows x 128 B
+constexpr int kPairStageBytes = 2 * kPairATile + 2 * kPairBTile;  // per CTA, corrected
+using PairSmemTail = SmemTailT<kPairStages>;
+constexpr size_t kPairSmemBytes = 1024 + size_t(kPairStages) * kPairStageBytes + sizeof(PairSmemTail);
+static_assert(size_t(BM) * kCStride * 4 <= size_t(kPairStages) * kPairStageBytes,
+              "C staging tile must fit in the operand stages");
+
+template <int FMT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
+    tcec_gemm_pair_kernel(const __grid_constant__ CUtensorMap map_ahi,
+                          const __grid_constant__ CUtensorMap map_alo,
+                          const __grid_constant__ CUtensorMap map_bhi,
+                          const __grid_constant__ CUtensorMap map_blo, float* __restrict__ c,
+                          int m, int n2, int kp, const DevDecision* __restrict__ dec, int kind_fixed,
+                          int corrected, int flush_kblocks) {
+    using T = Traits<FMT>;
+    constexpr uint32_t kIdesc2 = umma_idesc<FMT, 2 * BM, BN>();
+    const int kind = kind_fixed >= 0 ? kind_fixed : dec->kind;
+    const bool mine = FMT == kTf32 ? kind == kKindTf32 : (kind == kKindFp16 || kind == kKindFp16Scaled);
+    if (!mine) return;  // both CTAs of the pair read the same decision
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    PairSmemTail* tail =
+        reinterpret_cast<PairSmemTail*>(smem + size_t(kPairStages) * kPairStageBytes);
+    // stage layout: A_hi | A_lo | B_hi | B_lo
+    auto a_tile = [&](int s, int lo) -> uint8_t* {
+        return smem + size_t(s) * kPairStageBytes + size_t(lo) * kPairATile;
+    };
+    auto b_tile = [&](int s, int lo) -> uint8_t* {
+        return smem + size_t(s) * kPairStageBytes + 2 * kPairATile + size_t(lo) * kPairBTile;
+    };
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+
+    const int tiles_m = (m + 2 * BM - 1) / (2 * BM), tiles_n = (n2 + BN - 1) / BN;
+    const int id = blockIdx.x >> 1;
+    const int group = kGroupM * tiles_n;
+    const int first_m = (id / group) * kGroupM;
+    const int gsize = min(tiles_m - first_m, kGroupM);
+    const int m_blk = first_m + (id % group) % gsize;
+    const int n_blk = (id % group) / gsize;
+    const int m0 = m_blk * 2 * BM + int(rank) * BM;  // this CTA's 128 rows
+    const int n0 = n_blk * BN;                       // the pair's 128 columns
+
+    const int nkb = kp / T::kBK;
+    const int F = flush_kblocks > 0 ? flush_kblocks : (nkb > 0 ? nkb : 1);
+    const int nchunks = (nkb + F - 1) / F;
+    const uint32_t cta_bytes = corrected ? uint32_t(kPairStageBytes)
+                                         : uint32_t(kPairATile + kPairBTile);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kPairStages; ++s) {
+            mbar_init(&tail->full[s], 1);
+            mbar_init(&tail->empty[s], 1);
+        }
+        for (int b = 0; b < kMainBufs; ++b) {
+            mbar_init(&tail->tfull[b], 1);
+            mbar_init(&tail->tempty[b], 2 * kEpiWarps);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&map_ahi);
+        tma_prefetch(&map_bhi);
+        if (corrected) {
+            tma_prefetch(&map_alo);
+            tma_prefetch(&map_blo);
+        }
+    }
+    if (warp == 1) tmem_alloc_pair<kTmemCols>(&tail->tmem_base);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = tail->tmem_base;
+
+    if (warp == 0) {
+        // -------------------------------------------- TMA producer (both CTAs)
+        if (lane == 0) {
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int s = kb % kPairStages;
+                mbar_wait(&tail->empty[s], ((kb / kPairStages) & 1) ^ 1);
+                if (leader) mbar_expect_tx(&tail->full[s], 2 * cta_bytes);
+                const int kx = kb * T::kBK;
+                tma_load_2d_pair(a_tile(s, 0), &map_ahi, &tail->full[s], kx, m0);
+                tma_load_2d_pair(b_tile(s, 0), &map_bhi, &tail->full[s], kx, n0 + 64 * int(rank));
+                if (corrected) {
+                    tma_load_2d_pair(a_tile(s, 1), &map_alo, &tail->full[s], kx, m0);
+                    tma_load_2d_pair(b_tile(s, 1), &map_blo, &tail->full[s], kx, n0 + 64 * int(rank));
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------------------------------- MMA issuer (pair leader only)
+        if (leader && lane == 0) {
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int chunk = kb / F;
+                const int buf = chunk % kMainBufs;
+                const bool chunk_start = (kb % F) == 0;
+                if (chunk_start) {
+                    mbar_wait(&tail->tempty[buf], ((chunk / kMainBufs) & 1) ^ 1);
+                    tc_fence_after();
+                }
+                const int s = kb % kPairStages;
+                mbar_wait(&tail->full[s], (kb / kPairStages) & 1);
+                tc_fence_after();
+                const uint64_t dah = umma_desc_k_sw128(a_tile(s, 0));
+                const uint64_t dal = umma_desc_k_sw128(a_tile(s, 1));
+                const uint64_t dbh = umma_desc_k_sw128(b_tile(s, 0));
+                const uint64_t dbl = umma_desc_k_sw128(b_tile(s, 1));
+                const uint32_t d_main = tmem + uint32_t(buf * BN);
+                const uint32_t d_corr = tmem + kColCorr;
+#pragma unroll
+                for (int ks = 0; ks < T::kKSteps; ++ks) {
+                    const uint64_t adv = uint64_t((ks * T::kUK * T::kElem) >> 4);
+                    const uint32_t acc_main = (!chunk_start || ks > 0) ? 1u : 0u;
+                    const uint32_t acc_corr = (kb > 0 || ks > 0) ? 1u : 0u;
+                    if (FMT == kFp16) {
+                        mma2_f16(d_main, dah + adv, dbh + adv, kIdesc2, acc_main);
+                        if (corrected) {
+                            mma2_f16(d_corr, dal + adv, dbh + adv, kIdesc2, acc_corr);
+                            mma2_f16(d_corr, dah + adv, dbl + adv, kIdesc2, 1u);
+                        }
+                    } else {
+                        mma2_tf32(d_main, dah + adv, dbh + adv, kIdesc2, acc_main);
+                        if (corrected) {
+                            mma2_tf32(d_corr, dal + adv, dbh + adv, kIdesc2, acc_corr);
+                            mma2_tf32(d_corr, dah + adv, dbl + adv, kIdesc2, 1u);
+                        }
+                    }
+                }
+                mma_commit_pair(&tail->empty[s], 0x3);
+                if ((kb % F) == F - 1 || kb == nkb - 1) mma_commit_pair(&tail->tfull[buf], 0x3);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------ epilogue (both CTAs)
+        const int q = warp & 3;
+        const int half = (warp - 2) >> 2;
+        const int rloc = 32 * q + lane;
+        const uint32_t lane_base = tmem + (uint32_t(32 * q) << 16) + uint32_t(64 * half);
+        constexpr int kCols = BN / 2;
+        const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tail->tempty[0]), 0);
+        float acc[kCols];
+#pragma unroll
+        for (int i = 0; i < kCols; ++i) acc[i] = 0.0f;
+        for (int ch = 0; ch < nchunks; ++ch) {
+            const int buf = ch % kMainBufs;
+            mbar_wait(&tail->tfull[buf], (ch / kMainBufs) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int cb = 0; cb < kCols / 32; ++cb) {
+                float v[32];
+                tmem_ld32(lane_base + uint32_t(buf * BN + 32 * cb), v);
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    acc[32 * cb + i] = ch == 0 ? v[i] : __fadd_rn(acc[32 * cb + i], v[i]);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_leader0 + uint32_t(buf * sizeof(uint64_t)));
+        }
+        if (corrected && nkb > 0) {
+#pragma unroll
+            for (int cb = 0; cb < kCols / 32; ++cb) {
+                float v[32];
+                tmem_ld32(lane_base + kColCorr + uint32_t(32 * cb), v);
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    acc[32 * cb + i] = __fadd_rn(acc[32 * cb + i], __fmul_rn(v[i], 0x1.0p-11f));
+            }
+        }
+        const bool scaled = kind == kKindFp16Scaled && (dec->scale_a + dec->scale_b) != 0;
+        if (scaled) {
+            const double f = ldexp(1.0, -(dec->scale_a + dec->scale_b));
+#pragma unroll
+            for (int i = 0; i < kCols; ++i) acc[i] = scale_pow2(acc[i], f);
+        }
+        float* ctile = reinterpret_cast<float*>(smem);
+        float* myrow = ctile + size_t(rloc) * kCStride + kCols * half;
+#pragma unroll
+        for (int i = 0; i < kCols; i += 4)
+            *reinterpret_cast<float4*>(myrow + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+        epi_bar_sync();
+        const int ew = warp - 2;
+        const bool full_cols = n0 + BN <= n2 && (n2 & 3) == 0;
+        for (int r = ew; r < BM; r += kEpiWarps) {
+            const int grow = m0 + r;
+            if (grow >= m) break;
+            float* dst = c + size_t(grow) * n2 + n0;
+            const float* srow = ctile + size_t(r) * kCStride;
+            if (full_cols) {
+                reinterpret_cast<float4*>(dst)[lane] = reinterpret_cast<const float4*>(srow)[lane];
+            } else {
+                for (int i = lane; i < BN; i += 32)
+                    if (n0 + i < n2) dst[i] = srow[i];
+            }
+        }
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_pair<kTmemCols>(tmem);
+    }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
 
@@ -287,11 +508,12 @@ bool get_encode() {
 }
 
 // 2-D K-major operand: rows x kp elements, box = 128 rows x 128 B, swizzle 128B
-bool make_map(CUtensorMap* map, const void* base, int fmt, int64_t rows, int64_t kp) {
+bool make_map(CUtensorMap* map, const void* base, int fmt, int64_t rows, int64_t kp,
+              uint32_t box_rows) {
     const int elem = fmt == kFp16 ? 2 : 4;
     cuuint64_t dims[2] = {cuuint64_t(kp), cuuint64_t(rows)};
     cuuint64_t strides[1] = {cuuint64_t(kp) * elem};
-    cuuint32_t box[2] = {cuuint32_t(128 / elem), 128u};
+    cuuint32_t box[2] = {cuuint32_t(128 / elem), box_rows};
     cuuint32_t estr[2] = {1u, 1u};
     const CUresult r = g_encode(
         map, fmt == kFp16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
@@ -305,21 +527,34 @@ template <int FMT>
 int launch_fmt(const TcecGemmArgs& g, cudaStream_t s) {
     static bool attr_set = false;
     if (!attr_set) {
-        const cudaError_t e = cudaFuncSetAttribute(
-            tcec_gemm_kernel<FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes));
+        cudaError_t e = cudaFuncSetAttribute(tcec_gemm_kernel<FMT>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(kSmemBytes));
+        if (e != cudaSuccess) return int(e);
+        e = cudaFuncSetAttribute(tcec_gemm_pair_kernel<FMT>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPairSmemBytes));
         if (e != cudaSuccess) return int(e);
         attr_set = true;
     }
     CUtensorMap mah, mal, mbh, mbl;
     const void* alo = g.corrected ? g.a_lo : g.a_hi;
     const void* blo = g.corrected ? g.b_lo : g.b_hi;
-    if (!make_map(&mah, g.a_hi, FMT, g.m, g.kp) || !make_map(&mal, alo, FMT, g.m, g.kp) ||
-        !make_map(&mbh, g.b_hi, FMT, g.n2, g.kp) || !make_map(&mbl, blo, FMT, g.n2, g.kp))
+    const uint32_t b_box = g.pair ? 64u : 128u;
+    if (!make_map(&mah, g.a_hi, FMT, g.m, g.kp, 128u) || !make_map(&mal, alo, FMT, g.m, g.kp, 128u) ||
+        !make_map(&mbh, g.b_hi, FMT, g.n2, g.kp, b_box) ||
+        !make_map(&mbl, blo, FMT, g.n2, g.kp, b_box))
         return int(cudaErrorInvalidValue);
-    const int64_t tiles = ((g.m + BM - 1) / BM) * ((g.n2 + BN - 1) / BN);
-    tcec_gemm_kernel<FMT><<<unsigned(tiles), kThreadsGemm, kSmemBytes, s>>>(
-        mah, mal, mbh, mbl, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed, g.corrected,
-        g.flush_kblocks);
+    if (g.pair) {
+        const int64_t tiles = ((g.m + 2 * BM - 1) / (2 * BM)) * ((g.n2 + BN - 1) / BN);
+        tcec_gemm_pair_kernel<FMT><<<unsigned(2 * tiles), kThreadsGemm, kPairSmemBytes, s>>>(
+            mah, mal, mbh, mbl, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed,
+            g.corrected, g.flush_kblocks);
+    } else {
+        const int64_t tiles = ((g.m + BM - 1) / BM) * ((g.n2 + BN - 1) / BN);
+        tcec_gemm_kernel<FMT><<<unsigned(tiles), kThreadsGemm, kSmemBytes, s>>>(
+            mah, mal, mbh, mbl, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed,
+            g.corrected, g.flush_kblocks);
+    }
     return int(cudaGetLastError());
 }
 

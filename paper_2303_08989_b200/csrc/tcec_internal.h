@@ -87,6 +87,7 @@ struct TcecGemmArgs {
     int fmt;                              // 0 = f16 kernel, 1 = tf32 kernel
     int corrected;                        // 1 = TCEC (3 products), 0 = TC ablation
     int flush_kblocks;                    // RN flush interval of the main term, 0 = none
+    int pair;                             // 1 = cta_group::2 kernel (256x128 tile per CTA pair)
 };
 // returns a cudaError_t
 int launch_tcec_gemm(const TcecGemmArgs& args, cudaStream_t s);
