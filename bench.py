@@ -380,8 +380,132 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+RQC_METRIC = "RCS 4x4 (1+8+1) amplitudes/s (all 2^16 bitstrings, AUTO-0 default policy)"
+
+
+def rqc_reference_rate(bits, nq, rows, cols, depth, seed, threads, cfg_kw=None):
+    """The reference's run_rqc inner loop (one greedy path, contract_network per
+    bitstring) over host threads; returns (amplitudes/s, seconds, amplitudes)."""
+    import oracle as O
+    ref = O.reference()
+    if ref is None:
+        return None
+    fn = ref.lib.ref_rqc_amplitudes_batch
+    fn.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_void_p, C.c_int,
+                   C.POINTER(O.ConfigPod), C.c_void_p, C.c_int]
+    cfg = O.make_config(**(cfg_kw or {}))
+    out = np.empty(len(bits) * 2, np.float32)
+    t0 = time.perf_counter()
+    rc = fn(rows, cols, depth, seed, bits.ctypes.data, len(bits), C.byref(cfg), out.ctypes.data,
+            threads)
+    dt = time.perf_counter() - t0
+    assert rc == 0
+    return len(bits) / dt, dt, out.view(np.complex64)
+
+
+def run_rqc(args):
+    """configs[0]: 4x4 rectangular RQC, H + 8 CZ layers + H, every output amplitude."""
+    import torch
+    from oracle.network import statevector
+    from paper_2303_08989_b200 import Handle, make_config
+    from paper_2303_08989_b200.circuits import circuit_to_network, rqc_rectangular
+    from paper_2303_08989_b200.network import Network
+    rows, cols, depth, seed = 4, 4, 8, 1
+    nq = rows * cols
+    world, rank, local = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    circ = rqc_rectangular(rows, cols, depth, seed)
+    allx = np.array([[(v >> q) & 1 for q in range(nq)] for v in range(1 << nq)], np.uint8)
+    mine = allx[rank::world]
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        thr = os.cpu_count() or 1
+        sample = allx[: min(len(allx), 4096 * max(1, thr // 4))]
+        rqc_reference_rate(sample[: 2 * thr], nq, rows, cols, depth, seed, thr)  # warm
+        rates = [rqc_reference_rate(sample, nq, rows, cols, depth, seed, thr)[0]
+                 for _ in range(max(1, args.steps))]
+        value = float(np.mean(rates))
+        print(json.dumps({
+            "impl": "reference", "metric": RQC_METRIC, "value": round(value, 1),
+            "unit": "amplitudes/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(len(allx) / value * 1e3, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "c64", "data": "synthetic circuit",
+            "config": {"workload": "configs[0] 4x4 RQC (1+8+1), seed 1, all 65536 bitstrings",
+                       "parallelism": "host threads"},
+            "cpu_baseline": {"value": round(value, 1), "unit": "amplitudes/s", "cores": thr,
+                             "kind": "reference",
+                             "sample": f"{len(sample)} bitstrings per step, run_rqc loop "
+                                       f"(experiments.cpp:211-230) on {thr} threads"},
+            "e2e": {"value": round(value, 1), "unit": "amplitudes/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}), flush=True)
+        return
+    h = Handle(local)
+    stream = torch.cuda.ExternalStream(h.stream_ptr, device=dev)
+    net = Network(h, circuit_to_network(circ, [0] * nq))
+    path = net.greedy_path()
+    cfg = make_config()
+    for _ in range(args.warmup):
+        amps = net.selector_batch(path, mine, cfg)
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        e0.record(stream)
+        for _ in range(args.steps):
+            amps = net.selector_batch(path, mine, cfg)
+        e1.record(stream)
+        e1.synchronize()
+        wall = (time.perf_counter() - t0) / args.steps * 1e3
+    ms = max(e0.elapsed_time(e1) / args.steps, wall)
+    ms = max_over_ranks(ms, world)
+    # fused single-launch kernel time alone (device-resident inputs)
+    if rank == 0:
+        sv = statevector(circ)
+        idx = np.array([sum(int(b) << q for q, b in enumerate(x)) for x in mine])
+        ref = sv[idx]
+        err = float(np.max(np.abs(amps.astype(np.complex128) - ref) / np.abs(ref)))
+        med = float(np.median(np.abs(amps.astype(np.complex128) - ref) / np.abs(ref)))
+        norm = float(np.sum(np.abs(amps.astype(np.complex128)) ** 2)) if world == 1 else None
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            thr = os.cpu_count() or 1
+            r = rqc_reference_rate(allx[:4096], nq, rows, cols, depth, seed, thr)
+            if r is not None:
+                rate, dt, zr = r
+                same = bool(np.array_equal(zr.view(np.uint32), amps[:4096].view(np.uint32)))
+                cpu = {"value": round(rate, 1), "unit": "amplitudes/s", "cores": thr,
+                       "kind": "reference", "bit_identical_to_gpu": same,
+                       "sample": f"4096 bitstrings, run_rqc loop on {thr} threads, {dt:.2f} s"}
+        value = len(allx) / (ms * 1e-3)
+        line = {
+            "metric": RQC_METRIC, "value": round(value, 1), "unit": "amplitudes/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "c64 (FP32 tier, bit-identical to the reference)",
+            "data": "synthetic circuit rqc_rectangular(4,4,8,1)",
+            "config": {"workload": "configs[0] 4x4 RQC (1+8+1) single-amplitude TTGT contraction, "
+                                   "all 65536 bitstrings per step",
+                       "executor": "fused small-step kernel (one warp per bitstring)",
+                       "steps_per_amplitude": len(path), "parallelism": f"bitstrings / {world}"},
+            "fidelity": {"max_rel_err_vs_statevector": err, "median_rel_err": med,
+                         "sum_prob": norm},
+            "e2e": {"value": round(value, 1), "unit": "amplitudes/s",
+                    "h2d_bytes_per_step": int(mine.size), "d2h_bytes_per_step": int(len(mine) * 8)},
+            "gpu_launches": args.steps, "clocks": clk.summary(),
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    net.close()
+    h.close()
+
+
 def main():
     p = argparse.ArgumentParser()
+    p.add_argument("--workload", choices=["cgemm", "rqc"], default="cgemm")
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
@@ -394,7 +518,9 @@ def main():
     args = p.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.workload == "rqc":
+        run_rqc(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

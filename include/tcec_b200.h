@@ -63,9 +63,14 @@ int tcec_synchronize(tcec_handle h);
  * device counterpart of TilingConfig::k_tile (gemm.hpp:28-30). */
 int tcec_set_flush_kblocks(tcec_handle h, int kblocks);
 int tcec_get_flush_kblocks(tcec_handle h);
-/* tensor-core kernel variant: 1 = CTA pair (cta_group::2, 256 x 128 tiles,
- * default), 0 = single CTA (128 x 128 tiles) */
+/* tensor-core kernel variant: 0 = single CTA (128 x 128 tiles, default: measured
+ * faster with the per-k-block RN flush), 1 = CTA pair (cta_group::2, 256 x 128) */
 int tcec_set_gemm_variant(tcec_handle h, int variant);
+/* network executor: 0 = auto (fused small-step kernel -- one warp per network,
+ * intermediates in shared memory -- whenever every step is on a SIMT tier and
+ * the live intermediates fit; else per-step permute + dispatch through a
+ * captured CUDA graph), 1 = per-step only, 2 = fused only (error if ineligible) */
+int tcec_set_executor(tcec_handle h, int policy);
 /* stage tracing (the device counterpart of DecisionRecord::wall_ms,
  * precsel.hpp:92-101): when enabled, every synchronous tcec_dispatch_cgemm
  * records CUDA events around (statistics + selection), (operand preparation)

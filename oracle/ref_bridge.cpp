@@ -306,6 +306,34 @@ int ref_rqc_amplitude(int rows, int cols, int depth, std::uint64_t seed, const s
     }
 }
 
+// run_rqc's inner loop (experiments.cpp:211-230): one greedy path for the
+// circuit, then circuit_to_network + contract_network per bitstring, with the
+// bitstrings spread over host threads (amplitudes are independent).
+int ref_rqc_amplitudes_batch(int rows, int cols, int depth, std::uint64_t seed,
+                             const std::uint8_t* bits, int n_strings, const ConfigPod* cfg,
+                             float* out, int n_threads) {
+    try {
+        const Circuit c = rqc_rectangular(rows, cols, depth, seed);
+        const int nq = c.n_qubits;
+        const ContractionPath path = greedy_path(circuit_to_network(c, Bitstring(std::size_t(nq), 0)));
+        const DispatchConfig dc = to_config(cfg);
+        auto worker = [&](int t) {
+            for (int i = t; i < n_strings; i += n_threads) {
+                const TensorNetwork net = circuit_to_network(c, bits_of(bits + std::size_t(i) * nq, nq));
+                const TensorC32 r = contract_network(net, path, dc, nullptr);
+                out[2 * i] = r.data[0].real();
+                out[2 * i + 1] = r.data[0].imag();
+            }
+        };
+        std::vector<std::thread> pool;
+        for (int t = 0; t < std::max(1, n_threads); ++t) pool.emplace_back(worker, t);
+        for (auto& th : pool) th.join();
+        return 0;
+    } catch (...) {
+        return error_code();
+    }
+}
+
 // f64 TTGT pipeline on the same greedy path (network.cpp:179-186)
 void ref_rqc_amplitude_tn_oracle(int rows, int cols, int depth, std::uint64_t seed,
                                  const std::uint8_t* bits, double* out) {

@@ -122,6 +122,7 @@ def load() -> C.CDLL:
         "tcec_set_flush_kblocks": ([vp, i32], i32),
         "tcec_get_flush_kblocks": ([vp], i32),
         "tcec_set_gemm_variant": ([vp, i32], i32),
+        "tcec_set_executor": ([vp, i32], i32),
         "tcec_profile_enable": ([vp, i32], i32),
         "tcec_profile_read": ([vp, C.POINTER(dbl), C.POINTER(i64)], i32),
         "tcec_quantize_buf": ([vp, vp, vp, i64, i32, i32, ip], i32),

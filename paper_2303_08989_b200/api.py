@@ -98,6 +98,10 @@ class Handle:
     def flush_kblocks(self, v: int) -> None:
         check(self.lib.tcec_set_flush_kblocks(self.h, int(v)))
 
+    def set_executor(self, policy: int) -> None:
+        """0 auto, 1 per-step permute+dispatch graph only, 2 fused small-step only."""
+        check(self.lib.tcec_set_executor(self.h, int(policy)))
+
     def set_gemm_variant(self, pair: bool) -> None:
         """1 = CTA-pair (cta_group::2) TCEC kernel, 0 = single-CTA kernel."""
         check(self.lib.tcec_set_gemm_variant(self.h, int(pair)))

@@ -388,6 +388,13 @@ int tcec_set_flush_kblocks(tcec_handle h, int kblocks) {
 
 int tcec_get_flush_kblocks(tcec_handle h) { return h ? h->flush_kblocks : -1; }
 
+int tcec_set_executor(tcec_handle h, int policy) {
+    CHECK_HANDLE(h);
+    if (policy < 0 || policy > 2) return set_error(TCEC_ERR_INVALID_ARGUMENT, "executor must be 0, 1 or 2");
+    h->executor = policy;
+    return TCEC_OK;
+}
+
 int tcec_set_gemm_variant(tcec_handle h, int variant) {
     CHECK_HANDLE(h);
     if (variant < 0 || variant > 1) return set_error(TCEC_ERR_INVALID_ARGUMENT, "variant must be 0 or 1");

@@ -15,36 +15,9 @@
 #include <string>
 #include <vector>
 
-#include "tcec_handle.h"
+#include "network_plan.h"
 
 namespace tcec {
-
-struct NetNode {
-    std::vector<int> labels;
-    std::vector<int64_t> dims;
-    int64_t size() const {
-        int64_t s = 1;
-        for (auto d : dims) s *= d;
-        return s;
-    }
-};
-
-struct StepPlan {
-    int ia = 0, ib = 0;
-    int64_t m = 1, n = 1, k = 1;
-    bool perm_a = false, perm_b = false;
-    std::vector<int64_t> a_dims, b_dims;
-    std::vector<int> a_axis, b_axis;
-    int64_t a_size = 1, b_size = 1;
-    DispatchPlan dp;
-};
-
-struct FoldPlan {
-    std::vector<StepPlan> steps;
-    std::vector<int> out_labels;
-    std::vector<int64_t> out_dims;
-    size_t ws_bytes = 0;
-};
 
 static bool contains(const std::vector<int>& v, int x) {
     return std::find(v.begin(), v.end(), x) != v.end();
@@ -65,7 +38,9 @@ struct tcec_network_s {
     cudaGraphExec_t graph = nullptr;
     void* result_dev = nullptr;      // stable home of the final tensor
     int64_t result_size = 0;
+    tcec::SmallProgram small;        // fused small-step program (small_fold.cu)
     ~tcec_network_s() {
+        small.release();
         if (graph) cudaGraphExecDestroy(graph);
         if (node_dev) cudaFree(node_dev);
         if (result_dev) cudaFree(result_dev);
@@ -330,6 +305,33 @@ static int run_fold(tcec_network_s& net, const int* steps, int n_steps,
     return TCEC_OK;
 }
 
+// The fused small-step program for this (path, config, variable nodes), built
+// once and cached; nullptr when the executor policy or eligibility says no.
+static const SmallProgram* small_program(tcec_network_s& net, const int* steps, int n_steps,
+                                         const tcec_dispatch_config_t& cfg, const FoldPlan& plan,
+                                         const std::vector<int>& var_nodes, int* rc) {
+    *rc = TCEC_OK;
+    const int policy = net.h->executor;  // 0 auto, 1 per-step only, 2 fused only
+    if (policy == 1) return nullptr;
+    std::string key(reinterpret_cast<const char*>(steps), size_t(n_steps) * 2 * sizeof(int));
+    key.append(reinterpret_cast<const char*>(&cfg), sizeof(cfg));
+    key.append(reinterpret_cast<const char*>(var_nodes.data()), var_nodes.size() * sizeof(int));
+    if (net.small.key != key) {
+        net.small.release();
+        build_small_program(net.nodes, net.offset, plan, var_nodes, &net.small);
+        net.small.key = key;
+        if (net.small.ok) {
+            *rc = upload_small_program(&net.small);
+            if (*rc) return nullptr;
+        }
+    }
+    if (!net.small.ok) {
+        if (policy == 2) *rc = set_error(TCEC_ERR_INVALID_ARGUMENT, "fused executor: " + net.small.why);
+        return nullptr;
+    }
+    return &net.small;
+}
+
 // ------------------------------------------------------------- greedy path
 
 struct Summary {
@@ -502,7 +504,14 @@ int tcec_contract_network(tcec_network net, const int* steps, int n_steps,
     void* ws = nullptr;
     int rc = prepare(*net, steps, n_steps, *cfg, &plan, &dec, &ws);
     if (rc) return rc;
-    rc = run_fold(*net, steps, n_steps, *cfg, plan, dec, ws, false);
+    const SmallProgram* sp_fused = small_program(*net, steps, n_steps, *cfg, plan, {}, &rc);
+    if (rc) return rc;
+    if (sp_fused) {
+        rc = launch_small_program(*sp_fused, static_cast<const float2*>(net->node_dev), 1, nullptr, 0,
+                                  nullptr, static_cast<float2*>(net->result_dev), h.stream);
+    } else {
+        rc = run_fold(*net, steps, n_steps, *cfg, plan, dec, ws, false);
+    }
     if (rc) return rc;
     int64_t size = 1;
     for (auto d : plan.out_dims) size *= d;
@@ -511,7 +520,9 @@ int tcec_contract_network(tcec_network net, const int* steps, int n_steps,
                                     cudaMemcpyDeviceToHost, h.stream);
     if (e != cudaSuccess) return cuda_error(e, "result download");
     std::vector<DevDecision> dd(plan.steps.size());
-    if (!plan.steps.empty()) {
+    if (sp_fused) {
+        std::memset(dd.data(), 0, sizeof(DevDecision) * dd.size());  // SIMT tiers: no statistics
+    } else if (!plan.steps.empty()) {
         e = cudaMemcpyAsync(dd.data(), dec, sizeof(DevDecision) * dd.size(), cudaMemcpyDeviceToHost,
                             h.stream);
         if (e != cudaSuccess) return cuda_error(e, "decision download");
@@ -571,13 +582,23 @@ int tcec_contract_selector_batch(tcec_network net, const int* steps, int n_steps
     if (e != cudaSuccess) return cuda_error(e, "batch buffers");
     cudaMemcpyAsync(d_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice, s);
     if (nbits) cudaMemcpyAsync(d_bits, bits, nbits, cudaMemcpyHostToDevice, s);
-    for (int i = 0; i < n_strings; ++i) {
-        if (n_sel)
-            set_selectors_kernel<<<(n_sel + 127) / 128, 128, 0, s>>>(
-                static_cast<float2*>(net->node_dev), d_off, n_sel, d_bits + size_t(i) * n_sel);
-        rc = run_fold(*net, steps, n_steps, *cfg, plan, dec, ws, true);
+    const std::vector<int> sel_vec(sel_nodes, sel_nodes + n_sel);
+    const SmallProgram* fused = small_program(*net, steps, n_steps, *cfg, plan, sel_vec, &rc);
+    if (rc) return rc;
+    if (fused) {
+        // one launch: one warp per bitstring, selectors built from the bits
+        rc = launch_small_program(*fused, static_cast<const float2*>(net->node_dev), n_strings,
+                                  nullptr, 0, d_bits, d_out, s);
         if (rc) return rc;
-        cudaMemcpyAsync(d_out + i, net->result_dev, 8, cudaMemcpyDeviceToDevice, s);
+    } else {
+        for (int i = 0; i < n_strings; ++i) {
+            if (n_sel)
+                set_selectors_kernel<<<(n_sel + 127) / 128, 128, 0, s>>>(
+                    static_cast<float2*>(net->node_dev), d_off, n_sel, d_bits + size_t(i) * n_sel);
+            rc = run_fold(*net, steps, n_steps, *cfg, plan, dec, ws, true);
+            if (rc) return rc;
+            cudaMemcpyAsync(d_out + i, net->result_dev, 8, cudaMemcpyDeviceToDevice, s);
+        }
     }
     e = cudaMemcpyAsync(out_host, d_out, size_t(n_strings) * 8, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return cuda_error(e, "batch download");
@@ -631,13 +652,23 @@ int tcec_contract_node_batch(tcec_network net, const int* steps, int n_steps,
     if (!seg.empty()) cudaMemcpyAsync(d_seg, seg.data(), seg.size() * 8, cudaMemcpyHostToDevice, s);
     if (per_run * n_runs > 0)
         cudaMemcpyAsync(d_var, var_data, size_t(per_run * n_runs) * 8, cudaMemcpyHostToDevice, s);
-    for (int r = 0; r < n_runs; ++r) {
-        if (n_var)
-            scatter_nodes_kernel<<<std::min(n_var, 1024), 64, 0, s>>>(
-                static_cast<float2*>(net->node_dev), d_var + size_t(r) * size_t(per_run), d_seg, n_var);
-        rc = run_fold(*net, steps, n_steps, *cfg, plan, dec, ws, true);
+    const std::vector<int> var_vec(var_nodes, var_nodes + n_var);
+    const SmallProgram* fused = small_program(*net, steps, n_steps, *cfg, plan, var_vec, &rc);
+    if (rc) return rc;
+    if (fused) {
+        rc = launch_small_program(*fused, static_cast<const float2*>(net->node_dev), n_runs, d_var,
+                                  per_run, nullptr, d_out, s);
         if (rc) return rc;
-        cudaMemcpyAsync(d_out + r, net->result_dev, 8, cudaMemcpyDeviceToDevice, s);
+    } else {
+        for (int r = 0; r < n_runs; ++r) {
+            if (n_var)
+                scatter_nodes_kernel<<<std::min(n_var, 1024), 64, 0, s>>>(
+                    static_cast<float2*>(net->node_dev), d_var + size_t(r) * size_t(per_run), d_seg,
+                    n_var);
+            rc = run_fold(*net, steps, n_steps, *cfg, plan, dec, ws, true);
+            if (rc) return rc;
+            cudaMemcpyAsync(d_out + r, net->result_dev, 8, cudaMemcpyDeviceToDevice, s);
+        }
     }
     e = cudaMemcpyAsync(out_host, d_out, size_t(n_runs) * 8, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return cuda_error(e, "batch download");

@@ -14,6 +14,7 @@ struct tcec_handle_s {
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     int flush_kblocks = 1;  // RN flush of the main term every k-block (64 f16 / 32 tf32 K')
+    int executor = 0;       // network executor: 0 auto, 1 per-step only, 2 fused only
     int gemm_pair = 0;      // 1 = cta_group::2 TCEC kernel (tcec_set_gemm_variant); 0 measured faster
     // operand workspace (split hi/lo planes), grown on demand
     void* ws = nullptr;

@@ -84,8 +84,15 @@ def test_path_errors(handle):
         net.contract([(0, 1), (0, 2)], BASELINE)  # dead node
 
 
+@pytest.fixture(params=[1, 2], ids=["per-step", "fused"])
+def executor(request, handle):
+    handle.set_executor(request.param)
+    yield request.param
+    handle.set_executor(0)
+
+
 @pytest.mark.parametrize("case", [0, 1, 2, 3])
-def test_rqc_amplitudes_bit_exact_vs_reference(handle, golden, case):
+def test_rqc_amplitudes_bit_exact_vs_reference(handle, golden, case, executor):
     rq = golden("rqc.json")[case]
     c = rqc_rectangular(rq["rows"], rq["cols"], rq["depth"], rq["seed"])
     path = [tuple(s) for s in rq["path"]]
@@ -135,7 +142,7 @@ def test_rqc_tensor_core_modes_accuracy(handle, golden, case):
         assert med[m] <= 1e-4 and med[m] <= max(4 * mb, 1e-6), (m, med, mb)
 
 
-def test_selector_batch_equals_single_amplitudes(handle, golden):
+def test_selector_batch_equals_single_amplitudes(handle, golden, executor):
     rq = golden("rqc.json")[2]  # 4x4, depth 1+8+1
     c = rqc_rectangular(rq["rows"], rq["cols"], rq["depth"], rq["seed"])
     xs = [row["x"] for row in rq["amplitudes"]]
@@ -156,3 +163,38 @@ def test_amplitude_api_and_statevector(handle):
         got = complex(amplitude(handle, c, x, SelectionPolicy()))
         want = amplitude_sv(c, x)
         assert abs(got - want) <= 1e-5 * abs(want)
+
+
+def test_fused_and_per_step_agree_on_all_amplitudes_of_a_small_circuit(handle):
+    """Every 2^9 amplitude of a 3x3 circuit: the two executors give the same
+    bits and the probabilities sum to 1 (the circuit is unitary)."""
+    c = rqc_rectangular(3, 3, 8, 7)
+    xs = [[(v >> q) & 1 for q in range(9)] for v in range(512)]
+    net = Network(handle, circuit_to_network(c, xs[0]))
+    path = net.greedy_path()
+    handle.set_executor(2)
+    fused = net.selector_batch(path, xs, BASELINE)
+    handle.set_executor(1)
+    stepwise = net.selector_batch(path, xs, BASELINE)
+    handle.set_executor(0)
+    net.close()
+    assert np.array_equal(fused.view(np.uint32), stepwise.view(np.uint32))
+    assert abs(float(np.sum(np.abs(fused.astype(np.complex128)) ** 2)) - 1.0) < 1e-5
+
+
+def test_sliced_amplitude_on_device(handle):
+    from oracle.network import contract_network_f64
+    from paper_2303_08989_b200.slicing import (SlicePlan, device_evaluator, find_slices,
+                                               sliced_amplitude)
+    c = rqc_rectangular(3, 4, 8, 11)
+    spec = circuit_to_network(c, [1, 0] * 6)
+    path = Network(None, spec).greedy_path()
+    _, _, z = contract_network_f64(spec, path)
+    plan = SlicePlan.build(spec, path, find_slices(spec, path, n_labels=4))
+    net = Network(handle, plan.base)
+    for policy in (1, 2):
+        handle.set_executor(policy)
+        amp, full = sliced_amplitude(device_evaluator(net, plan, BASELINE), plan)
+        assert abs(amp - complex(z[0])) <= 1e-5 * abs(complex(z[0]))
+    handle.set_executor(0)
+    net.close()
