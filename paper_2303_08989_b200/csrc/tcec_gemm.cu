@@ -215,17 +215,14 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
             const int buf = ch % kMainBufs;
             mbar_wait(&tail->tfull[buf], (ch / kMainBufs) & 1);
             tc_fence_after();
-#pragma unroll
-            for (int cb = 0; cb < kCols / 32; ++cb) {
-                float v[32];
-                tmem_ld32(lane_base + uint32_t(buf * BN + 32 * cb), v);
-#pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    acc[32 * cb + i] = ch == 0 ? v[i] : __fadd_rn(acc[32 * cb + i], v[i]);
-            }
+            float v[kCols];
+            tmem_ld64(lane_base + uint32_t(buf * BN), v);
+            // the partial is in registers: hand the TMEM buffer back first
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tail->tempty[buf]);
+#pragma unroll
+            for (int i = 0; i < kCols; ++i) acc[i] = ch == 0 ? v[i] : __fadd_rn(acc[i], v[i]);
         }
         if (corrected && nkb > 0) {
 #pragma unroll
@@ -435,17 +432,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
             const int buf = ch % kMainBufs;
             mbar_wait(&tail->tfull[buf], (ch / kMainBufs) & 1);
             tc_fence_after();
-#pragma unroll
-            for (int cb = 0; cb < kCols / 32; ++cb) {
-                float v[32];
-                tmem_ld32(lane_base + uint32_t(buf * BN + 32 * cb), v);
-#pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    acc[32 * cb + i] = ch == 0 ? v[i] : __fadd_rn(acc[32 * cb + i], v[i]);
-            }
+            float v[kCols];
+            tmem_ld64(lane_base + uint32_t(buf * BN), v);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(tempty_leader0 + uint32_t(buf * sizeof(uint64_t)));
+#pragma unroll
+            for (int i = 0; i < kCols; ++i) acc[i] = ch == 0 ? v[i] : __fadd_rn(acc[i], v[i]);
         }
         if (corrected && nkb > 0) {
 #pragma unroll
