@@ -97,7 +97,7 @@ def contract_network_f64(spec, path):
 
 def statevector(circuit):
     """statevector_oracle (qcircuit.cpp:197-225): qubit q = bit q of the index."""
-    from paper_2303_08989_b200.circuits import CZ, gate_matrix  # workload definition only
+    from paper_2303_08989_b200.circuits import CZ, FSIM, gate_matrix  # workload definition only
     n = circuit.n_qubits
     if n > 24:
         raise ValueError("state-vector oracle limited to 24 qubits")
@@ -110,6 +110,16 @@ def statevector(circuit):
                 ma, mb = 1 << g.qubits[0], 1 << g.qubits[1]
                 sel = (idx & ma != 0) & (idx & mb != 0)
                 state[sel] = -state[sel]
+                continue
+            if g.kind == FSIM:
+                # generic two-qubit unitary, index bits (q_a, q_b) = row-major (oa, ob)
+                u = gate_matrix(g.kind).reshape(4, 4)
+                ma, mb = 1 << g.qubits[0], 1 << g.qubits[1]
+                base = idx[((idx & ma) == 0) & ((idx & mb) == 0)]
+                cols = [base, base | mb, base | ma, base | ma | mb]
+                vals = [state[c].copy() for c in cols]
+                for r in range(4):
+                    state[cols[r]] = sum(u[r, cc] * vals[cc] for cc in range(4))
                 continue
             u = gate_matrix(g.kind)
             mq = 1 << g.qubits[0]

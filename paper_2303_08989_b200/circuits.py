@@ -104,7 +104,9 @@ class Rng:
 
 # ------------------------------------------------------------------ gates
 H, T, SX, SY, CZ = "H", "T", "SX", "SY", "CZ"
+SW, FSIM = "SW", "FSIM"  # Sycamore-class extension (not in the reference gate set)
 _SINGLES = (T, SX, SY)
+TWO_QUBIT = (CZ, FSIM)
 
 
 def gate_matrix(kind: str) -> np.ndarray:
@@ -121,6 +123,17 @@ def gate_matrix(kind: str) -> np.ndarray:
     if kind == CZ:
         m = np.eye(4, dtype=np.complex128)
         m[3, 3] = -1.0
+        return m.reshape(-1)
+    if kind == SW:
+        # sqrt(W), W = (X + Y)/sqrt(2): 1/sqrt2 [[1, -e^{i pi/4}], [e^{-i pi/4}, 1]]
+        w = np.exp(1j * math.pi / 4)
+        return np.array([s, -s * w, s * np.conj(w), s], dtype=np.complex128)
+    if kind == FSIM:
+        # fSim(theta = pi/2, phi = pi/6) of the Sycamore RCS experiment
+        m = np.zeros((4, 4), dtype=np.complex128)
+        m[0, 0] = 1.0
+        m[1, 2] = m[2, 1] = -1j
+        m[3, 3] = np.exp(-1j * math.pi / 6)
         return m.reshape(-1)
     raise ValueError(f"unknown gate: {kind}")
 
@@ -142,7 +155,7 @@ def validate_circuit(c: Circuit) -> None:
     for layer in c.layers:
         touched = set()
         for g in layer:
-            want = 2 if g.kind == CZ else 1
+            want = 2 if g.kind in TWO_QUBIT else 1
             if len(g.qubits) != want:
                 raise ValueError("gate has wrong qubit count")
             for q in g.qubits:
@@ -231,7 +244,7 @@ def circuit_to_network(c: Circuit, x) -> NetworkSpec:
         net.data.append(np.array([1.0, 0.0], dtype=np.complex64))
     for layer in c.layers:
         for g in layer:
-            if g.kind == CZ:
+            if g.kind in TWO_QUBIT:
                 a, b = g.qubits
                 net.labels.append([_wire(a, step[a] + 1), _wire(b, step[b] + 1), _wire(a, step[a]),
                                    _wire(b, step[b])])
@@ -295,8 +308,70 @@ def load_circuit(text: str) -> Circuit:
         else:
             if not in_layer:
                 raise ValueError("gate outside layer block")
-            if tok[0] not in (H, T, SX, SY, CZ):
+            if tok[0] not in (H, T, SX, SY, CZ, SW, FSIM):
                 raise ValueError("unknown gate: " + tok[0])
             c.layers[-1].append(Gate(tok[0], tuple(int(q) for q in tok[1:])))
     validate_circuit(c)
+    return c
+
+
+# ------------------------------------------------- Sycamore-class (configs[3])
+def sycamore_qubits():
+    """The 54-site rotated-square layout of the Sycamore chip as grid
+    coordinates (row r has the listed column span); site (5, 0) is dropped to
+    leave 53 active qubits, as in the RCS experiment.  Qubit index = position
+    in this row-major list."""
+    spans = [(0, 5, 6), (1, 4, 7), (2, 3, 8), (3, 2, 9), (4, 1, 9), (5, 1, 8), (6, 1, 7),
+             (7, 2, 6), (8, 3, 5), (9, 4, 4)]
+    sites = []
+    for r, c0, c1 in spans:
+        for c in range(c0, c1 + 1):
+            sites.append((r, c))
+    return sites
+
+
+def sycamore_couplers(sites, pattern: str):
+    """Couplers of pattern A/B/C/D: A/B are the two halves of the horizontal
+    grid bonds, C/D of the vertical ones (alternating parity), so every qubit
+    has at most one coupler per pattern."""
+    pos = {s: i for i, s in enumerate(sites)}
+    pairs = []
+    for (r, c), i in pos.items():
+        if pattern in "AB":
+            nb = (r, c + 1)
+            par = (r + c) % 2 == (0 if pattern == "A" else 1)
+        else:
+            nb = (r + 1, c)
+            par = (r + c) % 2 == (0 if pattern == "C" else 1)
+        if par and nb in pos:
+            pairs.append((i, pos[nb]))
+    return pairs
+
+
+def sycamore_like(cycles: int, seed: int) -> Circuit:
+    """Sycamore-class random circuit: `cycles` cycles of (random single-qubit
+    gate from {sqrtX, sqrtY, sqrtW}, never repeating on a qubit) + fSim(pi/2,
+    pi/6) on the couplers of the pattern sequence ABCDCDAB, then a final
+    single-qubit layer.  Uses the reference Rng for reproducibility."""
+    sites = sycamore_qubits()
+    n = len(sites)
+    rng = Rng(seed)
+    c = Circuit(n_qubits=n)
+    singles = (SX, SY, SW)
+    last = [-1] * n
+    order = "ABCDCDAB"
+
+    def single_layer():
+        layer = []
+        for q in range(n):
+            allowed = [g for g in range(3) if g != last[q]]
+            pick = allowed[rng.next_below(len(allowed))]
+            last[q] = pick
+            layer.append(Gate(singles[pick], (q,)))
+        return layer
+
+    for cyc in range(cycles):
+        c.layers.append(single_layer())
+        c.layers.append([Gate(FSIM, pair) for pair in sycamore_couplers(sites, order[cyc % 8])])
+    c.layers.append(single_layer())
     return c

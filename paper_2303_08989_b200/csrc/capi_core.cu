@@ -3,6 +3,7 @@
 // device pipeline).  Mirrors reference precsel.cpp:225-322 (dispatch_cgemm),
 // cgemm.cpp:25-46 (cgemm) and gemm.cpp:60-125 (mode switch).
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -202,6 +203,8 @@ int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t
     g.d = d;
     g.kind_fixed = p.kind;
     g.corrected = p.corrected;
+    // diagnostic only (tools/gpu_variants.py): same MMAs, hi tiles loaded for lo
+    if (p.corrected && std::getenv("TCEC_DIAG_HALF_BYTES")) g.corrected = 2;
     g.flush_kblocks = p.corrected ? h.flush_kblocks : 0;
     g.pair = h.gemm_pair;
     const bool want16 = p.kind < 0 || p.kind == kKindFp16 || p.kind == kKindFp16Scaled;

@@ -9,6 +9,8 @@
 //   gemm_rows_rn (+ cgemm.cpp assembly)                        -> cgemm_fp32_ref_kernel
 //   gemm_rows_f64                                               -> cgemm_fp64_kernel
 //   permute (tensor.hpp:56-105)                                 -> permute_kernel
+#include <type_traits>
+
 #include "tcec_common.cuh"
 #include "tcec_internal.h"
 
@@ -367,7 +369,9 @@ __global__ void __launch_bounds__(256) prep_b_kernel(const float2* __restrict__ 
     const double factor = ldexp(1.0, pm.scale);
     __shared__ float2 tile[32][33];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-    const int64_t j0 = int64_t(blockIdx.x) * 32, kk0 = int64_t(blockIdx.y) * 32;
+    // 1-D grid (no 65535 limit on tall or long operands): x = kk_tile * tiles_j + j_tile
+    const int64_t tiles_j = (n + 31) / 32;
+    const int64_t j0 = (int64_t(blockIdx.x) % tiles_j) * 32, kk0 = (int64_t(blockIdx.x) / tiles_j) * 32;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
         const int64_t kk = kk0 + ty + 8 * r, j = j0 + tx;
@@ -425,7 +429,8 @@ __global__ void __launch_bounds__(256) cgemm_fp32_ref_kernel(const float2* __res
                                                              int64_t n, int64_t k) {
     __shared__ float sar[SB_K][SB_M], sai[SB_K][SB_M], sbr[SB_K][SB_N], sbi[SB_K][SB_N];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const int64_t i0 = int64_t(blockIdx.y) * SB_M, j0 = int64_t(blockIdx.x) * SB_N;
+    const int64_t tiles_n = (n + SB_N - 1) / SB_N;  // 1-D grid: x = i_tile * tiles_n + j_tile
+    const int64_t i0 = (int64_t(blockIdx.x) / tiles_n) * SB_M, j0 = (int64_t(blockIdx.x) % tiles_n) * SB_N;
     float p1[4][4], p2[4][4], p3[4][4], p4[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -489,8 +494,9 @@ __global__ void __launch_bounds__(256) cgemm_fp32_ref_kernel(const float2* __res
 // rounded to f32 (gemm.cpp:111-117), then assembled in f32 (cgemm.cpp:38-44)
 __global__ void cgemm_fp64_kernel(const float2* __restrict__ a, const float2* __restrict__ b,
                                   float2* __restrict__ c, int64_t m, int64_t n, int64_t k) {
-    const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-    const int64_t i = blockIdx.y;
+    const int64_t tiles_n = (n + int64_t(blockDim.x) - 1) / blockDim.x;
+    const int64_t j = (int64_t(blockIdx.x) % tiles_n) * blockDim.x + threadIdx.x;
+    const int64_t i = int64_t(blockIdx.x) / tiles_n;
     if (j >= n || i >= m) return;
     double p1 = 0.0, p2 = 0.0, p3 = 0.0, p4 = 0.0;
     for (int64_t kk = 0; kk < k; ++kk) {
@@ -503,6 +509,60 @@ __global__ void cgemm_fp64_kernel(const float2* __restrict__ a, const float2* __
     }
     c[i * n + j] = make_float2(__fsub_rn(__double2float_rn(p1), __double2float_rn(p2)),
                                __fadd_rn(__double2float_rn(p3), __double2float_rn(p4)));
+}
+
+// Long-k / few-output shapes (e.g. the (1, 1, 2^22) dot products of deep
+// circuits): one warp per output element, the warp loads 32 consecutive k of
+// A and B coalesced (prefetching the next 32), and every lane runs the same
+// four chains in ascending k on shuffled operands -- the reference order, so
+// the result is bit-identical to kernels_scalar.cpp:76-87 / :137-148.
+template <bool F64>
+__global__ void __launch_bounds__(256) cgemm_longk_kernel(const float2* __restrict__ a,
+                                                          const float2* __restrict__ b,
+                                                          float2* __restrict__ c, int64_t m,
+                                                          int64_t n, int64_t k) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+    if (w >= m * n) return;
+    const int64_t i = w / n, j = w - (w / n) * n;
+    using acc_t = typename std::conditional<F64, double, float>::type;
+    acc_t p1 = 0, p2 = 0, p3 = 0, p4 = 0;
+    const float2* arow = a + i * k;
+    const float2 zero = make_float2(0.0f, 0.0f);
+    float2 av = lane < k ? arow[lane] : zero;
+    float2 bv = lane < k ? b[int64_t(lane) * n + j] : zero;
+    for (int64_t k0 = 0; k0 < k; k0 += 32) {
+        const int64_t kn = k0 + 32 + lane;
+        const float2 an = kn < k ? arow[kn] : zero;
+        const float2 bn = kn < k ? b[kn * n + j] : zero;
+        const int cnt = (k - k0) < 32 ? int(k - k0) : 32;
+        for (int t = 0; t < cnt; ++t) {
+            const float ar = __shfl_sync(0xFFFFFFFFu, av.x, t);
+            const float ai = __shfl_sync(0xFFFFFFFFu, av.y, t);
+            const float br = __shfl_sync(0xFFFFFFFFu, bv.x, t);
+            const float bi = __shfl_sync(0xFFFFFFFFu, bv.y, t);
+            if (F64) {
+                p1 = __dadd_rn(p1, __dmul_rn(double(ar), double(br)));
+                p2 = __dadd_rn(p2, __dmul_rn(double(ai), double(bi)));
+                p3 = __dadd_rn(p3, __dmul_rn(double(ar), double(bi)));
+                p4 = __dadd_rn(p4, __dmul_rn(double(ai), double(br)));
+            } else {
+                p1 = __fadd_rn(float(p1), __fmul_rn(ar, br));
+                p2 = __fadd_rn(float(p2), __fmul_rn(ai, bi));
+                p3 = __fadd_rn(float(p3), __fmul_rn(ar, bi));
+                p4 = __fadd_rn(float(p4), __fmul_rn(ai, br));
+            }
+        }
+        av = an;
+        bv = bn;
+    }
+    if (lane == 0) {
+        if (F64)
+            c[i * n + j] = make_float2(__fsub_rn(__double2float_rn(double(p1)), __double2float_rn(double(p2))),
+                                       __fadd_rn(__double2float_rn(double(p3)), __double2float_rn(double(p4))));
+        else
+            c[i * n + j] = make_float2(__fsub_rn(float(p1), float(p2)), __fadd_rn(float(p3), float(p4)));
+    }
 }
 
 // --------------------------------------------------------------- permute
@@ -533,7 +593,151 @@ __global__ void __launch_bounds__(kThreads) permute_kernel(const float2* __restr
     }
 }
 
+// Tiled permute (cuTT-style "tiled" plan for high-rank, dim-2 tensors): the
+// innermost input axes I (product P_I <= 64, contiguous in the source) and the
+// innermost output axes O (product P_O <= 64, contiguous in the destination)
+// form a P_O x P_I tile staged through shared memory; every other axis is a
+// batch index decoded per block.  Both the global reads (along I) and the
+// global writes (along O) are coalesced.
+constexpr int kTileMax = 64;
+
+struct TiledPermDesc {
+    int pi, po;                       // tile extents
+    int nbatch;                       // batch axes (output order)
+    int64_t batches;
+    int64_t bdim[kMaxRank], bin[kMaxRank], bout[kMaxRank];
+    int32_t offi_out[kTileMax];       // output offset of input-inner index i
+    int32_t offo_in[kTileMax];        // input offset of output-inner index o
+};
+
+__global__ void __launch_bounds__(256) permute_tiled_kernel(const float2* __restrict__ src,
+                                                            float2* __restrict__ dst,
+                                                            const TiledPermDesc d) {
+    __shared__ float2 tile[kTileMax][kTileMax + 1];
+    __shared__ int32_t offi[kTileMax], offo[kTileMax];
+    if (threadIdx.x < kTileMax) {
+        offi[threadIdx.x] = d.offi_out[threadIdx.x];
+        offo[threadIdx.x] = d.offo_in[threadIdx.x];
+    }
+    const int tile_n = d.pi * d.po;
+    for (int64_t b = blockIdx.x; b < d.batches; b += gridDim.x) {
+        int64_t rem = b, base_in = 0, base_out = 0;
+        for (int a = d.nbatch - 1; a >= 0; --a) {
+            const int64_t q = rem / d.bdim[a];
+            const int64_t x = rem - q * d.bdim[a];
+            base_in += x * d.bin[a];
+            base_out += x * d.bout[a];
+            rem = q;
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < tile_n; t += blockDim.x) {
+            const int o = t / d.pi, i = t - o * d.pi;
+            tile[o][i] = src[base_in + offo[o] + i];
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < tile_n; t += blockDim.x) {
+            const int i = t / d.po, o = t - i * d.po;
+            dst[base_out + offi[i] + o] = tile[o][i];
+        }
+    }
+}
+
 }  // namespace
+
+// Plan the tiled permute; false when the shape does not suit it.
+static bool plan_tiled(int r, const int64_t* dim_in, const int64_t* in_stride_in, TiledPermDesc* d) {
+    // axes in output order with output strides, splitting large axes into
+    // (D/32, 32) so tiles stay <= 64 per side
+    int64_t dim[kMaxRank], ist[kMaxRank], ost[kMaxRank];
+    int n = 0;
+    int64_t os = 1;
+    int64_t tmp_dim[kMaxRank], tmp_ist[kMaxRank];
+    for (int a = 0; a < r; ++a) {
+        tmp_dim[a] = dim_in[a];
+        tmp_ist[a] = in_stride_in[a];
+    }
+    int64_t odim[kMaxRank], oist[kMaxRank];
+    int m = 0;
+    for (int a = 0; a < r; ++a) {
+        const int64_t D = tmp_dim[a], S = tmp_ist[a];
+        if (D > kTileMax) {
+            if (D % 32 != 0 || m + 2 > kMaxRank) return false;
+            odim[m] = D / 32;
+            oist[m++] = S * 32;
+            odim[m] = 32;
+            oist[m++] = S;
+        } else {
+            if (m + 1 > kMaxRank) return false;
+            odim[m] = D;
+            oist[m++] = S;
+        }
+    }
+    for (int a = m - 1; a >= 0; --a) {
+        dim[a] = odim[a];
+        ist[a] = oist[a];
+        ost[a] = os;
+        os *= odim[a];
+    }
+    n = m;
+    // input-inner group: axes by ascending input stride, contiguous block
+    int order[kMaxRank];
+    for (int a = 0; a < n; ++a) order[a] = a;
+    for (int a = 1; a < n; ++a)
+        for (int b = a; b > 0 && ist[order[b]] < ist[order[b - 1]]; --b) {
+            const int t = order[b];
+            order[b] = order[b - 1];
+            order[b - 1] = t;
+        }
+    bool in_I[kMaxRank] = {false}, in_O[kMaxRank] = {false};
+    int64_t pi = 1;
+    int nI = 0;
+    for (int j = 0; j < n; ++j) {
+        const int a = order[j];
+        if (ist[a] != pi || pi * dim[a] > kTileMax) break;
+        pi *= dim[a];
+        in_I[a] = true;
+        ++nI;
+    }
+    int64_t po = 1;
+    for (int a = n - 1; a >= 0; --a) {
+        if (po * dim[a] > kTileMax) break;
+        if (in_I[a]) return false;  // overlapping groups: the gather kernel handles it
+        po *= dim[a];
+        in_O[a] = true;
+    }
+    if (pi < 8 || po < 8) return false;
+    d->pi = int(pi);
+    d->po = int(po);
+    // offsets inside the tile
+    for (int i = 0; i < pi; ++i) {
+        int64_t rem = i, off = 0;
+        for (int j = 0; j < nI; ++j) {
+            const int a = order[j];
+            off += (rem % dim[a]) * ost[a];
+            rem /= dim[a];
+        }
+        d->offi_out[i] = int32_t(off);
+    }
+    for (int o = 0; o < po; ++o) {
+        int64_t rem = o, off = 0;
+        for (int a = n - 1; a >= 0 && in_O[a]; --a) {
+            off += (rem % dim[a]) * ist[a];
+            rem /= dim[a];
+        }
+        d->offo_in[o] = int32_t(off);
+    }
+    d->nbatch = 0;
+    d->batches = 1;
+    for (int a = 0; a < n; ++a) {
+        if (in_I[a] || in_O[a]) continue;
+        d->bdim[d->nbatch] = dim[a];
+        d->bin[d->nbatch] = ist[a];
+        d->bout[d->nbatch] = ost[a];
+        d->batches *= dim[a];
+        ++d->nbatch;
+    }
+    return true;
+}
 
 // ================================================================ launchers
 
@@ -591,7 +795,7 @@ void launch_prep_a(const float* a, int64_t m, int64_t k, int64_t kp, void* hi, v
 void launch_prep_b(const float* b, int64_t k, int64_t n, int64_t kp, void* hi, void* lo,
                    const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s) {
     if (n <= 0 || kp <= 0) return;
-    dim3 grid(unsigned((n + 31) / 32), unsigned((kp / 2 + 31) / 32));
+    const unsigned grid = unsigned(((n + 31) / 32) * ((kp / 2 + 31) / 32));
     prep_b_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const float2*>(b), k, n, kp, hi, lo, d,
                                        kind_fixed, corrected);
 }
@@ -599,14 +803,23 @@ void launch_prep_b(const float* b, int64_t k, int64_t n, int64_t kp, void* hi, v
 void launch_cgemm_fp32_ref(const float2* a, const float2* b, float2* c, int64_t m, int64_t n,
                            int64_t k, cudaStream_t s) {
     if (m <= 0 || n <= 0) return;
-    dim3 grid(unsigned((n + SB_N - 1) / SB_N), unsigned((m + SB_M - 1) / SB_M));
-    cgemm_fp32_ref_kernel<<<grid, 256, 0, s>>>(a, b, c, m, n, k);
+    const int64_t tiles = ((n + SB_N - 1) / SB_N) * ((m + SB_M - 1) / SB_M);
+    if (k >= 1024 && m * n <= 65536 && tiles < 2 * 148) {
+        const int64_t warps = m * n;
+        cgemm_longk_kernel<false><<<unsigned((warps + 7) / 8), 256, 0, s>>>(a, b, c, m, n, k);
+        return;
+    }
+    cgemm_fp32_ref_kernel<<<unsigned(tiles), 256, 0, s>>>(a, b, c, m, n, k);
 }
 
 void launch_cgemm_fp64(const float2* a, const float2* b, float2* c, int64_t m, int64_t n,
                        int64_t k, cudaStream_t s) {
     if (m <= 0 || n <= 0) return;
-    dim3 grid(unsigned((n + 127) / 128), unsigned(m));
+    if (k >= 256 && m * n <= 65536) {
+        cgemm_longk_kernel<true><<<unsigned((m * n + 7) / 8), 256, 0, s>>>(a, b, c, m, n, k);
+        return;
+    }
+    const unsigned grid = unsigned(((n + 127) / 128) * m);
     cgemm_fp64_kernel<<<grid, 128, 0, s>>>(a, b, c, m, n, k);
 }
 
@@ -636,6 +849,15 @@ void launch_permute(const float2* src, float2* dst, int rank, const int64_t* old
         }
     }
     desc.rank = r;
+    // innermost output axis not contiguous in the source: shared-memory tiles
+    if (r >= 2 && desc.in_stride[r - 1] != 1 && total >= 4096) {
+        static TiledPermDesc td;  // host-side scratch (kernel arguments are copied at launch)
+        if (plan_tiled(r, desc.out_dim, desc.in_stride, &td)) {
+            const int64_t g = td.batches < 148 * 16 ? td.batches : 148 * 16;
+            permute_tiled_kernel<<<unsigned(g), 256, 0, s>>>(src, dst, td);
+            return;
+        }
+    }
     permute_kernel<<<grid_for(total, kThreads, 148 * 32), kThreads, 0, s>>>(src, dst, desc);
 }
 

@@ -191,3 +191,41 @@ def test_tcec_full_size_row_sampled(handle, dev, n):
         c, _ = handle.cgemm(ad, bd, mode)
         e = relerr(c[torch.from_numpy(rows).to(dev)].cpu().numpy(), ref)
         assert e <= 2e-6, (mode, e)
+
+
+@pytest.mark.parametrize("shape", [(1 << 17, 2, 2), (2, 1 << 17, 2), (2, 2, 1 << 17),
+                                   (70000, 3, 1), (3, 1, 70000), (1, 70000, 5)])
+def test_extreme_aspect_shapes(handle, orc, dev, shape):
+    """(2, 2^N, 2)-family and tall/long operands: the grid
+    mappings must not hit the 65535 grid.y limit; FP32 tier bit-exact, TCEC
+    within tolerance."""
+    m, n, k = shape
+    a = matrix_recipe("uniform", m, k, 5)
+    b = matrix_recipe("uniform", k, n, 6)
+    ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    c, _ = handle.cgemm(ad, bd, "FP32_REF")
+    cr, _ = orc.cgemm(a, b, "FP32_REF")
+    assert np.array_equal(bits(c.cpu().numpy().view(np.float32)), bits(cr.view(np.float32)))
+    c64, _ = handle.cgemm(ad, bd, "FP64_ORACLE")
+    assert np.array_equal(bits(c64.cpu().numpy().view(np.float32)),
+                          bits(orc.cgemm(a, b, "FP64_ORACLE")[0].view(np.float32)))
+    ref = orc.cgemm_oracle(a, b)
+    err_ref = relerr(cr, ref)
+    for mode in ("FP16TCEC", "TF32TCEC"):
+        cm, _ = handle.cgemm(ad, bd, mode)
+        assert relerr(cm.cpu().numpy(), ref) <= max(TOL_FACTOR * err_ref, 3e-7), mode
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 300000), (3, 2, 50000), (1, 5, 4097), (64, 64, 2048),
+                                   (7, 1, 1025)])
+def test_long_k_kernels_bit_exact(handle, orc, dev, shape):
+    """Few outputs, long k (the dot products of deep circuits): the warp-per-
+    output kernels keep the reference's sequential chain order -> bit-exact."""
+    m, n, k = shape
+    a = matrix_recipe("uniform", m, k, 8)
+    b = matrix_recipe("uniform", k, n, 9)
+    ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    for mode in ("FP32_REF", "FP64_ORACLE"):
+        c, _ = handle.cgemm(ad, bd, mode)
+        cr, _ = orc.cgemm(a, b, mode)
+        assert np.array_equal(bits(c.cpu().numpy().view(np.float32)), bits(cr.view(np.float32))), mode

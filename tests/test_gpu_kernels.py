@@ -126,3 +126,15 @@ def test_permute_errors(handle, dev):
         handle.permute(t, [0, 1])
     with pytest.raises(InvalidPermutation):
         handle.permute(t, [0, 1, 1])
+
+
+@pytest.mark.parametrize("dims", [(2,) * 14, (2,) * 20, (4, 8, 16, 32), (128, 3, 256), (96, 64),
+                                  (2, 64, 2, 64), (33, 70, 5)])
+def test_permute_tiled_and_gather_paths(handle, dev, dims):
+    """Random permutations of shapes that exercise the shared-memory tiled plan
+    (high-rank dim-2, axes split at 32) and the gather fallback; bit-exact."""
+    g = np.random.default_rng(len(dims) * 7 + dims[0])
+    t = torch.randn(*dims, dtype=torch.complex64, device=dev)
+    for _ in range(4):
+        axis = [int(v) for v in g.permutation(len(dims))]
+        assert torch.equal(handle.permute(t, axis), t.permute(*axis).contiguous()), axis
