@@ -565,6 +565,81 @@ __global__ void __launch_bounds__(256) cgemm_longk_kernel(const float2* __restri
     }
 }
 
+// Very long k (>= 64K): one block per output element, the four chains
+// P1..P4 on four warps (four SMSPs: one FMUL + one FADD per k each), operands
+// staged through a cp.async double buffer by all 128 threads.  Same sequential
+// order per chain as the reference -> bit-identical.
+constexpr int kChainChunk = 1024;
+
+TCEC_DEV void cp_async8(void* smem, const void* gmem, bool valid) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    const int bytes = valid ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(bytes)
+                 : "memory");
+}
+
+template <bool F64>
+__global__ void __launch_bounds__(128) cgemm_chain_kernel(const float2* __restrict__ a,
+                                                          const float2* __restrict__ b,
+                                                          float2* __restrict__ c, int64_t m,
+                                                          int64_t n, int64_t k) {
+    __shared__ float2 sa[2][kChainChunk], sb[2][kChainChunk];
+    __shared__ double res[4];
+    const int64_t o = blockIdx.x;
+    const int64_t i = o / n, j = o - (o / n) * n;
+    const float2* arow = a + i * k;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    auto stage = [&](int buf, int64_t k0) {
+        for (int t = threadIdx.x; t < kChainChunk; t += blockDim.x) {
+            const int64_t kk = k0 + t;
+            const bool v = kk < k;
+            cp_async8(&sa[buf][t], arow + (v ? kk : 0), v);
+            cp_async8(&sb[buf][t], b + (v ? kk : 0) * n + j, v);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    using acc_t = typename std::conditional<F64, double, float>::type;
+    acc_t p = 0;
+    stage(0, 0);
+    int buf = 0;
+    for (int64_t k0 = 0; k0 < k; k0 += kChainChunk) {
+        if (k0 + kChainChunk < k) {
+            stage(buf ^ 1, k0 + kChainChunk);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        if (lane == 0) {
+            const int cnt = (k - k0) < kChainChunk ? int(k - k0) : kChainChunk;
+            const float2* A = sa[buf];
+            const float2* B = sb[buf];
+            // warp 0: Re*Re, 1: Im*Im, 2: Re*Im, 3: Im*Re (cgemm.cpp:33-36)
+#pragma unroll 8
+            for (int t = 0; t < cnt; ++t) {
+                const float x = (warp == 0 || warp == 2) ? A[t].x : A[t].y;
+                const float y = (warp == 0 || warp == 3) ? B[t].x : B[t].y;
+                if (F64)
+                    p = __dadd_rn(double(p), __dmul_rn(double(x), double(y)));
+                else
+                    p = __fadd_rn(float(p), __fmul_rn(x, y));
+            }
+        }
+        __syncthreads();
+        buf ^= 1;
+    }
+    if (lane == 0) res[warp] = double(p);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (F64)
+            c[o] = make_float2(__fsub_rn(__double2float_rn(res[0]), __double2float_rn(res[1])),
+                               __fadd_rn(__double2float_rn(res[2]), __double2float_rn(res[3])));
+        else
+            c[o] = make_float2(__fsub_rn(float(res[0]), float(res[1])),
+                               __fadd_rn(float(res[2]), float(res[3])));
+    }
+}
+
 // --------------------------------------------------------------- permute
 
 struct PermDesc {
@@ -804,6 +879,10 @@ void launch_cgemm_fp32_ref(const float2* a, const float2* b, float2* c, int64_t 
                            int64_t k, cudaStream_t s) {
     if (m <= 0 || n <= 0) return;
     const int64_t tiles = ((n + SB_N - 1) / SB_N) * ((m + SB_M - 1) / SB_M);
+    if (k >= 65536 && m * n <= 4096) {
+        cgemm_chain_kernel<false><<<unsigned(m * n), 128, 0, s>>>(a, b, c, m, n, k);
+        return;
+    }
     if (k >= 1024 && m * n <= 65536 && tiles < 2 * 148) {
         const int64_t warps = m * n;
         cgemm_longk_kernel<false><<<unsigned((warps + 7) / 8), 256, 0, s>>>(a, b, c, m, n, k);
@@ -815,6 +894,10 @@ void launch_cgemm_fp32_ref(const float2* a, const float2* b, float2* c, int64_t 
 void launch_cgemm_fp64(const float2* a, const float2* b, float2* c, int64_t m, int64_t n,
                        int64_t k, cudaStream_t s) {
     if (m <= 0 || n <= 0) return;
+    if (k >= 65536 && m * n <= 4096) {
+        cgemm_chain_kernel<true><<<unsigned(m * n), 128, 0, s>>>(a, b, c, m, n, k);
+        return;
+    }
     if (k >= 256 && m * n <= 65536) {
         cgemm_longk_kernel<true><<<unsigned((m * n + 7) / 8), 256, 0, s>>>(a, b, c, m, n, k);
         return;

@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
                 const int chunk = kb / F;
                 const int buf = chunk % kMainBufs;
                 const bool chunk_start = (kb % F) == 0;
-                if (chunk_start) {
+                if (chunk_start && !(diag & 2)) {
                     mbar_wait(&tail->tempty[buf], ((chunk / kMainBufs) & 1) ^ 1);
                     tc_fence_after();
                 }

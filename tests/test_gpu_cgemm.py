@@ -216,7 +216,7 @@ def test_extreme_aspect_shapes(handle, orc, dev, shape):
         assert relerr(cm.cpu().numpy(), ref) <= max(TOL_FACTOR * err_ref, 3e-7), mode
 
 
-@pytest.mark.parametrize("shape", [(1, 1, 300000), (3, 2, 50000), (1, 5, 4097), (64, 64, 2048),
+@pytest.mark.parametrize("shape", [(1, 1, 300000), (2, 1, 70000), (3, 2, 50000), (1, 5, 4097), (64, 64, 2048),
                                    (7, 1, 1025)])
 def test_long_k_kernels_bit_exact(handle, orc, dev, shape):
     """Few outputs, long k (the dot products of deep circuits): the warp-per-
