@@ -68,8 +68,10 @@ int tcec_get_flush_kblocks(tcec_handle h);
 int tcec_set_gemm_variant(tcec_handle h, int variant);
 /* network executor: 0 = auto (fused small-step kernel -- one warp per network,
  * intermediates in shared memory -- whenever every step is on a SIMT tier and
- * the live intermediates fit; else per-step permute + dispatch through a
- * captured CUDA graph), 1 = per-step only, 2 = fused only (error if ineligible) */
+ * the live intermediates fit; else the per-step fold -- permute + dispatch
+ * through a captured CUDA graph -- preceded by one launch that contracts every
+ * subtree of tiny SIMT steps, one warp per subtree), 1 = per-step only,
+ * 2 = fused only (error if ineligible), 3 = per-step + subtree launch */
 int tcec_set_executor(tcec_handle h, int policy);
 /* stage tracing (the device counterpart of DecisionRecord::wall_ms,
  * precsel.hpp:92-101): when enabled, every synchronous tcec_dispatch_cgemm

@@ -99,7 +99,8 @@ class Handle:
         check(self.lib.tcec_set_flush_kblocks(self.h, int(v)))
 
     def set_executor(self, policy: int) -> None:
-        """0 auto, 1 per-step permute+dispatch graph only, 2 fused small-step only."""
+        """0 auto, 1 per-step permute+dispatch graph only, 2 fused small-step only,
+        3 per-step graph preceded by the fused subtree launch (hybrid)."""
         check(self.lib.tcec_set_executor(self.h, int(policy)))
 
     def set_gemm_variant(self, pair: bool) -> None:

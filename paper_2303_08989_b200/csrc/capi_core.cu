@@ -203,8 +203,6 @@ int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t
     g.d = d;
     g.kind_fixed = p.kind;
     g.corrected = p.corrected;
-    // diagnostic only (tools/gpu_variants.py): same MMAs, hi tiles loaded for lo
-    if (p.corrected && std::getenv("TCEC_DIAG_HALF_BYTES")) g.corrected = 2;
     g.flush_kblocks = p.corrected ? h.flush_kblocks : 0;
     g.pair = h.gemm_pair;
     const bool want16 = p.kind < 0 || p.kind == kKindFp16 || p.kind == kKindFp16Scaled;
@@ -393,7 +391,7 @@ int tcec_get_flush_kblocks(tcec_handle h) { return h ? h->flush_kblocks : -1; }
 
 int tcec_set_executor(tcec_handle h, int policy) {
     CHECK_HANDLE(h);
-    if (policy < 0 || policy > 2) return set_error(TCEC_ERR_INVALID_ARGUMENT, "executor must be 0, 1 or 2");
+    if (policy < 0 || policy > 3) return set_error(TCEC_ERR_INVALID_ARGUMENT, "executor must be 0..3");
     h->executor = policy;
     return TCEC_OK;
 }

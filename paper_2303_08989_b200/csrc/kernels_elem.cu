@@ -566,69 +566,108 @@ __global__ void __launch_bounds__(256) cgemm_longk_kernel(const float2* __restri
 }
 
 // Very long k (>= 64K): one block per output element, the four chains
-// P1..P4 on four warps (four SMSPs: one FMUL + one FADD per k each), operands
-// staged through a cp.async double buffer by all 128 threads.  Same sequential
-// order per chain as the reference -> bit-identical.
+// P1..P4 (cgemm.cpp:33-36) each a single serial RN chain in ascending k, so the
+// FADD latency (4 cycles) x k is the floor.  Warps 4..7 are producers: they load
+// a chunk of A and B coalesced and write the four product streams
+// RN(x*y) to shared memory (products are independent of the chain order);
+// lane 0 of warps 0..3 (one per SMSP) runs its chain over the previous chunk's
+// products with 16-byte shared loads.  Same per-chain order as the reference ->
+// bit-identical.
 constexpr int kChainChunk = 1024;
-
-TCEC_DEV void cp_async8(void* smem, const void* gmem, bool valid) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    const int bytes = valid ? 8 : 0;
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(bytes)
-                 : "memory");
-}
+constexpr int kChainThreads = 256;
 
 template <bool F64>
-__global__ void __launch_bounds__(128) cgemm_chain_kernel(const float2* __restrict__ a,
-                                                          const float2* __restrict__ b,
-                                                          float2* __restrict__ c, int64_t m,
-                                                          int64_t n, int64_t k) {
-    __shared__ float2 sa[2][kChainChunk], sb[2][kChainChunk];
+__global__ void __launch_bounds__(kChainThreads) cgemm_chain_kernel(const float2* __restrict__ a,
+                                                                   const float2* __restrict__ b,
+                                                                   float2* __restrict__ c, int64_t m,
+                                                                   int64_t n, int64_t k) {
+    using acc_t = typename std::conditional<F64, double, float>::type;
+    constexpr int CH = F64 ? kChainChunk / 2 : kChainChunk;
+    extern __shared__ __align__(16) uint8_t chain_smem[];
+    acc_t* prod = reinterpret_cast<acc_t*>(chain_smem);  // [2][4][CH]
     __shared__ double res[4];
     const int64_t o = blockIdx.x;
     const int64_t i = o / n, j = o - (o / n) * n;
     const float2* arow = a + i * k;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    auto stage = [&](int buf, int64_t k0) {
-        for (int t = threadIdx.x; t < kChainChunk; t += blockDim.x) {
+    const int64_t nch = (k + CH - 1) / CH;
+    auto produce = [&](int buf, int64_t k0) {
+        acc_t* P = prod + size_t(buf) * 4 * CH;
+        for (int t = int(threadIdx.x) - 128; t < CH; t += 128) {
             const int64_t kk = k0 + t;
-            const bool v = kk < k;
-            cp_async8(&sa[buf][t], arow + (v ? kk : 0), v);
-            cp_async8(&sb[buf][t], b + (v ? kk : 0) * n + j, v);
+            float2 x = make_float2(0.f, 0.f), y = make_float2(0.f, 0.f);
+            if (kk < k) {
+                x = arow[kk];
+                y = b[kk * n + j];
+            }
+            if (F64) {
+                P[0 * CH + t] = acc_t(__dmul_rn(double(x.x), double(y.x)));
+                P[1 * CH + t] = acc_t(__dmul_rn(double(x.y), double(y.y)));
+                P[2 * CH + t] = acc_t(__dmul_rn(double(x.x), double(y.y)));
+                P[3 * CH + t] = acc_t(__dmul_rn(double(x.y), double(y.x)));
+            } else {
+                P[0 * CH + t] = acc_t(__fmul_rn(x.x, y.x));
+                P[1 * CH + t] = acc_t(__fmul_rn(x.y, y.y));
+                P[2 * CH + t] = acc_t(__fmul_rn(x.x, y.y));
+                P[3 * CH + t] = acc_t(__fmul_rn(x.y, y.x));
+            }
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    using acc_t = typename std::conditional<F64, double, float>::type;
     acc_t p = 0;
-    stage(0, 0);
-    int buf = 0;
-    for (int64_t k0 = 0; k0 < k; k0 += kChainChunk) {
-        if (k0 + kChainChunk < k) {
-            stage(buf ^ 1, k0 + kChainChunk);
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-        } else {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-        }
-        __syncthreads();
-        if (lane == 0) {
-            const int cnt = (k - k0) < kChainChunk ? int(k - k0) : kChainChunk;
-            const float2* A = sa[buf];
-            const float2* B = sb[buf];
-            // warp 0: Re*Re, 1: Im*Im, 2: Re*Im, 3: Im*Re (cgemm.cpp:33-36)
+    if (warp >= 4) produce(0, 0);
+    __syncthreads();
+    for (int64_t ch = 0; ch < nch; ++ch) {
+        const int buf = int(ch & 1);
+        if (warp >= 4) {
+            if (ch + 1 < nch) produce(buf ^ 1, (ch + 1) * CH);
+        } else if (lane == 0) {
+            const int64_t k0 = ch * CH;
+            const int cnt = (k - k0) < CH ? int(k - k0) : CH;
+            const acc_t* P = prod + (size_t(buf) * 4 + warp) * CH;
+            if (cnt == CH) {
+                if (F64) {
+                    const double2* q = reinterpret_cast<const double2*>(P);
 #pragma unroll 8
-            for (int t = 0; t < cnt; ++t) {
-                const float x = (warp == 0 || warp == 2) ? A[t].x : A[t].y;
-                const float y = (warp == 0 || warp == 3) ? B[t].x : B[t].y;
-                if (F64)
-                    p = __dadd_rn(double(p), __dmul_rn(double(x), double(y)));
-                else
-                    p = __fadd_rn(float(p), __fmul_rn(x, y));
+                    for (int t = 0; t < CH / 2; ++t) {
+                        const double2 v = q[t];
+                        p = acc_t(__dadd_rn(double(p), v.x));
+                        p = acc_t(__dadd_rn(double(p), v.y));
+                    }
+                } else {
+                    // software-pipelined: the next 32 products load while the
+                    // current 32 are chained
+                    const float4* q = reinterpret_cast<const float4*>(P);
+                    float4 cur[8], nxt[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) cur[u] = q[u];
+                    for (int g = 0; g < CH / 32; ++g) {
+                        if (g + 1 < CH / 32) {
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) nxt[u] = q[8 * (g + 1) + u];
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            p = acc_t(__fadd_rn(float(p), cur[u].x));
+                            p = acc_t(__fadd_rn(float(p), cur[u].y));
+                            p = acc_t(__fadd_rn(float(p), cur[u].z));
+                            p = acc_t(__fadd_rn(float(p), cur[u].w));
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) cur[u] = nxt[u];
+                    }
+                }
+            } else {
+                for (int t = 0; t < cnt; ++t) {
+                    if (F64)
+                        p = acc_t(__dadd_rn(double(p), double(P[t])));
+                    else
+                        p = acc_t(__fadd_rn(float(p), float(P[t])));
+                }
             }
         }
         __syncthreads();
-        buf ^= 1;
     }
-    if (lane == 0) res[warp] = double(p);
+    if (warp < 4 && lane == 0) res[warp] = double(p);
     __syncthreads();
     if (threadIdx.x == 0) {
         if (F64)
@@ -638,6 +677,15 @@ __global__ void __launch_bounds__(128) cgemm_chain_kernel(const float2* __restri
             c[o] = make_float2(__fsub_rn(float(res[0]), float(res[1])),
                                __fadd_rn(float(res[2]), float(res[3])));
     }
+}
+
+template <bool F64>
+void launch_chain(const float2* a, const float2* b, float2* c, int64_t m, int64_t n, int64_t k,
+                  cudaStream_t s) {
+    // two buffers x four chains x CH products: 32 KB for both F32 (CH floats)
+    // and F64 (CH/2 doubles)
+    const size_t smem = size_t(2) * 4 * kChainChunk * sizeof(float);
+    cgemm_chain_kernel<F64><<<unsigned(m * n), kChainThreads, smem, s>>>(a, b, c, m, n, k);
 }
 
 // --------------------------------------------------------------- permute
@@ -880,7 +928,7 @@ void launch_cgemm_fp32_ref(const float2* a, const float2* b, float2* c, int64_t 
     if (m <= 0 || n <= 0) return;
     const int64_t tiles = ((n + SB_N - 1) / SB_N) * ((m + SB_M - 1) / SB_M);
     if (k >= 65536 && m * n <= 4096) {
-        cgemm_chain_kernel<false><<<unsigned(m * n), 128, 0, s>>>(a, b, c, m, n, k);
+        launch_chain<false>(a, b, c, m, n, k, s);
         return;
     }
     if (k >= 1024 && m * n <= 65536 && tiles < 2 * 148) {
@@ -895,7 +943,7 @@ void launch_cgemm_fp64(const float2* a, const float2* b, float2* c, int64_t m, i
                        int64_t k, cudaStream_t s) {
     if (m <= 0 || n <= 0) return;
     if (k >= 65536 && m * n <= 4096) {
-        cgemm_chain_kernel<true><<<unsigned(m * n), 128, 0, s>>>(a, b, c, m, n, k);
+        launch_chain<true>(a, b, c, m, n, k, s);
         return;
     }
     if (k >= 256 && m * n <= 65536) {

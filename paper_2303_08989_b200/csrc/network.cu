@@ -39,8 +39,10 @@ struct tcec_network_s {
     void* result_dev = nullptr;      // stable home of the final tensor
     int64_t result_size = 0;
     tcec::SmallProgram small;        // fused small-step program (small_fold.cu)
+    tcec::HybridProgram hyb;         // subtree prologue of the per-step fold
     ~tcec_network_s() {
         small.release();
+        hyb.release();
         if (graph) cudaGraphExecDestroy(graph);
         if (node_dev) cudaFree(node_dev);
         if (result_dev) cudaFree(result_dev);
@@ -182,15 +184,33 @@ static int upload(tcec_network_s& net) {
 // allocations freed as soon as they are consumed; the final tensor is copied
 // into net.result_dev.
 static int enqueue_fold(tcec_network_s& net, const FoldPlan& plan, const tcec_dispatch_config_t& cfg,
-                        DevDecision* dec, void* ws) {
+                        DevDecision* dec, void* ws, const HybridProgram* hyb) {
     Handle& h = *net.h;
     cudaStream_t s = h.stream;
     std::map<int, std::pair<float2*, bool>> live;  // id -> (buffer, owned)
     float2* base = static_cast<float2*>(net.node_dev);
     for (size_t i = 0; i < net.nodes.size(); ++i) live[int(i)] = {base + net.offset[i], false};
     int next_id = int(net.nodes.size());
+    // hybrid prologue: every subtree of tiny SIMT steps in one launch
+    float2* tree_out = nullptr;
+    if (hyb && hyb->ok) {
+        const cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&tree_out),
+                                              size_t(std::max<int64_t>(hyb->out_elems, 1)) * 8, s);
+        if (e != cudaSuccess) return cuda_error(e, "subtree outputs");
+        const int rc = launch_hybrid_trees(*hyb, base, tree_out, s);
+        if (rc) return rc;
+    } else {
+        hyb = nullptr;
+    }
     for (size_t si = 0; si < plan.steps.size(); ++si) {
         const StepPlan& sp = plan.steps[si];
+        if (hyb && hyb->fused[si]) {
+            live.erase(sp.ia);
+            live.erase(sp.ib);
+            if (hyb->root_out[si] >= 0) live[next_id] = {tree_out + hyb->root_out[si], false};
+            ++next_id;
+            continue;
+        }
         auto [pa_src, own_a] = live[sp.ia];
         auto [pb_src, own_b] = live[sp.ib];
         float2* pa = pa_src;
@@ -229,6 +249,7 @@ static int enqueue_fold(tcec_network_s& net, const FoldPlan& plan, const tcec_di
         cudaMemcpyAsync(net.result_dev, res, size_t(size) * 8, cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) return cuda_error(e, "result copy");
     if (own) cudaFreeAsync(res, s);
+    if (tree_out) cudaFreeAsync(tree_out, s);
     return TCEC_OK;
 }
 
@@ -278,8 +299,27 @@ static int run_fold(tcec_network_s& net, const int* steps, int n_steps,
                     const tcec_dispatch_config_t& cfg, const FoldPlan& plan, DevDecision* dec,
                     void* ws, bool use_graph) {
     Handle& h = *net.h;
-    if (!use_graph) return enqueue_fold(net, plan, cfg, dec, ws);
-    const std::string key = plan_key(steps, n_steps, cfg, h, ws, dec);
+    // the subtree prologue (policy 0 auto / 3 hybrid), built and uploaded
+    // outside any capture
+    const HybridProgram* hyb = nullptr;
+    if (h.executor == 0 || h.executor == 3) {
+        std::string hkey(reinterpret_cast<const char*>(steps), size_t(n_steps) * 2 * sizeof(int));
+        hkey.append(reinterpret_cast<const char*>(&cfg), sizeof(cfg));
+        if (net.hyb.key != hkey) {
+            net.hyb.release();
+            build_hybrid_program(net.nodes, net.offset, plan, &net.hyb);
+            net.hyb.key = hkey;
+            const int rc = upload_hybrid_program(&net.hyb);
+            if (rc) {
+                net.hyb.key.clear();
+                return rc;
+            }
+        }
+        if (net.hyb.ok) hyb = &net.hyb;
+    }
+    if (!use_graph) return enqueue_fold(net, plan, cfg, dec, ws, hyb);
+    std::string key = plan_key(steps, n_steps, cfg, h, ws, dec);
+    key.append(reinterpret_cast<const char*>(&hyb), sizeof(hyb));
     if (!net.graph || key != net.graph_key) {
         if (net.graph) {
             cudaGraphExecDestroy(net.graph);
@@ -288,7 +328,7 @@ static int run_fold(tcec_network_s& net, const int* steps, int n_steps,
         cudaGraph_t g = nullptr;
         cudaError_t e = cudaStreamBeginCapture(h.stream, cudaStreamCaptureModeThreadLocal);
         if (e != cudaSuccess) return cuda_error(e, "graph capture");
-        const int rc = enqueue_fold(net, plan, cfg, dec, ws);
+        const int rc = enqueue_fold(net, plan, cfg, dec, ws, hyb);
         e = cudaStreamEndCapture(h.stream, &g);
         if (rc) {
             if (g) cudaGraphDestroy(g);
@@ -311,8 +351,10 @@ static const SmallProgram* small_program(tcec_network_s& net, const int* steps, 
                                          const tcec_dispatch_config_t& cfg, const FoldPlan& plan,
                                          const std::vector<int>& var_nodes, int* rc) {
     *rc = TCEC_OK;
-    const int policy = net.h->executor;  // 0 auto, 1 per-step only, 2 fused only
-    if (policy == 1) return nullptr;
+    // 0 auto (fused if eligible, else per-step + subtree prologue), 1 per-step
+    // only, 2 fused only, 3 per-step + subtree prologue
+    const int policy = net.h->executor;
+    if (policy == 1 || policy == 3) return nullptr;
     std::string key(reinterpret_cast<const char*>(steps), size_t(n_steps) * 2 * sizeof(int));
     key.append(reinterpret_cast<const char*>(&cfg), sizeof(cfg));
     key.append(reinterpret_cast<const char*>(var_nodes.data()), var_nodes.size() * sizeof(int));

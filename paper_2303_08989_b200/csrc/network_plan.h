@@ -69,6 +69,44 @@ struct SmallProgram {
     void release();
 };
 
+// ---------------------------------------------------------------- hybrid path
+// For networks the fused path cannot take whole (tensor-core steps, or
+// intermediates beyond shared memory), the per-step executor first runs every
+// maximal subtree of tiny SIMT steps (gate-absorption steps: a few to a few
+// hundred flops each) in ONE launch, one warp per subtree with its
+// intermediates in shared memory, writing each subtree's root tensor to a
+// device buffer; the per-step loop then skips those steps.  Same arithmetic
+// per step as the per-step SIMT kernels (reference FP32 chains / FP64), so the
+// result is bit-identical to the pure per-step fold.
+struct TreeDev {
+    int32_t step_begin, step_end;  // range in HybridProgram::steps
+    int32_t result_off;            // arena offset of the root tensor
+    int32_t pad_;
+    int64_t result_size;
+    int64_t out_off;               // element offset in the subtree-output buffer
+};
+
+struct HybridProgram {
+    bool ok = false;                 // at least one step is fused
+    std::vector<char> fused;         // per plan step: runs in the subtree launch
+    std::vector<int64_t> root_out;   // per plan step: output offset if a root, else -1
+    std::vector<SmallStepDev> steps;
+    std::vector<int32_t> tables;
+    std::vector<TreeDev> trees;
+    int64_t arena_elems = 0;         // max over trees
+    int64_t out_elems = 0;
+    SmallStepDev* d_steps = nullptr;
+    int32_t* d_tables = nullptr;
+    TreeDev* d_trees = nullptr;
+    std::string key;
+    void release();
+};
+
+void build_hybrid_program(const std::vector<NetNode>& nodes, const std::vector<int64_t>& node_offset,
+                          const FoldPlan& plan, HybridProgram* out);
+int upload_hybrid_program(HybridProgram* p);
+int launch_hybrid_trees(const HybridProgram& p, const float2* node_dev, float2* out, cudaStream_t s);
+
 // Build the fused program for `plan` with `var_nodes` held in the arena.
 void build_small_program(const std::vector<NetNode>& nodes, const std::vector<int64_t>& node_offset,
                          const FoldPlan& plan, const std::vector<int>& var_nodes,

@@ -190,7 +190,198 @@ int upload_small_program(SmallProgram* p) {
     return TCEC_OK;
 }
 
+// ------------------------------------------------------------ hybrid program
+void HybridProgram::release() {
+    if (d_steps) cudaFree(d_steps);
+    if (d_tables) cudaFree(d_tables);
+    if (d_trees) cudaFree(d_trees);
+    d_steps = nullptr;
+    d_tables = nullptr;
+    d_trees = nullptr;
+}
+
 namespace {
+constexpr int64_t kHybMaxOut = 1024;          // result elements of a fused step
+constexpr int64_t kHybMaxIn = 4096;           // elements of each operand
+constexpr int64_t kHybMaxMacs = int64_t(1) << 16;
+constexpr int64_t kHybArenaBytes = 16 * 1024;  // per warp (subtree)
+constexpr int kHybWarpsPerBlock = 4;
+}  // namespace
+
+void build_hybrid_program(const std::vector<NetNode>& nodes, const std::vector<int64_t>& node_offset,
+                          const FoldPlan& plan, HybridProgram* out) {
+    const int n_nodes = int(nodes.size());
+    const int S = int(plan.steps.size());
+    std::vector<int> consumer(size_t(S), -1);
+    for (int si = 0; si < S; ++si) {
+        const StepPlan& sp = plan.steps[size_t(si)];
+        if (sp.ia >= n_nodes) consumer[size_t(sp.ia - n_nodes)] = si;
+        if (sp.ib >= n_nodes) consumer[size_t(sp.ib - n_nodes)] = si;
+    }
+    std::vector<char> fusable(size_t(S), 0);
+    for (int si = 0; si < S; ++si) {
+        const StepPlan& sp = plan.steps[size_t(si)];
+        bool ok = (sp.dp.tier == kTierFp32 || sp.dp.tier == kTierFp64) && sp.m * sp.n <= kHybMaxOut &&
+                  sp.a_size <= kHybMaxIn && sp.b_size <= kHybMaxIn &&
+                  sp.m * sp.n * sp.k <= kHybMaxMacs;
+        ok = ok && (sp.ia < n_nodes || fusable[size_t(sp.ia - n_nodes)]);
+        ok = ok && (sp.ib < n_nodes || fusable[size_t(sp.ib - n_nodes)]);
+        fusable[size_t(si)] = ok;
+    }
+    HybridProgram p;
+    for (;;) {
+        p.steps.clear();
+        p.tables.clear();
+        p.trees.clear();
+        p.root_out.assign(size_t(S), -1);
+        p.arena_elems = 1;
+        p.out_elems = 0;
+        int unfuse = -1;
+        for (int root = 0; root < S && unfuse < 0; ++root) {
+            if (!fusable[size_t(root)]) continue;
+            const int c = consumer[size_t(root)];
+            if (c >= 0 && fusable[size_t(c)]) continue;  // not a subtree root
+            // the subtree: fusable producers reachable from the root
+            std::vector<int> members, stack{root};
+            while (!stack.empty()) {
+                const int s = stack.back();
+                stack.pop_back();
+                members.push_back(s);
+                for (int id : {plan.steps[size_t(s)].ia, plan.steps[size_t(s)].ib})
+                    if (id >= n_nodes) stack.push_back(id - n_nodes);
+            }
+            std::sort(members.begin(), members.end());
+            struct Loc {
+                int kind;
+                int64_t off, size;
+            };
+            std::map<int, Loc> live;
+            Arena arena;
+            TreeDev tr{};
+            tr.step_begin = int32_t(p.steps.size());
+            for (int s : members) {
+                const StepPlan& sp = plan.steps[size_t(s)];
+                auto loc = [&](int id) -> Loc {
+                    if (id < n_nodes) return {0, node_offset[size_t(id)], nodes[size_t(id)].size()};
+                    return live.at(id);
+                };
+                const Loc la = loc(sp.ia), lb = loc(sp.ib);
+                SmallStepDev st{};
+                st.m = int32_t(sp.m);
+                st.n = int32_t(sp.n);
+                st.k = int32_t(sp.k);
+                st.tier = sp.dp.tier == kTierFp64 ? 1 : 0;
+                st.a_kind = la.kind;
+                st.b_kind = lb.kind;
+                st.a_off = la.off;
+                st.b_off = lb.off;
+                st.ta = int32_t(p.tables.size());
+                gather_table(sp.a_dims, sp.a_axis, &p.tables);
+                st.tb = int32_t(p.tables.size());
+                gather_table(sp.b_dims, sp.b_axis, &p.tables);
+                const int64_t osz = std::max<int64_t>(sp.m * sp.n, 1);
+                const int64_t ooff = arena.alloc(osz);
+                st.out_off = int32_t(ooff);
+                if (la.kind == 1) arena.release(la.off, la.size);
+                if (lb.kind == 1) arena.release(lb.off, lb.size);
+                live.erase(sp.ia);
+                live.erase(sp.ib);
+                live[n_nodes + s] = {1, ooff, osz};
+                p.steps.push_back(st);
+            }
+            if (arena.top * 8 > kHybArenaBytes) {
+                unfuse = root;
+                break;
+            }
+            const Loc res = live.at(n_nodes + root);
+            tr.step_end = int32_t(p.steps.size());
+            tr.result_off = int32_t(res.off);
+            tr.result_size = res.size;
+            tr.out_off = p.out_elems;
+            p.root_out[size_t(root)] = p.out_elems;
+            p.out_elems += res.size;
+            p.arena_elems = std::max(p.arena_elems, arena.top);
+            p.trees.push_back(tr);
+        }
+        if (unfuse < 0) break;
+        fusable[size_t(unfuse)] = 0;  // its fused children become roots
+    }
+    p.fused = fusable;
+    p.ok = !p.trees.empty() && int64_t(p.tables.size()) <= kMaxTableEntries;
+    *out = std::move(p);
+}
+
+int upload_hybrid_program(HybridProgram* p) {
+    p->release();
+    if (!p->ok) return TCEC_OK;
+    cudaError_t e = cudaMalloc(&p->d_steps, std::max<size_t>(p->steps.size(), 1) * sizeof(SmallStepDev));
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_tables, std::max<size_t>(p->tables.size(), 1) * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_trees, std::max<size_t>(p->trees.size(), 1) * sizeof(TreeDev));
+    if (e != cudaSuccess) return cuda_error(e, "hybrid program upload");
+    cudaMemcpy(p->d_steps, p->steps.data(), p->steps.size() * sizeof(SmallStepDev), cudaMemcpyHostToDevice);
+    cudaMemcpy(p->d_tables, p->tables.data(), p->tables.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(p->d_trees, p->trees.data(), p->trees.size() * sizeof(TreeDev), cudaMemcpyHostToDevice);
+    return TCEC_OK;
+}
+
+namespace {
+
+// one contraction step by one warp: operands gathered through the step's
+// permutation tables, the reference FP32 schedule (or FP64) per output element
+__device__ __forceinline__ void warp_step(const SmallStepDev& st, float2* arena,
+                                          const float2* __restrict__ nodes,
+                                          const int32_t* __restrict__ tab, int lane) {
+    const float2* A = st.a_kind ? arena + st.a_off : nodes + st.a_off;
+    const float2* B = st.b_kind ? arena + st.b_off : nodes + st.b_off;
+    const int32_t* ta = tab + st.ta;
+    const int32_t* tb = tab + st.tb;
+    const int mn = st.m * st.n;
+    for (int o = lane; o < mn; o += 32) {
+        const int i = o / st.n, j = o - i * st.n;
+        float2 r;
+        if (st.tier == 0) {
+            float p1 = 0.0f, p2 = 0.0f, p3 = 0.0f, p4 = 0.0f;
+            for (int kk = 0; kk < st.k; ++kk) {
+                const float2 a = A[ta[i * st.k + kk]];
+                const float2 b = B[tb[kk * st.n + j]];
+                p1 = __fadd_rn(p1, __fmul_rn(a.x, b.x));
+                p2 = __fadd_rn(p2, __fmul_rn(a.y, b.y));
+                p3 = __fadd_rn(p3, __fmul_rn(a.x, b.y));
+                p4 = __fadd_rn(p4, __fmul_rn(a.y, b.x));
+            }
+            r = make_float2(__fsub_rn(p1, p2), __fadd_rn(p3, p4));
+        } else {
+            double p1 = 0.0, p2 = 0.0, p3 = 0.0, p4 = 0.0;
+            for (int kk = 0; kk < st.k; ++kk) {
+                const float2 a = A[ta[i * st.k + kk]];
+                const float2 b = B[tb[kk * st.n + j]];
+                p1 = __dadd_rn(p1, __dmul_rn(double(a.x), double(b.x)));
+                p2 = __dadd_rn(p2, __dmul_rn(double(a.y), double(b.y)));
+                p3 = __dadd_rn(p3, __dmul_rn(double(a.x), double(b.y)));
+                p4 = __dadd_rn(p4, __dmul_rn(double(a.y), double(b.x)));
+            }
+            r = make_float2(__fsub_rn(__double2float_rn(p1), __double2float_rn(p2)),
+                            __fadd_rn(__double2float_rn(p3), __double2float_rn(p4)));
+        }
+        arena[st.out_off + o] = r;
+    }
+    __syncwarp();
+}
+
+// hybrid prologue: one warp per subtree
+__global__ void tree_fold_kernel(const SmallStepDev* __restrict__ steps,
+                                 const int32_t* __restrict__ tab, const TreeDev* __restrict__ trees,
+                                 int n_trees, const float2* __restrict__ nodes, int64_t arena_elems,
+                                 float2* __restrict__ out) {
+    extern __shared__ float2 tree_arena[];
+    const int wic = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
+    const int t = int(blockIdx.x) * int(blockDim.x >> 5) + wic;
+    if (t >= n_trees) return;
+    float2* arena = tree_arena + size_t(wic) * size_t(arena_elems);
+    const TreeDev tr = trees[t];
+    for (int s = tr.step_begin; s < tr.step_end; ++s) warp_step(steps[s], arena, nodes, tab, lane);
+    for (int64_t e = lane; e < tr.result_size; e += 32) out[tr.out_off + e] = arena[tr.result_off + e];
+}
 
 __global__ void small_fold_kernel(const SmallStepDev* __restrict__ steps, int n_steps,
                                   const int32_t* __restrict__ tab, const float2* __restrict__ nodes,
@@ -221,48 +412,28 @@ __global__ void small_fold_kernel(const SmallStepDev* __restrict__ steps, int n_
         }
     }
     __syncwarp();
-    for (int s = 0; s < n_steps; ++s) {
-        const SmallStepDev st = steps[s];
-        const float2* A = st.a_kind ? arena + st.a_off : nodes + st.a_off;
-        const float2* B = st.b_kind ? arena + st.b_off : nodes + st.b_off;
-        const int32_t* ta = tab + st.ta;
-        const int32_t* tb = tab + st.tb;
-        const int mn = st.m * st.n;
-        for (int o = lane; o < mn; o += 32) {
-            const int i = o / st.n, j = o - i * st.n;
-            float2 r;
-            if (st.tier == 0) {
-                float p1 = 0.0f, p2 = 0.0f, p3 = 0.0f, p4 = 0.0f;
-                for (int kk = 0; kk < st.k; ++kk) {
-                    const float2 a = A[ta[i * st.k + kk]];
-                    const float2 b = B[tb[kk * st.n + j]];
-                    p1 = __fadd_rn(p1, __fmul_rn(a.x, b.x));
-                    p2 = __fadd_rn(p2, __fmul_rn(a.y, b.y));
-                    p3 = __fadd_rn(p3, __fmul_rn(a.x, b.y));
-                    p4 = __fadd_rn(p4, __fmul_rn(a.y, b.x));
-                }
-                r = make_float2(__fsub_rn(p1, p2), __fadd_rn(p3, p4));
-            } else {
-                double p1 = 0.0, p2 = 0.0, p3 = 0.0, p4 = 0.0;
-                for (int kk = 0; kk < st.k; ++kk) {
-                    const float2 a = A[ta[i * st.k + kk]];
-                    const float2 b = B[tb[kk * st.n + j]];
-                    p1 = __dadd_rn(p1, __dmul_rn(double(a.x), double(b.x)));
-                    p2 = __dadd_rn(p2, __dmul_rn(double(a.y), double(b.y)));
-                    p3 = __dadd_rn(p3, __dmul_rn(double(a.x), double(b.y)));
-                    p4 = __dadd_rn(p4, __dmul_rn(double(a.y), double(b.x)));
-                }
-                r = make_float2(__fsub_rn(__double2float_rn(p1), __double2float_rn(p2)),
-                                __fadd_rn(__double2float_rn(p3), __double2float_rn(p4)));
-            }
-            arena[st.out_off + o] = r;
-        }
-        __syncwarp();
-    }
+    for (int s = 0; s < n_steps; ++s) warp_step(steps[s], arena, nodes, tab, lane);
     for (int64_t e = lane; e < result_size; e += 32) out[run * result_size + e] = arena[result_off + e];
 }
 
 }  // namespace
+
+int launch_hybrid_trees(const HybridProgram& p, const float2* node_dev, float2* out, cudaStream_t s) {
+    if (!p.ok) return TCEC_OK;
+    const int n_trees = int(p.trees.size());
+    const size_t smem = size_t(kHybWarpsPerBlock) * size_t(p.arena_elems) * 8;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(tree_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(kHybWarpsPerBlock * kHybArenaBytes));
+        attr = true;
+    }
+    const unsigned grid = unsigned((n_trees + kHybWarpsPerBlock - 1) / kHybWarpsPerBlock);
+    tree_fold_kernel<<<grid, 32 * kHybWarpsPerBlock, smem, s>>>(p.d_steps, p.d_tables, p.d_trees, n_trees,
+                                                                node_dev, p.arena_elems, out);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? TCEC_OK : cuda_error(e, "tree_fold_kernel");
+}
 
 int launch_small_program(const SmallProgram& p, const float2* node_dev, int n_runs,
                          const float2* var_data, int64_t per_run, const uint8_t* bits, float2* out,

@@ -154,6 +154,18 @@ TCEC_DEV void tmem_dealloc(uint32_t taddr) {
                  : "memory");
 }
 
+// one lane of a converged warp (elect.sync); lets the whole warp run the MMA
+// issue loop so its operands stay in uniform registers
+TCEC_DEV bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n.reg .pred P;\n"
+        "elect.sync _|P, 0xffffffff;\n"
+        "selp.b32 %0, 1, 0, P;\n}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 // D[tmem] (+)= A[smem] * B[smem]; idesc selects kind/shape/majors
 TCEC_DEV void mma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                       uint32_t accumulate) {

@@ -13,15 +13,16 @@
 // main and corr accumulate in separate TMEM accumulators.  Following the
 // paper's rounding-mode care ("FP32 SIMT cores for addition with
 // RN ... to avoid the RZ rounding inside Tensor Cores"), the main term can be
-// flushed every `flush_kblocks` k-blocks: the MMA warp ping-pongs the main
-// accumulator between two TMEM buffers and the epilogue warps fold each
+// flushed every `flush_kblocks` k-blocks: the MMA warp rotates the main
+// accumulator over three TMEM buffers and the epilogue warps fold each
 // finished partial into a register accumulator with __fadd_rn while the tensor
 // core fills the other buffer.  The correction term stays in TMEM for the whole
 // K (its error is scaled by 2^-11).  The epilogue applies the FP16TCEC_SCALED
 // descale 2^-(sa+sb) (precsel.cpp:171-174) and stores C.
 //
-// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator +
-// single-thread MMA issuer, warps 2..5 = epilogue (TMEM lane quadrant warp%4).
+// Warp roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM allocator +
+// MMA issuer (the whole warp runs the loop, one elected lane issues), warps
+// 2..9 = epilogue (TMEM lane quadrant warp%4, two 64-column halves).
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
                      const __grid_constant__ CUtensorMap map_bhi,
                      const __grid_constant__ CUtensorMap map_blo, float* __restrict__ c,
                      int m, int n2, int kp, const DevDecision* __restrict__ dec, int kind_fixed,
-                     int corrected, int flush_kblocks, int diag) {
+                     int corrected, int flush_kblocks) {
     using T = Traits<FMT>;
     // device-side mode selection: the kernel of the unselected format exits
     // (the paper's "both kernels launched, one exits early")
@@ -112,7 +113,7 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
     const int nkb = kp / T::kBK;
     const int F = flush_kblocks > 0 ? flush_kblocks : (nkb > 0 ? nkb : 1);
     const int nchunks = (nkb + F - 1) / F;
-    const uint32_t stage_bytes = uint32_t(corrected == 1 ? 4 : 2) * kTileBytes;  // 2: diagnostic, hi tiles only
+    const uint32_t stage_bytes = uint32_t(corrected ? 4 : 2) * kTileBytes;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
                 const int kx = kb * T::kBK;
                 tma_load_2d(tile(s, 0), &map_ahi, &tail->full[s], kx, m0);
                 tma_load_2d(tile(s, 2), &map_bhi, &tail->full[s], kx, n0);
-                if (corrected == 1) {
+                if (corrected) {
                     tma_load_2d(tile(s, 1), &map_alo, &tail->full[s], kx, m0);
                     tma_load_2d(tile(s, 3), &map_blo, &tail->full[s], kx, n0);
                 }
@@ -158,24 +159,26 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
         }
     } else if (warp == 1) {
         // ------------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            for (int kb = 0; kb < nkb; ++kb) {
-                const int chunk = kb / F;
-                const int buf = chunk % kMainBufs;
-                const bool chunk_start = (kb % F) == 0;
-                if (chunk_start && !(diag & 2)) {
-                    mbar_wait(&tail->tempty[buf], ((chunk / kMainBufs) & 1) ^ 1);
-                    tc_fence_after();
-                }
-                const int s = kb % kStages;
-                mbar_wait(&tail->full[s], (kb / kStages) & 1);
+        // The whole warp runs the loop (waits and operand math stay
+        // warp-uniform, in uniform registers); one elected lane issues.
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int chunk = kb / F;
+            const int buf = chunk % kMainBufs;
+            const bool chunk_start = (kb % F) == 0;
+            if (chunk_start) {
+                mbar_wait(&tail->tempty[buf], ((chunk / kMainBufs) & 1) ^ 1);
                 tc_fence_after();
-                const uint64_t dah = umma_desc_k_sw128(tile(s, 0));
-                const uint64_t dal = corrected == 2 ? umma_desc_k_sw128(tile(s, 0)) : umma_desc_k_sw128(tile(s, 1));
-                const uint64_t dbh = umma_desc_k_sw128(tile(s, 2));
-                const uint64_t dbl = corrected == 2 ? umma_desc_k_sw128(tile(s, 2)) : umma_desc_k_sw128(tile(s, 3));
-                const uint32_t d_main = tmem + uint32_t(buf * BN);
-                const uint32_t d_corr = tmem + kColCorr;
+            }
+            const int s = kb % kStages;
+            mbar_wait(&tail->full[s], (kb / kStages) & 1);
+            tc_fence_after();
+            const uint64_t dah = umma_desc_k_sw128(tile(s, 0));
+            const uint64_t dal = umma_desc_k_sw128(tile(s, 1));
+            const uint64_t dbh = umma_desc_k_sw128(tile(s, 2));
+            const uint64_t dbl = umma_desc_k_sw128(tile(s, 3));
+            const uint32_t d_main = tmem + uint32_t(buf * BN);
+            const uint32_t d_corr = tmem + kColCorr;
+            if (elect_one()) {
 #pragma unroll
                 for (int ks = 0; ks < T::kKSteps; ++ks) {
                     const uint64_t adv = uint64_t((ks * T::kUK * T::kElem) >> 4);
@@ -198,8 +201,8 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
                 mma_commit(&tail->empty[s]);
                 if ((kb % F) == F - 1 || kb == nkb - 1) mma_commit(&tail->tfull[buf]);
             }
+            __syncwarp();
         }
-        __syncwarp();
     } else {
         // -------------------------------------------------------- epilogue
         // warp w owns TMEM lanes 32*(w%4).. (the hardware quadrant rule) and
@@ -209,26 +212,23 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
         const int rloc = 32 * q + lane;
         const uint32_t lane_base = tmem + (uint32_t(32 * q) << 16) + uint32_t(64 * half);
         constexpr int kCols = BN / 2;
+        // -0 is the identity of RN addition (-0 + x == x for every x, zeros
+        // included), so every partial folds in with one FADD
         float acc[kCols];
 #pragma unroll
-        for (int i = 0; i < kCols; ++i) acc[i] = 0.0f;
+        for (int i = 0; i < kCols; ++i) acc[i] = -0.0f;
         for (int ch = 0; ch < nchunks; ++ch) {
             const int buf = ch % kMainBufs;
             mbar_wait(&tail->tfull[buf], (ch / kMainBufs) & 1);
             tc_fence_after();
             float v[kCols];
-            if (diag & 1) {
-#pragma unroll
-                for (int i = 0; i < kCols; ++i) v[i] = 0.0f;
-            } else {
-                tmem_ld64(lane_base + uint32_t(buf * BN), v);
-            }
+            tmem_ld64(lane_base + uint32_t(buf * BN), v);
             // the partial is in registers: hand the TMEM buffer back first
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tail->tempty[buf]);
 #pragma unroll
-            for (int i = 0; i < kCols; ++i) acc[i] = ch == 0 ? v[i] : __fadd_rn(acc[i], v[i]);
+            for (int i = 0; i < kCols; ++i) acc[i] = __fadd_rn(acc[i], v[i]);
         }
         if (corrected && nkb > 0) {
 #pragma unroll
@@ -381,7 +381,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
         }
     } else if (warp == 1) {
         // ---------------------------------------- MMA issuer (pair leader only)
-        if (leader && lane == 0) {
+        if (leader) {
             for (int kb = 0; kb < nkb; ++kb) {
                 const int chunk = kb / F;
                 const int buf = chunk % kMainBufs;
@@ -399,30 +399,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
                 const uint64_t dbl = umma_desc_k_sw128(b_tile(s, 1));
                 const uint32_t d_main = tmem + uint32_t(buf * BN);
                 const uint32_t d_corr = tmem + kColCorr;
+                if (elect_one()) {
 #pragma unroll
-                for (int ks = 0; ks < T::kKSteps; ++ks) {
-                    const uint64_t adv = uint64_t((ks * T::kUK * T::kElem) >> 4);
-                    const uint32_t acc_main = (!chunk_start || ks > 0) ? 1u : 0u;
-                    const uint32_t acc_corr = (kb > 0 || ks > 0) ? 1u : 0u;
-                    if (FMT == kFp16) {
-                        mma2_f16(d_main, dah + adv, dbh + adv, kIdesc2, acc_main);
-                        if (corrected) {
-                            mma2_f16(d_corr, dal + adv, dbh + adv, kIdesc2, acc_corr);
-                            mma2_f16(d_corr, dah + adv, dbl + adv, kIdesc2, 1u);
-                        }
-                    } else {
-                        mma2_tf32(d_main, dah + adv, dbh + adv, kIdesc2, acc_main);
-                        if (corrected) {
-                            mma2_tf32(d_corr, dal + adv, dbh + adv, kIdesc2, acc_corr);
-                            mma2_tf32(d_corr, dah + adv, dbl + adv, kIdesc2, 1u);
+                    for (int ks = 0; ks < T::kKSteps; ++ks) {
+                        const uint64_t adv = uint64_t((ks * T::kUK * T::kElem) >> 4);
+                        const uint32_t acc_main = (!chunk_start || ks > 0) ? 1u : 0u;
+                        const uint32_t acc_corr = (kb > 0 || ks > 0) ? 1u : 0u;
+                        if (FMT == kFp16) {
+                            mma2_f16(d_main, dah + adv, dbh + adv, kIdesc2, acc_main);
+                            if (corrected) {
+                                mma2_f16(d_corr, dal + adv, dbh + adv, kIdesc2, acc_corr);
+                                mma2_f16(d_corr, dah + adv, dbl + adv, kIdesc2, 1u);
+                            }
+                        } else {
+                            mma2_tf32(d_main, dah + adv, dbh + adv, kIdesc2, acc_main);
+                            if (corrected) {
+                                mma2_tf32(d_corr, dal + adv, dbh + adv, kIdesc2, acc_corr);
+                                mma2_tf32(d_corr, dah + adv, dbl + adv, kIdesc2, 1u);
+                            }
                         }
                     }
+                    mma_commit_pair(&tail->empty[s], 0x3);
+                    if ((kb % F) == F - 1 || kb == nkb - 1) mma_commit_pair(&tail->tfull[buf], 0x3);
                 }
-                mma_commit_pair(&tail->empty[s], 0x3);
-                if ((kb % F) == F - 1 || kb == nkb - 1) mma_commit_pair(&tail->tfull[buf], 0x3);
+                __syncwarp();
             }
         }
-        __syncwarp();
     } else {
         // ------------------------------------------------ epilogue (both CTAs)
         const int q = warp & 3;
@@ -433,7 +435,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
         const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tail->tempty[0]), 0);
         float acc[kCols];
 #pragma unroll
-        for (int i = 0; i < kCols; ++i) acc[i] = 0.0f;
+        for (int i = 0; i < kCols; ++i) acc[i] = -0.0f;  // RN identity
         for (int ch = 0; ch < nchunks; ++ch) {
             const int buf = ch % kMainBufs;
             mbar_wait(&tail->tfull[buf], (ch / kMainBufs) & 1);
@@ -444,7 +446,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(tempty_leader0 + uint32_t(buf * sizeof(uint64_t)));
 #pragma unroll
-            for (int i = 0; i < kCols; ++i) acc[i] = ch == 0 ? v[i] : __fadd_rn(acc[i], v[i]);
+            for (int i = 0; i < kCols; ++i) acc[i] = __fadd_rn(acc[i], v[i]);
         }
         if (corrected && nkb > 0) {
 #pragma unroll
@@ -522,16 +524,6 @@ bool make_map(CUtensorMap* map, const void* base, int fmt, int64_t rows, int64_t
     return r == CUDA_SUCCESS;
 }
 
-// diagnostic bitmask for performance experiments (TCEC_DIAG_MASK; never set in
-// production): bit 0 = epilogue skips the per-chunk TMEM read
-int g_diag_mask() {
-    static const int mask = [] {
-        const char* e = std::getenv("TCEC_DIAG_MASK");
-        return e ? std::atoi(e) : 0;
-    }();
-    return mask;
-}
-
 template <int FMT>
 int launch_fmt(const TcecGemmArgs& g, cudaStream_t s) {
     static bool attr_set = false;
@@ -562,7 +554,7 @@ int launch_fmt(const TcecGemmArgs& g, cudaStream_t s) {
         const int64_t tiles = ((g.m + BM - 1) / BM) * ((g.n2 + BN - 1) / BN);
         tcec_gemm_kernel<FMT><<<unsigned(tiles), kThreadsGemm, kSmemBytes, s>>>(
             mah, mal, mbh, mbl, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed,
-            g.corrected, g.flush_kblocks, g_diag_mask());
+            g.corrected, g.flush_kblocks);
     }
     return int(cudaGetLastError());
 }

@@ -84,7 +84,7 @@ def test_path_errors(handle):
         net.contract([(0, 1), (0, 2)], BASELINE)  # dead node
 
 
-@pytest.fixture(params=[1, 2], ids=["per-step", "fused"])
+@pytest.fixture(params=[1, 2, 3], ids=["per-step", "fused", "hybrid"])
 def executor(request, handle):
     handle.set_executor(request.param)
     yield request.param
@@ -192,9 +192,36 @@ def test_sliced_amplitude_on_device(handle):
     _, _, z = contract_network_f64(spec, path)
     plan = SlicePlan.build(spec, path, find_slices(spec, path, n_labels=4))
     net = Network(handle, plan.base)
-    for policy in (1, 2):
+    for policy in (1, 2, 3):
         handle.set_executor(policy)
         amp, full = sliced_amplitude(device_evaluator(net, plan, BASELINE), plan)
         assert abs(amp - complex(z[0])) <= 1e-5 * abs(complex(z[0]))
     handle.set_executor(0)
     net.close()
+
+
+@pytest.mark.parametrize("seed", [3, 8])
+def test_hybrid_subtree_launch_matches_per_step_with_tensor_core_steps(handle, seed):
+    """Lowered size thresholds put the larger steps of a 5x5 network on the
+    tensor-core tiers, so the whole-network fused path is ineligible and the
+    auto / hybrid executors run the tiny SIMT subtrees in one launch before the
+    per-step graph: results must be bit-identical to the pure per-step fold
+    (single contraction, selector batch replays and node batches)."""
+    c = rqc_rectangular(5, 5, 12, seed)
+    xs = [[(v * 2654435761 >> q) & 1 for q in range(25)] for v in range(6)]
+    net = Network(handle, circuit_to_network(c, xs[0]))
+    path = net.greedy_path()
+    cfg = make_config(SelectionPolicy(size_auto=16, size_tf32=4))
+    out = {}
+    for policy in (1, 3, 0):
+        handle.set_executor(policy)
+        single, log = net.contract(path, cfg, want_log=True)
+        batch = net.selector_batch(path, xs, cfg)
+        out[policy] = (single.data.view(np.uint32).copy(), batch.view(np.uint32).copy(), log)
+    handle.set_executor(0)
+    net.close()
+    assert any("TF32" in line or "FP16" in line for line in out[1][2]), "no tensor-core step"
+    for policy in (3, 0):
+        assert np.array_equal(out[policy][0], out[1][0]), policy
+        assert np.array_equal(out[policy][1], out[1][1]), policy
+        assert out[policy][2] == out[1][2]

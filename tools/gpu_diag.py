@@ -21,5 +21,5 @@ for nn in (4096,):
             st, cnt = h.profile_read(); h.profile(False)
             g = st["gemm"] / cnt
             nprod = 1 if mode.endswith("TC") else 3
-            print(f"diag={os.environ.get('TCEC_DIAG_HALF_BYTES','0')} n={nn} flush={fl} {mode}: gemm {g:.2f} ms "
+            print(f"n={nn} flush={fl} {mode}: gemm {g:.2f} ms "
                   f"{8*nn**3/(g*1e-3)/1e12:.1f} TF useful, {nprod*8*nn**3/(g*1e-3)/1e12:.0f} TF tensor", flush=True)
