@@ -63,8 +63,9 @@ int tcec_synchronize(tcec_handle h);
  * device counterpart of TilingConfig::k_tile (gemm.hpp:28-30). */
 int tcec_set_flush_kblocks(tcec_handle h, int kblocks);
 int tcec_get_flush_kblocks(tcec_handle h);
-/* tensor-core kernel variant: 0 = single CTA (128 x 128 tiles, default: measured
- * faster with the per-k-block RN flush), 1 = CTA pair (cta_group::2, 256 x 128) */
+/* tensor-core kernel variant: 0 = auto (default: wide when its tiles fill the
+ * SMs, else single), 1 = CTA pair (cta_group::2, 256 x 128 tile), 2 = single
+ * CTA (128 x 128 tile), 3 = wide CTA pair (cta_group::2, 256 x 256 tile) */
 int tcec_set_gemm_variant(tcec_handle h, int variant);
 /* network executor: 0 = auto (fused small-step kernel -- one warp per network,
  * intermediates in shared memory -- whenever every step is on a SIMT tier and

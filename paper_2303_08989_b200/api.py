@@ -103,9 +103,13 @@ class Handle:
         3 per-step graph preceded by the fused subtree launch (hybrid)."""
         check(self.lib.tcec_set_executor(self.h, int(policy)))
 
-    def set_gemm_variant(self, pair: bool) -> None:
-        """1 = CTA-pair (cta_group::2) TCEC kernel, 0 = single-CTA kernel."""
-        check(self.lib.tcec_set_gemm_variant(self.h, int(pair)))
+    GEMM_VARIANTS = {"auto": 0, "pair": 1, "single": 2, "wide": 3}
+
+    def set_gemm_variant(self, variant) -> None:
+        """tcgen05 kernel variant: "auto" (default), "pair" (cta_group::2,
+        256x128 tile), "single" (128x128 tile), "wide" (cta_group::2, 256x256)."""
+        v = self.GEMM_VARIANTS[variant] if isinstance(variant, str) else int(variant)
+        check(self.lib.tcec_set_gemm_variant(self.h, v))
 
     def profile(self, on: bool = True) -> None:
         """Enable (and reset) per-stage CUDA-event tracing of dispatches."""

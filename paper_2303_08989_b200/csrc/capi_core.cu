@@ -204,7 +204,7 @@ int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t
     g.kind_fixed = p.kind;
     g.corrected = p.corrected;
     g.flush_kblocks = p.corrected ? h.flush_kblocks : 0;
-    g.pair = h.gemm_pair;
+    g.pair = resolve_gemm_variant(h.gemm_pair, m, 2 * n, h.sm_count);
     const bool want16 = p.kind < 0 || p.kind == kKindFp16 || p.kind == kKindFp16Scaled;
     const bool want32 = (p.kind < 0 && !p.forced_scaled) || p.kind == kKindTf32;
     if (want16) {
@@ -398,7 +398,7 @@ int tcec_set_executor(tcec_handle h, int policy) {
 
 int tcec_set_gemm_variant(tcec_handle h, int variant) {
     CHECK_HANDLE(h);
-    if (variant < 0 || variant > 1) return set_error(TCEC_ERR_INVALID_ARGUMENT, "variant must be 0 or 1");
+    if (variant < 0 || variant > 3) return set_error(TCEC_ERR_INVALID_ARGUMENT, "variant must be 0..3");
     h->gemm_pair = variant;
     return TCEC_OK;
 }

@@ -493,6 +493,270 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
     }
 }
 
+// ===================================================================== wide pair
+// cta_group::2 kernel with a 256 x 256 tile of C' per CTA pair (128 x 256 per
+// CTA).  Per k-block each CTA stages A_hi/A_lo (its 128 rows) and B_hi/B_lo
+// (its 128 of the pair's 256 columns): 64 KB for 3 x 128x256x64 MACs, i.e.
+// half the operand bytes per MAC of the 128 x 128 kernel, so neither the
+// L2->SM feed nor shared-memory bandwidth paces the tensor pipe.
+//
+// TMEM (512 columns per CTA): main partial as two 128-column halves (cols
+// 0..127 and 128..255), correction accumulator cols 256..511.  The main term
+// is issued per half (N = 128 MMAs) and committed per half, so the epilogue
+// drains half h while the tensor core runs the other half and the correction
+// products (5/6 of a k-block of slack); the correction MMAs run at N = 256.
+// Column maps (CTA r of the pair holds B rows n0 + 128 r + [0,128)):
+//   main half h, TMEM col j:  j < 64 -> n0 + 64h + j,  j >= 64 -> n0 + 128 + 64h + (j-64)
+//   corr, TMEM col 256 + j:   n0 + j
+constexpr int kWideStages = 3;
+constexpr int kWideBN = 256;
+constexpr int kWideStageBytes = 4 * kTileBytes;  // A_hi | A_lo | B_hi | B_lo, 16 KB each
+constexpr int kWideCStride = kWideBN + 4;
+struct alignas(8) WideSmemTail {
+    uint64_t full[kWideStages];
+    uint64_t empty[kWideStages];
+    uint64_t tfull[2];
+    uint64_t tempty[2];
+    uint64_t cfull;
+    uint32_t tmem_base;
+};
+constexpr size_t kWideSmemBytes = 1024 + size_t(kWideStages) * kWideStageBytes + sizeof(WideSmemTail);
+static_assert(size_t(BM) * kWideCStride * 4 <= size_t(kWideStages) * kWideStageBytes,
+              "C staging tile must fit in the operand stages");
+
+template <int FMT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
+    tcec_gemm_wide_kernel(const __grid_constant__ CUtensorMap map_ahi,
+                          const __grid_constant__ CUtensorMap map_alo,
+                          const __grid_constant__ CUtensorMap map_bhi,
+                          const __grid_constant__ CUtensorMap map_blo, float* __restrict__ c,
+                          int m, int n2, int kp, const DevDecision* __restrict__ dec, int kind_fixed,
+                          int corrected, int flush_kblocks) {
+    using T = Traits<FMT>;
+    constexpr uint32_t kIdescHalf = umma_idesc<FMT, 2 * BM, 128>();
+    constexpr uint32_t kIdescFull = umma_idesc<FMT, 2 * BM, kWideBN>();
+    const int kind = kind_fixed >= 0 ? kind_fixed : dec->kind;
+    const bool mine = FMT == kTf32 ? kind == kKindTf32 : (kind == kKindFp16 || kind == kKindFp16Scaled);
+    if (!mine) return;  // both CTAs of the pair read the same decision
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    WideSmemTail* tail =
+        reinterpret_cast<WideSmemTail*>(smem + size_t(kWideStages) * kWideStageBytes);
+    auto tile = [&](int s, int which) -> uint8_t* {
+        return smem + size_t(s) * kWideStageBytes + size_t(which) * kTileBytes;
+    };
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+
+    const int tiles_m = (m + 2 * BM - 1) / (2 * BM), tiles_n = (n2 + kWideBN - 1) / kWideBN;
+    const int id = blockIdx.x >> 1;
+    const int group = kGroupM * tiles_n;
+    const int first_m = (id / group) * kGroupM;
+    const int gsize = min(tiles_m - first_m, kGroupM);
+    const int m_blk = first_m + (id % group) % gsize;
+    const int n_blk = (id % group) / gsize;
+    const int m0 = m_blk * 2 * BM + int(rank) * BM;  // this CTA's 128 rows
+    const int n0 = n_blk * kWideBN;                  // the pair's 256 columns
+
+    const int nkb = kp / T::kBK;
+    const int F = flush_kblocks > 0 ? flush_kblocks : (nkb > 0 ? nkb : 1);
+    const int nchunks = (nkb + F - 1) / F;
+    const uint32_t cta_bytes = uint32_t(corrected ? 4 : 2) * kTileBytes;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kWideStages; ++s) {
+            mbar_init(&tail->full[s], 1);
+            mbar_init(&tail->empty[s], 1);
+        }
+        for (int h = 0; h < 2; ++h) {
+            mbar_init(&tail->tfull[h], 1);
+            mbar_init(&tail->tempty[h], 2 * kEpiWarps / 2);  // 4 warps per CTA drain a half
+        }
+        mbar_init(&tail->cfull, 1);
+        fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&map_ahi);
+        tma_prefetch(&map_bhi);
+        if (corrected) {
+            tma_prefetch(&map_alo);
+            tma_prefetch(&map_blo);
+        }
+    }
+    if (warp == 1) tmem_alloc_pair<kTmemCols>(&tail->tmem_base);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = tail->tmem_base;
+
+    if (warp == 0) {
+        // -------------------------------------------- TMA producer (both CTAs)
+        if (lane == 0) {
+            const int nb0 = n0 + 128 * int(rank);
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int s = kb % kWideStages;
+                mbar_wait(&tail->empty[s], ((kb / kWideStages) & 1) ^ 1);
+                if (leader) mbar_expect_tx(&tail->full[s], 2 * cta_bytes);
+                const int kx = kb * T::kBK;
+                tma_load_2d_pair(tile(s, 0), &map_ahi, &tail->full[s], kx, m0);
+                tma_load_2d_pair(tile(s, 2), &map_bhi, &tail->full[s], kx, nb0);
+                if (corrected) {
+                    tma_load_2d_pair(tile(s, 1), &map_alo, &tail->full[s], kx, m0);
+                    tma_load_2d_pair(tile(s, 3), &map_blo, &tail->full[s], kx, nb0);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------------------------------- MMA issuer (pair leader only)
+        if (leader) {
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int chunk = kb / F;
+                const bool chunk_start = (kb % F) == 0;
+                const bool chunk_end = (kb % F) == F - 1 || kb == nkb - 1;
+                const int s = kb % kWideStages;
+                mbar_wait(&tail->full[s], (kb / kWideStages) & 1);
+                tc_fence_after();
+                const uint64_t dah = umma_desc_k_sw128(tile(s, 0));
+                const uint64_t dal = umma_desc_k_sw128(tile(s, 1));
+                const uint64_t dbh = umma_desc_k_sw128(tile(s, 2));
+                const uint64_t dbl = umma_desc_k_sw128(tile(s, 3));
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (chunk_start && chunk > 0) {
+                        mbar_wait(&tail->tempty[h], (chunk - 1) & 1);
+                        tc_fence_after();
+                    }
+                    // B rows 64h.. of each CTA's tile: 64 rows x 128 B = 8 KB (>> 4 = 512)
+                    const uint64_t dbh_h = dbh + uint64_t(512 * h);
+                    if (elect_one()) {
+#pragma unroll
+                        for (int ks = 0; ks < T::kKSteps; ++ks) {
+                            const uint64_t adv = uint64_t((ks * T::kUK * T::kElem) >> 4);
+                            const uint32_t acc = (!chunk_start || ks > 0) ? 1u : 0u;
+                            if (FMT == kFp16)
+                                mma2_f16(tmem + uint32_t(128 * h), dah + adv, dbh_h + adv, kIdescHalf, acc);
+                            else
+                                mma2_tf32(tmem + uint32_t(128 * h), dah + adv, dbh_h + adv, kIdescHalf, acc);
+                        }
+                        if (chunk_end) mma_commit_pair(&tail->tfull[h], 0x3);
+                    }
+                    __syncwarp();
+                }
+                if (elect_one()) {
+                    if (corrected) {
+#pragma unroll
+                        for (int ks = 0; ks < T::kKSteps; ++ks) {
+                            const uint64_t adv = uint64_t((ks * T::kUK * T::kElem) >> 4);
+                            const uint32_t acc = (kb > 0 || ks > 0) ? 1u : 0u;
+                            if (FMT == kFp16) {
+                                mma2_f16(tmem + 256u, dal + adv, dbh + adv, kIdescFull, acc);
+                                mma2_f16(tmem + 256u, dah + adv, dbl + adv, kIdescFull, 1u);
+                            } else {
+                                mma2_tf32(tmem + 256u, dal + adv, dbh + adv, kIdescFull, acc);
+                                mma2_tf32(tmem + 256u, dah + adv, dbl + adv, kIdescFull, 1u);
+                            }
+                        }
+                    }
+                    mma_commit_pair(&tail->empty[s], 0x3);
+                    if (kb == nkb - 1) mma_commit_pair(&tail->cfull, 0x3);
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        // ------------------------------------------------ epilogue (both CTAs)
+        // warp w: TMEM lane quadrant q = w % 4, main half p; it owns C' columns
+        // n0 + 64p + [0,64) (acc[0..63]) and n0 + 128 + 64p + [0,64) (acc[64..127])
+        const int q = warp & 3;
+        const int p = (warp - 2) >> 2;
+        const int rloc = 32 * q + lane;
+        const uint32_t lane_base = tmem + (uint32_t(32 * q) << 16);
+        const uint32_t tempty_leader = mapa_shared(smem_u32(&tail->tempty[p]), 0);
+        float acc[128];
+#pragma unroll
+        for (int i = 0; i < 128; ++i) acc[i] = -0.0f;  // RN identity
+        for (int ch = 0; ch < nchunks; ++ch) {
+            mbar_wait(&tail->tfull[p], ch & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                float v[64];
+                tmem_ld64(lane_base + uint32_t(128 * p + 64 * hh), v);
+                if (hh == 1) {
+                    // the partial is in registers: hand the TMEM half back
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(tempty_leader);
+                }
+#pragma unroll
+                for (int i = 0; i < 64; ++i) acc[64 * hh + i] = __fadd_rn(acc[64 * hh + i], v[i]);
+            }
+        }
+        if (nkb > 0) {
+            mbar_wait(&tail->cfull, 0);
+            tc_fence_after();
+        }
+        if (corrected && nkb > 0) {
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+                for (int cb = 0; cb < 2; ++cb) {
+                    float v[32];
+                    tmem_ld32(lane_base + 256u + uint32_t(128 * hh + 64 * p + 32 * cb), v);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        float& a = acc[64 * hh + 32 * cb + i];
+                        a = __fadd_rn(a, __fmul_rn(v[i], 0x1.0p-11f));
+                    }
+                }
+            }
+        }
+        const bool scaled = kind == kKindFp16Scaled && (dec->scale_a + dec->scale_b) != 0;
+        if (scaled) {
+            const double f = ldexp(1.0, -(dec->scale_a + dec->scale_b));
+#pragma unroll
+            for (int i = 0; i < 128; ++i) acc[i] = scale_pow2(acc[i], f);
+        }
+        // stage the 128 x 256 tile in the idle operand smem, then store rows
+        float* ctile = reinterpret_cast<float*>(smem);
+        float* myrow = ctile + size_t(rloc) * kWideCStride;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+            for (int i = 0; i < 64; i += 4)
+                *reinterpret_cast<float4*>(myrow + 128 * hh + 64 * p + i) =
+                    make_float4(acc[64 * hh + i], acc[64 * hh + i + 1], acc[64 * hh + i + 2],
+                                acc[64 * hh + i + 3]);
+        epi_bar_sync();
+        const int ew = warp - 2;
+        const bool full_cols = n0 + kWideBN <= n2 && (n2 & 3) == 0;
+        for (int r = ew; r < BM; r += kEpiWarps) {
+            const int grow = m0 + r;
+            if (grow >= m) break;
+            float* dst = c + size_t(grow) * n2 + n0;
+            const float* srow = ctile + size_t(r) * kWideCStride;
+            if (full_cols) {
+                reinterpret_cast<float4*>(dst)[lane] = reinterpret_cast<const float4*>(srow)[lane];
+                reinterpret_cast<float4*>(dst)[lane + 32] =
+                    reinterpret_cast<const float4*>(srow)[lane + 32];
+            } else {
+                for (int i = lane; i < kWideBN; i += 32)
+                    if (n0 + i < n2) dst[i] = srow[i];
+            }
+        }
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_pair<kTmemCols>(tmem);
+    }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
 
@@ -535,17 +799,25 @@ int launch_fmt(const TcecGemmArgs& g, cudaStream_t s) {
         e = cudaFuncSetAttribute(tcec_gemm_pair_kernel<FMT>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPairSmemBytes));
         if (e != cudaSuccess) return int(e);
+        e = cudaFuncSetAttribute(tcec_gemm_wide_kernel<FMT>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(kWideSmemBytes));
+        if (e != cudaSuccess) return int(e);
         attr_set = true;
     }
     CUtensorMap mah, mal, mbh, mbl;
     const void* alo = g.corrected ? g.a_lo : g.a_hi;
     const void* blo = g.corrected ? g.b_lo : g.b_hi;
-    const uint32_t b_box = g.pair ? 64u : 128u;
+    const uint32_t b_box = g.pair == kVariantPair ? 64u : 128u;
     if (!make_map(&mah, g.a_hi, FMT, g.m, g.kp, 128u) || !make_map(&mal, alo, FMT, g.m, g.kp, 128u) ||
         !make_map(&mbh, g.b_hi, FMT, g.n2, g.kp, b_box) ||
         !make_map(&mbl, blo, FMT, g.n2, g.kp, b_box))
         return int(cudaErrorInvalidValue);
-    if (g.pair) {
+    if (g.pair == kVariantWide) {
+        const int64_t tiles = ((g.m + 2 * BM - 1) / (2 * BM)) * ((g.n2 + kWideBN - 1) / kWideBN);
+        tcec_gemm_wide_kernel<FMT><<<unsigned(2 * tiles), kThreadsGemm, kWideSmemBytes, s>>>(
+            mah, mal, mbh, mbl, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed,
+            g.corrected, g.flush_kblocks);
+    } else if (g.pair == kVariantPair) {
         const int64_t tiles = ((g.m + 2 * BM - 1) / (2 * BM)) * ((g.n2 + BN - 1) / BN);
         tcec_gemm_pair_kernel<FMT><<<unsigned(2 * tiles), kThreadsGemm, kPairSmemBytes, s>>>(
             mah, mal, mbh, mbl, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed,
@@ -560,6 +832,12 @@ int launch_fmt(const TcecGemmArgs& g, cudaStream_t s) {
 }
 
 }  // namespace
+
+int resolve_gemm_variant(int requested, int64_t m, int64_t n2, int sm_count) {
+    if (requested != kVariantAuto) return requested;
+    const int64_t wide_ctas = 2 * ((m + 2 * BM - 1) / (2 * BM)) * ((n2 + kWideBN - 1) / kWideBN);
+    return wide_ctas >= sm_count ? kVariantWide : kVariantSingle;
+}
 
 int launch_tcec_gemm(const TcecGemmArgs& g, cudaStream_t s) {
     if (!get_encode()) return int(cudaErrorNotSupported);

@@ -15,7 +15,7 @@ struct tcec_handle_s {
     cudaStream_t stream = nullptr;
     int flush_kblocks = 1;  // RN flush of the main term every k-block (64 f16 / 32 tf32 K')
     int executor = 0;       // network executor: 0 auto, 1 per-step only, 2 fused only
-    int gemm_pair = 0;      // 1 = cta_group::2 TCEC kernel (tcec_set_gemm_variant); 0 measured faster
+    int gemm_pair = 0;      // tcgen05 kernel variant (tcec_set_gemm_variant): 0 auto, 1 pair, 2 single, 3 wide
     // operand workspace (split hi/lo planes), grown on demand
     void* ws = nullptr;
     size_t ws_bytes = 0;

@@ -87,8 +87,12 @@ struct TcecGemmArgs {
     int fmt;                              // 0 = f16 kernel, 1 = tf32 kernel
     int corrected;                        // 1 = TCEC (3 products), 0 = TC ablation
     int flush_kblocks;                    // RN flush interval of the main term, 0 = none
-    int pair;                             // 1 = cta_group::2 kernel (256x128 tile per CTA pair)
+    int pair;                             // resolved kernel variant (kVariantSingle/Pair/Wide)
 };
+// tcgen05 kernel variants (tcec_set_gemm_variant): auto picks wide when its
+// 256 x 256 pair tiles fill the SMs, else single
+enum GemmVariant : int { kVariantAuto = 0, kVariantPair = 1, kVariantSingle = 2, kVariantWide = 3 };
+int resolve_gemm_variant(int requested, int64_t m, int64_t n2, int sm_count);
 // returns a cudaError_t
 int launch_tcec_gemm(const TcecGemmArgs& args, cudaStream_t s);
 

@@ -87,6 +87,53 @@ def test_tcec_ragged_shapes(handle, orc, dev, shape):
         assert e <= max(TOL_FACTOR * err_ref, 2e-7), (mode, e, err_ref)
 
 
+@pytest.mark.parametrize("variant", ["single", "pair", "wide"])
+@pytest.mark.parametrize("shape", [(3, 5, 7), (129, 65, 200), (300, 257, 31), (513, 385, 129),
+                                   (130, 130, 1100), (600, 300, 2100)])
+def test_tcec_kernel_variants(handle, orc, dev, variant, shape):
+    """Every tcgen05 kernel variant (128x128 single CTA, 256x128 and 256x256
+    CTA pairs) meets the reference bar on ragged shapes; the TC ablation
+    (no correction products) is >= 10x worse."""
+    m, n, k = shape
+    a = matrix_recipe("uniform", m, k, 41 + m)
+    b = matrix_recipe("uniform", k, n, 43 + n)
+    ref = orc.cgemm_oracle(a, b)
+    err_ref = relerr(orc.cgemm(a, b, "FP32_REF")[0], ref)
+    ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    handle.set_gemm_variant(variant)
+    try:
+        errs = {}
+        for mode in ("FP16TCEC", "TF32TCEC", "FP16TC"):
+            c, _ = handle.cgemm(ad, bd, mode)
+            errs[mode] = relerr(c.cpu().numpy(), ref)
+    finally:
+        handle.set_gemm_variant("auto")
+    for mode in ("FP16TCEC", "TF32TCEC"):
+        assert errs[mode] <= max(TOL_FACTOR * err_ref, 2e-7), (mode, errs, err_ref)
+    if k >= 64:
+        assert errs["FP16TC"] >= 10 * errs["FP16TCEC"], errs
+
+
+@pytest.mark.parametrize("variant", ["single", "wide"])
+def test_tcec_all_positive_long_k(handle, orc, dev, variant):
+    """All-positive operands make tensor-core truncation a systematic bias;
+    the per-k-block RN flush keeps TCEC within the reference bar."""
+    m, n, k = 256, 160, 4000
+    rng = np.random.default_rng(5)
+    a = (rng.random((m, k)) + 1j * rng.random((m, k))).astype(np.complex64)
+    b = (rng.random((k, n)) + 1j * rng.random((k, n))).astype(np.complex64)
+    ref = orc.cgemm_oracle(a, b)
+    err_ref = relerr(orc.cgemm(a, b, "FP32_REF")[0], ref)
+    handle.set_gemm_variant(variant)
+    try:
+        for mode in ("FP16TCEC", "TF32TCEC"):
+            c, _ = handle.cgemm(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev), mode)
+            e = relerr(c.cpu().numpy(), ref)
+            assert e <= TOL_FACTOR * err_ref, (variant, mode, e, err_ref)
+    finally:
+        handle.set_gemm_variant("auto")
+
+
 def test_exact_small_value_matrices_all_modes(handle, dev):
     # test_gemm.cpp:166-181: {0, +-1/2, +-1} products are exact in every mode
     g = np.random.default_rng(31)

@@ -13,6 +13,8 @@ from paper_2303_08989_b200 import Handle  # noqa: E402
 from tests.golden.recipes import matrix_recipe  # noqa: E402
 
 h = Handle(0)
+VARIANTS = os.environ.get("VARIANTS", "single,wide").split(",")
+FLUSHES = [int(x) for x in os.environ.get("FLUSHES", "1,0").split(",")]
 o = O.oracle()
 dev = torch.device("cuda:0")
 
@@ -29,7 +31,7 @@ for rec, m, n, k in cases:
     ref = o.cgemm_oracle(a, b)
     e32 = relerr(o.cgemm(a, b, "FP32_REF")[0], ref)
     ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
-    for pair in (0, 1):
+    for pair in ("single", "pair", "wide"):
         h.set_gemm_variant(pair)
         for fl in (1, 2, 4):
             h.flush_kblocks = fl
@@ -44,9 +46,9 @@ for nn in (4096, 8192):
     a = (torch.rand(nn, nn, 2, device=dev) * 2 - 1).view(torch.complex64)[..., 0].contiguous()
     b = (torch.rand(nn, nn, 2, device=dev) * 2 - 1).view(torch.complex64)[..., 0].contiguous()
     c = torch.empty(nn, nn, dtype=torch.complex64, device=dev)
-    for pair in (0, 1):
+    for pair in VARIANTS:
         h.set_gemm_variant(pair)
-        for fl in (1, 2, 4, 0):
+        for fl in FLUSHES:
             h.flush_kblocks = fl
             for mode in ("FP16TCEC", "TF32TCEC"):
                 h.cgemm(a, b, mode, out=c)
