@@ -318,7 +318,7 @@ def run_ours(args):
                        "flush_kblocks": h.flush_kblocks},
             "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": "tcec_gemm_kernel<f16>",
+                         "kernel": gemm_kernel_name(n, n, kind),
                          "note": f"3 x 8mnk tensor-pipe flops per launch / CUDA-event time; "
                                  f"peak = {src} dense bf16 sustained (fp16 = bf16 rate)"},
             "stages_ms": {k2: round(v / max(cnt, 1), 3) for k2, v in stage.items()},
@@ -588,9 +588,109 @@ def run_sycamore(args):
         dist.destroy_process_group()
 
 
+SKEWED_SHAPES = [(2048, 16384, 64), (512, 16384, 512), (512, 8192, 1024), (1024, 4096, 8192),
+                 (2048, 4096, 32), (256, 16384, 64), (128, 1024, 4096)]
+IRREGULAR_N = (20, 22, 24, 26)
+
+
+def type3_device(rows, cols, gen, dev):
+    """randtn Type-3 recipe (network.cpp:402-434): N(0, 1e-2) * 1e-6
+    components with 16 planted 1.0 values -> e_max = 0 and ~29% of the components
+    below 2^-28, so the selector must fall back to TF32TCEC."""
+    import torch
+    v = torch.randn((rows, cols, 2), generator=gen, device=dev).mul_(1e-2 * 1e-6)
+    flat = v.view(-1, 2)
+    idx = torch.randint(0, rows * cols, (16,), generator=gen, device=dev)
+    flat[idx, 0] = 1.0
+    flat[idx, 1] = 0.0
+    return v.view(torch.complex64)[..., 0].contiguous()
+
+
+def run_skewed(args):
+    """configs[2]: contraction-shaped skewed CGEMMs (tall-skinny, small k) with a wide
+    exponent range forcing the TF32TCEC fallback (policy size_auto = size_tf32 =
+    min(m, n, k) so the statistics engage), plus the paper's irregular
+    (2, 2^N, 2) / (2^N, 2, 2) family under the default policy (FP32 tier)."""
+    import torch
+    from paper_2303_08989_b200 import Handle, SelectionPolicy, make_config
+    world, rank, local = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    h = Handle(local)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(11 + rank)
+    bpk, bps, hbm, src = peaks()
+    rows_out, tot_flops, tot_ms = [], 0.0, 0.0
+    cases = [(s, "type3") for s in SKEWED_SHAPES]
+    cases += [((2, 1 << e, 2), "uniform") for e in IRREGULAR_N]
+    cases += [((1 << e, 2, 2), "uniform") for e in IRREGULAR_N]
+    with ClockSampler(local) as clk:
+        for (m, n, k), rec in cases:
+            if rec == "type3":
+                a, b = type3_device(m, k, gen, dev), type3_device(k, n, gen, dev)
+                mn = min(m, n, k)
+                cfg = make_config(SelectionPolicy(size_auto=mn, size_tf32=mn))
+            else:
+                a = (torch.rand((m, k, 2), generator=gen, device=dev) * 2 - 1).view(torch.complex64)[..., 0].contiguous()
+                b = (torch.rand((k, n, 2), generator=gen, device=dev) * 2 - 1).view(torch.complex64)[..., 0].contiguous()
+                cfg = make_config()
+            c = torch.empty((m, n), dtype=torch.complex64, device=dev)
+            for _ in range(args.warmup):
+                _, res = h.dispatch_cgemm(a, b, cfg, out=c)
+            h.profile(True)
+            barrier(world)
+            torch.cuda.synchronize(dev)
+            for _ in range(args.steps):
+                h.dispatch_cgemm(a, b, cfg, out=c)
+            stage, cnt = h.profile_read()
+            h.profile(False)
+            ms = sum(stage.values()) / max(cnt, 1)
+            ms = max_over_ranks(ms, world)
+            flops = 8.0 * m * n * k
+            floor_bytes = 8.0 * (m * k + k * n + m * n)
+            # fidelity on <= 8 sampled rows vs complex128 (and the bit-exact FP32 tier)
+            ridx = torch.arange(0, m, max(1, m // 8), device=dev)[:8]
+            ref = a[ridx].to(torch.complex128) @ b.to(torch.complex128)
+            den = float(torch.linalg.norm(ref))
+            err = float(torch.linalg.norm(c[ridx].to(torch.complex128) - ref)) / den if den else 0.0
+            c32, _ = h.cgemm(a[ridx].contiguous(), b, "FP32_REF")
+            err32 = float(torch.linalg.norm(c32.to(torch.complex128) - ref)) / den if den else 0.0
+            del ref, c32
+            tot_flops += flops
+            tot_ms += ms
+            rows_out.append({"m": m, "n": n, "k": k, "inputs": rec, "mode": res.line.split(",")[3],
+                             "ms": round(ms, 4), "tflops": round(flops / (ms * 1e-3) / 1e12, 2),
+                             "floor_gbs": round(floor_bytes / (ms * 1e-3) / 1e9, 1),
+                             "floor_frac_hbm": round(floor_bytes / (ms * 1e-3) / 1e9 / hbm, 3),
+                             "stages_ms": {k2: round(v / max(cnt, 1), 4) for k2, v in stage.items()},
+                             "rel_err": err, "fp32_ref_rel_err": err32})
+            del a, b, c
+            torch.cuda.empty_cache()
+    if rank == 0:
+        value = world * tot_flops / (tot_ms * 1e-3) / 1e12
+        line = {"metric": "skewed TCEC CGEMM TFLOP/s (useful 8mnk over the configs[2] shape set)",
+                "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(tot_ms, 3), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "c64 (TF32TCEC / FP32 tiers)",
+                "data": "synthetic: Type-3 wide-exponent-range (TF32 fallback) and uniform(-1,1)",
+                "config": {"workload": "configs[2] skewed contraction-shaped CGEMMs + (2,2^N,2) family",
+                           "timing": "device time of stats+prep+gemm stages (CUDA events)",
+                           "parallelism": f"replicas x{world}"},
+                "shapes": rows_out, "hbm_peak_gbs": hbm, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    h.close()
+
+
+def gemm_kernel_name(m, n, kind, sm_count=148):
+    """The tcgen05 kernel the auto variant runs (resolve_gemm_variant in tcec_gemm.cu)."""
+    wide = 2 * -(-m // 256) * -(-2 * n // 256) >= sm_count
+    fmt = "tf32" if kind == "TF32TCEC" else "f16"
+    return f"tcec_gemm_{'wide_' if wide else ''}kernel<{fmt}>"
+
+
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("--workload", choices=["cgemm", "rqc", "sycamore"], default="cgemm")
+    p.add_argument("--workload", choices=["cgemm", "rqc", "sycamore", "skewed"], default="cgemm")
     p.add_argument("--cycles", type=int, default=10)
     p.add_argument("--slices-log2", type=int, default=6)
     p.add_argument("--gpus", type=int, default=1)
@@ -609,6 +709,8 @@ def main():
         run_rqc(args)
     elif args.workload == "sycamore":
         run_sycamore(args)
+    elif args.workload == "skewed":
+        run_skewed(args)
     elif args.impl == "reference":
         run_reference(args)
     else:

@@ -145,7 +145,9 @@ int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t
         return set_error(TCEC_ERR_INVALID_ARGUMENT, "k_tile must be >= 1");
     const bool prof = h.prof && h.ev[0];
     if (prof) cudaEventRecord(h.ev[0], s);
-    cudaMemsetAsync(d, 0, sizeof(DevDecision), s);
+    // only the tensor-core tier writes the decision slot (finish_dispatch reads
+    // nothing from it for the SIMT tiers)
+    if (p.tier == kTierTc) cudaMemsetAsync(d, 0, sizeof(DevDecision), s);
     if (p.stats) {
         launch_stats1(a, 2 * m * k, b, 2 * k * n, d, s);
         const double t = p.forced_scaled ? 1.0 : cfg.threshold_t;
@@ -244,11 +246,12 @@ int finish_dispatch(const DispatchPlan& p, const DevDecision& dd, int64_t m, int
         res->scale_a = dd.scale_a;
         res->scale_b = dd.scale_b;
     }
-    res->overflow = dd.overflow ? 1 : 0;
+    const bool dev_written = p.tier == kTierTc;
+    res->overflow = dev_written && dd.overflow ? 1 : 0;
     const char* label = p.forced >= 0 ? forced_name(p.forced) : kind_name(kind);
     format_line(res->line, sizeof res->line, m, n, k, label, res->scale_a, res->scale_b,
                 &res->stats_a, &res->stats_b, res->has_stats != 0);
-    if (dd.scale_overflow)
+    if (dev_written && dd.scale_overflow)
         return set_error(TCEC_ERR_SCALE_OVERFLOW, "scaled component left the f32 range");
     return TCEC_OK;
 }

@@ -679,6 +679,119 @@ __global__ void __launch_bounds__(kChainThreads) cgemm_chain_kernel(const float2
     }
 }
 
+// Irregular skinny shapes, small k with one small outer dimension -- the
+// (2, 2^N, 2) / (2^N, 2, 2) contraction family.  Memory-bound:
+// one thread per column j (m <= MX, "column" kernel) or per row i (n <= MX,
+// "row" kernel) keeps the MX x 4 chains of its outputs in registers, reads the
+// long operand exactly once (coalesced / contiguous) and writes C once; the
+// short operand sits in shared memory.  Each output runs the reference's four
+// chains in ascending k (kernels_scalar.cpp:76-87) -> bit-identical.
+constexpr int kSkinnyMaxK = 32;
+
+template <bool F64>
+TCEC_DEV void chain4(float ar, float ai, float br, float bi, double (&p)[4]) {
+    p[0] = __dadd_rn(p[0], __dmul_rn(double(ar), double(br)));
+    p[1] = __dadd_rn(p[1], __dmul_rn(double(ai), double(bi)));
+    p[2] = __dadd_rn(p[2], __dmul_rn(double(ar), double(bi)));
+    p[3] = __dadd_rn(p[3], __dmul_rn(double(ai), double(br)));
+}
+template <bool F64>
+TCEC_DEV void chain4(float ar, float ai, float br, float bi, float (&p)[4]) {
+    p[0] = __fadd_rn(p[0], __fmul_rn(ar, br));
+    p[1] = __fadd_rn(p[1], __fmul_rn(ai, bi));
+    p[2] = __fadd_rn(p[2], __fmul_rn(ar, bi));
+    p[3] = __fadd_rn(p[3], __fmul_rn(ai, br));
+}
+template <bool F64, typename T>
+TCEC_DEV float2 assemble(const T (&p)[4]) {
+    if (F64)
+        return make_float2(__fsub_rn(__double2float_rn(double(p[0])), __double2float_rn(double(p[1]))),
+                           __fadd_rn(__double2float_rn(double(p[2])), __double2float_rn(double(p[3]))));
+    return make_float2(__fsub_rn(float(p[0]), float(p[1])), __fadd_rn(float(p[2]), float(p[3])));
+}
+
+// m <= MX: thread j owns column j of C
+template <bool F64, int MX>
+__global__ void __launch_bounds__(256) cgemm_skinny_col_kernel(const float2* __restrict__ a,
+                                                               const float2* __restrict__ b,
+                                                               float2* __restrict__ c, int m,
+                                                               int64_t n, int k) {
+    using acc_t = typename std::conditional<F64, double, float>::type;
+    __shared__ float2 as[MX * kSkinnyMaxK];
+    for (int t = threadIdx.x; t < m * k; t += blockDim.x) as[t] = a[t];
+    __syncthreads();
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    acc_t p[MX][4];
+#pragma unroll
+    for (int i = 0; i < MX; ++i) p[i][0] = p[i][1] = p[i][2] = p[i][3] = acc_t(0);
+    for (int kk = 0; kk < k; ++kk) {
+        const float2 bv = __ldcs(b + int64_t(kk) * n + j);
+#pragma unroll
+        for (int i = 0; i < MX; ++i)
+            if (i < m) {
+                const float2 av = as[i * k + kk];
+                chain4<F64>(av.x, av.y, bv.x, bv.y, p[i]);
+            }
+    }
+#pragma unroll
+    for (int i = 0; i < MX; ++i)
+        if (i < m) __stcs(c + int64_t(i) * n + j, assemble<F64>(p[i]));
+}
+
+// n <= MX: thread i owns row i of C
+template <bool F64, int MX>
+__global__ void __launch_bounds__(256) cgemm_skinny_row_kernel(const float2* __restrict__ a,
+                                                               const float2* __restrict__ b,
+                                                               float2* __restrict__ c, int64_t m,
+                                                               int n, int k) {
+    using acc_t = typename std::conditional<F64, double, float>::type;
+    __shared__ float2 bs[kSkinnyMaxK * MX];
+    for (int t = threadIdx.x; t < k * n; t += blockDim.x) bs[t] = b[t];
+    __syncthreads();
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    acc_t p[MX][4];
+#pragma unroll
+    for (int j = 0; j < MX; ++j) p[j][0] = p[j][1] = p[j][2] = p[j][3] = acc_t(0);
+    const float2* arow = a + i * k;
+    for (int kk = 0; kk < k; ++kk) {
+        const float2 av = __ldcs(arow + kk);
+#pragma unroll
+        for (int j = 0; j < MX; ++j)
+            if (j < n) {
+                const float2 bv = bs[kk * n + j];
+                chain4<F64>(av.x, av.y, bv.x, bv.y, p[j]);
+            }
+    }
+    float2* crow = c + i * n;
+#pragma unroll
+    for (int j = 0; j < MX; ++j)
+        if (j < n) __stcs(crow + j, assemble<F64>(p[j]));
+}
+
+template <bool F64, int MX>
+void launch_skinny_mx(const float2* a, const float2* b, float2* c, int64_t m, int64_t n, int64_t k,
+                      cudaStream_t s) {
+    if (m <= n)
+        cgemm_skinny_col_kernel<F64, MX><<<unsigned((n + 255) / 256), 256, 0, s>>>(a, b, c, int(m), n, int(k));
+    else
+        cgemm_skinny_row_kernel<F64, MX><<<unsigned((m + 255) / 256), 256, 0, s>>>(a, b, c, m, int(n), int(k));
+}
+
+// true when the skinny kernels take the shape
+template <bool F64>
+bool launch_skinny(const float2* a, const float2* b, float2* c, int64_t m, int64_t n, int64_t k,
+                   cudaStream_t s) {
+    const int64_t small = m < n ? m : n, large = m < n ? n : m;
+    if (k > kSkinnyMaxK || small > 16 || large < 4096) return false;
+    if (small <= 2) launch_skinny_mx<F64, 2>(a, b, c, m, n, k, s);
+    else if (small <= 4) launch_skinny_mx<F64, 4>(a, b, c, m, n, k, s);
+    else if (small <= 8) launch_skinny_mx<F64, 8>(a, b, c, m, n, k, s);
+    else launch_skinny_mx<F64, 16>(a, b, c, m, n, k, s);
+    return true;
+}
+
 template <bool F64>
 void launch_chain(const float2* a, const float2* b, float2* c, int64_t m, int64_t n, int64_t k,
                   cudaStream_t s) {
@@ -931,6 +1044,7 @@ void launch_cgemm_fp32_ref(const float2* a, const float2* b, float2* c, int64_t 
         launch_chain<false>(a, b, c, m, n, k, s);
         return;
     }
+    if (launch_skinny<false>(a, b, c, m, n, k, s)) return;
     if (k >= 1024 && m * n <= 65536 && tiles < 2 * 148) {
         const int64_t warps = m * n;
         cgemm_longk_kernel<false><<<unsigned((warps + 7) / 8), 256, 0, s>>>(a, b, c, m, n, k);
@@ -946,6 +1060,7 @@ void launch_cgemm_fp64(const float2* a, const float2* b, float2* c, int64_t m, i
         launch_chain<true>(a, b, c, m, n, k, s);
         return;
     }
+    if (launch_skinny<true>(a, b, c, m, n, k, s)) return;
     if (k >= 256 && m * n <= 65536) {
         cgemm_longk_kernel<true><<<unsigned((m * n + 7) / 8), 256, 0, s>>>(a, b, c, m, n, k);
         return;

@@ -276,3 +276,19 @@ def test_long_k_kernels_bit_exact(handle, orc, dev, shape):
         c, _ = handle.cgemm(ad, bd, mode)
         cr, _ = orc.cgemm(a, b, mode)
         assert np.array_equal(bits(c.cpu().numpy().view(np.float32)), bits(cr.view(np.float32))), mode
+
+
+@pytest.mark.parametrize("shape", [(2, 4096, 2), (3, 5000, 7), (16, 8192, 32), (9, 4100, 1),
+                                   (5000, 9, 31), (8192, 16, 1), (4096, 2, 2), (4097, 5, 17)])
+def test_skinny_kernels_bit_exact(handle, orc, dev, shape):
+    """Irregular skinny shapes (small k, one outer dim <= 16: PAPER.md:346-352)
+    take the thread-per-column / thread-per-row kernels; the chains keep the
+    reference order -> FP32_REF and FP64_ORACLE bit-exact."""
+    m, n, k = shape
+    a = matrix_recipe("uniform", m, k, 18 + m)
+    b = matrix_recipe("uniform", k, n, 19 + n)
+    ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    for mode in ("FP32_REF", "FP64_ORACLE"):
+        c, _ = handle.cgemm(ad, bd, mode)
+        cr, _ = orc.cgemm(a, b, mode)
+        assert np.array_equal(bits(c.cpu().numpy().view(np.float32)), bits(cr.view(np.float32))), mode
