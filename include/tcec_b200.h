@@ -65,7 +65,8 @@ int tcec_set_flush_kblocks(tcec_handle h, int kblocks);
 int tcec_get_flush_kblocks(tcec_handle h);
 /* tensor-core kernel variant: 0 = auto (default: wide when its tiles fill the
  * SMs, else single), 1 = CTA pair (cta_group::2, 256 x 128 tile), 2 = single
- * CTA (128 x 128 tile), 3 = wide CTA pair (cta_group::2, 256 x 256 tile) */
+ * CTA (128 x 128 tile), 3 = wide CTA pair (cta_group::2, 256 x 256 tile),
+ * 4 = the wide tile on persistent CTA pairs */
 int tcec_set_gemm_variant(tcec_handle h, int variant);
 /* network executor: 0 = auto (fused small-step kernel -- one warp per network,
  * intermediates in shared memory -- whenever every step is on a SIMT tier and

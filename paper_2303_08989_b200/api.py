@@ -103,11 +103,12 @@ class Handle:
         3 per-step graph preceded by the fused subtree launch (hybrid)."""
         check(self.lib.tcec_set_executor(self.h, int(policy)))
 
-    GEMM_VARIANTS = {"auto": 0, "pair": 1, "single": 2, "wide": 3}
+    GEMM_VARIANTS = {"auto": 0, "pair": 1, "single": 2, "wide": 3, "wide_persistent": 4}
 
     def set_gemm_variant(self, variant) -> None:
         """tcgen05 kernel variant: "auto" (default), "pair" (cta_group::2,
-        256x128 tile), "single" (128x128 tile), "wide" (cta_group::2, 256x256)."""
+        256x128 tile), "single" (128x128 tile), "wide" (cta_group::2, 256x256), "wide_persistent"
+        (the same tile, persistent CTA pairs)."""
         v = self.GEMM_VARIANTS[variant] if isinstance(variant, str) else int(variant)
         check(self.lib.tcec_set_gemm_variant(self.h, v))
 

@@ -207,17 +207,15 @@ int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t
     g.corrected = p.corrected;
     g.flush_kblocks = p.corrected ? h.flush_kblocks : 0;
     g.pair = resolve_gemm_variant(h.gemm_pair, m, 2 * n, h.sm_count);
-    const bool want16 = p.kind < 0 || p.kind == kKindFp16 || p.kind == kKindFp16Scaled;
-    const bool want32 = (p.kind < 0 && !p.forced_scaled) || p.kind == kKindTf32;
-    if (want16) {
-        g.fmt = kFp16;
+    g.sms = h.sm_count;
+    if (p.kind < 0 && !p.forced_scaled) {
+        g.fmt = -1;  // format chosen by the device decision
         const int e = launch_tcec_gemm(g, s);
-        if (e) return cuda_error(cudaError_t(e), "tcec_gemm f16");
-    }
-    if (want32) {
-        g.fmt = kTf32;
+        if (e) return cuda_error(cudaError_t(e), "tcec_gemm auto");
+    } else {
+        g.fmt = (p.kind == kKindTf32) ? kTf32 : kFp16;
         const int e = launch_tcec_gemm(g, s);
-        if (e) return cuda_error(cudaError_t(e), "tcec_gemm tf32");
+        if (e) return cuda_error(cudaError_t(e), g.fmt == kTf32 ? "tcec_gemm tf32" : "tcec_gemm f16");
     }
     if (prof) cudaEventRecord(h.ev[3], s);
     return TCEC_OK;
@@ -401,7 +399,7 @@ int tcec_set_executor(tcec_handle h, int policy) {
 
 int tcec_set_gemm_variant(tcec_handle h, int variant) {
     CHECK_HANDLE(h);
-    if (variant < 0 || variant > 3) return set_error(TCEC_ERR_INVALID_ARGUMENT, "variant must be 0..3");
+    if (variant < 0 || variant > 4) return set_error(TCEC_ERR_INVALID_ARGUMENT, "variant must be 0..4");
     h->gemm_pair = variant;
     return TCEC_OK;
 }

@@ -25,6 +25,7 @@
 // 2..9 = epilogue (TMEM lane quadrant warp%4, two 64-column halves).
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
@@ -42,6 +43,7 @@ constexpr int kTileBytes = 128 * 128;  // one operand tile: 128 rows x 128 B (sw
 constexpr int kEpiWarps = 8;      // 2 warps per TMEM lane quadrant, 64 columns each
 constexpr int kThreadsGemm = 64 + 32 * kEpiWarps;
 constexpr int kGroupM = 16;       // rasterization: CTAs of a wave share A/B panels in L2
+constexpr int kWideGroupM = 4;    // the same for the 256 x 256 pair tiles (swept: 4 minimises DRAM re-reads)
 constexpr uint32_t kTmemCols = 512;
 constexpr int kMainBufs = 3;      // ping-pong-pong main partials: cols 0, 128, 256
 constexpr uint32_t kColCorr = 384;
@@ -493,11 +495,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
     }
 }
 
-// ===================================================================== wide pair
-// cta_group::2 kernel with a 256 x 256 tile of C' per CTA pair (128 x 256 per
-// CTA).  Per k-block each CTA stages A_hi/A_lo (its 128 rows) and B_hi/B_lo
-// (its 128 of the pair's 256 columns): 64 KB for 3 x 128x256x64 MACs, i.e.
-// half the operand bytes per MAC of the 128 x 128 kernel, so neither the
+// ================================================== wide pair, persistent
+// Persistent cta_group::2 kernel (variant 4; measured on par with the
+// one-tile-per-cluster kernel below, which is the default "wide") with a 256 x 256 tile of C' per CTA pair
+// (128 x 256 per CTA), one pair per two SMs looping over a static tile
+// schedule.  Per k-block each CTA stages A_hi/A_lo (its 128 rows) and
+// B_hi/B_lo (its 128 of the pair's 256 columns): 64 KB for 3 x 128x256x64
+// MACs, half the operand bytes per MAC of the 128 x 128 kernel, so neither the
 // L2->SM feed nor shared-memory bandwidth paces the tensor pipe.
 //
 // TMEM (512 columns per CTA): main partial as two 128-column halves (cols
@@ -508,42 +512,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
 // Column maps (CTA r of the pair holds B rows n0 + 128 r + [0,128)):
 //   main half h, TMEM col j:  j < 64 -> n0 + 64h + j,  j >= 64 -> n0 + 128 + 64h + (j-64)
 //   corr, TMEM col 256 + j:   n0 + j
+// Across tiles: the smem ring and the main-half barriers run on continuous
+// counters, so the producer prefetches the next tile during the epilogue and
+// the next tile's main products start as soon as their halves are drained; the
+// next tile's correction products wait only for the epilogue's read of the
+// correction accumulator (cempty).  The epilogue stores C straight from
+// registers (each thread owns one row x 2 x 64 contiguous columns).
 constexpr int kWideStages = 3;
 constexpr int kWideBN = 256;
 constexpr int kWideStageBytes = 4 * kTileBytes;  // A_hi | A_lo | B_hi | B_lo, 16 KB each
-constexpr int kWideCStride = kWideBN + 4;
 struct alignas(8) WideSmemTail {
     uint64_t full[kWideStages];
     uint64_t empty[kWideStages];
     uint64_t tfull[2];
     uint64_t tempty[2];
     uint64_t cfull;
+    uint64_t cempty;
     uint32_t tmem_base;
 };
-constexpr size_t kWideSmemBytes = 1024 + size_t(kWideStages) * kWideStageBytes + sizeof(WideSmemTail);
-static_assert(size_t(BM) * kWideCStride * 4 <= size_t(kWideStages) * kWideStageBytes,
-              "C staging tile must fit in the operand stages");
+// C staging: 32 rows (one TMEM lane quadrant) x 256 columns, padded rows
+constexpr int kWideCStride = kWideBN + 4;
+constexpr size_t kWideStageCBytes = size_t(32) * kWideCStride * 4;
+constexpr size_t kWideSmemBytes =
+    1024 + size_t(kWideStages) * kWideStageBytes + kWideStageCBytes + sizeof(WideSmemTail);
+static_assert(kWideSmemBytes <= 232448, "exceeds the 227 KB dynamic shared memory of sm_100");
+
+struct WideMaps {
+    CUtensorMap ahi, alo, bhi, blo;
+};
 
 template <int FMT>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
-    tcec_gemm_wide_kernel(const __grid_constant__ CUtensorMap map_ahi,
-                          const __grid_constant__ CUtensorMap map_alo,
-                          const __grid_constant__ CUtensorMap map_bhi,
-                          const __grid_constant__ CUtensorMap map_blo, float* __restrict__ c,
-                          int m, int n2, int kp, const DevDecision* __restrict__ dec, int kind_fixed,
-                          int corrected, int flush_kblocks) {
+__device__ __forceinline__ void widep_body(const WideMaps& mp, float* __restrict__ c, int m, int n2,
+                                          int kp, const DevDecision* __restrict__ dec, int kind,
+                                          int corrected, int flush_kblocks) {
     using T = Traits<FMT>;
     constexpr uint32_t kIdescHalf = umma_idesc<FMT, 2 * BM, 128>();
     constexpr uint32_t kIdescFull = umma_idesc<FMT, 2 * BM, kWideBN>();
-    const int kind = kind_fixed >= 0 ? kind_fixed : dec->kind;
-    const bool mine = FMT == kTf32 ? kind == kKindTf32 : (kind == kKindFp16 || kind == kKindFp16Scaled);
-    if (!mine) return;  // both CTAs of the pair read the same decision
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
-    WideSmemTail* tail =
-        reinterpret_cast<WideSmemTail*>(smem + size_t(kWideStages) * kWideStageBytes);
+    float* cstage = reinterpret_cast<float*>(smem + size_t(kWideStages) * kWideStageBytes);
+    WideSmemTail* tail = reinterpret_cast<WideSmemTail*>(smem + size_t(kWideStages) * kWideStageBytes +
+                                                         kWideStageCBytes);
     auto tile = [&](int s, int which) -> uint8_t* {
         return smem + size_t(s) * kWideStageBytes + size_t(which) * kTileBytes;
     };
@@ -553,14 +564,329 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
     const bool leader = rank == 0;
 
     const int tiles_m = (m + 2 * BM - 1) / (2 * BM), tiles_n = (n2 + kWideBN - 1) / kWideBN;
-    const int id = blockIdx.x >> 1;
+    const int ntiles = tiles_m * tiles_n;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
     const int group = kGroupM * tiles_n;
-    const int first_m = (id / group) * kGroupM;
-    const int gsize = min(tiles_m - first_m, kGroupM);
+    auto tile_coords = [&](int t, int& m_blk, int& n_blk) {
+        const int first_m = (t / group) * kGroupM;
+        const int gsize = min(tiles_m - first_m, kGroupM);
+        m_blk = first_m + (t % group) % gsize;
+        n_blk = (t % group) / gsize;
+    };
+
+    const int nkb = kp / T::kBK;
+    const int F = flush_kblocks > 0 ? flush_kblocks : nkb;
+    const int nchunks = (nkb + F - 1) / F;
+    const uint32_t cta_bytes = uint32_t(corrected ? 4 : 2) * kTileBytes;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kWideStages; ++s) {
+            mbar_init(&tail->full[s], 1);
+            mbar_init(&tail->empty[s], 1);
+        }
+        for (int h = 0; h < 2; ++h) {
+            mbar_init(&tail->tfull[h], 1);
+            mbar_init(&tail->tempty[h], kEpiWarps);  // 4 warps per CTA drain a half, 2 CTAs
+        }
+        mbar_init(&tail->cfull, 1);
+        mbar_init(&tail->cempty, 2 * kEpiWarps);
+        fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&mp.ahi);
+        tma_prefetch(&mp.bhi);
+        if (corrected) {
+            tma_prefetch(&mp.alo);
+            tma_prefetch(&mp.blo);
+        }
+    }
+    if (warp == 1) tmem_alloc_pair<kTmemCols>(&tail->tmem_base);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = tail->tmem_base;
+
+    if (warp == 0) {
+        // -------------------------------------------- TMA producer (both CTAs)
+        if (lane == 0) {
+            int it = 0;
+            for (int t = pair; t < ntiles; t += npairs) {
+                int m_blk, n_blk;
+                tile_coords(t, m_blk, n_blk);
+                const int m0 = m_blk * 2 * BM + int(rank) * BM;
+                const int nb0 = n_blk * kWideBN + 128 * int(rank);
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int s = it % kWideStages;
+                    mbar_wait(&tail->empty[s], ((it / kWideStages) & 1) ^ 1);
+                    if (leader) mbar_expect_tx(&tail->full[s], 2 * cta_bytes);
+                    const int kx = kb * T::kBK;
+                    tma_load_2d_pair(tile(s, 0), &mp.ahi, &tail->full[s], kx, m0);
+                    tma_load_2d_pair(tile(s, 2), &mp.bhi, &tail->full[s], kx, nb0);
+                    if (corrected) {
+                        tma_load_2d_pair(tile(s, 1), &mp.alo, &tail->full[s], kx, m0);
+                        tma_load_2d_pair(tile(s, 3), &mp.blo, &tail->full[s], kx, nb0);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------------------------------- MMA issuer (pair leader only)
+        if (leader) {
+            int it = 0, gc = 0, lt = 0;
+            for (int t = pair; t < ntiles; t += npairs, ++lt) {
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const bool chunk_start = (kb % F) == 0;
+                    const bool chunk_end = (kb % F) == F - 1 || kb == nkb - 1;
+                    const int s = it % kWideStages;
+                    mbar_wait(&tail->full[s], (it / kWideStages) & 1);
+                    tc_fence_after();
+                    const uint64_t dah = umma_desc_k_sw128(tile(s, 0));
+                    const uint64_t dal = umma_desc_k_sw128(tile(s, 1));
+                    const uint64_t dbh = umma_desc_k_sw128(tile(s, 2));
+                    const uint64_t dbl = umma_desc_k_sw128(tile(s, 3));
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (chunk_start && gc > 0) {
+                            mbar_wait(&tail->tempty[h], (gc - 1) & 1);
+                            tc_fence_after();
+                        }
+                        // B rows 64h.. of each CTA's tile: 64 rows x 128 B = 8 KB (>> 4 = 512)
+                        const uint64_t dbh_h = dbh + uint64_t(512 * h);
+                        if (elect_one()) {
+#pragma unroll
+                            for (int ks = 0; ks < T::kKSteps; ++ks) {
+                                const uint64_t adv = uint64_t((ks * T::kUK * T::kElem) >> 4);
+                                const uint32_t acc = (!chunk_start || ks > 0) ? 1u : 0u;
+                                if (FMT == kFp16)
+                                    mma2_f16(tmem + uint32_t(128 * h), dah + adv, dbh_h + adv, kIdescHalf, acc);
+                                else
+                                    mma2_tf32(tmem + uint32_t(128 * h), dah + adv, dbh_h + adv, kIdescHalf, acc);
+                            }
+                            if (chunk_end) mma_commit_pair(&tail->tfull[h], 0x3);
+                        }
+                        __syncwarp();
+                    }
+                    if (chunk_end) ++gc;
+                    if (corrected && kb == 0 && lt > 0) {
+                        // the epilogue has read the previous tile's correction accumulator
+                        mbar_wait(&tail->cempty, (lt - 1) & 1);
+                        tc_fence_after();
+                    }
+                    if (elect_one()) {
+                        if (corrected) {
+#pragma unroll
+                            for (int ks = 0; ks < T::kKSteps; ++ks) {
+                                const uint64_t adv = uint64_t((ks * T::kUK * T::kElem) >> 4);
+                                const uint32_t acc = (kb > 0 || ks > 0) ? 1u : 0u;
+                                if (FMT == kFp16) {
+                                    mma2_f16(tmem + 256u, dal + adv, dbh + adv, kIdescFull, acc);
+                                    mma2_f16(tmem + 256u, dah + adv, dbl + adv, kIdescFull, 1u);
+                                } else {
+                                    mma2_tf32(tmem + 256u, dal + adv, dbh + adv, kIdescFull, acc);
+                                    mma2_tf32(tmem + 256u, dah + adv, dbl + adv, kIdescFull, 1u);
+                                }
+                            }
+                        }
+                        mma_commit_pair(&tail->empty[s], 0x3);
+                        if (kb == nkb - 1) mma_commit_pair(&tail->cfull, 0x3);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------ epilogue (both CTAs)
+        // warp w: TMEM lane quadrant q = w % 4, main half p; it owns C' columns
+        // n0 + 64p + [0,64) (acc[0..63]) and n0 + 128 + 64p + [0,64) (acc[64..127])
+        const int q = warp & 3;
+        const int p = (warp - 2) >> 2;
+        const uint32_t lane_base = tmem + (uint32_t(32 * q) << 16);
+        const uint32_t tempty_leader = mapa_shared(smem_u32(&tail->tempty[p]), 0);
+        const uint32_t cempty_leader = mapa_shared(smem_u32(&tail->cempty), 0);
+        const bool scaled = kind == kKindFp16Scaled && (dec->scale_a + dec->scale_b) != 0;
+        const double f = scaled ? ldexp(1.0, -(dec->scale_a + dec->scale_b)) : 1.0;
+        int gc = 0, lt = 0;
+        for (int t = pair; t < ntiles; t += npairs, ++lt) {
+            int m_blk, n_blk;
+            tile_coords(t, m_blk, n_blk);
+            float acc[128];
+#pragma unroll
+            for (int i = 0; i < 128; ++i) acc[i] = -0.0f;  // RN identity
+            for (int ch = 0; ch < nchunks; ++ch, ++gc) {
+                mbar_wait(&tail->tfull[p], gc & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int cb = 0; cb < 8; ++cb) {
+                    float v[16];
+                    tmem_ld16(lane_base + uint32_t(128 * p + 16 * cb), v);
+                    if (cb == 7) {
+                        // the partial is in registers: hand the TMEM half back
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_cluster(tempty_leader);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) acc[16 * cb + i] = __fadd_rn(acc[16 * cb + i], v[i]);
+                }
+            }
+            mbar_wait(&tail->cfull, lt & 1);
+            tc_fence_after();
+            if (corrected) {
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+                    for (int cb = 0; cb < 4; ++cb) {
+                        float v[16];
+                        tmem_ld16(lane_base + 256u + uint32_t(128 * hh + 64 * p + 16 * cb), v);
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            float& a = acc[64 * hh + 16 * cb + i];
+                            a = __fadd_rn(a, __fmul_rn(v[i], 0x1.0p-11f));
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(cempty_leader);
+            if (scaled) {
+#pragma unroll
+                for (int i = 0; i < 128; ++i) acc[i] = scale_pow2(acc[i], f);
+            }
+            // store through a 32-row smem stage, one lane quadrant at a time:
+            // the quadrant's two warps write their rows, then all eight warps
+            // store 4 rows each as coalesced 1 KB rows
+            const int m0 = m_blk * 2 * BM + int(rank) * BM;
+            const int n0 = n_blk * kWideBN;
+            const int ew = warp - 2;
+            const bool full_cols = n0 + kWideBN <= n2 && (n2 & 3) == 0;
+#pragma unroll 1
+            for (int qq = 0; qq < 4; ++qq) {
+                if (q == qq) {
+                    float* myrow = cstage + size_t(lane) * kWideCStride;
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                        for (int i = 0; i < 64; i += 4)
+                            *reinterpret_cast<float4*>(myrow + 128 * hh + 64 * p + i) =
+                                make_float4(acc[64 * hh + i], acc[64 * hh + i + 1], acc[64 * hh + i + 2],
+                                            acc[64 * hh + i + 3]);
+                }
+                epi_bar_sync();
+#pragma unroll
+                for (int rr = 0; rr < 4; ++rr) {
+                    const int r = 4 * ew + rr;
+                    const int grow = m0 + 32 * qq + r;
+                    if (grow < m) {
+                        float* dst = c + size_t(grow) * n2 + n0;
+                        const float* srow = cstage + size_t(r) * kWideCStride;
+                        if (full_cols) {
+                            __stcs(reinterpret_cast<float4*>(dst) + lane, reinterpret_cast<const float4*>(srow)[lane]);
+                            __stcs(reinterpret_cast<float4*>(dst) + lane + 32,
+                                   reinterpret_cast<const float4*>(srow)[lane + 32]);
+                        } else {
+                            for (int i = lane; i < kWideBN; i += 32)
+                                if (n0 + i < n2) dst[i] = srow[i];
+                        }
+                    }
+                }
+                epi_bar_sync();
+            }
+        }
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_pair<kTmemCols>(tmem);
+    }
+}
+
+// host-known format
+template <int FMT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
+    tcec_gemm_widep_kernel(const __grid_constant__ WideMaps maps, float* __restrict__ c, int m,
+                          int n2, int kp, const DevDecision* __restrict__ dec, int kind_fixed,
+                          int corrected, int flush_kblocks) {
+    const int kind = kind_fixed >= 0 ? kind_fixed : dec->kind;
+    const bool mine = FMT == kTf32 ? kind == kKindTf32 : (kind == kKindFp16 || kind == kKindFp16Scaled);
+    if (!mine) return;
+    widep_body<FMT>(maps, c, m, n2, kp, dec, kind, corrected, flush_kblocks);
+}
+
+// format decided on the device (AUTO): one launch that runs the selected
+// format (instead of launching both and letting one exit)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
+    tcec_gemm_widep_auto_kernel(const __grid_constant__ WideMaps maps16,
+                               const __grid_constant__ WideMaps maps32, float* __restrict__ c,
+                               int m, int n2, int kp, const DevDecision* __restrict__ dec,
+                               int corrected, int flush_kblocks) {
+    const int kind = dec->kind;
+    if (kind == kKindTf32)
+        widep_body<kTf32>(maps32, c, m, n2, kp, dec, kind, corrected, flush_kblocks);
+    else if (kind == kKindFp16 || kind == kKindFp16Scaled)
+        widep_body<kFp16>(maps16, c, m, n2, kp, dec, kind, corrected, flush_kblocks);
+}
+
+// ===================================================================== wide pair
+// cta_group::2 kernel with a 256 x 256 tile of C' per CTA pair (128 x 256 per
+// CTA), one tile per cluster (variant 3, the default for large shapes).  Per
+// k-block each CTA stages A_hi/A_lo (its 128 rows) and B_hi/B_lo (its 128 of
+// the pair's 256 columns): 64 KB for 3 x 128x256x64 MACs, half the operand
+// bytes per MAC of the 128 x 128 kernel, so neither the L2->SM feed nor
+// shared-memory bandwidth paces the tensor pipe.  TMEM: main partial as two
+// 128-column halves (issued and committed per half, N = 128 MMAs, drained by
+// the epilogue while the tensor core runs the other half and the N = 256
+// correction products), correction accumulator in cols 256..511.
+// Column maps (CTA r of the pair holds B rows n0 + 128 r + [0,128)):
+//   main half h, TMEM col j:  j < 64 -> n0 + 64h + j,  j >= 64 -> n0 + 128 + 64h + (j-64)
+//   corr, TMEM col 256 + j:   n0 + j
+constexpr int kNpStages = 3;
+constexpr int kNpBN = 256;
+constexpr int kNpStageBytes = 4 * kTileBytes;  // A_hi | A_lo | B_hi | B_lo, 16 KB each
+constexpr int kNpCStride = kNpBN + 4;
+struct alignas(8) NpSmemTail {
+    uint64_t full[kNpStages];
+    uint64_t empty[kNpStages];
+    uint64_t tfull[2];
+    uint64_t tempty[2];
+    uint64_t cfull;
+    uint32_t tmem_base;
+};
+constexpr size_t kNpSmemBytes = 1024 + size_t(kNpStages) * kNpStageBytes + sizeof(NpSmemTail);
+static_assert(size_t(BM) * kNpCStride * 4 <= size_t(kNpStages) * kNpStageBytes,
+              "C staging tile must fit in the operand stages");
+
+template <int FMT>
+__device__ __forceinline__ void wide_body(const WideMaps& mp, float* __restrict__ c, int m, int n2,
+                                          int kp, const DevDecision* __restrict__ dec, int kind,
+                                          int corrected, int flush_kblocks, int group_m) {
+    using T = Traits<FMT>;
+    constexpr uint32_t kIdescHalf = umma_idesc<FMT, 2 * BM, 128>();
+    constexpr uint32_t kIdescFull = umma_idesc<FMT, 2 * BM, kNpBN>();
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    NpSmemTail* tail =
+        reinterpret_cast<NpSmemTail*>(smem + size_t(kNpStages) * kNpStageBytes);
+    auto tile = [&](int s, int which) -> uint8_t* {
+        return smem + size_t(s) * kNpStageBytes + size_t(which) * kTileBytes;
+    };
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+
+    const int tiles_m = (m + 2 * BM - 1) / (2 * BM), tiles_n = (n2 + kNpBN - 1) / kNpBN;
+    const int id = blockIdx.x >> 1;
+    const int group = group_m * tiles_n;
+    const int first_m = (id / group) * group_m;
+    const int gsize = min(tiles_m - first_m, group_m);
     const int m_blk = first_m + (id % group) % gsize;
     const int n_blk = (id % group) / gsize;
     const int m0 = m_blk * 2 * BM + int(rank) * BM;  // this CTA's 128 rows
-    const int n0 = n_blk * kWideBN;                  // the pair's 256 columns
+    const int n0 = n_blk * kNpBN;                  // the pair's 256 columns
 
     const int nkb = kp / T::kBK;
     const int F = flush_kblocks > 0 ? flush_kblocks : (nkb > 0 ? nkb : 1);
@@ -568,7 +894,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
     const uint32_t cta_bytes = uint32_t(corrected ? 4 : 2) * kTileBytes;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kWideStages; ++s) {
+        for (int s = 0; s < kNpStages; ++s) {
             mbar_init(&tail->full[s], 1);
             mbar_init(&tail->empty[s], 1);
         }
@@ -580,11 +906,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
         fence_barrier_init();
     }
     if (warp == 0 && lane == 0) {
-        tma_prefetch(&map_ahi);
-        tma_prefetch(&map_bhi);
+        tma_prefetch(&mp.ahi);
+        tma_prefetch(&mp.bhi);
         if (corrected) {
-            tma_prefetch(&map_alo);
-            tma_prefetch(&map_blo);
+            tma_prefetch(&mp.alo);
+            tma_prefetch(&mp.blo);
         }
     }
     if (warp == 1) tmem_alloc_pair<kTmemCols>(&tail->tmem_base);
@@ -598,15 +924,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
         if (lane == 0) {
             const int nb0 = n0 + 128 * int(rank);
             for (int kb = 0; kb < nkb; ++kb) {
-                const int s = kb % kWideStages;
-                mbar_wait(&tail->empty[s], ((kb / kWideStages) & 1) ^ 1);
+                const int s = kb % kNpStages;
+                mbar_wait(&tail->empty[s], ((kb / kNpStages) & 1) ^ 1);
                 if (leader) mbar_expect_tx(&tail->full[s], 2 * cta_bytes);
                 const int kx = kb * T::kBK;
-                tma_load_2d_pair(tile(s, 0), &map_ahi, &tail->full[s], kx, m0);
-                tma_load_2d_pair(tile(s, 2), &map_bhi, &tail->full[s], kx, nb0);
+                tma_load_2d_pair(tile(s, 0), &mp.ahi, &tail->full[s], kx, m0);
+                tma_load_2d_pair(tile(s, 2), &mp.bhi, &tail->full[s], kx, nb0);
                 if (corrected) {
-                    tma_load_2d_pair(tile(s, 1), &map_alo, &tail->full[s], kx, m0);
-                    tma_load_2d_pair(tile(s, 3), &map_blo, &tail->full[s], kx, nb0);
+                    tma_load_2d_pair(tile(s, 1), &mp.alo, &tail->full[s], kx, m0);
+                    tma_load_2d_pair(tile(s, 3), &mp.blo, &tail->full[s], kx, nb0);
                 }
             }
         }
@@ -617,8 +943,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
                 const int chunk = kb / F;
                 const bool chunk_start = (kb % F) == 0;
                 const bool chunk_end = (kb % F) == F - 1 || kb == nkb - 1;
-                const int s = kb % kWideStages;
-                mbar_wait(&tail->full[s], (kb / kWideStages) & 1);
+                const int s = kb % kNpStages;
+                mbar_wait(&tail->full[s], (kb / kNpStages) & 1);
                 tc_fence_after();
                 const uint64_t dah = umma_desc_k_sw128(tile(s, 0));
                 const uint64_t dal = umma_desc_k_sw128(tile(s, 1));
@@ -683,17 +1009,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
             mbar_wait(&tail->tfull[p], ch & 1);
             tc_fence_after();
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                float v[64];
-                tmem_ld64(lane_base + uint32_t(128 * p + 64 * hh), v);
-                if (hh == 1) {
+            for (int cb = 0; cb < 8; ++cb) {
+                float v[16];
+                tmem_ld16(lane_base + uint32_t(128 * p + 16 * cb), v);
+                if (cb == 7) {
                     // the partial is in registers: hand the TMEM half back
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cluster(tempty_leader);
                 }
 #pragma unroll
-                for (int i = 0; i < 64; ++i) acc[64 * hh + i] = __fadd_rn(acc[64 * hh + i], v[i]);
+                for (int i = 0; i < 16; ++i) acc[16 * cb + i] = __fadd_rn(acc[16 * cb + i], v[i]);
             }
         }
         if (nkb > 0) {
@@ -723,7 +1049,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
         }
         // stage the 128 x 256 tile in the idle operand smem, then store rows
         float* ctile = reinterpret_cast<float*>(smem);
-        float* myrow = ctile + size_t(rloc) * kWideCStride;
+        float* myrow = ctile + size_t(rloc) * kNpCStride;
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh)
 #pragma unroll
@@ -733,18 +1059,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
                                 acc[64 * hh + i + 3]);
         epi_bar_sync();
         const int ew = warp - 2;
-        const bool full_cols = n0 + kWideBN <= n2 && (n2 & 3) == 0;
+        const bool full_cols = n0 + kNpBN <= n2 && (n2 & 3) == 0;
         for (int r = ew; r < BM; r += kEpiWarps) {
             const int grow = m0 + r;
             if (grow >= m) break;
             float* dst = c + size_t(grow) * n2 + n0;
-            const float* srow = ctile + size_t(r) * kWideCStride;
+            const float* srow = ctile + size_t(r) * kNpCStride;
             if (full_cols) {
                 reinterpret_cast<float4*>(dst)[lane] = reinterpret_cast<const float4*>(srow)[lane];
                 reinterpret_cast<float4*>(dst)[lane + 32] =
                     reinterpret_cast<const float4*>(srow)[lane + 32];
             } else {
-                for (int i = lane; i < kWideBN; i += 32)
+                for (int i = lane; i < kNpBN; i += 32)
                     if (n0 + i < n2) dst[i] = srow[i];
             }
         }
@@ -755,6 +1081,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
         tc_fence_after();
         tmem_dealloc_pair<kTmemCols>(tmem);
     }
+}
+
+// host-known format
+template <int FMT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
+    tcec_gemm_wide_kernel(const __grid_constant__ WideMaps maps, float* __restrict__ c, int m,
+                          int n2, int kp, const DevDecision* __restrict__ dec, int kind_fixed,
+                          int corrected, int flush_kblocks, int group_m) {
+    const int kind = kind_fixed >= 0 ? kind_fixed : dec->kind;
+    const bool mine = FMT == kTf32 ? kind == kKindTf32 : (kind == kKindFp16 || kind == kKindFp16Scaled);
+    if (!mine) return;  // both CTAs of the pair read the same decision
+    wide_body<FMT>(maps, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m);
+}
+
+// format decided on the device (AUTO): one launch that runs the selected
+// format instead of launching both and letting one exit
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
+    tcec_gemm_wide_auto_kernel(const __grid_constant__ WideMaps maps16,
+                               const __grid_constant__ WideMaps maps32, float* __restrict__ c,
+                               int m, int n2, int kp, const DevDecision* __restrict__ dec,
+                               int corrected, int flush_kblocks, int group_m) {
+    const int kind = dec->kind;
+    if (kind == kKindTf32)
+        wide_body<kTf32>(maps32, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m);
+    else if (kind == kKindFp16 || kind == kKindFp16Scaled)
+        wide_body<kFp16>(maps16, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -788,6 +1140,36 @@ bool make_map(CUtensorMap* map, const void* base, int fmt, int64_t rows, int64_t
     return r == CUDA_SUCCESS;
 }
 
+bool make_wide_maps(WideMaps* w, const TcecGemmArgs& g, int fmt) {
+    const void* alo = g.corrected ? g.a_lo : g.a_hi;
+    const void* blo = g.corrected ? g.b_lo : g.b_hi;
+    return make_map(&w->ahi, g.a_hi, fmt, g.m, g.kp, 128u) && make_map(&w->alo, alo, fmt, g.m, g.kp, 128u) &&
+           make_map(&w->bhi, g.b_hi, fmt, g.n2, g.kp, 128u) && make_map(&w->blo, blo, fmt, g.n2, g.kp, 128u);
+}
+
+// rasterization group (M tiles per group) of the wide kernel; TCEC_GROUP_M
+// overrides it for tuning
+int wide_group_m() {
+    static const int g = [] {
+        const char* e = std::getenv("TCEC_GROUP_M");
+        const int v = e ? std::atoi(e) : 0;
+        return v > 0 ? v : kWideGroupM;
+    }();
+    return g;
+}
+
+// one cluster per 256 x 256 tile
+unsigned wide_tiles_grid(const TcecGemmArgs& g) {
+    return unsigned(2 * ((g.m + 2 * BM - 1) / (2 * BM)) * ((g.n2 + kWideBN - 1) / kWideBN));
+}
+
+// persistent grid: one CTA pair per two SMs, never more pairs than tiles
+unsigned wide_grid(const TcecGemmArgs& g) {
+    const int64_t tiles = ((g.m + 2 * BM - 1) / (2 * BM)) * ((g.n2 + kWideBN - 1) / kWideBN);
+    const int64_t pairs = std::max<int64_t>(1, std::min<int64_t>(tiles, (g.sms > 1 ? g.sms : 148) / 2));
+    return unsigned(2 * pairs);
+}
+
 template <int FMT>
 int launch_fmt(const TcecGemmArgs& g, cudaStream_t s) {
     static bool attr_set = false;
@@ -800,9 +1182,24 @@ int launch_fmt(const TcecGemmArgs& g, cudaStream_t s) {
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPairSmemBytes));
         if (e != cudaSuccess) return int(e);
         e = cudaFuncSetAttribute(tcec_gemm_wide_kernel<FMT>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNpSmemBytes));
+        if (e != cudaSuccess) return int(e);
+        e = cudaFuncSetAttribute(tcec_gemm_widep_kernel<FMT>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(kWideSmemBytes));
         if (e != cudaSuccess) return int(e);
         attr_set = true;
+    }
+    if (g.pair == kVariantWide || g.pair == kVariantWidePersistent) {
+        WideMaps w;
+        if (!make_wide_maps(&w, g, FMT)) return int(cudaErrorInvalidValue);
+        if (g.pair == kVariantWide)
+            tcec_gemm_wide_kernel<FMT><<<wide_tiles_grid(g), kThreadsGemm, kNpSmemBytes, s>>>(
+                w, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed, g.corrected, g.flush_kblocks,
+                wide_group_m());
+        else
+            tcec_gemm_widep_kernel<FMT><<<wide_grid(g), kThreadsGemm, kWideSmemBytes, s>>>(
+                w, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed, g.corrected, g.flush_kblocks);
+        return int(cudaGetLastError());
     }
     CUtensorMap mah, mal, mbh, mbl;
     const void* alo = g.corrected ? g.a_lo : g.a_hi;
@@ -812,12 +1209,7 @@ int launch_fmt(const TcecGemmArgs& g, cudaStream_t s) {
         !make_map(&mbh, g.b_hi, FMT, g.n2, g.kp, b_box) ||
         !make_map(&mbl, blo, FMT, g.n2, g.kp, b_box))
         return int(cudaErrorInvalidValue);
-    if (g.pair == kVariantWide) {
-        const int64_t tiles = ((g.m + 2 * BM - 1) / (2 * BM)) * ((g.n2 + kWideBN - 1) / kWideBN);
-        tcec_gemm_wide_kernel<FMT><<<unsigned(2 * tiles), kThreadsGemm, kWideSmemBytes, s>>>(
-            mah, mal, mbh, mbl, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed,
-            g.corrected, g.flush_kblocks);
-    } else if (g.pair == kVariantPair) {
+    if (g.pair == kVariantPair) {
         const int64_t tiles = ((g.m + 2 * BM - 1) / (2 * BM)) * ((g.n2 + BN - 1) / BN);
         tcec_gemm_pair_kernel<FMT><<<unsigned(2 * tiles), kThreadsGemm, kPairSmemBytes, s>>>(
             mah, mal, mbh, mbl, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed,
@@ -828,6 +1220,31 @@ int launch_fmt(const TcecGemmArgs& g, cudaStream_t s) {
             mah, mal, mbh, mbl, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed,
             g.corrected, g.flush_kblocks);
     }
+    return int(cudaGetLastError());
+}
+
+// format decided on the device: one wide launch that runs the selected format
+int launch_wide_auto(const TcecGemmArgs& g, cudaStream_t s) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(tcec_gemm_wide_auto_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNpSmemBytes));
+        if (e != cudaSuccess) return int(e);
+        e = cudaFuncSetAttribute(tcec_gemm_widep_auto_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(kWideSmemBytes));
+        if (e != cudaSuccess) return int(e);
+        attr_set = true;
+    }
+    WideMaps w16, w32;
+    if (!make_wide_maps(&w16, g, kFp16) || !make_wide_maps(&w32, g, kTf32))
+        return int(cudaErrorInvalidValue);
+    if (g.pair == kVariantWide)
+        tcec_gemm_wide_auto_kernel<<<wide_tiles_grid(g), kThreadsGemm, kNpSmemBytes, s>>>(
+            w16, w32, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.corrected, g.flush_kblocks,
+            wide_group_m());
+    else
+        tcec_gemm_widep_auto_kernel<<<wide_grid(g), kThreadsGemm, kWideSmemBytes, s>>>(
+            w16, w32, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.corrected, g.flush_kblocks);
     return int(cudaGetLastError());
 }
 
@@ -842,6 +1259,13 @@ int resolve_gemm_variant(int requested, int64_t m, int64_t n2, int sm_count) {
 int launch_tcec_gemm(const TcecGemmArgs& g, cudaStream_t s) {
     if (!get_encode()) return int(cudaErrorNotSupported);
     if (g.m <= 0 || g.n2 <= 0) return 0;
+    if (g.fmt < 0) {
+        // device-decided format: the wide kernel branches on the decision; the
+        // other variants launch both formats and the unselected one exits
+        if (g.pair == kVariantWide || g.pair == kVariantWidePersistent) return launch_wide_auto(g, s);
+        const int e = launch_fmt<kFp16>(g, s);
+        return e ? e : launch_fmt<kTf32>(g, s);
+    }
     return g.fmt == kFp16 ? launch_fmt<kFp16>(g, s) : launch_fmt<kTf32>(g, s);
 }
 

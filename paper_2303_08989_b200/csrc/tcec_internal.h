@@ -84,14 +84,15 @@ struct TcecGemmArgs {
     int64_t m, n2, kp;
     const DevDecision* d;                 // device decision (kind / shifts)
     int kind_fixed;                       // >= 0: host-known kind; -1: read d->kind
-    int fmt;                              // 0 = f16 kernel, 1 = tf32 kernel
+    int fmt;                              // 0 = f16 kernel, 1 = tf32 kernel, -1 = device-decided
     int corrected;                        // 1 = TCEC (3 products), 0 = TC ablation
     int flush_kblocks;                    // RN flush interval of the main term, 0 = none
     int pair;                             // resolved kernel variant (kVariantSingle/Pair/Wide)
+    int sms;                              // SM count (persistent grid size)
 };
 // tcgen05 kernel variants (tcec_set_gemm_variant): auto picks wide when its
 // 256 x 256 pair tiles fill the SMs, else single
-enum GemmVariant : int { kVariantAuto = 0, kVariantPair = 1, kVariantSingle = 2, kVariantWide = 3 };
+enum GemmVariant : int { kVariantAuto = 0, kVariantPair = 1, kVariantSingle = 2, kVariantWide = 3, kVariantWidePersistent = 4 };
 int resolve_gemm_variant(int requested, int64_t m, int64_t n2, int sm_count);
 // returns a cudaError_t
 int launch_tcec_gemm(const TcecGemmArgs& args, cudaStream_t s);

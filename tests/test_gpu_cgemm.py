@@ -87,7 +87,7 @@ def test_tcec_ragged_shapes(handle, orc, dev, shape):
         assert e <= max(TOL_FACTOR * err_ref, 2e-7), (mode, e, err_ref)
 
 
-@pytest.mark.parametrize("variant", ["single", "pair", "wide"])
+@pytest.mark.parametrize("variant", ["single", "pair", "wide", "wide_persistent"])
 @pytest.mark.parametrize("shape", [(3, 5, 7), (129, 65, 200), (300, 257, 31), (513, 385, 129),
                                    (130, 130, 1100), (600, 300, 2100)])
 def test_tcec_kernel_variants(handle, orc, dev, variant, shape):
@@ -114,7 +114,7 @@ def test_tcec_kernel_variants(handle, orc, dev, variant, shape):
         assert errs["FP16TC"] >= 10 * errs["FP16TCEC"], errs
 
 
-@pytest.mark.parametrize("variant", ["single", "wide"])
+@pytest.mark.parametrize("variant", ["single", "wide", "wide_persistent"])
 def test_tcec_all_positive_long_k(handle, orc, dev, variant):
     """All-positive operands make tensor-core truncation a systematic bias;
     the per-k-block RN flush keeps TCEC within the reference bar."""
