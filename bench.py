@@ -681,6 +681,107 @@ def run_skewed(args):
     h.close()
 
 
+def contract_c128(spec, path, dev):
+    """complex128 contraction of a NetworkSpec along an SSA path (torch on the
+    GPU): the fidelity reference of the deep-circuit study.  Same label order
+    as ttgt_contract (free_a | free_b, network.cpp:58-85)."""
+    import torch
+    live = {i: (list(ls), torch.from_numpy(np.asarray(d, np.complex64).reshape(ds if ds else [1])
+                                           ).to(dev, torch.complex128).reshape(ds if ds else []))
+            for i, (ls, ds, d) in enumerate(zip(spec.labels, spec.dims, spec.data))}
+    nxt = len(spec.labels)
+    for ia, ib in path:
+        la, ta = live.pop(ia)
+        lb, tb = live.pop(ib)
+        shared = [l for l in la if l in lb]
+        ia_ax = [la.index(l) for l in shared]
+        ib_ax = [lb.index(l) for l in shared]
+        t = torch.tensordot(ta, tb, dims=(ia_ax, ib_ax))
+        live[nxt] = ([l for l in la if l not in shared] + [l for l in lb if l not in shared], t)
+        nxt += 1
+    (_, t), = live.values()
+    return complex(t.reshape(-1)[0].item())
+
+
+def run_rqc7x7(args):
+    """configs[4]: deep-circuit fidelity study -- 7x7 rectangular RQC with increasing
+    CZ depth, the reference's greedy path, AUTO-selected precision (default policy
+    and a lowered policy that engages the tensor cores on more steps) against the
+    FP32 baseline tier and a complex128 contraction of the same path."""
+    import torch
+    from paper_2303_08989_b200 import Handle, SelectionPolicy, make_config
+    from paper_2303_08989_b200.circuits import bitstrings_for, circuit_to_network, rqc_rectangular
+    from paper_2303_08989_b200.network import Network
+    from paper_2303_08989_b200.slicing import contraction_cost
+    world, rank, local = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    h = Handle(local)
+    depths = [int(d) for d in args.depths.split(",")]
+    nbits = 10
+    modes = [("AUTO-0", make_config()),
+             ("AUTO-0-lowered", make_config(SelectionPolicy(size_auto=256, size_tf32=64))),
+             ("FP32_BASELINE", make_config(force="FP32_REF"))]
+    rows_out = []
+    with ClockSampler(local) as clk:
+        for depth in depths:
+            circ = rqc_rectangular(7, 7, depth, 1)
+            xs = bitstrings_for(49, nbits, 1)[rank::world] or bitstrings_for(49, nbits, 1)[:1]
+            spec = circuit_to_network(circ, xs[0])
+            net = Network(h, spec)
+            path = net.greedy_path()
+            big, macs = contraction_cost(spec, path)
+            ref = np.array([contract_c128(circuit_to_network(circ, x), path, dev) for x in xs])
+            torch.cuda.empty_cache()
+            row = {"depth": depth, "steps": len(path), "max_intermediate": int(big),
+                   "gflop_per_amplitude": round(8.0 * macs / 1e9, 2), "modes": {}}
+            for label, cfg in modes:
+                _, lines = net.contract(path, cfg, want_log=True)
+                hist = {}
+                for ln in lines:
+                    kk = ln.split(",")[3]
+                    hist[kk] = hist.get(kk, 0) + 1
+                net.selector_batch(path, xs[:1], cfg)  # capture / warm
+                reps = max(1, args.steps // 5)
+                torch.cuda.synchronize(dev)
+                t0 = time.perf_counter()
+                for _ in range(reps):
+                    amps = net.selector_batch(path, xs, cfg)
+                ms = (time.perf_counter() - t0) / (reps * len(xs)) * 1e3
+                err = np.abs(amps.astype(np.complex128) - ref) / np.abs(ref)
+                row["modes"][label] = {"ms_per_amplitude": round(ms, 3),
+                                       "median_rel_err_vs_c128": float(np.median(err)),
+                                       "max_rel_err_vs_c128": float(np.max(err)),
+                                       "decisions": hist}
+            a, f = row["modes"]["AUTO-0"], row["modes"]["FP32_BASELINE"]
+            row["auto_speedup_vs_fp32_baseline"] = round(f["ms_per_amplitude"] / a["ms_per_amplitude"], 3)
+            row["auto_err_ratio_vs_fp32_baseline"] = (round(a["median_rel_err_vs_c128"] /
+                                                            f["median_rel_err_vs_c128"], 3)
+                                                      if f["median_rel_err_vs_c128"] else None)
+            if rank == 0 and not args.no_cpu and depth <= 12:
+                thr = os.cpu_count() or 1
+                bits = np.array(xs[:min(len(xs), thr)], np.uint8)
+                r = rqc_reference_rate(bits, 49, 7, 7, depth, 1, thr)
+                if r is not None:
+                    row["cpu_reference_ms_per_amplitude"] = round(1e3 / r[0], 3)
+                    row["cpu_reference_threads"] = thr
+            net.close()
+            rows_out.append(row)
+    if rank == 0:
+        deep = rows_out[-1]["modes"]["AUTO-0"]["ms_per_amplitude"]
+        line = {"metric": f"RCS 7x7 deep-circuit amplitude time (AUTO-0, depth {depths[-1]})",
+                "value": deep, "unit": "ms/amplitude", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": deep, "higher_is_better": False,
+                "scaling": "strong", "vs_baseline": None, "dtype": "c64 (AUTO-0 tiers)",
+                "data": "synthetic circuits rqc_rectangular(7, 7, d, 1), 10 bitstrings (experiments.cpp:185-196)",
+                "config": {"workload": "configs[4] deep-circuit fidelity study, reference greedy path",
+                           "fidelity_reference": "complex128 contraction of the same path (torch, GPU)",
+                           "parallelism": f"bitstrings / {world}"},
+                "depths": rows_out, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    h.close()
+
+
 def gemm_kernel_name(m, n, kind, sm_count=148, auto=True):
     """The tcgen05 kernel an AUTO dispatch runs (resolve_gemm_variant in tcec_gemm.cu):
     the wide cta_group::2 kernel branching on the device decision when its tiles
@@ -694,8 +795,9 @@ def gemm_kernel_name(m, n, kind, sm_count=148, auto=True):
 
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("--workload", choices=["cgemm", "rqc", "sycamore", "skewed"], default="cgemm")
+    p.add_argument("--workload", choices=["cgemm", "rqc", "sycamore", "skewed", "rqc7x7"], default="cgemm")
     p.add_argument("--cycles", type=int, default=10)
+    p.add_argument("--depths", default="4,8,12,14,16")
     p.add_argument("--slices-log2", type=int, default=6)
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
@@ -715,6 +817,8 @@ def main():
         run_sycamore(args)
     elif args.workload == "skewed":
         run_skewed(args)
+    elif args.workload == "rqc7x7":
+        run_rqc7x7(args)
     elif args.impl == "reference":
         run_reference(args)
     else:
