@@ -504,20 +504,40 @@ def run_rqc(args):
     h.close()
 
 
-SYC_METRIC = "Sycamore-class 53q sliced RCS amplitudes/s (m=10, 64 slices, AUTO-0)"
+SYC_METRIC = "Sycamore-class 53q sliced RCS amplitudes/s (AUTO-0)"
+
+
+def load_or_build_plan(spec, cycles, mode, log=None):
+    """Sliced contraction plan: the committed plans/sycamore_m{cycles}.json
+    (made by tools/make_plan.py) when it matches this network, else a fresh
+    hyper_path search (mode "hyper") or the randomized greedy (mode "greedy")."""
+    from paper_2303_08989_b200.paths import hyper_path, random_greedy_path
+    from paper_2303_08989_b200.slicing import find_slices
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from make_plan import spec_hash
+    fn = os.path.join(ROOT, "paper_2303_08989_b200", "plans", f"sycamore_m{cycles}.json")
+    if mode == "plan" and os.path.exists(fn):
+        d = json.load(open(fn))
+        if d["spec_hash"] == spec_hash(spec):
+            return [tuple(x) for x in d["path"]], list(d["sliced"]), f"hyper (cached {os.path.basename(fn)})"
+    if mode == "greedy":
+        path, _, _ = random_greedy_path(spec, trials=64, max_width=30)
+        return path, find_slices(spec, path, n_labels=6), "randomized greedy"
+    path, sliced, _, _ = hyper_path(spec, 28.0, trials=1, log=log)
+    return path, sliced, "hyper (searched)"
 
 
 def run_sycamore(args):
-    """configs[3] class: 53-qubit Sycamore-layout fSim circuit, randomized-greedy
-    path, 6 sliced bonds (64 slices) sharded round-robin over the ranks, one
+    """configs[3]: 53-qubit Sycamore-layout fSim circuit (m cycles), sliced
+    contraction plan (presimplify + partition tree + reconfiguration + exact
+    slicing, paths.hyper_path), slices sharded round-robin over the ranks, one
     NCCL all_gather of the slice values, slice-ordered float64 sum."""
     import torch
     from paper_2303_08989_b200 import Handle, make_config
     from paper_2303_08989_b200.circuits import circuit_to_network, sycamore_like
     from paper_2303_08989_b200.network import Network
-    from paper_2303_08989_b200.paths import random_greedy_path
     from paper_2303_08989_b200.slicing import (SlicePlan, contraction_cost, device_evaluator,
-                                               find_slices, sliced_amplitude)
+                                               sliced_amplitude)
     world, rank, local = dist_setup(args.gpus)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -526,12 +546,13 @@ def run_sycamore(args):
     x = [(q * 7 + 3) % 2 for q in range(circ.n_qubits)]
     spec = circuit_to_network(circ, x)
     t0 = time.perf_counter()
-    path, flops_unsliced, width = random_greedy_path(spec, trials=64, max_width=30)
-    sliced = find_slices(spec, path, n_labels=args.slices_log2)
+    path, sliced, path_kind = load_or_build_plan(spec, cycles, args.path)
     plan = SlicePlan.build(spec, path, sliced)
     plan_s = time.perf_counter() - t0
     big, macs = contraction_cost(spec, path, sliced)
     total_flops = 8.0 * macs * plan.n_slices
+    _, macs_unsliced = contraction_cost(spec, path)
+    width = math.log2(max(1, contraction_cost(spec, path)[0]))
     h = Handle(local)
     stream = torch.cuda.ExternalStream(h.stream_ptr, device=dev)
     net = Network(h, plan.base)
@@ -553,27 +574,26 @@ def run_sycamore(args):
         wall = (time.perf_counter() - tw) / args.steps * 1e3
     ms = max_over_ranks(max(e0.elapsed_time(e1) / args.steps, wall), world)
     if rank == 0:
-        # fidelity: slice 0 against the f64 TTGT oracle on the CPU (bounded)
-        fid = None
-        if not args.no_cpu:
-            from oracle.network import contract_network_f64
-            from paper_2303_08989_b200.slicing import assignment, slice_spec
-            sub = slice_spec(spec, plan.sliced, assignment(0, plan.dims))
-            t1 = time.perf_counter()
-            _, _, z64 = contract_network_f64(sub, path)
-            fid = {"slice0_rel_err_vs_f64": float(abs(complex(full[0]) - complex(z64[0])) /
-                                                  abs(complex(z64[0]))),
-                   "oracle_s": round(time.perf_counter() - t1, 2)}
+        # fidelity: slice 0 against a complex128 contraction of the same path (GPU)
+        from paper_2303_08989_b200.slicing import assignment, slice_spec
+        sub = slice_spec(spec, plan.sliced, assignment(0, plan.dims))
+        t1 = time.perf_counter()
+        z128 = contract_c128(sub, path, dev)
+        torch.cuda.empty_cache()
+        fid = {"slice0_rel_err_vs_c128": float(abs(complex(full[0]) - z128) / abs(z128)),
+               "reference": "complex128 contraction of slice 0 along the same path (torch)",
+               "reference_s": round(time.perf_counter() - t1, 2)}
         line = {
-            "metric": SYC_METRIC, "value": round(1e3 / ms, 4), "unit": "amplitudes/s",
+            "metric": f"{SYC_METRIC[:-9]}, m={cycles}, {plan.n_slices} slices, AUTO-0)", "value": round(1e3 / ms, 4), "unit": "amplitudes/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "c64 (AUTO-0: TF32TCEC / FP16TCEC* / FP32 tiers)",
             "data": f"synthetic circuit sycamore_like({cycles}, 1)",
             "config": {"workload": f"configs[3] class: 53-qubit Sycamore layout, {cycles} fSim cycles, "
                                    f"{plan.n_slices} slices ({len(sliced)} bonds) over {world} GPU(s)",
-                       "path": f"randomized greedy, {len(path)} steps, width 2^{width:.0f} unsliced, "
+                       "path": f"{path_kind}, {len(path)} steps, width 2^{width:.0f} unsliced, "
                                f"2^{math.log2(big):.0f} per slice", "plan_s": round(plan_s, 2),
+                       "flops_unsliced": 8.0 * macs_unsliced,
                        "flops_per_amplitude": total_flops,
                        "collective": "one all_gather of 8 B per slice (NCCL), slice-ordered f64 sum"},
             "achieved_tflops": round(total_flops / (ms * 1e-3) / 1e12, 2),
@@ -796,7 +816,8 @@ def gemm_kernel_name(m, n, kind, sm_count=148, auto=True):
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--workload", choices=["cgemm", "rqc", "sycamore", "skewed", "rqc7x7"], default="cgemm")
-    p.add_argument("--cycles", type=int, default=10)
+    p.add_argument("--cycles", type=int, default=12)
+    p.add_argument("--path", choices=["plan", "hyper", "greedy"], default="plan")
     p.add_argument("--depths", default="4,8,12,14,16")
     p.add_argument("--slices-log2", type=int, default=6)
     p.add_argument("--gpus", type=int, default=1)

@@ -11,7 +11,8 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtcec_b200.so")
+# TCEC_LIB_PATH: A/B of another build of the same C-ABI (development only)
+LIB_PATH = os.environ.get("TCEC_LIB_PATH") or os.path.join(HERE, "libtcec_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "tcec_b200.h")
 
 STATUS = {

@@ -90,6 +90,30 @@ class Handle:
     def synchronize(self) -> None:
         check(self.lib.tcec_synchronize(self.h))
 
+    def _ordered_call(self, fn, *args):
+        """Run one asynchronous device entry point on the handle stream, ordered
+        after the work torch queued on its current stream (the operands) and
+        before anything torch queues next (the results); then check its status."""
+        torch = _torch()
+        ext = self._ext_stream()
+        cur = torch.cuda.current_stream(ext.device)
+        if cur.cuda_stream != ext.cuda_stream:
+            ext.wait_stream(cur)
+        rc = fn(*args)
+        if cur.cuda_stream != ext.cuda_stream:
+            cur.wait_stream(ext)
+        check(rc)
+
+    def _ext_stream(self):
+        """torch view of the handle stream (cached)."""
+        torch = _torch()
+        ptr = self.stream_ptr
+        ext = getattr(self, "_ext", None)
+        if ext is None or ext[0] != ptr:
+            ext = (ptr, torch.cuda.ExternalStream(ptr, device=torch.device("cuda", self.device)))
+            self._ext = ext
+        return ext[1]
+
     @property
     def flush_kblocks(self) -> int:
         return self.lib.tcec_get_flush_kblocks(self.h)
@@ -130,30 +154,30 @@ class Handle:
     def quantize_buf(self, x, fmt: int, rounding: int = 0):
         y = self._out_like(x)
         ovf = C.c_int(0)
-        check(self.lib.tcec_quantize_buf(self.h, _ptr(x), _ptr(y), x.numel(), fmt, rounding,
-                                         C.byref(ovf)))
+        self._ordered_call(self.lib.tcec_quantize_buf, self.h, _ptr(x), _ptr(y), x.numel(), fmt, rounding,
+                                         C.byref(ovf))
         return y, bool(ovf.value)
 
     def split_buf(self, x, fmt: int):
         hi, lo = self._out_like(x), self._out_like(x)
         ovf = C.c_int(0)
-        check(self.lib.tcec_split_buf(self.h, _ptr(x), _ptr(hi), _ptr(lo), x.numel(), fmt,
-                                      C.byref(ovf)))
+        self._ordered_call(self.lib.tcec_split_buf, self.h, _ptr(x), _ptr(hi), _ptr(lo), x.numel(), fmt,
+                                      C.byref(ovf))
         return hi, lo, bool(ovf.value)
 
     def scale_buf(self, x, scale_exp: int):
         y = self._out_like(x)
-        check(self.lib.tcec_scale_buf(self.h, _ptr(x), _ptr(y), x.numel(), int(scale_exp)))
+        self._ordered_call(self.lib.tcec_scale_buf, self.h, _ptr(x), _ptr(y), x.numel(), int(scale_exp))
         return y
 
     def add_buf(self, a, b):
         y = self._out_like(a)
-        check(self.lib.tcec_add_buf(self.h, _ptr(a), _ptr(b), _ptr(y), a.numel()))
+        self._ordered_call(self.lib.tcec_add_buf, self.h, _ptr(a), _ptr(b), _ptr(y), a.numel())
         return y
 
     def sub_buf(self, a, b):
         y = self._out_like(a)
-        check(self.lib.tcec_sub_buf(self.h, _ptr(a), _ptr(b), _ptr(y), a.numel()))
+        self._ordered_call(self.lib.tcec_sub_buf, self.h, _ptr(a), _ptr(b), _ptr(y), a.numel())
         return y
 
     # ------------------------------------------------------------- precsel
@@ -161,22 +185,22 @@ class Handle:
         """exp_stats (precsel.hpp:68): both stages unconditionally."""
         out = ExpStats()
         rows, cols = (m.shape if m.dim() == 2 else (1, m.numel()))
-        check(self.lib.tcec_exp_stats(self.h, _ptr(m), rows, cols, target_max_exponent, 0, 0.0,
-                                      C.byref(out)))
+        self._ordered_call(self.lib.tcec_exp_stats, self.h, _ptr(m), rows, cols, target_max_exponent, 0, 0.0,
+                                      C.byref(out))
         return out
 
     def exp_stats_staged(self, m, target_max_exponent: int, t: float) -> ExpStats:
         """exp_stats_staged (precsel.hpp:70)."""
         out = ExpStats()
         rows, cols = (m.shape if m.dim() == 2 else (1, m.numel()))
-        check(self.lib.tcec_exp_stats(self.h, _ptr(m), rows, cols, target_max_exponent, 1,
-                                      float(t), C.byref(out)))
+        self._ordered_call(self.lib.tcec_exp_stats, self.h, _ptr(m), rows, cols, target_max_exponent, 1,
+                                      float(t), C.byref(out))
         return out
 
     def scale_matrix_inplace(self, m, scale_exp: int) -> None:
         """scale_matrix_inplace (precsel.hpp:82): ScaleOverflow on nonfinite."""
         x = m.view(_torch().float32)
-        check(self.lib.tcec_scale_components(self.h, _ptr(x), x.numel(), int(scale_exp), 1))
+        self._ordered_call(self.lib.tcec_scale_components, self.h, _ptr(x), x.numel(), int(scale_exp), 1)
 
     def scale_matrix(self, m, scale_exp: int):
         out = m.clone()
@@ -186,8 +210,8 @@ class Handle:
     def descale_output_inplace(self, c, scale_exp_a: int, scale_exp_b: int) -> None:
         """descale_output_inplace (precsel.hpp:88): no overflow check."""
         x = c.view(_torch().float32)
-        check(self.lib.tcec_scale_components(self.h, _ptr(x), x.numel(),
-                                             -(int(scale_exp_a) + int(scale_exp_b)), 0))
+        self._ordered_call(self.lib.tcec_scale_components, self.h, _ptr(x), x.numel(),
+                                             -(int(scale_exp_a) + int(scale_exp_b)), 0)
 
     # --------------------------------------------------------------- CGEMM
     def _shapes(self, a, b):
@@ -206,8 +230,8 @@ class Handle:
                                                        device=a.device)
         md = GEMM_MODES[mode] if isinstance(mode, str) else int(mode)
         ovf = C.c_int(0)
-        check(self.lib.tcec_cgemm(self.h, _ptr(a), _ptr(b), _ptr(c), m, n, k, md, int(k_tile),
-                                  C.byref(ovf)))
+        self._ordered_call(self.lib.tcec_cgemm, self.h, _ptr(a), _ptr(b), _ptr(c), m, n, k, md, int(k_tile),
+                                  C.byref(ovf))
         return c, bool(ovf.value)
 
     def cgemm_batched(self, pairs, mode, k_tile: int = 16):
@@ -228,8 +252,8 @@ class Handle:
         c = out if out is not None else _torch().empty((m, n), dtype=_torch().complex64,
                                                        device=a.device)
         res = DispatchResult()
-        check(self.lib.tcec_dispatch_cgemm(self.h, _ptr(a), _ptr(b), _ptr(c), m, n, k,
-                                           C.byref(config), C.byref(res)))
+        self._ordered_call(self.lib.tcec_dispatch_cgemm, self.h, _ptr(a), _ptr(b), _ptr(c), m, n, k,
+                                           C.byref(config), C.byref(res))
         return c, res
 
     def dispatch_cgemm_host(self, a: np.ndarray, b: np.ndarray, config=None, out=None):
@@ -257,7 +281,7 @@ class Handle:
         out = _torch().empty(tuple(t.shape[a] for a in axis_of), dtype=t.dtype, device=t.device)
         dims = (C.c_int64 * max(r, 1))(*t.shape)
         ax = (C.c_int * max(r, 1))(*axis_of)
-        check(self.lib.tcec_permute(self.h, _ptr(t), _ptr(out), r, dims, ax))
+        self._ordered_call(self.lib.tcec_permute, self.h, _ptr(t), _ptr(out), r, dims, ax)
         return out
 
 

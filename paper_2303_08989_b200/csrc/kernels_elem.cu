@@ -423,11 +423,14 @@ __global__ void __launch_bounds__(256) prep_b_kernel(const float2* __restrict__ 
 // then C = (P1 - P2, P3 + P4) in f32 RN (cgemm.cpp:38-44).
 constexpr int SB_M = 64, SB_N = 64, SB_K = 16;
 
+// 256 threads, thread (tx, ty) owns rows 4ty..4ty+3 and columns 4tx..4tx+3 of
+// the 64 x 64 tile, so every k step reads its operands with four 16-byte
+// shared loads (the issue slots go to the 128 FMUL/FADD of the four chains)
 __global__ void __launch_bounds__(256) cgemm_fp32_ref_kernel(const float2* __restrict__ a,
                                                              const float2* __restrict__ b,
                                                              float2* __restrict__ c, int64_t m,
                                                              int64_t n, int64_t k) {
-    __shared__ float sar[SB_K][SB_M], sai[SB_K][SB_M], sbr[SB_K][SB_N], sbi[SB_K][SB_N];
+    __shared__ __align__(16) float sar[SB_K][SB_M], sai[SB_K][SB_M], sbr[SB_K][SB_N], sbi[SB_K][SB_N];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const int64_t tiles_n = (n + SB_N - 1) / SB_N;  // 1-D grid: x = i_tile * tiles_n + j_tile
     const int64_t i0 = (int64_t(blockIdx.x) / tiles_n) * SB_M, j0 = (int64_t(blockIdx.x) % tiles_n) * SB_N;
@@ -456,17 +459,12 @@ __global__ void __launch_bounds__(256) cgemm_fp32_ref_kernel(const float2* __res
         __syncthreads();
         const int kend = (k - k0) < SB_K ? int(k - k0) : SB_K;  // never add padding terms
         for (int kk = 0; kk < kend; ++kk) {
-            float ar[4], ai[4], br[4], bi[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                ar[i] = sar[kk][ty + 16 * i];
-                ai[i] = sai[kk][ty + 16 * i];
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                br[j] = sbr[kk][tx + 16 * j];
-                bi[j] = sbi[kk][tx + 16 * j];
-            }
+            const float4 ar4 = *reinterpret_cast<const float4*>(&sar[kk][4 * ty]);
+            const float4 ai4 = *reinterpret_cast<const float4*>(&sai[kk][4 * ty]);
+            const float4 br4 = *reinterpret_cast<const float4*>(&sbr[kk][4 * tx]);
+            const float4 bi4 = *reinterpret_cast<const float4*>(&sbi[kk][4 * tx]);
+            const float ar[4] = {ar4.x, ar4.y, ar4.z, ar4.w}, ai[4] = {ai4.x, ai4.y, ai4.z, ai4.w};
+            const float br[4] = {br4.x, br4.y, br4.z, br4.w}, bi[4] = {bi4.x, bi4.y, bi4.z, bi4.w};
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -480,14 +478,24 @@ __global__ void __launch_bounds__(256) cgemm_fp32_ref_kernel(const float2* __res
         __syncthreads();
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 4; ++i) {
+        const int64_t gi = i0 + 4 * ty + i;
+        if (gi >= m) continue;
+        const int64_t gj = j0 + 4 * tx;
+        float2 o[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int64_t gi = i0 + ty + 16 * i, gj = j0 + tx + 16 * j;
-            if (gi < m && gj < n)
-                c[gi * n + gj] =
-                    make_float2(__fsub_rn(p1[i][j], p2[i][j]), __fadd_rn(p3[i][j], p4[i][j]));
+        for (int j = 0; j < 4; ++j)
+            o[j] = make_float2(__fsub_rn(p1[i][j], p2[i][j]), __fadd_rn(p3[i][j], p4[i][j]));
+        float2* dst = c + gi * n + gj;
+        if (gj + 4 <= n && ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0)) {
+            reinterpret_cast<float4*>(dst)[0] = make_float4(o[0].x, o[0].y, o[1].x, o[1].y);
+            reinterpret_cast<float4*>(dst)[1] = make_float4(o[2].x, o[2].y, o[3].x, o[3].y);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (gj + j < n) dst[j] = o[j];
         }
+    }
 }
 
 // FP64_ORACLE tier: f64 chains (kernels_scalar.cpp:137-148), each product
@@ -878,6 +886,104 @@ __global__ void __launch_bounds__(256) permute_tiled_kernel(const float2* __rest
     }
 }
 
+// Bit-permutation permute: when every extent is a power of two (the dim-2
+// bonds of circuit networks), a permutation of axes is a permutation of the
+// bits of the linear index.  The tile is spanned by the 5 lowest input bits
+// (32 consecutive source elements) and the input bits feeding the 5 lowest
+// output bits (32 consecutive destination elements): up to 1024 elements
+// staged through XOR-swizzled shared memory, so reads and writes are both
+// coalesced 256-B runs.  The remaining bits index the tiles.  Offsets inside a
+// tile come from per-block shared tables built once (persistent grid).
+constexpr int kBitTileMax = 10;  // tile bits
+
+struct BitPermDesc {
+    int nbits;                  // log2(total)
+    int ntile;                  // tile bits (|U|)
+    int nrest;                  // remaining bits
+    int8_t tile_in[kBitTileMax];    // input bit of tile bit t (input-bit order)
+    int8_t tile_out[kBitTileMax];   // output bit of tile bit t
+    int8_t out_rank[kBitTileMax];   // rank of tile bit t among the tile bits by output position
+    int8_t rest_in[64], rest_out[64];  // input / output bit of remaining bit r (output order)
+};
+
+TCEC_DEV uint32_t bp_swz(uint32_t s) { return s ^ (((s >> 4) ^ (s >> 8)) & 15u); }
+
+__global__ void __launch_bounds__(256) permute_bits_kernel(const float2* __restrict__ src,
+                                                           float2* __restrict__ dst,
+                                                           const BitPermDesc d) {
+    __shared__ float2 tile[1 << kBitTileMax];
+    __shared__ uint64_t in_off[1 << kBitTileMax], out_off[1 << kBitTileMax];
+    __shared__ uint16_t s_of_u[1 << kBitTileMax];
+    const int T = 1 << d.ntile;
+    // tables: t enumerates the tile in input-bit order (smem index), u in
+    // output-bit order; out_off[t] / in_off[t] are the element offsets
+    for (int t = threadIdx.x; t < T; t += blockDim.x) {
+        uint64_t io = 0, oo = 0;
+        for (int b = 0; b < d.ntile; ++b)
+            if ((t >> b) & 1) {
+                io |= uint64_t(1) << d.tile_in[b];
+                oo |= uint64_t(1) << d.tile_out[b];
+            }
+        in_off[t] = io;
+        out_off[t] = oo;
+    }
+    __syncthreads();
+    // u -> t: u enumerates the tile bits by output position
+    for (int u = threadIdx.x; u < T; u += blockDim.x) {
+        uint32_t t = 0;
+        for (int b = 0; b < d.ntile; ++b) t |= ((uint32_t(u) >> d.out_rank[b]) & 1u) << b;
+        s_of_u[u] = uint16_t(t);
+    }
+    __syncthreads();
+    const int64_t ntiles = int64_t(1) << d.nrest;
+    auto bases = [&](int64_t blk, int64_t& bi, int64_t& bo) {
+        bi = 0;
+        bo = 0;
+        for (int r = 0; r < d.nrest; ++r)
+            if ((blk >> r) & 1) {
+                bi |= int64_t(1) << d.rest_in[r];
+                bo |= int64_t(1) << d.rest_out[r];
+            }
+    };
+    // software pipeline: the next tile's loads are in flight while this
+    // tile's stores drain (T <= 1024 = 4 elements per thread)
+    constexpr int kPer = (1 << kBitTileMax) / 256;
+    float2 reg[kPer];
+    int64_t blk = blockIdx.x, base_in = 0, base_out = 0;
+    if (blk < ntiles) {
+        bases(blk, base_in, base_out);
+#pragma unroll
+        for (int e = 0; e < kPer; ++e) {
+            const int t = threadIdx.x + 256 * e;
+            if (t < T) reg[e] = __ldcs(src + base_in + in_off[t]);
+        }
+    }
+    while (blk < ntiles) {
+#pragma unroll
+        for (int e = 0; e < kPer; ++e) {
+            const int t = threadIdx.x + 256 * e;
+            if (t < T) tile[bp_swz(uint32_t(t))] = reg[e];
+        }
+        __syncthreads();
+        const int64_t next = blk + gridDim.x;
+        const int64_t out_base = base_out;
+        if (next < ntiles) {
+            bases(next, base_in, base_out);
+#pragma unroll
+            for (int e = 0; e < kPer; ++e) {
+                const int t = threadIdx.x + 256 * e;
+                if (t < T) reg[e] = __ldcs(src + base_in + in_off[t]);
+            }
+        }
+        for (int u = threadIdx.x; u < T; u += blockDim.x) {
+            const uint32_t t = s_of_u[u];
+            __stcs(dst + out_base + out_off[t], tile[bp_swz(t)]);
+        }
+        __syncthreads();
+        blk = next;
+    }
+}
+
 }  // namespace
 
 // Plan the tiled permute; false when the shape does not suit it.
@@ -1095,6 +1201,60 @@ void launch_permute(const float2* src, float2* dst, int rank, const int64_t* old
         }
     }
     desc.rank = r;
+    // power-of-two extents: permutation of index bits, coalesced on both sides
+    if (total >= 1024 && (total & (total - 1)) == 0) {
+        bool pow2 = true;
+        for (int a = 0; a < r; ++a) pow2 = pow2 && (desc.out_dim[a] & (desc.out_dim[a] - 1)) == 0;
+        if (pow2) {
+            BitPermDesc bd{};
+            int src_bit[64];
+            int j = 0;  // output bit, LSB first: axes from the innermost
+            for (int a = r - 1; a >= 0; --a) {
+                const int w = __builtin_ctzll(uint64_t(desc.out_dim[a]));
+                const int s0 = __builtin_ctzll(uint64_t(desc.in_stride[a]));
+                for (int b = 0; b < w; ++b) src_bit[j++] = s0 + b;
+            }
+            bd.nbits = j;
+            bool in_tile[64] = {false};
+            const int lo = j < 5 ? j : 5;
+            for (int b = 0; b < lo; ++b) in_tile[b] = true;           // input bits 0..4
+            for (int o = 0; o < lo; ++o) in_tile[src_bit[o]] = true;  // feeding output bits 0..4
+            // where the two groups overlap, widen the tile with the next input
+            // bits so every tile moves ~1024 elements (8 KB) per pass
+            int cnt = 0;
+            for (int b = 0; b < j; ++b) cnt += in_tile[b];
+            for (int b = lo; b < j && cnt < kBitTileMax; ++b)
+                if (!in_tile[b]) {
+                    in_tile[b] = true;
+                    ++cnt;
+                }
+            int out_of_in[64];
+            for (int o = 0; o < j; ++o) out_of_in[src_bit[o]] = o;
+            bd.ntile = 0;
+            for (int b = 0; b < j; ++b)
+                if (in_tile[b]) {
+                    bd.tile_in[bd.ntile] = int8_t(b);
+                    bd.tile_out[bd.ntile] = int8_t(out_of_in[b]);
+                    ++bd.ntile;
+                }
+            bd.nrest = 0;
+            for (int o = 0; o < j; ++o)
+                if (!in_tile[src_bit[o]]) {
+                    bd.rest_in[bd.nrest] = int8_t(src_bit[o]);
+                    bd.rest_out[bd.nrest] = int8_t(o);
+                    ++bd.nrest;
+                }
+            for (int b = 0; b < bd.ntile; ++b) {
+                int rk = 0;
+                for (int c = 0; c < bd.ntile; ++c) rk += bd.tile_out[c] < bd.tile_out[b];
+                bd.out_rank[b] = int8_t(rk);
+            }
+            const int64_t ntiles = int64_t(1) << bd.nrest;
+            const int64_t g = ntiles < 148 * 8 ? ntiles : 148 * 8;
+            permute_bits_kernel<<<unsigned(g), 256, 0, s>>>(src, dst, bd);
+            return;
+        }
+    }
     // innermost output axis not contiguous in the source: shared-memory tiles
     if (r >= 2 && desc.in_stride[r - 1] != 1 && total >= 4096) {
         static TiledPermDesc td;  // host-side scratch (kernel arguments are copied at launch)

@@ -112,15 +112,9 @@ def random_greedy_path(spec: NetworkSpec, trials: int = 64, max_width: float = 3
     return best[1], best[2], best[3]
 
 
-def bisection_path(spec: NetworkSpec, trials: int = 8, leaf: int = 12, seed: int = 0,
-                   max_width: float = 30.0):
-    """Recursive Kernighan-Lin bisection of the tensor graph (edge weight =
-    log2 bond dimension): every subtree is contracted before its sibling, so
-    a subtree's intermediate is exactly its cut; leaves (<= `leaf` tensors)
-    are ordered by the randomized greedy.  Best of `trials` seeds."""
+def _tensor_graph(spec: NetworkSpec):
+    """Graph of the network: nodes = tensors, edge weight = sum of log2 bond dims."""
     import networkx as nx
-    from networkx.algorithms.community import kernighan_lin_bisection
-
     dims_of, owners = {}, {}
     for i, (ls, ds) in enumerate(zip(spec.labels, spec.dims)):
         for l, d in zip(ls, ds):
@@ -136,6 +130,55 @@ def bisection_path(spec: NetworkSpec, trials: int = 8, leaf: int = 12, seed: int
                 g[a][b]["weight"] += w
             else:
                 g.add_edge(a, b, weight=w)
+    return g, dims_of
+
+
+def _spectral_split(sub, rng: random.Random, imbalance):
+    """Two-way cut of a connected graph: nodes ordered by the Fiedler vector,
+    cut at the cheapest position inside a randomly placed window (sampled
+    imbalance), refined by Kernighan-Lin swaps (sizes preserved)."""
+    import networkx as nx
+    from networkx.algorithms.community import kernighan_lin_bisection
+    nodes = list(sub.nodes)
+    n = len(nodes)
+    try:
+        fv = nx.fiedler_vector(sub, weight="weight", normalized=True, method="tracemin_lu",
+                               seed=rng.randrange(1 << 30))
+        order = [nodes[i] for i in np.argsort(fv, kind="stable")]
+    except Exception:  # tiny or degenerate graphs
+        order = list(nodes)
+        rng.shuffle(order)
+    lo, hi = imbalance
+    f = rng.uniform(lo, hi)
+    w0, w1 = max(1, int((f - 0.08) * n)), min(n - 1, int((f + 0.08) * n))
+    side = {}
+    cut, best = 0.0, None
+    for pos, v in enumerate(order[:-1]):
+        side[v] = 0
+        for u, d in sub[v].items():
+            cut += -d["weight"] if side.get(u) == 0 else d["weight"]
+        if w0 <= pos + 1 <= w1 and (best is None or cut < best[0]):
+            best = (cut, pos + 1)
+    k = best[1] if best else max(1, n // 2)
+    a, b = set(order[:k]), set(order[k:])
+    if n > 4:
+        a, b = kernighan_lin_bisection(sub, partition=(a, b), max_iter=4, weight="weight",
+                                       seed=rng.randrange(1 << 30))
+    return a, b
+
+
+def partition_path(spec: NetworkSpec, trials: int = 16, leaf: int = 10, seed: int = 0,
+                   max_width: float = 30.0, imbalance=(0.3, 0.7)):
+    """Divisive contraction tree (the hyper-optimized recipe of Gray & Kourtis,
+    with a spectral + Kernighan-Lin graph partitioner instead of a hypergraph
+    one): recursively cut the tensor graph in two (Fiedler-vector order,
+    cheapest cut inside a randomly sampled imbalance window, KL refinement);
+    every subtree is contracted before its sibling, so an intermediate is the
+    boundary of its part.  Parts of <= `leaf` tensors are ordered by a local
+    greedy.  Best of `trials` samples (lowest flops among widths <= max_width,
+    else lowest width).  Returns (path, flops, log2 width)."""
+    import networkx as nx
+    g, dims_of = _tensor_graph(spec)
 
     best = None
     for t in range(trials):
@@ -145,57 +188,19 @@ def bisection_path(spec: NetworkSpec, trials: int = 8, leaf: int = 12, seed: int
             if len(nodes) <= leaf:
                 return list(nodes)
             sub = g.subgraph(nodes)
-            comps = list(nx.connected_components(sub))
+            comps = sorted(nx.connected_components(sub), key=len)
             if len(comps) > 1:
-                comps.sort(key=len)
                 a = set(comps[0])
                 b = set(nodes) - a
             else:
-                a, b = kernighan_lin_bisection(sub, weight="weight", seed=rng.randrange(1 << 30))
+                a, b = _spectral_split(sub, rng, imbalance)
+            if not a or not b:
+                half = len(nodes) // 2
+                a, b = set(list(nodes)[:half]), set(list(nodes)[half:])
             return [split(sorted(a)), split(sorted(b))]
 
         tree = split(list(range(len(spec.labels))))
-        # post-order -> SSA steps; leaves (lists of ints) by a local greedy
-        live_labels = {i: list(ls) for i, ls in enumerate(spec.labels)}
-        counter = [len(spec.labels)]
-        steps = []
-
-        def contract(a, b):
-            la, lb = live_labels.pop(a), live_labels.pop(b)
-            sa, sb = set(la), set(lb)
-            live_labels[counter[0]] = [l for l in la if l not in sb] + [l for l in lb if l not in sa]
-            steps.append((min(a, b), max(a, b)))
-            counter[0] += 1
-            return counter[0] - 1
-
-        def leaf_order(ids):
-            ids = list(ids)
-            while len(ids) > 1:
-                bestp = None
-                for x in range(len(ids)):
-                    for y in range(x + 1, len(ids)):
-                        la, lb = live_labels[ids[x]], live_labels[ids[y]]
-                        shared = set(la) & set(lb)
-                        out = _log2size([dims_of[l] for l in la if l not in shared] +
-                                        [dims_of[l] for l in lb if l not in shared])
-                        key = (not shared, out + rng.random() * 1e-3)
-                        if bestp is None or key < bestp[0]:
-                            bestp = (key, x, y)
-                _, x, y = bestp
-                nid = contract(ids[x], ids[y])
-                ids = [i for j, i in enumerate(ids) if j not in (x, y)] + [nid]
-            return ids[0]
-
-        def walk(node):
-            if node and isinstance(node[0], list):
-                left = walk(node[0])
-                right = walk(node[1])
-                return contract(left, right)
-            if isinstance(node, list) and node and isinstance(node[0], int):
-                return leaf_order(node)
-            return walk(node[0])
-
-        walk(tree)
+        steps = _tree_to_steps(spec, tree, dims_of, rng)
         flops, width = path_cost(spec, steps)
         key = (width > max_width, flops if width <= max_width else width)
         if best is None or key < best[0]:
@@ -203,8 +208,53 @@ def bisection_path(spec: NetworkSpec, trials: int = 8, leaf: int = 12, seed: int
     return best[1], best[2], best[3]
 
 
+def _tree_to_steps(spec, tree, dims_of, rng):
+    """Post-order SSA steps of a nested-list contraction tree; leaf groups
+    (lists of tensor ids) are ordered by the smallest-result greedy."""
+    live_labels = {i: list(ls) for i, ls in enumerate(spec.labels)}
+    counter = [len(spec.labels)]
+    steps = []
+
+    def contract(a, b):
+        la, lb = live_labels.pop(a), live_labels.pop(b)
+        sa, sb = set(la), set(lb)
+        live_labels[counter[0]] = [l for l in la if l not in sb] + [l for l in lb if l not in sa]
+        steps.append((min(a, b), max(a, b)))
+        counter[0] += 1
+        return counter[0] - 1
+
+    def leaf_order(ids):
+        ids = list(ids)
+        while len(ids) > 1:
+            bestp = None
+            for x in range(len(ids)):
+                for y in range(x + 1, len(ids)):
+                    la, lb = live_labels[ids[x]], live_labels[ids[y]]
+                    shared = set(la) & set(lb)
+                    out = _log2size([dims_of[l] for l in la if l not in shared] +
+                                    [dims_of[l] for l in lb if l not in shared])
+                    key = (not shared, out + rng.random() * 1e-3)
+                    if bestp is None or key < bestp[0]:
+                        bestp = (key, x, y)
+            _, x, y = bestp
+            nid = contract(ids[x], ids[y])
+            ids = [i for j, i in enumerate(ids) if j not in (x, y)] + [nid]
+        return ids[0]
+
+    def walk(node):
+        if node and isinstance(node[0], list):
+            left = walk(node[0])
+            right = walk(node[1])
+            return contract(left, right)
+        return leaf_order(node)
+
+    walk(tree)
+    return steps
+
+
 def path_cost(spec: NetworkSpec, path):
-    """(flops, log2 of the largest intermediate) of an SSA path."""
+    """(flops, log2 of the largest intermediate) of an SSA path (float
+    arithmetic: no integer overflow on hopeless paths)."""
     dims_of = {}
     for ls, ds in zip(spec.labels, spec.dims):
         for l, d in zip(ls, ds):
@@ -216,9 +266,319 @@ def path_cost(spec: NetworkSpec, path):
         la, lb = live.pop(a), live.pop(b)
         sb, sa = set(lb), set(la)
         out = [l for l in la if l not in sb] + [l for l in lb if l not in sa]
-        k = float(np.prod([dims_of[l] for l in la if l in sb])) if la else 1.0
-        flops += 8.0 * float(np.prod([dims_of[l] for l in out]) if out else 1.0) * k
-        width = max(width, _log2size([dims_of[l] for l in out]))
+        lk = _log2size([dims_of[l] for l in la if l in sb])
+        lo = _log2size([dims_of[l] for l in out])
+        flops += 8.0 * 2.0 ** (lo + lk)
+        width = max(width, lo)
         live[nxt] = out
         nxt += 1
     return flops, width
+
+
+def presimplify(spec: NetworkSpec):
+    """Absorb every tensor of rank <= 2 (single-qubit gates, |0> states, <x|
+    selectors) into a neighbour until none is left -- the contractions never
+    grow a tensor, so they are free in width.  Returns (steps, ids, reduced):
+    the SSA steps taken, the SSA id of every surviving tensor, and a
+    NetworkSpec (labels/dims only) of the reduced network."""
+    live = {i: list(ls) for i, ls in enumerate(spec.labels)}
+    dims_of = {}
+    for ls, ds in zip(spec.labels, spec.dims):
+        for l, d in zip(ls, ds):
+            dims_of[l] = d
+    holder = {}
+    for i, ls in live.items():
+        for l in ls:
+            holder.setdefault(l, set()).add(i)
+    nxt = len(spec.labels)
+    steps = []
+    changed = True
+    while changed and len(live) > 1:
+        changed = False
+        for i in sorted(live):
+            if i not in live or len(live[i]) > 2:
+                continue
+            nbs = sorted({h for l in live[i] for h in holder[l] if h != i and h in live})
+            if not nbs:
+                continue
+            # the neighbour sharing the most bonds (the result is never larger than it)
+            j = max(nbs, key=lambda h: (len(set(live[h]) & set(live[i])), -h))
+            la, lb = live.pop(min(i, j)), live.pop(max(i, j))
+            sa, sb = set(la), set(lb)
+            out = [l for l in la if l not in sb] + [l for l in lb if l not in sa]
+            for l in la:
+                holder[l].discard(min(i, j))
+            for l in lb:
+                holder[l].discard(max(i, j))
+            live[nxt] = out
+            for l in out:
+                holder[l].add(nxt)
+            steps.append((min(i, j), max(i, j)))
+            nxt += 1
+            changed = True
+    ids = sorted(live)
+    reduced = NetworkSpec(labels=[list(live[i]) for i in ids],
+                          dims=[[dims_of[l] for l in live[i]] for i in ids], data=[])
+    return steps, ids, reduced
+
+
+def remap_path(steps_pre, ids, n_orig, reduced_path):
+    """Compose presimplify's steps with a path over the reduced network into
+    one SSA path over the original network."""
+    n_red = len(ids)
+    ssa = {r: ids[r] for r in range(n_red)}
+    nxt = n_orig + len(steps_pre)
+    out = list(steps_pre)
+    for r, (a, b) in enumerate(reduced_path):
+        x, y = ssa[a], ssa[b]
+        out.append((min(x, y), max(x, y)))
+        ssa[n_red + r] = nxt
+        nxt += 1
+    return out
+
+
+def reconfigure_path(spec: NetworkSpec, path, k: int = 8, passes: int = 3, seed: int = 0):
+    """Subtree reconfiguration (cotengra's `subtree_reconfigure`): for every
+    node of the contraction tree take a frontier of up to `k` sub-pieces and
+    replace the way they are combined by the flop-optimal order (dynamic
+    programming over subsets).  In a closed network every bond joins exactly
+    two tensors, so the open legs of a union of pieces are the XOR of their
+    leg bitmasks.  Returns (path, flops, log2 width)."""
+    rng = random.Random(seed)
+    bit, lw = {}, []
+    for ls, ds in zip(spec.labels, spec.dims):
+        for l, d in zip(ls, ds):
+            if l not in bit:
+                bit[l] = len(lw)
+                lw.append(math.log2(d))
+    uniform = all(w == 1.0 for w in lw)
+
+    def width(mask):
+        if uniform:
+            return float(mask.bit_count())
+        w, i = 0.0, 0
+        while mask:
+            if mask & 1:
+                w += lw[i]
+            mask >>= 1
+            i += 1
+        return w
+
+    n = len(spec.labels)
+    # tree nodes: id -> (left, right) for internal; leaves are ids < n
+    legs = {}
+    for i, ls in enumerate(spec.labels):
+        m = 0
+        for l in ls:
+            m |= 1 << bit[l]
+        legs[i] = m
+    children = {}
+    nxt = n
+    for a, b in path:
+        children[nxt] = (a, b)
+        legs[nxt] = legs[a] ^ legs[b]
+        nxt += 1
+    root = nxt - 1
+
+    def step_cost(ma, mb):
+        return 2.0 ** ((width(ma) + width(mb) + width(ma ^ mb)) / 2.0)
+
+    def optimize(node):
+        """Reconfigure the top of the subtree at `node`; True if improved."""
+        nonlocal nxt
+        if node not in children:
+            return False
+        frontier = [node]
+        internal_top = []
+        while len(frontier) < k:
+            cand = [p for p in frontier if p in children]
+            if not cand:
+                break
+            p = max(cand, key=lambda q: (width(legs[q]), rng.random()))
+            frontier.remove(p)
+            internal_top.append(p)
+            frontier.extend(children[p])
+        if len(frontier) < 3:
+            return False
+        old = sum(step_cost(legs[children[p][0]], legs[children[p][1]]) for p in internal_top)
+        K = len(frontier)
+        pm = [legs[p] for p in frontier]
+        full = (1 << K) - 1
+        sub_legs = [0] * (full + 1)
+        for s in range(1, full + 1):
+            low = s & -s
+            sub_legs[s] = sub_legs[s ^ low] ^ pm[low.bit_length() - 1]
+        cost = [0.0] * (full + 1)
+        choice = [0] * (full + 1)
+        order = sorted(range(1, full + 1), key=lambda s: s.bit_count())
+        for s in order:
+            if s & (s - 1) == 0:
+                continue
+            low = s & -s
+            best_c, best_a = None, 0
+            a = (s - 1) & s
+            while a:
+                if a & low:
+                    b = s ^ a
+                    c = cost[a] + cost[b] + step_cost(sub_legs[a], sub_legs[b])
+                    if best_c is None or c < best_c:
+                        best_c, best_a = c, a
+                a = (a - 1) & s
+            cost[s], choice[s] = best_c, best_a
+        if cost[full] >= old * (1 - 1e-9):
+            return False
+
+        # rebuild: the DP tree replaces internal_top; the root keeps its id
+        def build(s, node_id=None):
+            if s & (s - 1) == 0:
+                return frontier[s.bit_length() - 1]
+            nonlocal nxt
+            a = choice[s]
+            l, r = build(a), build(s ^ a)
+            if node_id is None:
+                node_id = nxt
+                nxt += 1
+            children[node_id] = (l, r)
+            legs[node_id] = legs[l] ^ legs[r]
+            return node_id
+
+        for p in internal_top:
+            if p != node:
+                del children[p]
+        build(full, node)
+        return True
+
+    for _ in range(passes):
+        improved = False
+        stack, order_nodes = [root], []
+        while stack:
+            x = stack.pop()
+            if x in children:
+                order_nodes.append(x)
+                stack.extend(children[x])
+        for x in reversed(order_nodes):   # bottom-up
+            if x in children:
+                improved |= optimize(x)
+        if not improved:
+            break
+
+    # tree -> SSA steps (post-order)
+    steps, ssa = [], {}
+    cnt = [n]
+
+    def emit(x):
+        if x < n:
+            return x
+        l, r = children[x]
+        a, b = emit(l), emit(r)
+        steps.append((min(a, b), max(a, b)))
+        cnt[0] += 1
+        return cnt[0] - 1
+
+    import sys
+    old_lim = sys.getrecursionlimit()
+    sys.setrecursionlimit(max(old_lim, 10000))
+    try:
+        emit(root)
+    finally:
+        sys.setrecursionlimit(old_lim)
+    flops, w = path_cost(spec, steps)
+    return steps, flops, w
+
+
+def _drop_labels(spec: NetworkSpec, drop) -> NetworkSpec:
+    drop = set(drop)
+    return NetworkSpec(labels=[[l for l in ls if l not in drop] for ls in spec.labels],
+                       dims=[[d for l, d in zip(ls, ds) if l not in drop]
+                             for ls, ds in zip(spec.labels, spec.dims)], data=[])
+
+
+def _sliced_cost(spec: NetworkSpec, path, drop):
+    """(total flops over all slices, log2 per-slice width) with `drop` sliced."""
+    dims_of = {}
+    for ls, ds in zip(spec.labels, spec.dims):
+        for l, d in zip(ls, ds):
+            dims_of[l] = d
+    f, w = path_cost(_drop_labels(spec, drop), path)
+    return f * float(np.prod([dims_of[l] for l in drop])) if drop else f, w
+
+
+def find_slices_exact(spec: NetworkSpec, path, max_log2: float, candidates: int = 32):
+    """Greedy slicer with exact evaluation: among the bonds of the currently
+    largest intermediates, slice the one that minimises the total flops over
+    all slices, until the per-slice width is <= max_log2."""
+    count = {}
+    for ls in spec.labels:
+        for l in ls:
+            count[l] = count.get(l, 0) + 1
+    sliced = []
+    while True:
+        red = _drop_labels(spec, sliced)
+        live = {i: list(ls) for i, ls in enumerate(red.labels)}
+        dims_of = {l: d for ls, ds in zip(spec.labels, spec.dims) for l, d in zip(ls, ds)}
+        nxt = len(red.labels)
+        inter = []
+        for a, b in path:
+            la, lb = live.pop(a), live.pop(b)
+            sa, sb = set(la), set(lb)
+            out = [l for l in la if l not in sb] + [l for l in lb if l not in sa]
+            inter.append(out)
+            live[nxt] = out
+            nxt += 1
+        widths = [_log2size([dims_of[l] for l in t]) for t in inter]
+        wmax = max(widths, default=0.0)
+        if wmax <= max_log2:
+            return sliced
+        cand = {}
+        for t, w in zip(inter, widths):
+            if w >= wmax - 1e-9:
+                for l in t:
+                    if count.get(l) == 2 and l not in sliced:
+                        cand[l] = cand.get(l, 0) + 1
+        if not cand:
+            return sliced
+        cl = sorted(cand, key=lambda l: (-cand[l], l))[:candidates]
+        best = None
+        for l in cl:
+            f, w = _sliced_cost(spec, path, sliced + [l])
+            key = (f, w, l)
+            if best is None or key < best[0]:
+                best = (key, l)
+        sliced.append(best[1])
+
+
+def slice_and_reconfigure(spec: NetworkSpec, path, max_log2: float, k: int = 10, rounds: int = 3):
+    """Alternate exact slicing and subtree reconfiguration of the sliced network
+    (cotengra's slice-and-reconfigure).  Returns (path, sliced, total flops,
+    per-slice log2 width)."""
+    sliced = []
+    for _ in range(rounds):
+        sliced = find_slices_exact(spec, path, max_log2)
+        sub = _drop_labels(spec, sliced)
+        path, _, _ = reconfigure_path(sub, path, k=k, passes=3)
+    sliced = find_slices_exact(spec, path, max_log2)
+    f, w = _sliced_cost(spec, path, sliced)
+    return path, sliced, f, w
+
+
+def hyper_path(spec: NetworkSpec, max_log2: float = 28.0, trials: int = 2, seed: int = 0,
+               leaf: int = 14, k: int = 10, log=None):
+    """Sliced contraction plan for large circuits:
+    presimplify (absorb rank <= 2 tensors) -> divisive partition tree
+    (`partition_path`) -> subtree reconfiguration -> exact slicing alternated
+    with reconfiguration until every per-slice intermediate is <= 2^max_log2.
+    Best of `trials` seeds by total flops over all slices.  Returns
+    (path over `spec`, sliced labels, total flops, per-slice log2 width)."""
+    pre, ids, red = presimplify(spec)
+    best = None
+    for t in range(trials):
+        s = seed + 1000 * t
+        p, f, w = partition_path(red, trials=8, leaf=leaf, max_width=60, imbalance=(0.2, 0.8), seed=s)
+        p, f, w = reconfigure_path(red, p, k=k, passes=3, seed=s)
+        p, sliced, fs, ws = slice_and_reconfigure(red, p, max_log2, k=k, rounds=2)
+        if log:
+            log(f"trial {t}: unsliced 2^{w:.0f} {f:.3g} flops -> {len(sliced)} sliced, 2^{ws:.0f}, {fs:.3g} flops")
+        if best is None or fs < best[2]:
+            best = (p, sliced, fs, ws)
+    p, sliced, fs, ws = best
+    return remap_path(pre, ids, len(spec.labels), p), sliced, fs, ws

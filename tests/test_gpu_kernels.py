@@ -129,10 +129,12 @@ def test_permute_errors(handle, dev):
 
 
 @pytest.mark.parametrize("dims", [(2,) * 14, (2,) * 20, (4, 8, 16, 32), (128, 3, 256), (96, 64),
-                                  (2, 64, 2, 64), (33, 70, 5)])
+                                  (2, 64, 2, 64), (33, 70, 5), (2,) * 25, (1024, 2, 512),
+                                  (8, 2, 1024, 4), (2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 4)])
 def test_permute_tiled_and_gather_paths(handle, dev, dims):
-    """Random permutations of shapes that exercise the shared-memory tiled plan
-    (high-rank dim-2, axes split at 32) and the gather fallback; bit-exact."""
+    """Random permutations of shapes that exercise the bit-permutation plan
+    (power-of-two extents), the shared-memory tiled plan (axes split at 32) and
+    the gather fallback; bit-exact."""
     g = np.random.default_rng(len(dims) * 7 + dims[0])
     t = torch.randn(*dims, dtype=torch.complex64, device=dev)
     for _ in range(4):
