@@ -761,8 +761,8 @@ def run_rqc7x7(args):
                 for ln in lines:
                     kk = ln.split(",")[3]
                     hist[kk] = hist.get(kk, 0) + 1
-                net.selector_batch(path, xs[:1], cfg)  # capture / warm
-                reps = max(1, args.steps // 5)
+                net.selector_batch(path, xs, cfg)  # capture / warm (one full pass)
+                reps = max(2, args.steps // 5)
                 torch.cuda.synchronize(dev)
                 t0 = time.perf_counter()
                 for _ in range(reps):

@@ -599,15 +599,24 @@ __global__ void __launch_bounds__(kChainThreads) cgemm_chain_kernel(const float2
     const float2* arow = a + i * k;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t nch = (k + CH - 1) / CH;
+    // each producer thread handles CH/128 products; all its global loads are
+    // issued before any product is formed, so a chunk costs one memory
+    // latency, not CH/128 of them (the chain consumes 1024 adds in ~4k cycles)
     auto produce = [&](int buf, int64_t k0) {
         acc_t* P = prod + size_t(buf) * 4 * CH;
-        for (int t = int(threadIdx.x) - 128; t < CH; t += 128) {
-            const int64_t kk = k0 + t;
-            float2 x = make_float2(0.f, 0.f), y = make_float2(0.f, 0.f);
-            if (kk < k) {
-                x = arow[kk];
-                y = b[kk * n + j];
-            }
+        constexpr int kPer = CH / 128;
+        const int t0 = int(threadIdx.x) - 128;
+        float2 xs[kPer], ys[kPer];
+#pragma unroll
+        for (int e = 0; e < kPer; ++e) {
+            const int64_t kk = k0 + t0 + 128 * e;
+            xs[e] = kk < k ? arow[kk] : make_float2(0.f, 0.f);
+            ys[e] = kk < k ? b[kk * n + j] : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int e = 0; e < kPer; ++e) {
+            const int t = t0 + 128 * e;
+            const float2 x = xs[e], y = ys[e];
             if (F64) {
                 P[0 * CH + t] = acc_t(__dmul_rn(double(x.x), double(y.x)));
                 P[1 * CH + t] = acc_t(__dmul_rn(double(x.y), double(y.y)));
@@ -643,26 +652,33 @@ __global__ void __launch_bounds__(kChainThreads) cgemm_chain_kernel(const float2
                     }
                 } else {
                     // software-pipelined: the next 32 products load while the
-                    // current 32 are chained
-                    const float4* q = reinterpret_cast<const float4*>(P);
-                    float4 cur[8], nxt[8];
+                    // current 32 are chained.  volatile asm pins the order (the
+                    // compiler otherwise sinks the loads next to their use and
+                    // exposes the shared-memory latency on the FADD chain)
+                    float q0[32], q1[32];
+                    const uint32_t base = smem_u32(P);
+                    auto ld32 = [&](float (&q)[32], int g) {
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) cur[u] = q[u];
-                    for (int g = 0; g < CH / 32; ++g) {
-                        if (g + 1 < CH / 32) {
+                        for (int u = 0; u < 8; ++u)
+                            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                                         : "=f"(q[4 * u]), "=f"(q[4 * u + 1]), "=f"(q[4 * u + 2]),
+                                           "=f"(q[4 * u + 3])
+                                         : "r"(base + uint32_t(128 * g + 16 * u)));
+                    };
+                    float pf = float(p);
+                    auto chain32 = [&](const float (&q)[32]) {
 #pragma unroll
-                            for (int u = 0; u < 8; ++u) nxt[u] = q[8 * (g + 1) + u];
-                        }
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            p = acc_t(__fadd_rn(float(p), cur[u].x));
-                            p = acc_t(__fadd_rn(float(p), cur[u].y));
-                            p = acc_t(__fadd_rn(float(p), cur[u].z));
-                            p = acc_t(__fadd_rn(float(p), cur[u].w));
-                        }
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) cur[u] = nxt[u];
+                        for (int u = 0; u < 32; ++u)
+                            asm volatile("add.rn.f32 %0, %0, %1;" : "+f"(pf) : "f"(q[u]));
+                    };
+                    ld32(q0, 0);
+                    for (int g = 0; g < CH / 32; g += 2) {
+                        ld32(q1, g + 1);
+                        chain32(q0);
+                        if (g + 2 < CH / 32) ld32(q0, g + 2);
+                        chain32(q1);
                     }
+                    p = acc_t(pf);
                 }
             } else {
                 for (int t = 0; t < cnt; ++t) {

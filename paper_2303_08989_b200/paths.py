@@ -337,13 +337,18 @@ def remap_path(steps_pre, ids, n_orig, reduced_path):
     return out
 
 
-def reconfigure_path(spec: NetworkSpec, path, k: int = 8, passes: int = 3, seed: int = 0):
+def reconfigure_path(spec: NetworkSpec, path, k: int = 8, passes: int = 3, seed: int = 0,
+                     latency_macs: float = 1e4):
     """Subtree reconfiguration (cotengra's `subtree_reconfigure`): for every
     node of the contraction tree take a frontier of up to `k` sub-pieces and
-    replace the way they are combined by the flop-optimal order (dynamic
+    replace the way they are combined by the cheapest order (dynamic
     programming over subsets).  In a closed network every bond joins exactly
     two tensors, so the open legs of a union of pieces are the XOR of their
-    leg bitmasks.  Returns (path, flops, log2 width)."""
+    leg bitmasks.  Step cost = m n k MACs, plus `latency_macs` per element of
+    k when the step has < 65536 outputs: the FP32 tier must add each output's
+    k products in one sequential RN chain (kernels_scalar.cpp:76-87), so a
+    few-output, long-k step is bound by FADD latency (~4 ns per add, about
+    1e4 MACs of throughput), not by its flops.  Returns (path, flops, log2 width)."""
     rng = random.Random(seed)
     bit, lw = {}, []
     for ls, ds in zip(spec.labels, spec.dims):
@@ -381,7 +386,11 @@ def reconfigure_path(spec: NetworkSpec, path, k: int = 8, passes: int = 3, seed:
     root = nxt - 1
 
     def step_cost(ma, mb):
-        return 2.0 ** ((width(ma) + width(mb) + width(ma ^ mb)) / 2.0)
+        wa, wb, wo = width(ma), width(mb), width(ma ^ mb)
+        c = 2.0 ** ((wa + wb + wo) / 2.0)
+        if latency_macs and wo < 16.0:
+            c += latency_macs * 2.0 ** ((wa + wb - wo) / 2.0)
+        return c
 
     def optimize(node):
         """Reconfigure the top of the subtree at `node`; True if improved."""

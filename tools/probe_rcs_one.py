@@ -15,3 +15,13 @@ cfg = make_config() if mode == "AUTO" else make_config(force=mode)
 z = net.contract(path, cfg).data[0]
 torch.cuda.synchronize()
 print(depth, mode, z)
+import time  # noqa: E402
+from paper_2303_08989_b200.circuits import bitstrings_for as _bs  # noqa: E402
+xs = _bs(49, 10, 1)
+net.selector_batch(path, xs[:1], cfg)
+for rep in range(2):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    net.selector_batch(path, xs, cfg)
+    torch.cuda.synchronize()
+    print(f"rep {rep}: {(time.perf_counter() - t0) / len(xs) * 1e3:.2f} ms per amplitude", flush=True)
