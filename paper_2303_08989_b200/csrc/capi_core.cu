@@ -347,6 +347,18 @@ int tcec_create(int device, tcec_handle* out) {
         return set_error(TCEC_ERR_CUDA, "stream creation failed");
     }
     h->stream = h->own_stream;
+    {
+        // contraction intermediates are stream-ordered allocations of up to
+        // GiBs; keep freed blocks in the pool across synchronizations instead
+        // of returning them to the OS (re-mapping them per slice / bitstring
+        // cost more than the kernels)
+        cudaMemPool_t pool = nullptr;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t keep = ~uint64_t(0);
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
+    }
     if (!h->decisions(64)) {
         delete h;
         return set_error(TCEC_ERR_CUDA, "decision buffer allocation failed");

@@ -498,6 +498,62 @@ __global__ void __launch_bounds__(256) cgemm_fp32_ref_kernel(const float2* __res
     }
 }
 
+// Medium output count, long k (e.g. (256, 64, 2^17) contraction steps): the
+// 64 x 64 register-tiled kernel would occupy only a handful of SMs and the
+// warp-per-output kernel spends its issue slots on shuffles, so here every
+// thread owns ONE output and runs its four chains (kernels_scalar.cpp:76-87)
+// over 32-deep k tiles staged in shared memory: 16 x 16 outputs per block,
+// ascending k per chain -> bit-identical.
+template <bool F64>
+__global__ void __launch_bounds__(256) cgemm_tpo_kernel(const float2* __restrict__ a,
+                                                        const float2* __restrict__ b,
+                                                        float2* __restrict__ c, int64_t m,
+                                                        int64_t n, int64_t k) {
+    using acc_t = typename std::conditional<F64, double, float>::type;
+    __shared__ float2 as[32][17], bs[32][16];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int64_t tiles_n = (n + 15) / 16;
+    const int64_t i0 = (int64_t(blockIdx.x) / tiles_n) * 16, j0 = (int64_t(blockIdx.x) % tiles_n) * 16;
+    const int64_t i = i0 + ty, j = j0 + tx;
+    acc_t p1 = 0, p2 = 0, p3 = 0, p4 = 0;
+    for (int64_t k0 = 0; k0 < k; k0 += 32) {
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int idx = threadIdx.x + 256 * r;
+            const int ar = idx >> 5, ak = idx & 31;   // A: 16 rows x 32 k
+            const int64_t gi = i0 + ar, gk = k0 + ak;
+            as[ak][ar] = (gi < m && gk < k) ? a[gi * k + gk] : make_float2(0.f, 0.f);
+            const int bk = idx >> 4, bj = idx & 15;   // B: 32 k x 16 cols
+            const int64_t gk2 = k0 + bk, gj = j0 + bj;
+            bs[bk][bj] = (gk2 < k && gj < n) ? b[gk2 * n + gj] : make_float2(0.f, 0.f);
+        }
+        __syncthreads();
+        const int kend = (k - k0) < 32 ? int(k - k0) : 32;  // never add padding terms
+        for (int kk = 0; kk < kend; ++kk) {
+            const float2 x = as[kk][ty], y = bs[kk][tx];
+            if (F64) {
+                p1 = acc_t(__dadd_rn(double(p1), __dmul_rn(double(x.x), double(y.x))));
+                p2 = acc_t(__dadd_rn(double(p2), __dmul_rn(double(x.y), double(y.y))));
+                p3 = acc_t(__dadd_rn(double(p3), __dmul_rn(double(x.x), double(y.y))));
+                p4 = acc_t(__dadd_rn(double(p4), __dmul_rn(double(x.y), double(y.x))));
+            } else {
+                p1 = acc_t(__fadd_rn(float(p1), __fmul_rn(x.x, y.x)));
+                p2 = acc_t(__fadd_rn(float(p2), __fmul_rn(x.y, y.y)));
+                p3 = acc_t(__fadd_rn(float(p3), __fmul_rn(x.x, y.y)));
+                p4 = acc_t(__fadd_rn(float(p4), __fmul_rn(x.y, y.x)));
+            }
+        }
+        __syncthreads();
+    }
+    if (i < m && j < n) {
+        if (F64)
+            c[i * n + j] = make_float2(__fsub_rn(__double2float_rn(double(p1)), __double2float_rn(double(p2))),
+                                       __fadd_rn(__double2float_rn(double(p3)), __double2float_rn(double(p4))));
+        else
+            c[i * n + j] = make_float2(__fsub_rn(float(p1), float(p2)), __fadd_rn(float(p3), float(p4)));
+    }
+}
+
 // FP64_ORACLE tier: f64 chains (kernels_scalar.cpp:137-148), each product
 // rounded to f32 (gemm.cpp:111-117), then assembled in f32 (cgemm.cpp:38-44)
 __global__ void cgemm_fp64_kernel(const float2* __restrict__ a, const float2* __restrict__ b,
@@ -1168,6 +1224,12 @@ void launch_cgemm_fp32_ref(const float2* a, const float2* b, float2* c, int64_t 
     }
     if (launch_skinny<false>(a, b, c, m, n, k, s)) return;
     if (k >= 1024 && m * n <= 65536 && tiles < 2 * 148) {
+        if (m * n >= 2048) {
+            // enough outputs for a thread each: one output per thread
+            const int64_t blocks = ((m + 15) / 16) * ((n + 15) / 16);
+            cgemm_tpo_kernel<false><<<unsigned(blocks), 256, 0, s>>>(a, b, c, m, n, k);
+            return;
+        }
         const int64_t warps = m * n;
         cgemm_longk_kernel<false><<<unsigned((warps + 7) / 8), 256, 0, s>>>(a, b, c, m, n, k);
         return;
@@ -1183,6 +1245,11 @@ void launch_cgemm_fp64(const float2* a, const float2* b, float2* c, int64_t m, i
         return;
     }
     if (launch_skinny<true>(a, b, c, m, n, k, s)) return;
+    if (k >= 256 && m * n <= 65536 && m * n >= 2048) {
+        const int64_t blocks = ((m + 15) / 16) * ((n + 15) / 16);
+        cgemm_tpo_kernel<true><<<unsigned(blocks), 256, 0, s>>>(a, b, c, m, n, k);
+        return;
+    }
     if (k >= 256 && m * n <= 65536) {
         cgemm_longk_kernel<true><<<unsigned((m * n + 7) / 8), 256, 0, s>>>(a, b, c, m, n, k);
         return;

@@ -264,7 +264,7 @@ def test_extreme_aspect_shapes(handle, orc, dev, shape):
 
 
 @pytest.mark.parametrize("shape", [(1, 1, 300000), (2, 1, 70000), (3, 2, 50000), (1, 5, 4097), (64, 64, 2048),
-                                   (7, 1, 1025)])
+                                   (7, 1, 1025), (100, 50, 5000), (256, 64, 4099), (33, 70, 1500)])
 def test_long_k_kernels_bit_exact(handle, orc, dev, shape):
     """Few outputs, long k (the dot products of deep circuits): the warp-per-
     output kernels keep the reference's sequential chain order -> bit-exact."""
