@@ -440,25 +440,38 @@ __global__ void __launch_bounds__(256) cgemm_fp32_ref_kernel(const float2* __res
 #pragma unroll
         for (int j = 0; j < 4; ++j) p1[i][j] = p2[i][j] = p3[i][j] = p4[i][j] = 0.0f;
 
+    // register double buffer: the next k tile's global loads are in flight
+    // while the current tile is chained
+    float2 va[4], vb[4];
+    auto load_tile = [&](int64_t k0) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int idx = threadIdx.x + 256 * r;
+            const int ar = idx / SB_K, ak = idx % SB_K;
+            const int64_t gi = i0 + ar, gk = k0 + ak;
+            va[r] = (gi < m && gk < k) ? a[gi * k + gk] : make_float2(0.f, 0.f);
+            const int bk = idx / SB_N, bj = idx % SB_N;
+            const int64_t gk2 = k0 + bk, gj = j0 + bj;
+            vb[r] = (gk2 < k && gj < n) ? b[gk2 * n + gj] : make_float2(0.f, 0.f);
+        }
+    };
+    load_tile(0);
     for (int64_t k0 = 0; k0 < k; k0 += SB_K) {
         // A tile: 64 rows x 16 k; B tile: 16 k x 64 cols (4 complex per thread)
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             const int idx = threadIdx.x + 256 * r;
             const int ar = idx / SB_K, ak = idx % SB_K;
-            const int64_t gi = i0 + ar, gk = k0 + ak;
-            const float2 va = (gi < m && gk < k) ? a[gi * k + gk] : make_float2(0.f, 0.f);
-            sar[ak][ar] = va.x;
-            sai[ak][ar] = va.y;
+            sar[ak][ar] = va[r].x;
+            sai[ak][ar] = va[r].y;
             const int bk = idx / SB_N, bj = idx % SB_N;
-            const int64_t gk2 = k0 + bk, gj = j0 + bj;
-            const float2 vb = (gk2 < k && gj < n) ? b[gk2 * n + gj] : make_float2(0.f, 0.f);
-            sbr[bk][bj] = vb.x;
-            sbi[bk][bj] = vb.y;
+            sbr[bk][bj] = vb[r].x;
+            sbi[bk][bj] = vb[r].y;
         }
         __syncthreads();
+        if (k0 + SB_K < k) load_tile(k0 + SB_K);
         const int kend = (k - k0) < SB_K ? int(k - k0) : SB_K;  // never add padding terms
-        for (int kk = 0; kk < kend; ++kk) {
+        auto step = [&](int kk) {
             const float4 ar4 = *reinterpret_cast<const float4*>(&sar[kk][4 * ty]);
             const float4 ai4 = *reinterpret_cast<const float4*>(&sai[kk][4 * ty]);
             const float4 br4 = *reinterpret_cast<const float4*>(&sbr[kk][4 * tx]);
@@ -474,6 +487,12 @@ __global__ void __launch_bounds__(256) cgemm_fp32_ref_kernel(const float2* __res
                     p3[i][j] = __fadd_rn(p3[i][j], __fmul_rn(ar[i], bi[j]));
                     p4[i][j] = __fadd_rn(p4[i][j], __fmul_rn(ai[i], br[j]));
                 }
+        };
+        if (kend == SB_K) {
+#pragma unroll
+            for (int kk = 0; kk < SB_K; ++kk) step(kk);
+        } else {
+            for (int kk = 0; kk < kend; ++kk) step(kk);
         }
         __syncthreads();
     }
