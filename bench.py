@@ -515,7 +515,8 @@ def load_or_build_plan(spec, cycles, mode, log=None):
     from paper_2303_08989_b200.slicing import find_slices
     sys.path.insert(0, os.path.join(ROOT, "tools"))
     from make_plan import spec_hash
-    fn = os.path.join(ROOT, "paper_2303_08989_b200", "plans", f"sycamore_m{cycles}.json")
+    fn = os.environ.get("TCEC_PLAN_FILE") or os.path.join(ROOT, "paper_2303_08989_b200", "plans",
+                                                          f"sycamore_m{cycles}.json")
     if mode == "plan" and os.path.exists(fn):
         d = json.load(open(fn))
         if d["spec_hash"] == spec_hash(spec):

@@ -338,13 +338,14 @@ def remap_path(steps_pre, ids, n_orig, reduced_path):
 
 
 def reconfigure_path(spec: NetworkSpec, path, k: int = 8, passes: int = 3, seed: int = 0,
-                     latency_macs: float = 1e4):
+                     latency_macs: float = 1e4, time_model: bool = False):
     """Subtree reconfiguration (cotengra's `subtree_reconfigure`): for every
     node of the contraction tree take a frontier of up to `k` sub-pieces and
     replace the way they are combined by the cheapest order (dynamic
     programming over subsets).  In a closed network every bond joins exactly
     two tensors, so the open legs of a union of pieces are the XOR of their
-    leg bitmasks.  Step cost = m n k MACs, plus `latency_macs` per element of
+    leg bitmasks.  `time_model` scores a step by its estimated B200 time
+    (tensor-core tiers faster, HBM floor) instead of its MACs.  Step cost = m n k MACs, plus `latency_macs` per element of
     k when the step has < 65536 outputs: the FP32 tier must add each output's
     k products in one sequential RN chain (kernels_scalar.cpp:76-87), so a
     few-output, long-k step is bound by FADD latency (~4 ns per add, about
@@ -386,11 +387,7 @@ def reconfigure_path(spec: NetworkSpec, path, k: int = 8, passes: int = 3, seed:
     root = nxt - 1
 
     def step_cost(ma, mb):
-        wa, wb, wo = width(ma), width(mb), width(ma ^ mb)
-        c = 2.0 ** ((wa + wb + wo) / 2.0)
-        if latency_macs and wo < 16.0:
-            c += latency_macs * 2.0 ** ((wa + wb - wo) / 2.0)
-        return c
+        return model_step_cost(width(ma), width(mb), width(ma ^ mb), time_model, latency_macs)
 
     def optimize(node):
         """Reconfigure the top of the subtree at `node`; True if improved."""
@@ -512,7 +509,8 @@ def _sliced_cost(spec: NetworkSpec, path, drop):
     return f * float(np.prod([dims_of[l] for l in drop])) if drop else f, w
 
 
-def find_slices_exact(spec: NetworkSpec, path, max_log2: float, candidates: int = 32):
+def find_slices_exact(spec: NetworkSpec, path, max_log2: float, candidates: int = 32,
+                      time_model: bool = False):
     """Greedy slicer with exact evaluation: among the bonds of the currently
     largest intermediates, slice the one that minimises the total flops over
     all slices, until the per-slice width is <= max_log2."""
@@ -549,29 +547,33 @@ def find_slices_exact(spec: NetworkSpec, path, max_log2: float, candidates: int 
         cl = sorted(cand, key=lambda l: (-cand[l], l))[:candidates]
         best = None
         for l in cl:
-            f, w = _sliced_cost(spec, path, sliced + [l])
+            if time_model:
+                f, w = path_model_cost(spec, path, sliced + [l]), 0.0
+            else:
+                f, w = _sliced_cost(spec, path, sliced + [l])
             key = (f, w, l)
             if best is None or key < best[0]:
                 best = (key, l)
         sliced.append(best[1])
 
 
-def slice_and_reconfigure(spec: NetworkSpec, path, max_log2: float, k: int = 10, rounds: int = 3):
+def slice_and_reconfigure(spec: NetworkSpec, path, max_log2: float, k: int = 10, rounds: int = 3,
+                          time_model: bool = False):
     """Alternate exact slicing and subtree reconfiguration of the sliced network
     (cotengra's slice-and-reconfigure).  Returns (path, sliced, total flops,
     per-slice log2 width)."""
     sliced = []
     for _ in range(rounds):
-        sliced = find_slices_exact(spec, path, max_log2)
+        sliced = find_slices_exact(spec, path, max_log2, time_model=time_model)
         sub = _drop_labels(spec, sliced)
-        path, _, _ = reconfigure_path(sub, path, k=k, passes=3)
-    sliced = find_slices_exact(spec, path, max_log2)
+        path, _, _ = reconfigure_path(sub, path, k=k, passes=3, time_model=time_model)
+    sliced = find_slices_exact(spec, path, max_log2, time_model=time_model)
     f, w = _sliced_cost(spec, path, sliced)
     return path, sliced, f, w
 
 
 def hyper_path(spec: NetworkSpec, max_log2: float = 28.0, trials: int = 2, seed: int = 0,
-               leaf: int = 14, k: int = 10, log=None):
+               leaf: int = 14, k: int = 10, log=None, time_model: bool = False):
     """Sliced contraction plan for large circuits:
     presimplify (absorb rank <= 2 tensors) -> divisive partition tree
     (`partition_path`) -> subtree reconfiguration -> exact slicing alternated
@@ -584,10 +586,53 @@ def hyper_path(spec: NetworkSpec, max_log2: float = 28.0, trials: int = 2, seed:
         s = seed + 1000 * t
         p, f, w = partition_path(red, trials=8, leaf=leaf, max_width=60, imbalance=(0.2, 0.8), seed=s)
         p, f, w = reconfigure_path(red, p, k=k, passes=3, seed=s)
-        p, sliced, fs, ws = slice_and_reconfigure(red, p, max_log2, k=k, rounds=2)
+        p, sliced, fs, ws = slice_and_reconfigure(red, p, max_log2, k=k, rounds=2, time_model=time_model)
+        score = path_model_cost(red, p, sliced, True) if time_model else fs
         if log:
-            log(f"trial {t}: unsliced 2^{w:.0f} {f:.3g} flops -> {len(sliced)} sliced, 2^{ws:.0f}, {fs:.3g} flops")
-        if best is None or fs < best[2]:
-            best = (p, sliced, fs, ws)
-    p, sliced, fs, ws = best
+            log(f"trial {t}: unsliced 2^{w:.0f} {f:.3g} flops -> {len(sliced)} sliced, 2^{ws:.0f}, "
+                f"{fs:.3g} flops, model time {path_model_cost(red, p, sliced, True):.3g}")
+        if best is None or score < best[4]:
+            best = (p, sliced, fs, ws, score)
+    p, sliced, fs, ws, _ = best
     return remap_path(pre, ids, len(spec.labels), p), sliced, fs, ws
+
+
+def model_step_cost(wa: float, wb: float, wo: float, time_model: bool = True,
+                    latency_macs: float = 1e4) -> float:
+    """Cost of one pairwise step from the log2 sizes of its operands and result
+    (FP32-tier MAC units).  MACs = 2^((wa+wb+wo)/2); with `time_model` the
+    tensor-core tiers of dispatch_cgemm (precsel.cpp:275-306) are ~8x (TF32TCEC,
+    min(m,n,k) >= 512) / ~14x (AUTO, >= 2048) faster than the bit-exact SIMT
+    tier and every step pays an HBM floor of 8 B per operand/result element;
+    few-output long-k steps pay the FP32 chain latency (~1e4 MACs per add)."""
+    wk = (wa + wb - wo) / 2.0
+    c = 2.0 ** ((wa + wb + wo) / 2.0)
+    if time_model:
+        wmin = min(wa - wk, wb - wk, wk)
+        if wmin >= 11:
+            c /= 14.0
+        elif wmin >= 9:
+            c /= 8.0
+        c = max(c, 4.0 * (2.0 ** wa + 2.0 ** wb + 2.0 ** wo))
+    if latency_macs and wo < 16.0:
+        c += latency_macs * 2.0 ** wk
+    return c
+
+
+def path_model_cost(spec: NetworkSpec, path, drop=(), time_model: bool = True) -> float:
+    """Sum of model_step_cost over the path with `drop` sliced, times the
+    number of slices."""
+    sub = _drop_labels(spec, drop)
+    dims_of = {l: d for ls, ds in zip(spec.labels, spec.dims) for l, d in zip(ls, ds)}
+    live = {i: list(ls) for i, ls in enumerate(sub.labels)}
+    nxt = len(sub.labels)
+    total = 0.0
+    for a, b in path:
+        la, lb = live.pop(a), live.pop(b)
+        sa, sb = set(la), set(lb)
+        out = [l for l in la if l not in sb] + [l for l in lb if l not in sa]
+        total += model_step_cost(_log2size([dims_of[l] for l in la]), _log2size([dims_of[l] for l in lb]),
+                                 _log2size([dims_of[l] for l in out]), time_model)
+        live[nxt] = out
+        nxt += 1
+    return total * float(np.prod([dims_of[l] for l in drop])) if drop else total
