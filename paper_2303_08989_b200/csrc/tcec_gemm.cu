@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
                      const __grid_constant__ CUtensorMap map_bhi,
                      const __grid_constant__ CUtensorMap map_blo, float* __restrict__ c,
                      int m, int n2, int kp, const DevDecision* __restrict__ dec, int kind_fixed,
-                     int corrected, int flush_kblocks) {
+                     int corrected, int flush_kblocks, float* __restrict__ partial, int kb_per) {
     using T = Traits<FMT>;
     // device-side mode selection: the kernel of the unselected format exits
     // (the paper's "both kernels launched, one exits early")
@@ -112,7 +112,13 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
     const int n_blk = (id % group) / gsize;
     const int m0 = m_blk * BM, n0 = n_blk * BN;
 
-    const int nkb = kp / T::kBK;
+    // split-K (gridDim.y > 1, few tiles and long K): this CTA chains k-blocks
+    // [kb_base, kb_base + nkb) and writes an un-descaled fp32 partial that
+    // split_reduce_kernel sums in split order
+    const int nkb_all = kp / T::kBK;
+    const int per = FMT == kTf32 ? 2 * kb_per : kb_per;  // kb_per counts 64-element f16 blocks
+    const int kb_base = partial ? int(blockIdx.y) * per : 0;
+    const int nkb = partial ? min(per, nkb_all - kb_base) : nkb_all;
     const int F = flush_kblocks > 0 ? flush_kblocks : (nkb > 0 ? nkb : 1);
     const int nchunks = (nkb + F - 1) / F;
     const uint32_t stage_bytes = uint32_t(corrected ? 4 : 2) * kTileBytes;
@@ -150,7 +156,7 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
                 const uint32_t ph = (kb / kStages) & 1;
                 mbar_wait(&tail->empty[s], ph ^ 1);
                 mbar_expect_tx(&tail->full[s], stage_bytes);
-                const int kx = kb * T::kBK;
+                const int kx = (kb_base + kb) * T::kBK;
                 tma_load_2d(tile(s, 0), &map_ahi, &tail->full[s], kx, m0);
                 tma_load_2d(tile(s, 2), &map_bhi, &tail->full[s], kx, n0);
                 if (corrected) {
@@ -242,12 +248,13 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
                     acc[32 * cb + i] = __fadd_rn(acc[32 * cb + i], __fmul_rn(v[i], 0x1.0p-11f));
             }
         }
-        const bool scaled = kind == kKindFp16Scaled && (dec->scale_a + dec->scale_b) != 0;
+        const bool scaled = !partial && kind == kKindFp16Scaled && (dec->scale_a + dec->scale_b) != 0;
         if (scaled) {
             const double f = ldexp(1.0, -(dec->scale_a + dec->scale_b));
 #pragma unroll
             for (int i = 0; i < kCols; ++i) acc[i] = scale_pow2(acc[i], f);
         }
+        if (partial) c = partial + size_t(blockIdx.y) * size_t(m) * size_t(n2);
         // stage the tile in the (now idle) operand smem, then store coalesced rows
         float* ctile = reinterpret_cast<float*>(smem);
         float* myrow = ctile + size_t(rloc) * kCStride + kCols * half;
@@ -275,6 +282,22 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc<kTmemCols>(tmem);
+    }
+}
+
+// split-K epilogue: C = descale(sum of the partials in split order), RN
+__global__ void __launch_bounds__(256) split_reduce_kernel(const float* __restrict__ partial,
+                                                           float* __restrict__ c, int64_t count,
+                                                           int splits, const DevDecision* __restrict__ dec,
+                                                           int kind_fixed) {
+    const int kind = kind_fixed >= 0 ? kind_fixed : dec->kind;
+    const bool scaled = kind == kKindFp16Scaled && (dec->scale_a + dec->scale_b) != 0;
+    const double f = scaled ? ldexp(1.0, -(dec->scale_a + dec->scale_b)) : 1.0;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        float s = partial[i];
+        for (int y = 1; y < splits; ++y) s = __fadd_rn(s, partial[size_t(y) * size_t(count) + size_t(i)]);
+        c[i] = scaled ? scale_pow2(s, f) : s;
     }
 }
 
@@ -1216,9 +1239,10 @@ int launch_fmt(const TcecGemmArgs& g, cudaStream_t s) {
             g.corrected, g.flush_kblocks);
     } else {
         const int64_t tiles = ((g.m + BM - 1) / BM) * ((g.n2 + BN - 1) / BN);
-        tcec_gemm_kernel<FMT><<<unsigned(tiles), kThreadsGemm, kSmemBytes, s>>>(
+        const dim3 grid(unsigned(tiles), unsigned(g.partial ? g.splits : 1));
+        tcec_gemm_kernel<FMT><<<grid, kThreadsGemm, kSmemBytes, s>>>(
             mah, mal, mbh, mbl, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed,
-            g.corrected, g.flush_kblocks);
+            g.corrected, g.flush_kblocks, g.partial, g.kb_per);
     }
     return int(cudaGetLastError());
 }
@@ -1256,9 +1280,56 @@ int resolve_gemm_variant(int requested, int64_t m, int64_t n2, int sm_count) {
     return wide_ctas >= sm_count ? kVariantWide : kVariantSingle;
 }
 
-int launch_tcec_gemm(const TcecGemmArgs& g, cudaStream_t s) {
+static int launch_formats(const TcecGemmArgs& g, cudaStream_t s);
+
+int launch_tcec_gemm(const TcecGemmArgs& g_in, cudaStream_t s) {
     if (!get_encode()) return int(cudaErrorNotSupported);
-    if (g.m <= 0 || g.n2 <= 0) return 0;
+    if (g_in.m <= 0 || g_in.n2 <= 0) return 0;
+    TcecGemmArgs g = g_in;
+    g.partial = nullptr;
+    g.splits = 1;
+    g.kb_per = 0;
+    if (g.pair == kVariantSingle) {
+        // few 128 x 128 tiles and a long K (e.g. (512, 512, 2^19) contraction
+        // steps): split K so the grid covers the SMs twice
+        const int64_t tiles = ((g.m + BM - 1) / BM) * ((g.n2 + BN - 1) / BN);
+        const int bk = (g.fmt == kTf32 || g.fmt < 0) ? 32 : 64;  // the finer format decides
+        const int64_t nkb = g.kp / bk;
+        const int sms = g.sms > 1 ? g.sms : 148;
+        if (tiles < sms && nkb >= 16) {
+            int64_t want = std::min<int64_t>((2 * sms + tiles - 1) / tiles, nkb / 8);
+            if (want >= 2) {
+                // k-blocks per split in units of the f16 block (2 tf32 blocks),
+                // so both format kernels cut K at the same element
+                const int64_t nkb16 = g.kp / 64;
+                const int64_t per16 = (nkb16 + want - 1) / want;
+                const int splits = int((nkb16 + per16 - 1) / per16);
+                if (splits >= 2) {
+                    const size_t bytes = size_t(splits) * size_t(g.m) * size_t(g.n2) * 4;
+                    if (cudaMallocAsync(reinterpret_cast<void**>(&g.partial), bytes, s) == cudaSuccess) {
+                        g.splits = splits;
+                        g.kb_per = int(per16);  // f16 units; the tf32 kernel doubles it
+                    } else {
+                        cudaGetLastError();
+                        g.partial = nullptr;
+                    }
+                }
+            }
+        }
+    }
+    int e = launch_formats(g, s);
+    if (!e && g.partial) {
+        const int64_t count = g.m * g.n2;
+        const int64_t blocks = std::min<int64_t>((count + 255) / 256, 148 * 16);
+        split_reduce_kernel<<<unsigned(blocks), 256, 0, s>>>(g.partial, g.c, count, g.splits, g.d,
+                                                            g.kind_fixed);
+        e = int(cudaGetLastError());
+    }
+    if (g.partial) cudaFreeAsync(g.partial, s);
+    return e;
+}
+
+static int launch_formats(const TcecGemmArgs& g, cudaStream_t s) {
     if (g.fmt < 0) {
         // device-decided format: the wide kernel branches on the decision; the
         // other variants launch both formats and the unselected one exits

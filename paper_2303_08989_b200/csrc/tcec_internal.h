@@ -89,6 +89,8 @@ struct TcecGemmArgs {
     int flush_kblocks;                    // RN flush interval of the main term, 0 = none
     int pair;                             // resolved kernel variant (kVariantSingle/Pair/Wide)
     int sms;                              // SM count (persistent grid size)
+    float* partial;                       // split-K partials (set by launch_tcec_gemm)
+    int splits, kb_per;                   // split count, 64-element k-blocks per split
 };
 // tcgen05 kernel variants (tcec_set_gemm_variant): auto picks wide when its
 // 256 x 256 pair tiles fill the SMs, else single

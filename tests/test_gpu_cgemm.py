@@ -12,7 +12,7 @@ import pytest
 import torch
 
 import oracle as O
-from paper_2303_08989_b200 import InvalidArgument, ShapeMismatch
+from paper_2303_08989_b200 import InvalidArgument, SelectionPolicy, ShapeMismatch
 from tests.conftest import bits
 from tests.golden.recipes import matrix_recipe
 
@@ -292,3 +292,22 @@ def test_skinny_kernels_bit_exact(handle, orc, dev, shape):
         c, _ = handle.cgemm(ad, bd, mode)
         cr, _ = orc.cgemm(a, b, mode)
         assert np.array_equal(bits(c.cpu().numpy().view(np.float32)), bits(cr.view(np.float32))), mode
+
+
+@pytest.mark.parametrize("shape", [(200, 150, 9000), (512, 512, 4096), (130, 70, 20000)])
+def test_split_k_few_tiles_long_k(handle, orc, dev, shape):
+    """Few 128x128 tiles and a long K run split-K (partials summed in split
+    order, descaled once): still within the reference bar for every TCEC
+    mode, the descaled FP16TCEC_SCALED path included."""
+    m, n, k = shape
+    a = matrix_recipe("uniform", m, k, 61 + m)
+    b = matrix_recipe("uniform", k, n, 67 + n)
+    ref = orc.cgemm_oracle(a, b)
+    err_ref = relerr(orc.cgemm(a, b, "FP32_REF")[0], ref)
+    ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    for mode in ("FP16TCEC", "TF32TCEC"):
+        c, _ = handle.cgemm(ad, bd, mode)
+        assert relerr(c.cpu().numpy(), ref) <= TOL_FACTOR * err_ref, mode
+    c, res = handle.dispatch_cgemm(ad * 2.0 ** -20, bd, SelectionPolicy(size_auto=64, size_tf32=32))
+    assert "FP16TCEC_SCALED" in res.line
+    assert relerr(c.cpu().numpy() * 2.0 ** 20, ref) <= TOL_FACTOR * err_ref
