@@ -1291,13 +1291,18 @@ int launch_tcec_gemm(const TcecGemmArgs& g_in, cudaStream_t s) {
     g.kb_per = 0;
     if (g.pair == kVariantSingle) {
         // few 128 x 128 tiles and a long K (e.g. (512, 512, 2^19) contraction
-        // steps): split K so the grid covers the SMs twice
+        // steps): split K so the grid covers the SMs several times
         const int64_t tiles = ((g.m + BM - 1) / BM) * ((g.n2 + BN - 1) / BN);
         const int bk = (g.fmt == kTf32 || g.fmt < 0) ? 32 : 64;  // the finer format decides
         const int64_t nkb = g.kp / bk;
         const int sms = g.sms > 1 ? g.sms : 148;
         if (tiles < sms && nkb >= 16) {
-            int64_t want = std::min<int64_t>((2 * sms + tiles - 1) / tiles, nkb / 8);
+            static const int waves = [] {
+                const char* e = std::getenv("TCEC_SPLIT_WAVES");  // tuning override
+                const int v = e ? std::atoi(e) : 0;
+                return v > 0 ? v : 8;  // swept 1/2/4/8: more waves balance best
+            }();
+            int64_t want = std::min<int64_t>((waves * sms + tiles - 1) / tiles, nkb / 8);
             if (want >= 2) {
                 // k-blocks per split in units of the f16 block (2 tf32 blocks),
                 // so both format kernels cut K at the same element
