@@ -138,7 +138,7 @@ size_t plan_workspace(const DispatchPlan& p, int64_t m, int64_t n) {
 // Launch the device pipeline of one dispatch (no host synchronization).
 int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t m, int64_t n,
                     int64_t k, const tcec_dispatch_config_t& cfg, const DispatchPlan& p,
-                    DevDecision* d, void* ws) {
+                    DevDecision* d, void* ws, const ChunkHook* hook) {
     cudaStream_t s = h.stream;
     if (p.tier == kTierInvalid) return set_error(TCEC_ERR_INVALID_ARGUMENT, "unknown forced mode");
     if (p.tier == kTierTc && cfg.k_tile < 1)
@@ -173,12 +173,12 @@ int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t
         launch_cgemm_fp32_ref(reinterpret_cast<const float2*>(a), reinterpret_cast<const float2*>(b),
                               reinterpret_cast<float2*>(c), m, n, k, s);
         if (prof) cudaEventRecord(h.ev[3], s);
-        return TCEC_OK;
+        return hook && hook->done ? hook->done(hook->ctx, 0, m) : TCEC_OK;
     case kTierFp64:
         launch_cgemm_fp64(reinterpret_cast<const float2*>(a), reinterpret_cast<const float2*>(b),
                           reinterpret_cast<float2*>(c), m, n, k, s);
         if (prof) cudaEventRecord(h.ev[3], s);
-        return TCEC_OK;
+        return hook && hook->done ? hook->done(hook->ctx, 0, m) : TCEC_OK;
     default: break;
     }
     // tensor-core tier: operand preparation + tcgen05 GEMM(s)
@@ -208,14 +208,26 @@ int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t
     g.flush_kblocks = p.corrected ? h.flush_kblocks : 0;
     g.pair = resolve_gemm_variant(h.gemm_pair, m, 2 * n, h.sm_count);
     g.sms = h.sm_count;
-    if (p.kind < 0 && !p.forced_scaled) {
-        g.fmt = -1;  // format chosen by the device decision
-        const int e = launch_tcec_gemm(g, s);
-        if (e) return cuda_error(cudaError_t(e), "tcec_gemm auto");
-    } else {
-        g.fmt = (p.kind == kKindTf32) ? kTf32 : kFp16;
-        const int e = launch_tcec_gemm(g, s);
-        if (e) return cuda_error(cudaError_t(e), g.fmt == kTf32 ? "tcec_gemm tf32" : "tcec_gemm f16");
+    g.fmt = (p.kind < 0 && !p.forced_scaled) ? -1  // format chosen by the device decision
+                                             : (p.kind == kKindTf32 ? kTf32 : kFp16);
+    // row chunks (host-buffer API): only the wide kernel indexes into A' by row
+    int chunks = hook ? std::max(1, hook->chunks) : 1;
+    if (g.pair != kVariantWide) chunks = 1;
+    const int64_t rows_per = round_up((m + chunks - 1) / chunks, 256);
+    g.a_rows = m;
+    for (int64_t r0 = 0; r0 < m; r0 += rows_per) {
+        const int64_t r1 = std::min(m, r0 + rows_per);
+        TcecGemmArgs gc = g;
+        gc.m = r1 - r0;
+        gc.a_row_off = r0;
+        gc.c = c + r0 * 2 * n;
+        const int e = launch_tcec_gemm(gc, s);
+        if (e) return cuda_error(cudaError_t(e), g.fmt < 0 ? "tcec_gemm auto"
+                                                 : (g.fmt == kTf32 ? "tcec_gemm tf32" : "tcec_gemm f16"));
+        if (hook && hook->done) {
+            const int rc = hook->done(hook->ctx, r0, r1);
+            if (rc) return rc;
+        }
     }
     if (prof) cudaEventRecord(h.ev[3], s);
     return TCEC_OK;
@@ -298,6 +310,9 @@ tcec_handle_s::~tcec_handle_s() {
     if (dec_host) cudaFreeHost(dec_host);
     if (scratch_host) cudaFreeHost(scratch_host);
     if (own_stream) cudaStreamDestroy(own_stream);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    for (auto& e : chunk_ev)
+        if (e) cudaEventDestroy(e);
     for (auto& e : ev)
         if (e) cudaEventDestroy(e);
 }
@@ -653,11 +668,65 @@ int tcec_dispatch_cgemm_host(tcec_handle h, const void* a, const void* b, void* 
     void* dc = base + ra + rb;
     CUDA_TRY(cudaMemcpyAsync(da, a, ab, cudaMemcpyHostToDevice, h->stream));
     CUDA_TRY(cudaMemcpyAsync(db, b, bb, cudaMemcpyHostToDevice, h->stream));
-    const int rc = tcec_dispatch_cgemm(h, da, db, dc, m, n, k, cfg, res);
+    if (!cfg || !res) return set_error(TCEC_ERR_INVALID_ARGUMENT, "null argument");
+    if (m < 0 || n < 0 || k < 0) return set_error(TCEC_ERR_SHAPE_MISMATCH, "negative extent");
+    // the GEMM runs in row chunks; each finished chunk of C is copied back on
+    // a second stream while the next chunk computes
+    if (!h->copy_stream) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+        for (auto& e : h->chunk_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const DispatchPlan p = plan_dispatch(m, n, k, *cfg);
+    void* ws = nullptr;
+    const size_t wsb = plan_workspace(p, m, n);
+    if (wsb) {
+        ws = h->workspace(wsb);
+        if (!ws) return set_error(TCEC_ERR_CUDA, "workspace allocation failed");
+    }
+    struct Ctx {
+        tcec_handle h;
+        uint8_t* c_host;
+        const uint8_t* dc;
+        int64_t row_bytes;
+        int used;
+        cudaError_t err;
+    } ctx{h, static_cast<uint8_t*>(c), static_cast<const uint8_t*>(dc), n * 8, 0, cudaSuccess};
+    ChunkHook hook;
+    hook.chunks = m >= 8192 ? 4 : 1;
+    hook.ctx = &ctx;
+    hook.done = [](void* vp, int64_t r0, int64_t r1) -> int {
+        Ctx& x = *static_cast<Ctx*>(vp);
+        cudaEvent_t ev = x.h->chunk_ev[x.used++ % 8];
+        cudaError_t e = cudaEventRecord(ev, x.h->stream);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(x.h->copy_stream, ev, 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(x.c_host + r0 * x.row_bytes, x.dc + r0 * x.row_bytes,
+                                size_t((r1 - r0) * x.row_bytes), cudaMemcpyDeviceToHost,
+                                x.h->copy_stream);
+        if (e != cudaSuccess) {
+            x.err = e;
+            return cuda_error(e, "chunk copy");
+        }
+        return TCEC_OK;
+    };
+    DevDecision* d = h->dec;
+    int rc = launch_dispatch(*h, static_cast<const float*>(da), static_cast<const float*>(db),
+                             static_cast<float*>(dc), m, n, k, *cfg, p, d, ws, &hook);
     if (rc) return rc;
-    CUDA_TRY(cudaMemcpyAsync(c, dc, cb, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaGetLastError());
+    if (ctx.used == 0 && m > 0 && n > 0)
+        CUDA_TRY(cudaMemcpyAsync(c, dc, cb, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaMemcpyAsync(h->dec_host, d, sizeof(DevDecision), cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(cudaStreamSynchronize(h->stream));
-    return TCEC_OK;
+    CUDA_TRY(cudaStreamSynchronize(h->copy_stream));
+    if (h->prof && h->ev[0]) {
+        for (int i = 0; i < 3; ++i) {
+            float ms = 0.0f;
+            if (cudaEventElapsedTime(&ms, h->ev[i], h->ev[i + 1]) == cudaSuccess) h->prof_ms[i] += ms;
+        }
+        ++h->prof_count;
+    }
+    return finish_dispatch(p, *h->dec_host, m, n, k, res);
 }
 
 // ---------------------------------------------------------------- permute

@@ -883,7 +883,8 @@ static_assert(size_t(BM) * kNpCStride * 4 <= size_t(kNpStages) * kNpStageBytes,
 template <int FMT>
 __device__ __forceinline__ void wide_body(const WideMaps& mp, float* __restrict__ c, int m, int n2,
                                           int kp, const DevDecision* __restrict__ dec, int kind,
-                                          int corrected, int flush_kblocks, int group_m) {
+                                          int corrected, int flush_kblocks, int group_m,
+                                          int a_row_off) {
     using T = Traits<FMT>;
     constexpr uint32_t kIdescHalf = umma_idesc<FMT, 2 * BM, 128>();
     constexpr uint32_t kIdescFull = umma_idesc<FMT, 2 * BM, kNpBN>();
@@ -951,10 +952,10 @@ __device__ __forceinline__ void wide_body(const WideMaps& mp, float* __restrict_
                 mbar_wait(&tail->empty[s], ((kb / kNpStages) & 1) ^ 1);
                 if (leader) mbar_expect_tx(&tail->full[s], 2 * cta_bytes);
                 const int kx = kb * T::kBK;
-                tma_load_2d_pair(tile(s, 0), &mp.ahi, &tail->full[s], kx, m0);
+                tma_load_2d_pair(tile(s, 0), &mp.ahi, &tail->full[s], kx, m0 + a_row_off);
                 tma_load_2d_pair(tile(s, 2), &mp.bhi, &tail->full[s], kx, nb0);
                 if (corrected) {
-                    tma_load_2d_pair(tile(s, 1), &mp.alo, &tail->full[s], kx, m0);
+                    tma_load_2d_pair(tile(s, 1), &mp.alo, &tail->full[s], kx, m0 + a_row_off);
                     tma_load_2d_pair(tile(s, 3), &mp.blo, &tail->full[s], kx, nb0);
                 }
             }
@@ -1111,11 +1112,11 @@ template <int FMT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
     tcec_gemm_wide_kernel(const __grid_constant__ WideMaps maps, float* __restrict__ c, int m,
                           int n2, int kp, const DevDecision* __restrict__ dec, int kind_fixed,
-                          int corrected, int flush_kblocks, int group_m) {
+                          int corrected, int flush_kblocks, int group_m, int a_row_off) {
     const int kind = kind_fixed >= 0 ? kind_fixed : dec->kind;
     const bool mine = FMT == kTf32 ? kind == kKindTf32 : (kind == kKindFp16 || kind == kKindFp16Scaled);
     if (!mine) return;  // both CTAs of the pair read the same decision
-    wide_body<FMT>(maps, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m);
+    wide_body<FMT>(maps, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off);
 }
 
 // format decided on the device (AUTO): one launch that runs the selected
@@ -1124,12 +1125,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
     tcec_gemm_wide_auto_kernel(const __grid_constant__ WideMaps maps16,
                                const __grid_constant__ WideMaps maps32, float* __restrict__ c,
                                int m, int n2, int kp, const DevDecision* __restrict__ dec,
-                               int corrected, int flush_kblocks, int group_m) {
+                               int corrected, int flush_kblocks, int group_m, int a_row_off) {
     const int kind = dec->kind;
     if (kind == kKindTf32)
-        wide_body<kTf32>(maps32, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m);
+        wide_body<kTf32>(maps32, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off);
     else if (kind == kKindFp16 || kind == kKindFp16Scaled)
-        wide_body<kFp16>(maps16, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m);
+        wide_body<kFp16>(maps16, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -1166,7 +1167,8 @@ bool make_map(CUtensorMap* map, const void* base, int fmt, int64_t rows, int64_t
 bool make_wide_maps(WideMaps* w, const TcecGemmArgs& g, int fmt) {
     const void* alo = g.corrected ? g.a_lo : g.a_hi;
     const void* blo = g.corrected ? g.b_lo : g.b_hi;
-    return make_map(&w->ahi, g.a_hi, fmt, g.m, g.kp, 128u) && make_map(&w->alo, alo, fmt, g.m, g.kp, 128u) &&
+    const int64_t arows = g.a_rows > 0 ? g.a_rows : g.m;  // the whole A' (row chunks index into it)
+    return make_map(&w->ahi, g.a_hi, fmt, arows, g.kp, 128u) && make_map(&w->alo, alo, fmt, arows, g.kp, 128u) &&
            make_map(&w->bhi, g.b_hi, fmt, g.n2, g.kp, 128u) && make_map(&w->blo, blo, fmt, g.n2, g.kp, 128u);
 }
 
@@ -1218,7 +1220,7 @@ int launch_fmt(const TcecGemmArgs& g, cudaStream_t s) {
         if (g.pair == kVariantWide)
             tcec_gemm_wide_kernel<FMT><<<wide_tiles_grid(g), kThreadsGemm, kNpSmemBytes, s>>>(
                 w, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed, g.corrected, g.flush_kblocks,
-                wide_group_m());
+                wide_group_m(), int(g.a_row_off));
         else
             tcec_gemm_widep_kernel<FMT><<<wide_grid(g), kThreadsGemm, kWideSmemBytes, s>>>(
                 w, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed, g.corrected, g.flush_kblocks);
@@ -1265,7 +1267,7 @@ int launch_wide_auto(const TcecGemmArgs& g, cudaStream_t s) {
     if (g.pair == kVariantWide)
         tcec_gemm_wide_auto_kernel<<<wide_tiles_grid(g), kThreadsGemm, kNpSmemBytes, s>>>(
             w16, w32, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.corrected, g.flush_kblocks,
-            wide_group_m());
+            wide_group_m(), int(g.a_row_off));
     else
         tcec_gemm_widep_auto_kernel<<<wide_grid(g), kThreadsGemm, kWideSmemBytes, s>>>(
             w16, w32, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.corrected, g.flush_kblocks);

@@ -27,6 +27,8 @@ struct tcec_handle_s {
     void* io = nullptr;
     size_t io_bytes = 0;
     void* scratch_host = nullptr;  // pinned 4 KiB
+    cudaStream_t copy_stream = nullptr;  // D2H of finished row chunks (host-buffer API)
+    cudaEvent_t chunk_ev[8] = {};
     // stage profiling (tcec_profile_*): CUDA events around the stages of a
     // dispatched CGEMM, accumulated after each synchronous dispatch
     bool prof = false;
@@ -62,9 +64,18 @@ struct DispatchPlan {
 
 DispatchPlan plan_dispatch(int64_t m, int64_t n, int64_t k, const tcec_dispatch_config_t& cfg);
 size_t plan_workspace(const DispatchPlan& p, int64_t m, int64_t n);
+// Optional row-chunk hook of launch_dispatch: the GEMM of a tensor-core
+// dispatch is launched in `chunks` row blocks and done(r0, r1) is called after
+// each block is enqueued (the host-buffer entry point overlaps the D2H copy of
+// finished rows with the GEMM of the next ones).
+struct ChunkHook {
+    int chunks = 1;
+    int (*done)(void* ctx, int64_t r0, int64_t r1) = nullptr;
+    void* ctx = nullptr;
+};
 int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t m, int64_t n,
                     int64_t k, const tcec_dispatch_config_t& cfg, const DispatchPlan& p,
-                    DevDecision* d, void* ws);
+                    DevDecision* d, void* ws, const ChunkHook* hook = nullptr);
 int finish_dispatch(const DispatchPlan& p, const DevDecision& dd, int64_t m, int64_t n, int64_t k,
                     tcec_dispatch_result_t* res);
 void format_line(char* out, size_t cap, int64_t m, int64_t n, int64_t k, const char* label, int sa,

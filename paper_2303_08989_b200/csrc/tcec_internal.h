@@ -89,6 +89,7 @@ struct TcecGemmArgs {
     int flush_kblocks;                    // RN flush interval of the main term, 0 = none
     int pair;                             // resolved kernel variant (kVariantSingle/Pair/Wide)
     int sms;                              // SM count (persistent grid size)
+    int64_t a_row_off, a_rows;            // row chunk of A' (wide kernel): first row, rows of the whole A'
     float* partial;                       // split-K partials (set by launch_tcec_gemm)
     int splits, kb_per;                   // split count, 64-element k-blocks per split
 };
