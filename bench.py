@@ -807,7 +807,7 @@ def gemm_kernel_name(m, n, kind, sm_count=148, auto=True):
     """The tcgen05 kernel an AUTO dispatch runs (resolve_gemm_variant in tcec_gemm.cu):
     the wide cta_group::2 kernel branching on the device decision when its tiles
     fill the SMs, else both single-CTA formats (the unselected one exits)."""
-    wide = 2 * -(-m // 256) * -(-2 * n // 256) >= sm_count
+    wide = 2 * -(-m // 256) * -(-2 * n // 256) >= sm_count or (2 * n) // 64 >= 256
     fmt = "tf32" if kind == "TF32TCEC" else "f16"
     if wide:
         return f"tcec_gemm_wide_auto_kernel ({fmt} path)" if auto else f"tcec_gemm_wide_kernel<{fmt}>"

@@ -206,7 +206,7 @@ int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t
     g.kind_fixed = p.kind;
     g.corrected = p.corrected;
     g.flush_kblocks = p.corrected ? h.flush_kblocks : 0;
-    g.pair = resolve_gemm_variant(h.gemm_pair, m, 2 * n, h.sm_count);
+    g.pair = resolve_gemm_variant(h.gemm_pair, m, 2 * n, p.kp, h.sm_count);
     g.sms = h.sm_count;
     g.fmt = (p.kind < 0 && !p.forced_scaled) ? -1  // format chosen by the device decision
                                              : (p.kind == kKindTf32 ? kTf32 : kFp16);

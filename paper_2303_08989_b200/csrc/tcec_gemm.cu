@@ -884,7 +884,7 @@ template <int FMT>
 __device__ __forceinline__ void wide_body(const WideMaps& mp, float* __restrict__ c, int m, int n2,
                                           int kp, const DevDecision* __restrict__ dec, int kind,
                                           int corrected, int flush_kblocks, int group_m,
-                                          int a_row_off) {
+                                          int a_row_off, float* __restrict__ partial, int kb_per) {
     using T = Traits<FMT>;
     constexpr uint32_t kIdescHalf = umma_idesc<FMT, 2 * BM, 128>();
     constexpr uint32_t kIdescFull = umma_idesc<FMT, 2 * BM, kNpBN>();
@@ -912,7 +912,12 @@ __device__ __forceinline__ void wide_body(const WideMaps& mp, float* __restrict_
     const int m0 = m_blk * 2 * BM + int(rank) * BM;  // this CTA's 128 rows
     const int n0 = n_blk * kNpBN;                  // the pair's 256 columns
 
-    const int nkb = kp / T::kBK;
+    // split-K (gridDim.y > 1): k-blocks [kb_base, kb_base + nkb), un-descaled
+    // fp32 partial per split (summed in split order by split_reduce_kernel)
+    const int nkb_all = kp / T::kBK;
+    const int per = FMT == kTf32 ? 2 * kb_per : kb_per;  // kb_per counts 64-element f16 blocks
+    const int kb_base = partial ? int(blockIdx.y) * per : 0;
+    const int nkb = partial ? min(per, nkb_all - kb_base) : nkb_all;
     const int F = flush_kblocks > 0 ? flush_kblocks : (nkb > 0 ? nkb : 1);
     const int nchunks = (nkb + F - 1) / F;
     const uint32_t cta_bytes = uint32_t(corrected ? 4 : 2) * kTileBytes;
@@ -951,7 +956,7 @@ __device__ __forceinline__ void wide_body(const WideMaps& mp, float* __restrict_
                 const int s = kb % kNpStages;
                 mbar_wait(&tail->empty[s], ((kb / kNpStages) & 1) ^ 1);
                 if (leader) mbar_expect_tx(&tail->full[s], 2 * cta_bytes);
-                const int kx = kb * T::kBK;
+                const int kx = (kb_base + kb) * T::kBK;
                 tma_load_2d_pair(tile(s, 0), &mp.ahi, &tail->full[s], kx, m0 + a_row_off);
                 tma_load_2d_pair(tile(s, 2), &mp.bhi, &tail->full[s], kx, nb0);
                 if (corrected) {
@@ -1065,7 +1070,8 @@ __device__ __forceinline__ void wide_body(const WideMaps& mp, float* __restrict_
                 }
             }
         }
-        const bool scaled = kind == kKindFp16Scaled && (dec->scale_a + dec->scale_b) != 0;
+        const bool scaled = !partial && kind == kKindFp16Scaled && (dec->scale_a + dec->scale_b) != 0;
+        if (partial) c = partial + size_t(blockIdx.y) * size_t(m) * size_t(n2);
         if (scaled) {
             const double f = ldexp(1.0, -(dec->scale_a + dec->scale_b));
 #pragma unroll
@@ -1112,11 +1118,13 @@ template <int FMT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
     tcec_gemm_wide_kernel(const __grid_constant__ WideMaps maps, float* __restrict__ c, int m,
                           int n2, int kp, const DevDecision* __restrict__ dec, int kind_fixed,
-                          int corrected, int flush_kblocks, int group_m, int a_row_off) {
+                          int corrected, int flush_kblocks, int group_m, int a_row_off,
+                          float* __restrict__ partial, int kb_per) {
     const int kind = kind_fixed >= 0 ? kind_fixed : dec->kind;
     const bool mine = FMT == kTf32 ? kind == kKindTf32 : (kind == kKindFp16 || kind == kKindFp16Scaled);
     if (!mine) return;  // both CTAs of the pair read the same decision
-    wide_body<FMT>(maps, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off);
+    wide_body<FMT>(maps, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off, partial,
+                   kb_per);
 }
 
 // format decided on the device (AUTO): one launch that runs the selected
@@ -1125,12 +1133,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
     tcec_gemm_wide_auto_kernel(const __grid_constant__ WideMaps maps16,
                                const __grid_constant__ WideMaps maps32, float* __restrict__ c,
                                int m, int n2, int kp, const DevDecision* __restrict__ dec,
-                               int corrected, int flush_kblocks, int group_m, int a_row_off) {
+                               int corrected, int flush_kblocks, int group_m, int a_row_off,
+                               float* __restrict__ partial, int kb_per) {
     const int kind = dec->kind;
     if (kind == kKindTf32)
-        wide_body<kTf32>(maps32, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off);
+        wide_body<kTf32>(maps32, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off,
+                         partial, kb_per);
     else if (kind == kKindFp16 || kind == kKindFp16Scaled)
-        wide_body<kFp16>(maps16, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off);
+        wide_body<kFp16>(maps16, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off,
+                         partial, kb_per);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -1218,9 +1229,10 @@ int launch_fmt(const TcecGemmArgs& g, cudaStream_t s) {
         WideMaps w;
         if (!make_wide_maps(&w, g, FMT)) return int(cudaErrorInvalidValue);
         if (g.pair == kVariantWide)
-            tcec_gemm_wide_kernel<FMT><<<wide_tiles_grid(g), kThreadsGemm, kNpSmemBytes, s>>>(
+            tcec_gemm_wide_kernel<FMT><<<dim3(wide_tiles_grid(g), unsigned(g.partial ? g.splits : 1)),
+                                         kThreadsGemm, kNpSmemBytes, s>>>(
                 w, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed, g.corrected, g.flush_kblocks,
-                wide_group_m(), int(g.a_row_off));
+                wide_group_m(), int(g.a_row_off), g.partial, g.kb_per);
         else
             tcec_gemm_widep_kernel<FMT><<<wide_grid(g), kThreadsGemm, kWideSmemBytes, s>>>(
                 w, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed, g.corrected, g.flush_kblocks);
@@ -1265,9 +1277,10 @@ int launch_wide_auto(const TcecGemmArgs& g, cudaStream_t s) {
     if (!make_wide_maps(&w16, g, kFp16) || !make_wide_maps(&w32, g, kTf32))
         return int(cudaErrorInvalidValue);
     if (g.pair == kVariantWide)
-        tcec_gemm_wide_auto_kernel<<<wide_tiles_grid(g), kThreadsGemm, kNpSmemBytes, s>>>(
+        tcec_gemm_wide_auto_kernel<<<dim3(wide_tiles_grid(g), unsigned(g.partial ? g.splits : 1)),
+                                     kThreadsGemm, kNpSmemBytes, s>>>(
             w16, w32, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.corrected, g.flush_kblocks,
-            wide_group_m(), int(g.a_row_off));
+            wide_group_m(), int(g.a_row_off), g.partial, g.kb_per);
     else
         tcec_gemm_widep_auto_kernel<<<wide_grid(g), kThreadsGemm, kWideSmemBytes, s>>>(
             w16, w32, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.corrected, g.flush_kblocks);
@@ -1276,10 +1289,11 @@ int launch_wide_auto(const TcecGemmArgs& g, cudaStream_t s) {
 
 }  // namespace
 
-int resolve_gemm_variant(int requested, int64_t m, int64_t n2, int sm_count) {
+int resolve_gemm_variant(int requested, int64_t m, int64_t n2, int64_t kp, int sm_count) {
     if (requested != kVariantAuto) return requested;
     const int64_t wide_ctas = 2 * ((m + 2 * BM - 1) / (2 * BM)) * ((n2 + kWideBN - 1) / kWideBN);
-    return wide_ctas >= sm_count ? kVariantWide : kVariantSingle;
+    // the 256 x 256 tiles fill the SMs, or K is long enough for split-K to fill them
+    return (wide_ctas >= sm_count || kp / 64 >= 256) ? kVariantWide : kVariantSingle;
 }
 
 static int launch_formats(const TcecGemmArgs& g, cudaStream_t s);
@@ -1291,10 +1305,12 @@ int launch_tcec_gemm(const TcecGemmArgs& g_in, cudaStream_t s) {
     g.partial = nullptr;
     g.splits = 1;
     g.kb_per = 0;
-    if (g.pair == kVariantSingle) {
-        // few 128 x 128 tiles and a long K (e.g. (512, 512, 2^19) contraction
-        // steps): split K so the grid covers the SMs several times
-        const int64_t tiles = ((g.m + BM - 1) / BM) * ((g.n2 + BN - 1) / BN);
+    if (g.pair == kVariantSingle || g.pair == kVariantWide) {
+        // few tiles and a long K (e.g. (512, 512, 2^19) contraction steps):
+        // split K so the grid covers the SMs several times
+        const int64_t tiles = g.pair == kVariantWide
+                                  ? int64_t(wide_tiles_grid(g))
+                                  : ((g.m + BM - 1) / BM) * ((g.n2 + BN - 1) / BN);
         const int bk = (g.fmt == kTf32 || g.fmt < 0) ? 32 : 64;  // the finer format decides
         const int64_t nkb = g.kp / bk;
         const int sms = g.sms > 1 ? g.sms : 148;

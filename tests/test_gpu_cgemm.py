@@ -294,8 +294,9 @@ def test_skinny_kernels_bit_exact(handle, orc, dev, shape):
         assert np.array_equal(bits(c.cpu().numpy().view(np.float32)), bits(cr.view(np.float32))), mode
 
 
-@pytest.mark.parametrize("shape", [(200, 150, 9000), (512, 512, 4096), (130, 70, 20000)])
-def test_split_k_few_tiles_long_k(handle, orc, dev, shape):
+@pytest.mark.parametrize("shape", [(200, 150, 9000), (512, 512, 4096), (130, 70, 20000), (300, 260, 9000)])
+@pytest.mark.parametrize("variant", ["single", "wide", "auto"])
+def test_split_k_few_tiles_long_k(handle, orc, dev, shape, variant):
     """Few 128x128 tiles and a long K run split-K (partials summed in split
     order, descaled once): still within the reference bar for every TCEC
     mode, the descaled FP16TCEC_SCALED path included."""
@@ -305,9 +306,13 @@ def test_split_k_few_tiles_long_k(handle, orc, dev, shape):
     ref = orc.cgemm_oracle(a, b)
     err_ref = relerr(orc.cgemm(a, b, "FP32_REF")[0], ref)
     ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
-    for mode in ("FP16TCEC", "TF32TCEC"):
-        c, _ = handle.cgemm(ad, bd, mode)
-        assert relerr(c.cpu().numpy(), ref) <= TOL_FACTOR * err_ref, mode
-    c, res = handle.dispatch_cgemm(ad * 2.0 ** -20, bd, SelectionPolicy(size_auto=64, size_tf32=32))
-    assert "FP16TCEC_SCALED" in res.line
-    assert relerr(c.cpu().numpy() * 2.0 ** 20, ref) <= TOL_FACTOR * err_ref
+    handle.set_gemm_variant(variant)
+    try:
+        for mode in ("FP16TCEC", "TF32TCEC"):
+            c, _ = handle.cgemm(ad, bd, mode)
+            assert relerr(c.cpu().numpy(), ref) <= TOL_FACTOR * err_ref, mode
+        c, res = handle.dispatch_cgemm(ad * 2.0 ** -20, bd, SelectionPolicy(size_auto=64, size_tf32=32))
+        assert "FP16TCEC_SCALED" in res.line
+        assert relerr(c.cpu().numpy() * 2.0 ** 20, ref) <= TOL_FACTOR * err_ref
+    finally:
+        handle.set_gemm_variant("auto")
