@@ -985,7 +985,8 @@ __global__ void __launch_bounds__(256) permute_tiled_kernel(const float2* __rest
 // staged through XOR-swizzled shared memory, so reads and writes are both
 // coalesced 256-B runs.  The remaining bits index the tiles.  Offsets inside a
 // tile come from per-block shared tables built once (persistent grid).
-constexpr int kBitTileMax = 10;  // tile bits
+constexpr int kBitTileMax = 12;   // tile bits: up to 4096 elements (32 KB)
+constexpr int kBitThreads = 512;  // 8 elements per thread in flight
 
 struct BitPermDesc {
     int nbits;                  // log2(total)
@@ -999,31 +1000,39 @@ struct BitPermDesc {
 
 TCEC_DEV uint32_t bp_swz(uint32_t s) { return s ^ (((s >> 4) ^ (s >> 8)) & 15u); }
 
-__global__ void __launch_bounds__(256) permute_bits_kernel(const float2* __restrict__ src,
-                                                           float2* __restrict__ dst,
-                                                           const BitPermDesc d) {
+__global__ void __launch_bounds__(kBitThreads) permute_bits_kernel(const float2* __restrict__ src,
+                                                                   float2* __restrict__ dst,
+                                                                   const BitPermDesc d) {
     __shared__ float2 tile[1 << kBitTileMax];
-    __shared__ uint64_t in_off[1 << kBitTileMax], out_off[1 << kBitTileMax];
-    __shared__ uint16_t s_of_u[1 << kBitTileMax];
+    // offsets are sums over index bits, so each table splits into a 6-bit low
+    // and a 6-bit high half: off(t) = lo[t & 63] + hi[t >> 6]
+    __shared__ uint64_t in_lo[64], in_hi[64], out_lo[64], out_hi[64];
+    __shared__ uint16_t s_lo[64], s_hi[64];
     const int T = 1 << d.ntile;
-    // tables: t enumerates the tile in input-bit order (smem index), u in
-    // output-bit order; out_off[t] / in_off[t] are the element offsets
-    for (int t = threadIdx.x; t < T; t += blockDim.x) {
-        uint64_t io = 0, oo = 0;
-        for (int b = 0; b < d.ntile; ++b)
-            if ((t >> b) & 1) {
-                io |= uint64_t(1) << d.tile_in[b];
-                oo |= uint64_t(1) << d.tile_out[b];
+    if (threadIdx.x < 64) {
+        const int v = threadIdx.x;
+        uint64_t il = 0, ih = 0, ol = 0, oh = 0;
+        uint32_t sl = 0, sh = 0;
+        for (int bt = 0; bt < d.ntile; ++bt) {
+            if (bt < 6 && ((v >> bt) & 1)) {
+                il |= uint64_t(1) << d.tile_in[bt];
+                ol |= uint64_t(1) << d.tile_out[bt];
             }
-        in_off[t] = io;
-        out_off[t] = oo;
-    }
-    __syncthreads();
-    // u -> t: u enumerates the tile bits by output position
-    for (int u = threadIdx.x; u < T; u += blockDim.x) {
-        uint32_t t = 0;
-        for (int b = 0; b < d.ntile; ++b) t |= ((uint32_t(u) >> d.out_rank[b]) & 1u) << b;
-        s_of_u[u] = uint16_t(t);
+            if (bt >= 6 && ((v >> (bt - 6)) & 1)) {
+                ih |= uint64_t(1) << d.tile_in[bt];
+                oh |= uint64_t(1) << d.tile_out[bt];
+            }
+            // u -> t: output rank r of tile bit bt sits at bit r of u
+            const int r = d.out_rank[bt];
+            if (r < 6 && ((v >> r) & 1)) sl |= 1u << bt;
+            if (r >= 6 && ((v >> (r - 6)) & 1)) sh |= 1u << bt;
+        }
+        in_lo[v] = il;
+        in_hi[v] = ih;
+        out_lo[v] = ol;
+        out_hi[v] = oh;
+        s_lo[v] = uint16_t(sl);
+        s_hi[v] = uint16_t(sh);
     }
     __syncthreads();
     const int64_t ntiles = int64_t(1) << d.nrest;
@@ -1036,23 +1045,24 @@ __global__ void __launch_bounds__(256) permute_bits_kernel(const float2* __restr
                 bo |= int64_t(1) << d.rest_out[r];
             }
     };
+    auto in_off = [&](int t) { return in_lo[t & 63] + in_hi[t >> 6]; };
     // software pipeline: the next tile's loads are in flight while this
-    // tile's stores drain (T <= 1024 = 4 elements per thread)
-    constexpr int kPer = (1 << kBitTileMax) / 256;
+    // tile's stores drain
+    constexpr int kPer = (1 << kBitTileMax) / kBitThreads;
     float2 reg[kPer];
     int64_t blk = blockIdx.x, base_in = 0, base_out = 0;
     if (blk < ntiles) {
         bases(blk, base_in, base_out);
 #pragma unroll
         for (int e = 0; e < kPer; ++e) {
-            const int t = threadIdx.x + 256 * e;
-            if (t < T) reg[e] = __ldcs(src + base_in + in_off[t]);
+            const int t = threadIdx.x + kBitThreads * e;
+            if (t < T) reg[e] = __ldcs(src + base_in + in_off(t));
         }
     }
     while (blk < ntiles) {
 #pragma unroll
         for (int e = 0; e < kPer; ++e) {
-            const int t = threadIdx.x + 256 * e;
+            const int t = threadIdx.x + kBitThreads * e;
             if (t < T) tile[bp_swz(uint32_t(t))] = reg[e];
         }
         __syncthreads();
@@ -1062,13 +1072,17 @@ __global__ void __launch_bounds__(256) permute_bits_kernel(const float2* __restr
             bases(next, base_in, base_out);
 #pragma unroll
             for (int e = 0; e < kPer; ++e) {
-                const int t = threadIdx.x + 256 * e;
-                if (t < T) reg[e] = __ldcs(src + base_in + in_off[t]);
+                const int t = threadIdx.x + kBitThreads * e;
+                if (t < T) reg[e] = __ldcs(src + base_in + in_off(t));
             }
         }
-        for (int u = threadIdx.x; u < T; u += blockDim.x) {
-            const uint32_t t = s_of_u[u];
-            __stcs(dst + out_base + out_off[t], tile[bp_swz(t)]);
+#pragma unroll
+        for (int e = 0; e < kPer; ++e) {
+            const int u = threadIdx.x + kBitThreads * e;
+            if (u < T) {
+                const uint32_t t = uint32_t(s_lo[u & 63]) | uint32_t(s_hi[u >> 6]);
+                __stcs(dst + out_base + out_lo[t & 63] + out_hi[t >> 6], tile[bp_swz(t)]);
+            }
         }
         __syncthreads();
         blk = next;
@@ -1352,8 +1366,8 @@ void launch_permute(const float2* src, float2* dst, int rank, const int64_t* old
                 bd.out_rank[b] = int8_t(rk);
             }
             const int64_t ntiles = int64_t(1) << bd.nrest;
-            const int64_t g = ntiles < 148 * 8 ? ntiles : 148 * 8;
-            permute_bits_kernel<<<unsigned(g), 256, 0, s>>>(src, dst, bd);
+            const int64_t g = ntiles < 148 * 4 ? ntiles : 148 * 4;
+            permute_bits_kernel<<<unsigned(g), kBitThreads, 0, s>>>(src, dst, bd);
             return;
         }
     }
