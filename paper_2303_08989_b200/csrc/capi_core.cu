@@ -218,6 +218,7 @@ int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t
     for (int64_t r0 = 0; r0 < m; r0 += rows_per) {
         const int64_t r1 = std::min(m, r0 + rows_per);
         TcecGemmArgs gc = g;
+        gc.no_split = chunks > 1;  // a chunk must compute exactly what the whole launch would
         gc.m = r1 - r0;
         gc.a_row_off = r0;
         gc.c = c + r0 * 2 * n;

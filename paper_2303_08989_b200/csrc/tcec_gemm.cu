@@ -1305,7 +1305,7 @@ int launch_tcec_gemm(const TcecGemmArgs& g_in, cudaStream_t s) {
     g.partial = nullptr;
     g.splits = 1;
     g.kb_per = 0;
-    if (g.pair == kVariantSingle || g.pair == kVariantWide) {
+    if (!g.no_split && (g.pair == kVariantSingle || g.pair == kVariantWide)) {
         // few tiles and a long K (e.g. (512, 512, 2^19) contraction steps):
         // split K so the grid covers the SMs several times
         const int64_t tiles = g.pair == kVariantWide

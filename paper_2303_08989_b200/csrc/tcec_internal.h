@@ -92,6 +92,7 @@ struct TcecGemmArgs {
     int64_t a_row_off, a_rows;            // row chunk of A' (wide kernel): first row, rows of the whole A'
     float* partial;                       // split-K partials (set by launch_tcec_gemm)
     int splits, kb_per;                   // split count, 64-element k-blocks per split
+    int no_split;                         // 1: never split K (row-chunked launches must match the one-launch bits)
 };
 // tcgen05 kernel variants (tcec_set_gemm_variant): auto picks wide when its
 // 256 x 256 pair tiles fill the SMs, else single
