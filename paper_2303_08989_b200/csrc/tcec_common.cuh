@@ -213,9 +213,13 @@ TCEC_DEV uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
     return r;
 }
 
+// arrive on an mbarrier of another CTA of the cluster.  Default semantics
+// (release at CTA scope, as cute's ClusterBarrier::arrive): the arrivals only
+// hand TMEM buffers back, which tcgen05.fence::before_thread_sync orders; an
+// explicit .release.cluster costs a GPU-scope MEMBAR per arrive (measured:
+// ~15 % of the warp stall samples of a small-k wide GEMM)
 TCEC_DEV void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-                 : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
 // TMA into this CTA's smem whose transaction bytes land on the pair leader's
