@@ -1320,7 +1320,9 @@ int launch_tcec_gemm(const TcecGemmArgs& g_in, cudaStream_t s) {
                 const int v = e ? std::atoi(e) : 0;
                 return v > 0 ? v : 8;  // swept 1/2/4/8: more waves balance best
             }();
-            int64_t want = std::min<int64_t>((waves * sms + tiles - 1) / tiles, nkb / 8);
+            // every split keeps >= 32 f16 k-blocks (2048 K' elements) so the
+            // partial round trip stays small against its MMA time
+            int64_t want = std::min<int64_t>((waves * sms + tiles - 1) / tiles, (g.kp / 64) / 32);
             if (want >= 2) {
                 // k-blocks per split in units of the f16 block (2 tf32 blocks),
                 // so both format kernels cut K at the same element
