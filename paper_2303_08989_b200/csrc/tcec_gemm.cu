@@ -1292,7 +1292,11 @@ int launch_wide_auto(const TcecGemmArgs& g, cudaStream_t s) {
 int resolve_gemm_variant(int requested, int64_t m, int64_t n2, int64_t kp, int sm_count) {
     if (requested != kVariantAuto) return requested;
     const int64_t wide_ctas = 2 * ((m + 2 * BM - 1) / (2 * BM)) * ((n2 + kWideBN - 1) / kWideBN);
-    // the 256 x 256 tiles fill the SMs, or K is long enough for split-K to fill them
+    // the 256 x 256 tiles fill the SMs, or K is long enough for split-K to fill
+    // them; with <= 8 k-blocks per tile the persistent pairs win (the next
+    // tile's loads and first MMAs overlap the epilogue: 2048x16384x64 TF32
+    // 0.176 -> 0.154 ms)
+    if (wide_ctas >= sm_count && kp / 64 <= 8) return kVariantWidePersistent;
     return (wide_ctas >= sm_count || kp / 64 >= 256) ? kVariantWide : kVariantSingle;
 }
 
