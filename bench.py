@@ -327,7 +327,10 @@ def run_ours(args):
                          "sample": "16 random rows vs complex128"},
             "e2e": {"value": round(world * flops / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
                     "h2d_bytes_per_step": 2 * n * n * 8, "d2h_bytes_per_step": n * n * 8},
-            "gpu_launches": 7 * args.steps,
+            # per AUTO dispatch: stats1, stats2, select, prep_a, prep_b and ONE
+            # tcgen05 GEMM (the wide kernel branches on the device decision),
+            # plus a cudaMemsetAsync of the decision slot
+            "gpu_launches": 6 * args.steps,
             "clocks": clk.summary(),
         }
         if cpu:
