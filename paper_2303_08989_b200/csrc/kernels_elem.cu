@@ -297,6 +297,68 @@ TCEC_DEV void convert(float x, const PrepMode& pm, double factor, bool corrected
     }
 }
 
+// Vectorised fast path of convert() for N components (N even).  The scale is
+// one float multiply by 2^s when 2^s is a float (s in [-149, 127]): that is
+// one rounding of the same exact product as float(double(x) * 2^s)
+// (scale_buf, kernels_scalar.cpp:34-40).  When no magnitude exceeds the
+// format maximum (and none is NaN/Inf -- checked on the bit patterns), the
+// split needs no saturation test: FP16 via paired cvt.rn.f16x2.f32, TF32 via
+// the integer round-to-nearest-even at bit 13 (lowprec.hpp:58-88).  Otherwise
+// the whole group takes the per-component reference path.  Outputs hi/lo as
+// floats holding FP16/TF32 values (bit-identical to convert()).
+template <int N>
+TCEC_DEV void convert_n(float (&x)[N], const PrepMode& pm, double factor, float fs, bool corrected,
+                        float (&h)[N], float (&l)[N], unsigned& ovf, unsigned& bad) {
+    if (pm.scale != 0) {
+        if (pm.scale >= -149 && pm.scale <= 127) {
+#pragma unroll
+            for (int e = 0; e < N; ++e) x[e] = __fmul_rn(x[e], fs);
+        } else {
+#pragma unroll
+            for (int e = 0; e < N; ++e) x[e] = scale_pow2(x[e], factor);
+        }
+    }
+    uint32_t mb = 0;
+#pragma unroll
+    for (int e = 0; e < N; ++e) mb = max(mb, __float_as_uint(x[e]) & 0x7FFFFFFFu);
+    if (pm.scale != 0) bad |= mb >= 0x7F800000u ? 1u : 0u;
+    const uint32_t lim = pm.fmt == kFp16 ? __float_as_uint(kFp16Max) : __float_as_uint(kTf32Max);
+    if (mb > lim) {
+        PrepMode ns = pm;
+        ns.scale = 0;
+#pragma unroll
+        for (int e = 0; e < N; ++e) convert(x[e], ns, 1.0, corrected, h[e], l[e], ovf, bad);
+        return;
+    }
+    if (pm.fmt == kFp16) {
+#pragma unroll
+        for (int e = 0; e < N; e += 2) {
+            const float2 hf = __half22float2(__floats2half2_rn(x[e], x[e + 1]));
+            h[e] = hf.x;
+            h[e + 1] = hf.y;
+            if (corrected) {
+                const float2 lf = __half22float2(__floats2half2_rn(__fmul_rn(__fsub_rn(x[e], hf.x), 2048.0f),
+                                                                   __fmul_rn(__fsub_rn(x[e + 1], hf.y), 2048.0f)));
+                l[e] = lf.x;
+                l[e + 1] = lf.y;
+            } else {
+                l[e] = l[e + 1] = 0.0f;
+            }
+        }
+    } else {
+        auto rne = [](float v) {
+            uint32_t b = __float_as_uint(v);
+            b += 0xFFFu + ((b >> 13) & 1u);
+            return __uint_as_float(b & ~0x1FFFu);
+        };
+#pragma unroll
+        for (int e = 0; e < N; ++e) {
+            h[e] = rne(x[e]);
+            l[e] = corrected ? rne(__fmul_rn(__fsub_rn(x[e], h[e]), 2048.0f)) : 0.0f;
+        }
+    }
+}
+
 // A (m x k complex) -> K-major m x kp; each thread converts 8 consecutive
 // real components of one row (16 B of f16 or 32 B of tf32 per output plane)
 __global__ void __launch_bounds__(kThreads) prep_a_kernel(const float* __restrict__ a, int64_t m,
@@ -306,6 +368,7 @@ __global__ void __launch_bounds__(kThreads) prep_a_kernel(const float* __restric
     const PrepMode pm = prep_mode(d, kind_fixed, false);
     if (!pm.active) return;
     const double factor = ldexp(1.0, pm.scale);
+    const float fs = (pm.scale >= -149 && pm.scale <= 127) ? ldexpf(1.0f, pm.scale) : 1.0f;
     const int64_t chunks_per_row = kp / 8;
     const int64_t total = m * chunks_per_row;
     unsigned ovf = 0, bad = 0;
@@ -325,8 +388,7 @@ __global__ void __launch_bounds__(kThreads) prep_a_kernel(const float* __restric
             for (int e = 0; e < 8; ++e) x[e] = (col + e < k2) ? a[row * k2 + col + e] : 0.0f;
         }
         float h[8], l[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) convert(x[e], pm, factor, corrected, h[e], l[e], ovf, bad);
+        convert_n<8>(x, pm, factor, fs, corrected, h, l, ovf, bad);
         if (pm.fmt == kFp16) {
             __half2 hh[4], ll[4];
 #pragma unroll
@@ -359,7 +421,13 @@ __global__ void __launch_bounds__(kThreads) prep_a_kernel(const float* __restric
 // B (k x n complex) -> B'^T (2n x kp, K-major) with the complex block expansion
 //   row 2j   : (Br, -Bi) at columns (2kk, 2kk+1)
 //   row 2j+1 : ( Bi,  Br)
-// via a 32x32 shared-memory transpose tile (coalesced reads along j, writes along kk)
+// Persistent blocks walk 64 (kk) x 32 (j) tiles: coalesced 256-B reads along
+// j into a [j][kk] shared tile (row stride 66 elements keeps the 16-B reads of
+// the write phase aligned and conflict-free), then each warp writes whole
+// 64-kk row segments -- 256 B (FP16) / 512 B (TF32) per store instruction
+// and plane -- converting two kk per lane with the vectorised split.
+constexpr int kPrepBKK = 64, kPrepBJ = 32, kPrepBStride = kPrepBKK + 2;
+
 __global__ void __launch_bounds__(256) prep_b_kernel(const float2* __restrict__ b, int64_t k,
                                                      int64_t n, int64_t kp, void* hi_v,
                                                      void* lo_v, const DevDecision* d,
@@ -367,48 +435,60 @@ __global__ void __launch_bounds__(256) prep_b_kernel(const float2* __restrict__ 
     const PrepMode pm = prep_mode(d, kind_fixed, true);
     if (!pm.active) return;
     const double factor = ldexp(1.0, pm.scale);
-    __shared__ float2 tile[32][33];
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-    // 1-D grid (no 65535 limit on tall or long operands): x = kk_tile * tiles_j + j_tile
-    const int64_t tiles_j = (n + 31) / 32;
-    const int64_t j0 = (int64_t(blockIdx.x) % tiles_j) * 32, kk0 = (int64_t(blockIdx.x) / tiles_j) * 32;
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const int64_t kk = kk0 + ty + 8 * r, j = j0 + tx;
-        tile[ty + 8 * r][tx] = (kk < k && j < n) ? b[kk * n + j] : make_float2(0.0f, 0.0f);
-    }
-    __syncthreads();
+    const float fs = (pm.scale >= -149 && pm.scale <= 127) ? ldexpf(1.0f, pm.scale) : 1.0f;
+    __shared__ __align__(16) float2 tile[kPrepBJ][kPrepBStride];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;  // 8 warps
+    const int64_t tiles_j = (n + kPrepBJ - 1) / kPrepBJ;
+    const int64_t kk_cols = kp / 2;                               // complex K extent incl. padding
+    const int64_t tiles_kk = (kk_cols + kPrepBKK - 1) / kPrepBKK;
+    const int64_t ntiles = tiles_j * tiles_kk;
     unsigned ovf = 0, bad = 0;
-    const int64_t kk = kk0 + tx;
-    const int64_t col = 2 * kk;
-    const bool in_cols = col < kp;
-    for (int jj = ty; jj < 32; jj += 8) {
-        const int64_t j = j0 + jj;
-        if (j >= n || !in_cols) continue;
-        const float2 v = tile[tx][jj];
-        float rh, rl, ih, il;
-        convert(v.x, pm, factor, corrected, rh, rl, ovf, bad);
-        convert(v.y, pm, factor, corrected, ih, il, ovf, bad);
-        const int64_t r0 = (2 * j) * kp + col, r1 = (2 * j + 1) * kp + col;
-        if (pm.fmt == kFp16) {
-            __half* hp = static_cast<__half*>(hi_v);
-            *reinterpret_cast<__half2*>(hp + r0) = __floats2half2_rn(rh, -ih);
-            *reinterpret_cast<__half2*>(hp + r1) = __floats2half2_rn(ih, rh);
-            if (corrected) {
-                __half* lp = static_cast<__half*>(lo_v);
-                *reinterpret_cast<__half2*>(lp + r0) = __floats2half2_rn(rl, -il);
-                *reinterpret_cast<__half2*>(lp + r1) = __floats2half2_rn(il, rl);
-            }
-        } else {
-            float* hp = static_cast<float*>(hi_v);
-            *reinterpret_cast<float2*>(hp + r0) = make_float2(rh, -ih);
-            *reinterpret_cast<float2*>(hp + r1) = make_float2(ih, rh);
-            if (corrected) {
-                float* lp = static_cast<float*>(lo_v);
-                *reinterpret_cast<float2*>(lp + r0) = make_float2(rl, -il);
-                *reinterpret_cast<float2*>(lp + r1) = make_float2(il, rl);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t j0 = (t % tiles_j) * kPrepBJ, kk0 = (t / tiles_j) * kPrepBKK;
+        // load: warp w reads rows kk0 + w, w+8, ... (32 consecutive j each)
+#pragma unroll
+        for (int r = 0; r < kPrepBKK / 8; ++r) {
+            const int kk = warp + 8 * r;
+            const int64_t gk = kk0 + kk, gj = j0 + lane;
+            tile[lane][kk] = (gk < k && gj < n) ? __ldcs(b + gk * n + gj) : make_float2(0.0f, 0.0f);
+        }
+        __syncthreads();
+        // write: warp w owns j = j0 + w, w+8, ...; lane owns kk0 + 2 lane, +1
+        const int64_t col = 2 * (kk0 + 2 * lane);                 // K' column of (kk0 + 2 lane, re)
+        if (col < kp) {
+            for (int jj = warp; jj < kPrepBJ; jj += 8) {
+                const int64_t j = j0 + jj;
+                if (j >= n) break;
+                const float4 v = *reinterpret_cast<const float4*>(&tile[jj][2 * lane]);
+                float xv[4] = {v.x, v.y, v.z, v.w}, hv[4], lv[4];   // (re0, im0, re1, im1)
+                convert_n<4>(xv, pm, factor, fs, corrected, hv, lv, ovf, bad);
+                const int64_t r0 = (2 * j) * kp + col, r1 = (2 * j + 1) * kp + col;
+                if (pm.fmt == kFp16) {
+                    __half* hp = static_cast<__half*>(hi_v);
+                    __half2 q0[2] = {__floats2half2_rn(hv[0], -hv[1]), __floats2half2_rn(hv[2], -hv[3])};
+                    __half2 q1[2] = {__floats2half2_rn(hv[1], hv[0]), __floats2half2_rn(hv[3], hv[2])};
+                    *reinterpret_cast<uint2*>(hp + r0) = *reinterpret_cast<uint2*>(q0);
+                    *reinterpret_cast<uint2*>(hp + r1) = *reinterpret_cast<uint2*>(q1);
+                    if (corrected) {
+                        __half* lp = static_cast<__half*>(lo_v);
+                        __half2 w0[2] = {__floats2half2_rn(lv[0], -lv[1]), __floats2half2_rn(lv[2], -lv[3])};
+                        __half2 w1[2] = {__floats2half2_rn(lv[1], lv[0]), __floats2half2_rn(lv[3], lv[2])};
+                        *reinterpret_cast<uint2*>(lp + r0) = *reinterpret_cast<uint2*>(w0);
+                        *reinterpret_cast<uint2*>(lp + r1) = *reinterpret_cast<uint2*>(w1);
+                    }
+                } else {
+                    float* hp = static_cast<float*>(hi_v);
+                    *reinterpret_cast<float4*>(hp + r0) = make_float4(hv[0], -hv[1], hv[2], -hv[3]);
+                    *reinterpret_cast<float4*>(hp + r1) = make_float4(hv[1], hv[0], hv[3], hv[2]);
+                    if (corrected) {
+                        float* lp = static_cast<float*>(lo_v);
+                        *reinterpret_cast<float4*>(lp + r0) = make_float4(lv[0], -lv[1], lv[2], -lv[3]);
+                        *reinterpret_cast<float4*>(lp + r1) = make_float4(lv[1], lv[0], lv[3], lv[2]);
+                    }
+                }
             }
         }
+        __syncthreads();
     }
     DevDecision* dm = const_cast<DevDecision*>(d);
     flag_or(&dm->overflow, ovf);
@@ -1242,7 +1322,8 @@ void launch_prep_a(const float* a, int64_t m, int64_t k, int64_t kp, void* hi, v
 void launch_prep_b(const float* b, int64_t k, int64_t n, int64_t kp, void* hi, void* lo,
                    const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s) {
     if (n <= 0 || kp <= 0) return;
-    const unsigned grid = unsigned(((n + 31) / 32) * ((kp / 2 + 31) / 32));
+    const int64_t tiles = ((n + kPrepBJ - 1) / kPrepBJ) * ((kp / 2 + kPrepBKK - 1) / kPrepBKK);
+    const unsigned grid = unsigned(tiles < 148 * 8 ? tiles : 148 * 8);
     prep_b_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const float2*>(b), k, n, kp, hi, lo, d,
                                        kind_fixed, corrected);
 }
