@@ -186,6 +186,16 @@ int tcec_network_destroy(tcec_network net);
 int tcec_network_set_node(tcec_network net, int node, const void* host_data);
 /* greedy_path, network.hpp:49 -- writes 2 * (n_nodes - 1) ints */
 int tcec_network_greedy_path(tcec_network net, int* steps);
+/* Contraction-tree reconfiguration (host code, no device needed; replaces the
+ * role of greedy_path, network.cpp:204-315, for large circuits): optimise the
+ * SSA path `steps` (n_nodes - 1 pairs) over frontiers of up to k pieces (3..16)
+ * by exact dynamic programming.  Network given as ranks[n_nodes] and the
+ * concatenated labels / dims of every node.  time_model = 0 scores MACs, 1 the
+ * estimated B200 time of each step's dispatch tier; latency_macs is the cost
+ * per element of k of a few-output FP32-chain step.  Writes the new path. */
+int tcec_path_reconfigure(int n_nodes, const int* ranks, const int* labels, const int64_t* dims,
+                          const int* steps, int n_steps, int k, int passes, int time_model,
+                          double latency_macs, unsigned long long seed, int* out_steps);
 /* contract_network, network.hpp:37-38 -- path as (a, b) id pairs in SSA
  * numbering (network.hpp:22-26).  The result tensor (host) has the labels
  * written to out_labels (may be NULL) and rank to *out_rank.  When log_lines is

@@ -148,6 +148,8 @@ def load() -> C.CDLL:
         "tcec_network_destroy": ([vp], i32),
         "tcec_network_set_node": ([vp, i32, vp], i32),
         "tcec_network_greedy_path": ([vp, ip], i32),
+        "tcec_path_reconfigure": ([i32, ip, ip, C.POINTER(i64), ip, i32, i32, i32, i32, C.c_double,
+                                   C.c_ulonglong, ip], i32),
         "tcec_contract_network": ([vp, ip, i32, C.POINTER(DispatchConfig), vp, i64, ip, ip,
                                    C.c_char_p, i64], i32),
         "tcec_contract_selector_batch": ([vp, ip, i32, C.POINTER(DispatchConfig), i32, ip, i32,

@@ -338,7 +338,39 @@ def remap_path(steps_pre, ids, n_orig, reduced_path):
 
 
 def reconfigure_path(spec: NetworkSpec, path, k: int = 8, passes: int = 3, seed: int = 0,
-                     latency_macs: float = 1e4, time_model: bool = False):
+                     latency_macs: float = 1e4, time_model: bool = False, native: bool = True):
+    """Subtree reconfiguration; the native C++ engine (tcec_path_reconfigure,
+    csrc/path_search.cu) unless native=False (the Python reference below)."""
+    if native:
+        return _reconfigure_native(spec, path, k, passes, seed, latency_macs, time_model)
+    return _reconfigure_py(spec, path, k, passes, seed, latency_macs, time_model)
+
+
+def _reconfigure_native(spec, path, k, passes, seed, latency_macs, time_model):
+    import ctypes as C
+    from ._lib import check, load
+    lib = load()
+    names = {}
+    ranks, labels, dims = [], [], []
+    for ls, ds in zip(spec.labels, spec.dims):
+        ranks.append(len(ls))
+        for l, d in zip(ls, ds):
+            labels.append(names.setdefault(l, len(names)))
+            dims.append(int(d))
+    n = len(spec.labels)
+    flat = [x for st in path for x in st]
+    out = (C.c_int * max(len(flat), 1))()
+    check(lib.tcec_path_reconfigure(
+        n, (C.c_int * max(n, 1))(*ranks), (C.c_int * max(len(labels), 1))(*labels),
+        (C.c_int64 * max(len(dims), 1))(*dims), (C.c_int * max(len(flat), 1))(*flat), len(path),
+        int(k), int(passes), int(bool(time_model)), float(latency_macs), int(seed) & (2 ** 64 - 1), out))
+    steps = [(out[2 * i], out[2 * i + 1]) for i in range(len(path))]
+    f, w = path_cost(spec, steps)
+    return steps, f, w
+
+
+def _reconfigure_py(spec: NetworkSpec, path, k: int = 8, passes: int = 3, seed: int = 0,
+                    latency_macs: float = 1e4, time_model: bool = False):
     """Subtree reconfiguration (cotengra's `subtree_reconfigure`): for every
     node of the contraction tree take a frontier of up to `k` sub-pieces and
     replace the way they are combined by the cheapest order (dynamic
@@ -573,7 +605,7 @@ def slice_and_reconfigure(spec: NetworkSpec, path, max_log2: float, k: int = 10,
 
 
 def hyper_path(spec: NetworkSpec, max_log2: float = 28.0, trials: int = 2, seed: int = 0,
-               leaf: int = 14, k: int = 10, log=None, time_model: bool = False):
+               leaf: int = 14, k: int = 12, log=None, time_model: bool = False):
     """Sliced contraction plan for large circuits:
     presimplify (absorb rank <= 2 tensors) -> divisive partition tree
     (`partition_path`) -> subtree reconfiguration -> exact slicing alternated

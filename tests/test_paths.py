@@ -59,13 +59,16 @@ def test_presimplify_then_partition_is_a_valid_equal_path(maker):
     assert abs(z - ref) <= 1e-9 * max(abs(ref), 1e-30)
 
 
-def test_reconfigure_never_raises_cost_and_keeps_the_value():
+@pytest.mark.parametrize("native", [True, False])
+def test_reconfigure_never_raises_cost_and_keeps_the_value(native):
+    """Both the native C++ engine (tcec_path_reconfigure, host code in the
+    library -- no GPU needed) and the Python restatement."""
     spec = _rqc(3, 4, 10)
     pre, ids, red = presimplify(spec)
     p, _, _ = random_greedy_path(red, trials=2, max_width=40)
     for tm in (False, True):
         before = path_model_cost(red, p, (), tm)
-        q, f, w = reconfigure_path(red, p, k=8, passes=2, time_model=tm)
+        q, f, w = reconfigure_path(red, p, k=8, passes=2, time_model=tm, native=native)
         _valid_ssa(red, q)
         assert path_model_cost(red, q, (), tm) <= before * (1 + 1e-9)
         full_p = remap_path(pre, ids, len(spec.labels), p)
@@ -113,3 +116,14 @@ def test_model_cost_tiers_and_latency():
     assert tc < simt
     # a 16-output, 2^21-long step pays the chain latency
     assert model_step_cost(2 + 21, 2 + 21, 4) > 1e3 * 2.0 ** 25 / 1e2
+
+
+def test_native_and_python_reconfigure_agree_on_cost():
+    spec = _syc(4)
+    pre, ids, red = presimplify(spec)
+    p, _, _ = random_greedy_path(red, trials=1, max_width=60)
+    qn, _, _ = reconfigure_path(red, p, k=8, passes=2, native=True, time_model=True)
+    qp, _, _ = reconfigure_path(red, p, k=8, passes=2, native=False, time_model=True)
+    cn, cp = path_model_cost(red, qn, (), True), path_model_cost(red, qp, (), True)
+    assert cn <= path_model_cost(red, p, (), True) and cp <= path_model_cost(red, p, (), True)
+    assert cn == pytest.approx(cp, rel=0.25)

@@ -30,6 +30,7 @@ if __name__ == "__main__":
     p.add_argument("--max-log2", type=float, default=28.0)
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--time-model", action="store_true")
+    p.add_argument("--k", type=int, default=12)
     p.add_argument("--out", default="")
     a = p.parse_args()
     circ = sycamore_like(a.cycles, 1)
@@ -37,7 +38,7 @@ if __name__ == "__main__":
     t0 = time.time()
     path, sliced, flops, width = hyper_path(spec, a.max_log2, trials=a.trials, seed=a.seed,
                                             log=lambda s: print(s, flush=True),
-                                            time_model=a.time_model)
+                                            time_model=a.time_model, k=a.k)
     out = {"circuit": f"sycamore_like({a.cycles}, 1)", "spec_hash": spec_hash(spec),
            "max_log2": a.max_log2, "sliced": sliced, "total_flops": flops, "width_log2": width,
            "search_s": round(time.time() - t0, 1), "time_model": a.time_model, "path": path}
