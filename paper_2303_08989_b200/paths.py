@@ -617,7 +617,7 @@ def hyper_path(spec: NetworkSpec, max_log2: float = 28.0, trials: int = 2, seed:
     for t in range(trials):
         s = seed + 1000 * t
         p, f, w = partition_path(red, trials=8, leaf=leaf, max_width=60, imbalance=(0.2, 0.8), seed=s)
-        p, f, w = reconfigure_path(red, p, k=k, passes=3, seed=s, time_model=time_model)
+        p, f, w = reconfigure_path(red, p, k=k, passes=3, seed=s)  # MAC model before slicing (measured better)
         p, sliced, fs, ws = slice_and_reconfigure(red, p, max_log2, k=k, rounds=2, time_model=time_model)
         score = path_model_cost(red, p, sliced, True) if time_model else fs
         if log:
