@@ -40,6 +40,11 @@ struct tcec_network_s {
     int64_t result_size = 0;
     tcec::SmallProgram small;        // fused small-step program (small_fold.cu)
     tcec::HybridProgram hyb;         // subtree prologue of the per-step fold
+    // node labels/dims are fixed at creation: validate once; the fold plan of
+    // the last (path, config) is reused by repeated batch calls
+    bool validated = false;
+    std::string plan_key;
+    tcec::FoldPlan plan_cache;
     ~tcec_network_s() {
         small.release();
         hyb.release();
@@ -256,10 +261,22 @@ static int enqueue_fold(tcec_network_s& net, const FoldPlan& plan, const tcec_di
 static int prepare(tcec_network_s& net, const int* steps, int n_steps,
                    const tcec_dispatch_config_t& cfg, FoldPlan* plan, DevDecision** dec,
                    void** ws) {
-    int rc = validate(net);
-    if (rc) return rc;
-    rc = build_plan(net, steps, n_steps, cfg, plan);
-    if (rc) return rc;
+    if (!net.validated) {
+        const int rv = validate(net);
+        if (rv) return rv;
+        net.validated = true;
+    }
+    std::string key(reinterpret_cast<const char*>(steps), size_t(std::max(n_steps, 0)) * 2 * sizeof(int));
+    key.append(reinterpret_cast<const char*>(&cfg), sizeof(cfg));
+    int rc = TCEC_OK;
+    if (key == net.plan_key) {
+        *plan = net.plan_cache;
+    } else {
+        rc = build_plan(net, steps, n_steps, cfg, plan);
+        if (rc) return rc;
+        net.plan_key = key;
+        net.plan_cache = *plan;
+    }
     Handle& h = *net.h;
     *dec = h.decisions(std::max(n_steps, 1));
     if (!*dec) return set_error(TCEC_ERR_CUDA, "decision buffer allocation failed");
