@@ -326,6 +326,8 @@ int upload_hybrid_program(HybridProgram* p) {
 
 namespace {
 
+constexpr int kBatchFoldMinRuns = 4096;  // thread-per-run kernel from this many runs
+
 // one contraction step by one warp: operands gathered through the step's
 // permutation tables, the reference FP32 schedule (or FP64) per output element
 __device__ __forceinline__ void warp_step(const SmallStepDev& st, float2* arena,
@@ -416,6 +418,78 @@ __global__ void small_fold_kernel(const SmallStepDev* __restrict__ steps, int n_
     for (int64_t e = lane; e < result_size; e += 32) out[run * result_size + e] = arena[result_off + e];
 }
 
+// Many runs of one small program (all 65536 bitstrings of a 4x4 RQC): one
+// THREAD per run instead of one warp, so every lane is busy even on the
+// many steps with fewer than 32 outputs.  The arena is structure-of-arrays in
+// global memory (element e of run r at e * n_runs + r): the steps are uniform
+// across runs, so every arena access of a warp is one coalesced 256-B line and
+// every node / table access is a broadcast.  Same per-element arithmetic (the
+// reference FP32 chains or FP64) as warp_step -> bit-identical.
+__global__ void __launch_bounds__(128) batch_fold_kernel(
+    const SmallStepDev* __restrict__ steps, int n_steps, const int32_t* __restrict__ tab,
+    const float2* __restrict__ nodes, int n_runs, const int64_t* __restrict__ var, int n_var,
+    const float2* __restrict__ var_data, int64_t per_run, const uint8_t* __restrict__ bits,
+    int32_t result_off, int64_t result_size, float2* __restrict__ out, float2* __restrict__ arena) {
+    const int64_t run = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (run >= n_runs) return;
+    const int64_t R = n_runs;
+    float2* ar = arena + run;  // element e at ar[e * R]
+    const int64_t* var_off = var;
+    const int64_t* var_cnt = var + n_var;
+    if (bits != nullptr) {
+        for (int v = 0; v < n_var; ++v) {
+            const bool one = bits[run * n_var + v] != 0;
+            ar[var_off[v] * R] = make_float2(one ? 0.0f : 1.0f, 0.0f);
+            ar[(var_off[v] + 1) * R] = make_float2(one ? 1.0f : 0.0f, 0.0f);
+        }
+    } else if (var_data != nullptr) {
+        const float2* src = var_data + run * per_run;
+        int64_t off = 0;
+        for (int v = 0; v < n_var; ++v) {
+            for (int64_t e = 0; e < var_cnt[v]; ++e) ar[(var_off[v] + e) * R] = src[off + e];
+            off += var_cnt[v];
+        }
+    }
+    for (int s = 0; s < n_steps; ++s) {
+        const SmallStepDev st = steps[s];
+        const int32_t* ta = tab + st.ta;
+        const int32_t* tb = tab + st.tb;
+        const int mn = st.m * st.n;
+        for (int o = 0; o < mn; ++o) {
+            const int i = o / st.n, j = o - i * st.n;
+            float2 r;
+            if (st.tier == 0) {
+                float p1 = 0.0f, p2 = 0.0f, p3 = 0.0f, p4 = 0.0f;
+                for (int kk = 0; kk < st.k; ++kk) {
+                    const int64_t ia = st.a_off + ta[i * st.k + kk], ib = st.b_off + tb[kk * st.n + j];
+                    const float2 a = st.a_kind ? ar[ia * R] : nodes[ia];
+                    const float2 b = st.b_kind ? ar[ib * R] : nodes[ib];
+                    p1 = __fadd_rn(p1, __fmul_rn(a.x, b.x));
+                    p2 = __fadd_rn(p2, __fmul_rn(a.y, b.y));
+                    p3 = __fadd_rn(p3, __fmul_rn(a.x, b.y));
+                    p4 = __fadd_rn(p4, __fmul_rn(a.y, b.x));
+                }
+                r = make_float2(__fsub_rn(p1, p2), __fadd_rn(p3, p4));
+            } else {
+                double p1 = 0.0, p2 = 0.0, p3 = 0.0, p4 = 0.0;
+                for (int kk = 0; kk < st.k; ++kk) {
+                    const int64_t ia = st.a_off + ta[i * st.k + kk], ib = st.b_off + tb[kk * st.n + j];
+                    const float2 a = st.a_kind ? ar[ia * R] : nodes[ia];
+                    const float2 b = st.b_kind ? ar[ib * R] : nodes[ib];
+                    p1 = __dadd_rn(p1, __dmul_rn(double(a.x), double(b.x)));
+                    p2 = __dadd_rn(p2, __dmul_rn(double(a.y), double(b.y)));
+                    p3 = __dadd_rn(p3, __dmul_rn(double(a.x), double(b.y)));
+                    p4 = __dadd_rn(p4, __dmul_rn(double(a.y), double(b.x)));
+                }
+                r = make_float2(__fsub_rn(__double2float_rn(p1), __double2float_rn(p2)),
+                                __fadd_rn(__double2float_rn(p3), __double2float_rn(p4)));
+            }
+            ar[(int64_t(st.out_off) + o) * R] = r;
+        }
+    }
+    for (int64_t e = 0; e < result_size; ++e) out[run * result_size + e] = ar[(result_off + e) * R];
+}
+
 }  // namespace
 
 int launch_hybrid_trees(const HybridProgram& p, const float2* node_dev, float2* out, cudaStream_t s) {
@@ -440,6 +514,21 @@ int launch_small_program(const SmallProgram& p, const float2* node_dev, int n_ru
                          cudaStream_t s) {
     if (!p.ok) return set_error(TCEC_ERR_INVALID_ARGUMENT, "small program not eligible: " + p.why);
     if (n_runs <= 0) return TCEC_OK;
+    if (n_runs >= kBatchFoldMinRuns) {
+        // thread per run, SoA arena in global memory (stream-ordered scratch)
+        float2* arena = nullptr;
+        const size_t bytes = size_t(n_runs) * size_t(std::max<int64_t>(p.arena_elems, 1)) * 8;
+        if (cudaMallocAsync(reinterpret_cast<void**>(&arena), bytes, s) == cudaSuccess) {
+            batch_fold_kernel<<<unsigned((n_runs + 127) / 128), 128, 0, s>>>(
+                p.d_steps, int(p.steps.size()), p.d_tables, node_dev, n_runs, p.d_var,
+                int(p.var_arena.size()), var_data, per_run, bits, p.result_off, p.result_size, out,
+                arena);
+            cudaFreeAsync(arena, s);
+            const cudaError_t e = cudaGetLastError();
+            return e == cudaSuccess ? TCEC_OK : cuda_error(e, "batch_fold_kernel");
+        }
+        cudaGetLastError();  // no room for the SoA arena: fall back to warp-per-run
+    }
     const int64_t arena_bytes = p.arena_elems * 8;
     int wpc = int(std::min<int64_t>(8, std::max<int64_t>(1, kMaxArenaBytes / std::max<int64_t>(arena_bytes, 1))));
     wpc = std::min(wpc, std::max(1, n_runs));

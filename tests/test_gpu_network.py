@@ -225,3 +225,21 @@ def test_hybrid_subtree_launch_matches_per_step_with_tensor_core_steps(handle, s
         assert np.array_equal(out[policy][0], out[1][0]), policy
         assert np.array_equal(out[policy][1], out[1][1]), policy
         assert out[policy][2] == out[1][2]
+
+
+def test_thread_per_run_batch_matches_warp_per_run(handle):
+    """From 4096 runs the fused program runs one thread per bitstring over a
+    structure-of-arrays arena; the same per-element chains as the
+    warp-per-bitstring kernel (itself pinned to the reference above) ->
+    bit-identical amplitudes, selectors and node-data batches alike."""
+    circ = rqc_rectangular(4, 4, 8, 1)
+    allx = np.array([[(v >> q) & 1 for q in range(16)] for v in range(1 << 16)], np.uint8)
+    xs = allx[::7][:6144]
+    net = Network(handle, circuit_to_network(circ, xs[0]))
+    path = net.greedy_path()
+    cfg = make_config()
+    big = net.selector_batch(path, xs, cfg)                        # thread per run
+    small = np.concatenate([net.selector_batch(path, xs[i:i + 2048], cfg)  # warp per run
+                            for i in range(0, len(xs), 2048)])
+    assert np.array_equal(big.view(np.uint32), small.view(np.uint32))
+    net.close()
