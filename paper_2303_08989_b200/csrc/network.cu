@@ -259,7 +259,7 @@ static int enqueue_fold(tcec_network_s& net, const FoldPlan& plan, const tcec_di
 }
 
 static int prepare(tcec_network_s& net, const int* steps, int n_steps,
-                   const tcec_dispatch_config_t& cfg, FoldPlan* plan, DevDecision** dec,
+                   const tcec_dispatch_config_t& cfg, const FoldPlan** plan_out, DevDecision** dec,
                    void** ws) {
     if (!net.validated) {
         const int rv = validate(net);
@@ -269,14 +269,14 @@ static int prepare(tcec_network_s& net, const int* steps, int n_steps,
     std::string key(reinterpret_cast<const char*>(steps), size_t(std::max(n_steps, 0)) * 2 * sizeof(int));
     key.append(reinterpret_cast<const char*>(&cfg), sizeof(cfg));
     int rc = TCEC_OK;
-    if (key == net.plan_key) {
-        *plan = net.plan_cache;
-    } else {
-        rc = build_plan(net, steps, n_steps, cfg, plan);
+    if (key != net.plan_key) {
+        net.plan_key.clear();
+        rc = build_plan(net, steps, n_steps, cfg, &net.plan_cache);
         if (rc) return rc;
         net.plan_key = key;
-        net.plan_cache = *plan;
     }
+    const FoldPlan* plan = &net.plan_cache;
+    *plan_out = plan;
     Handle& h = *net.h;
     *dec = h.decisions(std::max(n_steps, 1));
     if (!*dec) return set_error(TCEC_ERR_CUDA, "decision buffer allocation failed");
@@ -558,11 +558,12 @@ int tcec_contract_network(tcec_network net, const int* steps, int n_steps,
     if (!net->h) return set_error(TCEC_ERR_CUDA, "network has no device handle");
     Handle& h = *net->h;
     cudaSetDevice(h.device);
-    FoldPlan plan;
+    const FoldPlan* plan_ptr = nullptr;
     DevDecision* dec = nullptr;
     void* ws = nullptr;
-    int rc = prepare(*net, steps, n_steps, *cfg, &plan, &dec, &ws);
+    int rc = prepare(*net, steps, n_steps, *cfg, &plan_ptr, &dec, &ws);
     if (rc) return rc;
+    const FoldPlan& plan = *plan_ptr;
     const SmallProgram* sp_fused = small_program(*net, steps, n_steps, *cfg, plan, {}, &rc);
     if (rc) return rc;
     if (sp_fused) {
@@ -619,11 +620,12 @@ int tcec_contract_selector_batch(tcec_network net, const int* steps, int n_steps
         if (nd < 0 || nd >= int(net->nodes.size()) || net->nodes[size_t(nd)].size() != 2)
             return set_error(TCEC_ERR_SHAPE_MISMATCH, "selector nodes must be rank-1 of extent 2");
     }
-    FoldPlan plan;
+    const FoldPlan* plan_ptr = nullptr;
     DevDecision* dec = nullptr;
     void* ws = nullptr;
-    int rc = prepare(*net, steps, n_steps, *cfg, &plan, &dec, &ws);
+    int rc = prepare(*net, steps, n_steps, *cfg, &plan_ptr, &dec, &ws);
     if (rc) return rc;
+    const FoldPlan& plan = *plan_ptr;
     int64_t size = 1;
     for (auto d : plan.out_dims) size *= d;
     if (size != 1) return set_error(TCEC_ERR_SHAPE_MISMATCH, "amplitude networks must close");
@@ -690,11 +692,12 @@ int tcec_contract_node_batch(tcec_network net, const int* steps, int n_steps,
         seg.push_back(cnt);
         per_run += cnt;
     }
-    FoldPlan plan;
+    const FoldPlan* plan_ptr = nullptr;
     DevDecision* dec = nullptr;
     void* ws = nullptr;
-    int rc = prepare(*net, steps, n_steps, *cfg, &plan, &dec, &ws);
+    int rc = prepare(*net, steps, n_steps, *cfg, &plan_ptr, &dec, &ws);
     if (rc) return rc;
+    const FoldPlan& plan = *plan_ptr;
     int64_t size = 1;
     for (auto d : plan.out_dims) size *= d;
     if (size != 1) return set_error(TCEC_ERR_SHAPE_MISMATCH, "batched networks must close");

@@ -57,8 +57,22 @@ class Network:
         check(self.lib.tcec_network_create(handle.h if handle is not None else None, n, r, lab,
                                            dm, C.byref(net)))
         self.net = net
+        self._steps_cache = None
         for i, d in enumerate(spec.data):
             self.set_node(i, d)
+
+    def _steps(self, path):
+        """ctypes view of a path's SSA pairs, cached for repeated calls with the
+        same path object (batch loops call with one path many times)."""
+        c = self._steps_cache
+        if c is not None and c[0] is path and c[1] == len(path):
+            return c[2], c[3]
+        arr = np.ascontiguousarray(np.asarray(path, dtype=np.int32).reshape(-1))
+        if arr.size == 0:
+            arr = np.zeros(1, np.int32)
+        ptr = arr.ctypes.data_as(C.POINTER(C.c_int))
+        self._steps_cache = (path, len(path), arr, ptr)
+        return arr, ptr
 
     def close(self):
         if getattr(self, "net", None):
@@ -125,8 +139,7 @@ class Network:
     def selector_batch(self, path, bitstrings, config=None) -> np.ndarray:
         """Amplitudes of many bitstrings over one plan / one captured graph."""
         cfg = _cfg(config)
-        flat = [x for st in path for x in st]
-        steps = (C.c_int * max(len(flat), 1))(*flat)
+        _, steps = self._steps(path)
         sel = self.spec.selector_nodes
         nsel = len(sel)
         sel_arr = (C.c_int * max(nsel, 1))(*sel)
@@ -143,8 +156,7 @@ class Network:
         """Closed-network values of many runs that differ only in the data of
         `var_nodes`; runs[r][i] is the data of var_nodes[i] in run r."""
         cfg = _cfg(config)
-        flat = [x for st in path for x in st]
-        steps = (C.c_int * max(len(flat), 1))(*flat)
+        _, steps = self._steps(path)
         nv = len(var_nodes)
         vn = (C.c_int * max(nv, 1))(*var_nodes)
         blocks = [np.ascontiguousarray(np.asarray(d, dtype=np.complex64).reshape(-1))
