@@ -19,11 +19,42 @@
 
 namespace tcec {
 
+// concurrent replay lanes of the per-step fold in batch calls
+constexpr int kFoldLanes = 4;  // 8 measured noisier and slower at d14 (contention)
+
 static bool contains(const std::vector<int>& v, int x) {
     return std::find(v.begin(), v.end(), x) != v.end();
 }
 
 }  // namespace tcec
+
+// A concurrent replay lane of the per-step fold: its own stream, node buffer,
+// result slot, decision slots, operand workspace and captured graph, so the
+// folds of several bitstrings run at once (a latency-bound step -- e.g. the
+// one-block FP32 chain of a deep circuit's final dot product -- leaves the
+// rest of the GPU to the other lanes).
+struct FoldLane {
+    cudaStream_t s = nullptr;
+    cudaEvent_t ev = nullptr;
+    void* node_dev = nullptr;
+    void* result_dev = nullptr;
+    tcec::DevDecision* dec = nullptr;
+    int dec_slots = 0;
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
+    cudaGraphExec_t graph = nullptr;
+    std::string graph_key;
+    void release() {
+        if (graph) cudaGraphExecDestroy(graph);
+        if (node_dev) cudaFree(node_dev);
+        if (result_dev) cudaFree(result_dev);
+        if (dec) cudaFree(dec);
+        if (ws) cudaFree(ws);
+        if (ev) cudaEventDestroy(ev);
+        if (s) cudaStreamDestroy(s);
+        *this = FoldLane();
+    }
+};
 
 struct tcec_network_s {
     tcec_handle h = nullptr;
@@ -45,7 +76,9 @@ struct tcec_network_s {
     bool validated = false;
     std::string plan_key;
     tcec::FoldPlan plan_cache;
+    std::vector<FoldLane> lanes;
     ~tcec_network_s() {
+        for (auto& l : lanes) l.release();
         small.release();
         hyb.release();
         if (graph) cudaGraphExecDestroy(graph);
@@ -362,6 +395,57 @@ static int run_fold(tcec_network_s& net, const int* steps, int n_steps,
     return TCEC_OK;
 }
 
+// Run the (cached-graph) fold on lane `ln`: the lane's buffers and stream stand
+// in for the network's and the handle's while the graph is captured/launched.
+static int run_fold_lane(tcec_network_s& net, FoldLane& ln, const int* steps, int n_steps,
+                         const tcec_dispatch_config_t& cfg, const FoldPlan& plan) {
+    Handle& h = *net.h;
+    std::swap(net.node_dev, ln.node_dev);
+    std::swap(net.result_dev, ln.result_dev);
+    std::swap(net.graph, ln.graph);
+    std::swap(net.graph_key, ln.graph_key);
+    const cudaStream_t saved = h.stream;
+    h.stream = ln.s;
+    const int rc = run_fold(net, steps, n_steps, cfg, plan, ln.dec, ln.ws, true);
+    h.stream = saved;
+    std::swap(net.node_dev, ln.node_dev);
+    std::swap(net.result_dev, ln.result_dev);
+    std::swap(net.graph, ln.graph);
+    std::swap(net.graph_key, ln.graph_key);
+    return rc;
+}
+
+// Make `count` lanes able to run `plan` (grown on demand, kept across calls).
+static int ensure_lanes(tcec_network_s& net, int count, const FoldPlan& plan) {
+    if (int(net.lanes.size()) < count) net.lanes.resize(size_t(count));
+    const int slots = std::max<int>(int(plan.steps.size()), 1);
+    for (int i = 0; i < count; ++i) {
+        FoldLane& ln = net.lanes[size_t(i)];
+        cudaError_t e = cudaSuccess;
+        if (!ln.s) e = cudaStreamCreateWithFlags(&ln.s, cudaStreamNonBlocking);
+        if (e == cudaSuccess && !ln.ev) e = cudaEventCreateWithFlags(&ln.ev, cudaEventDisableTiming);
+        if (e == cudaSuccess && !ln.node_dev)
+            e = cudaMalloc(&ln.node_dev, size_t(std::max<int64_t>(net.total, 1)) * 8);
+        if (e == cudaSuccess && !ln.result_dev) e = cudaMalloc(&ln.result_dev, 8);
+        if (e == cudaSuccess && ln.dec_slots < slots) {
+            if (ln.dec) cudaFree(ln.dec);
+            ln.dec = nullptr;
+            ln.dec_slots = 0;
+            e = cudaMalloc(&ln.dec, sizeof(tcec::DevDecision) * size_t(slots));
+            if (e == cudaSuccess) ln.dec_slots = slots;
+        }
+        if (e == cudaSuccess && ln.ws_bytes < plan.ws_bytes) {
+            if (ln.ws) cudaFree(ln.ws);
+            ln.ws = nullptr;
+            ln.ws_bytes = 0;
+            e = cudaMalloc(&ln.ws, plan.ws_bytes);
+            if (e == cudaSuccess) ln.ws_bytes = plan.ws_bytes;
+        }
+        if (e != cudaSuccess) return cuda_error(e, "fold lane");
+    }
+    return TCEC_OK;
+}
+
 // The fused small-step program for this (path, config, variable nodes), built
 // once and cached; nullptr when the executor policy or eligibility says no.
 static const SmallProgram* small_program(tcec_network_s& net, const int* steps, int n_steps,
@@ -651,6 +735,33 @@ int tcec_contract_selector_batch(tcec_network net, const int* steps, int n_steps
         rc = launch_small_program(*fused, static_cast<const float2*>(net->node_dev), n_strings,
                                   nullptr, 0, d_bits, d_out, s);
         if (rc) return rc;
+    } else if (n_strings >= 2 && kFoldLanes > 1) {
+        // concurrent lanes: bitstring i runs on lane i % L with its own buffers
+        const int L = std::min(n_strings, kFoldLanes);
+        rc = ensure_lanes(*net, L, plan);
+        if (rc) return rc;
+        cudaEvent_t ready = net->lanes[0].ev;
+        cudaEventRecord(ready, s);  // uploads of nodes, offsets and bits are done
+        for (int l = 0; l < L; ++l) {
+            FoldLane& ln = net->lanes[size_t(l)];
+            cudaStreamWaitEvent(ln.s, ready, 0);
+            cudaMemcpyAsync(ln.node_dev, net->node_dev, size_t(net->total) * 8, cudaMemcpyDeviceToDevice,
+                            ln.s);
+        }
+        for (int i = 0; i < n_strings; ++i) {
+            FoldLane& ln = net->lanes[size_t(i % L)];
+            if (n_sel)
+                set_selectors_kernel<<<(n_sel + 127) / 128, 128, 0, ln.s>>>(
+                    static_cast<float2*>(ln.node_dev), d_off, n_sel, d_bits + size_t(i) * n_sel);
+            rc = run_fold_lane(*net, ln, steps, n_steps, *cfg, plan);
+            if (rc) return rc;
+            cudaMemcpyAsync(d_out + i, ln.result_dev, 8, cudaMemcpyDeviceToDevice, ln.s);
+        }
+        for (int l = 0; l < L; ++l) {
+            FoldLane& ln = net->lanes[size_t(l)];
+            cudaEventRecord(ln.ev, ln.s);
+            cudaStreamWaitEvent(s, ln.ev, 0);
+        }
     } else {
         for (int i = 0; i < n_strings; ++i) {
             if (n_sel)
