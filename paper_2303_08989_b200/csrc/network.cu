@@ -10,6 +10,7 @@
 // graph of the whole fold (the topology and path do not depend on the
 // bitstring, experiments.cpp:211-213).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -20,7 +21,19 @@
 namespace tcec {
 
 // concurrent replay lanes of the per-step fold in batch calls
-constexpr int kFoldLanes = 4;  // 8 measured noisier and slower at d14 (contention)
+constexpr int kFoldLanes = 4;
+
+// lanes of node batches: 1 by default -- the slices of a sliced contraction
+// already fill the GPU with large steps (Sycamore m=12: 68.8 / 74.3 / 80.7 ms
+// per slice with 1 / 2 / 3 lanes); TCEC_NODE_LANES overrides for tuning
+static int node_batch_lanes() {
+    static const int n = [] {
+        const char* e = std::getenv("TCEC_NODE_LANES");
+        const int v = e ? std::atoi(e) : 0;
+        return v > 0 ? v : 1;
+    }();
+    return n;
+}  // 8 measured noisier and slower at d14 (contention)
 
 static bool contains(const std::vector<int>& v, int x) {
     return std::find(v.begin(), v.end(), x) != v.end();
@@ -832,6 +845,34 @@ int tcec_contract_node_batch(tcec_network net, const int* steps, int n_steps,
         rc = launch_small_program(*fused, static_cast<const float2*>(net->node_dev), n_runs, d_var,
                                   per_run, nullptr, d_out, s);
         if (rc) return rc;
+    } else if (n_runs >= 2 && node_batch_lanes() > 1) {
+        // concurrent lanes (slices of a sliced contraction): run r on lane r % L
+        const int L = std::min(n_runs, node_batch_lanes());
+        rc = ensure_lanes(*net, L, plan);
+        if (rc) return rc;
+        cudaEvent_t ready = net->lanes[0].ev;
+        cudaEventRecord(ready, s);
+        for (int l = 0; l < L; ++l) {
+            FoldLane& ln = net->lanes[size_t(l)];
+            cudaStreamWaitEvent(ln.s, ready, 0);
+            cudaMemcpyAsync(ln.node_dev, net->node_dev, size_t(net->total) * 8, cudaMemcpyDeviceToDevice,
+                            ln.s);
+        }
+        for (int r = 0; r < n_runs; ++r) {
+            FoldLane& ln = net->lanes[size_t(r % L)];
+            if (n_var)
+                scatter_nodes_kernel<<<std::min(n_var, 1024), 64, 0, ln.s>>>(
+                    static_cast<float2*>(ln.node_dev), d_var + size_t(r) * size_t(per_run), d_seg,
+                    n_var);
+            rc = run_fold_lane(*net, ln, steps, n_steps, *cfg, plan);
+            if (rc) return rc;
+            cudaMemcpyAsync(d_out + r, ln.result_dev, 8, cudaMemcpyDeviceToDevice, ln.s);
+        }
+        for (int l = 0; l < L; ++l) {
+            FoldLane& ln = net->lanes[size_t(l)];
+            cudaEventRecord(ln.ev, ln.s);
+            cudaStreamWaitEvent(s, ln.ev, 0);
+        }
     } else {
         for (int r = 0; r < n_runs; ++r) {
             if (n_var)
