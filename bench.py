@@ -791,8 +791,64 @@ def run_rqc7x7(args):
                     row["cpu_reference_threads"] = thr
             net.close()
             rows_out.append(row)
+        # beyond the reference's reach: its greedy path needs a 2^33-element
+        # (69 GB) intermediate at depth 18 and 2^39 at depth 20; the sliced
+        # plan search (paths.hyper_path) keeps every intermediate <= 2^28
+        for depth in [int(d) for d in args.hyper_depths.split(",") if d]:
+            from paper_2303_08989_b200.paths import hyper_path
+            from paper_2303_08989_b200.slicing import assignment, slice_spec
+            circ = rqc_rectangular(7, 7, depth, 1)
+            xs = bitstrings_for(49, 4, 1)
+            spec0 = circuit_to_network(circ, xs[0])
+            t0 = time.perf_counter()
+            path, sliced, flops, width = hyper_path(spec0, max_log2=28.0, trials=1, k=12, time_model=True)
+            plan_s = time.perf_counter() - t0
+            dims_of = {l: d for ls, ds in zip(spec0.labels, spec0.dims) for l, d in zip(ls, ds)}
+            sdims = [dims_of[l] for l in sliced]
+            nsl = int(np.prod(sdims)) if sliced else 1
+            specs = [circuit_to_network(circ, x) for x in xs]
+            ref = []
+            for sp in specs:
+                z = 0j
+                for si in range(nsl):
+                    z += contract_c128(slice_spec(sp, sliced, assignment(si, sdims)) if sliced else sp,
+                                       path, dev)
+                ref.append(z)
+            ref = np.array(ref)
+            torch.cuda.empty_cache()
+            base = slice_spec(spec0, sliced, [0] * len(sliced)) if sliced else spec0
+            var = sorted(set(i for i, ls in enumerate(spec0.labels) if set(sliced) & set(ls)) |
+                         set(spec0.selector_nodes))
+            runs = []
+            for sp in specs:
+                for si in range(nsl):
+                    sub = slice_spec(sp, sliced, assignment(si, sdims)) if sliced else sp
+                    runs.append([sub.data[i] for i in var])
+            net = Network(h, base)
+            row = {"depth": depth, "path": "hyper (sliced plan search)", "steps": len(path),
+                   "slices": nsl, "width_log2": width, "gflop_per_amplitude": round(flops / 1e9, 2),
+                   "plan_s": round(plan_s, 1), "modes": {}}
+            for label, cfg in (modes[0], modes[2]):
+                net.node_batch(path, var, runs[:nsl], cfg)  # capture / warm
+                torch.cuda.synchronize(dev)
+                t0 = time.perf_counter()
+                vals = net.node_batch(path, var, runs, cfg)
+                ms = (time.perf_counter() - t0) / len(xs) * 1e3
+                amps = vals.astype(np.complex128).reshape(len(xs), nsl).sum(axis=1)
+                err = np.abs(amps - ref) / np.abs(ref)
+                row["modes"][label] = {"ms_per_amplitude": round(ms, 3),
+                                       "median_rel_err_vs_c128": float(np.median(err)),
+                                       "max_rel_err_vs_c128": float(np.max(err))}
+            a, f = row["modes"]["AUTO-0"], row["modes"]["FP32_BASELINE"]
+            row["auto_speedup_vs_fp32_baseline"] = round(f["ms_per_amplitude"] / a["ms_per_amplitude"], 3)
+            row["auto_err_ratio_vs_fp32_baseline"] = (round(a["median_rel_err_vs_c128"] /
+                                                            f["median_rel_err_vs_c128"], 3)
+                                                      if f["median_rel_err_vs_c128"] else None)
+            net.close()
+            torch.cuda.empty_cache()
+            rows_out.append(row)
     if rank == 0:
-        deep = rows_out[-1]["modes"]["AUTO-0"]["ms_per_amplitude"]
+        deep = [r for r in rows_out if r["depth"] == depths[-1]][0]["modes"]["AUTO-0"]["ms_per_amplitude"]
         line = {"metric": f"RCS 7x7 deep-circuit amplitude time (AUTO-0, depth {depths[-1]})",
                 "value": deep, "unit": "ms/amplitude", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": deep, "higher_is_better": False,
@@ -823,6 +879,7 @@ def main():
     p.add_argument("--cycles", type=int, default=12)
     p.add_argument("--path", choices=["plan", "hyper", "greedy"], default="plan")
     p.add_argument("--depths", default="4,8,12,14,16")
+    p.add_argument("--hyper-depths", default="18,20,24")
     p.add_argument("--slices-log2", type=int, default=6)
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
