@@ -904,14 +904,37 @@ __global__ void __launch_bounds__(256) cgemm_skinny_col_kernel(const float2* __r
     acc_t p[MX][4];
 #pragma unroll
     for (int i = 0; i < MX; ++i) p[i][0] = p[i][1] = p[i][2] = p[i][3] = acc_t(0);
-    for (int kk = 0; kk < k; ++kk) {
-        const float2 bv = __ldcs(b + int64_t(kk) * n + j);
+    if (k <= 4) {  // A/B on B200: the plain loop wins for k <= 4, grouped loads from 8 up
+        for (int kk = 0; kk < k; ++kk) {
+            const float2 bv = __ldcs(b + int64_t(kk) * n + j);
 #pragma unroll
-        for (int i = 0; i < MX; ++i)
-            if (i < m) {
-                const float2 av = as[i * k + kk];
-                chain4<F64>(av.x, av.y, bv.x, bv.y, p[i]);
-            }
+            for (int i = 0; i < MX; ++i)
+                if (i < m) {
+                    const float2 av = as[i * k + kk];
+                    chain4<F64>(av.x, av.y, bv.x, bv.y, p[i]);
+                }
+        }
+    } else {
+    // longer k: loads in groups of 8 issued together (8 in flight per thread
+    // instead of one memory latency per k)
+#pragma unroll 1
+    for (int k0 = 0; k0 < k; k0 += 8) {
+        float2 bcol[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (k0 + u < k) bcol[u] = __ldcs(b + int64_t(k0 + u) * n + j);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (k0 + u >= k) break;
+            const float2 bv = bcol[u];
+#pragma unroll
+            for (int i = 0; i < MX; ++i)
+                if (i < m) {
+                    const float2 av = as[i * k + k0 + u];
+                    chain4<F64>(av.x, av.y, bv.x, bv.y, p[i]);
+                }
+        }
+    }
     }
 #pragma unroll
     for (int i = 0; i < MX; ++i)
