@@ -865,7 +865,7 @@ __global__ void __launch_bounds__(kChainThreads) cgemm_chain_kernel(const float2
 // long operand exactly once (coalesced / contiguous) and writes C once; the
 // short operand sits in shared memory.  Each output runs the reference's four
 // chains in ascending k (kernels_scalar.cpp:76-87) -> bit-identical.
-constexpr int kSkinnyMaxK = 32;
+constexpr int kSkinnyMaxK = 128;
 
 template <bool F64>
 TCEC_DEV void chain4(float ar, float ai, float br, float bi, double (&p)[4]) {
@@ -946,10 +946,11 @@ template <bool F64, int MX>
 __global__ void __launch_bounds__(256) cgemm_skinny_row_kernel(const float2* __restrict__ a,
                                                                const float2* __restrict__ b,
                                                                float2* __restrict__ c, int64_t m,
-                                                               int n, int k) {
+                                                               int n, int k, int64_t ldn) {
+    // columns [0, n) of a block of B / C whose row stride is ldn
     using acc_t = typename std::conditional<F64, double, float>::type;
     __shared__ float2 bs[kSkinnyMaxK * MX];
-    for (int t = threadIdx.x; t < k * n; t += blockDim.x) bs[t] = b[t];
+    for (int t = threadIdx.x; t < k * n; t += blockDim.x) bs[t] = b[int64_t(t / n) * ldn + t % n];
     __syncthreads();
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= m) return;
@@ -966,7 +967,7 @@ __global__ void __launch_bounds__(256) cgemm_skinny_row_kernel(const float2* __r
                 chain4<F64>(av.x, av.y, bv.x, bv.y, p[j]);
             }
     }
-    float2* crow = c + i * n;
+    float2* crow = c + i * ldn;
 #pragma unroll
     for (int j = 0; j < MX; ++j)
         if (j < n) __stcs(crow + j, assemble<F64>(p[j]));
@@ -975,10 +976,21 @@ __global__ void __launch_bounds__(256) cgemm_skinny_row_kernel(const float2* __r
 template <bool F64, int MX>
 void launch_skinny_mx(const float2* a, const float2* b, float2* c, int64_t m, int64_t n, int64_t k,
                       cudaStream_t s) {
-    if (m <= n)
-        cgemm_skinny_col_kernel<F64, MX><<<unsigned((n + 255) / 256), 256, 0, s>>>(a, b, c, int(m), n, int(k));
-    else
-        cgemm_skinny_row_kernel<F64, MX><<<unsigned((m + 255) / 256), 256, 0, s>>>(a, b, c, m, int(n), int(k));
+    // more than 16 short-side rows/columns: passes of <= MX (each re-reads the
+    // long operand; register-resident 32-wide tiles measured slower)
+    if (m <= n) {
+        for (int64_t r0 = 0; r0 < m; r0 += MX) {
+            const int rows = int(std::min<int64_t>(MX, m - r0));
+            cgemm_skinny_col_kernel<F64, MX><<<unsigned((n + 255) / 256), 256, 0, s>>>(
+                a + r0 * k, b, c + r0 * n, rows, n, int(k));
+        }
+    } else {
+        for (int64_t j0 = 0; j0 < n; j0 += MX) {
+            const int cols = int(std::min<int64_t>(MX, n - j0));
+            cgemm_skinny_row_kernel<F64, MX><<<unsigned((m + 255) / 256), 256, 0, s>>>(
+                a, b + j0, c + j0, m, cols, int(k), n);
+        }
+    }
 }
 
 // true when the skinny kernels take the shape
@@ -986,11 +998,14 @@ template <bool F64>
 bool launch_skinny(const float2* a, const float2* b, float2* c, int64_t m, int64_t n, int64_t k,
                    cudaStream_t s) {
     const int64_t small = m < n ? m : n, large = m < n ? n : m;
-    if (k > kSkinnyMaxK || small > 16 || large < 4096) return false;
+    // up to 32 rows in register tiles of <= 16 (two passes above 16), k <= 128 in shared memory:
+    // the 64 x 64 tiled kernel would waste >= half of every tile on these
+    // (the (16, 2^22, 64) and (32, 2^23, 8) steps of Sycamore slices)
+    if (k > kSkinnyMaxK || small > 32 || large < 4096) return false;
     if (small <= 2) launch_skinny_mx<F64, 2>(a, b, c, m, n, k, s);
     else if (small <= 4) launch_skinny_mx<F64, 4>(a, b, c, m, n, k, s);
     else if (small <= 8) launch_skinny_mx<F64, 8>(a, b, c, m, n, k, s);
-    else launch_skinny_mx<F64, 16>(a, b, c, m, n, k, s);
+    else launch_skinny_mx<F64, 16>(a, b, c, m, n, k, s);  // 17..32: two passes
     return true;
 }
 

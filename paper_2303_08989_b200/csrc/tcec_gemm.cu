@@ -1318,6 +1318,23 @@ int launch_tcec_gemm(const TcecGemmArgs& g_in, cudaStream_t s) {
         const int bk = (g.fmt == kTf32 || g.fmt < 0) ? 32 : 64;  // the finer format decides
         const int64_t nkb = g.kp / bk;
         const int sms = g.sms > 1 ? g.sms : 148;
+        auto split_with = [&](int64_t want) {
+            if (want < 2) return;
+            // k-blocks per split in units of the f16 block (2 tf32 blocks), so
+            // both format kernels cut K at the same element
+            const int64_t nkb16 = g.kp / 64;
+            const int64_t per16 = (nkb16 + want - 1) / want;
+            const int splits = int((nkb16 + per16 - 1) / per16);
+            if (splits < 2) return;
+            const size_t bytes = size_t(splits) * size_t(g.m) * size_t(g.n2) * 4;
+            if (cudaMallocAsync(reinterpret_cast<void**>(&g.partial), bytes, s) == cudaSuccess) {
+                g.splits = splits;
+                g.kb_per = int(per16);  // f16 units; the tf32 kernel doubles it
+            } else {
+                cudaGetLastError();
+                g.partial = nullptr;
+            }
+        };
         if (tiles < sms && nkb >= 16) {
             static const int waves = [] {
                 const char* e = std::getenv("TCEC_SPLIT_WAVES");  // tuning override
@@ -1327,23 +1344,23 @@ int launch_tcec_gemm(const TcecGemmArgs& g_in, cudaStream_t s) {
             // every split keeps >= 32 f16 k-blocks (2048 K' elements) so the
             // partial round trip stays small against its MMA time
             int64_t want = std::min<int64_t>((waves * sms + tiles - 1) / tiles, (g.kp / 64) / 32);
-            if (want >= 2) {
-                // k-blocks per split in units of the f16 block (2 tf32 blocks),
-                // so both format kernels cut K at the same element
-                const int64_t nkb16 = g.kp / 64;
-                const int64_t per16 = (nkb16 + want - 1) / want;
-                const int splits = int((nkb16 + per16 - 1) / per16);
-                if (splits >= 2) {
-                    const size_t bytes = size_t(splits) * size_t(g.m) * size_t(g.n2) * 4;
-                    if (cudaMallocAsync(reinterpret_cast<void**>(&g.partial), bytes, s) == cudaSuccess) {
-                        g.splits = splits;
-                        g.kb_per = int(per16);  // f16 units; the tf32 kernel doubles it
-                    } else {
-                        cudaGetLastError();
-                        g.partial = nullptr;
-                    }
+            split_with(want);
+        } else if (tiles < 8 * sms && g.pair == kVariantWide && (g.kp / 64) / 32 >= 2) {
+            // a few waves of long tiles: split K just enough that the last wave
+            // is nearly full (e.g. 512 CTAs = 3.46 waves -> 2 splits = 6.92
+            // waves: (4096, 2048, 65536) TF32 steps of the Sycamore slices)
+            const double w1 = double(tiles) / sms;
+            int best = 1;
+            double best_eff = w1 / std::ceil(w1);
+            for (int sp = 2; sp <= 4 && sp <= (g.kp / 64) / 32; ++sp) {
+                const double w = w1 * sp;
+                const double eff = w / std::ceil(w);
+                if (best_eff < 0.95 && eff > best_eff + 0.02) {
+                    best = sp;
+                    best_eff = eff;
                 }
             }
+            if (best >= 2) split_with(best);
         }
     }
     int e = launch_formats(g, s);
