@@ -890,7 +890,7 @@ TCEC_DEV float2 assemble(const T (&p)[4]) {
 }
 
 // m <= MX: thread j owns column j of C
-template <bool F64, int MX>
+template <bool F64, int MX, bool GROUPED>
 __global__ void __launch_bounds__(256) cgemm_skinny_col_kernel(const float2* __restrict__ a,
                                                                const float2* __restrict__ b,
                                                                float2* __restrict__ c, int m,
@@ -904,7 +904,7 @@ __global__ void __launch_bounds__(256) cgemm_skinny_col_kernel(const float2* __r
     acc_t p[MX][4];
 #pragma unroll
     for (int i = 0; i < MX; ++i) p[i][0] = p[i][1] = p[i][2] = p[i][3] = acc_t(0);
-    if (k <= 4) {  // A/B on B200: the plain loop wins for k <= 4, grouped loads from 8 up
+    if (!GROUPED) {  // A/B on B200: the plain loop wins for k <= 4, grouped loads from 8 up
         for (int kk = 0; kk < k; ++kk) {
             const float2 bv = __ldcs(b + int64_t(kk) * n + j);
 #pragma unroll
@@ -981,8 +981,14 @@ void launch_skinny_mx(const float2* a, const float2* b, float2* c, int64_t m, in
     if (m <= n) {
         for (int64_t r0 = 0; r0 < m; r0 += MX) {
             const int rows = int(std::min<int64_t>(MX, m - r0));
-            cgemm_skinny_col_kernel<F64, MX><<<unsigned((n + 255) / 256), 256, 0, s>>>(
-                a + r0 * k, b, c + r0 * n, rows, n, int(k));
+            // separate instantiations: the grouped loop's registers must not
+            // lower the occupancy of the short-k kernel
+            if (k > 4)
+                cgemm_skinny_col_kernel<F64, MX, true><<<unsigned((n + 255) / 256), 256, 0, s>>>(
+                    a + r0 * k, b, c + r0 * n, rows, n, int(k));
+            else
+                cgemm_skinny_col_kernel<F64, MX, false><<<unsigned((n + 255) / 256), 256, 0, s>>>(
+                    a + r0 * k, b, c + r0 * n, rows, n, int(k));
         }
     } else {
         for (int64_t j0 = 0; j0 < n; j0 += MX) {
