@@ -942,7 +942,7 @@ __global__ void __launch_bounds__(256) cgemm_skinny_col_kernel(const float2* __r
 }
 
 // n <= MX: thread i owns row i of C
-template <bool F64, int MX>
+template <bool F64, int MX, bool GROUPED>
 __global__ void __launch_bounds__(256) cgemm_skinny_row_kernel(const float2* __restrict__ a,
                                                                const float2* __restrict__ b,
                                                                float2* __restrict__ c, int64_t m,
@@ -958,14 +958,39 @@ __global__ void __launch_bounds__(256) cgemm_skinny_row_kernel(const float2* __r
 #pragma unroll
     for (int j = 0; j < MX; ++j) p[j][0] = p[j][1] = p[j][2] = p[j][3] = acc_t(0);
     const float2* arow = a + i * k;
-    for (int kk = 0; kk < k; ++kk) {
-        const float2 av = __ldcs(arow + kk);
+    if (!GROUPED) {
+        for (int kk = 0; kk < k; ++kk) {
+            const float2 av = __ldcs(arow + kk);
 #pragma unroll
-        for (int j = 0; j < MX; ++j)
-            if (j < n) {
-                const float2 bv = bs[kk * n + j];
-                chain4<F64>(av.x, av.y, bv.x, bv.y, p[j]);
+            for (int j = 0; j < MX; ++j)
+                if (j < n) {
+                    const float2 bv = bs[kk * n + j];
+                    chain4<F64>(av.x, av.y, bv.x, bv.y, p[j]);
+                }
+        }
+    } else {
+        // even k: the row in 16-B loads, eight elements issued together (one
+        // 8-B load per k kept only ~16 KB in flight per SM -- latency-bound
+        // at 0.35 of HBM for (2^24, 8, 8))
+#pragma unroll 1
+        for (int k0 = 0; k0 < k; k0 += 8) {
+            float4 ar[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (k0 + 2 * u < k) ar[u] = __ldcs(reinterpret_cast<const float4*>(arow + k0) + u);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (k0 + u >= k) break;
+                const float4 q = ar[u / 2];
+                const float avx = (u & 1) ? q.z : q.x, avy = (u & 1) ? q.w : q.y;
+#pragma unroll
+                for (int j = 0; j < MX; ++j)
+                    if (j < n) {
+                        const float2 bv = bs[(k0 + u) * n + j];
+                        chain4<F64>(avx, avy, bv.x, bv.y, p[j]);
+                    }
             }
+        }
     }
     float2* crow = c + i * ldn;
 #pragma unroll
@@ -993,8 +1018,12 @@ void launch_skinny_mx(const float2* a, const float2* b, float2* c, int64_t m, in
     } else {
         for (int64_t j0 = 0; j0 < n; j0 += MX) {
             const int cols = int(std::min<int64_t>(MX, n - j0));
-            cgemm_skinny_row_kernel<F64, MX><<<unsigned((m + 255) / 256), 256, 0, s>>>(
-                a, b + j0, c + j0, m, cols, int(k), n);
+            if (k > 2 && k % 2 == 0 && (reinterpret_cast<uintptr_t>(a) & 15) == 0)
+                cgemm_skinny_row_kernel<F64, MX, true><<<unsigned((m + 255) / 256), 256, 0, s>>>(
+                    a, b + j0, c + j0, m, cols, int(k), n);
+            else
+                cgemm_skinny_row_kernel<F64, MX, false><<<unsigned((m + 255) / 256), 256, 0, s>>>(
+                    a, b + j0, c + j0, m, cols, int(k), n);
         }
     }
 }
