@@ -135,6 +135,50 @@ size_t plan_workspace(const DispatchPlan& p, int64_t m, int64_t n) {
     return 2 * round_up(int64_t(a), 1024) + 2 * round_up(int64_t(b), 1024);
 }
 
+// Operand planes in the workspace + the GEMM arguments of a tensor-core dispatch.
+TcecGemmArgs tc_gemm_args(const Handle& h, const DispatchPlan& p, void* ws, float* c, int64_t m,
+                          int64_t n, DevDecision* d) {
+    const int elem = (p.kind == kKindFp16 || p.forced_scaled) ? 2 : 4;
+    const size_t abytes = round_up(int64_t(size_t(m) * p.kp * elem), 1024);
+    const size_t bbytes = round_up(int64_t(size_t(2 * n) * p.kp * elem), 1024);
+    uint8_t* w = static_cast<uint8_t*>(ws);
+    TcecGemmArgs g{};
+    g.a_hi = w;
+    g.a_lo = w + abytes;
+    g.b_hi = w + 2 * abytes;
+    g.b_lo = w + 2 * abytes + bbytes;
+    g.c = c;
+    g.m = m;
+    g.a_rows = m;
+    g.n2 = 2 * n;
+    g.kp = p.kp;
+    g.d = d;
+    g.kind_fixed = p.kind;
+    g.corrected = p.corrected;
+    g.flush_kblocks = p.corrected ? h.flush_kblocks : 0;
+    g.pair = resolve_gemm_variant(h.gemm_pair, m, 2 * n, p.kp, h.sm_count);
+    g.sms = h.sm_count;
+    g.fmt = (p.kind < 0 && !p.forced_scaled) ? -1  // format chosen by the device decision
+                                             : (p.kind == kKindTf32 ? kTf32 : kFp16);
+    return g;
+}
+
+// GEMM of rows [r0, r1) of A' / C (chunked: no split-K, so a chunk computes
+// exactly what the whole launch would), then the hook's done(r0, r1)
+int launch_gemm_rows(const TcecGemmArgs& g, int64_t r0, int64_t r1, bool chunked,
+                     const ChunkHook* hook, cudaStream_t s) {
+    TcecGemmArgs gc = g;
+    gc.no_split = chunked;
+    gc.m = r1 - r0;
+    gc.a_row_off = r0;
+    gc.c = g.c + r0 * g.n2;
+    const int e = launch_tcec_gemm(gc, s);
+    if (e) return cuda_error(cudaError_t(e), g.fmt < 0 ? "tcec_gemm auto"
+                                             : (g.fmt == kTf32 ? "tcec_gemm tf32" : "tcec_gemm f16"));
+    if (hook && hook->done) return hook->done(hook->ctx, r0, r1);
+    return TCEC_OK;
+}
+
 // Launch the device pipeline of one dispatch (no host synchronization).
 int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t m, int64_t n,
                     int64_t k, const tcec_dispatch_config_t& cfg, const DispatchPlan& p,
@@ -182,53 +226,18 @@ int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t
     default: break;
     }
     // tensor-core tier: operand preparation + tcgen05 GEMM(s)
-    const int elem = (p.kind == kKindFp16 || p.forced_scaled) ? 2 : 4;
-    const size_t abytes = round_up(int64_t(size_t(m) * p.kp * elem), 1024);
-    const size_t bbytes = round_up(int64_t(size_t(2 * n) * p.kp * elem), 1024);
-    uint8_t* w = static_cast<uint8_t*>(ws);
-    void* ahi = w;
-    void* alo = w + abytes;
-    void* bhi = w + 2 * abytes;
-    void* blo = w + 2 * abytes + bbytes;
-    launch_prep_a(a, m, k, p.kp, ahi, alo, d, p.kind, p.corrected, s);
-    launch_prep_b(b, k, n, p.kp, bhi, blo, d, p.kind, p.corrected, s);
+    TcecGemmArgs g = tc_gemm_args(h, p, ws, c, m, n, d);
+    launch_prep_a(a, m, k, p.kp, const_cast<void*>(g.a_hi), const_cast<void*>(g.a_lo), d, p.kind, p.corrected, s);
+    launch_prep_b(b, k, n, p.kp, const_cast<void*>(g.b_hi), const_cast<void*>(g.b_lo), d, p.kind, p.corrected, s);
     if (prof) cudaEventRecord(h.ev[2], s);
-    TcecGemmArgs g{};
-    g.a_hi = ahi;
-    g.a_lo = alo;
-    g.b_hi = bhi;
-    g.b_lo = blo;
-    g.c = c;
-    g.m = m;
-    g.n2 = 2 * n;
-    g.kp = p.kp;
-    g.d = d;
-    g.kind_fixed = p.kind;
-    g.corrected = p.corrected;
-    g.flush_kblocks = p.corrected ? h.flush_kblocks : 0;
-    g.pair = resolve_gemm_variant(h.gemm_pair, m, 2 * n, p.kp, h.sm_count);
-    g.sms = h.sm_count;
-    g.fmt = (p.kind < 0 && !p.forced_scaled) ? -1  // format chosen by the device decision
-                                             : (p.kind == kKindTf32 ? kTf32 : kFp16);
     // row chunks (host-buffer API): only the wide kernel indexes into A' by row
     int chunks = hook ? std::max(1, hook->chunks) : 1;
     if (g.pair != kVariantWide) chunks = 1;
     const int64_t rows_per = round_up((m + chunks - 1) / chunks, 256);
-    g.a_rows = m;
     for (int64_t r0 = 0; r0 < m; r0 += rows_per) {
         const int64_t r1 = std::min(m, r0 + rows_per);
-        TcecGemmArgs gc = g;
-        gc.no_split = chunks > 1;  // a chunk must compute exactly what the whole launch would
-        gc.m = r1 - r0;
-        gc.a_row_off = r0;
-        gc.c = c + r0 * 2 * n;
-        const int e = launch_tcec_gemm(gc, s);
-        if (e) return cuda_error(cudaError_t(e), g.fmt < 0 ? "tcec_gemm auto"
-                                                 : (g.fmt == kTf32 ? "tcec_gemm tf32" : "tcec_gemm f16"));
-        if (hook && hook->done) {
-            const int rc = hook->done(hook->ctx, r0, r1);
-            if (rc) return rc;
-        }
+        const int rc = launch_gemm_rows(g, r0, r1, chunks > 1, hook, s);
+        if (rc) return rc;
     }
     if (prof) cudaEventRecord(h.ev[3], s);
     return TCEC_OK;
@@ -312,6 +321,9 @@ tcec_handle_s::~tcec_handle_s() {
     if (scratch_host) cudaFreeHost(scratch_host);
     if (own_stream) cudaStreamDestroy(own_stream);
     if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (in_stream) cudaStreamDestroy(in_stream);
+    for (auto& e : in_ev)
+        if (e) cudaEventDestroy(e);
     for (auto& e : chunk_ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : ev)
@@ -648,10 +660,82 @@ int tcec_dispatch_cgemm(tcec_handle h, const void* a, const void* b, void* c, in
     return finish_dispatch(p, *h->dec_host, m, n, k, res);
 }
 
+// Host-buffer pipeline of a large tensor-core dispatch (m >= 8192, wide
+// kernel).  B and then row chunks of A are copied on in_stream; the prep + GEMM
+// of A chunk i starts as soon as the chunk has landed and the finished rows of
+// C go back on copy_stream, so the PCIe transfers overlap the tensor-core work
+// instead of preceding it.  The precision decision needs statistics of all of
+// A, which lands last: the chunks therefore run under a decision taken from B
+// and the first chunk (slot 1); the exact decision over all of A and B (slot 0)
+// follows the last chunk, and the caller checks that the two agree in
+// everything prep and GEMM read (kind, scales, the selection-stage flags).
+// On disagreement the plain path reruns on the resident operands, so the
+// result is always the one the unpipelined dispatch produces.
+static int host_pipeline(Handle& h, const uint8_t* a, const uint8_t* b, uint8_t* c, int64_t m,
+                         int64_t n, int64_t k, const tcec_dispatch_config_t& cfg,
+                         const DispatchPlan& p, void* ws, uint8_t* da, uint8_t* db, uint8_t* dc,
+                         int chunks, ChunkHook& hook, DevDecision* d) {
+    cudaStream_t s = h.stream;
+    if (!h.in_stream) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&h.in_stream, cudaStreamNonBlocking));
+        for (auto& e : h.in_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    DevDecision* dr = d;      // exact decision (all of A)
+    DevDecision* ds = d + 1;  // decision the chunks run under
+    DevDecision* snap = d + 2;  // ds right after selection (before prep adds its flags)
+    const int64_t rows_per = round_up((m + chunks - 1) / chunks, 256);
+    const int nch = int((m + rows_per - 1) / rows_per);
+    const size_t row_bytes = size_t(k) * 8;
+    // the staging buffers may still be read by earlier work on the stream
+    CUDA_TRY(cudaEventRecord(h.in_ev[16], s));
+    CUDA_TRY(cudaStreamWaitEvent(h.in_stream, h.in_ev[16], 0));
+    CUDA_TRY(cudaMemcpyAsync(db, b, size_t(k) * n * 8, cudaMemcpyHostToDevice, h.in_stream));
+    CUDA_TRY(cudaEventRecord(h.in_ev[0], h.in_stream));
+    for (int i = 0; i < nch; ++i) {
+        const int64_t r0 = i * rows_per, r1 = std::min(m, r0 + rows_per);
+        CUDA_TRY(cudaMemcpyAsync(da + r0 * row_bytes, a + r0 * row_bytes, size_t(r1 - r0) * row_bytes,
+                                 cudaMemcpyHostToDevice, h.in_stream));
+        CUDA_TRY(cudaEventRecord(h.in_ev[1 + i], h.in_stream));
+    }
+    const float* fa = reinterpret_cast<const float*>(da);
+    const float* fb = reinterpret_cast<const float*>(db);
+    CUDA_TRY(cudaStreamWaitEvent(s, h.in_ev[0], 0));
+    CUDA_TRY(cudaStreamWaitEvent(s, h.in_ev[1], 0));
+    cudaMemsetAsync(ds, 0, sizeof(DevDecision), s);
+    const double t = p.forced_scaled ? 1.0 : cfg.threshold_t;
+    const int64_t rows0 = std::min(m, rows_per);
+    if (p.stats) {
+        launch_stats1(fa, 2 * rows0 * k, fb, 2 * k * n, ds, s);
+        launch_stats2(fa, 2 * rows0 * k, fb, 2 * k * n, ds, t, cfg.target_max_exponent, 0, s);
+        launch_select(ds, cfg.threshold_t, cfg.target_max_exponent, p.forced_scaled ? 1 : 0, s);
+        cudaMemcpyAsync(snap, ds, sizeof(DevDecision), cudaMemcpyDeviceToDevice, s);
+    }
+    TcecGemmArgs g = tc_gemm_args(h, p, ws, reinterpret_cast<float*>(dc), m, n, ds);
+    launch_prep_b(fb, k, n, p.kp, const_cast<void*>(g.b_hi), const_cast<void*>(g.b_lo), ds, p.kind, p.corrected, s);
+    for (int i = 0; i < nch; ++i) {
+        const int64_t r0 = i * rows_per, r1 = std::min(m, r0 + rows_per);
+        CUDA_TRY(cudaStreamWaitEvent(s, h.in_ev[1 + i], 0));
+        launch_prep_a(fa, r1 - r0, k, p.kp, const_cast<void*>(g.a_hi), const_cast<void*>(g.a_lo), ds, p.kind, p.corrected, s, r0);
+        const int rc = launch_gemm_rows(g, r0, r1, true, &hook, s);
+        if (rc) return rc;
+    }
+    if (p.stats) {
+        cudaMemsetAsync(dr, 0, sizeof(DevDecision), s);
+        launch_stats1(fa, 2 * m * k, fb, 2 * k * n, dr, s);
+        launch_stats2(fa, 2 * m * k, fb, 2 * k * n, dr, t, cfg.target_max_exponent, 0, s);
+        launch_select(dr, cfg.threshold_t, cfg.target_max_exponent, p.forced_scaled ? 1 : 0, s);
+    }
+    CUDA_TRY(cudaGetLastError());
+    (void)c;
+    return TCEC_OK;
+}
+
 int tcec_dispatch_cgemm_host(tcec_handle h, const void* a, const void* b, void* c, int64_t m,
                              int64_t n, int64_t k, const tcec_dispatch_config_t* cfg,
                              tcec_dispatch_result_t* res) {
     CHECK_HANDLE(h);
+    if (!cfg || !res) return set_error(TCEC_ERR_INVALID_ARGUMENT, "null argument");
+    if (m < 0 || n < 0 || k < 0) return set_error(TCEC_ERR_SHAPE_MISMATCH, "negative extent");
     const size_t ab = size_t(m) * k * 8, bb = size_t(k) * n * 8, cb = size_t(m) * n * 8;
     const size_t ra = size_t(round_up(int64_t(ab), 256)), rb = size_t(round_up(int64_t(bb), 256));
     const size_t need = ra + rb + cb + 256;
@@ -664,13 +748,9 @@ int tcec_dispatch_cgemm_host(tcec_handle h, const void* a, const void* b, void* 
         h->io_bytes = need;
     }
     uint8_t* base = static_cast<uint8_t*>(h->io);
-    void* da = base;
-    void* db = base + ra;
-    void* dc = base + ra + rb;
-    CUDA_TRY(cudaMemcpyAsync(da, a, ab, cudaMemcpyHostToDevice, h->stream));
-    CUDA_TRY(cudaMemcpyAsync(db, b, bb, cudaMemcpyHostToDevice, h->stream));
-    if (!cfg || !res) return set_error(TCEC_ERR_INVALID_ARGUMENT, "null argument");
-    if (m < 0 || n < 0 || k < 0) return set_error(TCEC_ERR_SHAPE_MISMATCH, "negative extent");
+    uint8_t* da = base;
+    uint8_t* db = base + ra;
+    uint8_t* dc = base + ra + rb;
     // the GEMM runs in row chunks; each finished chunk of C is copied back on
     // a second stream while the next chunk computes
     if (!h->copy_stream) {
@@ -691,7 +771,7 @@ int tcec_dispatch_cgemm_host(tcec_handle h, const void* a, const void* b, void* 
         int64_t row_bytes;
         int used;
         cudaError_t err;
-    } ctx{h, static_cast<uint8_t*>(c), static_cast<const uint8_t*>(dc), n * 8, 0, cudaSuccess};
+    } ctx{h, static_cast<uint8_t*>(c), dc, n * 8, 0, cudaSuccess};
     ChunkHook hook;
     hook.chunks = m >= 8192 ? 4 : 1;
     hook.ctx = &ctx;
@@ -710,9 +790,47 @@ int tcec_dispatch_cgemm_host(tcec_handle h, const void* a, const void* b, void* 
         }
         return TCEC_OK;
     };
-    DevDecision* d = h->dec;
-    int rc = launch_dispatch(*h, static_cast<const float*>(da), static_cast<const float*>(db),
-                             static_cast<float*>(dc), m, n, k, *cfg, p, d, ws, &hook);
+    // operand copies overlapped with the GEMM (host_pipeline) for large
+    // tensor-core dispatches; TCEC_HOST_CHUNKS = 0 disables
+    static const int pipe_chunks = [] {
+        const char* e = std::getenv("TCEC_HOST_CHUNKS");
+        return e ? std::max(0, std::min(15, std::atoi(e))) : 12;
+    }();
+    const bool pipelined = pipe_chunks > 1 && p.tier == kTierTc && m >= 8192 && n > 0 && k > 0 &&
+                           !(h->prof && h->ev[0]) &&
+                           resolve_gemm_variant(h->gemm_pair, m, 2 * n, p.kp, h->sm_count) == kVariantWide;
+    DevDecision* d = pipelined ? h->decisions(3) : h->dec;
+    if (!d) return set_error(TCEC_ERR_CUDA, "decision slots allocation failed");
+    if (pipelined) {
+        hook.chunks = pipe_chunks;
+        int rc = host_pipeline(*h, static_cast<const uint8_t*>(a), static_cast<const uint8_t*>(b),
+                               static_cast<uint8_t*>(c), m, n, k, *cfg, p, ws, da, db, dc, pipe_chunks,
+                               hook, d);
+        if (rc) return rc;
+        CUDA_TRY(cudaMemcpyAsync(h->dec_host, d, 3 * sizeof(DevDecision), cudaMemcpyDeviceToHost,
+                                 h->stream));
+        CUDA_TRY(cudaStreamSynchronize(h->stream));
+        CUDA_TRY(cudaStreamSynchronize(h->copy_stream));
+        const DevDecision& dr = h->dec_host[0];
+        const DevDecision& ds = h->dec_host[1];
+        const DevDecision& snap = h->dec_host[2];
+        if (!p.stats) return finish_dispatch(p, ds, m, n, k, res);
+        if (dr.kind == snap.kind && dr.scale_a == snap.scale_a && dr.scale_b == snap.scale_b &&
+            dr.overflow == snap.overflow && dr.scale_overflow == snap.scale_overflow) {
+            DevDecision merged = dr;
+            merged.overflow = ds.overflow;
+            merged.scale_overflow = ds.scale_overflow;
+            return finish_dispatch(p, merged, m, n, k, res);
+        }
+        // the first chunk was not representative: plain path on the resident operands
+        ctx.used = 0;
+        hook.chunks = 4;
+    } else {
+        CUDA_TRY(cudaMemcpyAsync(da, a, ab, cudaMemcpyHostToDevice, h->stream));
+        CUDA_TRY(cudaMemcpyAsync(db, b, bb, cudaMemcpyHostToDevice, h->stream));
+    }
+    int rc = launch_dispatch(*h, reinterpret_cast<const float*>(da), reinterpret_cast<const float*>(db),
+                             reinterpret_cast<float*>(dc), m, n, k, *cfg, p, d, ws, &hook);
     if (rc) return rc;
     CUDA_TRY(cudaGetLastError());
     if (ctx.used == 0 && m > 0 && n > 0)

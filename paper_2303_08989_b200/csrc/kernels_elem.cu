@@ -364,7 +364,9 @@ TCEC_DEV void convert_n(float (&x)[N], const PrepMode& pm, double factor, float 
 __global__ void __launch_bounds__(kThreads) prep_a_kernel(const float* __restrict__ a, int64_t m,
                                                           int64_t k2, int64_t kp, void* hi_v,
                                                           void* lo_v, const DevDecision* d,
-                                                          int kind_fixed, int corrected) {
+                                                          int kind_fixed, int corrected, int64_t row0) {
+    // rows [row0, row0 + m) of A (the host-buffer pipeline converts row chunks
+    // as they arrive; every row is independent)
     const PrepMode pm = prep_mode(d, kind_fixed, false);
     if (!pm.active) return;
     const double factor = ldexp(1.0, pm.scale);
@@ -375,8 +377,9 @@ __global__ void __launch_bounds__(kThreads) prep_a_kernel(const float* __restric
     const bool vec = (k2 % 8) == 0 && (reinterpret_cast<uintptr_t>(a) & 15u) == 0;
     for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < total;
          c += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t row = c / chunks_per_row;
-        const int64_t col = (c - row * chunks_per_row) * 8;
+        const int64_t rl = c / chunks_per_row;
+        const int64_t col = (c - rl * chunks_per_row) * 8;
+        const int64_t row = row0 + rl;
         float x[8];
         if (vec && col < k2) {
             const float4* p = reinterpret_cast<const float4*>(a + row * k2 + col);
@@ -1385,11 +1388,11 @@ void launch_select(DevDecision* d, double t, int target, int forced_scaled, cuda
 }
 
 void launch_prep_a(const float* a, int64_t m, int64_t k, int64_t kp, void* hi, void* lo,
-                   const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s) {
+                   const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s, int64_t row0) {
     const int64_t total = m * (kp / 8);
     if (total <= 0) return;
     prep_a_kernel<<<grid_for(total, kThreads, 148 * 32), kThreads, 0, s>>>(
-        a, m, 2 * k, kp, hi, lo, d, kind_fixed, corrected);
+        a, m, 2 * k, kp, hi, lo, d, kind_fixed, corrected, row0);
 }
 
 void launch_prep_b(const float* b, int64_t k, int64_t n, int64_t kp, void* hi, void* lo,

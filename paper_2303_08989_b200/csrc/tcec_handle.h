@@ -29,6 +29,8 @@ struct tcec_handle_s {
     void* scratch_host = nullptr;  // pinned 4 KiB
     cudaStream_t copy_stream = nullptr;  // D2H of finished row chunks (host-buffer API)
     cudaEvent_t chunk_ev[8] = {};
+    cudaStream_t in_stream = nullptr;  // H2D of operand row chunks (host-buffer pipeline)
+    cudaEvent_t in_ev[17] = {};
     // stage profiling (tcec_profile_*): CUDA events around the stages of a
     // dispatched CGEMM, accumulated after each synchronous dispatch
     bool prof = false;

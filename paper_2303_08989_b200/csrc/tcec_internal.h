@@ -55,7 +55,8 @@ void launch_select(DevDecision* d, double t, int target, int forced_scaled, cuda
 // decided format (f16 or tf32-in-f32); padded columns are zero.
 // kind_fixed >= 0 overrides the device decision (forced / size-gated modes).
 void launch_prep_a(const float* a, int64_t m, int64_t k, int64_t kp, void* hi, void* lo,
-                   const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s);
+                   const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s,
+                   int64_t row0 = 0);  // rows [row0, row0 + m) of a full A / A'
 // B (k x n complex) -> B'^T = 2n x Kp real, K-major, with the complex block
 // expansion [[Br, Bi], [-Bi, Br]] so one real GEMM yields interleaved C.
 void launch_prep_b(const float* b, int64_t k, int64_t n, int64_t kp, void* hi, void* lo,
