@@ -892,6 +892,28 @@ TCEC_DEV float2 assemble(const T (&p)[4]) {
     return make_float2(__fsub_rn(float(p[0]), float(p[1])), __fadd_rn(float(p[2]), float(p[3])));
 }
 
+// The short operand sits in shared memory as [k][MX], zero-padded beyond the
+// m (or n) real rows, so the inner loops carry no per-row predicates: every
+// thread runs all MX x 4 chains (the padded ones are never stored) and reads
+// two short-side elements per 16-B LDS.  Full groups of 8 k are unrolled
+// without bounds checks (ncu: predicates and loop branches were ~45% of the
+// issued instructions of the guarded version).
+template <bool F64, int MX>
+TCEC_DEV void skinny_mac(const float2* __restrict__ srow, float xr, float xi,
+                         typename std::conditional<F64, double, float>::type (&p)[MX][4], bool a_side) {
+#pragma unroll
+    for (int q = 0; q < MX / 2; ++q) {
+        const float4 s2 = reinterpret_cast<const float4*>(srow)[q];
+        if (a_side) {  // short side is A (column kernel): chains (a_i, x)
+            chain4<F64>(s2.x, s2.y, xr, xi, p[2 * q]);
+            chain4<F64>(s2.z, s2.w, xr, xi, p[2 * q + 1]);
+        } else {       // short side is B (row kernel): chains (x, b_j)
+            chain4<F64>(xr, xi, s2.x, s2.y, p[2 * q]);
+            chain4<F64>(xr, xi, s2.z, s2.w, p[2 * q + 1]);
+        }
+    }
+}
+
 // m <= MX: thread j owns column j of C
 template <bool F64, int MX, bool GROUPED>
 __global__ void __launch_bounds__(256) cgemm_skinny_col_kernel(const float2* __restrict__ a,
@@ -899,45 +921,33 @@ __global__ void __launch_bounds__(256) cgemm_skinny_col_kernel(const float2* __r
                                                                float2* __restrict__ c, int m,
                                                                int64_t n, int k) {
     using acc_t = typename std::conditional<F64, double, float>::type;
-    __shared__ float2 as[MX * kSkinnyMaxK];
-    for (int t = threadIdx.x; t < m * k; t += blockDim.x) as[t] = a[t];
+    __shared__ __align__(16) float2 as[kSkinnyMaxK * MX];  // [kk][i]
+    for (int t = threadIdx.x; t < k * MX; t += blockDim.x) {
+        const int kk = t / MX, i = t % MX;
+        as[t] = i < m ? a[i * k + kk] : make_float2(0.0f, 0.0f);
+    }
     __syncthreads();
     const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= n) return;
     acc_t p[MX][4];
 #pragma unroll
     for (int i = 0; i < MX; ++i) p[i][0] = p[i][1] = p[i][2] = p[i][3] = acc_t(0);
-    if (!GROUPED) {  // A/B on B200: the plain loop wins for k <= 4, grouped loads from 8 up
-        for (int kk = 0; kk < k; ++kk) {
-            const float2 bv = __ldcs(b + int64_t(kk) * n + j);
-#pragma unroll
-            for (int i = 0; i < MX; ++i)
-                if (i < m) {
-                    const float2 av = as[i * k + kk];
-                    chain4<F64>(av.x, av.y, bv.x, bv.y, p[i]);
-                }
-        }
-    } else {
-    // longer k: loads in groups of 8 issued together (8 in flight per thread
-    // instead of one memory latency per k)
+    int k0 = 0;
+    if (GROUPED) {  // A/B on B200: the plain loop wins for k <= 4, grouped loads from 8 up
+        // 8 loads in flight per thread instead of one memory latency per k
 #pragma unroll 1
-    for (int k0 = 0; k0 < k; k0 += 8) {
-        float2 bcol[8];
+        for (; k0 + 8 <= k; k0 += 8) {
+            float2 bcol[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-            if (k0 + u < k) bcol[u] = __ldcs(b + int64_t(k0 + u) * n + j);
+            for (int u = 0; u < 8; ++u) bcol[u] = __ldcs(b + int64_t(k0 + u) * n + j);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            if (k0 + u >= k) break;
-            const float2 bv = bcol[u];
-#pragma unroll
-            for (int i = 0; i < MX; ++i)
-                if (i < m) {
-                    const float2 av = as[i * k + k0 + u];
-                    chain4<F64>(av.x, av.y, bv.x, bv.y, p[i]);
-                }
+            for (int u = 0; u < 8; ++u) skinny_mac<F64, MX>(as + (k0 + u) * MX, bcol[u].x, bcol[u].y, p, true);
         }
     }
+#pragma unroll 1
+    for (; k0 < k; ++k0) {
+        const float2 bv = __ldcs(b + int64_t(k0) * n + j);
+        skinny_mac<F64, MX>(as + k0 * MX, bv.x, bv.y, p, true);
     }
 #pragma unroll
     for (int i = 0; i < MX; ++i)
@@ -952,8 +962,11 @@ __global__ void __launch_bounds__(256) cgemm_skinny_row_kernel(const float2* __r
                                                                int n, int k, int64_t ldn) {
     // columns [0, n) of a block of B / C whose row stride is ldn
     using acc_t = typename std::conditional<F64, double, float>::type;
-    __shared__ float2 bs[kSkinnyMaxK * MX];
-    for (int t = threadIdx.x; t < k * n; t += blockDim.x) bs[t] = b[int64_t(t / n) * ldn + t % n];
+    __shared__ __align__(16) float2 bs[kSkinnyMaxK * MX];  // [kk][j]
+    for (int t = threadIdx.x; t < k * MX; t += blockDim.x) {
+        const int kk = t / MX, jj = t % MX;
+        bs[t] = jj < n ? b[int64_t(kk) * ldn + jj] : make_float2(0.0f, 0.0f);
+    }
     __syncthreads();
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= m) return;
@@ -961,39 +974,26 @@ __global__ void __launch_bounds__(256) cgemm_skinny_row_kernel(const float2* __r
 #pragma unroll
     for (int j = 0; j < MX; ++j) p[j][0] = p[j][1] = p[j][2] = p[j][3] = acc_t(0);
     const float2* arow = a + i * k;
-    if (!GROUPED) {
-        for (int kk = 0; kk < k; ++kk) {
-            const float2 av = __ldcs(arow + kk);
-#pragma unroll
-            for (int j = 0; j < MX; ++j)
-                if (j < n) {
-                    const float2 bv = bs[kk * n + j];
-                    chain4<F64>(av.x, av.y, bv.x, bv.y, p[j]);
-                }
-        }
-    } else {
-        // even k: the row in 16-B loads, eight elements issued together (one
-        // 8-B load per k kept only ~16 KB in flight per SM -- latency-bound
-        // at 0.35 of HBM for (2^24, 8, 8))
+    int k0 = 0;
+    if (GROUPED) {
+        // even k, 16-B aligned A: the row in 16-B loads, eight elements issued
+        // together (one 8-B load per k kept only ~16 KB in flight per SM)
 #pragma unroll 1
-        for (int k0 = 0; k0 < k; k0 += 8) {
+        for (; k0 + 8 <= k; k0 += 8) {
             float4 ar[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (k0 + 2 * u < k) ar[u] = __ldcs(reinterpret_cast<const float4*>(arow + k0) + u);
+            for (int u = 0; u < 4; ++u) ar[u] = __ldcs(reinterpret_cast<const float4*>(arow + k0) + u);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                if (k0 + u >= k) break;
-                const float4 q = ar[u / 2];
-                const float avx = (u & 1) ? q.z : q.x, avy = (u & 1) ? q.w : q.y;
-#pragma unroll
-                for (int j = 0; j < MX; ++j)
-                    if (j < n) {
-                        const float2 bv = bs[(k0 + u) * n + j];
-                        chain4<F64>(avx, avy, bv.x, bv.y, p[j]);
-                    }
+            for (int u = 0; u < 4; ++u) {
+                skinny_mac<F64, MX>(bs + (k0 + 2 * u) * MX, ar[u].x, ar[u].y, p, false);
+                skinny_mac<F64, MX>(bs + (k0 + 2 * u + 1) * MX, ar[u].z, ar[u].w, p, false);
             }
         }
+    }
+#pragma unroll 1
+    for (; k0 < k; ++k0) {
+        const float2 av = __ldcs(arow + k0);
+        skinny_mac<F64, MX>(bs + k0 * MX, av.x, av.y, p, false);
     }
     float2* crow = c + i * ldn;
 #pragma unroll
@@ -1011,7 +1011,7 @@ void launch_skinny_mx(const float2* a, const float2* b, float2* c, int64_t m, in
             const int rows = int(std::min<int64_t>(MX, m - r0));
             // separate instantiations: the grouped loop's registers must not
             // lower the occupancy of the short-k kernel
-            if (k > 4)
+            if (k >= 8)
                 cgemm_skinny_col_kernel<F64, MX, true><<<unsigned((n + 255) / 256), 256, 0, s>>>(
                     a + r0 * k, b, c + r0 * n, rows, n, int(k));
             else
@@ -1021,7 +1021,7 @@ void launch_skinny_mx(const float2* a, const float2* b, float2* c, int64_t m, in
     } else {
         for (int64_t j0 = 0; j0 < n; j0 += MX) {
             const int cols = int(std::min<int64_t>(MX, n - j0));
-            if (k > 2 && k % 2 == 0 && (reinterpret_cast<uintptr_t>(a) & 15) == 0)
+            if (k >= 8 && k % 2 == 0 && (reinterpret_cast<uintptr_t>(a) & 15) == 0)
                 cgemm_skinny_row_kernel<F64, MX, true><<<unsigned((m + 255) / 256), 256, 0, s>>>(
                     a, b + j0, c + j0, m, cols, int(k), n);
             else
