@@ -954,7 +954,10 @@ __global__ void __launch_bounds__(256) cgemm_skinny_col_kernel(const float2* __r
         if (i < m) __stcs(c + int64_t(i) * n + j, assemble<F64>(p[i]));
 }
 
-// n <= MX: thread i owns row i of C
+// n <= MX: thread i owns row i of C.  GROUPED (k >= 8, MX <= 8): each warp
+// stages its 32 rows of A through shared memory eight k at a time and writes
+// its 32 x n block of C back the same way, so global loads and stores are
+// row-contiguous runs instead of one lane-strided 8-B access per element.
 template <bool F64, int MX, bool GROUPED>
 __global__ void __launch_bounds__(256) cgemm_skinny_row_kernel(const float2* __restrict__ a,
                                                                const float2* __restrict__ b,
@@ -962,43 +965,78 @@ __global__ void __launch_bounds__(256) cgemm_skinny_row_kernel(const float2* __r
                                                                int n, int k, int64_t ldn) {
     // columns [0, n) of a block of B / C whose row stride is ldn
     using acc_t = typename std::conditional<F64, double, float>::type;
+    constexpr int SW = (MX + 1) > 9 ? (MX + 1) : 9;  // staging row stride (odd: conflict-free)
     __shared__ __align__(16) float2 bs[kSkinnyMaxK * MX];  // [kk][j]
+    __shared__ float2 stage[GROUPED ? 8 * 32 * SW : 1];
     for (int t = threadIdx.x; t < k * MX; t += blockDim.x) {
         const int kk = t / MX, jj = t % MX;
         bs[t] = jj < n ? b[int64_t(kk) * ldn + jj] : make_float2(0.0f, 0.0f);
     }
     __syncthreads();
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= m) return;
     acc_t p[MX][4];
 #pragma unroll
     for (int j = 0; j < MX; ++j) p[j][0] = p[j][1] = p[j][2] = p[j][3] = acc_t(0);
-    const float2* arow = a + i * k;
-    int k0 = 0;
-    if (GROUPED) {
-        // even k, 16-B aligned A: the row in 16-B loads, eight elements issued
-        // together (one 8-B load per k kept only ~16 KB in flight per SM)
+    if (!GROUPED) {
+        const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+        if (i >= m) return;
+        const float2* arow = a + i * k;
 #pragma unroll 1
-        for (; k0 + 8 <= k; k0 += 8) {
-            float4 ar[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) ar[u] = __ldcs(reinterpret_cast<const float4*>(arow + k0) + u);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                skinny_mac<F64, MX>(bs + (k0 + 2 * u) * MX, ar[u].x, ar[u].y, p, false);
-                skinny_mac<F64, MX>(bs + (k0 + 2 * u + 1) * MX, ar[u].z, ar[u].w, p, false);
-            }
+        for (int k0 = 0; k0 < k; ++k0) {
+            const float2 av = __ldcs(arow + k0);
+            skinny_mac<F64, MX>(bs + k0 * MX, av.x, av.y, p, false);
         }
+        float2* crow = c + i * ldn;
+#pragma unroll
+        for (int j = 0; j < MX; ++j)
+            if (j < n) __stcs(crow + j, assemble<F64>(p[j]));
+        return;
+    }
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31);
+    if (w0 >= m) return;  // whole warp past the end
+    const int rows = int(min(int64_t(32), m - w0));
+    float2* st = stage + (threadIdx.x >> 5) * 32 * SW;
+    const float2* ablk = a + w0 * k;
+    int k0 = 0;
+#pragma unroll 1
+    for (; k0 + 8 <= k; k0 += 8) {
+        float2 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {  // element e = lane + 32u of the 32 x 8 slab: row e / 8, column e % 8
+            const int r = (lane >> 3) + 4 * u;
+            v[u] = r < rows ? __ldcs(ablk + int64_t(r) * k + k0 + (lane & 7)) : make_float2(0.0f, 0.0f);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) st[((lane >> 3) + 4 * u) * SW + (lane & 7)] = v[u];
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const float2 av = st[lane * SW + q];
+            skinny_mac<F64, MX>(bs + (k0 + q) * MX, av.x, av.y, p, false);
+        }
+        __syncwarp();
     }
 #pragma unroll 1
     for (; k0 < k; ++k0) {
-        const float2 av = __ldcs(arow + k0);
+        const float2 av = lane < rows ? __ldcs(ablk + int64_t(lane) * k + k0) : make_float2(0.0f, 0.0f);
         skinny_mac<F64, MX>(bs + k0 * MX, av.x, av.y, p, false);
     }
-    float2* crow = c + i * ldn;
 #pragma unroll
-    for (int j = 0; j < MX; ++j)
-        if (j < n) __stcs(crow + j, assemble<F64>(p[j]));
+    for (int j = 0; j < MX; ++j) st[lane * SW + j] = assemble<F64>(p[j]);
+    __syncwarp();
+    float2* cblk = c + w0 * ldn;
+    if (n == MX) {
+#pragma unroll
+        for (int u = 0; u < MX; ++u) {
+            const int e = lane + 32 * u, r = e / MX, j = e % MX;
+            if (r < rows) __stcs(cblk + int64_t(r) * ldn + j, st[r * SW + j]);
+        }
+    } else {
+        for (int e = lane; e < rows * n; e += 32) {
+            const int r = e / n, j = e - r * n;
+            __stcs(cblk + int64_t(r) * ldn + j, st[r * SW + j]);
+        }
+    }
 }
 
 template <bool F64, int MX>
@@ -1021,12 +1059,15 @@ void launch_skinny_mx(const float2* a, const float2* b, float2* c, int64_t m, in
     } else {
         for (int64_t j0 = 0; j0 < n; j0 += MX) {
             const int cols = int(std::min<int64_t>(MX, n - j0));
-            if (k >= 8 && k % 2 == 0 && (reinterpret_cast<uintptr_t>(a) & 15) == 0)
-                cgemm_skinny_row_kernel<F64, MX, true><<<unsigned((m + 255) / 256), 256, 0, s>>>(
-                    a, b + j0, c + j0, m, cols, int(k), n);
-            else
-                cgemm_skinny_row_kernel<F64, MX, false><<<unsigned((m + 255) / 256), 256, 0, s>>>(
-                    a, b + j0, c + j0, m, cols, int(k), n);
+            if constexpr (MX <= 8) {  // the staging buffer of MX = 16 would not fit next to B
+                if (k >= 8) {
+                    cgemm_skinny_row_kernel<F64, MX, true><<<unsigned((m + 255) / 256), 256, 0, s>>>(
+                        a, b + j0, c + j0, m, cols, int(k), n);
+                    continue;
+                }
+            }
+            cgemm_skinny_row_kernel<F64, MX, false><<<unsigned((m + 255) / 256), 256, 0, s>>>(
+                a, b + j0, c + j0, m, cols, int(k), n);
         }
     }
 }

@@ -280,7 +280,8 @@ def test_long_k_kernels_bit_exact(handle, orc, dev, shape):
 
 @pytest.mark.parametrize("shape", [(2, 4096, 2), (3, 5000, 7), (16, 8192, 32), (9, 4100, 1),
                                    (5000, 9, 31), (8192, 16, 1), (4096, 2, 2), (4097, 5, 17),
-                                   (32, 5000, 8), (20, 4200, 100), (5000, 32, 128), (17, 4096, 64)])
+                                   (32, 5000, 8), (20, 4200, 100), (5000, 32, 128), (17, 4096, 64),
+                                   (4100, 8, 8), (6000, 3, 24), (4133, 7, 9), (4096, 4, 16), (4111, 2, 40)])
 def test_skinny_kernels_bit_exact(handle, orc, dev, shape):
     """Irregular skinny shapes (k <= 128, one outer dim <= 32: PAPER.md:346-352)
     take the thread-per-column / thread-per-row kernels; the chains keep the
