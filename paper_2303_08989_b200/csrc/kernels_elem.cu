@@ -967,7 +967,7 @@ __global__ void __launch_bounds__(256) cgemm_skinny_row_kernel(const float2* __r
     using acc_t = typename std::conditional<F64, double, float>::type;
     constexpr int SW = (MX + 1) > 9 ? (MX + 1) : 9;  // staging row stride (odd: conflict-free)
     __shared__ __align__(16) float2 bs[kSkinnyMaxK * MX];  // [kk][j]
-    __shared__ float2 stage[GROUPED ? 8 * 32 * SW : 1];
+    extern __shared__ float2 stage[];  // GROUPED: 8 warps x 32 rows x SW (dynamic, > 48 KB with B at MX = 16)
     for (int t = threadIdx.x; t < k * MX; t += blockDim.x) {
         const int kk = t / MX, jj = t % MX;
         bs[t] = jj < n ? b[int64_t(kk) * ldn + jj] : make_float2(0.0f, 0.0f);
@@ -1059,9 +1059,14 @@ void launch_skinny_mx(const float2* a, const float2* b, float2* c, int64_t m, in
     } else {
         for (int64_t j0 = 0; j0 < n; j0 += MX) {
             const int cols = int(std::min<int64_t>(MX, n - j0));
-            if constexpr (MX <= 8) {  // the staging buffer of MX = 16 would not fit next to B
-                if (k >= 8) {
-                    cgemm_skinny_row_kernel<F64, MX, true><<<unsigned((m + 255) / 256), 256, 0, s>>>(
+            if (k >= 8) {
+                constexpr int SW = (MX + 1) > 9 ? (MX + 1) : 9;
+                constexpr int stage_bytes = 8 * 32 * SW * int(sizeof(float2));
+                static const bool attr = cudaFuncSetAttribute(cgemm_skinny_row_kernel<F64, MX, true>,
+                                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                              stage_bytes) == cudaSuccess;
+                if (attr) {
+                    cgemm_skinny_row_kernel<F64, MX, true><<<unsigned((m + 255) / 256), 256, stage_bytes, s>>>(
                         a, b + j0, c + j0, m, cols, int(k), n);
                     continue;
                 }

@@ -10,8 +10,11 @@ from paper_2303_08989_b200 import Handle, make_config  # noqa: E402
 h = Handle(0)
 dev = torch.device("cuda:0")
 cfg = make_config(force="FP32_REF")
-for (m, n, k) in [(2, 1 << 26, 2), (8, 1 << 24, 8), (16, 1 << 22, 16), (16, 1 << 24, 16), (4, 1 << 24, 32),
-                  (1 << 24, 8, 8), (1 << 26, 2, 2)]:
+SHAPES = [(2, 1 << 26, 2), (8, 1 << 24, 8), (16, 1 << 22, 16), (16, 1 << 24, 16), (4, 1 << 24, 32),
+          (1 << 24, 8, 8), (1 << 26, 2, 2), (1 << 22, 32, 8), (1 << 21, 16, 32), (1 << 20, 16, 16)]
+if os.environ.get("SHAPES"):
+    SHAPES = [tuple(int(v) for v in s.split("x")) for s in os.environ["SHAPES"].split(",")]
+for (m, n, k) in SHAPES:
     a = torch.randn(m, k, dtype=torch.complex64, device=dev)
     b = torch.randn(k, n, dtype=torch.complex64, device=dev)
     c = torch.empty(m, n, dtype=torch.complex64, device=dev)

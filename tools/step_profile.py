@@ -54,5 +54,5 @@ for (m, n, k), cnt in shapes.items():
 rows.sort(reverse=True)
 tot = sum(r[0] for r in rows)
 print(f"total GEMM time per slice (steps >= 2^20 MACs): {tot:.2f} ms")
-for r in rows[:25]:
+for r in rows[:int(os.environ.get("TOP", "25"))]:
     print(f"{r[0]:7.2f} ms  x{r[1]:<3d} {str(r[2]):26s} {r[3]:16s} {r[4]:7.3f} ms  {r[5]:7.1f} TF  {r[6]:6.0f} GB/s")
