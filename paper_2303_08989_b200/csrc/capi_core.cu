@@ -322,6 +322,7 @@ tcec_handle_s::~tcec_handle_s() {
     if (own_stream) cudaStreamDestroy(own_stream);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (in_stream) cudaStreamDestroy(in_stream);
+    if (gemm_stream2) cudaStreamDestroy(gemm_stream2);
     for (auto& e : in_ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : chunk_ev)
@@ -661,63 +662,142 @@ int tcec_dispatch_cgemm(tcec_handle h, const void* a, const void* b, void* c, in
 }
 
 // Host-buffer pipeline of a large tensor-core dispatch (m >= 8192, wide
-// kernel).  B and then row chunks of A are copied on in_stream; the prep + GEMM
-// of A chunk i starts as soon as the chunk has landed and the finished rows of
-// C go back on copy_stream, so the PCIe transfers overlap the tensor-core work
-// instead of preceding it.  The precision decision needs statistics of all of
-// A, which lands last: the chunks therefore run under a decision taken from B
-// and the first chunk (slot 1); the exact decision over all of A and B (slot 0)
-// follows the last chunk, and the caller checks that the two agree in
-// everything prep and GEMM read (kind, scales, the selection-stage flags).
-// On disagreement the plain path reruns on the resident operands, so the
-// result is always the one the unpipelined dispatch produces.
+// kernel).  Operands go up on in_stream as column parts of B (packed part by
+// part into the staging buffer) and row chunks of A, in the order
+// B[front parts], A[0..], B[back parts]; every (A chunk, B column block) GEMM
+// starts as soon as both have landed, and each finished block of C goes back
+// on copy_stream -- the PCIe transfers overlap the tensor-core work instead of
+// preceding it (16384^3: the GEMM starts after ~1/2 of B and 1/12 of A instead
+// of all of B).  GEMM blocks alternate between two streams so one block's
+// tail overlaps the next block's start.
+//
+// The precision decision needs statistics of all of A and B, which land last:
+// the blocks therefore run under a decision taken from the front parts of B
+// and the first chunk of A (slot 1); the exact decision over everything (slot
+// 0) follows, and the caller checks that the two agree in everything prep and
+// GEMM read (kind, scales, the selection-stage flags).  On disagreement the
+// plain path reruns (tcec_dispatch_cgemm_host), so the result is always the
+// one the unpipelined dispatch produces.  Statistics are order-free counts and
+// maxima, so the part-packed staging of B yields the same statistics.
+struct HostPipe {
+    int nch = 1, q = 1, front = 1;
+    int64_t rows_per = 0, wq = 0;
+};
+
+static HostPipe plan_host_pipe(int64_t m, int64_t n, int chunks, int parts) {
+    HostPipe hp;
+    hp.rows_per = round_up((m + chunks - 1) / chunks, 256);
+    hp.nch = int((m + hp.rows_per - 1) / hp.rows_per);
+    hp.q = n >= 512 * parts ? parts : 1;
+    hp.wq = round_up((n + hp.q - 1) / hp.q, 128);  // even column offsets keep C blocks 16-B aligned
+    hp.q = int((n + hp.wq - 1) / hp.wq);
+    hp.front = std::max(1, hp.q / 2);
+    return hp;
+}
+
 static int host_pipeline(Handle& h, const uint8_t* a, const uint8_t* b, uint8_t* c, int64_t m,
                          int64_t n, int64_t k, const tcec_dispatch_config_t& cfg,
                          const DispatchPlan& p, void* ws, uint8_t* da, uint8_t* db, uint8_t* dc,
-                         int chunks, ChunkHook& hook, DevDecision* d) {
+                         const HostPipe& hp, DevDecision* d) {
     cudaStream_t s = h.stream;
     if (!h.in_stream) {
         CUDA_TRY(cudaStreamCreateWithFlags(&h.in_stream, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&h.gemm_stream2, cudaStreamNonBlocking));
         for (auto& e : h.in_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
-    DevDecision* dr = d;      // exact decision (all of A)
-    DevDecision* ds = d + 1;  // decision the chunks run under
+    DevDecision* dr = d;        // exact decision (all of A and B)
+    DevDecision* ds = d + 1;    // decision the blocks run under
     DevDecision* snap = d + 2;  // ds right after selection (before prep adds its flags)
-    const int64_t rows_per = round_up((m + chunks - 1) / chunks, 256);
-    const int nch = int((m + rows_per - 1) / rows_per);
     const size_t row_bytes = size_t(k) * 8;
+    auto j0_of = [&](int j) { return int64_t(j) * hp.wq; };
+    auto w_of = [&](int j) { return std::min(hp.wq, n - j0_of(j)); };
+    cudaEvent_t* ev_b = h.in_ev;              // B column parts
+    cudaEvent_t* ev_a = h.in_ev + hp.q;       // A row chunks
+    cudaEvent_t ev_sync = h.in_ev[16];        // stream-to-stream ordering
     // the staging buffers may still be read by earlier work on the stream
-    CUDA_TRY(cudaEventRecord(h.in_ev[16], s));
-    CUDA_TRY(cudaStreamWaitEvent(h.in_stream, h.in_ev[16], 0));
-    CUDA_TRY(cudaMemcpyAsync(db, b, size_t(k) * n * 8, cudaMemcpyHostToDevice, h.in_stream));
-    CUDA_TRY(cudaEventRecord(h.in_ev[0], h.in_stream));
-    for (int i = 0; i < nch; ++i) {
-        const int64_t r0 = i * rows_per, r1 = std::min(m, r0 + rows_per);
+    CUDA_TRY(cudaEventRecord(ev_sync, s));
+    CUDA_TRY(cudaStreamWaitEvent(h.in_stream, ev_sync, 0));
+    auto put_b = [&](int j) -> int {
+        const int64_t j0 = j0_of(j), w = w_of(j);
+        CUDA_TRY(cudaMemcpy2DAsync(db + size_t(k) * j0 * 8, size_t(w) * 8, b + j0 * 8, size_t(n) * 8,
+                                   size_t(w) * 8, size_t(k), cudaMemcpyHostToDevice, h.in_stream));
+        CUDA_TRY(cudaEventRecord(ev_b[j], h.in_stream));
+        return TCEC_OK;
+    };
+    for (int j = 0; j < hp.front; ++j)
+        if (int rc = put_b(j)) return rc;
+    for (int i = 0; i < hp.nch; ++i) {
+        const int64_t r0 = i * hp.rows_per, r1 = std::min(m, r0 + hp.rows_per);
         CUDA_TRY(cudaMemcpyAsync(da + r0 * row_bytes, a + r0 * row_bytes, size_t(r1 - r0) * row_bytes,
                                  cudaMemcpyHostToDevice, h.in_stream));
-        CUDA_TRY(cudaEventRecord(h.in_ev[1 + i], h.in_stream));
+        CUDA_TRY(cudaEventRecord(ev_a[i], h.in_stream));
     }
+    for (int j = hp.front; j < hp.q; ++j)
+        if (int rc = put_b(j)) return rc;
+
     const float* fa = reinterpret_cast<const float*>(da);
     const float* fb = reinterpret_cast<const float*>(db);
-    CUDA_TRY(cudaStreamWaitEvent(s, h.in_ev[0], 0));
-    CUDA_TRY(cudaStreamWaitEvent(s, h.in_ev[1], 0));
+    for (int j = 0; j < hp.front; ++j) CUDA_TRY(cudaStreamWaitEvent(s, ev_b[j], 0));
+    CUDA_TRY(cudaStreamWaitEvent(s, ev_a[0], 0));
     cudaMemsetAsync(ds, 0, sizeof(DevDecision), s);
     const double t = p.forced_scaled ? 1.0 : cfg.threshold_t;
-    const int64_t rows0 = std::min(m, rows_per);
+    const int64_t rows0 = std::min(m, hp.rows_per);
+    const int64_t bfront = k * std::min(n, j0_of(hp.front));  // the packed front parts
     if (p.stats) {
-        launch_stats1(fa, 2 * rows0 * k, fb, 2 * k * n, ds, s);
-        launch_stats2(fa, 2 * rows0 * k, fb, 2 * k * n, ds, t, cfg.target_max_exponent, 0, s);
+        launch_stats1(fa, 2 * rows0 * k, fb, 2 * bfront, ds, s);
+        launch_stats2(fa, 2 * rows0 * k, fb, 2 * bfront, ds, t, cfg.target_max_exponent, 0, s);
         launch_select(ds, cfg.threshold_t, cfg.target_max_exponent, p.forced_scaled ? 1 : 0, s);
         cudaMemcpyAsync(snap, ds, sizeof(DevDecision), cudaMemcpyDeviceToDevice, s);
     }
     TcecGemmArgs g = tc_gemm_args(h, p, ws, reinterpret_cast<float*>(dc), m, n, ds);
-    launch_prep_b(fb, k, n, p.kp, const_cast<void*>(g.b_hi), const_cast<void*>(g.b_lo), ds, p.kind, p.corrected, s);
-    for (int i = 0; i < nch; ++i) {
-        const int64_t r0 = i * rows_per, r1 = std::min(m, r0 + rows_per);
-        CUDA_TRY(cudaStreamWaitEvent(s, h.in_ev[1 + i], 0));
-        launch_prep_a(fa, r1 - r0, k, p.kp, const_cast<void*>(g.a_hi), const_cast<void*>(g.a_lo), ds, p.kind, p.corrected, s, r0);
-        const int rc = launch_gemm_rows(g, r0, r1, true, &hook, s);
-        if (rc) return rc;
+    g.ldc = 2 * n;
+    g.no_split = 1;
+    void* bhi = const_cast<void*>(g.b_hi);
+    void* blo = const_cast<void*>(g.b_lo);
+    auto prep_part = [&](int j) {
+        launch_prep_b(fb + 2 * k * j0_of(j), k, w_of(j), p.kp, bhi, blo, ds, p.kind, p.corrected, s,
+                      j0_of(j));
+    };
+    int unit = 0;
+    // GEMM of rows [r0, r1) x columns [c0, c0 + w), then its block of C goes back
+    auto block = [&](int64_t r0, int64_t r1, int64_t c0, int64_t w) -> int {
+        cudaStream_t gs = (unit++ & 1) ? h.gemm_stream2 : s;
+        if (gs != s) {
+            CUDA_TRY(cudaEventRecord(ev_sync, s));  // the preps this block reads
+            CUDA_TRY(cudaStreamWaitEvent(gs, ev_sync, 0));
+        }
+        TcecGemmArgs gb = g;
+        gb.m = r1 - r0;
+        gb.a_row_off = r0;
+        gb.n2 = 2 * w;
+        gb.b_row_off = 2 * c0;
+        gb.c = g.c + r0 * 2 * n + 2 * c0;
+        const int e = launch_tcec_gemm(gb, gs);
+        if (e) return cuda_error(cudaError_t(e), "tcec_gemm (host pipeline)");
+        cudaEvent_t ev = h.chunk_ev[unit % 8];
+        CUDA_TRY(cudaEventRecord(ev, gs));
+        CUDA_TRY(cudaStreamWaitEvent(h.copy_stream, ev, 0));
+        const size_t off = size_t(r0 * n + c0) * 8;
+        CUDA_TRY(cudaMemcpy2DAsync(c + off, size_t(n) * 8, dc + off, size_t(n) * 8, size_t(w) * 8,
+                                   size_t(r1 - r0), cudaMemcpyDeviceToHost, h.copy_stream));
+        return TCEC_OK;
+    };
+    for (int j = 0; j < hp.front; ++j) prep_part(j);
+    const int64_t wfront = std::min(n, j0_of(hp.front));  // front parts are contiguous columns
+    for (int i = 0; i < hp.nch; ++i) {
+        const int64_t r0 = i * hp.rows_per, r1 = std::min(m, r0 + hp.rows_per);
+        CUDA_TRY(cudaStreamWaitEvent(s, ev_a[i], 0));
+        launch_prep_a(fa, r1 - r0, k, p.kp, const_cast<void*>(g.a_hi), const_cast<void*>(g.a_lo), ds,
+                      p.kind, p.corrected, s, r0);
+        if (int rc = block(r0, r1, 0, wfront)) return rc;
+    }
+    for (int j = hp.front; j < hp.q; ++j) {
+        CUDA_TRY(cudaStreamWaitEvent(s, ev_b[j], 0));
+        prep_part(j);
+        for (int i = 0; i < hp.nch; ++i) {
+            const int64_t r0 = i * hp.rows_per, r1 = std::min(m, r0 + hp.rows_per);
+            if (int rc = block(r0, r1, j0_of(j), w_of(j))) return rc;
+        }
     }
     if (p.stats) {
         cudaMemsetAsync(dr, 0, sizeof(DevDecision), s);
@@ -725,8 +805,9 @@ static int host_pipeline(Handle& h, const uint8_t* a, const uint8_t* b, uint8_t*
         launch_stats2(fa, 2 * m * k, fb, 2 * k * n, dr, t, cfg.target_max_exponent, 0, s);
         launch_select(dr, cfg.threshold_t, cfg.target_max_exponent, p.forced_scaled ? 1 : 0, s);
     }
+    CUDA_TRY(cudaEventRecord(ev_sync, h.gemm_stream2));  // s covers the second GEMM stream
+    CUDA_TRY(cudaStreamWaitEvent(s, ev_sync, 0));
     CUDA_TRY(cudaGetLastError());
-    (void)c;
     return TCEC_OK;
 }
 
@@ -794,7 +875,11 @@ int tcec_dispatch_cgemm_host(tcec_handle h, const void* a, const void* b, void* 
     // tensor-core dispatches; TCEC_HOST_CHUNKS = 0 disables
     static const int pipe_chunks = [] {
         const char* e = std::getenv("TCEC_HOST_CHUNKS");
-        return e ? std::max(0, std::min(15, std::atoi(e))) : 12;
+        return e ? std::max(0, std::min(12, std::atoi(e))) : 12;
+    }();
+    static const int pipe_parts = [] {  // column parts of B (front half sent before A)
+        const char* e = std::getenv("TCEC_HOST_BPARTS");
+        return e ? std::max(1, std::min(4, std::atoi(e))) : 4;
     }();
     const bool pipelined = pipe_chunks > 1 && p.tier == kTierTc && m >= 8192 && n > 0 && k > 0 &&
                            !(h->prof && h->ev[0]) &&
@@ -802,10 +887,9 @@ int tcec_dispatch_cgemm_host(tcec_handle h, const void* a, const void* b, void* 
     DevDecision* d = pipelined ? h->decisions(3) : h->dec;
     if (!d) return set_error(TCEC_ERR_CUDA, "decision slots allocation failed");
     if (pipelined) {
-        hook.chunks = pipe_chunks;
+        const HostPipe hp = plan_host_pipe(m, n, pipe_chunks, pipe_parts);
         int rc = host_pipeline(*h, static_cast<const uint8_t*>(a), static_cast<const uint8_t*>(b),
-                               static_cast<uint8_t*>(c), m, n, k, *cfg, p, ws, da, db, dc, pipe_chunks,
-                               hook, d);
+                               static_cast<uint8_t*>(c), m, n, k, *cfg, p, ws, da, db, dc, hp, d);
         if (rc) return rc;
         CUDA_TRY(cudaMemcpyAsync(h->dec_host, d, 3 * sizeof(DevDecision), cudaMemcpyDeviceToHost,
                                  h->stream));
@@ -822,9 +906,10 @@ int tcec_dispatch_cgemm_host(tcec_handle h, const void* a, const void* b, void* 
             merged.scale_overflow = ds.scale_overflow;
             return finish_dispatch(p, merged, m, n, k, res);
         }
-        // the first chunk was not representative: plain path on the resident operands
+        // the first chunks were not representative: plain path on the resident A
+        // and a row-major copy of B (the staging holds it packed by column part)
         ctx.used = 0;
-        hook.chunks = 4;
+        CUDA_TRY(cudaMemcpyAsync(db, b, bb, cudaMemcpyHostToDevice, h->stream));
     } else {
         CUDA_TRY(cudaMemcpyAsync(da, a, ab, cudaMemcpyHostToDevice, h->stream));
         CUDA_TRY(cudaMemcpyAsync(db, b, bb, cudaMemcpyHostToDevice, h->stream));

@@ -434,7 +434,8 @@ constexpr int kPrepBKK = 64, kPrepBJ = 32, kPrepBStride = kPrepBKK + 2;
 __global__ void __launch_bounds__(256) prep_b_kernel(const float2* __restrict__ b, int64_t k,
                                                      int64_t n, int64_t kp, void* hi_v,
                                                      void* lo_v, const DevDecision* d,
-                                                     int kind_fixed, int corrected) {
+                                                     int kind_fixed, int corrected, int64_t jout0) {
+    // b is a k x n column block whose B' rows start at 2 jout0
     const PrepMode pm = prep_mode(d, kind_fixed, true);
     if (!pm.active) return;
     const double factor = ldexp(1.0, pm.scale);
@@ -465,7 +466,7 @@ __global__ void __launch_bounds__(256) prep_b_kernel(const float2* __restrict__ 
                 const float4 v = *reinterpret_cast<const float4*>(&tile[jj][2 * lane]);
                 float xv[4] = {v.x, v.y, v.z, v.w}, hv[4], lv[4];   // (re0, im0, re1, im1)
                 convert_n<4>(xv, pm, factor, fs, corrected, hv, lv, ovf, bad);
-                const int64_t r0 = (2 * j) * kp + col, r1 = (2 * j + 1) * kp + col;
+                const int64_t r0 = (2 * (jout0 + j)) * kp + col, r1 = r0 + kp;
                 if (pm.fmt == kFp16) {
                     __half* hp = static_cast<__half*>(hi_v);
                     __half2 q0[2] = {__floats2half2_rn(hv[0], -hv[1]), __floats2half2_rn(hv[2], -hv[3])};
@@ -1442,12 +1443,12 @@ void launch_prep_a(const float* a, int64_t m, int64_t k, int64_t kp, void* hi, v
 }
 
 void launch_prep_b(const float* b, int64_t k, int64_t n, int64_t kp, void* hi, void* lo,
-                   const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s) {
+                   const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s, int64_t jout0) {
     if (n <= 0 || kp <= 0) return;
     const int64_t tiles = ((n + kPrepBJ - 1) / kPrepBJ) * ((kp / 2 + kPrepBKK - 1) / kPrepBKK);
     const unsigned grid = unsigned(tiles < 148 * 8 ? tiles : 148 * 8);
     prep_b_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const float2*>(b), k, n, kp, hi, lo, d,
-                                       kind_fixed, corrected);
+                                       kind_fixed, corrected, jout0);
 }
 
 void launch_cgemm_fp32_ref(const float2* a, const float2* b, float2* c, int64_t m, int64_t n,

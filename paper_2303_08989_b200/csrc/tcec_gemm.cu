@@ -884,7 +884,8 @@ template <int FMT>
 __device__ __forceinline__ void wide_body(const WideMaps& mp, float* __restrict__ c, int m, int n2,
                                           int kp, const DevDecision* __restrict__ dec, int kind,
                                           int corrected, int flush_kblocks, int group_m,
-                                          int a_row_off, float* __restrict__ partial, int kb_per) {
+                                          int a_row_off, int ldc, float* __restrict__ partial,
+                                          int kb_per) {
     using T = Traits<FMT>;
     constexpr uint32_t kIdescHalf = umma_idesc<FMT, 2 * BM, 128>();
     constexpr uint32_t kIdescFull = umma_idesc<FMT, 2 * BM, kNpBN>();
@@ -1089,11 +1090,12 @@ __device__ __forceinline__ void wide_body(const WideMaps& mp, float* __restrict_
                                 acc[64 * hh + i + 3]);
         epi_bar_sync();
         const int ew = warp - 2;
-        const bool full_cols = n0 + kNpBN <= n2 && (n2 & 3) == 0;
+        const int ld = partial ? n2 : ldc;  // C may be a column block of a wider matrix
+        const bool full_cols = n0 + kNpBN <= n2 && (ld & 3) == 0;
         for (int r = ew; r < BM; r += kEpiWarps) {
             const int grow = m0 + r;
             if (grow >= m) break;
-            float* dst = c + size_t(grow) * n2 + n0;
+            float* dst = c + size_t(grow) * ld + n0;
             const float* srow = ctile + size_t(r) * kNpCStride;
             if (full_cols) {
                 reinterpret_cast<float4*>(dst)[lane] = reinterpret_cast<const float4*>(srow)[lane];
@@ -1118,13 +1120,13 @@ template <int FMT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
     tcec_gemm_wide_kernel(const __grid_constant__ WideMaps maps, float* __restrict__ c, int m,
                           int n2, int kp, const DevDecision* __restrict__ dec, int kind_fixed,
-                          int corrected, int flush_kblocks, int group_m, int a_row_off,
+                          int corrected, int flush_kblocks, int group_m, int a_row_off, int ldc,
                           float* __restrict__ partial, int kb_per) {
     const int kind = kind_fixed >= 0 ? kind_fixed : dec->kind;
     const bool mine = FMT == kTf32 ? kind == kKindTf32 : (kind == kKindFp16 || kind == kKindFp16Scaled);
     if (!mine) return;  // both CTAs of the pair read the same decision
-    wide_body<FMT>(maps, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off, partial,
-                   kb_per);
+    wide_body<FMT>(maps, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off, ldc,
+                   partial, kb_per);
 }
 
 // format decided on the device (AUTO): one launch that runs the selected
@@ -1134,14 +1136,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
                                const __grid_constant__ WideMaps maps32, float* __restrict__ c,
                                int m, int n2, int kp, const DevDecision* __restrict__ dec,
                                int corrected, int flush_kblocks, int group_m, int a_row_off,
-                               float* __restrict__ partial, int kb_per) {
+                               int ldc, float* __restrict__ partial, int kb_per) {
     const int kind = dec->kind;
     if (kind == kKindTf32)
         wide_body<kTf32>(maps32, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off,
-                         partial, kb_per);
+                         ldc, partial, kb_per);
     else if (kind == kKindFp16 || kind == kKindFp16Scaled)
         wide_body<kFp16>(maps16, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off,
-                         partial, kb_per);
+                         ldc, partial, kb_per);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -1179,8 +1181,13 @@ bool make_wide_maps(WideMaps* w, const TcecGemmArgs& g, int fmt) {
     const void* alo = g.corrected ? g.a_lo : g.a_hi;
     const void* blo = g.corrected ? g.b_lo : g.b_hi;
     const int64_t arows = g.a_rows > 0 ? g.a_rows : g.m;  // the whole A' (row chunks index into it)
+    // a column block of B: its n2 rows of B' start b_row_off rows in (the byte
+    // offset depends on the format, so each format's map gets its own base)
+    const size_t boff = size_t(g.b_row_off) * size_t(g.kp) * (fmt == kFp16 ? 2 : 4);
+    const void* bhi = static_cast<const uint8_t*>(g.b_hi) + boff;
+    blo = static_cast<const uint8_t*>(blo) + boff;
     return make_map(&w->ahi, g.a_hi, fmt, arows, g.kp, 128u) && make_map(&w->alo, alo, fmt, arows, g.kp, 128u) &&
-           make_map(&w->bhi, g.b_hi, fmt, g.n2, g.kp, 128u) && make_map(&w->blo, blo, fmt, g.n2, g.kp, 128u);
+           make_map(&w->bhi, bhi, fmt, g.n2, g.kp, 128u) && make_map(&w->blo, blo, fmt, g.n2, g.kp, 128u);
 }
 
 // rasterization group (M tiles per group) of the wide kernel; TCEC_GROUP_M
@@ -1232,7 +1239,7 @@ int launch_fmt(const TcecGemmArgs& g, cudaStream_t s) {
             tcec_gemm_wide_kernel<FMT><<<dim3(wide_tiles_grid(g), unsigned(g.partial ? g.splits : 1)),
                                          kThreadsGemm, kNpSmemBytes, s>>>(
                 w, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed, g.corrected, g.flush_kblocks,
-                wide_group_m(), int(g.a_row_off), g.partial, g.kb_per);
+                wide_group_m(), int(g.a_row_off), int(g.ldc > 0 ? g.ldc : g.n2), g.partial, g.kb_per);
         else
             tcec_gemm_widep_kernel<FMT><<<wide_grid(g), kThreadsGemm, kWideSmemBytes, s>>>(
                 w, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed, g.corrected, g.flush_kblocks);
@@ -1280,7 +1287,7 @@ int launch_wide_auto(const TcecGemmArgs& g, cudaStream_t s) {
         tcec_gemm_wide_auto_kernel<<<dim3(wide_tiles_grid(g), unsigned(g.partial ? g.splits : 1)),
                                      kThreadsGemm, kNpSmemBytes, s>>>(
             w16, w32, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.corrected, g.flush_kblocks,
-            wide_group_m(), int(g.a_row_off), g.partial, g.kb_per);
+            wide_group_m(), int(g.a_row_off), int(g.ldc > 0 ? g.ldc : g.n2), g.partial, g.kb_per);
     else
         tcec_gemm_widep_auto_kernel<<<wide_grid(g), kThreadsGemm, kWideSmemBytes, s>>>(
             w16, w32, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.corrected, g.flush_kblocks);
@@ -1309,6 +1316,7 @@ int launch_tcec_gemm(const TcecGemmArgs& g_in, cudaStream_t s) {
     g.partial = nullptr;
     g.splits = 1;
     g.kb_per = 0;
+    if (g.ldc > 0 && g.ldc != g.n2) g.no_split = 1;  // partials and their reduction assume ldc = n2
     if (!g.no_split && (g.pair == kVariantSingle || g.pair == kVariantWide)) {
         // few tiles and a long K (e.g. (512, 512, 2^19) contraction steps):
         // split K so the grid covers the SMs several times

@@ -30,6 +30,7 @@ struct tcec_handle_s {
     cudaStream_t copy_stream = nullptr;  // D2H of finished row chunks (host-buffer API)
     cudaEvent_t chunk_ev[8] = {};
     cudaStream_t in_stream = nullptr;  // H2D of operand row chunks (host-buffer pipeline)
+    cudaStream_t gemm_stream2 = nullptr;  // second GEMM stream of the host-buffer pipeline
     cudaEvent_t in_ev[17] = {};
     // stage profiling (tcec_profile_*): CUDA events around the stages of a
     // dispatched CGEMM, accumulated after each synchronous dispatch

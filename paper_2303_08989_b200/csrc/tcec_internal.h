@@ -60,7 +60,8 @@ void launch_prep_a(const float* a, int64_t m, int64_t k, int64_t kp, void* hi, v
 // B (k x n complex) -> B'^T = 2n x Kp real, K-major, with the complex block
 // expansion [[Br, Bi], [-Bi, Br]] so one real GEMM yields interleaved C.
 void launch_prep_b(const float* b, int64_t k, int64_t n, int64_t kp, void* hi, void* lo,
-                   const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s);
+                   const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s,
+                   int64_t jout0 = 0);  // b = a k x n column block, B' rows from 2 jout0
 
 // -------------------------------------------------------------- SIMT GEMM
 // FP32_REF complex GEMM, bit-identical to the reference schedule
@@ -94,6 +95,8 @@ struct TcecGemmArgs {
     float* partial;                       // split-K partials (set by launch_tcec_gemm)
     int splits, kb_per;                   // split count, 64-element k-blocks per split
     int no_split;                         // 1: never split K (row-chunked launches must match the one-launch bits)
+    int64_t ldc;                          // row stride of C in floats, 0 = n2 (wide kernel: column blocks of C)
+    int64_t b_row_off;                    // first B' row of this launch (wide kernel: column blocks of B)
 };
 // tcgen05 kernel variants (tcec_set_gemm_variant): auto picks wide when its
 // 256 x 256 pair tiles fill the SMs, else single

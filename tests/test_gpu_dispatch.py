@@ -157,32 +157,37 @@ def test_host_buffer_row_chunks_match_the_device_path(handle, dev):
     assert np.array_equal(c_host.view(np.uint32), c_dev.cpu().numpy().view(np.uint32))
 
 
-@pytest.mark.parametrize("case", ["uniform", "late_outlier", "late_tiny", "first_outlier",
+@pytest.mark.parametrize("shape", [(16384, 768, 384), (8448, 2304, 160)])
+@pytest.mark.parametrize("case", ["uniform", "late_outlier", "late_tiny", "first_outlier", "late_b_outlier",
                                   "FP16TCEC", "TF32TCEC", "FP16TCEC_SCALED", "fp16_overflow"])
-def test_host_pipeline_matches_the_device_path(handle, dev, case):
+def test_host_pipeline_matches_the_device_path(handle, dev, case, shape):
     """Large host-buffer dispatches copy A in row chunks and start each chunk's
     GEMM under a decision taken from B and the first chunk; the exact decision
     follows, and a disagreement reruns the plain path.  Either way C and the
     decision record are bit-identical to the device-buffer dispatch -- including
     inputs whose later rows change the decision (late outlier / late tiny rows)."""
     g = np.random.default_rng(21)
-    m, n, k = 16384, 768, 384
+    m, n, k = shape  # n = 2304: B in four column parts (640, 640, 640, 384), two sent after A
     a = (g.random((m, k, 2), dtype=np.float32) * 2 - 1).view(np.complex64)[..., 0].copy()
     b = (g.random((k, n, 2), dtype=np.float32) * 2 - 1).view(np.complex64)[..., 0].copy()
-    pol = SelectionPolicy(size_auto=256, size_tf32=128)
+    pol = SelectionPolicy(size_auto=128, size_tf32=64)
     if case == "late_outlier":
         a[m - 5, 7] = 3.0e20 + 1.0e20j
     elif case == "late_tiny":
         a[m // 2:] *= np.float32(2.0 ** -30)
     elif case == "first_outlier":
         a[3, 2] = 1.0e6
+    elif case == "late_b_outlier":
+        b[k // 2, n - 3] = 2.0e9 - 1.0e9j
     elif case == "fp16_overflow":
-        a[9000, 3] = 9.0e4
+        a[m - 100, 3] = 9.0e4
         pol = make_config(force="FP16TCEC")
     elif case in ("FP16TCEC", "TF32TCEC", "FP16TCEC_SCALED"):
         pol = make_config(force=case)
     c_host, res_h = handle.dispatch_cgemm_host(a, b, pol)
     c_dev, res_d = handle.dispatch_cgemm(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev), pol)
+    if case in ("uniform", "late_outlier", "late_tiny", "late_b_outlier"):
+        assert res_d.has_stats  # the AUTO tier: decided from statistics on the device
     assert res_h.line == res_d.line
     assert res_h.overflow == res_d.overflow
     assert np.array_equal(c_host.view(np.uint32), c_dev.cpu().numpy().view(np.uint32))
