@@ -248,6 +248,7 @@ def run_ours(args):
     e1.synchronize()
     e2e_ms = max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3) / args.steps
     e2e_ms = max_over_ranks(e2e_ms, world)
+    pipe_runs, pipe_reruns = h.host_pipeline_stats()
 
     # ---- fidelity: sampled rows vs complex128, and the bit-exact FP32 tier on the same rows
     rows = torch.from_numpy(np.random.default_rng(3).choice(n, 16, replace=False)).to(dev)
@@ -326,7 +327,11 @@ def run_ours(args):
                          "ratio_vs_fp32": round(err / err32, 3) if err32 else None,
                          "sample": "16 random rows vs complex128"},
             "e2e": {"value": round(world * flops / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
-                    "h2d_bytes_per_step": 2 * n * n * 8, "d2h_bytes_per_step": n * n * 8},
+                    "h2d_bytes_per_step": 2 * n * n * 8, "d2h_bytes_per_step": n * n * 8,
+                    "pipeline": {"runs": pipe_runs, "reruns": pipe_reruns,
+                                 "note": "H2D of B column parts / A row chunks overlapped with the GEMM "
+                                         "blocks under a decision from the first parts, checked against "
+                                         "the exact one (reruns = recomputed on disagreement)"}},
             # per AUTO dispatch: stats1, stats2, select, prep_a, prep_b and ONE
             # tcgen05 GEMM (the wide kernel branches on the device decision),
             # plus a cudaMemsetAsync of the decision slot

@@ -82,6 +82,11 @@ int tcec_set_executor(tcec_handle h, int policy);
  * milliseconds of the three stages and the number of dispatches; enable resets. */
 int tcec_profile_enable(tcec_handle h, int on);
 int tcec_profile_read(tcec_handle h, double* stage_ms, int64_t* count);
+/* host-buffer pipeline counters (tcec_dispatch_cgemm_host on large tensor-core
+ * dispatches): runs = dispatches that overlapped the operand copies with the
+ * GEMM under a decision taken from the first operand parts; reruns = those
+ * whose exact decision differed and were recomputed on the plain path. */
+int tcec_host_pipeline_stats(tcec_handle h, int64_t* runs, int64_t* reruns);
 
 /* ------------------------------------------------ format emulation (device)
  * KernelTable entries, kernels.hpp:20-63; bit-identical to the reference

@@ -147,6 +147,13 @@ class Handle:
         check(self.lib.tcec_profile_read(self.h, arr, C.byref(cnt)))
         return {"stats": arr[0], "prep": arr[1], "gemm": arr[2]}, cnt.value
 
+    def host_pipeline_stats(self):
+        """-> (runs, reruns) of the pipelined host-buffer dispatch (reruns: the
+        decision taken from the first operand parts differed from the exact one)."""
+        runs, reruns = C.c_int64(0), C.c_int64(0)
+        check(self.lib.tcec_host_pipeline_stats(self.h, C.byref(runs), C.byref(reruns)))
+        return runs.value, reruns.value
+
     # ------------------------------------------------------ KernelTable level
     def _out_like(self, x):
         return _torch().empty_like(x)

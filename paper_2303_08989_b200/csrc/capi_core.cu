@@ -455,6 +455,13 @@ int tcec_profile_enable(tcec_handle h, int on) {
     return TCEC_OK;
 }
 
+int tcec_host_pipeline_stats(tcec_handle h, int64_t* runs, int64_t* reruns) {
+    CHECK_HANDLE(h);
+    if (runs) *runs = h->pipe_runs;
+    if (reruns) *reruns = h->pipe_reruns;
+    return TCEC_OK;
+}
+
 int tcec_profile_read(tcec_handle h, double* stage_ms, int64_t* count) {
     CHECK_HANDLE(h);
     for (int i = 0; i < 3; ++i) stage_ms[i] = h->prof_ms[i];
@@ -688,7 +695,7 @@ static HostPipe plan_host_pipe(int64_t m, int64_t n, int chunks, int parts) {
     HostPipe hp;
     hp.rows_per = round_up((m + chunks - 1) / chunks, 256);
     hp.nch = int((m + hp.rows_per - 1) / hp.rows_per);
-    hp.q = n >= 512 * parts ? parts : 1;
+    hp.q = int(std::max<int64_t>(1, std::min<int64_t>(parts, n / 256)));  // parts of >= 256 columns
     hp.wq = round_up((n + hp.q - 1) / hp.q, 128);  // even column offsets keep C blocks 16-B aligned
     hp.q = int((n + hp.wq - 1) / hp.wq);
     hp.front = std::max(1, hp.q / 2);
@@ -713,7 +720,7 @@ static int host_pipeline(Handle& h, const uint8_t* a, const uint8_t* b, uint8_t*
     auto w_of = [&](int j) { return std::min(hp.wq, n - j0_of(j)); };
     cudaEvent_t* ev_b = h.in_ev;              // B column parts
     cudaEvent_t* ev_a = h.in_ev + hp.q;       // A row chunks
-    cudaEvent_t ev_sync = h.in_ev[16];        // stream-to-stream ordering
+    cudaEvent_t ev_sync = h.in_ev[24];        // stream-to-stream ordering
     // the staging buffers may still be read by earlier work on the stream
     CUDA_TRY(cudaEventRecord(ev_sync, s));
     CUDA_TRY(cudaStreamWaitEvent(h.in_stream, ev_sync, 0));
@@ -875,11 +882,11 @@ int tcec_dispatch_cgemm_host(tcec_handle h, const void* a, const void* b, void* 
     // tensor-core dispatches; TCEC_HOST_CHUNKS = 0 disables
     static const int pipe_chunks = [] {
         const char* e = std::getenv("TCEC_HOST_CHUNKS");
-        return e ? std::max(0, std::min(12, std::atoi(e))) : 12;
+        return e ? std::max(0, std::min(16, std::atoi(e))) : 12;
     }();
     static const int pipe_parts = [] {  // column parts of B (front half sent before A)
         const char* e = std::getenv("TCEC_HOST_BPARTS");
-        return e ? std::max(1, std::min(4, std::atoi(e))) : 4;
+        return e ? std::max(1, std::min(8, std::atoi(e))) : 8;
     }();
     const bool pipelined = pipe_chunks > 1 && p.tier == kTierTc && m >= 8192 && n > 0 && k > 0 &&
                            !(h->prof && h->ev[0]) &&
@@ -891,6 +898,7 @@ int tcec_dispatch_cgemm_host(tcec_handle h, const void* a, const void* b, void* 
         int rc = host_pipeline(*h, static_cast<const uint8_t*>(a), static_cast<const uint8_t*>(b),
                                static_cast<uint8_t*>(c), m, n, k, *cfg, p, ws, da, db, dc, hp, d);
         if (rc) return rc;
+        ++h->pipe_runs;
         CUDA_TRY(cudaMemcpyAsync(h->dec_host, d, 3 * sizeof(DevDecision), cudaMemcpyDeviceToHost,
                                  h->stream));
         CUDA_TRY(cudaStreamSynchronize(h->stream));
@@ -909,6 +917,7 @@ int tcec_dispatch_cgemm_host(tcec_handle h, const void* a, const void* b, void* 
         // the first chunks were not representative: plain path on the resident A
         // and a row-major copy of B (the staging holds it packed by column part)
         ctx.used = 0;
+        ++h->pipe_reruns;
         CUDA_TRY(cudaMemcpyAsync(db, b, bb, cudaMemcpyHostToDevice, h->stream));
     } else {
         CUDA_TRY(cudaMemcpyAsync(da, a, ab, cudaMemcpyHostToDevice, h->stream));

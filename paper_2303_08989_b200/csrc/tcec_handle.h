@@ -31,7 +31,8 @@ struct tcec_handle_s {
     cudaEvent_t chunk_ev[8] = {};
     cudaStream_t in_stream = nullptr;  // H2D of operand row chunks (host-buffer pipeline)
     cudaStream_t gemm_stream2 = nullptr;  // second GEMM stream of the host-buffer pipeline
-    cudaEvent_t in_ev[17] = {};
+    int64_t pipe_runs = 0, pipe_reruns = 0;  // tcec_host_pipeline_stats
+    cudaEvent_t in_ev[25] = {};  // B parts (<= 8), A chunks (<= 16), ordering
     // stage profiling (tcec_profile_*): CUDA events around the stages of a
     // dispatched CGEMM, accumulated after each synchronous dispatch
     bool prof = false;

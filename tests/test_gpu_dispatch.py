@@ -157,7 +157,7 @@ def test_host_buffer_row_chunks_match_the_device_path(handle, dev):
     assert np.array_equal(c_host.view(np.uint32), c_dev.cpu().numpy().view(np.uint32))
 
 
-@pytest.mark.parametrize("shape", [(16384, 768, 384), (8448, 2304, 160)])
+@pytest.mark.parametrize("shape", [(16384, 768, 384), (8448, 2304, 640)])
 @pytest.mark.parametrize("case", ["uniform", "late_outlier", "late_tiny", "first_outlier", "late_b_outlier",
                                   "FP16TCEC", "TF32TCEC", "FP16TCEC_SCALED", "fp16_overflow"])
 def test_host_pipeline_matches_the_device_path(handle, dev, case, shape):
@@ -167,7 +167,7 @@ def test_host_pipeline_matches_the_device_path(handle, dev, case, shape):
     decision record are bit-identical to the device-buffer dispatch -- including
     inputs whose later rows change the decision (late outlier / late tiny rows)."""
     g = np.random.default_rng(21)
-    m, n, k = shape  # n = 2304: B in four column parts (640, 640, 640, 384), two sent after A
+    m, n, k = shape  # n = 2304: B in six column parts of 384, three sent after A; n = 768: three of 256
     a = (g.random((m, k, 2), dtype=np.float32) * 2 - 1).view(np.complex64)[..., 0].copy()
     b = (g.random((k, n, 2), dtype=np.float32) * 2 - 1).view(np.complex64)[..., 0].copy()
     pol = SelectionPolicy(size_auto=128, size_tf32=64)
@@ -184,7 +184,12 @@ def test_host_pipeline_matches_the_device_path(handle, dev, case, shape):
         pol = make_config(force="FP16TCEC")
     elif case in ("FP16TCEC", "TF32TCEC", "FP16TCEC_SCALED"):
         pol = make_config(force=case)
+    runs0, reruns0 = handle.host_pipeline_stats()
     c_host, res_h = handle.dispatch_cgemm_host(a, b, pol)
+    runs1, reruns1 = handle.host_pipeline_stats()
+    assert runs1 == runs0 + 1  # m >= 8192 on the tensor-core tier: pipelined
+    if case in ("late_outlier", "late_b_outlier"):
+        assert reruns1 == reruns0 + 1  # the first parts could not predict the scale
     c_dev, res_d = handle.dispatch_cgemm(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev), pol)
     if case in ("uniform", "late_outlier", "late_tiny", "late_b_outlier"):
         assert res_d.has_stats  # the AUTO tier: decided from statistics on the device
