@@ -120,6 +120,22 @@ def test_permute_high_rank_dim2(handle, dev):
         assert torch.equal(handle.permute(t, axis), t.permute(*axis).contiguous())
 
 
+@pytest.mark.parametrize("rank,axis", [
+    (22, [20, 21, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19]),
+    (22, [9, 3, 14, 0, 1, 2, 4, 5, 6, 7, 8, 10, 11, 12, 13, 15, 16, 17, 18, 19, 20, 21]),
+    (20, [14, 2, 0, 1, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 15, 16, 17, 18, 19]),
+    (12, [11, 10, 9, 8, 7, 0, 1, 2, 3, 4, 5, 6]),
+    (24, [1, 12, 5, 23, 18, 14, 0, 2, 3, 4, 6, 7, 8, 9, 10, 11, 13, 15, 16, 17, 19, 20, 21, 22]),
+    (21, [0, 1, 2, 3, 4, 5, 6, 8, 9, 10, 11, 12, 13, 14, 15, 7, 16, 17, 18, 19, 20]),
+])
+def test_permute_run_copy(handle, dev, rank, axis):
+    """Permutations that keep >= 32 innermost elements in place (a few outer
+    axes moved -- the common TTGT case of sliced circuit intermediates) take
+    the run-copy kernel; bit-exact, including runs of exactly 32."""
+    t = torch.randn(*([2] * rank), dtype=torch.complex64, device=dev)
+    assert torch.equal(handle.permute(t, axis), t.permute(*axis).contiguous())
+
+
 def test_permute_errors(handle, dev):
     t = torch.zeros(2, 3, 4, dtype=torch.complex64, device=dev)
     with pytest.raises(InvalidPermutation):
