@@ -1063,10 +1063,11 @@ void launch_skinny_mx(const float2* a, const float2* b, float2* c, int64_t m, in
             if (k >= 8) {
                 constexpr int SW = (MX + 1) > 9 ? (MX + 1) : 9;
                 constexpr int stage_bytes = 8 * 32 * SW * int(sizeof(float2));
-                static const bool attr = cudaFuncSetAttribute(cgemm_skinny_row_kernel<F64, MX, true>,
-                                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                              stage_bytes) == cudaSuccess;
-                if (attr) {
+                static std::atomic<uint64_t> attr{0};
+                if (ensure_smem_attr(attr, [] {
+                        return cudaFuncSetAttribute(cgemm_skinny_row_kernel<F64, MX, true>,
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes);
+                    }) == cudaSuccess) {
                     cgemm_skinny_row_kernel<F64, MX, true><<<unsigned((m + 255) / 256), 256, stage_bytes, s>>>(
                         a, b + j0, c + j0, m, cols, int(k), n);
                     continue;
@@ -1643,7 +1644,7 @@ void launch_permute(const float2* src, float2* dst, int rank, const int64_t* old
     }
     // innermost output axis not contiguous in the source: shared-memory tiles
     if (r >= 2 && desc.in_stride[r - 1] != 1 && total >= 4096) {
-        static TiledPermDesc td;  // host-side scratch (kernel arguments are copied at launch)
+        TiledPermDesc td{};  // per call: the planner is reentrant (handles may run on several host threads)
         if (plan_tiled(r, desc.out_dim, desc.in_stride, &td)) {
             const int64_t g = td.batches < 148 * 16 ? td.batches : 148 * 16;
             permute_tiled_kernel<<<unsigned(g), 256, 0, s>>>(src, dst, td);

@@ -496,12 +496,11 @@ int launch_hybrid_trees(const HybridProgram& p, const float2* node_dev, float2* 
     if (!p.ok) return TCEC_OK;
     const int n_trees = int(p.trees.size());
     const size_t smem = size_t(kHybWarpsPerBlock) * size_t(p.arena_elems) * 8;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(tree_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(kHybWarpsPerBlock * kHybArenaBytes));
-        attr = true;
-    }
+    static std::atomic<uint64_t> attr{0};
+    ensure_smem_attr(attr, [] {
+        return cudaFuncSetAttribute(tree_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(kHybWarpsPerBlock * kHybArenaBytes));
+    });
     const unsigned grid = unsigned((n_trees + kHybWarpsPerBlock - 1) / kHybWarpsPerBlock);
     tree_fold_kernel<<<grid, 32 * kHybWarpsPerBlock, smem, s>>>(p.d_steps, p.d_tables, p.d_trees, n_trees,
                                                                 node_dev, p.arena_elems, out);
@@ -533,12 +532,11 @@ int launch_small_program(const SmallProgram& p, const float2* node_dev, int n_ru
     int wpc = int(std::min<int64_t>(8, std::max<int64_t>(1, kMaxArenaBytes / std::max<int64_t>(arena_bytes, 1))));
     wpc = std::min(wpc, std::max(1, n_runs));
     const size_t smem = size_t(wpc) * size_t(arena_bytes);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(small_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(kMaxArenaBytes + 8 * 1024));
-        attr = true;
-    }
+    static std::atomic<uint64_t> attr{0};
+    ensure_smem_attr(attr, [] {
+        return cudaFuncSetAttribute(small_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(kMaxArenaBytes + 8 * 1024));
+    });
     const unsigned grid = unsigned((n_runs + wpc - 1) / wpc);
     small_fold_kernel<<<grid, 32 * wpc, smem, s>>>(
         p.d_steps, int(p.steps.size()), p.d_tables, node_dev, n_runs, p.arena_elems, p.d_var,

@@ -9,6 +9,23 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per device for a group
+// of kernels (the attribute is per device context); `done` holds one bit per
+// device, so concurrent callers and several devices in one process are safe
+// (setting it twice is harmless).
+template <typename F>
+inline cudaError_t ensure_smem_attr(std::atomic<uint64_t>& done, F&& set_all) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = uint64_t(1) << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    const cudaError_t e = set_all();
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+}
+
 #define TCEC_DEV __device__ __forceinline__
 
 namespace tcec {

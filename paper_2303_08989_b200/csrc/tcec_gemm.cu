@@ -1215,23 +1215,23 @@ unsigned wide_grid(const TcecGemmArgs& g) {
 
 template <int FMT>
 int launch_fmt(const TcecGemmArgs& g, cudaStream_t s) {
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::atomic<uint64_t> attr_set{0};
+    const cudaError_t ea = ensure_smem_attr(attr_set, [] {
         cudaError_t e = cudaFuncSetAttribute(tcec_gemm_kernel<FMT>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              int(kSmemBytes));
-        if (e != cudaSuccess) return int(e);
-        e = cudaFuncSetAttribute(tcec_gemm_pair_kernel<FMT>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPairSmemBytes));
-        if (e != cudaSuccess) return int(e);
-        e = cudaFuncSetAttribute(tcec_gemm_wide_kernel<FMT>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNpSmemBytes));
-        if (e != cudaSuccess) return int(e);
-        e = cudaFuncSetAttribute(tcec_gemm_widep_kernel<FMT>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(kWideSmemBytes));
-        if (e != cudaSuccess) return int(e);
-        attr_set = true;
-    }
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(tcec_gemm_pair_kernel<FMT>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPairSmemBytes));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(tcec_gemm_wide_kernel<FMT>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNpSmemBytes));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(tcec_gemm_widep_kernel<FMT>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(kWideSmemBytes));
+        return e;
+    });
+    if (ea != cudaSuccess) return int(ea);
     if (g.pair == kVariantWide || g.pair == kVariantWidePersistent) {
         WideMaps w;
         if (!make_wide_maps(&w, g, FMT)) return int(cudaErrorInvalidValue);
@@ -1270,16 +1270,16 @@ int launch_fmt(const TcecGemmArgs& g, cudaStream_t s) {
 
 // format decided on the device: one wide launch that runs the selected format
 int launch_wide_auto(const TcecGemmArgs& g, cudaStream_t s) {
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::atomic<uint64_t> attr_set{0};
+    const cudaError_t ea = ensure_smem_attr(attr_set, [] {
         cudaError_t e = cudaFuncSetAttribute(tcec_gemm_wide_auto_kernel,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNpSmemBytes));
-        if (e != cudaSuccess) return int(e);
-        e = cudaFuncSetAttribute(tcec_gemm_widep_auto_kernel,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(kWideSmemBytes));
-        if (e != cudaSuccess) return int(e);
-        attr_set = true;
-    }
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(tcec_gemm_widep_auto_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(kWideSmemBytes));
+        return e;
+    });
+    if (ea != cudaSuccess) return int(ea);
     WideMaps w16, w32;
     if (!make_wide_maps(&w16, g, kFp16) || !make_wide_maps(&w32, g, kTf32))
         return int(cudaErrorInvalidValue);
