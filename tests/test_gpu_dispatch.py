@@ -212,3 +212,45 @@ def test_empty_and_zero_operands(handle, dev):
     for mode in ("FP32_REF", "FP16TCEC", "TF32TCEC"):
         c, _ = handle.cgemm(a, b, mode)
         assert c.shape == (5, 7) and torch.count_nonzero(c) == 0
+
+
+def test_handles_on_concurrent_host_threads(dev):
+    """Reentrancy (SURVEY.md 8(b) threading: pure and reentrant): one handle per
+    host thread, dispatches and permutes issued concurrently (ctypes releases
+    the GIL) give the bits of the same calls made serially."""
+    import threading
+    from paper_2303_08989_b200 import Handle
+    g = np.random.default_rng(33)
+    jobs = []
+    for m, n, k in [(1024, 768, 512), (300, 200, 9000), (4096, 16, 8), (2048, 2048, 64)]:
+        a = torch.from_numpy((g.random((m, k, 2), dtype=np.float32) * 2 - 1).view(np.complex64)[..., 0].copy()).to(dev)
+        b = torch.from_numpy((g.random((k, n, 2), dtype=np.float32) * 2 - 1).view(np.complex64)[..., 0].copy()).to(dev)
+        jobs.append((a, b))
+    t = torch.randn(*([2] * 20), dtype=torch.complex64, device=dev)
+    axes = [[int(v) for v in g.permutation(20)] for _ in range(4)]
+    pol = SelectionPolicy(size_auto=64, size_tf32=32)
+
+    def work(h, out):
+        for a, b in jobs:
+            c, res = h.dispatch_cgemm(a, b, pol)
+            out.append((c.cpu(), res.line))
+        for ax in axes:
+            out.append((h.permute(t, ax).cpu(), ""))
+        torch.cuda.synchronize()
+
+    handles = [Handle(0) for _ in range(3)]
+    serial = []
+    work(handles[0], serial)
+    outs = [[] for _ in handles]
+    threads = [threading.Thread(target=work, args=(h, o)) for h, o in zip(handles, outs)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    for o in outs:
+        assert len(o) == len(serial)
+        for (x, lx), (y, ly) in zip(o, serial):
+            assert lx == ly
+            assert torch.equal(x.view(torch.float32), y.view(torch.float32))
+    for h in handles:
+        h.close()
