@@ -82,6 +82,10 @@ int tcec_set_executor(tcec_handle h, int policy);
  * milliseconds of the three stages and the number of dispatches; enable resets. */
 int tcec_profile_enable(tcec_handle h, int on);
 int tcec_profile_read(tcec_handle h, double* stage_ms, int64_t* count);
+/* the same for contraction batches (tcec_contract_selector_batch / node_batch):
+ * summed device milliseconds from the end of the call's uploads to the start of
+ * its download (inputs resident in HBM), and the number of batches. */
+int tcec_profile_read_batches(tcec_handle h, double* ms, int64_t* count);
 /* host-buffer pipeline counters (tcec_dispatch_cgemm_host on large tensor-core
  * dispatches): runs = dispatches that overlapped the operand copies with the
  * GEMM under a decision taken from the first operand parts; reruns = those

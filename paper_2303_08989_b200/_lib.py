@@ -127,6 +127,7 @@ def load() -> C.CDLL:
         "tcec_profile_enable": ([vp, i32], i32),
         "tcec_profile_read": ([vp, C.POINTER(dbl), C.POINTER(i64)], i32),
         "tcec_host_pipeline_stats": ([vp, C.POINTER(i64), C.POINTER(i64)], i32),
+        "tcec_profile_read_batches": ([vp, C.POINTER(dbl), C.POINTER(i64)], i32),
         "tcec_quantize_buf": ([vp, vp, vp, i64, i32, i32, ip], i32),
         "tcec_split_buf": ([vp, vp, vp, vp, i64, i32, ip], i32),
         "tcec_scale_buf": ([vp, vp, vp, i64, i32], i32),

@@ -147,6 +147,13 @@ class Handle:
         check(self.lib.tcec_profile_read(self.h, arr, C.byref(cnt)))
         return {"stats": arr[0], "prep": arr[1], "gemm": arr[2]}, cnt.value
 
+    def profile_read_batches(self):
+        """-> (device ms summed over contraction batches from the end of their
+        uploads to the start of their download, number of batches)"""
+        ms, cnt = C.c_double(0.0), C.c_int64(0)
+        check(self.lib.tcec_profile_read_batches(self.h, C.byref(ms), C.byref(cnt)))
+        return ms.value, cnt.value
+
     def host_pipeline_stats(self):
         """-> (runs, reruns) of the pipelined host-buffer dispatch (reruns: the
         decision taken from the first operand parts differed from the exact one)."""

@@ -329,6 +329,8 @@ tcec_handle_s::~tcec_handle_s() {
         if (e) cudaEventDestroy(e);
     for (auto& e : ev)
         if (e) cudaEventDestroy(e);
+    for (auto& e : batch_ev)
+        if (e) cudaEventDestroy(e);
 }
 
 
@@ -449,9 +451,20 @@ int tcec_profile_enable(tcec_handle h, int on) {
     CHECK_HANDLE(h);
     if (on && !h->ev[0])
         for (auto& e : h->ev) CUDA_TRY(cudaEventCreate(&e));
+    if (on && !h->batch_ev[0])
+        for (auto& e : h->batch_ev) CUDA_TRY(cudaEventCreate(&e));
     h->prof = on != 0;
     h->prof_ms[0] = h->prof_ms[1] = h->prof_ms[2] = 0.0;
     h->prof_count = 0;
+    h->batch_ms = 0.0;
+    h->batch_count = 0;
+    return TCEC_OK;
+}
+
+int tcec_profile_read_batches(tcec_handle h, double* ms, int64_t* count) {
+    CHECK_HANDLE(h);
+    if (ms) *ms = h->batch_ms;
+    if (count) *count = h->batch_count;
     return TCEC_OK;
 }
 

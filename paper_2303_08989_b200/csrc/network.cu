@@ -705,6 +705,15 @@ int tcec_contract_network(tcec_network net, const int* steps, int n_steps,
     return TCEC_OK;
 }
 
+// tcec_profile_read_batches: device time between a batch's uploads and its download
+static void account_batch(Handle& h) {
+    float ms = 0.0f;
+    if (cudaEventElapsedTime(&ms, h.batch_ev[0], h.batch_ev[1]) == cudaSuccess) {
+        h.batch_ms += ms;
+        ++h.batch_count;
+    }
+}
+
 int tcec_contract_selector_batch(tcec_network net, const int* steps, int n_steps,
                                  const tcec_dispatch_config_t* cfg, int n_sel, const int* sel_nodes,
                                  int n_strings, const uint8_t* bits, void* out_host) {
@@ -740,6 +749,8 @@ int tcec_contract_selector_batch(tcec_network net, const int* steps, int n_steps
     if (e != cudaSuccess) return cuda_error(e, "batch buffers");
     cudaMemcpyAsync(d_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice, s);
     if (nbits) cudaMemcpyAsync(d_bits, bits, nbits, cudaMemcpyHostToDevice, s);
+    const bool prof = h.prof && h.batch_ev[0];
+    if (prof) cudaEventRecord(h.batch_ev[0], s);
     const std::vector<int> sel_vec(sel_nodes, sel_nodes + n_sel);
     const SmallProgram* fused = small_program(*net, steps, n_steps, *cfg, plan, sel_vec, &rc);
     if (rc) return rc;
@@ -785,6 +796,7 @@ int tcec_contract_selector_batch(tcec_network net, const int* steps, int n_steps
             cudaMemcpyAsync(d_out + i, net->result_dev, 8, cudaMemcpyDeviceToDevice, s);
         }
     }
+    if (prof) cudaEventRecord(h.batch_ev[1], s);
     e = cudaMemcpyAsync(out_host, d_out, size_t(n_strings) * 8, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return cuda_error(e, "batch download");
     cudaFreeAsync(d_off, s);
@@ -792,6 +804,7 @@ int tcec_contract_selector_batch(tcec_network net, const int* steps, int n_steps
     cudaFreeAsync(d_out, s);
     e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_error(e, "selector batch");
+    if (prof) account_batch(h);
     // the host copy of the selector slots no longer matches the device
     net->dirty = true;
     return TCEC_OK;
@@ -838,6 +851,8 @@ int tcec_contract_node_batch(tcec_network net, const int* steps, int n_steps,
     if (!seg.empty()) cudaMemcpyAsync(d_seg, seg.data(), seg.size() * 8, cudaMemcpyHostToDevice, s);
     if (per_run * n_runs > 0)
         cudaMemcpyAsync(d_var, var_data, size_t(per_run * n_runs) * 8, cudaMemcpyHostToDevice, s);
+    const bool prof = h.prof && h.batch_ev[0];
+    if (prof) cudaEventRecord(h.batch_ev[0], s);
     const std::vector<int> var_vec(var_nodes, var_nodes + n_var);
     const SmallProgram* fused = small_program(*net, steps, n_steps, *cfg, plan, var_vec, &rc);
     if (rc) return rc;
@@ -884,6 +899,7 @@ int tcec_contract_node_batch(tcec_network net, const int* steps, int n_steps,
             cudaMemcpyAsync(d_out + r, net->result_dev, 8, cudaMemcpyDeviceToDevice, s);
         }
     }
+    if (prof) cudaEventRecord(h.batch_ev[1], s);
     e = cudaMemcpyAsync(out_host, d_out, size_t(n_runs) * 8, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return cuda_error(e, "batch download");
     cudaFreeAsync(d_seg, s);
@@ -891,6 +907,7 @@ int tcec_contract_node_batch(tcec_network net, const int* steps, int n_steps,
     cudaFreeAsync(d_out, s);
     e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_error(e, "node batch");
+    if (prof) account_batch(h);
     net->dirty = true;  // device node data now holds the last run
     return TCEC_OK;
 }

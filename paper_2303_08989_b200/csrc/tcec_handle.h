@@ -39,6 +39,11 @@ struct tcec_handle_s {
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     double prof_ms[3] = {0.0, 0.0, 0.0};  // statistics+selection, operand prep, GEMM
     int64_t prof_count = 0;
+    // contraction batches (selector / node batch): device time from the end of
+    // the uploads to the start of the download, while profiling is enabled
+    cudaEvent_t batch_ev[2] = {nullptr, nullptr};
+    double batch_ms = 0.0;
+    int64_t batch_count = 0;
 
     void* workspace(size_t bytes);
     tcec::DevDecision* decisions(int slots);

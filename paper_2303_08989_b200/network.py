@@ -136,8 +136,9 @@ class Network:
             return t, lines
         return t
 
-    def selector_batch(self, path, bitstrings, config=None) -> np.ndarray:
-        """Amplitudes of many bitstrings over one plan / one captured graph."""
+    def selector_batch(self, path, bitstrings, config=None, out=None) -> np.ndarray:
+        """Amplitudes of many bitstrings over one plan / one captured graph.
+        `bitstrings` / `out` may live in pinned host memory (faster copies)."""
         cfg = _cfg(config)
         _, steps = self._steps(path)
         sel = self.spec.selector_nodes
@@ -145,7 +146,10 @@ class Network:
         sel_arr = (C.c_int * max(nsel, 1))(*sel)
         bits = np.ascontiguousarray(np.asarray(bitstrings, dtype=np.uint8).reshape(-1))
         n = len(bitstrings)
-        out = np.empty(n, dtype=np.complex64)
+        if out is None:
+            out = np.empty(n, dtype=np.complex64)
+        elif out.dtype != np.complex64 or out.size != n or not out.flags.c_contiguous:
+            raise ValueError("out must be a contiguous complex64 array with one slot per bitstring")
         check(self.lib.tcec_contract_selector_batch(
             self.net, steps, len(path), C.byref(cfg), nsel, sel_arr, n,
             bits.ctypes.data_as(C.POINTER(C.c_uint8)), out.ctypes.data_as(C.c_void_p)))
