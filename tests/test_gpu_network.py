@@ -155,6 +155,34 @@ def test_selector_batch_equals_single_amplitudes(handle, golden, executor):
     net.close()
 
 
+def test_selector_batch_pinned_out_and_batch_profile(handle, golden):
+    """selector_batch into a caller-provided (pinned) output array gives the
+    same bits; tcec_profile_read_batches counts each batch with a positive
+    device time while profiling is on, and nothing after it is switched off."""
+    import torch
+    rq = golden("rqc.json")[2]
+    c = rqc_rectangular(rq["rows"], rq["cols"], rq["depth"], rq["seed"])
+    xs = np.array([row["x"] for row in rq["amplitudes"]], np.uint8)
+    net = Network(handle, circuit_to_network(c, list(xs[0])))
+    path = [tuple(s) for s in rq["path"]]
+    want = net.selector_batch(path, xs, BASELINE)
+    pin_bits = torch.empty(xs.shape, dtype=torch.uint8, pin_memory=True).numpy()
+    pin_bits[...] = xs
+    out = torch.empty(len(xs), dtype=torch.complex64, pin_memory=True).numpy()
+    handle.profile(True)
+    got = net.selector_batch(path, pin_bits, BASELINE, out=out)
+    net.selector_batch(path, pin_bits, BASELINE, out=out)
+    ms, count = handle.profile_read_batches()
+    handle.profile(False)
+    assert got is out and np.array_equal(out.view(np.uint32), want.view(np.uint32))
+    assert count == 2 and ms > 0
+    net.selector_batch(path, pin_bits, BASELINE, out=out)
+    assert handle.profile_read_batches()[1] == 0  # profile(False) resets and stops counting
+    with pytest.raises(ValueError):
+        net.selector_batch(path, pin_bits, BASELINE, out=np.empty(3, np.complex64))
+    net.close()
+
+
 def test_amplitude_api_and_statevector(handle):
     c = rqc_rectangular(2, 3, 6, 21)
     g = np.random.default_rng(99)
