@@ -924,6 +924,7 @@ def run_rqc7x7(args):
     if rank == 0:
         deep_row = [r for r in rows_out if r["depth"] == depths[-1]][0]["modes"]["AUTO-0"]
         deep, deep_e2e = deep_row["ms_per_amplitude"], deep_row["e2e_ms_per_amplitude"]
+        hyper_same = [r for r in rows_out if r["depth"] == depths[-1] and r.get("path", "").startswith("hyper")]
         line = {"metric": f"RCS 7x7 deep-circuit amplitude time (AUTO-0, depth {depths[-1]})",
                 "value": deep, "unit": "ms/amplitude", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": deep, "higher_is_better": False,
@@ -937,6 +938,12 @@ def run_rqc7x7(args):
                         "note": "the whole tcec_contract_selector_batch call per bitstring (host bits in, "
                                 "host amplitude out); value = its device time after the upload"},
                 "depths": rows_out, "clocks": clk.summary()}
+        if hyper_same:
+            # the same circuit through this repo's path finder
+            line["with_path_search"] = {
+                "ms_per_amplitude": hyper_same[0]["modes"]["AUTO-0"]["ms_per_amplitude"],
+                "gflop_per_amplitude": hyper_same[0]["gflop_per_amplitude"],
+                "greedy_gflop_per_amplitude": [r for r in rows_out if r["depth"] == depths[-1]][0]["gflop_per_amplitude"]}
         print(json.dumps(line), flush=True)
     h.close()
 
@@ -958,7 +965,7 @@ def main():
     p.add_argument("--cycles", type=int, default=12)
     p.add_argument("--path", choices=["plan", "hyper", "greedy"], default="plan")
     p.add_argument("--depths", default="4,8,12,14,16")
-    p.add_argument("--hyper-depths", default="18,20,24")
+    p.add_argument("--hyper-depths", default="16,18,20,24")
     p.add_argument("--slices-log2", type=int, default=6)
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
