@@ -711,7 +711,12 @@ static HostPipe plan_host_pipe(int64_t m, int64_t n, int chunks, int parts) {
     hp.q = int(std::max<int64_t>(1, std::min<int64_t>(parts, n / 256)));  // parts of >= 256 columns
     hp.wq = round_up((n + hp.q - 1) / hp.q, 128);  // even column offsets keep C blocks 16-B aligned
     hp.q = int((n + hp.wq - 1) / hp.wq);
-    hp.front = std::max(1, hp.q / 2);
+    static const int front_num = [] {  // front parts in eighths of q (tuning: TCEC_HOST_BFRONT)
+        const char* e = std::getenv("TCEC_HOST_BFRONT");
+        const int v = e ? std::atoi(e) : 0;
+        return v > 0 && v <= 8 ? v : 4;
+    }();
+    hp.front = std::max(1, hp.q * front_num / 8);
     return hp;
 }
 
