@@ -45,6 +45,22 @@ struct tcec_handle_s {
     double batch_ms = 0.0;
     int64_t batch_count = 0;
 
+    // replayable graphs of small device-pointer dispatches (tcec_dispatch_cgemm):
+    // the whole launch sequence of one (pointers, shape, config) as one graph
+    // launch instead of ~7 host-enqueued operations
+    struct DispatchGraph {
+        const void *a, *b;
+        void *c, *ws, *dec;
+        int64_t m, n, k;
+        double t;
+        int64_t size_auto, size_tf32;
+        int target, k_tile, force, variant, flush;
+        cudaStream_t stream;
+        cudaGraphExec_t exec;
+    };
+    DispatchGraph graphs[8] = {};
+    int n_graphs = 0, next_graph = 0;
+
     void* workspace(size_t bytes);
     tcec::DevDecision* decisions(int slots);
     ~tcec_handle_s();

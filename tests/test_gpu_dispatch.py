@@ -254,3 +254,33 @@ def test_handles_on_concurrent_host_threads(dev):
             assert torch.equal(x.view(torch.float32), y.view(torch.float32))
     for h in handles:
         h.close()
+
+
+def test_graph_replay_reads_new_data(handle, orc, dev):
+    """Small device-pointer dispatches replay a captured graph when the same
+    pointers, shape and configuration come again: in-place changes to the
+    operands (including ones that change the device decision) must show up
+    exactly as in a fresh dispatch."""
+    from paper_2303_08989_b200 import Handle
+    g = np.random.default_rng(5)
+    m, n, k = 384, 320, 256
+    a_np = (g.random((m, k, 2), dtype=np.float32) * 2 - 1).view(np.complex64)[..., 0].copy()
+    b_np = (g.random((k, n, 2), dtype=np.float32) * 2 - 1).view(np.complex64)[..., 0].copy()
+    a, b = torch.from_numpy(a_np).to(dev), torch.from_numpy(b_np).to(dev)
+    c = torch.empty(m, n, dtype=torch.complex64, device=dev)
+    pol = SelectionPolicy(size_auto=128, size_tf32=64)
+    fresh = Handle(0)
+    for step in range(4):
+        if step == 2:
+            a.mul_(2.0 ** -20)  # moves e_max: another FP16TCEC_SCALED shift
+        elif step == 3:
+            a.copy_(torch.from_numpy((g.random((m, k, 2), dtype=np.float32) * 2 - 1)
+                                     .view(np.complex64)[..., 0].copy()).to(dev))
+        _, res = handle.dispatch_cgemm(a, b, pol, out=c)
+        want, res_w = fresh.dispatch_cgemm(a.clone(), b.clone(), pol)
+        assert res.line == res_w.line
+        assert torch.equal(c.view(torch.float32), want.view(torch.float32))
+        c32, _ = handle.dispatch_cgemm(a, b, make_config(force="FP32_REF"), out=c)
+        ref, _ = orc.cgemm(a.cpu().numpy(), b.cpu().numpy(), "FP32_REF")
+        assert np.array_equal(c32.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+    fresh.close()
