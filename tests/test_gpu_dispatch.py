@@ -284,3 +284,28 @@ def test_graph_replay_reads_new_data(handle, orc, dev):
         ref, _ = orc.cgemm(a.cpu().numpy(), b.cpu().numpy(), "FP32_REF")
         assert np.array_equal(c32.cpu().numpy().view(np.uint32), ref.view(np.uint32))
     fresh.close()
+
+
+def test_host_pipeline_on_a_caller_stream(dev):
+    """The pipelined host-buffer dispatch on a handle bound to the caller's
+    stream (tcec_set_stream) gives the bits of the handle's own stream, call
+    after call (the staging buffers and side streams are reused)."""
+    from paper_2303_08989_b200 import Handle
+    g = np.random.default_rng(8)
+    m, n, k = 8448, 2304, 640
+    a = (g.random((m, k, 2), dtype=np.float32) * 2 - 1).view(np.complex64)[..., 0].copy()
+    b = (g.random((k, n, 2), dtype=np.float32) * 2 - 1).view(np.complex64)[..., 0].copy()
+    pol = SelectionPolicy(size_auto=128, size_tf32=64)
+    h0 = Handle(0)
+    want, res_w = h0.dispatch_cgemm_host(a, b, pol)
+    h1 = Handle(0)
+    s = torch.cuda.Stream(device=dev)
+    h1.set_stream(s)
+    for _ in range(2):
+        got, res = h1.dispatch_cgemm_host(a, b, pol)
+        assert res.line == res_w.line
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    assert h1.host_pipeline_stats()[0] == 2
+    h1.set_stream(None)
+    h0.close()
+    h1.close()
