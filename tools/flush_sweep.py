@@ -10,11 +10,11 @@ from paper_2303_08989_b200 import Handle, make_config  # noqa: E402
 
 h = Handle(0)
 dev = torch.device("cuda:0")
-for nn in (4096, 8192):
+for nn in [int(v) for v in os.environ.get("NS", "4096,8192").split(",")]:
     a = (torch.rand(nn, nn, 2, device=dev) * 2 - 1).view(torch.complex64)[..., 0].contiguous()
     b = (torch.rand(nn, nn, 2, device=dev) * 2 - 1).view(torch.complex64)[..., 0].contiguous()
     c = torch.empty(nn, nn, dtype=torch.complex64, device=dev)
-    for mode in ("FP16TCEC", "TF32TCEC"):
+    for mode in os.environ.get("MODES", "FP16TCEC,TF32TCEC").split(","):
         for fl in (1, 2, 4, 0):
             h.flush_kblocks = fl
             cfg = make_config(force=mode)
