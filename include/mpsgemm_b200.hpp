@@ -171,11 +171,19 @@ struct DeviceBuffer {
     DeviceBuffer& operator=(const DeviceBuffer&) = delete;
 };
 
+// Copies run on the handle's own (non-blocking) stream, so they are ordered
+// with the kernels the C-ABI enqueues there; the stream is synchronised before
+// the host touches the result (a legacy-stream cudaMemcpy would not be).
 inline void upload(void* d, const void* h, std::size_t bytes) {
-    if (bytes && cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice) != cudaSuccess) throw DeviceError("H2D failed");
+    if (!bytes) return;
+    cudaStream_t s = static_cast<cudaStream_t>(tcec_get_stream(handle()));
+    if (cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) throw DeviceError("H2D failed");
 }
 inline void download(void* h, const void* d, std::size_t bytes) {
-    if (bytes && cudaMemcpy(h, d, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) throw DeviceError("D2H failed");
+    cudaStream_t s = static_cast<cudaStream_t>(tcec_get_stream(handle()));
+    if (bytes && cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        throw DeviceError("D2H failed");
+    throw_status(tcec_synchronize(handle()));
 }
 
 inline tcec_dispatch_config_t to_c(const DispatchConfig& cfg) {

@@ -104,6 +104,20 @@ int tcec_scale_buf(tcec_handle h, const float* src, float* dst, int64_t n, int s
 int tcec_add_buf(tcec_handle h, const float* a, const float* b, float* dst, int64_t n);
 int tcec_sub_buf(tcec_handle h, const float* a, const float* b, float* dst, int64_t n);
 
+/* Test hook (no reference counterpart; it exposes an internal stage of
+ * dispatch_cgemm so it can be pinned bit for bit): the hot path's operand
+ * preparation for a fixed decision kind (0 FP16TCEC, 1 FP16TCEC_SCALED,
+ * 2 TF32TCEC) and shifts -- scale_buf + split_buf (kernels_scalar.cpp:24-40)
+ * fused with the K-major layout.  Device outputs: a_hi/a_lo m x kp and
+ * b_hi/b_lo 2n x kp elements (binary16 for the FP16 kinds, f32 for TF32),
+ * kp = tcec_prep_kp(k) = round_up(2k, 64), zero padded; A' row i = the
+ * interleaved (re, im) row i of A; B' row 2j = (Br, -Bi), row 2j+1 = (Bi, Br)
+ * per complex k.  flags[0] = format overflow, flags[1] = ScaleOverflow. */
+int64_t tcec_prep_kp(int64_t k);
+int tcec_debug_prep(tcec_handle h, const void* a, const void* b, int64_t m, int64_t n, int64_t k,
+                    int kind, int scale_a, int scale_b, int corrected, void* a_hi, void* a_lo,
+                    void* b_hi, void* b_lo, int* flags);
+
 /* ------------------------------------------------- precision selection */
 /* ExpStats, precsel.hpp:18-36 (e_max_valid == 0 <=> std::nullopt) */
 typedef struct {
@@ -226,6 +240,21 @@ int tcec_contract_selector_batch(tcec_network net, const int* steps, int n_steps
 int tcec_contract_node_batch(tcec_network net, const int* steps, int n_steps,
                              const tcec_dispatch_config_t* cfg, int n_var, const int* var_nodes,
                              int n_runs, const void* var_data, void* out_host);
+
+/* ------------------------------------------------- workload generation
+ * The reference's deterministic random source (Rng, rng.hpp:13-56: the
+ * standard std::mt19937_64 + its hand-rolled maps), host code, so benchmark
+ * inputs are the reference's own -- configs[1] fills A then B from one
+ * Rng(seed + n) with two uniform_pm1f draws per complex element
+ * (experiments.cpp:76-83).  No device work. */
+typedef struct tcec_rng_s* tcec_rng;
+int tcec_rng_create(uint64_t seed, tcec_rng* out);
+int tcec_rng_destroy(tcec_rng r);
+uint64_t tcec_rng_next_u64(tcec_rng r);
+/* n successive Rng::uniform_pm1f() draws (rng.hpp:35) */
+int tcec_rng_fill_uniform_pm1f(tcec_rng r, float* dst, int64_t n);
+/* n successive Rng::gaussian(stddev) draws (rng.hpp:38-50) */
+int tcec_rng_fill_gaussian(tcec_rng r, double stddev, double* dst, int64_t n);
 
 #ifdef __cplusplus
 }

@@ -12,6 +12,7 @@
 #include <cstdint>
 #include <cstring>
 #include <functional>
+#include <optional>
 #include <sstream>
 #include <string>
 #include <thread>
@@ -228,6 +229,20 @@ void ref_rng_uniform_c32(std::uint64_t seed, std::int64_t rows, std::int64_t col
         const std::complex<float> v{rng.uniform_pm1f(), rng.uniform_pm1f()};
         out[2 * i] = v.real();
         out[2 * i + 1] = v.imag();
+    }
+}
+
+// run_gemm_bench operands (experiments.cpp:80-83): one Rng(seed), A then B
+void ref_gemm_bench_operands(std::uint64_t seed, std::int64_t m, std::int64_t k, std::int64_t n,
+                             float* a, float* b) {
+    Rng rng(seed);
+    for (std::int64_t i = 0; i < m * k; ++i) {
+        a[2 * i] = rng.uniform_pm1f();
+        a[2 * i + 1] = rng.uniform_pm1f();
+    }
+    for (std::int64_t i = 0; i < k * n; ++i) {
+        b[2 * i] = rng.uniform_pm1f();
+        b[2 * i + 1] = rng.uniform_pm1f();
     }
 }
 
@@ -459,6 +474,95 @@ int ref_cgemm_rows_threaded_timed(const float* a, const float* b, float* c, std:
         gemm_s[0] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_prep).count();
     (void)t_gemm;
     return ovf ? 1 : 0;
+}
+
+
+// The reference's dispatch_cgemm (precsel.cpp:225-322) on the full operands,
+// timed on a bounded row block: the selection half runs exactly as the
+// reference runs it (exp_stats_staged on all of A and B, matrix_tolerance,
+// select_mode, DecisionRecord::to_line -> *line), then the selected kind's
+// CGEMM computes output rows [row_begin, row_end) with the reference kernels
+// over n_threads (FP16TCEC_SCALED: scale_matrix of the A rows and of B by the
+// selected shifts, FP16TCEC rows, descale -- precsel.cpp:209-216).  Times:
+// t[0] statistics + selection, t[1] O(n^2) operand scaling/preparation,
+// t[2] row GEMM.  Returns 0, or the error_code() of a thrown exception.
+int ref_dispatch_rows_threaded_timed(const float* a, const float* b, float* c, std::int64_t m,
+                                     std::int64_t n, std::int64_t k, std::int64_t row_begin,
+                                     std::int64_t row_end, const ConfigPod* cfg, int n_threads,
+                                     char* line, int line_cap, int* kind_out, double* t) {
+    try {
+        const DispatchConfig dc = to_config(cfg);
+        const SelectionPolicy& pol = dc.policy;
+        const int target = pol.target_max_exponent;
+        const auto t0 = std::chrono::steady_clock::now();
+        ComputeMode decision{ComputeKind::fp32_baseline, 0, 0};
+        std::optional<ExpStats> sa, sb;
+        std::string label;
+        if (dc.force) throw std::invalid_argument("forced modes are not timed here");
+        if (std::min({m, n, k}) >= pol.size_auto) {
+            {
+                const MatrixC32 ma = load_c32(a, m, k);
+                sa = exp_stats_staged(ma, target, pol.threshold_t);
+            }
+            {
+                const MatrixC32 mb = load_c32(b, k, n);
+                sb = exp_stats_staged(mb, target, pol.threshold_t);
+            }
+            decision = select_mode(matrix_tolerance(*sa, pol.threshold_t, target),
+                                   matrix_tolerance(*sb, pol.threshold_t, target), target);
+        } else if (std::min({m, n, k}) >= pol.size_tf32) {
+            decision = {ComputeKind::tf32_tcec, 0, 0};
+        }
+        label = to_string(decision.kind);
+        DecisionRecord rec;
+        rec.m = m;
+        rec.n = n;
+        rec.k = k;
+        rec.mode = label;
+        rec.scale_a = decision.scale_exp_a;
+        rec.scale_b = decision.scale_exp_b;
+        rec.stats_a = sa;
+        rec.stats_b = sb;
+        std::snprintf(line, static_cast<std::size_t>(line_cap), "%s", rec.to_line().c_str());
+        *kind_out = static_cast<int>(decision.kind);
+        const auto t1 = std::chrono::steady_clock::now();
+
+        GemmMode gm = GemmMode::fp32_ref;
+        switch (decision.kind) {
+        case ComputeKind::fp16_tcec:
+        case ComputeKind::fp16_tcec_scaled: gm = GemmMode::fp16_tcec; break;
+        case ComputeKind::tf32_tcec: gm = GemmMode::tf32_tcec; break;
+        default: break;
+        }
+        const std::int64_t rows = row_end - row_begin;
+        const float* ap = a + 2 * row_begin * k;
+        const float* bp = b;
+        MatrixC32 a_s, b_s;
+        if (decision.kind == ComputeKind::fp16_tcec_scaled) {
+            a_s = scale_matrix(load_c32(ap, rows, k), decision.scale_exp_a);
+            b_s = scale_matrix(load_c32(b, k, n), decision.scale_exp_b);
+            ap = reinterpret_cast<const float*>(a_s.data.data());
+            bp = reinterpret_cast<const float*>(b_s.data.data());
+        }
+        const auto t2 = std::chrono::steady_clock::now();
+        double prep = 0.0, gemm = 0.0;
+        ref_cgemm_rows_threaded_timed(ap, bp, c, rows, n, k, 0, rows, static_cast<int>(gm),
+                                      dc.tiling.k_tile, n_threads, &prep, &gemm);
+        const auto t3 = std::chrono::steady_clock::now();
+        if (decision.kind == ComputeKind::fp16_tcec_scaled) {
+            MatrixC32 cm = load_c32(c, rows, n);
+            descale_output_inplace(cm, decision.scale_exp_a, decision.scale_exp_b);
+            std::memcpy(c, cm.data.data(), sizeof(float) * 2 * static_cast<std::size_t>(rows * n));
+        }
+        const auto t4 = std::chrono::steady_clock::now();
+        t[0] = std::chrono::duration<double>(t1 - t0).count();
+        t[1] = std::chrono::duration<double>(t2 - t1).count() + prep +
+               std::chrono::duration<double>(t4 - t3).count();
+        t[2] = gemm;
+        return 0;
+    } catch (...) {
+        return error_code();
+    }
 }
 
 } // extern "C"

@@ -158,6 +158,13 @@ def load() -> C.CDLL:
                                           C.POINTER(C.c_uint8), vp], i32),
         "tcec_contract_node_batch": ([vp, ip, i32, C.POINTER(DispatchConfig), i32, ip, i32, vp,
                                       vp], i32),
+        "tcec_prep_kp": ([i64], i64),
+        "tcec_rng_create": ([C.c_uint64, C.POINTER(vp)], i32),
+        "tcec_rng_destroy": ([vp], i32),
+        "tcec_rng_next_u64": ([vp], C.c_uint64),
+        "tcec_rng_fill_uniform_pm1f": ([vp, vp, i64], i32),
+        "tcec_rng_fill_gaussian": ([vp, dbl, vp, i64], i32),
+        "tcec_debug_prep": ([vp, vp, vp, i64, i64, i64, i32, i32, i32, i32, vp, vp, vp, vp, ip], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name, None)

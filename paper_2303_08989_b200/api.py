@@ -52,6 +52,12 @@ def _torch():
 
 
 def _ptr(t) -> C.c_void_p:
+    """Device pointer of a tensor the C-ABI may read as dense row-major memory.
+    A strided view would be computed on the wrong layout, so it is rejected."""
+    if not t.is_cuda:
+        raise _lib.ShapeMismatch(1, "operand must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise _lib.ShapeMismatch(1, "operand must be contiguous (call .contiguous())")
     return C.c_void_p(t.data_ptr())
 
 
@@ -163,7 +169,12 @@ class Handle:
 
     # ------------------------------------------------------ KernelTable level
     def _out_like(self, x):
-        return _torch().empty_like(x)
+        torch = _torch()
+        if x.dtype != torch.float32:
+            raise _lib.ShapeMismatch(1, f"buffer dtype must be float32, got {x.dtype}")
+        if not x.is_cuda or x.device.index != self.device or not x.is_contiguous():
+            raise _lib.ShapeMismatch(1, f"buffer must be a contiguous tensor on cuda:{self.device}")
+        return torch.empty_like(x)
 
     def quantize_buf(self, x, fmt: int, rounding: int = 0):
         y = self._out_like(x)
@@ -186,11 +197,17 @@ class Handle:
 
     def add_buf(self, a, b):
         y = self._out_like(a)
+        self._out_like(b)
+        if b.numel() != a.numel():
+            raise _lib.ShapeMismatch(1, "add_buf: buffers differ in length")
         self._ordered_call(self.lib.tcec_add_buf, self.h, _ptr(a), _ptr(b), _ptr(y), a.numel())
         return y
 
     def sub_buf(self, a, b):
         y = self._out_like(a)
+        self._out_like(b)
+        if b.numel() != a.numel():
+            raise _lib.ShapeMismatch(1, "sub_buf: buffers differ in length")
         self._ordered_call(self.lib.tcec_sub_buf, self.h, _ptr(a), _ptr(b), _ptr(y), a.numel())
         return y
 
@@ -198,6 +215,7 @@ class Handle:
     def exp_stats(self, m, target_max_exponent: int = 14) -> ExpStats:
         """exp_stats (precsel.hpp:68): both stages unconditionally."""
         out = ExpStats()
+        self._check_c64(m)
         rows, cols = (m.shape if m.dim() == 2 else (1, m.numel()))
         self._ordered_call(self.lib.tcec_exp_stats, self.h, _ptr(m), rows, cols, target_max_exponent, 0, 0.0,
                                       C.byref(out))
@@ -206,6 +224,7 @@ class Handle:
     def exp_stats_staged(self, m, target_max_exponent: int, t: float) -> ExpStats:
         """exp_stats_staged (precsel.hpp:70)."""
         out = ExpStats()
+        self._check_c64(m)
         rows, cols = (m.shape if m.dim() == 2 else (1, m.numel()))
         self._ordered_call(self.lib.tcec_exp_stats, self.h, _ptr(m), rows, cols, target_max_exponent, 1,
                                       float(t), C.byref(out))
@@ -213,6 +232,7 @@ class Handle:
 
     def scale_matrix_inplace(self, m, scale_exp: int) -> None:
         """scale_matrix_inplace (precsel.hpp:82): ScaleOverflow on nonfinite."""
+        self._check_c64(m)
         x = m.view(_torch().float32)
         self._ordered_call(self.lib.tcec_scale_components, self.h, _ptr(x), x.numel(), int(scale_exp), 1)
 
@@ -223,14 +243,26 @@ class Handle:
 
     def descale_output_inplace(self, c, scale_exp_a: int, scale_exp_b: int) -> None:
         """descale_output_inplace (precsel.hpp:88): no overflow check."""
+        self._check_c64(c)
         x = c.view(_torch().float32)
         self._ordered_call(self.lib.tcec_scale_components, self.h, _ptr(x), x.numel(),
                                              -(int(scale_exp_a) + int(scale_exp_b)), 0)
 
     # --------------------------------------------------------------- CGEMM
+    def _check_c64(self, *ts):
+        torch = _torch()
+        for t in ts:
+            if t.dtype != torch.complex64:
+                raise _lib.ShapeMismatch(1, f"operand dtype must be complex64, got {t.dtype}")
+            if not t.is_cuda or t.device.index != self.device:
+                raise _lib.ShapeMismatch(1, f"operand must live on cuda:{self.device}")
+            if not t.is_contiguous():
+                raise _lib.ShapeMismatch(1, "operand must be contiguous (call .contiguous())")
+
     def _shapes(self, a, b):
         if a.dim() != 2 or b.dim() != 2:
             raise _lib.ShapeMismatch(1, "operands must be matrices")
+        self._check_c64(a, b)
         m, k = a.shape
         k2, n = b.shape
         if k != k2:
@@ -242,6 +274,10 @@ class Handle:
         m, n, k = self._shapes(a, b)
         c = out if out is not None else _torch().empty((m, n), dtype=_torch().complex64,
                                                        device=a.device)
+        if out is not None:
+            self._check_c64(c)
+            if tuple(c.shape) != (m, n):
+                raise _lib.ShapeMismatch(1, "output shape must be (m, n)")
         md = GEMM_MODES[mode] if isinstance(mode, str) else int(mode)
         ovf = C.c_int(0)
         self._ordered_call(self.lib.tcec_cgemm, self.h, _ptr(a), _ptr(b), _ptr(c), m, n, k, md, int(k_tile),
@@ -265,6 +301,10 @@ class Handle:
         m, n, k = self._shapes(a, b)
         c = out if out is not None else _torch().empty((m, n), dtype=_torch().complex64,
                                                        device=a.device)
+        if out is not None:
+            self._check_c64(c)
+            if tuple(c.shape) != (m, n):
+                raise _lib.ShapeMismatch(1, "output shape must be (m, n)")
         res = DispatchResult()
         self._ordered_call(self.lib.tcec_dispatch_cgemm, self.h, _ptr(a), _ptr(b), _ptr(c), m, n, k,
                                            C.byref(config), C.byref(res))
@@ -279,6 +319,10 @@ class Handle:
         m, k = a.shape
         n = b.shape[1]
         c = out if out is not None else np.empty((m, n), dtype=np.complex64)
+        if b.shape[0] != k:
+            raise _lib.ShapeMismatch(1, "dispatch_cgemm: inner dimensions differ")
+        if c.dtype != np.complex64 or c.shape != (m, n) or not c.flags.c_contiguous:
+            raise _lib.ShapeMismatch(1, "output must be a contiguous complex64 (m, n) array")
         res = DispatchResult()
         check(self.lib.tcec_dispatch_cgemm_host(self.h, a.ctypes.data_as(C.c_void_p),
                                                 b.ctypes.data_as(C.c_void_p),
@@ -286,10 +330,34 @@ class Handle:
                                                 C.byref(config), C.byref(res)))
         return c, res
 
+    # ------------------------------------------- operand preparation (test hook)
+    def debug_prep(self, a, b, kind: str | int, scale_a: int = 0, scale_b: int = 0,
+                   corrected: bool = True):
+        """Run the hot path's prep_a / prep_b for a fixed decision and return the
+        tensor-core operand planes (tcec_debug_prep): A' hi/lo (m x kp) and B'
+        hi/lo (2n x kp), binary16 for the FP16 kinds and f32 for TF32, plus the
+        (format overflow, ScaleOverflow) flags."""
+        torch = _torch()
+        self._check_c64(a, b)
+        kd = KINDS.index(kind) if isinstance(kind, str) else int(kind)
+        m, k = a.shape
+        k2, n = b.shape
+        if k != k2:
+            raise _lib.ShapeMismatch(1, "debug_prep: inner dimensions differ")
+        kp = int(self.lib.tcec_prep_kp(k))
+        dt = torch.float32 if kd == 2 else torch.float16
+        planes = [torch.zeros((r, kp), dtype=dt, device=a.device) for r in (m, m, 2 * n, 2 * n)]
+        flags = (C.c_int * 2)()
+        self._ordered_call(self.lib.tcec_debug_prep, self.h, _ptr(a), _ptr(b), m, n, k, kd,
+                           int(scale_a), int(scale_b), int(bool(corrected)),
+                           *[_ptr(t) for t in planes], flags)
+        return (*planes, bool(flags[0]), bool(flags[1]))
+
     # ------------------------------------------------------------- permute
     def permute(self, t, axis_of):
         """permute (tensor.hpp:56-57): new axis a is old axis axis_of[a]."""
         r = t.dim()
+        self._check_c64(t)
         if len(axis_of) != r:
             raise _lib.InvalidPermutation(4, "permutation has wrong length")
         out = _torch().empty(tuple(t.shape[a] for a in axis_of), dtype=t.dtype, device=t.device)

@@ -280,9 +280,21 @@ int finish_dispatch(const DispatchPlan& p, const DevDecision& dd, int64_t m, int
 
 using namespace tcec;
 
+// Captured dispatch graphs bake in the workspace / decision addresses (and the
+// pinned decision mirror their D2H copy targets); any reallocation retires them.
+void tcec_handle_s::drop_graphs() {
+    for (auto& g : graphs) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        g = DispatchGraph{};
+    }
+    n_graphs = 0;
+    next_graph = 0;
+}
+
 void* tcec_handle_s::workspace(size_t bytes) {
     if (bytes <= ws_bytes) return ws;
     cudaStreamSynchronize(stream);
+    drop_graphs();
     if (ws) cudaFree(ws);
     ws = nullptr;
     ws_bytes = 0;
@@ -302,6 +314,7 @@ void* tcec_handle_s::workspace(size_t bytes) {
 tcec::DevDecision* tcec_handle_s::decisions(int slots) {
     if (slots <= dec_slots) return dec;
     cudaStreamSynchronize(stream);
+    drop_graphs();
     if (dec) cudaFree(dec);
     if (dec_host) cudaFreeHost(dec_host);
     dec = nullptr;
@@ -315,7 +328,9 @@ tcec::DevDecision* tcec_handle_s::decisions(int slots) {
 }
 
 tcec_handle_s::~tcec_handle_s() {
+    if (stream) cudaStreamSynchronize(stream);
     if (ws) cudaFree(ws);
+    if (io) cudaFree(io);
     if (dec) cudaFree(dec);
     if (dec_host) cudaFreeHost(dec_host);
     if (scratch_host) cudaFreeHost(scratch_host);
@@ -549,6 +564,44 @@ int tcec_scale_components(tcec_handle h, float* x, int64_t n, int scale_exp, int
     const int rc = read_flag(h, &d->scale_overflow, &bad);
     if (rc) return rc;
     if (bad) return set_error(TCEC_ERR_SCALE_OVERFLOW, "scaled component left the f32 range");
+    return TCEC_OK;
+}
+
+// Test hook for the hot-path operand preparation (prep_a / prep_b): the same
+// kernels launch_dispatch runs, for a decision fixed by the caller, writing
+// straight into caller planes so a test can compare them bit for bit with the
+// reference's split_buf(scale_buf(x)) (kernels_scalar.cpp:24-40).
+int64_t tcec_prep_kp(int64_t k) { return round_up(2 * k, 64); }
+
+int tcec_debug_prep(tcec_handle h, const void* a, const void* b, int64_t m, int64_t n, int64_t k,
+                    int kind, int scale_a, int scale_b, int corrected, void* a_hi, void* a_lo,
+                    void* b_hi, void* b_lo, int* flags) {
+    CHECK_HANDLE(h);
+    if (m < 0 || n < 0 || k < 0) return set_error(TCEC_ERR_SHAPE_MISMATCH, "negative extent");
+    if (kind != kKindFp16 && kind != kKindFp16Scaled && kind != kKindTf32)
+        return set_error(TCEC_ERR_INVALID_ARGUMENT, "debug_prep: kind must be a tensor-core kind");
+    DevDecision* d = h->decisions(1);
+    if (!d) return set_error(TCEC_ERR_CUDA, "decision buffer allocation failed");
+    DevDecision* hd = h->dec_host;
+    std::memset(hd, 0, sizeof(DevDecision));
+    hd->kind = kind;
+    hd->scale_a = scale_a;
+    hd->scale_b = scale_b;
+    CUDA_TRY(cudaMemcpyAsync(d, hd, sizeof(DevDecision), cudaMemcpyHostToDevice, h->stream));
+    const int64_t kp = tcec_prep_kp(k);
+    if (a && m > 0 && k > 0)
+        launch_prep_a(static_cast<const float*>(a), m, k, kp, a_hi, a_lo, d, -1, corrected ? 1 : 0,
+                      h->stream, 0);
+    if (b && n > 0 && k > 0)
+        launch_prep_b(static_cast<const float*>(b), k, n, kp, b_hi, b_lo, d, -1, corrected ? 1 : 0,
+                      h->stream, 0);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(hd, d, sizeof(DevDecision), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (flags) {
+        flags[0] = hd->overflow ? 1 : 0;
+        flags[1] = hd->scale_overflow ? 1 : 0;
+    }
     return TCEC_OK;
 }
 

@@ -268,6 +268,9 @@ struct PrepMode {
     int fmt;       // kFp16 / kTf32
     int scale;     // power-of-two shift (FP16TCEC_SCALED)
     bool active;   // false: this dispatch does not use tensor cores
+    bool scaled;   // FP16TCEC_SCALED: the operand goes through scale_matrix, which
+                   // throws ScaleOverflow on any nonfinite result -- even for a
+                   // zero shift (precsel.cpp:209-216, 139-152)
 };
 
 TCEC_DEV PrepMode prep_mode(const DevDecision* d, int kind_fixed, bool is_b) {
@@ -276,16 +279,15 @@ TCEC_DEV PrepMode prep_mode(const DevDecision* d, int kind_fixed, bool is_b) {
     p.active = kind == kKindFp16 || kind == kKindFp16Scaled || kind == kKindTf32;
     p.fmt = kind == kKindTf32 ? kTf32 : kFp16;
     p.scale = kind == kKindFp16Scaled ? (is_b ? d->scale_b : d->scale_a) : 0;
+    p.scaled = kind == kKindFp16Scaled;
     return p;
 }
 
 // scale (optional) + split/quantize one component; returns hi, lo
 TCEC_DEV void convert(float x, const PrepMode& pm, double factor, bool corrected, float& hi,
                       float& lo, unsigned& ovf, unsigned& bad) {
-    if (pm.scale != 0) {
-        x = scale_pow2(x, factor);
-        bad |= isfinite(x) ? 0u : 1u;
-    }
+    if (pm.scale != 0) x = scale_pow2(x, factor);
+    if (pm.scaled) bad |= isfinite(x) ? 0u : 1u;
     if (corrected) {
         if (pm.fmt == kFp16)
             split<kFp16>(x, hi, lo, ovf);
@@ -321,11 +323,12 @@ TCEC_DEV void convert_n(float (&x)[N], const PrepMode& pm, double factor, float 
     uint32_t mb = 0;
 #pragma unroll
     for (int e = 0; e < N; ++e) mb = max(mb, __float_as_uint(x[e]) & 0x7FFFFFFFu);
-    if (pm.scale != 0) bad |= mb >= 0x7F800000u ? 1u : 0u;
+    if (pm.scaled) bad |= mb >= 0x7F800000u ? 1u : 0u;
     const uint32_t lim = pm.fmt == kFp16 ? __float_as_uint(kFp16Max) : __float_as_uint(kTf32Max);
     if (mb > lim) {
         PrepMode ns = pm;
-        ns.scale = 0;
+        ns.scale = 0;       // already scaled (and checked) above
+        ns.scaled = false;
 #pragma unroll
         for (int e = 0; e < N; ++e) convert(x[e], ns, 1.0, corrected, h[e], l[e], ovf, bad);
         return;
@@ -466,27 +469,34 @@ __global__ void __launch_bounds__(256) prep_b_kernel(const float2* __restrict__ 
                 const float4 v = *reinterpret_cast<const float4*>(&tile[jj][2 * lane]);
                 float xv[4] = {v.x, v.y, v.z, v.w}, hv[4], lv[4];   // (re0, im0, re1, im1)
                 convert_n<4>(xv, pm, factor, fs, corrected, hv, lv, ovf, bad);
+                // negated imaginary parts; the K padding stays +0 in every
+                // plane (negating the zero fill would write -0)
+                float hn1 = -hv[1], hn3 = -hv[3], ln1 = -lv[1], ln3 = -lv[3];
+                if (kk0 + 2 * lane + 1 >= k) {
+                    hn3 = ln3 = 0.0f;
+                    if (kk0 + 2 * lane >= k) hn1 = ln1 = 0.0f;
+                }
                 const int64_t r0 = (2 * (jout0 + j)) * kp + col, r1 = r0 + kp;
                 if (pm.fmt == kFp16) {
                     __half* hp = static_cast<__half*>(hi_v);
-                    __half2 q0[2] = {__floats2half2_rn(hv[0], -hv[1]), __floats2half2_rn(hv[2], -hv[3])};
+                    __half2 q0[2] = {__floats2half2_rn(hv[0], hn1), __floats2half2_rn(hv[2], hn3)};
                     __half2 q1[2] = {__floats2half2_rn(hv[1], hv[0]), __floats2half2_rn(hv[3], hv[2])};
                     *reinterpret_cast<uint2*>(hp + r0) = *reinterpret_cast<uint2*>(q0);
                     *reinterpret_cast<uint2*>(hp + r1) = *reinterpret_cast<uint2*>(q1);
                     if (corrected) {
                         __half* lp = static_cast<__half*>(lo_v);
-                        __half2 w0[2] = {__floats2half2_rn(lv[0], -lv[1]), __floats2half2_rn(lv[2], -lv[3])};
+                        __half2 w0[2] = {__floats2half2_rn(lv[0], ln1), __floats2half2_rn(lv[2], ln3)};
                         __half2 w1[2] = {__floats2half2_rn(lv[1], lv[0]), __floats2half2_rn(lv[3], lv[2])};
                         *reinterpret_cast<uint2*>(lp + r0) = *reinterpret_cast<uint2*>(w0);
                         *reinterpret_cast<uint2*>(lp + r1) = *reinterpret_cast<uint2*>(w1);
                     }
                 } else {
                     float* hp = static_cast<float*>(hi_v);
-                    *reinterpret_cast<float4*>(hp + r0) = make_float4(hv[0], -hv[1], hv[2], -hv[3]);
+                    *reinterpret_cast<float4*>(hp + r0) = make_float4(hv[0], hn1, hv[2], hn3);
                     *reinterpret_cast<float4*>(hp + r1) = make_float4(hv[1], hv[0], hv[3], hv[2]);
                     if (corrected) {
                         float* lp = static_cast<float*>(lo_v);
-                        *reinterpret_cast<float4*>(lp + r0) = make_float4(lv[0], -lv[1], lv[2], -lv[3]);
+                        *reinterpret_cast<float4*>(lp + r0) = make_float4(lv[0], ln1, lv[2], ln3);
                         *reinterpret_cast<float4*>(lp + r1) = make_float4(lv[1], lv[0], lv[3], lv[2]);
                     }
                 }

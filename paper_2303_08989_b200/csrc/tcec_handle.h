@@ -61,6 +61,7 @@ struct tcec_handle_s {
     DispatchGraph graphs[8] = {};
     int n_graphs = 0, next_graph = 0;
 
+    void drop_graphs();
     void* workspace(size_t bytes);
     tcec::DevDecision* decisions(int slots);
     ~tcec_handle_s();
