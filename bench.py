@@ -1,23 +1,33 @@
 #!/usr/bin/env python
-"""bench.py -- TCEC CGEMM TFLOP/s (+ fidelity) on B200, BASELINE.json configs[1].
+"""bench.py -- TCEC CGEMM TFLOP/s (+ fidelity) and sliced RCS time on B200
+(BASELINE.json: "TCEC CGEMM TFLOP/s + fidelity; RCS contraction time at 1/2/4/8 GPUs").
 
-Workload (one "step"): one AUTO-0 dispatch_cgemm (precsel.cpp:225-322 semantics:
-device exponent statistics -> selection -> scale+split -> tcgen05 TCEC CGEMM ->
-descale) of the top of the configs[1] sweep, m = n = k = 16384, uniform(-1,1)
-complex64 inputs (synthetic; the selector picks FP16TCEC_SCALED, s = 15).
+Default line (one "step" = one AUTO-0 dispatch_cgemm of configs[1]'s top point,
+m = n = k = 16384, on the reference's own inputs -- Rng(1 + n), A then B,
+uniform_pm1f, experiments.cpp:76-83 -- with precsel.cpp:225-322 semantics:
+device exponent statistics -> selection -> scale+split -> tcgen05 TCEC CGEMM
+-> descale):
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-value   = useful 8mnk flops / device time (CUDA events on the handle stream), inputs
-          resident in HBM; N>1 runs N independent replicas (replicas only: the
-          standalone CGEMM does not shard) -> whole-job flops / max time.
-e2e     = the same through the host-buffer C-ABI entry point tcec_dispatch_cgemm_host
-          (H2D of A and B from pinned memory + dispatch + D2H of C inside the timed region).
-roofline= the dominant kernel (tcec_gemm_kernel<f16>), tensor-pipe flops 3 x 8mnk per
-          launch over its CUDA-event duration, against the measured dense bf16/fp16 peak.
-cpu_baseline / --impl reference = the reference's own kernels (oracle/_ref, the
-          unmodified mpsgemm sources) row-partitioned over all host threads on a bounded
-          row block of the same CGEMM.
+value      = useful 8mnk flops / device time (CUDA events on the handle stream), inputs
+             resident in HBM; N > 1 runs N replicas (the standalone CGEMM does not shard,
+             SURVEY.md 8(e)) -> whole-job flops / max-over-ranks time.  `--gpus N` outside
+             torchrun re-executes itself under torch.distributed.run (one rank per GPU).
+e2e        = the same through tcec_dispatch_cgemm_host (H2D of A and B + dispatch + D2H of C
+             inside the timed region), from pinned buffers and from pageable ones.
+roofline   = the dominant kernel (the tcgen05 TCEC GEMM), 3 x 8mnk tensor-pipe flops per
+             launch over its CUDA-event duration, against the measured dense bf16/fp16 peak.
+cpu_baseline / decision_parity = the unmodified reference (oracle/_ref) on the same operands:
+             its exp_stats_staged + select_mode over all of A and B give the decision line that
+             must equal the device's byte for byte (exit 3 otherwise), then its kernels on a
+             bounded row block over all host threads, extrapolated.
+sliced_rcs = configs[3]: Sycamore-class 53q m=12 amplitude, slices sharded round-robin over
+             the N ranks, one NCCL all_gather, slice-ordered f64 sum (every N).
+legs       = (N = 1) compact configs[0] (4x4 RQC, bit-identity to the reference), configs[2]
+             (skewed shapes, HBM-floor fractions), configs[4] (7x7 d16, AUTO vs FP32 tier
+             against the CPU FP64 oracle).
+--impl reference = the reference's own dispatch_cgemm on the same config (rank 0 only).
 """
 from __future__ import annotations
 
@@ -47,6 +57,21 @@ def peaks():
         d = json.load(open(p))
         return d["bf16_tflops"], d["bf16_tflops_sustained"], d["hbm_gbs"], "measured"
     return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+def tf32_peak():
+    """Dense TF32 peak for the TF32TCEC path: profiles/r02_tf32_peak.json
+    (tools/peak_tf32.py, cuBLAS TF32 8192^3 on this pool's B200s).  The burst
+    figure is used: the TCEC kernel, timed back to back inside the step, runs
+    above cuBLAS's sustained TF32 rate under the 1000 W cap, so the sustained
+    figure would not bound it.  Fallback: B200_PROFILING.md's 1.1 PF dense."""
+    p = os.path.join(ROOT, "profiles", "r02_tf32_peak.json")
+    if os.path.exists(p):
+        d = json.load(open(p))["tf32"]
+        return d["burst_tflops"], (f"measured dense TF32 burst {d['burst_tflops']} TFLOP/s (cuBLAS, "
+                                   f"profiles/r02_tf32_peak.json; its sustained figure is "
+                                   f"{d['sustained_tflops']})")
+    return 1100.0, "B200_PROFILING.md fallback: 1.1 PFLOP/s dense TF32"
 
 
 # ------------------------------------------------------------------ clocks
@@ -105,54 +130,61 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------- CPU reference
-def cpu_reference_sample(a_host, b_host, budget_s=10.0, threads=None, min_rows=None):
-    """The reference's own kernels on a row block of the same CGEMM, all host
-    threads (row partitioning is allowed by kernels.hpp:16-19 and bit-identical).
-    Returns (tflops, rows, seconds, threads, kind)."""
+def _ref_dispatch_fn():
+    """oracle/_ref's bridge onto the reference's own dispatch_cgemm selection +
+    row-partitioned kernels (ref_dispatch_rows_threaded_timed), or None."""
     import oracle as O
-    threads = threads or os.cpu_count() or 1
-    n = b_host.shape[1]
-    k = b_host.shape[0]
     ref = O.reference()
+    if ref is None:
+        return None, None
+    fn = ref.lib.ref_dispatch_rows_threaded_timed
+    fn.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                   C.c_int64, C.POINTER(O.ConfigPod), C.c_int, C.c_char_p, C.c_int,
+                   C.POINTER(C.c_int), C.POINTER(C.c_double)]
+    fn.restype = C.c_int
+    return fn, O
+
+
+def reference_dispatch_sample(a_host, b_host, rows, threads):
+    """The reference's dispatch_cgemm (precsel.cpp:225-322, default policy) on
+    the full operands -- exp_stats_staged of all of A and B, matrix_tolerance,
+    select_mode, DecisionRecord::to_line -- with the selected kind's CGEMM
+    timed on output rows [0, rows) over `threads` host threads (row
+    partitioning is bit-identical, kernels.hpp:16-19).  Returns
+    (decision line, [stats_s, prep_s, gemm_s]) or None without oracle/_ref."""
+    fn, O = _ref_dispatch_fn()
+    if fn is None:
+        return None
+    m, k = a_host.shape
+    n = b_host.shape[1]
+    c = np.empty((max(rows, 1), n), np.complex64)
+    line = C.create_string_buffer(256)
+    kind = C.c_int(0)
+    t = (C.c_double * 3)()
+    cfg = O.make_config()
+    rc = fn(a_host.ctypes.data, b_host.ctypes.data, c.ctypes.data, m, n, k, 0, rows, C.byref(cfg),
+            threads, line, 256, C.byref(kind), t)
+    if rc:
+        raise RuntimeError(f"reference dispatch failed (rc={rc})")
+    return line.value.decode(), [t[0], t[1], t[2]]
+
+
+def calibrate_rows(a_host, b_host, budget_s, threads):
+    """Rows of the bounded CPU sample: the row GEMM of `threads` rows timed
+    once, scaled to about budget_s of GEMM work."""
+    r = reference_dispatch_sample(a_host, b_host, threads, threads)
+    if r is None:
+        return None
+    per_row = r[1][2] / threads
     m = a_host.shape[0]
-    if ref is not None:
-        lib = ref.lib
-        fn = lib.ref_cgemm_rows_threaded_timed
-        fn.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
-                       C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int,
-                       C.POINTER(C.c_double), C.POINTER(C.c_double)]
-        kind = "reference"
-
-        def run(rows):
-            c = np.empty((rows, n), np.complex64)
-            prep, gemm = C.c_double(0), C.c_double(0)
-            fn(a_host.ctypes.data, b_host.ctypes.data, c.ctypes.data, m, n, k, 0, rows,
-               5, 16, threads, C.byref(prep), C.byref(gemm))  # GemmMode::fp16_tcec, k_tile 16
-            return prep.value, gemm.value
-    else:
-        o = O.oracle()
-        kind = "port"
-        threads = 1
-
-        def run(rows):
-            t0 = time.perf_counter()
-            o.cgemm(a_host[:rows], b_host, "FP16TCEC")
-            return 0.0, time.perf_counter() - t0
-    if min_rows is None:
-        _, g1 = run(max(1, threads))
-        per_row = g1 / max(1, threads)
-        rows = int(max(threads, min(m, budget_s / max(per_row, 1e-9))))
-        rows = max(threads, (rows // threads) * threads)
-    else:
-        rows = min_rows
-    prep, gemm = run(rows)
-    # the full CGEMM runs the O(n^2) preparation once and the row loop m/rows times
-    full_s = prep + gemm * m / rows
-    return 8.0 * m * n * k / full_s / 1e12, rows, prep + gemm, threads, kind, prep, gemm
+    rows = int(max(threads, min(m, budget_s / max(per_row, 1e-9))))
+    return max(threads, (rows // threads) * threads)
 
 
 # ---------------------------------------------------------------- helpers
-def dist_setup(gpus):
+def dist_setup(gpus=None):
+    """One process per GPU (RANK / LOCAL_RANK / WORLD_SIZE from torchrun);
+    idempotent so the legs of one run share the process group."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -160,8 +192,21 @@ def dist_setup(gpus):
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL's own log stays on (transport / NVLS lines), in files next to the run
+        logdir = os.path.join(ROOT, "gpurun_out")
+        os.makedirs(logdir, exist_ok=True)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", os.path.join(logdir, "nccl.%h.%p.log"))
+        if not dist.is_initialized():
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
+
+
+def dist_teardown(world):
+    if world > 1:
+        import torch.distributed as dist
+        if dist.is_initialized():
+            dist.destroy_process_group()
 
 
 def max_over_ranks(x, world):
@@ -180,30 +225,33 @@ def barrier(world):
         dist.barrier()
 
 
-def host_inputs(n, seed):
-    import torch
-    g = np.random.default_rng(seed)
-    pin = torch.cuda.is_available()
-    a = torch.empty((n, n), dtype=torch.complex64, pin_memory=pin)
-    b = torch.empty((n, n), dtype=torch.complex64, pin_memory=pin)
-    for t in (a, b):
-        v = t.numpy().view(np.float32)
-        for r0 in range(0, n, 1024):
-            v[r0:r0 + 1024] = g.random((min(1024, n - r0), 2 * n), dtype=np.float32) * 2 - 1
-    return a, b
+INPUTS_NOTE = ("reference inputs: one Rng(1 + n) (std::mt19937_64), A then B, two uniform_pm1f "
+               "draws per complex element (experiments.cpp:76-83, rng.hpp:35)")
+
+
+def workload_name(n):
+    return (f"configs[1] CGEMM sweep top: m=n=k={n}, AUTO-0 dispatch_cgemm (default "
+            f"SelectionPolicy: device statistics -> selection -> scale+split -> TCEC GEMM)")
+
+
+def host_inputs(n):
+    """configs[1] operands exactly as run_gemm_bench makes them (pinned host)."""
+    from paper_2303_08989_b200.workload import sweep_operands
+    return sweep_operands(n, seed=1)
 
 
 # ------------------------------------------------------------------- arms
-def run_ours(args):
+def cgemm_headline(args, world, rank, local):
+    """configs[1] top point on every rank (replicas); returns rank 0's line."""
     import torch
     from paper_2303_08989_b200 import Handle, make_config
-    world, rank, local = dist_setup(args.gpus)
-    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     n = args.n
     h = Handle(local)
     stream = torch.cuda.ExternalStream(h.stream_ptr, device=dev)
-    a_h, b_h = host_inputs(n, 1 + n + rank)
+    t_gen = time.perf_counter()
+    a_h, b_h = host_inputs(n)
+    t_gen = time.perf_counter() - t_gen
     a = a_h.to(dev)
     b = b_h.to(dev)
     c = torch.empty((n, n), dtype=torch.complex64, device=dev)
@@ -233,22 +281,33 @@ def run_ours(args):
     ms_max = max_over_ranks(ms, world)
     gemm_ms = stage["gemm"] / max(cnt, 1)
 
-    # ---- end to end through the host-buffer C-ABI
+    # ---- end to end through the host-buffer C-ABI (pinned, then pageable)
     a_np, b_np = a_h.numpy(), b_h.numpy()
     c_h = torch.empty((n, n), dtype=torch.complex64, pin_memory=True)
     c_np = c_h.numpy()
-    h.dispatch_cgemm_host(a_np, b_np, cfg, out=c_np)  # allocate staging once
-    barrier(world)
-    torch.cuda.synchronize(dev)
-    t0 = time.perf_counter()
-    e0.record(stream)
-    for _ in range(args.steps):
-        h.dispatch_cgemm_host(a_np, b_np, cfg, out=c_np)
-    e1.record(stream)
-    e1.synchronize()
-    e2e_ms = max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3) / args.steps
-    e2e_ms = max_over_ranks(e2e_ms, world)
+
+    def e2e_run(an, bn, cn, steps):
+        h.dispatch_cgemm_host(an, bn, cfg, out=cn)  # allocate staging once
+        barrier(world)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        e0.record(stream)
+        for _ in range(steps):
+            h.dispatch_cgemm_host(an, bn, cfg, out=cn)
+        e1.record(stream)
+        e1.synchronize()
+        return max_over_ranks(max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3) / steps,
+                              world)
+
+    e2e_ms = e2e_run(a_np, b_np, c_np, args.steps)
     pipe_runs, pipe_reruns = h.host_pipeline_stats()
+    e2e_pageable_ms = None
+    if args.pageable:
+        # the drop-in's std::vector storage is pageable: same call on plain numpy copies
+        a_pg, b_pg = np.array(a_np, copy=True), np.array(b_np, copy=True)
+        c_pg = np.empty_like(c_np)
+        e2e_pageable_ms = e2e_run(a_pg, b_pg, c_pg, max(2, args.steps // 2))
+        del a_pg, b_pg, c_pg
 
     # ---- fidelity: sampled rows vs complex128, and the bit-exact FP32 tier on the same rows
     rows = torch.from_numpy(np.random.default_rng(3).choice(n, 16, replace=False)).to(dev)
@@ -258,12 +317,13 @@ def run_ours(args):
     err32 = float(torch.linalg.norm(c32.to(torch.complex128) - ref) / torch.linalg.norm(ref))
     del ref
 
-    # ---- small sweep (configs[1] 1024..8192), AUTO and forced formats
-    sweep = {}
+    # ---- small sweep (configs[1] 1024..8192 on the reference inputs), AUTO and forced formats
+    sweep, sweep_ops = {}, {}
     if args.sweep and rank == 0:
         for sn in (1024, 2048, 4096, 8192):
-            sa = torch.rand(sn, sn, 2, device=dev).mul_(2).sub_(1).view(torch.complex64)[..., 0].contiguous()
-            sb = torch.rand(sn, sn, 2, device=dev).mul_(2).sub_(1).view(torch.complex64)[..., 0].contiguous()
+            sa_h, sb_h = host_inputs(sn)
+            sweep_ops[sn] = (sa_h.numpy(), sb_h.numpy())
+            sa, sb = sa_h.to(dev), sb_h.to(dev)
             sc = torch.empty(sn, sn, dtype=torch.complex64, device=dev)
             row = {}
             for label, sc_cfg in (("AUTO-0", make_config()), ("FP16TCEC", make_config(force="FP16TCEC")),
@@ -280,58 +340,82 @@ def run_ours(args):
                 e1.synchronize()
                 row[label] = round(8.0 * sn ** 3 / (e0.elapsed_time(e1) / reps * 1e-3) / 1e12, 2)
                 if label == "AUTO-0":
-                    row["AUTO-0 mode"] = r.line.split(",")[3]
+                    row["AUTO-0 decision"] = r.line
             sweep[str(sn)] = row
             del sa, sb, sc
 
-    # ---- CPU baseline (rank 0, N=1 only)
-    cpu = None
+    # ---- CPU baseline (rank 0, N=1 only): the reference's own dispatch on the
+    # same operands -- its decision line must equal the device's byte for byte
+    cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu:
-        tf, r_rows, dt, thr, kindc, prep, gemm = cpu_reference_sample(a_np, b_np,
-                                                                     budget_s=args.cpu_budget)
-        cpu = {"value": round(tf, 6), "unit": "TFLOP/s", "cores": thr, "kind": kindc,
-               "sample": f"rows 0..{r_rows} of the same m=n=k={n} CGEMM with the reference's "
-                         f"FP16TCEC kernels on {thr} threads: operand prep {prep:.1f} s + row "
-                         f"GEMM {gemm:.1f} s, extrapolated to all {n} rows (prep once)"}
+        thr = os.cpu_count() or 1
+        rows_s = calibrate_rows(a_np, b_np, args.cpu_budget, thr)
+        if rows_s is not None:
+            ref_line, (st_s, prep_s, gemm_s) = reference_dispatch_sample(a_np, b_np, rows_s, thr)
+            full_s = st_s + prep_s + gemm_s * n / rows_s
+            parity = {str(n): {"reference": ref_line, "device": decision,
+                               "identical": ref_line == decision}}
+            for sn, (sa_np, sb_np) in sweep_ops.items():
+                rl, _ = reference_dispatch_sample(sa_np, sb_np, 0, thr)
+                parity[str(sn)] = {"reference": rl, "device": sweep[str(sn)]["AUTO-0 decision"],
+                                   "identical": rl == sweep[str(sn)]["AUTO-0 decision"]}
+            cpu = {"value": round(flops / full_s / 1e12, 6), "unit": "TFLOP/s", "cores": thr,
+                   "kind": "reference",
+                   "sample": f"the reference's dispatch_cgemm on the same operands: exp_stats_staged "
+                             f"+ select_mode over all of A and B ({st_s:.1f} s), scale+split "
+                             f"({prep_s:.1f} s), {kind} rows 0..{rows_s} with its kernels on {thr} "
+                             f"threads ({gemm_s:.1f} s), row GEMM extrapolated to all {n} rows"}
+    del sweep_ops
 
+    line = None
     if rank == 0:
         bpk, bps, hbm, src = peaks()
         tensor_flops = 3.0 * flops  # hi*hi, lo*hi, hi*lo tensor-core products per launch
         achieved = tensor_flops / (gemm_ms * 1e-3) / 1e12
-        peak = bps if kind != "TF32TCEC" else bps / 2
+        tf32 = kind == "TF32TCEC"
+        if tf32:
+            peak, psrc = tf32_peak()
+        else:
+            peak, psrc = bps, f"{src} dense bf16 sustained (MEASURED_PEAKS.json; fp16 = bf16 rate)"
         traffic = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tp):
-            traffic = json.load(open(tp)).get(f"tcec_gemm_f16_n{n}")
+            traffic = json.load(open(tp)).get(f"tcec_gemm_{'tf32' if tf32 else 'f16'}_n{n}")
         value = world * flops / (ms_max * 1e-3) / 1e12
+        e2e = {"value": round(world * flops / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
+               "h2d_bytes_per_step": 2 * n * n * 8, "d2h_bytes_per_step": n * n * 8,
+               "host_buffers": "pinned",
+               "pipeline": {"runs": pipe_runs, "reruns": pipe_reruns,
+                            "note": "H2D of B column parts / A row chunks overlapped with the GEMM "
+                                    "blocks under a decision from the first parts, checked against "
+                                    "the exact one (reruns = recomputed on disagreement)"}}
+        if e2e_pageable_ms:
+            e2e["pageable"] = {"value": round(world * flops / (e2e_pageable_ms * 1e-3) / 1e12, 2),
+                               "unit": "TFLOP/s",
+                               "note": "same call from pageable numpy buffers (the C++ drop-in's "
+                                       "std::vector storage): staged through a pinned ring"}
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 3),
             "higher_is_better": True, "scaling": "weak",
             "vs_baseline": round(value / PAPER_A100_FP16TCEC, 2),
             "baseline_ref": "54.2 TFLOP/s FP16TCEC CGEMM max on A100 (PAPER.md:246)",
-            "dtype": "c64 (FP32 via error-corrected FP16 tensor cores)",
-            "data": "synthetic uniform(-1,1) complex64 (numpy default_rng), resident in HBM",
-            "config": {"workload": f"configs[1] CGEMM sweep top: m=n=k={n}, AUTO-0 "
-                                   f"(default SelectionPolicy) -> {kind}",
-                       "decision": decision, "parallelism": f"replicas x{world}",
-                       "l2": "inputs (2 GiB per operand) exceed the 126 MB L2",
-                       "flush_kblocks": h.flush_kblocks},
+            "dtype": "c64 (FP32-level via error-corrected FP16 products)",
+            "data": "synthetic, the reference's own generator, resident in HBM",
+            "config": {"workload": workload_name(n), "decision": decision, "inputs": INPUTS_NOTE},
+            "parallelism": f"replicas x{world} (the standalone CGEMM does not shard, SURVEY 8(e))",
+            "l2": "inputs (2 GiB per operand) exceed the 126 MB L2",
+            "flush_kblocks": h.flush_kblocks, "input_generation_s": round(t_gen, 2),
             "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "kernel": gemm_kernel_name(n, n, kind),
                          "note": f"3 x 8mnk tensor-pipe flops per launch / CUDA-event time; "
-                                 f"peak = {src} dense bf16 sustained (fp16 = bf16 rate)"},
+                                 f"peak = {psrc}"},
             "stages_ms": {k2: round(v / max(cnt, 1), 3) for k2, v in stage.items()},
             "fidelity": {"rel_err": err, "fp32_ref_rel_err": err32,
                          "ratio_vs_fp32": round(err / err32, 3) if err32 else None,
                          "sample": "16 random rows vs complex128"},
-            "e2e": {"value": round(world * flops / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
-                    "h2d_bytes_per_step": 2 * n * n * 8, "d2h_bytes_per_step": n * n * 8,
-                    "pipeline": {"runs": pipe_runs, "reruns": pipe_reruns,
-                                 "note": "H2D of B column parts / A row chunks overlapped with the GEMM "
-                                         "blocks under a decision from the first parts, checked against "
-                                         "the exact one (reruns = recomputed on disagreement)"}},
+            "e2e": e2e,
             # per AUTO dispatch: stats1, stats2, select, prep_a, prep_b and ONE
             # tcgen05 GEMM (the wide kernel branches on the device decision),
             # plus a cudaMemsetAsync of the decision slot
@@ -340,49 +424,96 @@ def run_ours(args):
         }
         if cpu:
             line["cpu_baseline"] = cpu
+        if parity:
+            line["decision_parity"] = parity
         if sweep:
             line["sweep_tflops"] = sweep
-        print(json.dumps(line), flush=True)
     h.close()
-    if world > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
+    del a, b, c
+    torch.cuda.empty_cache()
+    return line
+
+
+def run_ours(args):
+    """The default line: the configs[1] headline (replicas over the ranks),
+    the sliced Sycamore-class RCS (configs[3], slices sharded over the ranks,
+    one NCCL all_gather) and, at N = 1, compact legs of configs[0], [2], [4]."""
+    world, rank, local = dist_setup(args.gpus)
+    line = cgemm_headline(args, world, rank, local)
+    syc = None
+    if args.sliced:
+        sub = argparse.Namespace(**vars(args))
+        sub.steps, sub.warmup = args.sliced_steps, 3
+        syc = run_sycamore(sub, emit=False)
+    legs = {}
+    if world == 1 and args.legs:
+        sub = argparse.Namespace(**vars(args))
+        sub.steps, sub.warmup = 5, 3
+        for name, fn in (("configs[0]_rqc4x4", run_rqc), ("configs[2]_skewed", run_skewed),
+                         ("configs[4]_rqc7x7_d16", run_rqc7x7_leg)):
+            t0 = time.perf_counter()
+            try:
+                legs[name] = fn(sub, emit=False)
+            except Exception as e:  # a leg must not take the headline down
+                legs[name] = {"error": f"{type(e).__name__}: {e}"}
+            if isinstance(legs[name], dict):
+                legs[name]["leg_s"] = round(time.perf_counter() - t0, 1)
+    if rank == 0:
+        if syc:
+            line["sliced_rcs"] = syc
+        if legs:
+            line["legs"] = legs
+        print(json.dumps(line), flush=True)
+    dist_teardown(world)
+    if rank == 0 and line.get("decision_parity"):
+        bad = [k for k, v in line["decision_parity"].items() if not v["identical"]]
+        if bad:
+            print(f"DECISION PARITY FAILED for n = {bad}", file=sys.stderr, flush=True)
+            sys.exit(3)
 
 
 def run_reference(args):
+    """The reference's own CPU path on the same config: its dispatch_cgemm
+    (statistics + selection over all of A and B, then the selected kind) on
+    the same inputs, the row GEMM timed on a bounded row block over all host
+    threads and extrapolated.  Rank 0 only."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import torch  # noqa: F401  (pinned inputs share the generator with our arm)
     n = args.n
-    a_h, b_h = host_inputs(n, 1 + n)
+    a_h, b_h = host_inputs(n)
     a_np, b_np = a_h.numpy(), b_h.numpy()
-    # calibrate the bounded per-step sample once, then warm up and time
-    _, rows, _, thr, kind, _, _ = cpu_reference_sample(a_np, b_np, budget_s=args.ref_step_s)
+    thr = os.cpu_count() or 1
+    rows = calibrate_rows(a_np, b_np, args.ref_step_s, thr)
+    if rows is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref (the reference build) "
+                          "is missing on this machine"}), flush=True)
+        return
     for _ in range(args.warmup):
-        cpu_reference_sample(a_np, b_np, min_rows=rows)
-    vals, wall = [], 0.0
+        reference_dispatch_sample(a_np, b_np, rows, thr)
+    vals, wall, ref_line = [], 0.0, None
     for _ in range(args.steps):
-        tf, _, dt, _, _, _, _ = cpu_reference_sample(a_np, b_np, min_rows=rows)
-        vals.append(tf)
-        wall += dt
-    value = float(np.mean(vals))
-    ms = 8.0 * n * n * n / (value * 1e12) * 1e3  # full-CGEMM time implied by the sample
+        t0 = time.perf_counter()
+        ref_line, (st_s, prep_s, gemm_s) = reference_dispatch_sample(a_np, b_np, rows, thr)
+        wall += time.perf_counter() - t0
+        vals.append(st_s + prep_s + gemm_s * n / rows)
+    full_s = float(np.mean(vals))
+    value = 8.0 * n * n * n / full_s / 1e12
+    kind = ref_line.split(",")[3]
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "TFLOP/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 1),
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(full_s * 1e3, 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "c64 (FP32 via error-corrected FP16 emulation, reference CPU)",
-        "data": "synthetic uniform(-1,1) complex64",
-        "config": {"workload": f"configs[1] CGEMM sweep top: m=n=k={n}, AUTO-0 -> FP16TCEC_SCALED",
-                   "parallelism": "host threads"},
-        "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": thr, "kind": kind,
-                         "sample": f"{rows} rows of the m=n=k={n} CGEMM per step (FP16TCEC "
-                                   f"kernels of the unmodified reference, row-partitioned over "
-                                   f"{thr} threads; O(n^2) operand prep timed per step and "
-                                   f"amortized over the full {n} rows); {wall / args.steps:.1f} s "
-                                   f"wall per step"},
+        "dtype": "c64 (FP32-level via error-corrected FP16 products)",
+        "data": "synthetic, the reference's own generator, resident in HBM",
+        "config": {"workload": workload_name(n), "decision": ref_line, "inputs": INPUTS_NOTE},
+        "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": thr, "kind": "reference",
+                         "sample": f"per step: the unmodified reference's dispatch_cgemm selection "
+                                   f"(exp_stats_staged + matrix_tolerance + select_mode over all of "
+                                   f"A and B), then {kind} on rows 0..{rows} of C with its kernels "
+                                   f"over {thr} threads; the row GEMM extrapolated to all {n} rows "
+                                   f"({wall / args.steps:.1f} s wall per step)"},
         "e2e": {"value": round(value, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -453,7 +584,7 @@ def statevector_c128(circuit, dev):
     return st
 
 
-def run_rqc(args):
+def run_rqc(args, emit=True):
     """configs[0]: 4x4 rectangular RQC, H + 8 CZ layers + H, every output amplitude."""
     import torch
     from paper_2303_08989_b200 import Handle, make_config
@@ -558,9 +689,12 @@ def run_rqc(args):
         }
         if cpu:
             line["cpu_baseline"] = cpu
-        print(json.dumps(line), flush=True)
+        if emit:
+            print(json.dumps(line), flush=True)
     net.close()
     h.close()
+    if not emit:
+        return _compact_leg(line) if rank == 0 else None
 
 
 SYC_METRIC = "Sycamore-class 53q sliced RCS amplitudes/s (AUTO-0)"
@@ -587,7 +721,7 @@ def load_or_build_plan(spec, cycles, mode, log=None):
     return path, sliced, "hyper (searched)"
 
 
-def run_sycamore(args):
+def run_sycamore(args, emit=True):
     """configs[3]: 53-qubit Sycamore-layout fSim circuit (m cycles), sliced
     contraction plan (presimplify + partition tree + reconfiguration + exact
     slicing, paths.hyper_path), slices sharded round-robin over the ranks, one
@@ -670,12 +804,15 @@ def run_sycamore(args):
             "amplitude": [float(amp.real), float(amp.imag)],
             "fidelity": fid, "clocks": clk.summary(),
         }
-        print(json.dumps(line), flush=True)
+        if emit:
+            print(json.dumps(line), flush=True)
     net.close()
     h.close()
-    if world > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
+    torch.cuda.empty_cache()
+    if emit:
+        dist_teardown(world)
+        return None
+    return _compact_leg(line) if rank == 0 else None
 
 
 SKEWED_SHAPES = [(2048, 16384, 64), (512, 16384, 512), (512, 8192, 1024), (1024, 4096, 8192),
@@ -696,7 +833,7 @@ def type3_device(rows, cols, gen, dev):
     return v.view(torch.complex64)[..., 0].contiguous()
 
 
-def run_skewed(args):
+def run_skewed(args, emit=True):
     """configs[2]: contraction-shaped skewed CGEMMs (tall-skinny, small k) with a wide
     exponent range forcing the TF32TCEC fallback (policy size_auto = size_tf32 =
     min(m, n, k) so the statistics engage), plus the paper's irregular
@@ -767,8 +904,11 @@ def run_skewed(args):
                            "timing": "device time of stats+prep+gemm stages (CUDA events)",
                            "parallelism": f"replicas x{world}"},
                 "shapes": rows_out, "hbm_peak_gbs": hbm, "clocks": clk.summary()}
-        print(json.dumps(line), flush=True)
+        if emit:
+            print(json.dumps(line), flush=True)
     h.close()
+    if not emit:
+        return _compact_leg(line) if rank == 0 else None
 
 
 def contract_c128(spec, path, dev):
@@ -791,6 +931,84 @@ def contract_c128(spec, path, dev):
         nxt += 1
     (_, t), = live.values()
     return complex(t.reshape(-1)[0].item())
+
+
+def _compact_leg(line):
+    """A sub-workload's JSON line without the per-run boilerplate."""
+    if not line:
+        return None
+    drop = {"steps", "warmup", "higher_is_better", "vs_baseline", "n_gpus", "clocks", "dtype", "data",
+            "hbm_peak_gbs"}
+    out = {k: v for k, v in line.items() if k not in drop}
+    if "shapes" in out:
+        out["shapes"] = [{k: r[k] for k in ("m", "n", "k", "inputs", "mode", "ms", "tflops",
+                                            "floor_frac_hbm", "rel_err", "fp32_ref_rel_err") if k in r}
+                         for r in out["shapes"]]
+    return out
+
+
+def run_rqc7x7_leg(args, emit=False):
+    """configs[4] deep point (7x7, depth 16) on the reference's greedy path:
+    AUTO-0 vs the FP32 baseline tier per amplitude, errors against the CPU
+    FP64 contraction oracle (contract_network_oracle, network.cpp:179-186) of
+    the same path and bitstrings (the checker, timed on the host)."""
+    import torch
+    from paper_2303_08989_b200 import Handle, make_config
+    from paper_2303_08989_b200.circuits import bitstrings_for, circuit_to_network, rqc_rectangular
+    from paper_2303_08989_b200.network import Network
+    from paper_2303_08989_b200.slicing import contraction_cost
+    world, rank, local = dist_setup(args.gpus)
+    if rank != 0:
+        return None
+    dev = torch.device("cuda", local)
+    h = Handle(local)
+    depth, nb = 16, 3
+    circ = rqc_rectangular(7, 7, depth, 1)
+    xs = bitstrings_for(49, 10, 1)[:nb]  # experiments.cpp:185-196
+    spec = circuit_to_network(circ, xs[0])
+    net = Network(h, spec)
+    path = net.greedy_path()
+    big, macs = contraction_cost(spec, path)
+    out = {"metric": "7x7 RQC depth-16 amplitude time (reference greedy path)", "unit": "ms/amplitude",
+           "steps_per_amplitude": len(path), "gflop_per_amplitude": round(8.0 * macs / 1e9, 1),
+           "max_intermediate": int(big), "bitstrings": nb, "modes": {}}
+    amps_by = {}
+    for label, cfg in (("AUTO-0", make_config()), ("FP32_BASELINE", make_config(force="FP32_REF"))):
+        net.selector_batch(path, xs, cfg)  # capture / warm
+        torch.cuda.synchronize(dev)
+        h.profile(True)
+        t0 = time.perf_counter()
+        reps = 2
+        for _ in range(reps):
+            amps = net.selector_batch(path, xs, cfg)
+        e2e = (time.perf_counter() - t0) / (reps * nb) * 1e3
+        dev_ms, _ = h.profile_read_batches()
+        h.profile(False)
+        amps_by[label] = amps.astype(np.complex128)
+        out["modes"][label] = {"ms_per_amplitude": round(dev_ms / (reps * nb), 3),
+                               "e2e_ms_per_amplitude": round(e2e, 3)}
+    net.close()
+    h.close()
+    out["value"] = out["modes"]["AUTO-0"]["ms_per_amplitude"]
+    out["auto_speedup_vs_fp32_baseline"] = round(out["modes"]["FP32_BASELINE"]["ms_per_amplitude"]
+                                                 / out["value"], 3)
+    if not args.no_cpu:
+        from oracle.network import contract_network_f64  # CPU checker (reference restatement)
+        t0 = time.perf_counter()
+        zref = np.array([complex(contract_network_f64(circuit_to_network(circ, x), path)[2].reshape(-1)[0])
+                         for x in xs])
+        for label, amps in amps_by.items():
+            err = np.abs(amps - zref) / np.abs(zref)
+            out["modes"][label]["median_rel_err_vs_cpu_f64"] = float(np.median(err))
+            out["modes"][label]["max_rel_err_vs_cpu_f64"] = float(np.max(err))
+        fa = out["modes"]["FP32_BASELINE"]["median_rel_err_vs_cpu_f64"]
+        out["auto_err_ratio_vs_fp32_baseline"] = (round(out["modes"]["AUTO-0"]["median_rel_err_vs_cpu_f64"]
+                                                        / fa, 3) if fa else None)
+        out["cpu_baseline"] = {"kind": "port", "cores": os.cpu_count() or 1,
+                               "reference_s": round(time.perf_counter() - t0, 1),
+                               "sample": f"FP64 contract_network_oracle (oracle/network.py restatement of "
+                                         f"network.cpp:179-186, numpy) of the same path for {nb} bitstrings"}
+    return out
 
 
 def run_rqc7x7(args):
@@ -959,6 +1177,25 @@ def gemm_kernel_name(m, n, kind, sm_count=148, auto=True):
     return f"tcec_gemm_kernel<{fmt}>"
 
 
+def spawn_ranks(gpus):
+    """`python bench.py --gpus N` outside torchrun: re-exec this command under
+    torch.distributed.run with N local ranks (one process per GPU, NCCL,
+    rendezvous on 127.0.0.1) and return its exit code."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # NCCL's own log (NVLS / NVLink transport lines)
+    logdir = os.path.join(ROOT, "gpurun_out")
+    os.makedirs(logdir, exist_ok=True)
+    env.setdefault("NCCL_DEBUG_FILE", os.path.join(logdir, "nccl.%h.%p.log"))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)]
+    cmd += sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--workload", choices=["cgemm", "rqc", "sycamore", "skewed", "rqc7x7"], default="cgemm")
@@ -974,11 +1211,23 @@ def main():
     p.add_argument("--n", type=int, default=N_DEFAULT)
     p.add_argument("--no-sweep", dest="sweep", action="store_false")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-sliced", dest="sliced", action="store_false",
+                   help="skip the sliced Sycamore-class RCS object of the default line")
+    p.add_argument("--sliced-steps", type=int, default=3)
+    p.add_argument("--no-legs", dest="legs", action="store_false",
+                   help="skip the configs[0]/[2]/[4] legs of the default line (N = 1)")
+    p.add_argument("--no-pageable", dest="pageable", action="store_false")
     p.add_argument("--cpu-budget", type=float, default=12.0)
     p.add_argument("--ref-step-s", type=float, default=8.0)
     args = p.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
+    if args.impl == "reference" and args.workload in ("sycamore", "skewed", "rqc7x7"):
+        print(json.dumps({"impl": "reference", "unavailable":
+                          f"the reference has no {args.workload} CPU arm beyond the default line"}))
+        return
     if args.workload == "rqc":
         run_rqc(args)
     elif args.workload == "sycamore":

@@ -19,14 +19,21 @@ p.add_argument("--k", type=int, default=0)
 p.add_argument("--mode", default="AUTO")
 p.add_argument("--flush", type=int, default=-1)
 p.add_argument("--reps", type=int, default=3)
+p.add_argument("--ref-inputs", action="store_true",
+               help="configs[1] operands from the reference generator Rng(1 + n) (square only)")
 a = p.parse_args()
 m, n, k = a.m or a.n, a.n, a.k or a.n
 dev = torch.device("cuda:0")
 h = Handle(0)
 if a.flush >= 0:
     h.flush_kblocks = a.flush
-A = (torch.rand(m, k, 2, device=dev) * 2 - 1).view(torch.complex64)[..., 0].contiguous()
-B = (torch.rand(k, n, 2, device=dev) * 2 - 1).view(torch.complex64)[..., 0].contiguous()
+if a.ref_inputs:
+    from paper_2303_08989_b200.workload import sweep_operands
+    Ah, Bh = sweep_operands(n, m=m, k=k)
+    A, B = Ah.to(dev), Bh.to(dev)
+else:
+    A = (torch.rand(m, k, 2, device=dev) * 2 - 1).view(torch.complex64)[..., 0].contiguous()
+    B = (torch.rand(k, n, 2, device=dev) * 2 - 1).view(torch.complex64)[..., 0].contiguous()
 C = torch.empty(m, n, dtype=torch.complex64, device=dev)
 cfg = make_config() if a.mode == "AUTO" else make_config(force=a.mode)
 for _ in range(a.reps):
