@@ -125,6 +125,9 @@ class _Backend:
         getattr(L, p + "dispatch_cgemm").argtypes = [fp, fp, fp, i64, i64, i64,
                                                      C.POINTER(ConfigPod), C.POINTER(ResultPod)]
         getattr(L, p + "permute_c64").argtypes = [fp, fp, i32, C.POINTER(i64), ip]
+        if p == "orc_":
+            L.orc_dispatch_decision.argtypes = [fp, fp, i64, i64, i64, C.POINTER(ConfigPod),
+                                                C.POINTER(ResultPod)]
 
     # --- lowprec / kernel table -------------------------------------------------
     def quantize_buf(self, x, fmt, rounding=RN):
@@ -232,6 +235,18 @@ class _Backend:
                                       _fp(c.view(np.float32)), m, n, k, C.byref(cfg),
                                       C.byref(res))
         return rc, c, res
+
+    def dispatch_decision(self, a, b, cfg: ConfigPod):
+        """The selection half of dispatch_cgemm (oracle only): statistics,
+        ComputeMode and the DecisionRecord line, no GEMM."""
+        a = np.ascontiguousarray(a, dtype=np.complex64)
+        b = np.ascontiguousarray(b, dtype=np.complex64)
+        m, k = a.shape
+        n = b.shape[1]
+        res = ResultPod()
+        rc = self.lib.orc_dispatch_decision(_fp(a.view(np.float32)), _fp(b.view(np.float32)), m, n, k,
+                                            C.byref(cfg), C.byref(res))
+        return rc, res
 
     def permute(self, t, axis_of):
         t = np.ascontiguousarray(t, dtype=np.complex64)

@@ -470,8 +470,9 @@ static int run_scaled(const float* a, const float* b, float* c, int64_t m, int64
     return 0;
 }
 
-int orc_dispatch_cgemm(const float* a, const float* b, float* c, int64_t m, int64_t n, int64_t k,
-                       const orc_dispatch_config_t* cfg, orc_dispatch_result_t* res) {
+/* compute == 0: the selection half only (statistics, decision, log line), C untouched */
+static int dispatch_impl(const float* a, const float* b, float* c, int64_t m, int64_t n, int64_t k,
+                         const orc_dispatch_config_t* cfg, orc_dispatch_result_t* res, int compute) {
     /* precsel.cpp:225-322 */
     memset(res, 0, sizeof(*res));
     const int target = cfg->target_max_exponent;
@@ -484,17 +485,17 @@ int orc_dispatch_cgemm(const float* a, const float* b, float* c, int64_t m, int6
     if (cfg->force >= 0) {
         label = forced_name(cfg->force);
         switch (cfg->force) {
-        case 0: rc = orc_cgemm(a, b, c, m, n, k, ORC_MODE_FP32_REF, kt, &res->overflow);
+        case 0: rc = !compute ? 0 : orc_cgemm(a, b, c, m, n, k, ORC_MODE_FP32_REF, kt, &res->overflow);
                 res->kind = ORC_KIND_FP32_BASELINE; break;
-        case 1: rc = orc_cgemm(a, b, c, m, n, k, ORC_MODE_FP64_ORACLE, kt, &res->overflow);
+        case 1: rc = !compute ? 0 : orc_cgemm(a, b, c, m, n, k, ORC_MODE_FP64_ORACLE, kt, &res->overflow);
                 res->kind = ORC_KIND_FP32_BASELINE; break;
-        case 2: rc = orc_cgemm(a, b, c, m, n, k, ORC_MODE_TF32_TC, kt, &res->overflow);
+        case 2: rc = !compute ? 0 : orc_cgemm(a, b, c, m, n, k, ORC_MODE_TF32_TC, kt, &res->overflow);
                 res->kind = ORC_KIND_TF32_TCEC; break;
-        case 3: rc = orc_cgemm(a, b, c, m, n, k, ORC_MODE_FP16_TC, kt, &res->overflow);
+        case 3: rc = !compute ? 0 : orc_cgemm(a, b, c, m, n, k, ORC_MODE_FP16_TC, kt, &res->overflow);
                 res->kind = ORC_KIND_FP16_TCEC; break;
-        case 4: rc = orc_cgemm(a, b, c, m, n, k, ORC_MODE_TF32_TCEC, kt, &res->overflow);
+        case 4: rc = !compute ? 0 : orc_cgemm(a, b, c, m, n, k, ORC_MODE_TF32_TCEC, kt, &res->overflow);
                 res->kind = ORC_KIND_TF32_TCEC; break;
-        case 5: rc = orc_cgemm(a, b, c, m, n, k, ORC_MODE_FP16_TCEC, kt, &res->overflow);
+        case 5: rc = !compute ? 0 : orc_cgemm(a, b, c, m, n, k, ORC_MODE_FP16_TCEC, kt, &res->overflow);
                 res->kind = ORC_KIND_FP16_TCEC; break;
         case 6: {
             orc_exp_stats_staged(a, 2 * m * k, target, 1.0, &res->stats_a);
@@ -502,7 +503,7 @@ int orc_dispatch_cgemm(const float* a, const float* b, float* c, int64_t m, int6
             res->has_stats = 1;
             res->scale_a = res->stats_a.e_max_valid ? target - res->stats_a.e_max : 0;
             res->scale_b = res->stats_b.e_max_valid ? target - res->stats_b.e_max : 0;
-            rc = run_scaled(a, b, c, m, n, k, res->scale_a, res->scale_b, kt, &res->overflow);
+            rc = !compute ? 0 : run_scaled(a, b, c, m, n, k, res->scale_a, res->scale_b, kt, &res->overflow);
             res->kind = ORC_KIND_FP16_TCEC_SCALED;
             break;
         }
@@ -521,23 +522,23 @@ int orc_dispatch_cgemm(const float* a, const float* b, float* c, int64_t m, int6
         label = kind_name(res->kind);
         switch (res->kind) {
         case ORC_KIND_FP16_TCEC:
-            rc = orc_cgemm(a, b, c, m, n, k, ORC_MODE_FP16_TCEC, kt, &res->overflow); break;
+            rc = !compute ? 0 : orc_cgemm(a, b, c, m, n, k, ORC_MODE_FP16_TCEC, kt, &res->overflow); break;
         case ORC_KIND_TF32_TCEC:
-            rc = orc_cgemm(a, b, c, m, n, k, ORC_MODE_TF32_TCEC, kt, &res->overflow); break;
+            rc = !compute ? 0 : orc_cgemm(a, b, c, m, n, k, ORC_MODE_TF32_TCEC, kt, &res->overflow); break;
         case ORC_KIND_FP16_TCEC_SCALED:
-            rc = run_scaled(a, b, c, m, n, k, res->scale_a, res->scale_b, kt, &res->overflow);
+            rc = !compute ? 0 : run_scaled(a, b, c, m, n, k, res->scale_a, res->scale_b, kt, &res->overflow);
             break;
         default:
-            rc = orc_cgemm(a, b, c, m, n, k, ORC_MODE_FP32_REF, kt, &res->overflow); break;
+            rc = !compute ? 0 : orc_cgemm(a, b, c, m, n, k, ORC_MODE_FP32_REF, kt, &res->overflow); break;
         }
     } else if (mn >= cfg->size_tf32) {
         res->kind = ORC_KIND_TF32_TCEC;
         label = kind_name(res->kind);
-        rc = orc_cgemm(a, b, c, m, n, k, ORC_MODE_TF32_TCEC, kt, &res->overflow);
+        rc = !compute ? 0 : orc_cgemm(a, b, c, m, n, k, ORC_MODE_TF32_TCEC, kt, &res->overflow);
     } else {
         res->kind = ORC_KIND_FP32_BASELINE;
         label = kind_name(res->kind);
-        rc = orc_cgemm(a, b, c, m, n, k, ORC_MODE_FP32_REF, kt, &res->overflow);
+        rc = !compute ? 0 : orc_cgemm(a, b, c, m, n, k, ORC_MODE_FP32_REF, kt, &res->overflow);
     }
     if (rc) return rc;
 
@@ -553,6 +554,17 @@ int orc_dispatch_cgemm(const float* a, const float* b, float* c, int64_t m, int6
              (long long)m, (long long)n, (long long)k, label, res->scale_a, res->scale_b, r1a, r2a,
              r1b, r2b, ea, eb);
     return 0;
+}
+
+int orc_dispatch_cgemm(const float* a, const float* b, float* c, int64_t m, int64_t n, int64_t k,
+                       const orc_dispatch_config_t* cfg, orc_dispatch_result_t* res) {
+    return dispatch_impl(a, b, c, m, n, k, cfg, res, 1);
+}
+
+/* the decision of dispatch_cgemm (stats, selection, DecisionRecord line) without the GEMM */
+int orc_dispatch_decision(const float* a, const float* b, int64_t m, int64_t n, int64_t k,
+                          const orc_dispatch_config_t* cfg, orc_dispatch_result_t* res) {
+    return dispatch_impl(a, b, NULL, m, n, k, cfg, res, 0);
 }
 
 /* ------------------------------------------------------------------ permute */

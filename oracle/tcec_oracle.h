@@ -124,6 +124,9 @@ typedef struct {
 
 int orc_dispatch_cgemm(const float* a, const float* b, float* c, int64_t m, int64_t n, int64_t k,
                        const orc_dispatch_config_t* cfg, orc_dispatch_result_t* res);
+/* the selection half of dispatch_cgemm only (statistics, ComputeMode, line) */
+int orc_dispatch_decision(const float* a, const float* b, int64_t m, int64_t n, int64_t k,
+                          const orc_dispatch_config_t* cfg, orc_dispatch_result_t* res);
 
 /* tensor.hpp:56-105 -- permute of complex (8-byte) elements.  axis_of[a] is
  * the old axis feeding new axis a; dims are the OLD dims. */

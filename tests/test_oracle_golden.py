@@ -210,3 +210,36 @@ def test_network_oracle_matches_reference_amplitudes(golden, case):
         assert abs(complex(z64[0]) - complex(*row["tn_oracle"])) <= 1e-12 * max(abs(complex(*row["tn_oracle"])), 1e-30)
         sv = amplitude_sv(c, row["x"])
         assert abs(sv - complex(*row["sv_oracle"])) <= 1e-12
+
+
+def test_workload_generator_is_the_reference_rng():
+    """paper_2303_08989_b200.workload (the bench's configs[1] inputs) draws the
+    same stream as rng.hpp's Rng: pinned against the oracle restatement and,
+    where it is built, the reference's own ref_gemm_bench_operands."""
+    import ctypes as C
+
+    import oracle as O
+    from paper_2303_08989_b200.workload import WorkloadRng, sweep_operands
+    a, b = sweep_operands(96, pinned=False, m=40, k=72)
+    r = O.Rng(1 + 96)
+    assert np.array_equal(a.numpy().view(np.uint32), r.uniform_c32(40, 72).view(np.uint32))
+    assert np.array_equal(b.numpy().view(np.uint32), r.uniform_c32(72, 96).view(np.uint32))
+    g = WorkloadRng(5)
+    o = O.Rng(5)
+    assert [g.next_u64() for _ in range(5)] == [o.next_u64() for _ in range(5)]
+    assert np.array_equal(WorkloadRng(9).gaussian(7, 1e-2), np.array(_gauss(9, 7)))
+    ref = O.reference()
+    if ref is not None:
+        fa = np.empty((40, 72), np.complex64)
+        fb = np.empty((72, 96), np.complex64)
+        ref.lib.ref_gemm_bench_operands.argtypes = [C.c_uint64, C.c_int64, C.c_int64, C.c_int64,
+                                                    C.c_void_p, C.c_void_p]
+        ref.lib.ref_gemm_bench_operands(1 + 96, 40, 72, 96, fa.ctypes.data, fb.ctypes.data)
+        assert np.array_equal(a.numpy().view(np.uint32), fa.view(np.uint32))
+        assert np.array_equal(b.numpy().view(np.uint32), fb.view(np.uint32))
+
+
+def _gauss(seed, n):
+    import oracle as O
+    r = O.Rng(seed)
+    return [r.gaussian(1e-2) for _ in range(n)]
