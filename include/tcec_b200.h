@@ -241,6 +241,15 @@ int tcec_contract_node_batch(tcec_network net, const int* steps, int n_steps,
                              const tcec_dispatch_config_t* cfg, int n_var, const int* var_nodes,
                              int n_runs, const void* var_data, void* out_host);
 
+/* After a selector / node batch: run `run`'s format-overflow flag (OR over its
+ * GEMMs, DispatchResult::overflow, precsel.hpp:146-151) and its decision-log
+ * lines ('\n'-separated DecisionRecord::to_line, one per step -- what
+ * amplitude(..., log) records, qcircuit.cpp:184-195).  A batch in which any
+ * run hit ScaleOverflow (precsel.cpp:54-57) or a skipped stage 2
+ * (precsel.cpp:117-118) fails with that error, naming the run. */
+int tcec_network_batch_run_info(tcec_network net, int run, int* overflow, char* log_lines,
+                                int64_t log_capacity);
+
 /* ------------------------------------------------- workload generation
  * The reference's deterministic random source (Rng, rng.hpp:13-56: the
  * standard std::mt19937_64 + its hand-rolled maps), host code, so benchmark

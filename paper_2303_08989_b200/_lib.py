@@ -159,6 +159,7 @@ def load() -> C.CDLL:
         "tcec_contract_node_batch": ([vp, ip, i32, C.POINTER(DispatchConfig), i32, ip, i32, vp,
                                       vp], i32),
         "tcec_prep_kp": ([i64], i64),
+        "tcec_network_batch_run_info": ([vp, i32, ip, C.c_char_p, i64], i32),
         "tcec_rng_create": ([C.c_uint64, C.POINTER(vp)], i32),
         "tcec_rng_destroy": ([vp], i32),
         "tcec_rng_next_u64": ([vp], C.c_uint64),

@@ -90,6 +90,13 @@ struct tcec_network_s {
     std::string plan_key;
     tcec::FoldPlan plan_cache;
     std::vector<FoldLane> lanes;
+    // decisions of the last batch call (selector / node batch): the tensor-core
+    // steps' DevDecision of every run, archived on the device after each run's
+    // fold and read back with the amplitudes (tcec_network_batch_run_info)
+    std::vector<tcec::DevDecision> batch_dec;
+    std::vector<int> batch_tc;       // step indices of the tensor-core steps
+    int batch_runs = 0;
+    std::string batch_plan_key;
     ~tcec_network_s() {
         for (auto& l : lanes) l.release();
         small.release();
@@ -586,6 +593,79 @@ __global__ void set_selectors_kernel(float2* node_base, const int64_t* sel_off, 
     p[1] = make_float2(one ? 1.0f : 0.0f, 0.0f);
 }
 
+// copy the decision slots of one run's tensor-core steps into its archive row
+__global__ void archive_decisions_kernel(const DevDecision* dec, const int* tc_steps, int n_tc,
+                                         DevDecision* arch) {
+    for (int i = threadIdx.x; i < n_tc; i += blockDim.x) arch[i] = dec[tc_steps[i]];
+}
+
+// Per-call state of the decision archive of a batch.
+struct BatchArchive {
+    std::vector<int> tc;        // tensor-core step indices
+    int* d_tc = nullptr;
+    DevDecision* d_arch = nullptr;
+    int n_runs = 0;
+    int begin(const FoldPlan& plan, int runs, cudaStream_t s) {
+        tc.clear();
+        for (size_t i = 0; i < plan.steps.size(); ++i)
+            if (plan.steps[i].dp.tier == kTierTc) tc.push_back(int(i));
+        n_runs = runs;
+        if (tc.empty() || runs <= 0) return TCEC_OK;
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d_tc), tc.size() * sizeof(int), s);
+        if (e == cudaSuccess)
+            e = cudaMallocAsync(reinterpret_cast<void**>(&d_arch),
+                                tc.size() * size_t(runs) * sizeof(DevDecision), s);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(d_tc, tc.data(), tc.size() * sizeof(int), cudaMemcpyHostToDevice, s);
+        return e == cudaSuccess ? TCEC_OK : cuda_error(e, "decision archive");
+    }
+    // after run r's fold on stream s (reading that fold's decision slots)
+    void record(const DevDecision* dec, int r, cudaStream_t s) const {
+        if (tc.empty()) return;
+        archive_decisions_kernel<<<1, 128, 0, s>>>(dec, d_tc, int(tc.size()), d_arch + size_t(r) * tc.size());
+    }
+    int download(std::vector<DevDecision>* out, cudaStream_t s) const {
+        out->assign(tc.size() * size_t(n_runs), DevDecision{});
+        if (tc.empty() || n_runs <= 0) return TCEC_OK;
+        const cudaError_t e = cudaMemcpyAsync(out->data(), d_arch, out->size() * sizeof(DevDecision),
+                                              cudaMemcpyDeviceToHost, s);
+        return e == cudaSuccess ? TCEC_OK : cuda_error(e, "decision archive download");
+    }
+    void release(cudaStream_t s) {
+        if (d_tc) cudaFreeAsync(d_tc, s);
+        if (d_arch) cudaFreeAsync(d_arch, s);
+        d_tc = nullptr;
+        d_arch = nullptr;
+    }
+};
+
+// After the batch synchronized: keep the archive on the network and raise
+// what the reference would have raised on the first failing run -- the
+// ScaleOverflow of scale_matrix (precsel.cpp:54-57, 209-216) or the
+// logic_error of a skipped stage 2 (precsel.cpp:117-118).  The format
+// overflow flag is not an error (DispatchResult::overflow); it is reported
+// per run by tcec_network_batch_run_info.
+static int settle_batch(tcec_network_s& net, BatchArchive& ar) {
+    net.batch_tc = ar.tc;
+    net.batch_runs = ar.n_runs;
+    net.batch_plan_key = net.plan_key;
+    const size_t nt = ar.tc.size();
+    for (int r = 0; r < ar.n_runs; ++r)
+        for (size_t i = 0; i < nt; ++i) {
+            const DevDecision& d = net.batch_dec[size_t(r) * nt + i];
+            const StepPlan& sp = net.plan_cache.steps[size_t(ar.tc[i])];
+            if (sp.dp.stats && d.kind < 0)
+                return set_error(TCEC_ERR_LOGIC, "run " + std::to_string(r) + ", step " +
+                                                     std::to_string(ar.tc[i]) +
+                                                     ": matrix_tolerance: stage-2 statistics required but skipped");
+            if (d.scale_overflow)
+                return set_error(TCEC_ERR_SCALE_OVERFLOW, "run " + std::to_string(r) + ", step " +
+                                                              std::to_string(ar.tc[i]) +
+                                                              ": scaled component left the f32 range");
+        }
+    return TCEC_OK;
+}
+
 }  // namespace tcec
 
 using namespace tcec;
@@ -756,6 +836,9 @@ int tcec_contract_selector_batch(tcec_network net, const int* steps, int n_steps
     const std::vector<int> sel_vec(sel_nodes, sel_nodes + n_sel);
     const SmallProgram* fused = small_program(*net, steps, n_steps, *cfg, plan, sel_vec, &rc);
     if (rc) return rc;
+    BatchArchive ar;
+    rc = ar.begin(plan, n_strings, s);  // (the fused program is eligible only without tensor-core steps)
+    if (rc) return rc;
     if (fused) {
         // one launch: one warp per bitstring, selectors built from the bits
         rc = launch_small_program(*fused, static_cast<const float2*>(net->node_dev), n_strings,
@@ -781,6 +864,7 @@ int tcec_contract_selector_batch(tcec_network net, const int* steps, int n_steps
                     static_cast<float2*>(ln.node_dev), d_off, n_sel, d_bits + size_t(i) * n_sel);
             rc = run_fold_lane(*net, ln, steps, n_steps, *cfg, plan);
             if (rc) return rc;
+            ar.record(ln.dec, i, ln.s);
             cudaMemcpyAsync(d_out + i, ln.result_dev, 8, cudaMemcpyDeviceToDevice, ln.s);
         }
         for (int l = 0; l < L; ++l) {
@@ -795,12 +879,16 @@ int tcec_contract_selector_batch(tcec_network net, const int* steps, int n_steps
                     static_cast<float2*>(net->node_dev), d_off, n_sel, d_bits + size_t(i) * n_sel);
             rc = run_fold(*net, steps, n_steps, *cfg, plan, dec, ws, true);
             if (rc) return rc;
+            ar.record(dec, i, s);
             cudaMemcpyAsync(d_out + i, net->result_dev, 8, cudaMemcpyDeviceToDevice, s);
         }
     }
     if (prof) cudaEventRecord(h.batch_ev[1], s);
     e = cudaMemcpyAsync(out_host, d_out, size_t(n_strings) * 8, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return cuda_error(e, "batch download");
+    rc = ar.download(&net->batch_dec, s);
+    if (rc) return rc;
+    ar.release(s);
     cudaFreeAsync(d_off, s);
     cudaFreeAsync(d_bits, s);
     cudaFreeAsync(d_out, s);
@@ -809,7 +897,7 @@ int tcec_contract_selector_batch(tcec_network net, const int* steps, int n_steps
     if (prof) account_batch(h);
     // the host copy of the selector slots no longer matches the device
     net->dirty = true;
-    return TCEC_OK;
+    return settle_batch(*net, ar);
 }
 
 int tcec_contract_node_batch(tcec_network net, const int* steps, int n_steps,
@@ -858,6 +946,9 @@ int tcec_contract_node_batch(tcec_network net, const int* steps, int n_steps,
     const std::vector<int> var_vec(var_nodes, var_nodes + n_var);
     const SmallProgram* fused = small_program(*net, steps, n_steps, *cfg, plan, var_vec, &rc);
     if (rc) return rc;
+    BatchArchive ar;
+    rc = ar.begin(plan, n_runs, s);
+    if (rc) return rc;
     if (fused) {
         rc = launch_small_program(*fused, static_cast<const float2*>(net->node_dev), n_runs, d_var,
                                   per_run, nullptr, d_out, s);
@@ -883,6 +974,7 @@ int tcec_contract_node_batch(tcec_network net, const int* steps, int n_steps,
                     n_var);
             rc = run_fold_lane(*net, ln, steps, n_steps, *cfg, plan);
             if (rc) return rc;
+            ar.record(ln.dec, r, ln.s);
             cudaMemcpyAsync(d_out + r, ln.result_dev, 8, cudaMemcpyDeviceToDevice, ln.s);
         }
         for (int l = 0; l < L; ++l) {
@@ -898,12 +990,16 @@ int tcec_contract_node_batch(tcec_network net, const int* steps, int n_steps,
                     n_var);
             rc = run_fold(*net, steps, n_steps, *cfg, plan, dec, ws, true);
             if (rc) return rc;
+            ar.record(dec, r, s);
             cudaMemcpyAsync(d_out + r, net->result_dev, 8, cudaMemcpyDeviceToDevice, s);
         }
     }
     if (prof) cudaEventRecord(h.batch_ev[1], s);
     e = cudaMemcpyAsync(out_host, d_out, size_t(n_runs) * 8, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return cuda_error(e, "batch download");
+    rc = ar.download(&net->batch_dec, s);
+    if (rc) return rc;
+    ar.release(s);
     cudaFreeAsync(d_seg, s);
     cudaFreeAsync(d_var, s);
     cudaFreeAsync(d_out, s);
@@ -911,6 +1007,36 @@ int tcec_contract_node_batch(tcec_network net, const int* steps, int n_steps,
     if (e != cudaSuccess) return cuda_error(e, "node batch");
     if (prof) account_batch(h);
     net->dirty = true;  // device node data now holds the last run
+    return settle_batch(*net, ar);
+}
+
+int tcec_network_batch_run_info(tcec_network net, int run, int* overflow, char* log_lines,
+                                int64_t log_capacity) {
+    if (!net) return set_error(TCEC_ERR_INVALID_ARGUMENT, "null network");
+    if (run < 0 || run >= net->batch_runs || net->batch_plan_key != net->plan_key)
+        return set_error(TCEC_ERR_INVALID_ARGUMENT, "no such run in the last batch");
+    const FoldPlan& plan = net->plan_cache;
+    const size_t nt = net->batch_tc.size();
+    int ovf = 0;
+    std::string log;
+    size_t ti = 0;
+    for (size_t i = 0; i < plan.steps.size(); ++i) {
+        const StepPlan& sp = plan.steps[i];
+        DevDecision d{};
+        if (ti < nt && net->batch_tc[ti] == int(i)) d = net->batch_dec[size_t(run) * nt + ti++];
+        tcec_dispatch_result_t res;
+        const int rc = finish_dispatch(sp.dp, d, sp.m, sp.n, sp.k, &res);
+        if (rc) return rc;
+        ovf |= res.overflow;
+        log += res.line;
+        log += "\n";
+    }
+    if (overflow) *overflow = ovf;
+    if (log_lines && log_capacity > 0) {
+        const size_t nb = std::min(size_t(log_capacity - 1), log.size());
+        std::memcpy(log_lines, log.data(), nb);
+        log_lines[nb] = '\0';
+    }
     return TCEC_OK;
 }
 

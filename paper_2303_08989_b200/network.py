@@ -172,6 +172,15 @@ class Network:
                                                 out.ctypes.data_as(C.c_void_p)))
         return out[:len(runs)]
 
+    def batch_run_info(self, run: int, n_steps: int | None = None):
+        """(overflow flag, decision-log lines) of run `run` of the last batch
+        (tcec_network_batch_run_info)."""
+        steps = n_steps if n_steps is not None else max(self.n_nodes - 1, 1)
+        ovf = C.c_int(0)
+        log = C.create_string_buffer(200 * (steps + 1))
+        check(self.lib.tcec_network_batch_run_info(self.net, int(run), C.byref(ovf), log, len(log)))
+        return bool(ovf.value), [ln for ln in log.value.decode().split("\n") if ln]
+
 
 def contract_pair(handle: Handle, a: Tensor, b: Tensor, config=None) -> Tensor:
     """contract_pair (network.hpp:29-32) as a two-node fold."""
