@@ -1,0 +1,5 @@
+// Drop-in forwarding header: mpsgemm/common.hpp of the reference API
+// (/root/reference/proj/include/mpsgemm/common.hpp) is provided by the B200
+// implementation in ../mpsgemm_b200.hpp (namespace mpsgemm, libtcec_b200.so).
+#pragma once
+#include "../mpsgemm_b200.hpp"

@@ -4,7 +4,7 @@
  * One shared library, paper_2303_08989_b200/libtcec_b200.so (sm_100a CUDA
  * kernels + the C++ host orchestration), exports exactly these symbols.  They
  * replace the reference mpsgemm entry points (/root/reference/proj/include/
- * mpsgemm/*.hpp) for the north-star path; each declaration cites the interface
+ * mpsgemm/<name>.hpp) for the north-star path; each declaration cites the interface
  * it replaces.  Plain pointers and sizes only: "device" buffers are CUDA device
  * pointers (e.g. from torch or cudaMalloc); "host" buffers are ordinary memory.
  * Complex data is interleaved (re, im) float32, row-major, exactly the layout
@@ -226,6 +226,10 @@ int tcec_path_reconfigure(int n_nodes, const int* ranks, const int* labels, cons
 int tcec_contract_network(tcec_network net, const int* steps, int n_steps,
                           const tcec_dispatch_config_t* cfg, void* out_host, int64_t out_capacity,
                           int* out_rank, int* out_labels, char* log_lines, int64_t log_capacity);
+/* the DispatchResult + DecisionRecord of every step of the network's last
+ * tcec_contract_network call (the records contract_network appends to its
+ * DecisionLog, network.cpp:129-134); *count = steps written */
+int tcec_network_step_results(tcec_network net, tcec_dispatch_result_t* out, int capacity, int* count);
 /* amplitude batch (qcircuit.hpp:49-52 over many bitstrings): the network's
  * closing selector nodes (one per entry of sel_nodes) are replaced per
  * bitstring; the same plan is replayed; out_host gets one complex per string */
@@ -249,6 +253,33 @@ int tcec_contract_node_batch(tcec_network net, const int* steps, int n_steps,
  * (precsel.cpp:117-118) fails with that error, naming the run. */
 int tcec_network_batch_run_info(tcec_network net, int run, int* overflow, char* log_lines,
                                 int64_t log_capacity);
+
+/* ------------------------------------------------- f64 reference functions
+ * The reference's f64 "truth" functions, computed on the device in the
+ * reference's accumulation order (ascending-k RN chains from +0.0, separate
+ * multiply and add), so they are bit-identical to it.  They are reference
+ * API, not part of the TCEC path. */
+/* cgemm_oracle, cgemm.hpp:26 / cgemm.cpp:62-74: a, b complex64 (device),
+ * c complex128 (device), m x n */
+int tcec_cgemm_oracle(tcec_handle h, const void* a, const void* b, void* c, int64_t m, int64_t n,
+                      int64_t k);
+/* cgemm_f64 of contract_pair_oracle (network.cpp:87-110): complex128 in and out */
+int tcec_cgemm_c128(tcec_handle h, const void* a, const void* b, void* c, int64_t m, int64_t n,
+                    int64_t k);
+/* permute (tensor.hpp:56-105) of a complex128 tensor (device) */
+int tcec_permute_c128(tcec_handle h, const void* src, void* dst, int rank, const int64_t* old_dims,
+                      const int* axis_of);
+/* contract_network_oracle, network.hpp:39 / network.cpp:179-186: the result
+ * tensor (complex128, host) of the f64 TTGT fold along `steps` */
+int tcec_contract_network_oracle(tcec_network net, const int* steps, int n_steps, void* out_host,
+                                 int64_t out_capacity, int* out_rank, int* out_labels);
+/* statevector_oracle, qcircuit.hpp:56 / qcircuit.cpp:197-225: apply n_gates
+ * gates in order to |0...0> (qubit q = bit q of the index); gate g acts on
+ * qubit qa[g] with the row-major 2x2 complex128 matrix u[8g .. 8g+7]
+ * (gate_matrix_f64), or is a CZ on (qa[g], qb[g]) when qb[g] >= 0.
+ * state: 2^n_qubits complex128 (device). */
+int tcec_statevector_f64(tcec_handle h, int n_qubits, int n_gates, const int* qa, const int* qb,
+                         const double* u, void* state);
 
 /* ------------------------------------------------- workload generation
  * The reference's deterministic random source (Rng, rng.hpp:13-56: the

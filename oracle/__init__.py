@@ -79,7 +79,7 @@ def build(with_ref: bool | None = None) -> None:
     if with_ref is None:
         with_ref = os.path.isdir(REF_SRC)
     if with_ref:
-        targets.append("ref")
+        targets += ["ref", "reftests"]  # reftests: the reference's own tests vs the drop-in
     subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
 
 

@@ -159,6 +159,12 @@ def load() -> C.CDLL:
         "tcec_contract_node_batch": ([vp, ip, i32, C.POINTER(DispatchConfig), i32, ip, i32, vp,
                                       vp], i32),
         "tcec_prep_kp": ([i64], i64),
+        "tcec_network_step_results": ([vp, C.POINTER(DispatchResult), i32, ip], i32),
+        "tcec_cgemm_oracle": ([vp, vp, vp, vp, i64, i64, i64], i32),
+        "tcec_cgemm_c128": ([vp, vp, vp, vp, i64, i64, i64], i32),
+        "tcec_permute_c128": ([vp, vp, vp, i32, C.POINTER(i64), ip], i32),
+        "tcec_contract_network_oracle": ([vp, ip, i32, vp, i64, ip, ip], i32),
+        "tcec_statevector_f64": ([vp, i32, i32, ip, ip, C.POINTER(C.c_double), vp], i32),
         "tcec_network_batch_run_info": ([vp, i32, ip, C.c_char_p, i64], i32),
         "tcec_rng_create": ([C.c_uint64, C.POINTER(vp)], i32),
         "tcec_rng_destroy": ([vp], i32),

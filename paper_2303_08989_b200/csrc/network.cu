@@ -93,6 +93,7 @@ struct tcec_network_s {
     // decisions of the last batch call (selector / node batch): the tensor-core
     // steps' DevDecision of every run, archived on the device after each run's
     // fold and read back with the amplitudes (tcec_network_batch_run_info)
+    std::vector<tcec_dispatch_result_t> step_results;  // of the last contract_network
     std::vector<tcec::DevDecision> batch_dec;
     std::vector<int> batch_tc;       // step indices of the tensor-core steps
     int batch_runs = 0;
@@ -771,9 +772,10 @@ int tcec_contract_network(tcec_network net, const int* steps, int n_steps,
     if (out_rank) *out_rank = int(plan.out_labels.size());
     if (out_labels) std::copy(plan.out_labels.begin(), plan.out_labels.end(), out_labels);
     std::string log;
+    net->step_results.assign(plan.steps.size(), tcec_dispatch_result_t{});
     for (size_t i = 0; i < plan.steps.size(); ++i) {
         const StepPlan& sp = plan.steps[i];
-        tcec_dispatch_result_t res;
+        tcec_dispatch_result_t& res = net->step_results[i];
         rc = finish_dispatch(sp.dp, dd[i], sp.m, sp.n, sp.k, &res);
         if (rc) return rc;
         log += res.line;
@@ -1008,6 +1010,86 @@ int tcec_contract_node_batch(tcec_network net, const int* steps, int n_steps,
     if (prof) account_batch(h);
     net->dirty = true;  // device node data now holds the last run
     return settle_batch(*net, ar);
+}
+
+int tcec_network_step_results(tcec_network net, tcec_dispatch_result_t* out, int capacity, int* count) {
+    if (!net || (capacity > 0 && !out)) return set_error(TCEC_ERR_INVALID_ARGUMENT, "null argument");
+    const int n = int(net->step_results.size());
+    for (int i = 0; i < n && i < capacity; ++i) out[i] = net->step_results[size_t(i)];
+    if (count) *count = std::min(n, capacity);
+    return TCEC_OK;
+}
+
+// contract_network_oracle (network.cpp:179-186): the same TTGT fold with every
+// value widened to complex128 and f64 GEMMs in the reference's order
+// (gemm_rows_dd), on the device; the result tensor goes to out_host (c128).
+int tcec_contract_network_oracle(tcec_network net, const int* steps, int n_steps, void* out_host,
+                                 int64_t out_capacity, int* out_rank, int* out_labels) {
+    if (!net) return set_error(TCEC_ERR_INVALID_ARGUMENT, "null argument");
+    if (!net->h) return set_error(TCEC_ERR_CUDA, "network has no device handle");
+    Handle& h = *net->h;
+    cudaSetDevice(h.device);
+    int rc = validate(*net);
+    if (rc) return rc;
+    tcec_dispatch_config_t cfg;
+    tcec_default_config(&cfg);
+    cfg.force = TCEC_FORCE_FP64_ORACLE;
+    FoldPlan plan;
+    rc = build_plan(*net, steps, n_steps, cfg, &plan);
+    if (rc) return rc;
+    int64_t size = 1;
+    for (auto d : plan.out_dims) size *= d;
+    if (out_capacity < size) return set_error(TCEC_ERR_SHAPE_MISMATCH, "output buffer too small");
+    rc = upload(*net);
+    if (rc) return rc;
+    cudaStream_t s = h.stream;
+    std::map<int, double2*> live;
+    std::vector<void*> owned;
+    auto alloc = [&](int64_t elems, double2** p) {
+        const cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(p),
+                                              size_t(std::max<int64_t>(elems, 1)) * 16, s);
+        if (e != cudaSuccess) return cuda_error(e, "f64 contraction buffer");
+        return int(TCEC_OK);
+    };
+    const float2* base = static_cast<const float2*>(net->node_dev);
+    for (size_t i = 0; i < net->nodes.size(); ++i) {
+        double2* w = nullptr;
+        if ((rc = alloc(net->nodes[i].size(), &w))) return rc;
+        launch_widen(base + net->offset[i], w, net->nodes[i].size(), s);
+        live[int(i)] = w;
+    }
+    int next_id = int(net->nodes.size());
+    for (const StepPlan& sp : plan.steps) {
+        double2* pa = live[sp.ia];
+        double2* pb = live[sp.ib];
+        double2 *ta = nullptr, *tb = nullptr, *pc = nullptr;
+        if (sp.perm_a) {
+            if ((rc = alloc(sp.a_size, &ta))) return rc;
+            launch_permute_c128(pa, ta, int(sp.a_dims.size()), sp.a_dims.data(), sp.a_axis.data(), s);
+        }
+        if (sp.perm_b) {
+            if ((rc = alloc(sp.b_size, &tb))) return rc;
+            launch_permute_c128(pb, tb, int(sp.b_dims.size()), sp.b_dims.data(), sp.b_axis.data(), s);
+        }
+        if ((rc = alloc(sp.m * sp.n, &pc))) return rc;
+        launch_cgemm_c128(ta ? ta : pa, false, tb ? tb : pb, false, pc, sp.m, sp.n, sp.k, s);
+        if (ta) cudaFreeAsync(ta, s);
+        if (tb) cudaFreeAsync(tb, s);
+        cudaFreeAsync(pa, s);
+        cudaFreeAsync(pb, s);
+        live.erase(sp.ia);
+        live.erase(sp.ib);
+        live[next_id++] = pc;
+    }
+    double2* res = live.begin()->second;
+    cudaError_t e = cudaMemcpyAsync(out_host, res, size_t(size) * 16, cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(res, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_error(e, "contract_network_oracle");
+    if (out_rank) *out_rank = int(plan.out_labels.size());
+    if (out_labels) std::copy(plan.out_labels.begin(), plan.out_labels.end(), out_labels);
+    return TCEC_OK;
 }
 
 int tcec_network_batch_run_info(tcec_network net, int run, int* overflow, char* log_lines,

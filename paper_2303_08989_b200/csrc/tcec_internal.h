@@ -75,6 +75,13 @@ void launch_cgemm_fp64(const float2* a, const float2* b, float2* c, int64_t m, i
 
 // ---------------------------------------------------------------- permute
 constexpr int kMaxRank = 48;
+
+// ------------------------------------------------- f64 reference (f64_ref.cu)
+void launch_cgemm_c128(const void* a, bool a_f32, const void* b, bool b_f32, double2* c, int64_t m,
+                       int64_t n, int64_t k, cudaStream_t s);
+void launch_permute_c128(const double2* src, double2* dst, int rank, const int64_t* old_dims,
+                         const int* axis_of, cudaStream_t s);
+void launch_widen(const float2* src, double2* dst, int64_t n, cudaStream_t s);
 void launch_permute(const float2* src, float2* dst, int rank, const int64_t* old_dims,
                     const int* axis_of, cudaStream_t s);
 
