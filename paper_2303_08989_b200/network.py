@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from ._lib import check
+from ._lib import ExtentMismatch, ShapeMismatch, check
 from .api import Handle, SelectionPolicy, make_config
 from .circuits import Circuit, NetworkSpec, circuit_to_network
 
@@ -180,6 +180,59 @@ class Network:
         log = C.create_string_buffer(200 * (steps + 1))
         check(self.lib.tcec_network_batch_run_info(self.net, int(run), C.byref(ovf), log, len(log)))
         return bool(ovf.value), [ln for ln in log.value.decode().split("\n") if ln]
+
+
+def _fmt9(v: float) -> str:
+    """printf("%.9g") of a float widened to double (network.cpp:451-453)."""
+    return "%.9g" % float(v)
+
+
+def save_network(spec: NetworkSpec) -> str:
+    """save_network text format (network.hpp:62-66, network.cpp:440-458): per node
+    "node <id> labels l1,l2 dims d1,d2" ("-" for rank 0), then the values as
+    "%.9g %.9g" pairs (an exact round trip for f32)."""
+    out = []
+    for i, (ls, ds, d) in enumerate(zip(spec.labels, spec.dims, spec.data)):
+        lab = ",".join(str(x) for x in ls) if ls else "-"
+        dim = ",".join(str(int(x)) for x in ds) if ds else "-"
+        out.append(f"node {i} labels {lab} dims {dim}\n")
+        v = np.asarray(d, dtype=np.complex64).reshape(-1)
+        out.append(" ".join(f"{_fmt9(z.real)} {_fmt9(z.imag)}" for z in v) + "\n")
+    return "".join(out)
+
+
+def load_network(text: str) -> NetworkSpec:
+    """load_network (network.cpp:472-501): the inverse of save_network,
+    validated like validate_network."""
+    tok = text.split()
+    spec = NetworkSpec()
+    i = 0
+    while i < len(tok):
+        if tok[i] != "node":
+            raise ShapeMismatch(1, "expected 'node' header, got: " + tok[i])
+        if i + 5 >= len(tok) or tok[i + 2] != "labels" or tok[i + 4] != "dims":
+            raise ShapeMismatch(1, "malformed node header")
+        labels = [] if tok[i + 3] == "-" else tok[i + 3].split(",")
+        dims = [] if tok[i + 5] == "-" else [int(x) for x in tok[i + 5].split(",")]
+        i += 6
+        n = int(np.prod(dims)) if dims else 1
+        if i + 2 * n > len(tok):
+            raise ShapeMismatch(1, "truncated tensor data")
+        vals = np.array([float(x) for x in tok[i:i + 2 * n]], dtype=np.float64).astype(np.float32)
+        i += 2 * n
+        spec.labels.append(labels)
+        spec.dims.append(dims)
+        spec.data.append(vals.view(np.complex64).reshape(dims if dims else [1]))
+    occ = {}
+    for ls, ds in zip(spec.labels, spec.dims):
+        for l, d in zip(ls, ds):
+            occ.setdefault(l, []).append(d)
+    for l, ds in occ.items():
+        if len(ds) > 2:
+            raise ShapeMismatch(1, f"label {l} appears in more than two nodes")
+        if len(ds) == 2 and ds[0] != ds[1]:
+            raise ExtentMismatch(5, f"label {l} has mismatched extents")
+    return spec
 
 
 def contract_pair(handle: Handle, a: Tensor, b: Tensor, config=None) -> Tensor:

@@ -243,3 +243,24 @@ def _gauss(seed, n):
     import oracle as O
     r = O.Rng(seed)
     return [r.gaussian(1e-2) for _ in range(n)]
+
+
+def test_network_text_format_matches_the_reference(golden):
+    """save_network (network.cpp:440-458) of the reference's circuit networks is
+    byte-identical to the reference's own text (golden sha), and load_network
+    round-trips it exactly."""
+    import hashlib
+
+    from paper_2303_08989_b200.circuits import circuit_to_network, load_circuit
+    from paper_2303_08989_b200.network import load_network, save_network
+    for case in golden("rqc.json"):
+        circ = load_circuit(case["circuit_text"])
+        spec = circuit_to_network(circ, [0] * circ.n_qubits)
+        text = save_network(spec)
+        assert hashlib.sha256(text.encode()).hexdigest() == case["network_text_sha"]
+        back = load_network(text)
+        assert back.labels == [list(map(str, l)) for l in spec.labels]
+        assert back.dims == [list(d) for d in spec.dims]
+        for x, y in zip(back.data, spec.data):
+            assert np.array_equal(np.asarray(x).reshape(-1).view(np.uint32),
+                                  np.asarray(y, np.complex64).reshape(-1).view(np.uint32))
