@@ -329,6 +329,7 @@ tcec::DevDecision* tcec_handle_s::decisions(int slots) {
 
 tcec_handle_s::~tcec_handle_s() {
     if (stream) cudaStreamSynchronize(stream);
+    stage.reset();
     if (ws) cudaFree(ws);
     if (io) cudaFree(io);
     if (dec) cudaFree(dec);
@@ -827,10 +828,37 @@ static HostPipe plan_host_pipe(int64_t m, int64_t n, int chunks, int parts) {
     return hp;
 }
 
+// Host<->device copies of the host-buffer entry point: direct DMA for pinned
+// buffers, the pinned staging ring (host_stage.h) for pageable ones.
+struct HostIO {
+    bool a_dma = true, b_dma = true, c_dma = true;
+    StageRing* ring = nullptr;
+    cudaError_t h2d(bool dma_ok, uint8_t* dst, size_t dpitch, const uint8_t* src, size_t spitch, size_t width,
+                    size_t height, cudaStream_t st) const {
+        if (dma_ok)
+            return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyHostToDevice, st);
+        if (height == 1 && width > StageRing::kSlotBytes) {  // one flat buffer: slot-sized pieces
+            for (size_t off = 0; off < width; off += StageRing::kSlotBytes) {
+                const size_t w = std::min(StageRing::kSlotBytes, width - off);
+                const cudaError_t e = ring->h2d(dst + off, w, src + off, w, w, 1, st);
+                if (e != cudaSuccess) return e;
+            }
+            return cudaSuccess;
+        }
+        return ring->h2d(dst, dpitch, src, spitch, width, height, st);
+    }
+    cudaError_t d2h(uint8_t* dst, size_t dpitch, const uint8_t* src, size_t spitch, size_t width,
+                    size_t height, cudaStream_t st) const {
+        if (c_dma)
+            return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDeviceToHost, st);
+        return ring->d2h(dst, dpitch, src, spitch, width, height, st);
+    }
+};
+
 static int host_pipeline(Handle& h, const uint8_t* a, const uint8_t* b, uint8_t* c, int64_t m,
                          int64_t n, int64_t k, const tcec_dispatch_config_t& cfg,
                          const DispatchPlan& p, void* ws, uint8_t* da, uint8_t* db, uint8_t* dc,
-                         const HostPipe& hp, DevDecision* d) {
+                         const HostPipe& hp, DevDecision* d, const HostIO& io) {
     cudaStream_t s = h.stream;
     if (!h.in_stream) {
         CUDA_TRY(cudaStreamCreateWithFlags(&h.in_stream, cudaStreamNonBlocking));
@@ -851,8 +879,8 @@ static int host_pipeline(Handle& h, const uint8_t* a, const uint8_t* b, uint8_t*
     CUDA_TRY(cudaStreamWaitEvent(h.in_stream, ev_sync, 0));
     auto put_b = [&](int j) -> int {
         const int64_t j0 = j0_of(j), w = w_of(j);
-        CUDA_TRY(cudaMemcpy2DAsync(db + size_t(k) * j0 * 8, size_t(w) * 8, b + j0 * 8, size_t(n) * 8,
-                                   size_t(w) * 8, size_t(k), cudaMemcpyHostToDevice, h.in_stream));
+        CUDA_TRY(io.h2d(io.b_dma, db + size_t(k) * j0 * 8, size_t(w) * 8, b + j0 * 8, size_t(n) * 8,
+                        size_t(w) * 8, size_t(k), h.in_stream));
         CUDA_TRY(cudaEventRecord(ev_b[j], h.in_stream));
         return TCEC_OK;
     };
@@ -860,8 +888,8 @@ static int host_pipeline(Handle& h, const uint8_t* a, const uint8_t* b, uint8_t*
         if (int rc = put_b(j)) return rc;
     for (int i = 0; i < hp.nch; ++i) {
         const int64_t r0 = i * hp.rows_per, r1 = std::min(m, r0 + hp.rows_per);
-        CUDA_TRY(cudaMemcpyAsync(da + r0 * row_bytes, a + r0 * row_bytes, size_t(r1 - r0) * row_bytes,
-                                 cudaMemcpyHostToDevice, h.in_stream));
+        CUDA_TRY(io.h2d(io.a_dma, da + r0 * row_bytes, row_bytes, a + r0 * row_bytes, row_bytes, row_bytes,
+                        size_t(r1 - r0), h.in_stream));
         CUDA_TRY(cudaEventRecord(ev_a[i], h.in_stream));
     }
     for (int j = hp.front; j < hp.q; ++j)
@@ -910,8 +938,8 @@ static int host_pipeline(Handle& h, const uint8_t* a, const uint8_t* b, uint8_t*
         CUDA_TRY(cudaEventRecord(ev, gs));
         CUDA_TRY(cudaStreamWaitEvent(h.copy_stream, ev, 0));
         const size_t off = size_t(r0 * n + c0) * 8;
-        CUDA_TRY(cudaMemcpy2DAsync(c + off, size_t(n) * 8, dc + off, size_t(n) * 8, size_t(w) * 8,
-                                   size_t(r1 - r0), cudaMemcpyDeviceToHost, h.copy_stream));
+        CUDA_TRY(io.d2h(c + off, size_t(n) * 8, dc + off, size_t(n) * 8, size_t(w) * 8, size_t(r1 - r0),
+                        h.copy_stream));
         return TCEC_OK;
     };
     for (int j = 0; j < hp.front; ++j) prep_part(j);
@@ -977,6 +1005,24 @@ int tcec_dispatch_cgemm_host(tcec_handle h, const void* a, const void* b, void* 
         ws = h->workspace(wsb);
         if (!ws) return set_error(TCEC_ERR_CUDA, "workspace allocation failed");
     }
+    // pageable host buffers (a std::vector, a numpy array) go through the
+    // pinned staging ring so the copies stay asynchronous and overlapped
+    HostIO io;
+    io.a_dma = ab == 0 || dma_capable(a);
+    io.b_dma = bb == 0 || dma_capable(b);
+    io.c_dma = cb == 0 || dma_capable(c);
+    if (!(io.a_dma && io.b_dma && io.c_dma)) {
+        if (!h->stage) h->stage = std::make_unique<StageRing>();
+        CUDA_TRY(h->stage->init());
+        io.ring = h->stage.get();
+    }
+    auto finish_io = [&]() -> int {
+        if (io.ring) {
+            CUDA_TRY(cudaStreamSynchronize(io.ring->host));
+            io.ring->finish();
+        }
+        return TCEC_OK;
+    };
     struct Ctx {
         tcec_handle h;
         uint8_t* c_host;
@@ -984,7 +1030,8 @@ int tcec_dispatch_cgemm_host(tcec_handle h, const void* a, const void* b, void* 
         int64_t row_bytes;
         int used;
         cudaError_t err;
-    } ctx{h, static_cast<uint8_t*>(c), dc, n * 8, 0, cudaSuccess};
+        const HostIO* io;
+    } ctx{h, static_cast<uint8_t*>(c), dc, n * 8, 0, cudaSuccess, &io};
     ChunkHook hook;
     hook.chunks = m >= 8192 ? 4 : 1;
     hook.ctx = &ctx;
@@ -994,9 +1041,8 @@ int tcec_dispatch_cgemm_host(tcec_handle h, const void* a, const void* b, void* 
         cudaError_t e = cudaEventRecord(ev, x.h->stream);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(x.h->copy_stream, ev, 0);
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(x.c_host + r0 * x.row_bytes, x.dc + r0 * x.row_bytes,
-                                size_t((r1 - r0) * x.row_bytes), cudaMemcpyDeviceToHost,
-                                x.h->copy_stream);
+            e = x.io->d2h(x.c_host + r0 * x.row_bytes, size_t(x.row_bytes), x.dc + r0 * x.row_bytes,
+                          size_t(x.row_bytes), size_t(x.row_bytes), size_t(r1 - r0), x.h->copy_stream);
         if (e != cudaSuccess) {
             x.err = e;
             return cuda_error(e, "chunk copy");
@@ -1021,13 +1067,14 @@ int tcec_dispatch_cgemm_host(tcec_handle h, const void* a, const void* b, void* 
     if (pipelined) {
         const HostPipe hp = plan_host_pipe(m, n, pipe_chunks, pipe_parts);
         int rc = host_pipeline(*h, static_cast<const uint8_t*>(a), static_cast<const uint8_t*>(b),
-                               static_cast<uint8_t*>(c), m, n, k, *cfg, p, ws, da, db, dc, hp, d);
+                               static_cast<uint8_t*>(c), m, n, k, *cfg, p, ws, da, db, dc, hp, d, io);
         if (rc) return rc;
         ++h->pipe_runs;
         CUDA_TRY(cudaMemcpyAsync(h->dec_host, d, 3 * sizeof(DevDecision), cudaMemcpyDeviceToHost,
                                  h->stream));
         CUDA_TRY(cudaStreamSynchronize(h->stream));
         CUDA_TRY(cudaStreamSynchronize(h->copy_stream));
+        if ((rc = finish_io())) return rc;
         const DevDecision& dr = h->dec_host[0];
         const DevDecision& ds = h->dec_host[1];
         const DevDecision& snap = h->dec_host[2];
@@ -1043,20 +1090,22 @@ int tcec_dispatch_cgemm_host(tcec_handle h, const void* a, const void* b, void* 
         // and a row-major copy of B (the staging holds it packed by column part)
         ctx.used = 0;
         ++h->pipe_reruns;
-        CUDA_TRY(cudaMemcpyAsync(db, b, bb, cudaMemcpyHostToDevice, h->stream));
+        CUDA_TRY(io.h2d(io.b_dma, db, bb, static_cast<const uint8_t*>(b), bb, bb, bb ? 1 : 0, h->stream));
     } else {
-        CUDA_TRY(cudaMemcpyAsync(da, a, ab, cudaMemcpyHostToDevice, h->stream));
-        CUDA_TRY(cudaMemcpyAsync(db, b, bb, cudaMemcpyHostToDevice, h->stream));
+        CUDA_TRY(io.h2d(io.a_dma, da, ab, static_cast<const uint8_t*>(a), ab, ab, ab ? 1 : 0, h->stream));
+        CUDA_TRY(io.h2d(io.b_dma, db, bb, static_cast<const uint8_t*>(b), bb, bb, bb ? 1 : 0, h->stream));
     }
     int rc = launch_dispatch(*h, reinterpret_cast<const float*>(da), reinterpret_cast<const float*>(db),
                              reinterpret_cast<float*>(dc), m, n, k, *cfg, p, d, ws, &hook);
     if (rc) return rc;
     CUDA_TRY(cudaGetLastError());
     if (ctx.used == 0 && m > 0 && n > 0)
-        CUDA_TRY(cudaMemcpyAsync(c, dc, cb, cudaMemcpyDeviceToHost, h->stream));
+        CUDA_TRY(io.d2h(static_cast<uint8_t*>(c), size_t(n) * 8, dc, size_t(n) * 8, size_t(n) * 8, size_t(m),
+                        h->stream));
     CUDA_TRY(cudaMemcpyAsync(h->dec_host, d, sizeof(DevDecision), cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(cudaStreamSynchronize(h->stream));
     CUDA_TRY(cudaStreamSynchronize(h->copy_stream));
+    if (int rc = finish_io()) return rc;
     if (h->prof && h->ev[0]) {
         for (int i = 0; i < 3; ++i) {
             float ms = 0.0f;

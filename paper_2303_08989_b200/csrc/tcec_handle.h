@@ -2,11 +2,13 @@
 #pragma once
 
 #include <algorithm>
+#include <memory>
 #include <string>
 
 #include "../../include/tcec_b200.h"
 #include "tcec_common.cuh"
 #include "tcec_internal.h"
+#include "host_stage.h"
 
 struct tcec_handle_s {
     int device = 0;
@@ -32,6 +34,7 @@ struct tcec_handle_s {
     cudaStream_t in_stream = nullptr;  // H2D of operand row chunks (host-buffer pipeline)
     cudaStream_t gemm_stream2 = nullptr;  // second GEMM stream of the host-buffer pipeline
     int64_t pipe_runs = 0, pipe_reruns = 0;  // tcec_host_pipeline_stats
+    std::unique_ptr<tcec::StageRing> stage;  // pinned ring for pageable host buffers
     cudaEvent_t in_ev[25] = {};  // B parts (<= 8), A chunks (<= 16), ordering
     // stage profiling (tcec_profile_*): CUDA events around the stages of a
     // dispatched CGEMM, accumulated after each synchronous dispatch

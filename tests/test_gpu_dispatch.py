@@ -309,3 +309,31 @@ def test_host_pipeline_on_a_caller_stream(dev):
     h1.set_stream(None)
     h0.close()
     h1.close()
+
+
+@pytest.mark.parametrize("shape", [(8448, 1536, 640), (300, 200, 100)])
+@pytest.mark.parametrize("pinned", ["", "a", "b", "c", "abc"])
+def test_host_buffers_pinned_or_pageable(handle, dev, shape, pinned):
+    """Pageable host buffers (the C++ drop-in's std::vector storage) go through
+    the pinned staging ring; any mix of pinned and pageable A / B / C gives the
+    bits of the device-buffer dispatch, pipelined (m >= 8192) or not."""
+    m, n, k = shape
+    g = np.random.default_rng(5)
+
+    def host(shape_, fill, pin):
+        if pin:
+            t = torch.empty(shape_, dtype=torch.complex64, pin_memory=True).numpy()
+        else:
+            t = np.empty(shape_, dtype=np.complex64)
+        if fill:
+            t.view(np.float32)[...] = g.random(t.view(np.float32).shape, dtype=np.float32) * 2 - 1
+        return t
+
+    a = host((m, k), True, "a" in pinned)
+    b = host((k, n), True, "b" in pinned)
+    c = host((m, n), False, "c" in pinned)
+    pol = SelectionPolicy(size_auto=96, size_tf32=64)
+    c_host, res_h = handle.dispatch_cgemm_host(a, b, pol, out=c)
+    c_dev, res_d = handle.dispatch_cgemm(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev), pol)
+    assert res_h.line == res_d.line
+    assert np.array_equal(c_host.view(np.uint32), c_dev.cpu().numpy().view(np.uint32))
