@@ -66,7 +66,8 @@ int tcec_get_flush_kblocks(tcec_handle h);
 /* tensor-core kernel variant: 0 = auto (default: wide when its tiles fill the
  * SMs, else single), 1 = CTA pair (cta_group::2, 256 x 128 tile), 2 = single
  * CTA (128 x 128 tile), 3 = wide CTA pair (cta_group::2, 256 x 256 tile),
- * 4 = the wide tile on persistent CTA pairs */
+ * 4 = the wide tile on persistent CTA pairs, 5 = the wide tile on clusters of
+ * two CTA pairs that share each B' tile by TMA multicast */
 int tcec_set_gemm_variant(tcec_handle h, int variant);
 /* network executor: 0 = auto (fused small-step kernel -- one warp per network,
  * intermediates in shared memory -- whenever every step is on a SIMT tier and

@@ -133,7 +133,7 @@ class Handle:
         3 per-step graph preceded by the fused subtree launch (hybrid)."""
         check(self.lib.tcec_set_executor(self.h, int(policy)))
 
-    GEMM_VARIANTS = {"auto": 0, "pair": 1, "single": 2, "wide": 3, "wide_persistent": 4}
+    GEMM_VARIANTS = {"auto": 0, "pair": 1, "single": 2, "wide": 3, "wide_persistent": 4, "wide_mc": 5}
 
     def set_gemm_variant(self, variant) -> None:
         """tcgen05 kernel variant: "auto" (default), "pair" (cta_group::2,

@@ -232,7 +232,7 @@ int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t
     if (prof) cudaEventRecord(h.ev[2], s);
     // row chunks (host-buffer API): only the wide kernel indexes into A' by row
     int chunks = hook ? std::max(1, hook->chunks) : 1;
-    if (g.pair != kVariantWide) chunks = 1;
+    if (g.pair != kVariantWide && g.pair != kVariantWideMc) chunks = 1;
     const int64_t rows_per = round_up((m + chunks - 1) / chunks, 256);
     for (int64_t r0 = 0; r0 < m; r0 += rows_per) {
         const int64_t r1 = std::min(m, r0 + rows_per);
@@ -460,7 +460,7 @@ int tcec_set_executor(tcec_handle h, int policy) {
 
 int tcec_set_gemm_variant(tcec_handle h, int variant) {
     CHECK_HANDLE(h);
-    if (variant < 0 || variant > 4) return set_error(TCEC_ERR_INVALID_ARGUMENT, "variant must be 0..4");
+    if (variant < 0 || variant > 5) return set_error(TCEC_ERR_INVALID_ARGUMENT, "variant must be 0..5");
     h->gemm_pair = variant;
     return TCEC_OK;
 }
@@ -1061,7 +1061,8 @@ int tcec_dispatch_cgemm_host(tcec_handle h, const void* a, const void* b, void* 
     }();
     const bool pipelined = pipe_chunks > 1 && p.tier == kTierTc && m >= 8192 && n > 0 && k > 0 &&
                            !(h->prof && h->ev[0]) &&
-                           resolve_gemm_variant(h->gemm_pair, m, 2 * n, p.kp, h->sm_count) == kVariantWide;
+                           (resolve_gemm_variant(h->gemm_pair, m, 2 * n, p.kp, h->sm_count) == kVariantWide ||
+                            resolve_gemm_variant(h->gemm_pair, m, 2 * n, p.kp, h->sm_count) == kVariantWideMc);
     DevDecision* d = pipelined ? h->decisions(3) : h->dec;
     if (!d) return set_error(TCEC_ERR_CUDA, "decision slots allocation failed");
     if (pipelined) {

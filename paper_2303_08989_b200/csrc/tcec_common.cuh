@@ -250,6 +250,19 @@ TCEC_DEV void tma_load_2d_pair(void* smem_dst, const void* tmap, uint64_t* bar, 
         : "memory");
 }
 
+// the same load multicast to the CTAs of `mask` (same smem offset in each);
+// every destination's bytes land on the leader of the destination's pair
+// (cute SM100_TMA_2SM_LOAD_MULTICAST)
+TCEC_DEV void tma_load_2d_pair_mc(void* smem_dst, const void* tmap, uint64_t* bar, int x, int y,
+                                  uint16_t mask) {
+    const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(mbar), "r"(x), "r"(y), "h"(mask)
+        : "memory");
+}
+
 template <uint32_t kCols>
 TCEC_DEV void tmem_alloc_pair(uint32_t* smem_slot) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(

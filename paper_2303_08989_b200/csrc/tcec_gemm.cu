@@ -562,6 +562,7 @@ static_assert(kWideSmemBytes <= 232448, "exceeds the 227 KB dynamic shared memor
 
 struct WideMaps {
     CUtensorMap ahi, alo, bhi, blo;
+    CUtensorMap bhi_h, blo_h;  // 64-row boxes: the halves a pair multicasts (clusters of 2 pairs)
 };
 
 template <int FMT>
@@ -880,7 +881,14 @@ constexpr size_t kNpSmemBytes = 1024 + size_t(kNpStages) * kNpStageBytes + sizeo
 static_assert(size_t(BM) * kNpCStride * 4 <= size_t(kNpStages) * kNpStageBytes,
               "C staging tile must fit in the operand stages");
 
-template <int FMT>
+// CL = CTA pairs per cluster.  CL = 2: two pairs on vertically adjacent
+// 256-row tiles of the same 256 B' columns share each B' tile -- CTA r of pair
+// p loads rows [64p, 64p + 64) of its 128-row B' tile and multicasts them to
+// CTA r of both pairs -- which halves the B' traffic from L2 to the SMs and
+// keeps the two pairs' B' reads in k-lockstep (one DRAM read per cluster).
+// A stage is refilled only when BOTH pairs' MMAs released it (empty barriers
+// count one commit per pair; the commits multicast to all four CTAs).
+template <int FMT, int CL>
 __device__ __forceinline__ void wide_body(const WideMaps& mp, float* __restrict__ c, int m, int n2,
                                           int kp, const DevDecision* __restrict__ dec, int kind,
                                           int corrected, int flush_kblocks, int group_m,
@@ -900,15 +908,22 @@ __device__ __forceinline__ void wide_body(const WideMaps& mp, float* __restrict_
     };
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_ctarank();
+    const uint32_t crank = cluster_ctarank();
+    const uint32_t rank = CL == 2 ? (crank & 1u) : crank;  // CTA within its pair
+    const int pr = CL == 2 ? int(crank >> 1) : 0;            // pair within the cluster
     const bool leader = rank == 0;
+    const uint16_t pair_mask = CL == 2 ? uint16_t(0x3u << (2 * pr)) : uint16_t(0x3);  // this pair's CTAs
+    const uint16_t all_mask = CL == 2 ? uint16_t(0xF) : uint16_t(0x3);
 
+    // raster over cluster tiles (CL vertically adjacent pair tiles), groups of
+    // group_m of them share B' panels in L2
     const int tiles_m = (m + 2 * BM - 1) / (2 * BM), tiles_n = (n2 + kNpBN - 1) / kNpBN;
-    const int id = blockIdx.x >> 1;
+    const int tiles_mc = CL == 2 ? (tiles_m + 1) >> 1 : tiles_m;
+    const int id = CL == 2 ? int(blockIdx.x >> 2) : int(blockIdx.x >> 1);
     const int group = group_m * tiles_n;
     const int first_m = (id / group) * group_m;
-    const int gsize = min(tiles_m - first_m, group_m);
-    const int m_blk = first_m + (id % group) % gsize;
+    const int gsize = min(tiles_mc - first_m, group_m);
+    const int m_blk = CL == 2 ? 2 * (first_m + (id % group) % gsize) + pr : first_m + (id % group) % gsize;
     const int n_blk = (id % group) / gsize;
     const int m0 = m_blk * 2 * BM + int(rank) * BM;  // this CTA's 128 rows
     const int n0 = n_blk * kNpBN;                  // the pair's 256 columns
@@ -926,7 +941,7 @@ __device__ __forceinline__ void wide_body(const WideMaps& mp, float* __restrict_
     if (threadIdx.x == 0) {
         for (int s = 0; s < kNpStages; ++s) {
             mbar_init(&tail->full[s], 1);
-            mbar_init(&tail->empty[s], 1);
+            mbar_init(&tail->empty[s], CL);  // one MMA commit per pair of the cluster
         }
         for (int h = 0; h < 2; ++h) {
             mbar_init(&tail->tfull[h], 1);
@@ -937,10 +952,10 @@ __device__ __forceinline__ void wide_body(const WideMaps& mp, float* __restrict_
     }
     if (warp == 0 && lane == 0) {
         tma_prefetch(&mp.ahi);
-        tma_prefetch(&mp.bhi);
+        tma_prefetch(CL == 2 ? &mp.bhi_h : &mp.bhi);
         if (corrected) {
             tma_prefetch(&mp.alo);
-            tma_prefetch(&mp.blo);
+            tma_prefetch(CL == 2 ? &mp.blo_h : &mp.blo);
         }
     }
     if (warp == 1) tmem_alloc_pair<kTmemCols>(&tail->tmem_base);
@@ -959,10 +974,17 @@ __device__ __forceinline__ void wide_body(const WideMaps& mp, float* __restrict_
                 if (leader) mbar_expect_tx(&tail->full[s], 2 * cta_bytes);
                 const int kx = (kb_base + kb) * T::kBK;
                 tma_load_2d_pair(tile(s, 0), &mp.ahi, &tail->full[s], kx, m0 + a_row_off);
-                tma_load_2d_pair(tile(s, 2), &mp.bhi, &tail->full[s], kx, nb0);
-                if (corrected) {
-                    tma_load_2d_pair(tile(s, 1), &mp.alo, &tail->full[s], kx, m0 + a_row_off);
-                    tma_load_2d_pair(tile(s, 3), &mp.blo, &tail->full[s], kx, nb0);
+                if (corrected) tma_load_2d_pair(tile(s, 1), &mp.alo, &tail->full[s], kx, m0 + a_row_off);
+                if constexpr (CL == 2) {
+                    // B' rows [64 pr, 64 pr + 64) of this CTA's tile, to CTA `rank` of both pairs
+                    const uint16_t mc = uint16_t((1u << rank) | (1u << (2 + rank)));
+                    const int off = pr * 64 * 128;
+                    tma_load_2d_pair_mc(tile(s, 2) + off, &mp.bhi_h, &tail->full[s], kx, nb0 + 64 * pr, mc);
+                    if (corrected)
+                        tma_load_2d_pair_mc(tile(s, 3) + off, &mp.blo_h, &tail->full[s], kx, nb0 + 64 * pr, mc);
+                } else {
+                    tma_load_2d_pair(tile(s, 2), &mp.bhi, &tail->full[s], kx, nb0);
+                    if (corrected) tma_load_2d_pair(tile(s, 3), &mp.blo, &tail->full[s], kx, nb0);
                 }
             }
         }
@@ -998,7 +1020,7 @@ __device__ __forceinline__ void wide_body(const WideMaps& mp, float* __restrict_
                             else
                                 mma2_tf32(tmem + uint32_t(128 * h), dah + adv, dbh_h + adv, kIdescHalf, acc);
                         }
-                        if (chunk_end) mma_commit_pair(&tail->tfull[h], 0x3);
+                        if (chunk_end) mma_commit_pair(&tail->tfull[h], pair_mask);
                     }
                     __syncwarp();
                 }
@@ -1017,8 +1039,8 @@ __device__ __forceinline__ void wide_body(const WideMaps& mp, float* __restrict_
                             }
                         }
                     }
-                    mma_commit_pair(&tail->empty[s], 0x3);
-                    if (kb == nkb - 1) mma_commit_pair(&tail->cfull, 0x3);
+                    mma_commit_pair(&tail->empty[s], all_mask);
+                    if (kb == nkb - 1) mma_commit_pair(&tail->cfull, pair_mask);
                 }
                 __syncwarp();
             }
@@ -1031,7 +1053,7 @@ __device__ __forceinline__ void wide_body(const WideMaps& mp, float* __restrict_
         const int p = (warp - 2) >> 2;
         const int rloc = 32 * q + lane;
         const uint32_t lane_base = tmem + (uint32_t(32 * q) << 16);
-        const uint32_t tempty_leader = mapa_shared(smem_u32(&tail->tempty[p]), 0);
+        const uint32_t tempty_leader = mapa_shared(smem_u32(&tail->tempty[p]), CL == 2 ? (crank & ~1u) : 0u);
         float acc[128];
 #pragma unroll
         for (int i = 0; i < 128; ++i) acc[i] = -0.0f;  // RN identity
@@ -1125,8 +1147,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
     const int kind = kind_fixed >= 0 ? kind_fixed : dec->kind;
     const bool mine = FMT == kTf32 ? kind == kKindTf32 : (kind == kKindFp16 || kind == kKindFp16Scaled);
     if (!mine) return;  // both CTAs of the pair read the same decision
-    wide_body<FMT>(maps, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off, ldc,
-                   partial, kb_per);
+    wide_body<FMT, 1>(maps, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off, ldc,
+                      partial, kb_per);
+}
+
+// clusters of two CTA pairs sharing B' tiles by TMA multicast
+template <int FMT>
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreadsGemm, 1)
+    tcec_gemm_widemc_kernel(const __grid_constant__ WideMaps maps, float* __restrict__ c, int m,
+                            int n2, int kp, const DevDecision* __restrict__ dec, int kind_fixed,
+                            int corrected, int flush_kblocks, int group_m, int a_row_off, int ldc,
+                            float* __restrict__ partial, int kb_per) {
+    const int kind = kind_fixed >= 0 ? kind_fixed : dec->kind;
+    const bool mine = FMT == kTf32 ? kind == kKindTf32 : (kind == kKindFp16 || kind == kKindFp16Scaled);
+    if (!mine) return;  // all four CTAs read the same decision
+    wide_body<FMT, 2>(maps, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off, ldc,
+                      partial, kb_per);
 }
 
 // format decided on the device (AUTO): one launch that runs the selected
@@ -1139,11 +1175,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
                                int ldc, float* __restrict__ partial, int kb_per) {
     const int kind = dec->kind;
     if (kind == kKindTf32)
-        wide_body<kTf32>(maps32, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off,
-                         ldc, partial, kb_per);
+        wide_body<kTf32, 1>(maps32, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off,
+                            ldc, partial, kb_per);
     else if (kind == kKindFp16 || kind == kKindFp16Scaled)
-        wide_body<kFp16>(maps16, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off,
-                         ldc, partial, kb_per);
+        wide_body<kFp16, 1>(maps16, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off,
+                            ldc, partial, kb_per);
+}
+
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreadsGemm, 1)
+    tcec_gemm_widemc_auto_kernel(const __grid_constant__ WideMaps maps16,
+                                 const __grid_constant__ WideMaps maps32, float* __restrict__ c,
+                                 int m, int n2, int kp, const DevDecision* __restrict__ dec,
+                                 int corrected, int flush_kblocks, int group_m, int a_row_off,
+                                 int ldc, float* __restrict__ partial, int kb_per) {
+    const int kind = dec->kind;
+    if (kind == kKindTf32)
+        wide_body<kTf32, 2>(maps32, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off,
+                            ldc, partial, kb_per);
+    else if (kind == kKindFp16 || kind == kKindFp16Scaled)
+        wide_body<kFp16, 2>(maps16, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off,
+                            ldc, partial, kb_per);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -1187,7 +1238,8 @@ bool make_wide_maps(WideMaps* w, const TcecGemmArgs& g, int fmt) {
     const void* bhi = static_cast<const uint8_t*>(g.b_hi) + boff;
     blo = static_cast<const uint8_t*>(blo) + boff;
     return make_map(&w->ahi, g.a_hi, fmt, arows, g.kp, 128u) && make_map(&w->alo, alo, fmt, arows, g.kp, 128u) &&
-           make_map(&w->bhi, bhi, fmt, g.n2, g.kp, 128u) && make_map(&w->blo, blo, fmt, g.n2, g.kp, 128u);
+           make_map(&w->bhi, bhi, fmt, g.n2, g.kp, 128u) && make_map(&w->blo, blo, fmt, g.n2, g.kp, 128u) &&
+           make_map(&w->bhi_h, bhi, fmt, g.n2, g.kp, 64u) && make_map(&w->blo_h, blo, fmt, g.n2, g.kp, 64u);
 }
 
 // rasterization group (M tiles per group) of the wide kernel; TCEC_GROUP_M
@@ -1229,13 +1281,21 @@ int launch_fmt(const TcecGemmArgs& g, cudaStream_t s) {
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(tcec_gemm_widep_kernel<FMT>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(kWideSmemBytes));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(tcec_gemm_widemc_kernel<FMT>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNpSmemBytes));
         return e;
     });
     if (ea != cudaSuccess) return int(ea);
-    if (g.pair == kVariantWide || g.pair == kVariantWidePersistent) {
+    if (g.pair == kVariantWide || g.pair == kVariantWidePersistent || g.pair == kVariantWideMc) {
         WideMaps w;
         if (!make_wide_maps(&w, g, FMT)) return int(cudaErrorInvalidValue);
-        if (g.pair == kVariantWide)
+        if (g.pair == kVariantWideMc)
+            tcec_gemm_widemc_kernel<FMT><<<dim3(wide_tiles_grid(g), unsigned(g.partial ? g.splits : 1)),
+                                           kThreadsGemm, kNpSmemBytes, s>>>(
+                w, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed, g.corrected, g.flush_kblocks,
+                wide_group_m(), int(g.a_row_off), int(g.ldc > 0 ? g.ldc : g.n2), g.partial, g.kb_per);
+        else if (g.pair == kVariantWide)
             tcec_gemm_wide_kernel<FMT><<<dim3(wide_tiles_grid(g), unsigned(g.partial ? g.splits : 1)),
                                          kThreadsGemm, kNpSmemBytes, s>>>(
                 w, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed, g.corrected, g.flush_kblocks,
@@ -1277,13 +1337,21 @@ int launch_wide_auto(const TcecGemmArgs& g, cudaStream_t s) {
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(tcec_gemm_widep_auto_kernel,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(kWideSmemBytes));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(tcec_gemm_widemc_auto_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNpSmemBytes));
         return e;
     });
     if (ea != cudaSuccess) return int(ea);
     WideMaps w16, w32;
     if (!make_wide_maps(&w16, g, kFp16) || !make_wide_maps(&w32, g, kTf32))
         return int(cudaErrorInvalidValue);
-    if (g.pair == kVariantWide)
+    if (g.pair == kVariantWideMc)
+        tcec_gemm_widemc_auto_kernel<<<dim3(wide_tiles_grid(g), unsigned(g.partial ? g.splits : 1)),
+                                       kThreadsGemm, kNpSmemBytes, s>>>(
+            w16, w32, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.corrected, g.flush_kblocks,
+            wide_group_m(), int(g.a_row_off), int(g.ldc > 0 ? g.ldc : g.n2), g.partial, g.kb_per);
+    else if (g.pair == kVariantWide)
         tcec_gemm_wide_auto_kernel<<<dim3(wide_tiles_grid(g), unsigned(g.partial ? g.splits : 1)),
                                      kThreadsGemm, kNpSmemBytes, s>>>(
             w16, w32, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.corrected, g.flush_kblocks,
@@ -1316,11 +1384,13 @@ int launch_tcec_gemm(const TcecGemmArgs& g_in, cudaStream_t s) {
     g.partial = nullptr;
     g.splits = 1;
     g.kb_per = 0;
+    // clusters of two pairs need an even number of 256-row tiles
+    if (g.pair == kVariantWideMc && ((g.m + 2 * BM - 1) / (2 * BM)) % 2 != 0) g.pair = kVariantWide;
     if (g.ldc > 0 && g.ldc != g.n2) g.no_split = 1;  // partials and their reduction assume ldc = n2
-    if (!g.no_split && (g.pair == kVariantSingle || g.pair == kVariantWide)) {
+    if (!g.no_split && (g.pair == kVariantSingle || g.pair == kVariantWide || g.pair == kVariantWideMc)) {
         // few tiles and a long K (e.g. (512, 512, 2^19) contraction steps):
         // split K so the grid covers the SMs several times
-        const int64_t tiles = g.pair == kVariantWide
+        const int64_t tiles = g.pair != kVariantSingle
                                   ? int64_t(wide_tiles_grid(g))
                                   : ((g.m + BM - 1) / BM) * ((g.n2 + BN - 1) / BN);
         const int bk = (g.fmt == kTf32 || g.fmt < 0) ? 32 : 64;  // the finer format decides
@@ -1353,7 +1423,7 @@ int launch_tcec_gemm(const TcecGemmArgs& g_in, cudaStream_t s) {
             // partial round trip stays small against its MMA time
             int64_t want = std::min<int64_t>((waves * sms + tiles - 1) / tiles, (g.kp / 64) / 32);
             split_with(want);
-        } else if (tiles < 8 * sms && g.pair == kVariantWide && (g.kp / 64) / 32 >= 2) {
+        } else if (tiles < 8 * sms && g.pair != kVariantSingle && (g.kp / 64) / 32 >= 2) {
             // a few waves of long tiles: split K just enough that the last wave
             // is nearly full (e.g. 512 CTAs = 3.46 waves -> 2 splits = 6.92
             // waves: (4096, 2048, 65536) TF32 steps of the Sycamore slices)
@@ -1387,7 +1457,8 @@ static int launch_formats(const TcecGemmArgs& g, cudaStream_t s) {
     if (g.fmt < 0) {
         // device-decided format: the wide kernel branches on the decision; the
         // other variants launch both formats and the unselected one exits
-        if (g.pair == kVariantWide || g.pair == kVariantWidePersistent) return launch_wide_auto(g, s);
+        if (g.pair == kVariantWide || g.pair == kVariantWidePersistent || g.pair == kVariantWideMc)
+            return launch_wide_auto(g, s);
         const int e = launch_fmt<kFp16>(g, s);
         return e ? e : launch_fmt<kTf32>(g, s);
     }

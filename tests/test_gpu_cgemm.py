@@ -12,7 +12,7 @@ import pytest
 import torch
 
 import oracle as O
-from paper_2303_08989_b200 import InvalidArgument, SelectionPolicy, ShapeMismatch
+from paper_2303_08989_b200 import InvalidArgument, SelectionPolicy, ShapeMismatch, make_config
 from tests.conftest import bits
 from tests.golden.recipes import matrix_recipe
 
@@ -87,7 +87,7 @@ def test_tcec_ragged_shapes(handle, orc, dev, shape):
         assert e <= max(TOL_FACTOR * err_ref, 2e-7), (mode, e, err_ref)
 
 
-@pytest.mark.parametrize("variant", ["single", "pair", "wide", "wide_persistent"])
+@pytest.mark.parametrize("variant", ["single", "pair", "wide", "wide_persistent", "wide_mc"])
 @pytest.mark.parametrize("shape", [(3, 5, 7), (129, 65, 200), (300, 257, 31), (513, 385, 129),
                                    (130, 130, 1100), (600, 300, 2100)])
 def test_tcec_kernel_variants(handle, orc, dev, variant, shape):
@@ -114,7 +114,7 @@ def test_tcec_kernel_variants(handle, orc, dev, variant, shape):
         assert errs["FP16TC"] >= 10 * errs["FP16TCEC"], errs
 
 
-@pytest.mark.parametrize("variant", ["single", "wide", "wide_persistent"])
+@pytest.mark.parametrize("variant", ["single", "wide", "wide_persistent", "wide_mc"])
 def test_tcec_all_positive_long_k(handle, orc, dev, variant):
     """All-positive operands make tensor-core truncation a systematic bias;
     the per-k-block RN flush keeps TCEC within the reference bar."""
@@ -318,3 +318,34 @@ def test_split_k_few_tiles_long_k(handle, orc, dev, shape, variant):
         assert relerr(c.cpu().numpy() * 2.0 ** 20, ref) <= TOL_FACTOR * err_ref
     finally:
         handle.set_gemm_variant("auto")
+
+
+@pytest.mark.parametrize("shape", [(512, 256, 64), (512, 300, 100), (1024, 1000, 333), (2048, 512, 1000),
+                                   (768, 640, 129), (512, 512, 9000), (4096, 2048, 512)])
+@pytest.mark.parametrize("mode", ["FP16TCEC", "TF32TCEC", "AUTO", "SCALED"])
+def test_multicast_clusters_bit_identical_to_pairs(handle, dev, shape, mode):
+    """Clusters of two CTA pairs sharing B' tiles by TMA multicast run the same
+    MMA sequence on the same operand bits as the single-pair wide kernel, so C
+    is bit-identical -- odd tile counts (fallback), split-K (512^2 x 9000),
+    the device-decided format (AUTO) and the scaled kind included."""
+    m, n, k = shape
+    a = matrix_recipe("uniform", m, k, 7 + m)
+    b = matrix_recipe("uniform", k, n, 9 + n)
+    if mode == "SCALED":
+        a = (a * np.float32(2.0 ** -20)).astype(np.complex64)
+    ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    if mode in ("AUTO", "SCALED"):
+        cfg = make_config(SelectionPolicy(size_auto=32, size_tf32=16))
+    else:
+        cfg = make_config(force=mode)
+    outs, lines = {}, {}
+    for variant in ("wide", "wide_mc"):
+        handle.set_gemm_variant(variant)
+        try:
+            c, res = handle.dispatch_cgemm(ad, bd, cfg)
+            outs[variant] = c.cpu().numpy()
+            lines[variant] = res.line
+        finally:
+            handle.set_gemm_variant("auto")
+    assert lines["wide"] == lines["wide_mc"]
+    assert np.array_equal(outs["wide"].view(np.uint32), outs["wide_mc"].view(np.uint32)), lines["wide"]
