@@ -302,7 +302,7 @@ def cgemm_headline(args, world, rank, local):
     e2e_ms = e2e_run(a_np, b_np, c_np, args.steps)
     pipe_runs, pipe_reruns = h.host_pipeline_stats()
     e2e_pageable_ms = None
-    if args.pageable:
+    if args.pageable and world == 1:
         # the drop-in's std::vector storage is pageable: same call on plain numpy copies
         a_pg, b_pg = np.array(a_np, copy=True), np.array(b_np, copy=True)
         c_pg = np.empty_like(c_np)

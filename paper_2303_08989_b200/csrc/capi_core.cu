@@ -155,7 +155,13 @@ TcecGemmArgs tc_gemm_args(const Handle& h, const DispatchPlan& p, void* ws, floa
     g.d = d;
     g.kind_fixed = p.kind;
     g.corrected = p.corrected;
-    g.flush_kblocks = p.corrected ? h.flush_kblocks : 0;
+    // TF32 flush interval (its own 32-element k-blocks) in the high half;
+    // TCEC_TF32_FLUSH overrides it (0 = as many k-blocks as FP16)
+    static const int tf32_flush = [] {
+        const char* e = std::getenv("TCEC_TF32_FLUSH");
+        return e ? std::max(0, std::min(64, std::atoi(e))) : 0;
+    }();
+    g.flush_kblocks = p.corrected ? (h.flush_kblocks | (h.flush_kblocks > 0 ? tf32_flush << 16 : 0)) : 0;
     g.pair = resolve_gemm_variant(h.gemm_pair, m, 2 * n, p.kp, h.sm_count);
     g.sms = h.sm_count;
     g.fmt = (p.kind < 0 && !p.forced_scaled) ? -1  // format chosen by the device decision

@@ -211,6 +211,14 @@ TCEC_DEV void mma_commit(uint64_t* bar) {
         : "memory");
 }
 
+// RN flush interval of the TCEC main term in the kernel's own k-blocks:
+// `packed` carries the FP16 interval (k-blocks of 64 elements) in its low 16
+// bits and, when non-zero, the TF32 interval (k-blocks of 32) in its high 16
+TCEC_DEV int flush_of(int packed, int fmt) {
+    const int tf = (packed >> 16) & 0xFFFF;
+    return (fmt == 1 && tf > 0) ? tf : (packed & 0xFFFF);
+}
+
 // ---------------------------------------------------- CTA pair (cta_group::2)
 TCEC_DEV uint32_t cluster_ctarank() {
     uint32_t r;

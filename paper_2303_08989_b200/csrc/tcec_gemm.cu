@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
     const int per = FMT == kTf32 ? 2 * kb_per : kb_per;  // kb_per counts 64-element f16 blocks
     const int kb_base = partial ? int(blockIdx.y) * per : 0;
     const int nkb = partial ? min(per, nkb_all - kb_base) : nkb_all;
-    const int F = flush_kblocks > 0 ? flush_kblocks : (nkb > 0 ? nkb : 1);
+    const int F = flush_of(flush_kblocks, FMT) > 0 ? flush_of(flush_kblocks, FMT) : (nkb > 0 ? nkb : 1);
     const int nchunks = (nkb + F - 1) / F;
     const uint32_t stage_bytes = uint32_t(corrected ? 4 : 2) * kTileBytes;
 
@@ -358,7 +358,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
     const int n0 = n_blk * BN;                       // the pair's 128 columns
 
     const int nkb = kp / T::kBK;
-    const int F = flush_kblocks > 0 ? flush_kblocks : (nkb > 0 ? nkb : 1);
+    const int F = flush_of(flush_kblocks, FMT) > 0 ? flush_of(flush_kblocks, FMT) : (nkb > 0 ? nkb : 1);
     const int nchunks = (nkb + F - 1) / F;
     const uint32_t cta_bytes = corrected ? uint32_t(kPairStageBytes)
                                          : uint32_t(kPairATile + kPairBTile);
@@ -599,7 +599,7 @@ __device__ __forceinline__ void widep_body(const WideMaps& mp, float* __restrict
     };
 
     const int nkb = kp / T::kBK;
-    const int F = flush_kblocks > 0 ? flush_kblocks : nkb;
+    const int F = flush_of(flush_kblocks, FMT) > 0 ? flush_of(flush_kblocks, FMT) : nkb;
     const int nchunks = (nkb + F - 1) / F;
     const uint32_t cta_bytes = uint32_t(corrected ? 4 : 2) * kTileBytes;
 
@@ -934,7 +934,7 @@ __device__ __forceinline__ void wide_body(const WideMaps& mp, float* __restrict_
     const int per = FMT == kTf32 ? 2 * kb_per : kb_per;  // kb_per counts 64-element f16 blocks
     const int kb_base = partial ? int(blockIdx.y) * per : 0;
     const int nkb = partial ? min(per, nkb_all - kb_base) : nkb_all;
-    const int F = flush_kblocks > 0 ? flush_kblocks : (nkb > 0 ? nkb : 1);
+    const int F = flush_of(flush_kblocks, FMT) > 0 ? flush_of(flush_kblocks, FMT) : (nkb > 0 ? nkb : 1);
     const int nchunks = (nkb + F - 1) / F;
     const uint32_t cta_bytes = uint32_t(corrected ? 4 : 2) * kTileBytes;
 
