@@ -329,6 +329,10 @@ tcec::DevDecision* tcec_handle_s::decisions(int slots) {
     const int want = slots < 16 ? 16 : slots;
     if (cudaMalloc(&dec, sizeof(tcec::DevDecision) * want) != cudaSuccess) return nullptr;
     if (cudaMallocHost(&dec_host, sizeof(tcec::DevDecision) * want) != cudaSuccess) return nullptr;
+    // slots of SIMT-tier steps are never written by a kernel but are read back
+    // with the others (contraction logs): start them defined
+    if (cudaMemset(dec, 0, sizeof(tcec::DevDecision) * want) != cudaSuccess) return nullptr;
+    std::memset(dec_host, 0, sizeof(tcec::DevDecision) * want);
     dec_slots = want;
     return dec;
 }

@@ -455,6 +455,7 @@ static int ensure_lanes(tcec_network_s& net, int count, const FoldPlan& plan) {
             ln.dec = nullptr;
             ln.dec_slots = 0;
             e = cudaMalloc(&ln.dec, sizeof(tcec::DevDecision) * size_t(slots));
+            if (e == cudaSuccess) e = cudaMemset(ln.dec, 0, sizeof(tcec::DevDecision) * size_t(slots));
             if (e == cudaSuccess) ln.dec_slots = slots;
         }
         if (e == cudaSuccess && ln.ws_bytes < plan.ws_bytes) {

@@ -19,6 +19,7 @@ p.add_argument("--k", type=int, default=0)
 p.add_argument("--mode", default="AUTO")
 p.add_argument("--flush", type=int, default=-1)
 p.add_argument("--reps", type=int, default=3)
+p.add_argument("--variant", default="auto")
 p.add_argument("--ref-inputs", action="store_true",
                help="configs[1] operands from the reference generator Rng(1 + n) (square only)")
 a = p.parse_args()
@@ -27,6 +28,7 @@ dev = torch.device("cuda:0")
 h = Handle(0)
 if a.flush >= 0:
     h.flush_kblocks = a.flush
+h.set_gemm_variant(a.variant)
 if a.ref_inputs:
     from paper_2303_08989_b200.workload import sweep_operands
     Ah, Bh = sweep_operands(n, m=m, k=k)
