@@ -113,46 +113,62 @@ TCEC_DEV unsigned block_max(unsigned v, unsigned* red) {
     return r;
 }
 
+// Both statistics stages sweep the two operands in one 1-D grid: blocks
+// [0, nb_a) take contiguous float4 chunks of A, the rest of B, so each
+// operand gets blocks in proportion to its size (a 2 MB A next to a 64 MB B
+// no longer idles half the grid), and every thread keeps four independent
+// 16-B loads in flight (these sweeps were latency-bound at mid sizes).
+template <typename Visit>
+TCEC_DEV void sweep_operand(const float* __restrict__ x, int64_t n, int part, int nparts, Visit&& visit) {
+    const bool vec = (reinterpret_cast<uintptr_t>(x) & 15u) == 0;
+    const int64_t n4 = vec ? n / 4 : 0;
+    const int64_t per = (n4 + nparts - 1) / nparts;
+    const int64_t b0 = min(n4, int64_t(part) * per), b1 = min(n4, b0 + per);
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    const int bd = int(blockDim.x);
+    int64_t i = b0 + threadIdx.x;
+    for (; i + 3 * bd < b1; i += 4 * bd) {
+        const float4 v0 = __ldcs(x4 + i), v1 = __ldcs(x4 + i + bd), v2 = __ldcs(x4 + i + 2 * bd),
+                     v3 = __ldcs(x4 + i + 3 * bd);
+        visit(v0.x); visit(v0.y); visit(v0.z); visit(v0.w);
+        visit(v1.x); visit(v1.y); visit(v1.z); visit(v1.w);
+        visit(v2.x); visit(v2.y); visit(v2.z); visit(v2.w);
+        visit(v3.x); visit(v3.y); visit(v3.z); visit(v3.w);
+    }
+    for (; i < b1; i += bd) {
+        const float4 v = __ldcs(x4 + i);
+        visit(v.x); visit(v.y); visit(v.z); visit(v.w);
+    }
+    if (part == nparts - 1)  // scalar tail (and the whole operand when unaligned)
+        for (int64_t j = n4 * 4 + threadIdx.x; j < n; j += bd) visit(x[j]);
+}
+
 // stage 1 (precsel.cpp:23-32 via abs_stats, kernels_scalar.cpp:50-65):
-// nonzero count, count of |x| >= 2^-14, max |x| -- one coalesced float4 sweep
+// nonzero count, count of |x| >= 2^-14, max |x|
 __global__ void __launch_bounds__(kThreads) stats1_kernel(const float* a, int64_t na,
                                                           const float* b, int64_t nb,
-                                                          DevDecision* d) {
-    const float* x = blockIdx.y ? b : a;
-    const int64_t n = blockIdx.y ? nb : na;
-    if (x == nullptr || n == 0) return;
+                                                          DevDecision* d, int nb_a) {
+    const int op = int(blockIdx.x) < nb_a ? 0 : 1;
+    const float* x = op ? b : a;
+    const int64_t n = op ? nb : na;
+    const int part = op ? int(blockIdx.x) - nb_a : int(blockIdx.x);
+    const int nparts = op ? int(gridDim.x) - nb_a : nb_a;
+    if (x == nullptr || n == 0 || nparts <= 0) return;
     unsigned nz = 0, n1 = 0, mx = 0;
-    auto visit = [&](float v) {
+    sweep_operand(x, n, part, nparts, [&](float v) {
         const uint32_t m = __float_as_uint(v) & 0x7FFFFFFFu;
         const bool ok = valid_mag(m);
         nz += ok;
         n1 += ok && m >= kFp16MinNormalBits;
         mx = max(mx, ok ? m : 0u);
-    };
-    const int64_t tid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    int64_t head = 0;
-    if ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) {
-        const int64_t n4 = n / 4;
-        const float4* x4 = reinterpret_cast<const float4*>(x);
-        for (int64_t i = tid; i < n4; i += stride) {
-            const float4 v = __ldcs(x4 + i);
-            visit(v.x);
-            visit(v.y);
-            visit(v.z);
-            visit(v.w);
-        }
-        head = n4 * 4;
-    }
-    for (int64_t i = head + tid; i < n; i += stride) visit(x[i]);
-
+    });
     __shared__ unsigned long long red64[kThreads / 32];
     __shared__ unsigned red32[kThreads / 32];
     const unsigned long long snz = block_sum<unsigned long long>(nz, red64);
     const unsigned long long sn1 = block_sum<unsigned long long>(n1, red64);
     const unsigned smx = block_max(mx, red32);
     if (threadIdx.x == 0) {
-        DevStats& st = d->st[blockIdx.y];
+        DevStats& st = d->st[op];
         if (snz) atomicAdd(&st.n_nonzero, snz);
         if (sn1) atomicAdd(&st.n1, sn1);
         if (smx) atomicMax(&st.max_bits, smx);
@@ -172,40 +188,27 @@ TCEC_DEV bool stage1_passes(unsigned long long nz, unsigned long long n1, unsign
 __global__ void __launch_bounds__(kThreads) stats2_kernel(const float* a, int64_t na,
                                                           const float* b, int64_t nb,
                                                           DevDecision* d, double t, int target,
-                                                          int always) {
-    const float* x = blockIdx.y ? b : a;
-    const int64_t n = blockIdx.y ? nb : na;
-    if (x == nullptr || n == 0) return;
-    const DevStats st = d->st[blockIdx.y];
+                                                          int always, int nb_a) {
+    const int op = int(blockIdx.x) < nb_a ? 0 : 1;
+    const float* x = op ? b : a;
+    const int64_t n = op ? nb : na;
+    const int part = op ? int(blockIdx.x) - nb_a : int(blockIdx.x);
+    const int nparts = op ? int(gridDim.x) - nb_a : nb_a;
+    if (x == nullptr || n == 0 || nparts <= 0) return;
+    const DevStats st = d->st[op];
     if (!always && stage1_passes(st.n_nonzero, st.n1, st.max_bits, t, target)) return;
     if (st.max_bits == 0) return;  // no e_max: n2 = 0
     const int w = exponent_of_bits(st.max_bits) - (target + 14);
     // ldexp(1.0f, w): a normal, a subnormal power of two, or 0 (all nonzero pass)
     const uint32_t thr = w >= -126 ? uint32_t(w + 127) << 23 : (w >= -149 ? 1u << (w + 149) : 1u);
     unsigned cnt = 0;
-    auto visit = [&](float v) {
+    sweep_operand(x, n, part, nparts, [&](float v) {
         const uint32_t m = __float_as_uint(v) & 0x7FFFFFFFu;
         cnt += valid_mag(m) && m >= thr;
-    };
-    const int64_t tid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    int64_t head = 0;
-    if ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) {
-        const int64_t n4 = n / 4;
-        const float4* x4 = reinterpret_cast<const float4*>(x);
-        for (int64_t i = tid; i < n4; i += stride) {
-            const float4 v = __ldcs(x4 + i);
-            visit(v.x);
-            visit(v.y);
-            visit(v.z);
-            visit(v.w);
-        }
-        head = n4 * 4;
-    }
-    for (int64_t i = head + tid; i < n; i += stride) visit(x[i]);
+    });
     __shared__ unsigned long long red64[kThreads / 32];
     const unsigned long long s = block_sum<unsigned long long>(cnt, red64);
-    if (threadIdx.x == 0 && s) atomicAdd(&d->st[blockIdx.y].n2, s);
+    if (threadIdx.x == 0 && s) atomicAdd(&d->st[op].n2, s);
 }
 
 // finalize ExpStats, tolerance levels and the pair rule (precsel.cpp:95-135)
@@ -1467,18 +1470,31 @@ void launch_add_sub(const float* a, const float* b, float* dst, int64_t n, int s
     add_sub_kernel<<<grid_for(n, kThreads), kThreads, 0, s>>>(a, b, dst, n, sub);
 }
 
+// blocks of the statistics sweeps: one wave of 8 x 256-thread blocks per SM
+// at most, split between A and B in proportion to their sizes (>= 1 each)
+static void stats_grid(int64_t na, int64_t nb, const float* a, const float* b, int* total, int* nb_a) {
+    const int64_t ea = a ? na : 0, eb = b ? nb : 0;
+    const int64_t want = (ea + eb) / (4 * kThreads * 4) + 2;  // >= 4 float4 per thread
+    const int tot = int(std::min<int64_t>(148 * 8, std::max<int64_t>(2, want)));
+    int ba = ea ? int(std::max<int64_t>(1, std::min<int64_t>(tot - 1, (tot * ea + ea + eb - 1) / (ea + eb))))
+                : 0;
+    if (!eb) ba = ea ? tot : 0;
+    *nb_a = ba;
+    *total = std::max(1, eb ? tot : ba);
+}
+
 void launch_stats1(const float* a, int64_t na, const float* b, int64_t nb, DevDecision* d,
                    cudaStream_t s) {
-    const int64_t nmax = na > nb ? na : nb;
-    dim3 grid(grid_for(nmax / 4 + 1, kThreads, 148 * 8), 2);
-    stats1_kernel<<<grid, kThreads, 0, s>>>(a, na, b, nb, d);
+    int total = 0, nb_a = 0;
+    stats_grid(na, nb, a, b, &total, &nb_a);
+    stats1_kernel<<<total, kThreads, 0, s>>>(a, na, b, nb, d, nb_a);
 }
 
 void launch_stats2(const float* a, int64_t na, const float* b, int64_t nb, DevDecision* d,
                    double t, int target, int always, cudaStream_t s) {
-    const int64_t nmax = na > nb ? na : nb;
-    dim3 grid(grid_for(nmax / 4 + 1, kThreads, 148 * 8), 2);
-    stats2_kernel<<<grid, kThreads, 0, s>>>(a, na, b, nb, d, t, target, always);
+    int total = 0, nb_a = 0;
+    stats_grid(na, nb, a, b, &total, &nb_a);
+    stats2_kernel<<<total, kThreads, 0, s>>>(a, na, b, nb, d, t, target, always, nb_a);
 }
 
 void launch_select(DevDecision* d, double t, int target, int forced_scaled, cudaStream_t s) {
