@@ -188,10 +188,19 @@ def dist_setup(gpus=None):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TCEC_BENCH_SHARED_GPU=1: every rank on cuda:0 with gloo -- exercises the
+    # N > 1 code path on a one-GPU box (NCCL refuses two ranks on one GPU);
+    # never used for a reported number
+    shared = os.environ.get("TCEC_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
+        if shared and not dist.is_initialized():
+            dist.init_process_group("gloo")
+            return world, rank, local
         # NCCL's own log stays on (transport / NVLS lines), in files next to the run
         logdir = os.path.join(ROOT, "gpurun_out")
         os.makedirs(logdir, exist_ok=True)
@@ -214,7 +223,8 @@ def max_over_ranks(x, world):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
