@@ -1200,8 +1200,10 @@ def spawn_ranks(gpus):
     logdir = os.path.join(ROOT, "gpurun_out")
     os.makedirs(logdir, exist_ok=True)
     env.setdefault("NCCL_DEBUG_FILE", os.path.join(logdir, "nccl.%h.%p.log"))
+    # "--" ends torchrun's own options, so none of ours is taken as an
+    # abbreviation of one of its flags
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
-           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)]
+           "--master-addr", "127.0.0.1", "--master-port", str(port), "--", os.path.abspath(__file__)]
     cmd += sys.argv[1:]
     return subprocess.call(cmd, env=env)
 
