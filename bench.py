@@ -553,47 +553,6 @@ def rqc_reference_rate(bits, nq, rows, cols, depth, seed, threads, cfg_kw=None):
     return len(bits) / dt, dt, out.view(np.complex64)
 
 
-def statevector_c128(circuit, dev):
-    """complex128 state vector of a circuit on the GPU (torch; qubit q = bit q
-    of the index): the fidelity reference of the 4x4 leg (the oracle package is
-    test infrastructure and stays out of the measured legs)."""
-    import torch
-    from paper_2303_08989_b200.circuits import CZ, gate_matrix
-    n = circuit.n_qubits
-    st = torch.zeros(1 << n, dtype=torch.complex128, device=dev)
-    st[0] = 1.0
-    for layer in circuit.layers:
-        for g in layer:
-            if g.kind == CZ:
-                # index bit q is tensor axis n-1-q of a (2,)*n view
-                v = st.view((2,) * n)
-                ax_a, ax_b = n - 1 - g.qubits[0], n - 1 - g.qubits[1]
-                idx = [slice(None)] * n
-                idx[ax_a] = 1
-                idx[ax_b] = 1
-                v[tuple(idx)] *= -1
-                continue
-            u = torch.tensor(np.asarray(gate_matrix(g.kind), np.complex128), device=dev)
-            if len(g.qubits) == 2:
-                u = u.reshape(2, 2, 2, 2)  # (out_a, out_b, in_a, in_b)
-                v = st.view((2,) * n)
-                ax_a, ax_b = n - 1 - g.qubits[0], n - 1 - g.qubits[1]
-                v = torch.tensordot(u, v, dims=([2, 3], [ax_a, ax_b]))  # new axes 0,1 = a, b
-                rest = [i for i in range(n) if i not in (ax_a, ax_b)]
-                order = [0] * n
-                order[ax_a], order[ax_b] = 0, 1
-                for pos, ax in enumerate(rest):
-                    order[ax] = 2 + pos
-                st = v.permute(*order).contiguous().reshape(-1)
-            else:
-                u = u.reshape(2, 2)
-                v = st.view((2,) * n)
-                ax = n - 1 - g.qubits[0]
-                v = torch.movedim(torch.tensordot(u, v, dims=([1], [ax])), 0, ax)
-                st = v.contiguous().reshape(-1)
-    return st
-
-
 def run_rqc(args, emit=True):
     """configs[0]: 4x4 rectangular RQC, H + 8 CZ layers + H, every output amplitude."""
     import torch
@@ -661,7 +620,8 @@ def run_rqc(args, emit=True):
     e2e_ms = max_over_ranks(max(e0.elapsed_time(e1) / args.steps, wall), world)
     ms = max_over_ranks(dev_ms / max(n_batches, 1), world)  # bitstrings resident in HBM
     if rank == 0:
-        sv = statevector_c128(circ, dev).cpu().numpy()
+        from paper_2303_08989_b200.network import statevector_oracle
+        sv = statevector_oracle(h, circ).cpu().numpy()  # the reference's f64 oracle, on the device
         idx = np.array([sum(int(b) << q for q, b in enumerate(x)) for x in mine])
         ref = sv[idx]
         err = float(np.max(np.abs(amps.astype(np.complex128) - ref) / np.abs(ref)))
@@ -786,10 +746,13 @@ def run_sycamore(args, emit=True):
         from paper_2303_08989_b200.slicing import assignment, slice_spec
         sub = slice_spec(spec, plan.sliced, assignment(0, plan.dims))
         t1 = time.perf_counter()
-        z128 = contract_c128(sub, path, dev)
+        onet = Network(h, sub)
+        z64 = complex(onet.contract_oracle(path).data.reshape(-1)[0])
+        onet.close()
         torch.cuda.empty_cache()
-        fid = {"slice0_rel_err_vs_c128": float(abs(complex(full[0]) - z128) / abs(z128)),
-               "reference": "complex128 contraction of slice 0 along the same path (torch)",
+        fid = {"slice0_rel_err_vs_f64_oracle": float(abs(complex(full[0]) - z64) / abs(z64)),
+               "reference": "contract_network_oracle of slice 0 along the same path (network.cpp:179-186; "
+                            "f64 fold on the device, bit-identical to the reference's CPU oracle)",
                "reference_s": round(time.perf_counter() - t1, 2)}
         line = {
             "metric": f"{SYC_METRIC[:-9]}, m={cycles}, {plan.n_slices} slices, AUTO-0)", "value": round(1e3 / ms, 4), "unit": "amplitudes/s",
@@ -921,26 +884,16 @@ def run_skewed(args, emit=True):
         return _compact_leg(line) if rank == 0 else None
 
 
-def contract_c128(spec, path, dev):
-    """complex128 contraction of a NetworkSpec along an SSA path (torch on the
-    GPU): the fidelity reference of the deep-circuit study.  Same label order
-    as ttgt_contract (free_a | free_b, network.cpp:58-85)."""
-    import torch
-    live = {i: (list(ls), torch.from_numpy(np.asarray(d, np.complex64).reshape(ds if ds else [1])
-                                           ).to(dev, torch.complex128).reshape(ds if ds else []))
-            for i, (ls, ds, d) in enumerate(zip(spec.labels, spec.dims, spec.data))}
-    nxt = len(spec.labels)
-    for ia, ib in path:
-        la, ta = live.pop(ia)
-        lb, tb = live.pop(ib)
-        shared = [l for l in la if l in lb]
-        ia_ax = [la.index(l) for l in shared]
-        ib_ax = [lb.index(l) for l in shared]
-        t = torch.tensordot(ta, tb, dims=(ia_ax, ib_ax))
-        live[nxt] = ([l for l in la if l not in shared] + [l for l in lb if l not in shared], t)
-        nxt += 1
-    (_, t), = live.values()
-    return complex(t.reshape(-1)[0].item())
+def contract_f64(h, spec, path):
+    """contract_network_oracle (network.cpp:179-186) of a closed network along
+    `path`: the f64 fold on the device, bit-identical to the reference's CPU
+    oracle -- the fidelity reference of the deep-circuit legs."""
+    from paper_2303_08989_b200.network import Network
+    onet = Network(h, spec)
+    try:
+        return complex(onet.contract_oracle(path).data.reshape(-1)[0])
+    finally:
+        onet.close()
 
 
 def _compact_leg(line):
@@ -1002,22 +955,28 @@ def run_rqc7x7_leg(args, emit=False):
     out["value"] = out["modes"]["AUTO-0"]["ms_per_amplitude"]
     out["auto_speedup_vs_fp32_baseline"] = round(out["modes"]["FP32_BASELINE"]["ms_per_amplitude"]
                                                  / out["value"], 3)
-    if not args.no_cpu:
-        from oracle.network import contract_network_f64  # CPU checker (reference restatement)
-        t0 = time.perf_counter()
-        zref = np.array([complex(contract_network_f64(circuit_to_network(circ, x), path)[2].reshape(-1)[0])
-                         for x in xs])
-        for label, amps in amps_by.items():
-            err = np.abs(amps - zref) / np.abs(zref)
-            out["modes"][label]["median_rel_err_vs_cpu_f64"] = float(np.median(err))
-            out["modes"][label]["max_rel_err_vs_cpu_f64"] = float(np.max(err))
-        fa = out["modes"]["FP32_BASELINE"]["median_rel_err_vs_cpu_f64"]
-        out["auto_err_ratio_vs_fp32_baseline"] = (round(out["modes"]["AUTO-0"]["median_rel_err_vs_cpu_f64"]
-                                                        / fa, 3) if fa else None)
-        out["cpu_baseline"] = {"kind": "port", "cores": os.cpu_count() or 1,
-                               "reference_s": round(time.perf_counter() - t0, 1),
-                               "sample": f"FP64 contract_network_oracle (oracle/network.py restatement of "
-                                         f"network.cpp:179-186, numpy) of the same path for {nb} bitstrings"}
+    # fidelity reference: contract_network_oracle (network.cpp:179-186) of the
+    # same path, the f64 fold on the device -- bit-identical to the reference's
+    # CPU oracle (tests/test_gpu_network.py::test_device_f64_oracle_is_the_reference_oracle)
+    t0 = time.perf_counter()
+    h = Handle(local)
+    zref = []
+    for x in xs:
+        onet = Network(h, circuit_to_network(circ, x))
+        zref.append(complex(onet.contract_oracle(path).data.reshape(-1)[0]))
+        onet.close()
+    h.close()
+    zref = np.array(zref)
+    for label, amps in amps_by.items():
+        err = np.abs(amps - zref) / np.abs(zref)
+        out["modes"][label]["median_rel_err_vs_f64_oracle"] = float(np.median(err))
+        out["modes"][label]["max_rel_err_vs_f64_oracle"] = float(np.max(err))
+    fa = out["modes"]["FP32_BASELINE"]["median_rel_err_vs_f64_oracle"]
+    out["auto_err_ratio_vs_fp32_baseline"] = (round(out["modes"]["AUTO-0"]["median_rel_err_vs_f64_oracle"]
+                                                    / fa, 3) if fa else None)
+    out["fidelity_reference"] = {"what": "contract_network_oracle of the same greedy path, f64 on the device "
+                                         "(bit-identical to the reference's CPU oracle)",
+                                 "seconds": round(time.perf_counter() - t0, 2), "bitstrings": nb}
     return out
 
 
@@ -1049,7 +1008,7 @@ def run_rqc7x7(args):
             net = Network(h, spec)
             path = net.greedy_path()
             big, macs = contraction_cost(spec, path)
-            ref = np.array([contract_c128(circuit_to_network(circ, x), path, dev) for x in xs])
+            ref = np.array([contract_f64(h, circuit_to_network(circ, x), path) for x in xs])
             torch.cuda.empty_cache()
             row = {"depth": depth, "steps": len(path), "max_intermediate": int(big),
                    "gflop_per_amplitude": round(8.0 * macs / 1e9, 2), "modes": {}}
@@ -1072,14 +1031,14 @@ def run_rqc7x7(args):
                 ms = dev_ms / (reps * len(xs))  # device time after the bitstring upload
                 err = np.abs(amps.astype(np.complex128) - ref) / np.abs(ref)
                 row["modes"][label] = {"ms_per_amplitude": round(ms, 3), "e2e_ms_per_amplitude": round(e2e, 3),
-                                       "median_rel_err_vs_c128": float(np.median(err)),
-                                       "max_rel_err_vs_c128": float(np.max(err)),
+                                       "median_rel_err_vs_f64_oracle": float(np.median(err)),
+                                       "max_rel_err_vs_f64_oracle": float(np.max(err)),
                                        "decisions": hist}
             a, f = row["modes"]["AUTO-0"], row["modes"]["FP32_BASELINE"]
             row["auto_speedup_vs_fp32_baseline"] = round(f["ms_per_amplitude"] / a["ms_per_amplitude"], 3)
-            row["auto_err_ratio_vs_fp32_baseline"] = (round(a["median_rel_err_vs_c128"] /
-                                                            f["median_rel_err_vs_c128"], 3)
-                                                      if f["median_rel_err_vs_c128"] else None)
+            row["auto_err_ratio_vs_fp32_baseline"] = (round(a["median_rel_err_vs_f64_oracle"] /
+                                                            f["median_rel_err_vs_f64_oracle"], 3)
+                                                      if f["median_rel_err_vs_f64_oracle"] else None)
             if rank == 0 and not args.no_cpu and depth <= 12:
                 thr = os.cpu_count() or 1
                 bits = np.array(xs[:min(len(xs), thr)], np.uint8)
@@ -1109,8 +1068,8 @@ def run_rqc7x7(args):
             for sp in specs:
                 z = 0j
                 for si in range(nsl):
-                    z += contract_c128(slice_spec(sp, sliced, assignment(si, sdims)) if sliced else sp,
-                                       path, dev)
+                    z += contract_f64(h, slice_spec(sp, sliced, assignment(si, sdims)) if sliced else sp,
+                                      path)
                 ref.append(z)
             ref = np.array(ref)
             torch.cuda.empty_cache()
@@ -1139,13 +1098,13 @@ def run_rqc7x7(args):
                 amps = vals.astype(np.complex128).reshape(len(xs), nsl).sum(axis=1)
                 err = np.abs(amps - ref) / np.abs(ref)
                 row["modes"][label] = {"ms_per_amplitude": round(ms, 3), "e2e_ms_per_amplitude": round(e2e, 3),
-                                       "median_rel_err_vs_c128": float(np.median(err)),
-                                       "max_rel_err_vs_c128": float(np.max(err))}
+                                       "median_rel_err_vs_f64_oracle": float(np.median(err)),
+                                       "max_rel_err_vs_f64_oracle": float(np.max(err))}
             a, f = row["modes"]["AUTO-0"], row["modes"]["FP32_BASELINE"]
             row["auto_speedup_vs_fp32_baseline"] = round(f["ms_per_amplitude"] / a["ms_per_amplitude"], 3)
-            row["auto_err_ratio_vs_fp32_baseline"] = (round(a["median_rel_err_vs_c128"] /
-                                                            f["median_rel_err_vs_c128"], 3)
-                                                      if f["median_rel_err_vs_c128"] else None)
+            row["auto_err_ratio_vs_fp32_baseline"] = (round(a["median_rel_err_vs_f64_oracle"] /
+                                                            f["median_rel_err_vs_f64_oracle"], 3)
+                                                      if f["median_rel_err_vs_f64_oracle"] else None)
             net.close()
             torch.cuda.empty_cache()
             rows_out.append(row)
@@ -1159,7 +1118,7 @@ def run_rqc7x7(args):
                 "scaling": "strong", "vs_baseline": None, "dtype": "c64 (AUTO-0 tiers)",
                 "data": "synthetic circuits rqc_rectangular(7, 7, d, 1), 10 bitstrings (experiments.cpp:185-196)",
                 "config": {"workload": "configs[4] deep-circuit fidelity study, reference greedy path",
-                           "fidelity_reference": "complex128 contraction of the same path (torch, GPU)",
+                           "fidelity_reference": "contract_network_oracle of the same path (f64 fold on the device, bit-identical to the reference's CPU oracle)",
                            "parallelism": f"bitstrings / {world}"},
                 "e2e": {"value": deep_e2e, "unit": "ms/amplitude", "h2d_bytes_per_step": 49,
                         "d2h_bytes_per_step": 8,

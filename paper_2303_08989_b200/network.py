@@ -136,6 +136,34 @@ class Network:
             return t, lines
         return t
 
+    def contract_oracle(self, path) -> Tensor:
+        """contract_network_oracle (network.hpp:39, network.cpp:179-186): the
+        same TTGT fold with every value widened to complex128 and the
+        reference's f64 GEMM order, computed on the device
+        (tcec_contract_network_oracle; bit-identical to the reference's CPU
+        oracle).  Returns a complex128 Tensor."""
+        flat = [x for st in path for x in st]
+        steps = (C.c_int * max(len(flat), 1))(*flat)
+        open_dims = {}
+        for ls, ds in zip(self.spec.labels, self.spec.dims):
+            for l, d in zip(ls, ds):
+                open_dims[l] = d if l not in open_dims else None
+        cap = 1
+        for d in open_dims.values():
+            if d is not None:
+                cap *= d
+        out = np.empty(max(cap, 1), dtype=np.complex128)
+        rank = C.c_int(0)
+        labels = (C.c_int * max(len(open_dims), 1))()
+        check(self.lib.tcec_contract_network_oracle(self.net, steps, len(path),
+                                                    out.ctypes.data_as(C.c_void_p), out.size,
+                                                    C.byref(rank), labels))
+        names = [self.names[labels[i]] for i in range(rank.value)]
+        dims = [next(d for ls, ds in zip(self.spec.labels, self.spec.dims) for l, d in zip(ls, ds)
+                     if l == nm) for nm in names]
+        size = int(np.prod(dims)) if dims else 1
+        return Tensor(names, dims, out[:size].copy())
+
     def selector_batch(self, path, bitstrings, config=None, out=None) -> np.ndarray:
         """Amplitudes of many bitstrings over one plan / one captured graph.
         `bitstrings` / `out` may live in pinned host memory (faster copies)."""
@@ -244,6 +272,40 @@ def contract_pair(handle: Handle, a: Tensor, b: Tensor, config=None) -> Tensor:
         return net.contract([(0, 1)], config)
     finally:
         net.close()
+
+
+def statevector_oracle(handle: Handle, circuit: Circuit):
+    """statevector_oracle (qcircuit.hpp:56, qcircuit.cpp:197-225): the f64 state
+    vector of |0...0> under the circuit, on the device (tcec_statevector_f64,
+    the reference's gate order and complex arithmetic -> bit-identical); qubit q
+    is bit q of the index.  Returns a complex128 CUDA tensor."""
+    import torch
+    from .circuits import CZ, gate_matrix, validate_circuit
+    validate_circuit(circuit)
+    if circuit.n_qubits > 24:
+        raise _lib.TooManyQubits(11, "state-vector oracle limited to 24 qubits")
+    qa, qb, u = [], [], []
+    for layer in circuit.layers:
+        for g in layer:
+            if g.kind == CZ:
+                qa.append(g.qubits[0])
+                qb.append(g.qubits[1])
+                u.extend([0.0] * 8)
+                continue
+            if len(g.qubits) != 1:
+                raise ValueError(f"statevector_oracle: gate {g.kind} is not in the reference gate set")
+            m = gate_matrix(g.kind)
+            qa.append(g.qubits[0])
+            qb.append(-1)
+            u.extend(v for z in m for v in (z.real, z.imag))
+    n = len(qa)
+    st = torch.empty(1 << circuit.n_qubits, dtype=torch.complex128, device=torch.device("cuda", handle.device))
+    ia = (C.c_int * max(n, 1))(*qa)
+    ib = (C.c_int * max(n, 1))(*qb)
+    du = (C.c_double * max(8 * n, 8))(*u)
+    handle._ordered_call(handle.lib.tcec_statevector_f64, handle.h, circuit.n_qubits, n, ia, ib, du,
+                         C.c_void_p(st.data_ptr()))
+    return st
 
 
 def amplitude(handle: Handle, circuit: Circuit, x, config=None) -> np.complex64:

@@ -271,3 +271,74 @@ def test_thread_per_run_batch_matches_warp_per_run(handle):
                             for i in range(0, len(xs), 2048)])
     assert np.array_equal(big.view(np.uint32), small.view(np.uint32))
     net.close()
+
+
+def test_device_f64_oracle_is_the_reference_oracle(handle, golden):
+    """tcec_contract_network_oracle (the f64 TTGT fold on the device) equals the
+    reference's own contract_network_oracle (network.cpp:179-186) bit for bit:
+    the golden `tn_oracle` amplitudes were computed by the unmodified reference
+    along its greedy path for every golden circuit and bitstring (numpy's zgemm
+    would not match: the reference sums four real planes in ascending k)."""
+    from paper_2303_08989_b200.circuits import circuit_to_network, load_circuit
+    from paper_2303_08989_b200.network import Network
+    checked = 0
+    for case in golden("rqc.json"):
+        circ = load_circuit(case["circuit_text"])
+        path = [tuple(p) for p in case["path"]]
+        for row in case["amplitudes"]:
+            net = Network(handle, circuit_to_network(circ, row["x"]))
+            z = complex(net.contract_oracle(path).data.reshape(-1)[0])
+            net.close()
+            assert (z.real, z.imag) == tuple(row["tn_oracle"]), (case["rows"], case["cols"], row["x"])
+            checked += 1
+    assert checked >= 40
+
+
+@pytest.mark.parametrize("depth", [12, 14])
+def test_rqc7x7_tensor_core_amplitudes(handle, depth):
+    """configs[4]: 7x7 RQC at depth 12 / 14 on the reference's greedy path with
+    a lowered policy that routes the large steps to the tensor-core tiers --
+    median amplitude error vs the f64 contraction oracle <= 1e-4 and <= 4x the
+    FP32 baseline tier's (experiments.cpp:240-256)."""
+    from paper_2303_08989_b200 import SelectionPolicy, make_config
+    from paper_2303_08989_b200.circuits import bitstrings_for, circuit_to_network, rqc_rectangular
+    from paper_2303_08989_b200.network import Network
+    circ = rqc_rectangular(7, 7, depth, 1)
+    xs = bitstrings_for(49, 10, 1)[:4]
+    spec = circuit_to_network(circ, xs[0])
+    net = Network(handle, spec)
+    path = net.greedy_path()
+    ref = []
+    for x in xs:
+        n2 = Network(handle, circuit_to_network(circ, x))
+        ref.append(complex(n2.contract_oracle(path).data.reshape(-1)[0]))
+        n2.close()
+    ref = np.array(ref)
+    auto = make_config(SelectionPolicy(size_auto=256, size_tf32=64))
+    _, lines = net.contract(path, auto, want_log=True)
+    kinds = {ln.split(",")[3] for ln in lines}
+    assert kinds & {"TF32TCEC", "FP16TCEC", "FP16TCEC_SCALED"}, kinds
+    z_auto = net.selector_batch(path, xs, auto).astype(np.complex128)
+    z_fp32 = net.selector_batch(path, xs, make_config(force="FP32_REF")).astype(np.complex128)
+    net.close()
+    e_auto = np.median(np.abs(z_auto - ref) / np.abs(ref))
+    e_fp32 = np.median(np.abs(z_fp32 - ref) / np.abs(ref))
+    assert e_auto <= 1e-4, (e_auto, kinds)
+    assert e_auto <= 4 * e_fp32, (e_auto, e_fp32, kinds)
+
+
+def test_device_statevector_is_the_reference_oracle(handle, golden):
+    """tcec_statevector_f64 == the reference's statevector_oracle bit for bit
+    (golden `sv_oracle` amplitudes computed by the unmodified reference)."""
+    from paper_2303_08989_b200.circuits import load_circuit
+    from paper_2303_08989_b200.network import statevector_oracle
+    checked = 0
+    for case in golden("rqc.json"):
+        circ = load_circuit(case["circuit_text"])
+        sv = statevector_oracle(handle, circ).cpu().numpy()
+        for row in case["amplitudes"]:
+            idx = sum(int(b) << q for q, b in enumerate(row["x"]))
+            z = sv[idx]
+            assert (z.real, z.imag) == tuple(row["sv_oracle"]), (case["rows"], case["cols"], row["x"])
+            checked += 1
+    assert checked >= 40
