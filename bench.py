@@ -1189,7 +1189,7 @@ def main():
                    help="skip the configs[0]/[2]/[4] legs of the default line (N = 1)")
     p.add_argument("--no-pageable", dest="pageable", action="store_false")
     p.add_argument("--cpu-budget", type=float, default=12.0)
-    p.add_argument("--ref-step-s", type=float, default=8.0)
+    p.add_argument("--ref-step-s", type=float, default=4.0)
     args = p.parse_args()
     if args.warmup < 3:
         args.warmup = 3
