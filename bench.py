@@ -60,18 +60,24 @@ def peaks():
 
 
 def tf32_peak():
-    """Dense TF32 peak for the TF32TCEC path: profiles/r02_tf32_peak.json
-    (tools/peak_tf32.py, cuBLAS TF32 8192^3 on this pool's B200s).  The burst
-    figure is used: the TCEC kernel, timed back to back inside the step, runs
-    above cuBLAS's sustained TF32 rate under the 1000 W cap, so the sustained
-    figure would not bound it.  Fallback: B200_PROFILING.md's 1.1 PF dense."""
+    """Dense TF32 peak for the TF32TCEC path: half the measured dense bf16 burst
+    peak of MEASURED_PEAKS.json (sm_100 tensor cores run TF32 at half the
+    bf16/fp16 rate: B200_PROFILING.md 1.1 vs 2.25 PFLOP/s dense).  The cuBLAS
+    TF32 8192^3 figure of profiles/r02_tf32_peak.json (tools/peak_tf32.py) is
+    quoted next to it: cuBLAS's TF32 kernel does not reach the hardware rate on
+    this pool (the TCEC kernel runs above it), so it cannot be the bound.
+    Fallback: B200_PROFILING.md's 1.1 PF dense."""
+    bpk, _, _, src = peaks()
+    cub = ""
     p = os.path.join(ROOT, "profiles", "r02_tf32_peak.json")
     if os.path.exists(p):
         d = json.load(open(p))["tf32"]
-        return d["burst_tflops"], (f"measured dense TF32 burst {d['burst_tflops']} TFLOP/s (cuBLAS, "
-                                   f"profiles/r02_tf32_peak.json; its sustained figure is "
-                                   f"{d['sustained_tflops']})")
-    return 1100.0, "B200_PROFILING.md fallback: 1.1 PFLOP/s dense TF32"
+        cub = (f"; cuBLAS TF32 8192^3 on the same pool: {d['burst_tflops']} burst / "
+               f"{d['sustained_tflops']} sustained (profiles/r02_tf32_peak.json)")
+    if src == "measured":
+        return round(bpk / 2, 1), (f"measured dense bf16 burst {bpk} TFLOP/s (MEASURED_PEAKS.json) / 2 "
+                                   f"= the dense TF32 rate (1:2 on sm_100, B200_PROFILING.md){cub}")
+    return 1100.0, "B200_PROFILING.md fallback: 1.1 PFLOP/s dense TF32" + cub
 
 
 # ------------------------------------------------------------------ clocks
@@ -410,7 +416,7 @@ def cgemm_headline(args, world, rank, local):
             "higher_is_better": True, "scaling": "weak",
             "vs_baseline": round(value / PAPER_A100_FP16TCEC, 2),
             "baseline_ref": "54.2 TFLOP/s FP16TCEC CGEMM max on A100 (PAPER.md:246)",
-            "dtype": "c64 (FP32-level via error-corrected FP16 products)",
+            "dtype": f"c64 (FP32-level via error-corrected {'TF32' if tf32 else 'FP16'} products)",
             "data": "synthetic, the reference's own generator, resident in HBM",
             "config": {"workload": workload_name(n), "decision": decision, "inputs": INPUTS_NOTE},
             "parallelism": f"replicas x{world} (the standalone CGEMM does not shard, SURVEY 8(e))",

@@ -69,6 +69,16 @@ int tcec_get_flush_kblocks(tcec_handle h);
  * 4 = the wide tile on persistent CTA pairs, 5 = the wide tile on clusters of
  * two CTA pairs that share each B' tile by TMA multicast */
 int tcec_set_gemm_variant(tcec_handle h, int variant);
+/* operand layout of tensor-core dispatches: the complex GEMM runs as one real
+ * GEMM in which one operand carries the 2x2 complex block expansion.
+ * 0 = auto (default: expand the smaller operand -- A when m < n),
+ * 1 = B-expanded (A' = A as m x 2k, B' = [[Br, Bi], [-Bi, Br]], 2n columns),
+ * 2 = A-expanded (A'' rows (Ar, -Ai) / (Ai, Ar), 2m rows; B'' = B^T as n x 2k).
+ * Results are FP32-level either way (same products, hardware accumulation
+ * order); the choice only changes bytes moved.  No reference counterpart
+ * (its cgemm deinterleaves into four real GEMMs, cgemm.cpp:25-46). */
+int tcec_set_operand_layout(tcec_handle h, int layout);
+int tcec_get_operand_layout(tcec_handle h);
 /* network executor: 0 = auto (fused small-step kernel -- one warp per network,
  * intermediates in shared memory -- whenever every step is on a SIMT tier and
  * the live intermediates fit; else the per-step fold -- permute + dispatch
@@ -118,6 +128,13 @@ int64_t tcec_prep_kp(int64_t k);
 int tcec_debug_prep(tcec_handle h, const void* a, const void* b, int64_t m, int64_t n, int64_t k,
                     int kind, int scale_a, int scale_b, int corrected, void* a_hi, void* a_lo,
                     void* b_hi, void* b_lo, int* flags);
+/* the same for either operand layout: xa = 0 as above; xa = 1 the A-expanded
+ * layout (tcec_set_operand_layout): a_hi/a_lo 2m x kp with row 2i = (Ar, -Ai),
+ * row 2i+1 = (Ai, Ar) per complex k; b_hi/b_lo n x kp with row j = (Br, Bi)
+ * (column j of B) */
+int tcec_debug_prep_layout(tcec_handle h, const void* a, const void* b, int64_t m, int64_t n, int64_t k,
+                           int kind, int scale_a, int scale_b, int corrected, int xa, void* a_hi,
+                           void* a_lo, void* b_hi, void* b_lo, int* flags);
 
 /* ------------------------------------------------- precision selection */
 /* ExpStats, precsel.hpp:18-36 (e_max_valid == 0 <=> std::nullopt) */

@@ -123,6 +123,8 @@ def load() -> C.CDLL:
         "tcec_set_flush_kblocks": ([vp, i32], i32),
         "tcec_get_flush_kblocks": ([vp], i32),
         "tcec_set_gemm_variant": ([vp, i32], i32),
+        "tcec_set_operand_layout": ([vp, i32], i32),
+        "tcec_get_operand_layout": ([vp], i32),
         "tcec_set_executor": ([vp, i32], i32),
         "tcec_profile_enable": ([vp, i32], i32),
         "tcec_profile_read": ([vp, C.POINTER(dbl), C.POINTER(i64)], i32),
@@ -172,6 +174,8 @@ def load() -> C.CDLL:
         "tcec_rng_fill_uniform_pm1f": ([vp, vp, i64], i32),
         "tcec_rng_fill_gaussian": ([vp, dbl, vp, i64], i32),
         "tcec_debug_prep": ([vp, vp, vp, i64, i64, i64, i32, i32, i32, i32, vp, vp, vp, vp, ip], i32),
+        "tcec_debug_prep_layout": ([vp, vp, vp, i64, i64, i64, i32, i32, i32, i32, i32, vp, vp, vp, vp, ip],
+                                   i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name, None)

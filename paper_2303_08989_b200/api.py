@@ -135,6 +135,12 @@ class Handle:
 
     GEMM_VARIANTS = {"auto": 0, "pair": 1, "single": 2, "wide": 3, "wide_persistent": 4, "wide_mc": 5}
 
+    def set_operand_layout(self, layout) -> None:
+        """tcec_set_operand_layout: "auto" (expand the smaller operand), "b" (B' =
+        [[Br, Bi], [-Bi, Br]]) or "a" (A'' rows (Ar, -Ai) / (Ai, Ar))."""
+        v = {"auto": 0, "b": 1, "a": 2}.get(layout, layout)
+        check(self.lib.tcec_set_operand_layout(self.h, int(v)))
+
     def set_gemm_variant(self, variant) -> None:
         """tcgen05 kernel variant: "auto" (default), "pair" (cta_group::2,
         256x128 tile), "single" (128x128 tile), "wide" (cta_group::2, 256x256), "wide_persistent"
@@ -332,11 +338,12 @@ class Handle:
 
     # ------------------------------------------- operand preparation (test hook)
     def debug_prep(self, a, b, kind: str | int, scale_a: int = 0, scale_b: int = 0,
-                   corrected: bool = True):
+                   corrected: bool = True, xa: bool = False):
         """Run the hot path's prep_a / prep_b for a fixed decision and return the
-        tensor-core operand planes (tcec_debug_prep): A' hi/lo (m x kp) and B'
-        hi/lo (2n x kp), binary16 for the FP16 kinds and f32 for TF32, plus the
-        (format overflow, ScaleOverflow) flags."""
+        tensor-core operand planes (tcec_debug_prep_layout): A' hi/lo (m x kp) and
+        B' hi/lo (2n x kp), binary16 for the FP16 kinds and f32 for TF32, plus the
+        (format overflow, ScaleOverflow) flags.  xa=True: the A-expanded layout
+        (A'' hi/lo 2m x kp, B'' hi/lo n x kp)."""
         torch = _torch()
         self._check_c64(a, b)
         kd = KINDS.index(kind) if isinstance(kind, str) else int(kind)
@@ -346,10 +353,11 @@ class Handle:
             raise _lib.ShapeMismatch(1, "debug_prep: inner dimensions differ")
         kp = int(self.lib.tcec_prep_kp(k))
         dt = torch.float32 if kd == 2 else torch.float16
-        planes = [torch.zeros((r, kp), dtype=dt, device=a.device) for r in (m, m, 2 * n, 2 * n)]
+        ra, rb = (2 * m, n) if xa else (m, 2 * n)
+        planes = [torch.zeros((r, kp), dtype=dt, device=a.device) for r in (ra, ra, rb, rb)]
         flags = (C.c_int * 2)()
-        self._ordered_call(self.lib.tcec_debug_prep, self.h, _ptr(a), _ptr(b), m, n, k, kd,
-                           int(scale_a), int(scale_b), int(bool(corrected)),
+        self._ordered_call(self.lib.tcec_debug_prep_layout, self.h, _ptr(a), _ptr(b), m, n, k, kd,
+                           int(scale_a), int(scale_b), int(bool(corrected)), int(bool(xa)),
                            *[_ptr(t) for t in planes], flags)
         return (*planes, bool(flags[0]), bool(flags[1]))
 

@@ -131,16 +131,30 @@ DispatchPlan plan_dispatch(int64_t m, int64_t n, int64_t k, const tcec_dispatch_
 size_t plan_workspace(const DispatchPlan& p, int64_t m, int64_t n) {
     if (p.tier != kTierTc) return 0;
     const int elem = (p.kind == kKindFp16 || p.forced_scaled) ? 2 : 4;  // auto: sized for tf32
-    const size_t a = size_t(m) * p.kp * elem, b = size_t(2 * n) * p.kp * elem;
-    return 2 * round_up(int64_t(a), 1024) + 2 * round_up(int64_t(b), 1024);
+    // room for either operand layout: B-expanded (m + 2n rows) or A-expanded (2m + n)
+    auto planes = [&](int64_t ra, int64_t rb) {
+        return 2 * round_up(int64_t(size_t(ra) * p.kp * elem), 1024) +
+               2 * round_up(int64_t(size_t(rb) * p.kp * elem), 1024);
+    };
+    return size_t(std::max(planes(m, 2 * n), planes(2 * m, n)));
+}
+
+// Operand layout of a tensor-core dispatch: the complex block expansion goes to
+// the smaller operand (A-expanded when m < n), unless the handle forces one.
+bool use_xa(const Handle& h, int64_t m, int64_t n) {
+    if (h.layout == 1) return false;
+    if (h.layout == 2) return true;
+    return m < n && h.gemm_pair != kVariantPair;
 }
 
 // Operand planes in the workspace + the GEMM arguments of a tensor-core dispatch.
 TcecGemmArgs tc_gemm_args(const Handle& h, const DispatchPlan& p, void* ws, float* c, int64_t m,
-                          int64_t n, DevDecision* d) {
+                          int64_t n, DevDecision* d, bool allow_xa) {
     const int elem = (p.kind == kKindFp16 || p.forced_scaled) ? 2 : 4;
-    const size_t abytes = round_up(int64_t(size_t(m) * p.kp * elem), 1024);
-    const size_t bbytes = round_up(int64_t(size_t(2 * n) * p.kp * elem), 1024);
+    const bool xa = allow_xa && use_xa(h, m, n);
+    const int64_t rows_a = xa ? 2 * m : m, rows_b = xa ? n : 2 * n;  // GEMM M and N
+    const size_t abytes = round_up(int64_t(size_t(rows_a) * p.kp * elem), 1024);
+    const size_t bbytes = round_up(int64_t(size_t(rows_b) * p.kp * elem), 1024);
     uint8_t* w = static_cast<uint8_t*>(ws);
     TcecGemmArgs g{};
     g.a_hi = w;
@@ -148,10 +162,11 @@ TcecGemmArgs tc_gemm_args(const Handle& h, const DispatchPlan& p, void* ws, floa
     g.b_hi = w + 2 * abytes;
     g.b_lo = w + 2 * abytes + bbytes;
     g.c = c;
-    g.m = m;
-    g.a_rows = m;
-    g.n2 = 2 * n;
+    g.m = rows_a;
+    g.a_rows = rows_a;
+    g.n2 = rows_b;
     g.kp = p.kp;
+    g.xa = xa ? 1 : 0;
     g.d = d;
     g.kind_fixed = p.kind;
     g.corrected = p.corrected;
@@ -162,15 +177,17 @@ TcecGemmArgs tc_gemm_args(const Handle& h, const DispatchPlan& p, void* ws, floa
         return e ? std::max(0, std::min(64, std::atoi(e))) : 0;
     }();
     g.flush_kblocks = p.corrected ? (h.flush_kblocks | (h.flush_kblocks > 0 ? tf32_flush << 16 : 0)) : 0;
-    g.pair = resolve_gemm_variant(h.gemm_pair, m, 2 * n, p.kp, h.sm_count);
+    g.pair = resolve_gemm_variant(h.gemm_pair, rows_a, rows_b, p.kp, h.sm_count);
     g.sms = h.sm_count;
     g.fmt = (p.kind < 0 && !p.forced_scaled) ? -1  // format chosen by the device decision
                                              : (p.kind == kKindTf32 ? kTf32 : kFp16);
     return g;
 }
 
-// GEMM of rows [r0, r1) of A' / C (chunked: no split-K, so a chunk computes
-// exactly what the whole launch would), then the hook's done(r0, r1)
+// GEMM of rows [r0, r1) of A' (chunked: no split-K, so a chunk computes
+// exactly what the whole launch would), then the hook's done() on the C rows
+// they produce (A-expanded layout: GEMM rows 2i, 2i+1 -> C row i; r0 even, and
+// C row r0 / 2 starts at float r0 * n2 = r0 / 2 * 2n in both layouts)
 int launch_gemm_rows(const TcecGemmArgs& g, int64_t r0, int64_t r1, bool chunked,
                      const ChunkHook* hook, cudaStream_t s) {
     TcecGemmArgs gc = g;
@@ -181,7 +198,7 @@ int launch_gemm_rows(const TcecGemmArgs& g, int64_t r0, int64_t r1, bool chunked
     const int e = launch_tcec_gemm(gc, s);
     if (e) return cuda_error(cudaError_t(e), g.fmt < 0 ? "tcec_gemm auto"
                                              : (g.fmt == kTf32 ? "tcec_gemm tf32" : "tcec_gemm f16"));
-    if (hook && hook->done) return hook->done(hook->ctx, r0, r1);
+    if (hook && hook->done) return g.xa ? hook->done(hook->ctx, r0 / 2, r1 / 2) : hook->done(hook->ctx, r0, r1);
     return TCEC_OK;
 }
 
@@ -232,16 +249,26 @@ int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t
     default: break;
     }
     // tensor-core tier: operand preparation + tcgen05 GEMM(s)
-    TcecGemmArgs g = tc_gemm_args(h, p, ws, c, m, n, d);
-    launch_prep_a(a, m, k, p.kp, const_cast<void*>(g.a_hi), const_cast<void*>(g.a_lo), d, p.kind, p.corrected, s);
-    launch_prep_b(b, k, n, p.kp, const_cast<void*>(g.b_hi), const_cast<void*>(g.b_lo), d, p.kind, p.corrected, s);
+    TcecGemmArgs g = tc_gemm_args(h, p, ws, c, m, n, d, true);
+    void* ahi = const_cast<void*>(g.a_hi);
+    void* alo = const_cast<void*>(g.a_lo);
+    void* bhi = const_cast<void*>(g.b_hi);
+    void* blo = const_cast<void*>(g.b_lo);
+    if (g.xa) {
+        launch_prep_ax(a, m, k, p.kp, ahi, alo, d, p.kind, p.corrected, s);
+        launch_prep_bx(b, k, n, p.kp, bhi, blo, d, p.kind, p.corrected, s);
+    } else {
+        launch_prep_a(a, m, k, p.kp, ahi, alo, d, p.kind, p.corrected, s);
+        launch_prep_b(b, k, n, p.kp, bhi, blo, d, p.kind, p.corrected, s);
+    }
     if (prof) cudaEventRecord(h.ev[2], s);
     // row chunks (host-buffer API): only the wide kernel indexes into A' by row
     int chunks = hook ? std::max(1, hook->chunks) : 1;
     if (g.pair != kVariantWide && g.pair != kVariantWideMc) chunks = 1;
-    const int64_t rows_per = round_up((m + chunks - 1) / chunks, 256);
-    for (int64_t r0 = 0; r0 < m; r0 += rows_per) {
-        const int64_t r1 = std::min(m, r0 + rows_per);
+    const int64_t gm = g.m;  // GEMM rows (2m in the A-expanded layout)
+    const int64_t rows_per = round_up((gm + chunks - 1) / chunks, 256);
+    for (int64_t r0 = 0; r0 < gm; r0 += rows_per) {
+        const int64_t r1 = std::min(gm, r0 + rows_per);
         const int rc = launch_gemm_rows(g, r0, r1, chunks > 1, hook, s);
         if (rc) return rc;
     }
@@ -475,6 +502,15 @@ int tcec_set_gemm_variant(tcec_handle h, int variant) {
     return TCEC_OK;
 }
 
+int tcec_set_operand_layout(tcec_handle h, int layout) {
+    CHECK_HANDLE(h);
+    if (layout < 0 || layout > 2) return set_error(TCEC_ERR_INVALID_ARGUMENT, "layout must be 0..2");
+    h->layout = layout;
+    return TCEC_OK;
+}
+
+int tcec_get_operand_layout(tcec_handle h) { return h ? h->layout : -1; }
+
 int tcec_profile_enable(tcec_handle h, int on) {
     CHECK_HANDLE(h);
     if (on && !h->ev[0])
@@ -587,6 +623,13 @@ int64_t tcec_prep_kp(int64_t k) { return round_up(2 * k, 64); }
 int tcec_debug_prep(tcec_handle h, const void* a, const void* b, int64_t m, int64_t n, int64_t k,
                     int kind, int scale_a, int scale_b, int corrected, void* a_hi, void* a_lo,
                     void* b_hi, void* b_lo, int* flags) {
+    return tcec_debug_prep_layout(h, a, b, m, n, k, kind, scale_a, scale_b, corrected, 0, a_hi, a_lo,
+                                  b_hi, b_lo, flags);
+}
+
+int tcec_debug_prep_layout(tcec_handle h, const void* a, const void* b, int64_t m, int64_t n, int64_t k,
+                           int kind, int scale_a, int scale_b, int corrected, int xa, void* a_hi,
+                           void* a_lo, void* b_hi, void* b_lo, int* flags) {
     CHECK_HANDLE(h);
     if (m < 0 || n < 0 || k < 0) return set_error(TCEC_ERR_SHAPE_MISMATCH, "negative extent");
     if (kind != kKindFp16 && kind != kKindFp16Scaled && kind != kKindTf32)
@@ -600,12 +643,19 @@ int tcec_debug_prep(tcec_handle h, const void* a, const void* b, int64_t m, int6
     hd->scale_b = scale_b;
     CUDA_TRY(cudaMemcpyAsync(d, hd, sizeof(DevDecision), cudaMemcpyHostToDevice, h->stream));
     const int64_t kp = tcec_prep_kp(k);
-    if (a && m > 0 && k > 0)
-        launch_prep_a(static_cast<const float*>(a), m, k, kp, a_hi, a_lo, d, -1, corrected ? 1 : 0,
-                      h->stream, 0);
-    if (b && n > 0 && k > 0)
-        launch_prep_b(static_cast<const float*>(b), k, n, kp, b_hi, b_lo, d, -1, corrected ? 1 : 0,
-                      h->stream, 0);
+    const int cr = corrected ? 1 : 0;
+    if (a && m > 0 && k > 0) {
+        if (xa)
+            launch_prep_ax(static_cast<const float*>(a), m, k, kp, a_hi, a_lo, d, -1, cr, h->stream);
+        else
+            launch_prep_a(static_cast<const float*>(a), m, k, kp, a_hi, a_lo, d, -1, cr, h->stream, 0);
+    }
+    if (b && n > 0 && k > 0) {
+        if (xa)
+            launch_prep_bx(static_cast<const float*>(b), k, n, kp, b_hi, b_lo, d, -1, cr, h->stream);
+        else
+            launch_prep_b(static_cast<const float*>(b), k, n, kp, b_hi, b_lo, d, -1, cr, h->stream, 0);
+    }
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(hd, d, sizeof(DevDecision), cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(cudaStreamSynchronize(h->stream));
@@ -738,13 +788,13 @@ int tcec_dispatch_cgemm(tcec_handle h, const void* a, const void* b, void* c, in
                        !(h->prof && h->ev[0]);
     Handle::DispatchGraph key{a, b, c, ws, d, m, n, k, cfg->threshold_t, cfg->size_auto,
                               cfg->size_tf32, cfg->target_max_exponent, cfg->k_tile, cfg->force,
-                              h->gemm_pair, h->flush_kblocks, h->stream, nullptr};
+                              h->gemm_pair, h->flush_kblocks, h->layout, h->stream, nullptr};
     auto same = [&](const Handle::DispatchGraph& g) {
         return g.a == key.a && g.b == key.b && g.c == key.c && g.ws == key.ws && g.dec == key.dec &&
                g.m == m && g.n == n && g.k == k && g.t == key.t && g.size_auto == key.size_auto &&
                g.size_tf32 == key.size_tf32 && g.target == key.target && g.k_tile == key.k_tile &&
                g.force == key.force && g.variant == key.variant && g.flush == key.flush &&
-               g.stream == key.stream;
+               g.layout == key.layout && g.stream == key.stream;
     };
     const Handle::DispatchGraph* hit = nullptr;
     if (small)
@@ -919,7 +969,7 @@ static int host_pipeline(Handle& h, const uint8_t* a, const uint8_t* b, uint8_t*
         launch_select(ds, cfg.threshold_t, cfg.target_max_exponent, p.forced_scaled ? 1 : 0, s);
         cudaMemcpyAsync(snap, ds, sizeof(DevDecision), cudaMemcpyDeviceToDevice, s);
     }
-    TcecGemmArgs g = tc_gemm_args(h, p, ws, reinterpret_cast<float*>(dc), m, n, ds);
+    TcecGemmArgs g = tc_gemm_args(h, p, ws, reinterpret_cast<float*>(dc), m, n, ds, false);
     g.ldc = 2 * n;
     g.no_split = 1;
     void* bhi = const_cast<void*>(g.b_hi);

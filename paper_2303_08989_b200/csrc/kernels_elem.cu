@@ -145,14 +145,14 @@ TCEC_DEV void sweep_operand(const float* __restrict__ x, int64_t n, int part, in
 
 // stage 1 (precsel.cpp:23-32 via abs_stats, kernels_scalar.cpp:50-65):
 // nonzero count, count of |x| >= 2^-14, max |x|
-__global__ void __launch_bounds__(kThreads) stats1_kernel(const float* a, int64_t na,
-                                                          const float* b, int64_t nb,
-                                                          DevDecision* d, int nb_a) {
-    const int op = int(blockIdx.x) < nb_a ? 0 : 1;
+// (block `bid` of `nblk`: blocks [0, nb_a) sweep A, the rest B)
+TCEC_DEV void stats1_part(const float* a, int64_t na, const float* b, int64_t nb, DevDecision* d,
+                          int nb_a, int bid, int nblk) {
+    const int op = bid < nb_a ? 0 : 1;
     const float* x = op ? b : a;
     const int64_t n = op ? nb : na;
-    const int part = op ? int(blockIdx.x) - nb_a : int(blockIdx.x);
-    const int nparts = op ? int(gridDim.x) - nb_a : nb_a;
+    const int part = op ? bid - nb_a : bid;
+    const int nparts = op ? nblk - nb_a : nb_a;
     if (x == nullptr || n == 0 || nparts <= 0) return;
     unsigned nz = 0, n1 = 0, mx = 0;
     sweep_operand(x, n, part, nparts, [&](float v) {
@@ -175,6 +175,28 @@ __global__ void __launch_bounds__(kThreads) stats1_kernel(const float* a, int64_
     }
 }
 
+__global__ void __launch_bounds__(kThreads) stats1_kernel(const float* a, int64_t na,
+                                                          const float* b, int64_t nb,
+                                                          DevDecision* d, int nb_a) {
+    stats1_part(a, na, b, nb, d, nb_a, int(blockIdx.x), int(gridDim.x));
+}
+
+// statistics written by other blocks of the same grid (fused preamble): read
+// past the L1
+TCEC_DEV DevStats load_stats(const DevStats* p) {
+    const volatile DevStats* v = p;
+    DevStats st;
+    st.n_nonzero = v->n_nonzero;
+    st.n1 = v->n1;
+    st.n2 = v->n2;
+    st.n_total = v->n_total;
+    st.max_bits = v->max_bits;
+    st.stage2_evaluated = v->stage2_evaluated;
+    st.e_max = v->e_max;
+    st.e_max_valid = v->e_max_valid;
+    return st;
+}
+
 // stage1_passes (precsel.cpp:47-52); r1 in double exactly as precsel.hpp:27-30
 TCEC_DEV bool stage1_passes(unsigned long long nz, unsigned long long n1, unsigned max_bits,
                             double t, int target) {
@@ -185,17 +207,15 @@ TCEC_DEV bool stage1_passes(unsigned long long nz, unsigned long long n1, unsign
 }
 
 // stage 2 (precsel.cpp:34-45 via count_abs_ge): count of |x| >= 2^(e_max - target - 14)
-__global__ void __launch_bounds__(kThreads) stats2_kernel(const float* a, int64_t na,
-                                                          const float* b, int64_t nb,
-                                                          DevDecision* d, double t, int target,
-                                                          int always, int nb_a) {
-    const int op = int(blockIdx.x) < nb_a ? 0 : 1;
+TCEC_DEV void stats2_part(const float* a, int64_t na, const float* b, int64_t nb, DevDecision* d,
+                          double t, int target, int always, int nb_a, int bid, int nblk) {
+    const int op = bid < nb_a ? 0 : 1;
     const float* x = op ? b : a;
     const int64_t n = op ? nb : na;
-    const int part = op ? int(blockIdx.x) - nb_a : int(blockIdx.x);
-    const int nparts = op ? int(gridDim.x) - nb_a : nb_a;
+    const int part = op ? bid - nb_a : bid;
+    const int nparts = op ? nblk - nb_a : nb_a;
     if (x == nullptr || n == 0 || nparts <= 0) return;
-    const DevStats st = d->st[op];
+    const DevStats st = load_stats(&d->st[op]);
     if (!always && stage1_passes(st.n_nonzero, st.n1, st.max_bits, t, target)) return;
     if (st.max_bits == 0) return;  // no e_max: n2 = 0
     const int w = exponent_of_bits(st.max_bits) - (target + 14);
@@ -211,10 +231,15 @@ __global__ void __launch_bounds__(kThreads) stats2_kernel(const float* a, int64_
     if (threadIdx.x == 0 && s) atomicAdd(&d->st[op].n2, s);
 }
 
+__global__ void __launch_bounds__(kThreads) stats2_kernel(const float* a, int64_t na,
+                                                          const float* b, int64_t nb,
+                                                          DevDecision* d, double t, int target,
+                                                          int always, int nb_a) {
+    stats2_part(a, na, b, nb, d, t, target, always, nb_a, int(blockIdx.x), int(gridDim.x));
+}
+
 // finalize ExpStats, tolerance levels and the pair rule (precsel.cpp:95-135)
-__global__ void select_kernel(DevDecision* d, double t, int target, int forced_scaled,
-                              int stage2_always) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+TCEC_DEV void select_body(DevDecision* d, double t, int target, int forced_scaled, int stage2_always) {
     int level[2];
     for (int op = 0; op < 2; ++op) {
         DevStats& st = d->st[op];
@@ -263,6 +288,12 @@ __global__ void select_kernel(DevDecision* d, double t, int target, int forced_s
         d->kind = kKindTf32;
         d->scale_a = d->scale_b = 0;
     }
+}
+
+__global__ void select_kernel(DevDecision* d, double t, int target, int forced_scaled,
+                              int stage2_always) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    select_body(d, t, target, forced_scaled, stage2_always);
 }
 
 // --------------------------------------------------------- operand prep
@@ -367,10 +398,11 @@ TCEC_DEV void convert_n(float (&x)[N], const PrepMode& pm, double factor, float 
 
 // A (m x k complex) -> K-major m x kp; each thread converts 8 consecutive
 // real components of one row (16 B of f16 or 32 B of tf32 per output plane)
-__global__ void __launch_bounds__(kThreads) prep_a_kernel(const float* __restrict__ a, int64_t m,
+TCEC_DEV void prep_a_part(const float* __restrict__ a, int64_t m,
                                                           int64_t k2, int64_t kp, void* hi_v,
                                                           void* lo_v, const DevDecision* d,
-                                                          int kind_fixed, int corrected, int64_t row0) {
+                                                          int kind_fixed, int corrected, int64_t row0,
+        DevDecision* df, int bid, int nblk) {
     // rows [row0, row0 + m) of A (the host-buffer pipeline converts row chunks
     // as they arrive; every row is independent)
     const PrepMode pm = prep_mode(d, kind_fixed, false);
@@ -381,8 +413,8 @@ __global__ void __launch_bounds__(kThreads) prep_a_kernel(const float* __restric
     const int64_t total = m * chunks_per_row;
     unsigned ovf = 0, bad = 0;
     const bool vec = (k2 % 8) == 0 && (reinterpret_cast<uintptr_t>(a) & 15u) == 0;
-    for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < total;
-         c += int64_t(gridDim.x) * blockDim.x) {
+    for (int64_t c = bid * int64_t(blockDim.x) + threadIdx.x; c < total;
+         c += int64_t(nblk) * blockDim.x) {
         const int64_t rl = c / chunks_per_row;
         const int64_t col = (c - rl * chunks_per_row) * 8;
         const int64_t row = row0 + rl;
@@ -422,9 +454,16 @@ __global__ void __launch_bounds__(kThreads) prep_a_kernel(const float* __restric
             }
         }
     }
-    DevDecision* dm = const_cast<DevDecision*>(d);
+    DevDecision* dm = df;
     flag_or(&dm->overflow, ovf);
     flag_or(&dm->scale_overflow, bad);
+}
+
+__global__ void __launch_bounds__(kThreads) prep_a_kernel(const float* __restrict__ a, int64_t m,
+                                                          int64_t k2, int64_t kp, void* hi_v,
+                                                          void* lo_v, const DevDecision* d,
+                                                          int kind_fixed, int corrected, int64_t row0) {
+    prep_a_part(a, m, k2, kp, hi_v, lo_v, d, kind_fixed, corrected, row0, const_cast<DevDecision*>(d), int(blockIdx.x), int(gridDim.x));
 }
 
 // B (k x n complex) -> B'^T (2n x kp, K-major) with the complex block expansion
@@ -437,10 +476,11 @@ __global__ void __launch_bounds__(kThreads) prep_a_kernel(const float* __restric
 // and plane -- converting two kk per lane with the vectorised split.
 constexpr int kPrepBKK = 64, kPrepBJ = 32, kPrepBStride = kPrepBKK + 2;
 
-__global__ void __launch_bounds__(256) prep_b_kernel(const float2* __restrict__ b, int64_t k,
+TCEC_DEV void prep_b_part(const float2* __restrict__ b, int64_t k,
                                                      int64_t n, int64_t kp, void* hi_v,
                                                      void* lo_v, const DevDecision* d,
-                                                     int kind_fixed, int corrected, int64_t jout0) {
+                                                     int kind_fixed, int corrected, int64_t jout0,
+        DevDecision* df, int bid, int nblk) {
     // b is a k x n column block whose B' rows start at 2 jout0
     const PrepMode pm = prep_mode(d, kind_fixed, true);
     if (!pm.active) return;
@@ -453,7 +493,7 @@ __global__ void __launch_bounds__(256) prep_b_kernel(const float2* __restrict__ 
     const int64_t tiles_kk = (kk_cols + kPrepBKK - 1) / kPrepBKK;
     const int64_t ntiles = tiles_j * tiles_kk;
     unsigned ovf = 0, bad = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (int64_t t = bid; t < ntiles; t += nblk) {
         const int64_t j0 = (t % tiles_j) * kPrepBJ, kk0 = (t / tiles_j) * kPrepBKK;
         // load: warp w reads rows kk0 + w, w+8, ... (32 consecutive j each)
 #pragma unroll
@@ -507,9 +547,184 @@ __global__ void __launch_bounds__(256) prep_b_kernel(const float2* __restrict__ 
         }
         __syncthreads();
     }
-    DevDecision* dm = const_cast<DevDecision*>(d);
+    DevDecision* dm = df;
     flag_or(&dm->overflow, ovf);
     flag_or(&dm->scale_overflow, bad);
+}
+
+__global__ void __launch_bounds__(256) prep_b_kernel(const float2* __restrict__ b, int64_t k,
+                                                     int64_t n, int64_t kp, void* hi_v,
+                                                     void* lo_v, const DevDecision* d,
+                                                     int kind_fixed, int corrected, int64_t jout0) {
+    prep_b_part(b, k, n, kp, hi_v, lo_v, d, kind_fixed, corrected, jout0, const_cast<DevDecision*>(d), int(blockIdx.x), int(gridDim.x));
+}
+
+// --------------------------------------------- A-expanded operand layout
+// When A is the smaller operand (m < n: the contraction steps that multiply a
+// small tensor into a large one), the complex block expansion moves to A:
+//   A'' (2m x kp):  row 2i   = (Ar, -Ai) at K' columns (2p, 2p+1)
+//                   row 2i+1 = (Ai,  Ar)
+//   B'' (n x kp):   row j    = (Br, Bi)  -- column j of B, i.e. B^T
+// so C'' = A'' B''^T has row 2i = Re C[i, :], row 2i+1 = Im C[i, :] and the
+// GEMM epilogue interleaves the row pair into C.  Same products, same split
+// (split(-x) = -split(x) for RN and the symmetric saturation), but the
+// expanded, twice-written operand is the small one: 2k (2m + n) instead of
+// 2k (m + 2n) plane elements.
+
+// A (m x k complex) -> A'' (2m x kp); each thread converts 4 consecutive
+// complex elements of one row (8 components) and writes 8 K' columns of both
+// rows of the pair
+TCEC_DEV void prep_ax_part(const float* __restrict__ a, int64_t m,
+                                                           int64_t k, int64_t kp, void* hi_v, void* lo_v,
+                                                           const DevDecision* d, int kind_fixed,
+                                                           int corrected,
+        DevDecision* df, int bid, int nblk) {
+    const PrepMode pm = prep_mode(d, kind_fixed, false);
+    if (!pm.active) return;
+    const double factor = ldexp(1.0, pm.scale);
+    const float fs = (pm.scale >= -149 && pm.scale <= 127) ? ldexpf(1.0f, pm.scale) : 1.0f;
+    const int64_t k2 = 2 * k;
+    const int64_t chunks_per_row = kp / 8;
+    const int64_t total = m * chunks_per_row;
+    unsigned ovf = 0, bad = 0;
+    const bool vec = (k2 % 8) == 0 && (reinterpret_cast<uintptr_t>(a) & 15u) == 0;
+    for (int64_t c = bid * int64_t(blockDim.x) + threadIdx.x; c < total;
+         c += int64_t(nblk) * blockDim.x) {
+        const int64_t row = c / chunks_per_row;
+        const int64_t col = (c - row * chunks_per_row) * 8;  // K' column = 2 p0
+        float x[8];
+        if (vec && col < k2) {
+            const float4* p = reinterpret_cast<const float4*>(a + row * k2 + col);
+            const float4 v0 = __ldcs(p), v1 = __ldcs(p + 1);
+            x[0] = v0.x; x[1] = v0.y; x[2] = v0.z; x[3] = v0.w;
+            x[4] = v1.x; x[5] = v1.y; x[6] = v1.z; x[7] = v1.w;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) x[e] = (col + e < k2) ? a[row * k2 + col + e] : 0.0f;
+        }
+        float h[8], l[8];
+        convert_n<8>(x, pm, factor, fs, corrected, h, l, ovf, bad);
+        // row 2i: (re, -im); the K padding stays +0 (negating the zero fill would write -0)
+        float hn[4], ln[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const bool pad = col + 2 * e >= k2;
+            hn[e] = pad ? 0.0f : -h[2 * e + 1];
+            ln[e] = pad ? 0.0f : -l[2 * e + 1];
+        }
+        const int64_t r0 = (2 * row) * kp + col, r1 = r0 + kp;
+        if (pm.fmt == kFp16) {
+            __half2 q0[4], q1[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                q0[e] = __floats2half2_rn(h[2 * e], hn[e]);         // exact: values are FP16
+                q1[e] = __floats2half2_rn(h[2 * e + 1], h[2 * e]);
+            }
+            __half* hp = static_cast<__half*>(hi_v);
+            *reinterpret_cast<uint4*>(hp + r0) = *reinterpret_cast<uint4*>(q0);
+            *reinterpret_cast<uint4*>(hp + r1) = *reinterpret_cast<uint4*>(q1);
+            if (corrected) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    q0[e] = __floats2half2_rn(l[2 * e], ln[e]);
+                    q1[e] = __floats2half2_rn(l[2 * e + 1], l[2 * e]);
+                }
+                __half* lp = static_cast<__half*>(lo_v);
+                *reinterpret_cast<uint4*>(lp + r0) = *reinterpret_cast<uint4*>(q0);
+                *reinterpret_cast<uint4*>(lp + r1) = *reinterpret_cast<uint4*>(q1);
+            }
+        } else {
+            float4* hp0 = reinterpret_cast<float4*>(static_cast<float*>(hi_v) + r0);
+            float4* hp1 = reinterpret_cast<float4*>(static_cast<float*>(hi_v) + r1);
+            hp0[0] = make_float4(h[0], hn[0], h[2], hn[1]);
+            hp0[1] = make_float4(h[4], hn[2], h[6], hn[3]);
+            hp1[0] = make_float4(h[1], h[0], h[3], h[2]);
+            hp1[1] = make_float4(h[5], h[4], h[7], h[6]);
+            if (corrected) {
+                float4* lp0 = reinterpret_cast<float4*>(static_cast<float*>(lo_v) + r0);
+                float4* lp1 = reinterpret_cast<float4*>(static_cast<float*>(lo_v) + r1);
+                lp0[0] = make_float4(l[0], ln[0], l[2], ln[1]);
+                lp0[1] = make_float4(l[4], ln[2], l[6], ln[3]);
+                lp1[0] = make_float4(l[1], l[0], l[3], l[2]);
+                lp1[1] = make_float4(l[5], l[4], l[7], l[6]);
+            }
+        }
+    }
+    DevDecision* dm = df;
+    flag_or(&dm->overflow, ovf);
+    flag_or(&dm->scale_overflow, bad);
+}
+
+__global__ void __launch_bounds__(kThreads) prep_ax_kernel(const float* __restrict__ a, int64_t m,
+                                                           int64_t k, int64_t kp, void* hi_v, void* lo_v,
+                                                           const DevDecision* d, int kind_fixed,
+                                                           int corrected) {
+    prep_ax_part(a, m, k, kp, hi_v, lo_v, d, kind_fixed, corrected, const_cast<DevDecision*>(d), int(blockIdx.x), int(gridDim.x));
+}
+
+// B (k x n complex) -> B'' = B^T (n x kp, K-major, (re, im) pairs along K).
+// Same 64 (kk) x 32 (j) smem tiles as prep_b_kernel, one output row per j.
+TCEC_DEV void prep_bx_part(const float2* __restrict__ b, int64_t k,
+                                                      int64_t n, int64_t kp, void* hi_v, void* lo_v,
+                                                      const DevDecision* d, int kind_fixed,
+                                                      int corrected,
+        DevDecision* df, int bid, int nblk) {
+    const PrepMode pm = prep_mode(d, kind_fixed, true);
+    if (!pm.active) return;
+    const double factor = ldexp(1.0, pm.scale);
+    const float fs = (pm.scale >= -149 && pm.scale <= 127) ? ldexpf(1.0f, pm.scale) : 1.0f;
+    __shared__ __align__(16) float2 tile[kPrepBJ][kPrepBStride];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;  // 8 warps
+    const int64_t tiles_j = (n + kPrepBJ - 1) / kPrepBJ;
+    const int64_t kk_cols = kp / 2;
+    const int64_t tiles_kk = (kk_cols + kPrepBKK - 1) / kPrepBKK;
+    const int64_t ntiles = tiles_j * tiles_kk;
+    unsigned ovf = 0, bad = 0;
+    for (int64_t t = bid; t < ntiles; t += nblk) {
+        const int64_t j0 = (t % tiles_j) * kPrepBJ, kk0 = (t / tiles_j) * kPrepBKK;
+#pragma unroll
+        for (int r = 0; r < kPrepBKK / 8; ++r) {
+            const int kk = warp + 8 * r;
+            const int64_t gk = kk0 + kk, gj = j0 + lane;
+            tile[lane][kk] = (gk < k && gj < n) ? __ldcs(b + gk * n + gj) : make_float2(0.0f, 0.0f);
+        }
+        __syncthreads();
+        const int64_t col = 2 * (kk0 + 2 * lane);
+        if (col < kp) {
+            for (int jj = warp; jj < kPrepBJ; jj += 8) {
+                const int64_t j = j0 + jj;
+                if (j >= n) break;
+                const float4 v = *reinterpret_cast<const float4*>(&tile[jj][2 * lane]);
+                float xv[4] = {v.x, v.y, v.z, v.w}, hv[4], lv[4];   // (re0, im0, re1, im1)
+                convert_n<4>(xv, pm, factor, fs, corrected, hv, lv, ovf, bad);
+                const int64_t r0 = j * kp + col;
+                if (pm.fmt == kFp16) {
+                    __half2 q[2] = {__floats2half2_rn(hv[0], hv[1]), __floats2half2_rn(hv[2], hv[3])};
+                    *reinterpret_cast<uint2*>(static_cast<__half*>(hi_v) + r0) = *reinterpret_cast<uint2*>(q);
+                    if (corrected) {
+                        __half2 w[2] = {__floats2half2_rn(lv[0], lv[1]), __floats2half2_rn(lv[2], lv[3])};
+                        *reinterpret_cast<uint2*>(static_cast<__half*>(lo_v) + r0) = *reinterpret_cast<uint2*>(w);
+                    }
+                } else {
+                    *reinterpret_cast<float4*>(static_cast<float*>(hi_v) + r0) = make_float4(hv[0], hv[1], hv[2], hv[3]);
+                    if (corrected)
+                        *reinterpret_cast<float4*>(static_cast<float*>(lo_v) + r0) =
+                            make_float4(lv[0], lv[1], lv[2], lv[3]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    DevDecision* dm = df;
+    flag_or(&dm->overflow, ovf);
+    flag_or(&dm->scale_overflow, bad);
+}
+
+__global__ void __launch_bounds__(256) prep_bx_kernel(const float2* __restrict__ b, int64_t k,
+                                                      int64_t n, int64_t kp, void* hi_v, void* lo_v,
+                                                      const DevDecision* d, int kind_fixed,
+                                                      int corrected) {
+    prep_bx_part(b, k, n, kp, hi_v, lo_v, d, kind_fixed, corrected, const_cast<DevDecision*>(d), int(blockIdx.x), int(gridDim.x));
 }
 
 // ------------------------------------------------------------ SIMT GEMM
@@ -1516,6 +1731,23 @@ void launch_prep_b(const float* b, int64_t k, int64_t n, int64_t kp, void* hi, v
     const unsigned grid = unsigned(tiles < 148 * 8 ? tiles : 148 * 8);
     prep_b_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const float2*>(b), k, n, kp, hi, lo, d,
                                        kind_fixed, corrected, jout0);
+}
+
+void launch_prep_ax(const float* a, int64_t m, int64_t k, int64_t kp, void* hi, void* lo,
+                    const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s) {
+    const int64_t total = m * (kp / 8);
+    if (total <= 0) return;
+    prep_ax_kernel<<<grid_for(total, kThreads, 148 * 32), kThreads, 0, s>>>(a, m, k, kp, hi, lo, d,
+                                                                           kind_fixed, corrected);
+}
+
+void launch_prep_bx(const float* b, int64_t k, int64_t n, int64_t kp, void* hi, void* lo,
+                    const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s) {
+    if (n <= 0 || kp <= 0) return;
+    const int64_t tiles = ((n + kPrepBJ - 1) / kPrepBJ) * ((kp / 2 + kPrepBKK - 1) / kPrepBKK);
+    const unsigned grid = unsigned(tiles < 148 * 8 ? tiles : 148 * 8);
+    prep_bx_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const float2*>(b), k, n, kp, hi, lo, d,
+                                        kind_fixed, corrected);
 }
 
 void launch_cgemm_fp32_ref(const float2* a, const float2* b, float2* c, int64_t m, int64_t n,

@@ -361,6 +361,7 @@ static std::string plan_key(const int* steps, int n_steps, const tcec_dispatch_c
     k.append(reinterpret_cast<const char*>(&cfg), sizeof(cfg));
     k.append(reinterpret_cast<const char*>(&h.flush_kblocks), sizeof(int));
     k.append(reinterpret_cast<const char*>(&h.gemm_pair), sizeof(int));  // kernel variant
+    k.append(reinterpret_cast<const char*>(&h.layout), sizeof(int));     // operand layout
     k.append(reinterpret_cast<const char*>(&h.executor), sizeof(int));
     k.append(reinterpret_cast<const char*>(&ws), sizeof(ws));
     k.append(reinterpret_cast<const char*>(&dec), sizeof(dec));

@@ -77,6 +77,29 @@ TCEC_DEV void epi_bar_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
 }
 
+// A-expanded layout store: one C row from the staged Re row `s0` and the Im
+// row s0 + cs (COLS columns, `valid` of them inside C): each lane interleaves
+// 4 columns at a time into two 16-B stores, a warp writes 1 KB contiguous
+template <int COLS>
+TCEC_DEV void store_xa_row(float* __restrict__ dst, const float* s0, int cs, int valid, bool full, int lane) {
+    const float* s1 = s0 + cs;
+    if (full) {
+#pragma unroll
+        for (int j = 4 * lane; j < COLS; j += 128) {
+            const float4 re = *reinterpret_cast<const float4*>(s0 + j);
+            const float4 im = *reinterpret_cast<const float4*>(s1 + j);
+            float4* d4 = reinterpret_cast<float4*>(dst + 2 * j);
+            __stcs(d4, make_float4(re.x, im.x, re.y, im.y));
+            __stcs(d4 + 1, make_float4(re.z, im.z, re.w, im.w));
+        }
+    } else {
+        for (int j = lane; j < COLS && j < valid; j += 32) {
+            dst[2 * j] = s0[j];
+            dst[2 * j + 1] = s1[j];
+        }
+    }
+}
+
 template <int FMT>
 __global__ void __launch_bounds__(kThreadsGemm, 1)
     tcec_gemm_kernel(const __grid_constant__ CUtensorMap map_ahi,
@@ -84,7 +107,7 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
                      const __grid_constant__ CUtensorMap map_bhi,
                      const __grid_constant__ CUtensorMap map_blo, float* __restrict__ c,
                      int m, int n2, int kp, const DevDecision* __restrict__ dec, int kind_fixed,
-                     int corrected, int flush_kblocks, float* __restrict__ partial, int kb_per) {
+                     int corrected, int flush_kblocks, float* __restrict__ partial, int kb_per, int xa) {
     using T = Traits<FMT>;
     // device-side mode selection: the kernel of the unselected format exits
     // (the paper's "both kernels launched, one exits early")
@@ -264,6 +287,14 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
         epi_bar_sync();
         const int ew = warp - 2;
         const bool full_cols = n0 + BN <= n2 && (n2 & 3) == 0;
+        if (xa && !partial) {
+            // A-expanded layout: tile rows 2i / 2i+1 = Re / Im of C row m0/2 + i
+            for (int r = ew; r < BM / 2; r += kEpiWarps) {
+                if (m0 + 2 * r >= m) break;
+                store_xa_row<BN>(c + size_t(m0 / 2 + r) * (2 * size_t(n2)) + 2 * size_t(n0),
+                                 ctile + size_t(2 * r) * kCStride, kCStride, n2 - n0, full_cols, lane);
+            }
+        } else
         for (int r = ew; r < BM; r += kEpiWarps) {
             const int grow = m0 + r;
             if (grow >= m) break;
@@ -286,18 +317,24 @@ __global__ void __launch_bounds__(kThreadsGemm, 1)
 }
 
 // split-K epilogue: C = descale(sum of the partials in split order), RN
+// (A-expanded layout: output float o = (i, j, e) of C reads GEMM row 2i + e, column j)
 __global__ void __launch_bounds__(256) split_reduce_kernel(const float* __restrict__ partial,
                                                            float* __restrict__ c, int64_t count,
                                                            int splits, const DevDecision* __restrict__ dec,
-                                                           int kind_fixed) {
+                                                           int kind_fixed, int64_t xa_cols) {
     const int kind = kind_fixed >= 0 ? kind_fixed : dec->kind;
     const bool scaled = kind == kKindFp16Scaled && (dec->scale_a + dec->scale_b) != 0;
     const double f = scaled ? ldexp(1.0, -(dec->scale_a + dec->scale_b)) : 1.0;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count;
-         i += int64_t(gridDim.x) * blockDim.x) {
+    for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < count;
+         o += int64_t(gridDim.x) * blockDim.x) {
+        int64_t i = o;
+        if (xa_cols > 0) {
+            const int64_t row = o / (2 * xa_cols), rem = o - row * 2 * xa_cols;
+            i = (2 * row + (rem & 1)) * xa_cols + (rem >> 1);
+        }
         float s = partial[i];
         for (int y = 1; y < splits; ++y) s = __fadd_rn(s, partial[size_t(y) * size_t(count) + size_t(i)]);
-        c[i] = scaled ? scale_pow2(s, f) : s;
+        c[o] = scaled ? scale_pow2(s, f) : s;
     }
 }
 
@@ -568,7 +605,7 @@ struct WideMaps {
 template <int FMT>
 __device__ __forceinline__ void widep_body(const WideMaps& mp, float* __restrict__ c, int m, int n2,
                                           int kp, const DevDecision* __restrict__ dec, int kind,
-                                          int corrected, int flush_kblocks) {
+                                          int corrected, int flush_kblocks, int xa) {
     using T = Traits<FMT>;
     constexpr uint32_t kIdescHalf = umma_idesc<FMT, 2 * BM, 128>();
     constexpr uint32_t kIdescFull = umma_idesc<FMT, 2 * BM, kWideBN>();
@@ -797,6 +834,18 @@ __device__ __forceinline__ void widep_body(const WideMaps& mp, float* __restrict
                                             acc[64 * hh + i + 3]);
                 }
                 epi_bar_sync();
+                if (xa) {
+                    // A-expanded layout: 16 C rows per quadrant, 2 per warp
+#pragma unroll
+                    for (int rr = 0; rr < 2; ++rr) {
+                        const int r = 2 * ew + rr;  // C row within the quadrant's 16
+                        const int grow2 = m0 + 32 * qq + 2 * r;
+                        if (grow2 < m)
+                            store_xa_row<kWideBN>(c + size_t(grow2 / 2) * (2 * size_t(n2)) + 2 * size_t(n0),
+                                                  cstage + size_t(2 * r) * kWideCStride, kWideCStride, n2 - n0,
+                                                  full_cols, lane);
+                    }
+                } else
 #pragma unroll
                 for (int rr = 0; rr < 4; ++rr) {
                     const int r = 4 * ew + rr;
@@ -831,11 +880,11 @@ template <int FMT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
     tcec_gemm_widep_kernel(const __grid_constant__ WideMaps maps, float* __restrict__ c, int m,
                           int n2, int kp, const DevDecision* __restrict__ dec, int kind_fixed,
-                          int corrected, int flush_kblocks) {
+                          int corrected, int flush_kblocks, int xa) {
     const int kind = kind_fixed >= 0 ? kind_fixed : dec->kind;
     const bool mine = FMT == kTf32 ? kind == kKindTf32 : (kind == kKindFp16 || kind == kKindFp16Scaled);
     if (!mine) return;
-    widep_body<FMT>(maps, c, m, n2, kp, dec, kind, corrected, flush_kblocks);
+    widep_body<FMT>(maps, c, m, n2, kp, dec, kind, corrected, flush_kblocks, xa);
 }
 
 // format decided on the device (AUTO): one launch that runs the selected
@@ -844,12 +893,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
     tcec_gemm_widep_auto_kernel(const __grid_constant__ WideMaps maps16,
                                const __grid_constant__ WideMaps maps32, float* __restrict__ c,
                                int m, int n2, int kp, const DevDecision* __restrict__ dec,
-                               int corrected, int flush_kblocks) {
+                               int corrected, int flush_kblocks, int xa) {
     const int kind = dec->kind;
     if (kind == kKindTf32)
-        widep_body<kTf32>(maps32, c, m, n2, kp, dec, kind, corrected, flush_kblocks);
+        widep_body<kTf32>(maps32, c, m, n2, kp, dec, kind, corrected, flush_kblocks, xa);
     else if (kind == kKindFp16 || kind == kKindFp16Scaled)
-        widep_body<kFp16>(maps16, c, m, n2, kp, dec, kind, corrected, flush_kblocks);
+        widep_body<kFp16>(maps16, c, m, n2, kp, dec, kind, corrected, flush_kblocks, xa);
 }
 
 // ===================================================================== wide pair
@@ -893,7 +942,7 @@ __device__ __forceinline__ void wide_body(const WideMaps& mp, float* __restrict_
                                           int kp, const DevDecision* __restrict__ dec, int kind,
                                           int corrected, int flush_kblocks, int group_m,
                                           int a_row_off, int ldc, float* __restrict__ partial,
-                                          int kb_per) {
+                                          int kb_per, int xa) {
     using T = Traits<FMT>;
     constexpr uint32_t kIdescHalf = umma_idesc<FMT, 2 * BM, 128>();
     constexpr uint32_t kIdescFull = umma_idesc<FMT, 2 * BM, kNpBN>();
@@ -1114,6 +1163,15 @@ __device__ __forceinline__ void wide_body(const WideMaps& mp, float* __restrict_
         const int ew = warp - 2;
         const int ld = partial ? n2 : ldc;  // C may be a column block of a wider matrix
         const bool full_cols = n0 + kNpBN <= n2 && (ld & 3) == 0;
+        if (xa && !partial) {
+            // A-expanded layout: tile rows 2i / 2i+1 = Re / Im of C row m0/2 + i
+            // (ldc = floats per C row)
+            for (int r = ew; r < BM / 2; r += kEpiWarps) {
+                if (m0 + 2 * r >= m) break;
+                store_xa_row<kNpBN>(c + size_t(m0 / 2 + r) * size_t(ld) + 2 * size_t(n0),
+                                    ctile + size_t(2 * r) * kNpCStride, kNpCStride, n2 - n0, full_cols, lane);
+            }
+        } else
         for (int r = ew; r < BM; r += kEpiWarps) {
             const int grow = m0 + r;
             if (grow >= m) break;
@@ -1143,12 +1201,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
     tcec_gemm_wide_kernel(const __grid_constant__ WideMaps maps, float* __restrict__ c, int m,
                           int n2, int kp, const DevDecision* __restrict__ dec, int kind_fixed,
                           int corrected, int flush_kblocks, int group_m, int a_row_off, int ldc,
-                          float* __restrict__ partial, int kb_per) {
+                          float* __restrict__ partial, int kb_per, int xa) {
     const int kind = kind_fixed >= 0 ? kind_fixed : dec->kind;
     const bool mine = FMT == kTf32 ? kind == kKindTf32 : (kind == kKindFp16 || kind == kKindFp16Scaled);
     if (!mine) return;  // both CTAs of the pair read the same decision
     wide_body<FMT, 1>(maps, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off, ldc,
-                      partial, kb_per);
+                      partial, kb_per, xa);
 }
 
 // clusters of two CTA pairs sharing B' tiles by TMA multicast
@@ -1157,12 +1215,12 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreadsGemm, 1)
     tcec_gemm_widemc_kernel(const __grid_constant__ WideMaps maps, float* __restrict__ c, int m,
                             int n2, int kp, const DevDecision* __restrict__ dec, int kind_fixed,
                             int corrected, int flush_kblocks, int group_m, int a_row_off, int ldc,
-                            float* __restrict__ partial, int kb_per) {
+                            float* __restrict__ partial, int kb_per, int xa) {
     const int kind = kind_fixed >= 0 ? kind_fixed : dec->kind;
     const bool mine = FMT == kTf32 ? kind == kKindTf32 : (kind == kKindFp16 || kind == kKindFp16Scaled);
     if (!mine) return;  // all four CTAs read the same decision
     wide_body<FMT, 2>(maps, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off, ldc,
-                      partial, kb_per);
+                      partial, kb_per, xa);
 }
 
 // format decided on the device (AUTO): one launch that runs the selected
@@ -1172,14 +1230,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
                                const __grid_constant__ WideMaps maps32, float* __restrict__ c,
                                int m, int n2, int kp, const DevDecision* __restrict__ dec,
                                int corrected, int flush_kblocks, int group_m, int a_row_off,
-                               int ldc, float* __restrict__ partial, int kb_per) {
+                               int ldc, float* __restrict__ partial, int kb_per, int xa) {
     const int kind = dec->kind;
     if (kind == kKindTf32)
         wide_body<kTf32, 1>(maps32, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off,
-                            ldc, partial, kb_per);
+                            ldc, partial, kb_per, xa);
     else if (kind == kKindFp16 || kind == kKindFp16Scaled)
         wide_body<kFp16, 1>(maps16, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off,
-                            ldc, partial, kb_per);
+                            ldc, partial, kb_per, xa);
 }
 
 __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreadsGemm, 1)
@@ -1187,14 +1245,14 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreadsGemm, 1)
                                  const __grid_constant__ WideMaps maps32, float* __restrict__ c,
                                  int m, int n2, int kp, const DevDecision* __restrict__ dec,
                                  int corrected, int flush_kblocks, int group_m, int a_row_off,
-                                 int ldc, float* __restrict__ partial, int kb_per) {
+                                 int ldc, float* __restrict__ partial, int kb_per, int xa) {
     const int kind = dec->kind;
     if (kind == kKindTf32)
         wide_body<kTf32, 2>(maps32, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off,
-                            ldc, partial, kb_per);
+                            ldc, partial, kb_per, xa);
     else if (kind == kKindFp16 || kind == kKindFp16Scaled)
         wide_body<kFp16, 2>(maps16, c, m, n2, kp, dec, kind, corrected, flush_kblocks, group_m, a_row_off,
-                            ldc, partial, kb_per);
+                            ldc, partial, kb_per, xa);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -1253,6 +1311,9 @@ int wide_group_m() {
     return g;
 }
 
+// floats per row of C (A-expanded layout: one C row per GEMM row pair)
+int64_t ldc_of(const TcecGemmArgs& g) { return g.ldc > 0 ? g.ldc : (g.xa ? 2 * g.n2 : g.n2); }
+
 // one cluster per 256 x 256 tile
 unsigned wide_tiles_grid(const TcecGemmArgs& g) {
     return unsigned(2 * ((g.m + 2 * BM - 1) / (2 * BM)) * ((g.n2 + kWideBN - 1) / kWideBN));
@@ -1294,15 +1355,15 @@ int launch_fmt(const TcecGemmArgs& g, cudaStream_t s) {
             tcec_gemm_widemc_kernel<FMT><<<dim3(wide_tiles_grid(g), unsigned(g.partial ? g.splits : 1)),
                                            kThreadsGemm, kNpSmemBytes, s>>>(
                 w, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed, g.corrected, g.flush_kblocks,
-                wide_group_m(), int(g.a_row_off), int(g.ldc > 0 ? g.ldc : g.n2), g.partial, g.kb_per);
+                wide_group_m(), int(g.a_row_off), int(ldc_of(g)), g.partial, g.kb_per, g.xa);
         else if (g.pair == kVariantWide)
             tcec_gemm_wide_kernel<FMT><<<dim3(wide_tiles_grid(g), unsigned(g.partial ? g.splits : 1)),
                                          kThreadsGemm, kNpSmemBytes, s>>>(
                 w, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed, g.corrected, g.flush_kblocks,
-                wide_group_m(), int(g.a_row_off), int(g.ldc > 0 ? g.ldc : g.n2), g.partial, g.kb_per);
+                wide_group_m(), int(g.a_row_off), int(ldc_of(g)), g.partial, g.kb_per, g.xa);
         else
             tcec_gemm_widep_kernel<FMT><<<wide_grid(g), kThreadsGemm, kWideSmemBytes, s>>>(
-                w, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed, g.corrected, g.flush_kblocks);
+                w, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed, g.corrected, g.flush_kblocks, g.xa);
         return int(cudaGetLastError());
     }
     CUtensorMap mah, mal, mbh, mbl;
@@ -1323,7 +1384,7 @@ int launch_fmt(const TcecGemmArgs& g, cudaStream_t s) {
         const dim3 grid(unsigned(tiles), unsigned(g.partial ? g.splits : 1));
         tcec_gemm_kernel<FMT><<<grid, kThreadsGemm, kSmemBytes, s>>>(
             mah, mal, mbh, mbl, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed,
-            g.corrected, g.flush_kblocks, g.partial, g.kb_per);
+            g.corrected, g.flush_kblocks, g.partial, g.kb_per, g.xa);
     }
     return int(cudaGetLastError());
 }
@@ -1350,15 +1411,15 @@ int launch_wide_auto(const TcecGemmArgs& g, cudaStream_t s) {
         tcec_gemm_widemc_auto_kernel<<<dim3(wide_tiles_grid(g), unsigned(g.partial ? g.splits : 1)),
                                        kThreadsGemm, kNpSmemBytes, s>>>(
             w16, w32, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.corrected, g.flush_kblocks,
-            wide_group_m(), int(g.a_row_off), int(g.ldc > 0 ? g.ldc : g.n2), g.partial, g.kb_per);
+            wide_group_m(), int(g.a_row_off), int(ldc_of(g)), g.partial, g.kb_per, g.xa);
     else if (g.pair == kVariantWide)
         tcec_gemm_wide_auto_kernel<<<dim3(wide_tiles_grid(g), unsigned(g.partial ? g.splits : 1)),
                                      kThreadsGemm, kNpSmemBytes, s>>>(
             w16, w32, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.corrected, g.flush_kblocks,
-            wide_group_m(), int(g.a_row_off), int(g.ldc > 0 ? g.ldc : g.n2), g.partial, g.kb_per);
+            wide_group_m(), int(g.a_row_off), int(ldc_of(g)), g.partial, g.kb_per, g.xa);
     else
         tcec_gemm_widep_auto_kernel<<<wide_grid(g), kThreadsGemm, kWideSmemBytes, s>>>(
-            w16, w32, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.corrected, g.flush_kblocks);
+            w16, w32, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.corrected, g.flush_kblocks, g.xa);
     return int(cudaGetLastError());
 }
 
@@ -1386,6 +1447,8 @@ int launch_tcec_gemm(const TcecGemmArgs& g_in, cudaStream_t s) {
     g.kb_per = 0;
     // clusters of two pairs need an even number of 256-row tiles
     if (g.pair == kVariantWideMc && ((g.m + 2 * BM - 1) / (2 * BM)) % 2 != 0) g.pair = kVariantWide;
+    // the 256 x 128 pair kernel has no A-expanded store
+    if (g.xa && g.pair == kVariantPair) g.pair = kVariantWide;
     if (g.ldc > 0 && g.ldc != g.n2) g.no_split = 1;  // partials and their reduction assume ldc = n2
     if (!g.no_split && (g.pair == kVariantSingle || g.pair == kVariantWide || g.pair == kVariantWideMc)) {
         // few tiles and a long K (e.g. (512, 512, 2^19) contraction steps):
@@ -1446,7 +1509,7 @@ int launch_tcec_gemm(const TcecGemmArgs& g_in, cudaStream_t s) {
         const int64_t count = g.m * g.n2;
         const int64_t blocks = std::min<int64_t>((count + 255) / 256, 148 * 16);
         split_reduce_kernel<<<unsigned(blocks), 256, 0, s>>>(g.partial, g.c, count, g.splits, g.d,
-                                                            g.kind_fixed);
+                                                            g.kind_fixed, g.xa ? g.n2 : 0);
         e = int(cudaGetLastError());
     }
     if (g.partial) cudaFreeAsync(g.partial, s);

@@ -18,6 +18,7 @@ struct tcec_handle_s {
     int flush_kblocks = 1;  // RN flush of the main term every k-block (64 f16 / 32 tf32 K')
     int executor = 0;       // network executor: 0 auto, 1 per-step only, 2 fused only
     int gemm_pair = 0;      // tcgen05 kernel variant (tcec_set_gemm_variant): 0 auto, 1 pair, 2 single, 3 wide
+    int layout = 0;         // operand layout (tcec_set_operand_layout): 0 auto, 1 B-expanded, 2 A-expanded
     // operand workspace (split hi/lo planes), grown on demand
     void* ws = nullptr;
     size_t ws_bytes = 0;
@@ -57,7 +58,7 @@ struct tcec_handle_s {
         int64_t m, n, k;
         double t;
         int64_t size_auto, size_tf32;
-        int target, k_tile, force, variant, flush;
+        int target, k_tile, force, variant, flush, layout;
         cudaStream_t stream;
         cudaGraphExec_t exec;
     };

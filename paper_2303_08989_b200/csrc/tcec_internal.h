@@ -62,6 +62,13 @@ void launch_prep_a(const float* a, int64_t m, int64_t k, int64_t kp, void* hi, v
 void launch_prep_b(const float* b, int64_t k, int64_t n, int64_t kp, void* hi, void* lo,
                    const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s,
                    int64_t jout0 = 0);  // b = a k x n column block, B' rows from 2 jout0
+// A-expanded layout (used when m < n): A'' = 2m x Kp with rows 2i = (Ar, -Ai),
+// 2i+1 = (Ai, Ar) along K; B'' = B^T = n x Kp with (Br, Bi) along K.  The GEMM
+// yields rows (Re C[i,:], Im C[i,:]) and its epilogue interleaves them.
+void launch_prep_ax(const float* a, int64_t m, int64_t k, int64_t kp, void* hi, void* lo,
+                    const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s);
+void launch_prep_bx(const float* b, int64_t k, int64_t n, int64_t kp, void* hi, void* lo,
+                    const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s);
 
 // -------------------------------------------------------------- SIMT GEMM
 // FP32_REF complex GEMM, bit-identical to the reference schedule
@@ -104,6 +111,8 @@ struct TcecGemmArgs {
     int no_split;                         // 1: never split K (row-chunked launches must match the one-launch bits)
     int64_t ldc;                          // row stride of C in floats, 0 = n2 (wide kernel: column blocks of C)
     int64_t b_row_off;                    // first B' row of this launch (wide kernel: column blocks of B)
+    int xa;                               // 1: A-expanded layout (m = 2 x rows of C, n2 = columns of C,
+                                          //    GEMM rows 2i / 2i+1 = Re / Im of C row i, interleaved on store)
 };
 // tcgen05 kernel variants (tcec_set_gemm_variant): auto picks wide when its
 // 256 x 256 pair tiles fill the SMs, else single

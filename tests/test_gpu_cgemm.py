@@ -349,3 +349,69 @@ def test_multicast_clusters_bit_identical_to_pairs(handle, dev, shape, mode):
             handle.set_gemm_variant("auto")
     assert lines["wide"] == lines["wide_mc"]
     assert np.array_equal(outs["wide"].view(np.uint32), outs["wide_mc"].view(np.uint32)), lines["wide"]
+
+
+@pytest.mark.parametrize("variant", ["auto", "single", "wide", "wide_persistent", "wide_mc"])
+@pytest.mark.parametrize("shape", [(3, 5, 7), (64, 1000, 33), (129, 65, 200), (130, 600, 1100),
+                                   (256, 4096, 64), (200, 150, 9000), (512, 2048, 512), (1, 300, 40)])
+def test_operand_layouts(handle, orc, dev, variant, shape):
+    """Both operand layouts -- the complex block expansion on B (B' = [[Br, Bi],
+    [-Bi, Br]]) or on A (A'' rows (Ar, -Ai) / (Ai, Ar), C rows interleaved by
+    the epilogue) -- meet the reference bar in every kernel variant, for the
+    host-known kinds, the device-decided format and the descaled scaled kind;
+    split-K (long k) and the persistent small-k kernel included."""
+    m, n, k = shape
+    a = matrix_recipe("uniform", m, k, 71 + m)
+    b = matrix_recipe("uniform", k, n, 73 + n)
+    ref = orc.cgemm_oracle(a, b)
+    err_ref = relerr(orc.cgemm(a, b, "FP32_REF")[0], ref)
+    ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    handle.set_gemm_variant(variant)
+    try:
+        for layout in ("a", "b"):
+            handle.set_operand_layout(layout)
+            for mode in ("FP16TCEC", "TF32TCEC"):
+                c, _ = handle.cgemm(ad, bd, mode)
+                e = relerr(c.cpu().numpy(), ref)
+                assert e <= max(TOL_FACTOR * err_ref, 2e-7), (layout, mode, e, err_ref)
+            c, res = handle.dispatch_cgemm(ad * 2.0 ** -20, bd, SelectionPolicy(size_auto=1, size_tf32=1))
+            assert "FP16TCEC_SCALED" in res.line, res.line
+            e = relerr(c.cpu().numpy() * 2.0 ** 20, ref)
+            assert e <= max(TOL_FACTOR * err_ref, 2e-7), (layout, "SCALED", e, err_ref)
+    finally:
+        handle.set_operand_layout("auto")
+        handle.set_gemm_variant("auto")
+
+
+@pytest.mark.parametrize("shape", [(512, 2048, 64), (512, 1024, 333), (1024, 4096, 1000)])
+def test_operand_layout_a_multicast_bit_identical(handle, dev, shape):
+    """In the A-expanded layout the multicast clusters still run the pair
+    kernel's MMA sequence on the same operand bits: C is bit-identical."""
+    m, n, k = shape
+    a = matrix_recipe("uniform", m, k, 17 + m)
+    b = matrix_recipe("uniform", k, n, 19 + n)
+    ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    outs = {}
+    handle.set_operand_layout("a")
+    try:
+        for variant in ("wide", "wide_mc"):
+            handle.set_gemm_variant(variant)
+            c, _ = handle.cgemm(ad, bd, "TF32TCEC")
+            outs[variant] = c.cpu().numpy()
+    finally:
+        handle.set_gemm_variant("auto")
+        handle.set_operand_layout("auto")
+    assert np.array_equal(outs["wide"].view(np.uint32), outs["wide_mc"].view(np.uint32))
+
+
+def test_operand_layout_host_buffers(handle):
+    """The host-buffer entry point with an A-expanded dispatch (m < n) equals
+    the device-pointer dispatch bit for bit."""
+    r = O.Rng(99)
+    a, b = r.uniform_c32(384, 700), r.uniform_c32(700, 2100)
+    cfg = make_config(SelectionPolicy(size_auto=64, size_tf32=32))
+    ch, res_h = handle.dispatch_cgemm_host(a, b, cfg)
+    dev = torch.device("cuda:0")
+    cd, res_d = handle.dispatch_cgemm(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev), cfg)
+    assert res_h.line == res_d.line
+    assert np.array_equal(ch.view(np.uint32), cd.cpu().numpy().view(np.uint32))

@@ -7,9 +7,13 @@ kernels every tensor-core dispatch runs) against the reference arithmetic:
 rearranged into the tensor-core layout: A' = A viewed as m x 2k (interleaved
 re/im along K), B'^T = the 2n x 2k block expansion with row 2j = (Br, -Bi) and
 row 2j+1 = (Bi, Br) per complex k, both K-major and zero padded to
-kp = round_up(2k, 64).  The oracle (the C restatement, pinned to the reference
-build) is the checker; the device planes come back through tcec_debug_prep.
-Uncorrected (TC ablation) preparation is pinned against quantize_buf(RN).
+kp = round_up(2k, 64).  Every case is checked in both operand layouts: the
+B-expanded one above and the A-expanded one (tcec_set_operand_layout, used
+when m < n): A'' row 2i = (Ar, -Ai), row 2i+1 = (Ai, Ar); B'' row j = (Br, Bi)
+= column j of B.  The oracle (the C restatement, pinned to the reference
+build) is the checker; the device planes come back through
+tcec_debug_prep_layout.  Uncorrected (TC ablation) preparation is pinned
+against quantize_buf(RN).
 """
 import numpy as np
 import pytest
@@ -28,7 +32,7 @@ def _to_fmt(v, fmt):
     return v.astype(np.float16) if fmt == 0 else v.astype(np.float32)
 
 
-def _expected(orc, a, b, kind, sa, sb, corrected):
+def _expected(orc, a, b, kind, sa, sb, corrected, xa=False):
     fmt = 1 if kind == 2 else 0
     m, k = a.shape
     n = b.shape[1]
@@ -51,12 +55,27 @@ def _expected(orc, a, b, kind, sa, sb, corrected):
         return hi, lo
 
     ah, al = prep(a.view(np.float32), sa)
+    bh, bl = prep(b.view(np.float32), sb)
+    if xa:
+        A_hi = np.zeros((2 * m, kp), np.float32)
+        A_lo = np.zeros((2 * m, kp), np.float32)
+        for src, dst in ((ah, A_hi), (al, A_lo)):
+            s = src.reshape(m, k, 2)
+            re, im = s[:, :, 0], s[:, :, 1]                     # m x k
+            dst[0::2, 0:2 * k:2] = re
+            dst[0::2, 1:2 * k:2] = -im
+            dst[1::2, 0:2 * k:2] = im
+            dst[1::2, 1:2 * k:2] = re
+        B_hi = np.zeros((n, kp), np.float32)
+        B_lo = np.zeros((n, kp), np.float32)
+        for src, dst in ((bh, B_hi), (bl, B_lo)):
+            dst[:, :2 * k] = src.reshape(k, n, 2).transpose(1, 0, 2).reshape(n, 2 * k)
+        return [_to_fmt(p, fmt) for p in (A_hi, A_lo, B_hi, B_lo)], ovf, bad
     A_hi = np.zeros((m, kp), np.float32)
     A_lo = np.zeros((m, kp), np.float32)
     A_hi[:, :2 * k] = ah.reshape(m, 2 * k)
     A_lo[:, :2 * k] = al.reshape(m, 2 * k)
 
-    bh, bl = prep(b.view(np.float32), sb)
     B_hi = np.zeros((2 * n, kp), np.float32)
     B_lo = np.zeros((2 * n, kp), np.float32)
     for src, dst in ((bh, B_hi), (bl, B_lo)):
@@ -80,22 +99,27 @@ def _same_bits(got, want):
 
 
 def _check(handle, orc, a, b, kind, sa=0, sb=0, corrected=True, check_bits=True):
+    for xa in (False, True):
+        _check_layout(handle, orc, a, b, kind, sa, sb, corrected, check_bits, xa)
+
+
+def _check_layout(handle, orc, a, b, kind, sa, sb, corrected, check_bits, xa):
     dev = torch.device("cuda:0")
     ad = torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     bd = torch.from_numpy(np.ascontiguousarray(b)).to(dev)
-    *planes, ovf, bad = handle.debug_prep(ad, bd, kind, sa, sb, corrected)
-    want, wovf, wbad = _expected(orc, a, b, KIND[kind], sa, sb, corrected)
-    assert bad == wbad, ("ScaleOverflow flag", bad, wbad)
+    *planes, ovf, bad = handle.debug_prep(ad, bd, kind, sa, sb, corrected, xa=xa)
+    want, wovf, wbad = _expected(orc, a, b, KIND[kind], sa, sb, corrected, xa)
+    assert bad == wbad, ("ScaleOverflow flag", bad, wbad, xa)
     if bad:
         return  # the reference throws ScaleOverflow before splitting (precsel.cpp:54-57)
-    assert ovf == wovf, ("overflow flag", ovf, wovf)
+    assert ovf == wovf, ("overflow flag", ovf, wovf, xa)
     names = ("A_hi", "A_lo", "B'_hi", "B'_lo") if corrected else ("A_hi", None, "B'_hi", None)
     for name, g, w in zip(names, planes, want):
         if name is None:
             continue
         g = g.cpu().numpy()
         if check_bits:
-            assert _same_bits(g, w), (name, kind, sa, sb, np.argwhere(
+            assert _same_bits(g, w), (name, "xa" if xa else "bx", kind, sa, sb, np.argwhere(
                 g.view(np.uint16 if g.dtype == np.float16 else np.uint32)
                 != w.view(np.uint16 if w.dtype == np.float16 else np.uint32))[:5])
 
