@@ -12,6 +12,7 @@ H2D/D2H); every computation runs in libtcec_b200.so.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -70,11 +71,17 @@ class Handle:
         h = C.c_void_p()
         check(self.lib.tcec_create(device, C.byref(h)))
         self.h = h
+        # networks bound to this handle: destroyed before the handle (a network
+        # still alive when the handle closes would otherwise free its device
+        # buffers through a dead handle)
+        self._networks = weakref.WeakSet()
         if stream is not None:
             self.set_stream(stream)
 
     def close(self):
         if getattr(self, "h", None):
+            for net in list(getattr(self, "_networks", ())):
+                net.close()
             self.lib.tcec_destroy(self.h)
             self.h = None
 

@@ -1143,75 +1143,148 @@ TCEC_DEV void skinny_mac(const float2* __restrict__ srow, float xr, float xi,
     }
 }
 
-// m <= MX: thread j owns column j of C
-template <bool F64, int MX, bool GROUPED>
-__global__ void __launch_bounds__(256) cgemm_skinny_col_kernel(const float2* __restrict__ a,
+// offset of index idx in a run map (runs outermost first, innermost last)
+TCEC_DEV int64_t run_offset(const RunMap& rm, uint32_t idx) {
+    int64_t off = 0;
+#pragma unroll
+    for (int r = kMaxRuns - 1; r >= 0; --r) {
+        if (r < rm.n) {
+            uint32_t dgt;
+            if (rm.pow2) {
+                dgt = idx & ((1u << rm.shift[r]) - 1u);
+                idx >>= rm.shift[r];
+            } else {
+                dgt = idx % rm.ext[r];
+                idx /= rm.ext[r];
+            }
+            off += int64_t(dgt) * rm.stride[r];
+        }
+    }
+    return off;
+}
+
+// m <= MX: thread j owns column j of C.  VIEW: B is read through a matrix
+// view of the unpermuted tensor (fused TTGT gather): B(kk, j) =
+// b[view.rows(kk) + view.cols(j)], the same elements in the same order.
+template <bool F64, int MX, bool GROUPED, bool VIEW = false>
+__global__ void __launch_bounds__(256, 2) cgemm_skinny_col_kernel(const float2* __restrict__ a,
                                                                const float2* __restrict__ b,
                                                                float2* __restrict__ c, int m,
-                                                               int64_t n, int k) {
+                                                               int64_t n, int k, const MatrixView view) {
     using acc_t = typename std::conditional<F64, double, float>::type;
     __shared__ __align__(16) float2 as[kSkinnyMaxK * MX];  // [kk][i]
+    __shared__ int64_t koff[VIEW ? kSkinnyMaxK : 1];
     for (int t = threadIdx.x; t < k * MX; t += blockDim.x) {
         const int kk = t / MX, i = t % MX;
         as[t] = i < m ? a[i * k + kk] : make_float2(0.0f, 0.0f);
     }
+    if (VIEW)
+        for (int t = threadIdx.x; t < k; t += blockDim.x) koff[t] = run_offset(view.rows, uint32_t(t));
     __syncthreads();
-    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (j >= n) return;
-    acc_t p[MX][4];
+    // persistent blocks walk 256-column chunks: the short operand is staged
+    // once per block, and with k a multiple of 8 the first load group of the
+    // next chunk is issued during the last MACs of the current one (ncu: the
+    // per-block prologue -- A from L2, barrier, first B loads -- left the
+    // schedulers without eligible warps, long-scoreboard 45% of the stalls)
+    auto col_ptr = [&](int64_t jj) {
+        return VIEW ? b + run_offset(view.cols, uint32_t(jj)) : b + jj;
+    };
+    auto bel = [&](const float2* bj, int kk) {
+        return VIEW ? __ldcs(bj + koff[kk]) : __ldcs(bj + int64_t(kk) * n);
+    };
+    const int64_t step = int64_t(gridDim.x) * blockDim.x;
+    int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool grouped = GROUPED && k >= 8;
+    const bool chain_next = grouped && (k % 8) == 0;
+    float2 bcol[8], bnxt[8];
+    const float2* bj = col_ptr(j < n ? j : 0);
+    if (grouped && j < n) {
 #pragma unroll
-    for (int i = 0; i < MX; ++i) p[i][0] = p[i][1] = p[i][2] = p[i][3] = acc_t(0);
-    int k0 = 0;
-    if (GROUPED) {  // A/B on B200: the plain loop wins for k <= 4, grouped loads from 8 up
-        // 8 loads in flight per thread instead of one memory latency per k
+        for (int u = 0; u < 8; ++u) bcol[u] = bel(bj, u);
+    }
 #pragma unroll 1
-        for (; k0 + 8 <= k; k0 += 8) {
-            float2 bcol[8];
+    for (; j - threadIdx.x < n; j += step) {
+        const bool live = j < n;
+        const int64_t jn = j + step;
+        const float2* bjn = col_ptr(jn < n ? jn : 0);
+        acc_t p[MX][4];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) bcol[u] = __ldcs(b + int64_t(k0 + u) * n + j);
+        for (int i = 0; i < MX; ++i) p[i][0] = p[i][1] = p[i][2] = p[i][3] = acc_t(0);
+        int k0 = 0;
+        if (grouped) {  // A/B on B200: the plain loop wins for k <= 4, grouped loads from 8 up
+#pragma unroll 1
+            for (; k0 + 8 <= k; k0 += 8) {
+                const bool more = k0 + 16 <= k;
+                if (more && live) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u) skinny_mac<F64, MX>(as + (k0 + u) * MX, bcol[u].x, bcol[u].y, p, true);
+                    for (int u = 0; u < 8; ++u) bnxt[u] = bel(bj, k0 + 8 + u);
+                } else if (!more && chain_next && jn < n) {
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) bnxt[u] = bel(bjn, u);
+                }
+                if (live) {
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        skinny_mac<F64, MX>(as + (k0 + u) * MX, bcol[u].x, bcol[u].y, p, true);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) bcol[u] = bnxt[u];
+            }
         }
-    }
+        if (live) {
 #pragma unroll 1
-    for (; k0 < k; ++k0) {
-        const float2 bv = __ldcs(b + int64_t(k0) * n + j);
-        skinny_mac<F64, MX>(as + k0 * MX, bv.x, bv.y, p, true);
-    }
+            for (; k0 < k; ++k0) {
+                const float2 bv = bel(bj, k0);
+                skinny_mac<F64, MX>(as + k0 * MX, bv.x, bv.y, p, true);
+            }
 #pragma unroll
-    for (int i = 0; i < MX; ++i)
-        if (i < m) __stcs(c + int64_t(i) * n + j, assemble<F64>(p[i]));
+            for (int i = 0; i < MX; ++i)
+                if (i < m) __stcs(c + int64_t(i) * n + j, assemble<F64>(p[i]));
+        }
+        if (grouped && !chain_next && jn < n) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) bcol[u] = bel(bjn, u);
+        }
+        bj = bjn;
+    }
 }
 
 // n <= MX: thread i owns row i of C.  GROUPED (k >= 8, MX <= 8): each warp
 // stages its 32 rows of A through shared memory eight k at a time and writes
 // its 32 x n block of C back the same way, so global loads and stores are
 // row-contiguous runs instead of one lane-strided 8-B access per element.
-template <bool F64, int MX, bool GROUPED>
+// VIEW: A is read through a matrix view of the unpermuted tensor, A(i, kk) =
+// a[view.rows(i) + view.cols(kk)].
+template <bool F64, int MX, bool GROUPED, bool VIEW = false>
 __global__ void __launch_bounds__(256) cgemm_skinny_row_kernel(const float2* __restrict__ a,
                                                                const float2* __restrict__ b,
                                                                float2* __restrict__ c, int64_t m,
-                                                               int n, int k, int64_t ldn) {
+                                                               int n, int k, int64_t ldn,
+                                                               const MatrixView view) {
     // columns [0, n) of a block of B / C whose row stride is ldn
     using acc_t = typename std::conditional<F64, double, float>::type;
     constexpr int SW = (MX + 1) > 9 ? (MX + 1) : 9;  // staging row stride (odd: conflict-free)
     __shared__ __align__(16) float2 bs[kSkinnyMaxK * MX];  // [kk][j]
+    __shared__ int64_t koff[VIEW ? kSkinnyMaxK : 1];
     extern __shared__ float2 stage[];  // GROUPED: 8 warps x 32 rows x SW (dynamic, > 48 KB with B at MX = 16)
     for (int t = threadIdx.x; t < k * MX; t += blockDim.x) {
         const int kk = t / MX, jj = t % MX;
         bs[t] = jj < n ? b[int64_t(kk) * ldn + jj] : make_float2(0.0f, 0.0f);
     }
+    if (VIEW)
+        for (int t = threadIdx.x; t < k; t += blockDim.x) koff[t] = run_offset(view.cols, uint32_t(t));
     __syncthreads();
+    auto koffs = [&](int kk) -> int64_t { return VIEW ? koff[kk] : int64_t(kk); };
     acc_t p[MX][4];
 #pragma unroll
     for (int j = 0; j < MX; ++j) p[j][0] = p[j][1] = p[j][2] = p[j][3] = acc_t(0);
     if (!GROUPED) {
         const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
         if (i >= m) return;
-        const float2* arow = a + i * k;
+        const float2* arow = VIEW ? a + run_offset(view.rows, uint32_t(i)) : a + i * k;
 #pragma unroll 1
         for (int k0 = 0; k0 < k; ++k0) {
-            const float2 av = __ldcs(arow + k0);
+            const float2 av = __ldcs(arow + koffs(k0));
             skinny_mac<F64, MX>(bs + k0 * MX, av.x, av.y, p, false);
         }
         float2* crow = c + i * ldn;
@@ -1226,6 +1299,8 @@ __global__ void __launch_bounds__(256) cgemm_skinny_row_kernel(const float2* __r
     const int rows = int(min(int64_t(32), m - w0));
     float2* st = stage + (threadIdx.x >> 5) * 32 * SW;
     const float2* ablk = a + w0 * k;
+    // VIEW: row offsets of the warp's 32 rows, one per lane (shuffled to the loaders)
+    const int64_t my_roff = VIEW && lane < rows ? run_offset(view.rows, uint32_t(w0 + lane)) : 0;
     int k0 = 0;
 #pragma unroll 1
     for (; k0 + 8 <= k; k0 += 8) {
@@ -1233,7 +1308,12 @@ __global__ void __launch_bounds__(256) cgemm_skinny_row_kernel(const float2* __r
 #pragma unroll
         for (int u = 0; u < 8; ++u) {  // element e = lane + 32u of the 32 x 8 slab: row e / 8, column e % 8
             const int r = (lane >> 3) + 4 * u;
-            v[u] = r < rows ? __ldcs(ablk + int64_t(r) * k + k0 + (lane & 7)) : make_float2(0.0f, 0.0f);
+            if (VIEW) {
+                const int64_t ro = __shfl_sync(0xFFFFFFFFu, my_roff, r);
+                v[u] = r < rows ? __ldcs(a + ro + koff[k0 + (lane & 7)]) : make_float2(0.0f, 0.0f);
+            } else {
+                v[u] = r < rows ? __ldcs(ablk + int64_t(r) * k + k0 + (lane & 7)) : make_float2(0.0f, 0.0f);
+            }
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) st[((lane >> 3) + 4 * u) * SW + (lane & 7)] = v[u];
@@ -1247,7 +1327,8 @@ __global__ void __launch_bounds__(256) cgemm_skinny_row_kernel(const float2* __r
     }
 #pragma unroll 1
     for (; k0 < k; ++k0) {
-        const float2 av = lane < rows ? __ldcs(ablk + int64_t(lane) * k + k0) : make_float2(0.0f, 0.0f);
+        const float2 av = lane < rows ? __ldcs(VIEW ? a + my_roff + koff[k0] : ablk + int64_t(lane) * k + k0)
+                                      : make_float2(0.0f, 0.0f);
         skinny_mac<F64, MX>(bs + k0 * MX, av.x, av.y, p, false);
     }
 #pragma unroll
@@ -1268,9 +1349,27 @@ __global__ void __launch_bounds__(256) cgemm_skinny_row_kernel(const float2* __r
     }
 }
 
-template <bool F64, int MX>
+// persistent grid of the column kernels: the co-resident blocks (queried once
+// per kernel), never more than the 256-column chunks
+template <bool F64, int MX, bool GROUPED, bool VIEW>
+unsigned col_grid(int64_t n) {
+    static const int per_sm = [] {
+        int nb = 0;
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                   &nb, cgemm_skinny_col_kernel<F64, MX, GROUPED, VIEW>, 256, 0) == cudaSuccess && nb > 0
+                   ? nb
+                   : 2;
+    }();
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t chunks = (n + 255) / 256;
+    return unsigned(std::max<int64_t>(1, std::min<int64_t>(chunks, int64_t(per_sm) * sms)));
+}
+
+template <bool F64, int MX, bool VIEW = false>
 void launch_skinny_mx(const float2* a, const float2* b, float2* c, int64_t m, int64_t n, int64_t k,
-                      cudaStream_t s) {
+                      cudaStream_t s, const MatrixView& view = MatrixView{}) {
     // more than 16 short-side rows/columns: passes of <= MX (each re-reads the
     // long operand; register-resident 32-wide tiles measured slower)
     if (m <= n) {
@@ -1279,11 +1378,13 @@ void launch_skinny_mx(const float2* a, const float2* b, float2* c, int64_t m, in
             // separate instantiations: the grouped loop's registers must not
             // lower the occupancy of the short-k kernel
             if (k >= 8)
-                cgemm_skinny_col_kernel<F64, MX, true><<<unsigned((n + 255) / 256), 256, 0, s>>>(
-                    a + r0 * k, b, c + r0 * n, rows, n, int(k));
+                cgemm_skinny_col_kernel<F64, MX, true, VIEW>
+                    <<<col_grid<F64, MX, true, VIEW>(n), 256, 0, s>>>(
+                        a + r0 * k, b, c + r0 * n, rows, n, int(k), view);
             else
-                cgemm_skinny_col_kernel<F64, MX, false><<<unsigned((n + 255) / 256), 256, 0, s>>>(
-                    a + r0 * k, b, c + r0 * n, rows, n, int(k));
+                cgemm_skinny_col_kernel<F64, MX, false, VIEW>
+                    <<<col_grid<F64, MX, false, VIEW>(n), 256, 0, s>>>(
+                        a + r0 * k, b, c + r0 * n, rows, n, int(k), view);
         }
     } else {
         for (int64_t j0 = 0; j0 < n; j0 += MX) {
@@ -1293,29 +1394,38 @@ void launch_skinny_mx(const float2* a, const float2* b, float2* c, int64_t m, in
                 constexpr int stage_bytes = 8 * 32 * SW * int(sizeof(float2));
                 static std::atomic<uint64_t> attr{0};
                 if (ensure_smem_attr(attr, [] {
-                        return cudaFuncSetAttribute(cgemm_skinny_row_kernel<F64, MX, true>,
+                        return cudaFuncSetAttribute(cgemm_skinny_row_kernel<F64, MX, true, VIEW>,
                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes);
                     }) == cudaSuccess) {
-                    cgemm_skinny_row_kernel<F64, MX, true><<<unsigned((m + 255) / 256), 256, stage_bytes, s>>>(
-                        a, b + j0, c + j0, m, cols, int(k), n);
+                    cgemm_skinny_row_kernel<F64, MX, true, VIEW><<<unsigned((m + 255) / 256), 256, stage_bytes, s>>>(
+                        a, b + j0, c + j0, m, cols, int(k), n, view);
                     continue;
                 }
             }
-            cgemm_skinny_row_kernel<F64, MX, false><<<unsigned((m + 255) / 256), 256, 0, s>>>(
-                a, b + j0, c + j0, m, cols, int(k), n);
+            cgemm_skinny_row_kernel<F64, MX, false, VIEW><<<unsigned((m + 255) / 256), 256, 0, s>>>(
+                a, b + j0, c + j0, m, cols, int(k), n, view);
         }
     }
 }
+
+}  // namespace
+
+bool skinny_shape(int64_t m, int64_t n, int64_t k) {
+    const int64_t small = m < n ? m : n, large = m < n ? n : m;
+    return !(k > kSkinnyMaxK || small > 32 || large < 4096);
+}
+
+namespace {
 
 // true when the skinny kernels take the shape
 template <bool F64>
 bool launch_skinny(const float2* a, const float2* b, float2* c, int64_t m, int64_t n, int64_t k,
                    cudaStream_t s) {
-    const int64_t small = m < n ? m : n, large = m < n ? n : m;
+    const int64_t small = m < n ? m : n;
     // up to 32 rows in register tiles of <= 16 (two passes above 16), k <= 128 in shared memory:
     // the 64 x 64 tiled kernel would waste >= half of every tile on these
     // (the (16, 2^22, 64) and (32, 2^23, 8) steps of Sycamore slices)
-    if (k > kSkinnyMaxK || small > 32 || large < 4096) return false;
+    if (!skinny_shape(m, n, k)) return false;
     if (small <= 2) launch_skinny_mx<F64, 2>(a, b, c, m, n, k, s);
     else if (small <= 4) launch_skinny_mx<F64, 4>(a, b, c, m, n, k, s);
     else if (small <= 8) launch_skinny_mx<F64, 8>(a, b, c, m, n, k, s);
@@ -1910,6 +2020,60 @@ void launch_permute(const float2* src, float2* dst, int rank, const int64_t* old
         }
     }
     permute_kernel<<<grid_for(total, kThreads, 148 * 32), kThreads, 0, s>>>(src, dst, desc);
+}
+
+bool launch_skinny_view(const float2* a, const float2* b, float2* c, int64_t m, int64_t n, int64_t k,
+                        const MatrixView& v, cudaStream_t s) {
+    if (!skinny_shape(m, n, k) || m <= 0 || n <= 0 || k <= 0) return false;
+    // the view indexes fit 32 bits (run_offset): rows/cols < 2^32
+    if (m > int64_t(0xFFFFFFFF) || n > int64_t(0xFFFFFFFF)) return false;
+    const int64_t small = m < n ? m : n;
+    if (small <= 2) launch_skinny_mx<false, 2, true>(a, b, c, m, n, k, s, v);
+    else if (small <= 4) launch_skinny_mx<false, 4, true>(a, b, c, m, n, k, s, v);
+    else if (small <= 8) launch_skinny_mx<false, 8, true>(a, b, c, m, n, k, s, v);
+    else launch_skinny_mx<false, 16, true>(a, b, c, m, n, k, s, v);
+    return true;
+}
+
+// runs of new axes [a0, a1): adjacent new axes merge when they are adjacent
+// (and in order) in the tensor's physical layout
+static bool make_runs(int a0, int a1, const int64_t* dims, const int64_t* pstride, const int* axis_of,
+                      RunMap* rm) {
+    RunMap r;
+    for (int a = a0; a < a1; ++a) {
+        const int o = axis_of[a];
+        const int64_t e = dims[o], st = pstride[o];
+        if (e == 1) continue;
+        if (r.n > 0 && r.stride[r.n - 1] == st * e && uint64_t(r.ext[r.n - 1]) * uint64_t(e) <= 0xFFFFFFFFull) {
+            r.ext[r.n - 1] = uint32_t(uint64_t(r.ext[r.n - 1]) * uint64_t(e));
+            r.stride[r.n - 1] = st;
+            continue;
+        }
+        if (r.n == kMaxRuns || e > int64_t(0xFFFFFFFF)) return false;
+        r.ext[r.n] = uint32_t(e);
+        r.stride[r.n] = st;
+        ++r.n;
+    }
+    r.pow2 = 1;
+    for (int i = 0; i < r.n; ++i) {
+        if (r.ext[i] & (r.ext[i] - 1)) r.pow2 = 0;
+        int sh = 0;
+        while ((1ull << sh) < r.ext[i]) ++sh;
+        r.shift[i] = uint32_t(sh);
+    }
+    *rm = r;
+    return true;
+}
+
+bool make_matrix_view(int rank, const int64_t* dims, const int* axis_of, int n_row_axes, MatrixView* v) {
+    int64_t pstride[kMaxRank];
+    int64_t acc = 1;
+    for (int i = rank - 1; i >= 0; --i) {
+        pstride[i] = acc;
+        acc *= dims[i];
+    }
+    return make_runs(0, n_row_axes, dims, pstride, axis_of, &v->rows) &&
+           make_runs(n_row_axes, rank, dims, pstride, axis_of, &v->cols);
 }
 
 }  // namespace tcec

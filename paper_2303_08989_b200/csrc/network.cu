@@ -137,6 +137,15 @@ static int validate(const tcec_network_s& net) {
     return TCEC_OK;
 }
 
+// TCEC_VIEW_GATHER = 0 disables the fused TTGT gather of skinny steps (A/B)
+static bool view_gather_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("TCEC_VIEW_GATHER");
+        return !e || std::atoi(e) != 0;
+    }();
+    return on;
+}
+
 // fold_path + ttgt_contract bookkeeping (network.cpp:33-85, :149-168)
 static int build_plan(const tcec_network_s& net, const int* steps, int n_steps,
                       const tcec_dispatch_config_t& cfg, FoldPlan* out) {
@@ -204,7 +213,18 @@ static int build_plan(const tcec_network_s& net, const int* steps, int n_steps,
         sp.b_dims = B.dims;
         sp.a_size = A.size();
         sp.b_size = B.size();
+        sp.n_shared = int(shared.size());
         sp.dp = plan_dispatch(sp.m, sp.n, sp.k, cfg);
+        // skinny FP32-tier step: read the long operand in place (the view
+        // addresses the same elements in the same order -> identical bits)
+        if (sp.dp.tier == kTierFp32 && skinny_shape(sp.m, sp.n, sp.k) && view_gather_enabled()) {
+            if (sp.m <= sp.n && sp.perm_b)
+                sp.view_b = make_matrix_view(int(B.dims.size()), B.dims.data(), sp.b_axis.data(), sp.n_shared,
+                                             &sp.view);
+            else if (sp.m > sp.n && sp.perm_a)
+                sp.view_a = make_matrix_view(int(A.dims.size()), A.dims.data(), sp.a_axis.data(),
+                                             int(A.dims.size()) - sp.n_shared, &sp.view);
+        }
         if (sp.dp.tier == kTierTc && cfg.k_tile < 1)
             return set_error(TCEC_ERR_INVALID_ARGUMENT, "k_tile must be >= 1");
         plan.ws_bytes = std::max(plan.ws_bytes, plan_workspace(sp.dp, sp.m, sp.n));
@@ -275,12 +295,13 @@ static int enqueue_fold(tcec_network_s& net, const FoldPlan& plan, const tcec_di
         float2* pa = pa_src;
         float2* pb = pb_src;
         cudaError_t e;
-        if (sp.perm_a) {
+        const bool perm_a = sp.perm_a && !sp.view_a, perm_b = sp.perm_b && !sp.view_b;
+        if (perm_a) {
             e = cudaMallocAsync(reinterpret_cast<void**>(&pa), size_t(sp.a_size) * 8, s);
             if (e != cudaSuccess) return cuda_error(e, "permute buffer");
             launch_permute(pa_src, pa, int(sp.a_dims.size()), sp.a_dims.data(), sp.a_axis.data(), s);
         }
-        if (sp.perm_b) {
+        if (perm_b) {
             e = cudaMallocAsync(reinterpret_cast<void**>(&pb), size_t(sp.b_size) * 8, s);
             if (e != cudaSuccess) return cuda_error(e, "permute buffer");
             launch_permute(pb_src, pb, int(sp.b_dims.size()), sp.b_dims.data(), sp.b_axis.data(), s);
@@ -288,13 +309,21 @@ static int enqueue_fold(tcec_network_s& net, const FoldPlan& plan, const tcec_di
         float2* pc = nullptr;
         e = cudaMallocAsync(reinterpret_cast<void**>(&pc), size_t(std::max<int64_t>(sp.m * sp.n, 1)) * 8, s);
         if (e != cudaSuccess) return cuda_error(e, "step output");
-        const int rc = launch_dispatch(h, reinterpret_cast<const float*>(pa),
-                                       reinterpret_cast<const float*>(pb),
-                                       reinterpret_cast<float*>(pc), sp.m, sp.n, sp.k, cfg, sp.dp,
-                                       dec + si, ws);
-        if (rc) return rc;
-        if (sp.perm_a) cudaFreeAsync(pa, s);
-        if (sp.perm_b) cudaFreeAsync(pb, s);
+        if (sp.view_a || sp.view_b) {
+            // fused TTGT gather (FP32 tier: no decision slot, nothing else to launch)
+            if (!launch_skinny_view(pa, pb, pc, sp.m, sp.n, sp.k, sp.view, s))
+                return set_error(TCEC_ERR_LOGIC, "skinny view step: shape not skinny");
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return cuda_error(e, "skinny view step");
+        } else {
+            const int rc = launch_dispatch(h, reinterpret_cast<const float*>(pa),
+                                           reinterpret_cast<const float*>(pb),
+                                           reinterpret_cast<float*>(pc), sp.m, sp.n, sp.k, cfg, sp.dp,
+                                           dec + si, ws);
+            if (rc) return rc;
+        }
+        if (perm_a) cudaFreeAsync(pa, s);
+        if (perm_b) cudaFreeAsync(pb, s);
         if (own_a) cudaFreeAsync(pa_src, s);
         if (own_b) cudaFreeAsync(pb_src, s);
         live.erase(sp.ia);

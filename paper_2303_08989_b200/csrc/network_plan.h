@@ -27,7 +27,12 @@ struct StepPlan {
     std::vector<int64_t> a_dims, b_dims;
     std::vector<int> a_axis, b_axis;  // new axis -> old axis (free_a|shared, shared|free_b)
     int64_t a_size = 1, b_size = 1;
+    int n_shared = 0;
     DispatchPlan dp;
+    // fused TTGT gather: a skinny FP32-tier step reads its long operand through
+    // a strided view of the unpermuted tensor instead of a permuted copy
+    bool view_a = false, view_b = false;
+    MatrixView view;
 };
 
 struct FoldPlan {

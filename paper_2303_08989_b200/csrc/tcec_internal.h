@@ -76,6 +76,34 @@ void launch_prep_bx(const float* b, int64_t k, int64_t n, int64_t kp, void* hi, 
 // fused TTGT gathers: element (i, kk) of A is at a[ (row_off(i) + col_off(kk)) ]
 void launch_cgemm_fp32_ref(const float2* a, const float2* b, float2* c, int64_t m, int64_t n,
                            int64_t k, cudaStream_t s);
+// Matrix view of a permuted tensor (fused TTGT gather): element (r, c) of the
+// rows x cols matrix is at base + rows.offset(r) + cols.offset(c), each offset
+// a mixed-radix sum over runs of merged tensor axes (innermost run last).
+constexpr int kMaxRuns = 8;
+struct RunMap {
+    int n = 0;                      // runs
+    int pow2 = 1;                   // every extent a power of two (shift / mask decomposition)
+    uint32_t ext[kMaxRuns] = {};    // run extents
+    uint32_t shift[kMaxRuns] = {};  // log2(ext) when pow2
+    int64_t stride[kMaxRuns] = {};  // element stride of each run
+};
+struct MatrixView {
+    RunMap rows, cols;
+};
+// Build the view of operand `role` (0 = A: rows = free_a, cols = shared;
+// 1 = B: rows = shared, cols = free_b) of a tensor with physical extents
+// dims[0..rank) permuted by axis_of (new axis a = old axis axis_of[a]) whose
+// first n_row_axes new axes are the matrix rows.  false when it needs more
+// than kMaxRuns runs per side.
+bool make_matrix_view(int rank, const int64_t* dims, const int* axis_of, int n_row_axes, MatrixView* v);
+// FP32_REF complex GEMM of a skinny shape (k <= 128, min(m, n) <= 32,
+// max(m, n) >= 4096) whose LONG operand is read through a view instead of a
+// materialised permute (B when m <= n, else A); the short operand is a plain
+// row-major matrix.  Bit-identical to launch_cgemm_fp32_ref on the permuted
+// operand.  false when the shape is not skinny.
+bool launch_skinny_view(const float2* a, const float2* b, float2* c, int64_t m, int64_t n, int64_t k,
+                        const MatrixView& long_view, cudaStream_t s);
+bool skinny_shape(int64_t m, int64_t n, int64_t k);
 // FP64_ORACLE mode (gemm.cpp:68-74, :111-117)
 void launch_cgemm_fp64(const float2* a, const float2* b, float2* c, int64_t m, int64_t n,
                        int64_t k, cudaStream_t s);

@@ -57,6 +57,8 @@ class Network:
         check(self.lib.tcec_network_create(handle.h if handle is not None else None, n, r, lab,
                                            dm, C.byref(net)))
         self.net = net
+        if handle is not None:
+            handle._networks.add(self)
         self._steps_cache = None
         for i, d in enumerate(spec.data):
             self.set_node(i, d)

@@ -342,3 +342,66 @@ def test_device_statevector_is_the_reference_oracle(handle, golden):
             assert (z.real, z.imag) == tuple(row["sv_oracle"]), (case["rows"], case["cols"], row["x"])
             checked += 1
     assert checked >= 40
+
+
+def _skinny_chain(seed, t_dims, gates):
+    """A big tensor T contracted with a chain of small tensors on scattered
+    axes -- the skinny FP32-tier steps of sliced RCS contractions.  gates:
+    (number of T axes contracted, new axis extents, T first?)."""
+    g = np.random.default_rng(seed)
+    labels = [[f"t{i}" for i in range(len(t_dims))]]
+    dims = [list(t_dims)]
+    cur = list(zip(labels[0], t_dims))
+    path, nxt = [], 1 + len(gates)
+    prev = 0
+    for gi, (nk, new_dims, t_first) in enumerate(gates):
+        pick = sorted(g.choice(len(cur), size=nk, replace=False), key=lambda _: g.random())
+        shared = [cur[i] for i in pick]
+        new = [(f"n{gi}_{j}", d) for j, d in enumerate(new_dims)]
+        gl = [l for l, _ in shared] + [l for l, _ in new]
+        gd = [d for _, d in shared] + [d for _, d in new]
+        order = g.permutation(len(gl))
+        labels.append([gl[i] for i in order])
+        dims.append([gd[i] for i in order])
+        path.append((prev, gi + 1) if t_first else (gi + 1, prev))
+        keep = [c for c in cur if c not in shared]
+        cur = keep + new if t_first else new + keep
+        prev = nxt
+        nxt += 1
+    data = [matrix_recipe("uniform", 1, int(np.prod(d)), seed + 7 * i).reshape(-1) for i, d in enumerate(dims)]
+    return NetworkSpec(labels=labels, dims=dims, data=data), path
+
+
+@pytest.mark.parametrize("case", [
+    ([2] * 16, [(2, [2, 2], False), (3, [2, 2, 2], False), (4, [2] * 4, True), (1, [2], True)]),
+    ([2] * 18, [(4, [2] * 5, False), (3, [2] * 3, True), (2, [2] * 4, False)]),     # m = 32: two passes
+    ([3, 2, 4, 2, 2, 5, 2, 2, 2, 2, 2, 3, 2, 2], [(2, [3, 2], False), (2, [5], True), (2, [2, 2], False)]),
+    ([2] * 21, [(7, [2] * 3, False), (5, [2] * 2, True)]),                       # k = 128 / 32
+])
+@pytest.mark.parametrize("executor", [0, 1, 3], ids=["auto", "per-step", "hybrid"])
+def test_skinny_view_gather_bit_exact(handle, case, executor):
+    """Skinny FP32-tier steps read their long operand through a strided view of
+    the unpermuted tensor (fused TTGT gather; col kernel when the long operand
+    is B, row kernel when it is A; power-of-two and mixed extents): the fold
+    equals the oracle's permute-then-GEMM fold bit for bit, decision lines
+    included."""
+    t_dims, gates = case
+    spec, path = _skinny_chain(5 + len(t_dims), t_dims, gates)
+    _, _, _, lines0 = oracle_fold(spec, path, O.make_config(force="FP32_REF"))
+    for ln in lines0:  # every step takes the skinny kernels
+        m, n, k = (int(v) for v in ln.split(",")[:3])
+        assert k <= 128 and min(m, n) <= 32 and max(m, n) >= 4096, ln
+    handle.set_executor(executor)
+    net = Network(handle, spec)
+    try:
+        got, lines = net.contract(path, BASELINE, want_log=True)
+        labels, _, want, want_lines = oracle_fold(spec, path, O.make_config(force="FP32_REF"))
+        assert got.labels == labels
+        assert np.array_equal(bits(got.data.view(np.float32)), bits(want.view(np.float32)))
+        assert lines == want_lines
+        got2, _ = net.contract(path, make_config(), want_log=True)
+        _, _, want2, _ = oracle_fold(spec, path, O.make_config())
+        assert np.array_equal(bits(got2.data.view(np.float32)), bits(want2.view(np.float32)))
+    finally:
+        net.close()
+        handle.set_executor(0)
