@@ -177,7 +177,7 @@ TcecGemmArgs tc_gemm_args(const Handle& h, const DispatchPlan& p, void* ws, floa
         return e ? std::max(0, std::min(64, std::atoi(e))) : 0;
     }();
     g.flush_kblocks = p.corrected ? (h.flush_kblocks | (h.flush_kblocks > 0 ? tf32_flush << 16 : 0)) : 0;
-    g.pair = resolve_gemm_variant(h.gemm_pair, rows_a, rows_b, p.kp, h.sm_count);
+    g.pair = resolve_gemm_variant(h.gemm_pair, rows_a, rows_b, p.kp, h.sm_count, !xa);  // no A-expanded pair kernel
     g.sms = h.sm_count;
     g.fmt = (p.kind < 0 && !p.forced_scaled) ? -1  // format chosen by the device decision
                                              : (p.kind == kKindTf32 ? kTf32 : kFp16);

@@ -1425,9 +1425,13 @@ int launch_wide_auto(const TcecGemmArgs& g, cudaStream_t s) {
 
 }  // namespace
 
-int resolve_gemm_variant(int requested, int64_t m, int64_t n2, int64_t kp, int sm_count) {
+int resolve_gemm_variant(int requested, int64_t m, int64_t n2, int64_t kp, int sm_count, bool allow_pair) {
     if (requested != kVariantAuto) return requested;
     const int64_t wide_ctas = 2 * ((m + 2 * BM - 1) / (2 * BM)) * ((n2 + kWideBN - 1) / kWideBN);
+    // too few 256 x 256 tiles and a K too short to split: the 256 x 128 pair
+    // tiles double the CTAs at ~0.9 of the wide tile's MMA efficiency --
+    // 1024^3 TF32TCEC 58 (single) -> 42 us, 768^3 46 -> 34 us
+    if (allow_pair && wide_ctas < sm_count && kp / 64 < 64) return kVariantPair;
     // the 256 x 256 tiles fill the SMs, or K is long enough for split-K to fill
     // them; with <= 8 k-blocks per tile the persistent pairs win (the next
     // tile's loads and first MMAs overlap the epilogue: 2048x16384x64 TF32
@@ -1476,6 +1480,12 @@ int launch_tcec_gemm(const TcecGemmArgs& g_in, cudaStream_t s) {
                 g.partial = nullptr;
             }
         };
+        // minimum f16 k-blocks (64 K' elements each) per split; TCEC_SPLIT_MINKB overrides
+        static const int min_kb = [] {
+            const char* e = std::getenv("TCEC_SPLIT_MINKB");
+            const int v = e ? std::atoi(e) : 0;
+            return v > 0 ? v : 32;
+        }();
         if (tiles < sms && nkb >= 16) {
             static const int waves = [] {
                 const char* e = std::getenv("TCEC_SPLIT_WAVES");  // tuning override
@@ -1484,16 +1494,16 @@ int launch_tcec_gemm(const TcecGemmArgs& g_in, cudaStream_t s) {
             }();
             // every split keeps >= 32 f16 k-blocks (2048 K' elements) so the
             // partial round trip stays small against its MMA time
-            int64_t want = std::min<int64_t>((waves * sms + tiles - 1) / tiles, (g.kp / 64) / 32);
+            int64_t want = std::min<int64_t>((waves * sms + tiles - 1) / tiles, (g.kp / 64) / min_kb);
             split_with(want);
-        } else if (tiles < 8 * sms && g.pair != kVariantSingle && (g.kp / 64) / 32 >= 2) {
+        } else if (tiles < 8 * sms && g.pair != kVariantSingle && (g.kp / 64) / min_kb >= 2) {
             // a few waves of long tiles: split K just enough that the last wave
             // is nearly full (e.g. 512 CTAs = 3.46 waves -> 2 splits = 6.92
             // waves: (4096, 2048, 65536) TF32 steps of the Sycamore slices)
             const double w1 = double(tiles) / sms;
             int best = 1;
             double best_eff = w1 / std::ceil(w1);
-            for (int sp = 2; sp <= 4 && sp <= (g.kp / 64) / 32; ++sp) {
+            for (int sp = 2; sp <= 4 && sp <= (g.kp / 64) / min_kb; ++sp) {
                 const double w = w1 * sp;
                 const double eff = w / std::ceil(w);
                 if (best_eff < 0.95 && eff > best_eff + 0.02) {

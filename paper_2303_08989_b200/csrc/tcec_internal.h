@@ -146,7 +146,8 @@ struct TcecGemmArgs {
 // 256 x 256 pair tiles fill the SMs, else single
 enum GemmVariant : int { kVariantAuto = 0, kVariantPair = 1, kVariantSingle = 2, kVariantWide = 3, kVariantWidePersistent = 4,
                          kVariantWideMc = 5 };
-int resolve_gemm_variant(int requested, int64_t m, int64_t n2, int64_t kp, int sm_count);
+int resolve_gemm_variant(int requested, int64_t m, int64_t n2, int64_t kp, int sm_count,
+                         bool allow_pair = true);
 // returns a cudaError_t
 int launch_tcec_gemm(const TcecGemmArgs& args, cudaStream_t s);
 
