@@ -181,21 +181,6 @@ __global__ void __launch_bounds__(kThreads) stats1_kernel(const float* a, int64_
     stats1_part(a, na, b, nb, d, nb_a, int(blockIdx.x), int(gridDim.x));
 }
 
-// statistics written by other blocks of the same grid (fused preamble): read
-// past the L1
-TCEC_DEV DevStats load_stats(const DevStats* p) {
-    const volatile DevStats* v = p;
-    DevStats st;
-    st.n_nonzero = v->n_nonzero;
-    st.n1 = v->n1;
-    st.n2 = v->n2;
-    st.n_total = v->n_total;
-    st.max_bits = v->max_bits;
-    st.stage2_evaluated = v->stage2_evaluated;
-    st.e_max = v->e_max;
-    st.e_max_valid = v->e_max_valid;
-    return st;
-}
 
 // stage1_passes (precsel.cpp:47-52); r1 in double exactly as precsel.hpp:27-30
 TCEC_DEV bool stage1_passes(unsigned long long nz, unsigned long long n1, unsigned max_bits,
@@ -215,12 +200,23 @@ TCEC_DEV void stats2_part(const float* a, int64_t na, const float* b, int64_t nb
     const int part = op ? bid - nb_a : bid;
     const int nparts = op ? nblk - nb_a : nb_a;
     if (x == nullptr || n == 0 || nparts <= 0) return;
-    const DevStats st = load_stats(&d->st[op]);
-    if (!always && stage1_passes(st.n_nonzero, st.n1, st.max_bits, t, target)) return;
-    if (st.max_bits == 0) return;  // no e_max: n2 = 0
-    const int w = exponent_of_bits(st.max_bits) - (target + 14);
-    // ldexp(1.0f, w): a normal, a subnormal power of two, or 0 (all nonzero pass)
-    const uint32_t thr = w >= -126 ? uint32_t(w + 127) << 23 : (w >= -149 ? 1u << (w + 149) : 1u);
+    // one thread reads the stage-1 statistics and derives the threshold
+    // (every thread reading them put ~2.4 M same-address loads per 66 MB
+    // sweep in front of the data stream: 2x the stage-1 time at 2^24 elements)
+    __shared__ uint32_t thr_s;
+    if (threadIdx.x == 0) {
+        const DevStats st = d->st[op];
+        uint32_t th = 0;  // 0: this operand needs no stage 2 (stage 1 passed, or no e_max: n2 = 0)
+        if ((always || !stage1_passes(st.n_nonzero, st.n1, st.max_bits, t, target)) && st.max_bits != 0) {
+            const int w = exponent_of_bits(st.max_bits) - (target + 14);
+            // ldexp(1.0f, w): a normal, a subnormal power of two, or 0 (all nonzero pass)
+            th = w >= -126 ? uint32_t(w + 127) << 23 : (w >= -149 ? 1u << (w + 149) : 1u);
+        }
+        thr_s = th;
+    }
+    __syncthreads();
+    const uint32_t thr = thr_s;
+    if (thr == 0) return;
     unsigned cnt = 0;
     sweep_operand(x, n, part, nparts, [&](float v) {
         const uint32_t m = __float_as_uint(v) & 0x7FFFFFFFu;
