@@ -80,6 +80,18 @@ def tf32_peak():
     return 1100.0, "B200_PROFILING.md fallback: 1.1 PFLOP/s dense TF32" + cub
 
 
+def frac_at_clock(achieved_tflops, tf32, clk):
+    """achieved / the dense tensor rate at the median SM clock of the run (TF32
+    4096, FP16/BF16 8192 flop/clk/SM on sm_100: 1.1 / 2.25 PF at ~1.85 GHz)."""
+    try:
+        mhz = clk.summary().get("sm_mhz")
+    except Exception:
+        mhz = None
+    if not mhz:
+        return None
+    return round(achieved_tflops * 1e12 / (148 * (4096 if tf32 else 8192) * mhz * 1e6), 4)
+
+
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -425,8 +437,12 @@ def cgemm_headline(args, world, rank, local):
             "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "kernel": gemm_kernel_name(n, n, kind),
+                         "frac_at_clock": frac_at_clock(achieved, tf32, clk),
                          "note": f"3 x 8mnk tensor-pipe flops per launch / CUDA-event time; "
-                                 f"peak = {psrc}"},
+                                 f"peak = {psrc}; frac_at_clock = achieved / (148 SMs x "
+                                 f"{4096 if tf32 else 8192} dense flop/clk/SM x the median SM clock "
+                                 f"sampled under load): the tensor pipe's share at the clock the "
+                                 f"power cap left"},
             "stages_ms": {k2: round(v / max(cnt, 1), 3) for k2, v in stage.items()},
             "fidelity": {"rel_err": err, "fp32_ref_rel_err": err32,
                          "ratio_vs_fp32": round(err / err32, 3) if err32 else None,
