@@ -205,9 +205,12 @@ int launch_gemm_rows(const TcecGemmArgs& g, int64_t r0, int64_t r1, bool chunked
 // Launch the device pipeline of one dispatch (no host synchronization).
 int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t m, int64_t n,
                     int64_t k, const tcec_dispatch_config_t& cfg, const DispatchPlan& p,
-                    DevDecision* d, void* ws, const ChunkHook* hook) {
+                    DevDecision* d, void* ws, const ChunkHook* hook, const MatrixView* va,
+                    const MatrixView* vb) {
     cudaStream_t s = h.stream;
     if (p.tier == kTierInvalid) return set_error(TCEC_ERR_INVALID_ARGUMENT, "unknown forced mode");
+    if ((va || vb) && (p.tier != kTierTc || hook))
+        return set_error(TCEC_ERR_LOGIC, "operand views need the tensor-core tier");
     if (p.tier == kTierTc && cfg.k_tile < 1)
         return set_error(TCEC_ERR_INVALID_ARGUMENT, "k_tile must be >= 1");
     const bool prof = h.prof && h.ev[0];
@@ -255,11 +258,11 @@ int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t
     void* bhi = const_cast<void*>(g.b_hi);
     void* blo = const_cast<void*>(g.b_lo);
     if (g.xa) {
-        launch_prep_ax(a, m, k, p.kp, ahi, alo, d, p.kind, p.corrected, s);
-        launch_prep_bx(b, k, n, p.kp, bhi, blo, d, p.kind, p.corrected, s);
+        launch_prep_ax(a, m, k, p.kp, ahi, alo, d, p.kind, p.corrected, s, va);
+        launch_prep_bx(b, k, n, p.kp, bhi, blo, d, p.kind, p.corrected, s, vb);
     } else {
-        launch_prep_a(a, m, k, p.kp, ahi, alo, d, p.kind, p.corrected, s);
-        launch_prep_b(b, k, n, p.kp, bhi, blo, d, p.kind, p.corrected, s);
+        launch_prep_a(a, m, k, p.kp, ahi, alo, d, p.kind, p.corrected, s, 0, va);
+        launch_prep_b(b, k, n, p.kp, bhi, blo, d, p.kind, p.corrected, s, 0, vb);
     }
     if (prof) cudaEventRecord(h.ev[2], s);
     // row chunks (host-buffer API): only the wide kernel indexes into A' by row

@@ -35,6 +35,53 @@ TCEC_DEV void flag_or(unsigned* flag, unsigned v) {
     if (any && flag && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
 }
 
+// offset of index idx in a run map (runs outermost first, innermost last)
+TCEC_DEV int64_t run_offset(const RunMap& rm, uint32_t idx) {
+    int64_t off = 0;
+#pragma unroll
+    for (int r = kMaxRuns - 1; r >= 0; --r) {
+        if (r < rm.n) {
+            uint32_t dgt;
+            if (rm.pow2) {
+                dgt = idx & ((1u << rm.shift[r]) - 1u);
+                idx >>= rm.shift[r];
+            } else {
+                dgt = idx % rm.ext[r];
+                idx /= rm.ext[r];
+            }
+            off += int64_t(dgt) * rm.stride[r];
+        }
+    }
+    return off;
+}
+
+// 4 consecutive complex elements (row, kc .. kc + 3) of a matrix view of a
+// tensor (zero past column k): one run offset and four loads when the four
+// sit in the innermost unit-stride run, else one offset each
+TCEC_DEV void load4_view(const float* a, const MatrixView& v, int64_t row, int64_t kc, int64_t k,
+                         float (&x)[8]) {
+    const float2* t = reinterpret_cast<const float2*>(a);
+    const int64_t ro = run_offset(v.rows, uint32_t(row));
+    const int n = v.cols.n;
+    if (kc + 4 <= k && n > 0 && v.cols.stride[n - 1] == 1 &&
+        (uint32_t(kc) % v.cols.ext[n - 1]) + 4u <= v.cols.ext[n - 1]) {
+        const float2* q = t + ro + run_offset(v.cols, uint32_t(kc));
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float2 w = __ldcs(q + e);
+            x[2 * e] = w.x;
+            x[2 * e + 1] = w.y;
+        }
+        return;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const float2 w = kc + e < k ? __ldcs(t + ro + run_offset(v.cols, uint32_t(kc + e))) : make_float2(0.0f, 0.0f);
+        x[2 * e] = w.x;
+        x[2 * e + 1] = w.y;
+    }
+}
+
 // ------------------------------------------------------------ elementwise
 
 __global__ void quantize_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t n,
@@ -394,11 +441,12 @@ TCEC_DEV void convert_n(float (&x)[N], const PrepMode& pm, double factor, float 
 
 // A (m x k complex) -> K-major m x kp; each thread converts 8 consecutive
 // real components of one row (16 B of f16 or 32 B of tf32 per output plane)
+template <bool VIEW>
 TCEC_DEV void prep_a_part(const float* __restrict__ a, int64_t m,
                                                           int64_t k2, int64_t kp, void* hi_v,
                                                           void* lo_v, const DevDecision* d,
                                                           int kind_fixed, int corrected, int64_t row0,
-        DevDecision* df, int bid, int nblk) {
+        DevDecision* df, int bid, int nblk, const MatrixView& view) {
     // rows [row0, row0 + m) of A (the host-buffer pipeline converts row chunks
     // as they arrive; every row is independent)
     const PrepMode pm = prep_mode(d, kind_fixed, false);
@@ -415,7 +463,10 @@ TCEC_DEV void prep_a_part(const float* __restrict__ a, int64_t m,
         const int64_t col = (c - rl * chunks_per_row) * 8;
         const int64_t row = row0 + rl;
         float x[8];
-        if (vec && col < k2) {
+        if (VIEW) {
+            // A is a view of the unpermuted tensor (fused TTGT gather)
+            load4_view(a, view, row, col / 2, k2 / 2, x);
+        } else if (vec && col < k2) {
             const float4* p = reinterpret_cast<const float4*>(a + row * k2 + col);
             const float4 v0 = __ldcs(p), v1 = __ldcs(p + 1);
             x[0] = v0.x; x[1] = v0.y; x[2] = v0.z; x[3] = v0.w;
@@ -455,11 +506,14 @@ TCEC_DEV void prep_a_part(const float* __restrict__ a, int64_t m,
     flag_or(&dm->scale_overflow, bad);
 }
 
+template <bool VIEW>
 __global__ void __launch_bounds__(kThreads) prep_a_kernel(const float* __restrict__ a, int64_t m,
                                                           int64_t k2, int64_t kp, void* hi_v,
                                                           void* lo_v, const DevDecision* d,
-                                                          int kind_fixed, int corrected, int64_t row0) {
-    prep_a_part(a, m, k2, kp, hi_v, lo_v, d, kind_fixed, corrected, row0, const_cast<DevDecision*>(d), int(blockIdx.x), int(gridDim.x));
+                                                          int kind_fixed, int corrected, int64_t row0,
+                                                          const MatrixView view) {
+    prep_a_part<VIEW>(a, m, k2, kp, hi_v, lo_v, d, kind_fixed, corrected, row0, const_cast<DevDecision*>(d),
+                      int(blockIdx.x), int(gridDim.x), view);
 }
 
 // B (k x n complex) -> B'^T (2n x kp, K-major) with the complex block expansion
@@ -472,17 +526,19 @@ __global__ void __launch_bounds__(kThreads) prep_a_kernel(const float* __restric
 // and plane -- converting two kk per lane with the vectorised split.
 constexpr int kPrepBKK = 64, kPrepBJ = 32, kPrepBStride = kPrepBKK + 2;
 
+template <bool VIEW>
 TCEC_DEV void prep_b_part(const float2* __restrict__ b, int64_t k,
                                                      int64_t n, int64_t kp, void* hi_v,
                                                      void* lo_v, const DevDecision* d,
                                                      int kind_fixed, int corrected, int64_t jout0,
-        DevDecision* df, int bid, int nblk) {
+        DevDecision* df, int bid, int nblk, const MatrixView& view) {
     // b is a k x n column block whose B' rows start at 2 jout0
     const PrepMode pm = prep_mode(d, kind_fixed, true);
     if (!pm.active) return;
     const double factor = ldexp(1.0, pm.scale);
     const float fs = (pm.scale >= -149 && pm.scale <= 127) ? ldexpf(1.0f, pm.scale) : 1.0f;
     __shared__ __align__(16) float2 tile[kPrepBJ][kPrepBStride];
+    __shared__ int64_t roff_s[VIEW ? kPrepBKK : 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;  // 8 warps
     const int64_t tiles_j = (n + kPrepBJ - 1) / kPrepBJ;
     const int64_t kk_cols = kp / 2;                               // complex K extent incl. padding
@@ -491,12 +547,20 @@ TCEC_DEV void prep_b_part(const float2* __restrict__ b, int64_t k,
     unsigned ovf = 0, bad = 0;
     for (int64_t t = bid; t < ntiles; t += nblk) {
         const int64_t j0 = (t % tiles_j) * kPrepBJ, kk0 = (t / tiles_j) * kPrepBKK;
-        // load: warp w reads rows kk0 + w, w+8, ... (32 consecutive j each)
+        // load: warp w reads rows kk0 + w, w+8, ... (32 consecutive j each);
+        // VIEW: B is a view of the unpermuted tensor (fused TTGT gather)
+        const int64_t co = VIEW && j0 + lane < n ? run_offset(view.cols, uint32_t(j0 + lane)) : 0;
+        if (VIEW) {  // the tile's 64 row offsets, one thread each
+            if (threadIdx.x < kPrepBKK)
+                roff_s[threadIdx.x] = kk0 + threadIdx.x < k ? run_offset(view.rows, uint32_t(kk0 + threadIdx.x)) : 0;
+            __syncthreads();
+        }
 #pragma unroll
         for (int r = 0; r < kPrepBKK / 8; ++r) {
             const int kk = warp + 8 * r;
             const int64_t gk = kk0 + kk, gj = j0 + lane;
-            tile[lane][kk] = (gk < k && gj < n) ? __ldcs(b + gk * n + gj) : make_float2(0.0f, 0.0f);
+            const float2* src = VIEW ? b + roff_s[kk] + co : b + gk * n + gj;
+            tile[lane][kk] = (gk < k && gj < n) ? __ldcs(src) : make_float2(0.0f, 0.0f);
         }
         __syncthreads();
         // write: warp w owns j = j0 + w, w+8, ...; lane owns kk0 + 2 lane, +1
@@ -548,11 +612,13 @@ TCEC_DEV void prep_b_part(const float2* __restrict__ b, int64_t k,
     flag_or(&dm->scale_overflow, bad);
 }
 
+template <bool VIEW>
 __global__ void __launch_bounds__(256) prep_b_kernel(const float2* __restrict__ b, int64_t k,
                                                      int64_t n, int64_t kp, void* hi_v,
                                                      void* lo_v, const DevDecision* d,
-                                                     int kind_fixed, int corrected, int64_t jout0) {
-    prep_b_part(b, k, n, kp, hi_v, lo_v, d, kind_fixed, corrected, jout0, const_cast<DevDecision*>(d), int(blockIdx.x), int(gridDim.x));
+                                                     int kind_fixed, int corrected, int64_t jout0,
+        const MatrixView view) {
+    prep_b_part<VIEW>(b, k, n, kp, hi_v, lo_v, d, kind_fixed, corrected, jout0, const_cast<DevDecision*>(d), int(blockIdx.x), int(gridDim.x), view);
 }
 
 // --------------------------------------------- A-expanded operand layout
@@ -570,11 +636,12 @@ __global__ void __launch_bounds__(256) prep_b_kernel(const float2* __restrict__ 
 // A (m x k complex) -> A'' (2m x kp); each thread converts 4 consecutive
 // complex elements of one row (8 components) and writes 8 K' columns of both
 // rows of the pair
+template <bool VIEW>
 TCEC_DEV void prep_ax_part(const float* __restrict__ a, int64_t m,
                                                            int64_t k, int64_t kp, void* hi_v, void* lo_v,
                                                            const DevDecision* d, int kind_fixed,
                                                            int corrected,
-        DevDecision* df, int bid, int nblk) {
+        DevDecision* df, int bid, int nblk, const MatrixView& view) {
     const PrepMode pm = prep_mode(d, kind_fixed, false);
     if (!pm.active) return;
     const double factor = ldexp(1.0, pm.scale);
@@ -589,7 +656,10 @@ TCEC_DEV void prep_ax_part(const float* __restrict__ a, int64_t m,
         const int64_t row = c / chunks_per_row;
         const int64_t col = (c - row * chunks_per_row) * 8;  // K' column = 2 p0
         float x[8];
-        if (vec && col < k2) {
+        if (VIEW) {
+            // A is a view of the unpermuted tensor (fused TTGT gather)
+            load4_view(a, view, row, col / 2, k2 / 2, x);
+        } else if (vec && col < k2) {
             const float4* p = reinterpret_cast<const float4*>(a + row * k2 + col);
             const float4 v0 = __ldcs(p), v1 = __ldcs(p + 1);
             x[0] = v0.x; x[1] = v0.y; x[2] = v0.z; x[3] = v0.w;
@@ -651,25 +721,30 @@ TCEC_DEV void prep_ax_part(const float* __restrict__ a, int64_t m,
     flag_or(&dm->scale_overflow, bad);
 }
 
+template <bool VIEW>
 __global__ void __launch_bounds__(kThreads) prep_ax_kernel(const float* __restrict__ a, int64_t m,
                                                            int64_t k, int64_t kp, void* hi_v, void* lo_v,
                                                            const DevDecision* d, int kind_fixed,
-                                                           int corrected) {
-    prep_ax_part(a, m, k, kp, hi_v, lo_v, d, kind_fixed, corrected, const_cast<DevDecision*>(d), int(blockIdx.x), int(gridDim.x));
+                                                           int corrected,
+        const MatrixView view) {
+    prep_ax_part<VIEW>(a, m, k, kp, hi_v, lo_v, d, kind_fixed, corrected, const_cast<DevDecision*>(d),
+                       int(blockIdx.x), int(gridDim.x), view);
 }
 
 // B (k x n complex) -> B'' = B^T (n x kp, K-major, (re, im) pairs along K).
 // Same 64 (kk) x 32 (j) smem tiles as prep_b_kernel, one output row per j.
+template <bool VIEW>
 TCEC_DEV void prep_bx_part(const float2* __restrict__ b, int64_t k,
                                                       int64_t n, int64_t kp, void* hi_v, void* lo_v,
                                                       const DevDecision* d, int kind_fixed,
                                                       int corrected,
-        DevDecision* df, int bid, int nblk) {
+        DevDecision* df, int bid, int nblk, const MatrixView& view) {
     const PrepMode pm = prep_mode(d, kind_fixed, true);
     if (!pm.active) return;
     const double factor = ldexp(1.0, pm.scale);
     const float fs = (pm.scale >= -149 && pm.scale <= 127) ? ldexpf(1.0f, pm.scale) : 1.0f;
     __shared__ __align__(16) float2 tile[kPrepBJ][kPrepBStride];
+    __shared__ int64_t roff_s[VIEW ? kPrepBKK : 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;  // 8 warps
     const int64_t tiles_j = (n + kPrepBJ - 1) / kPrepBJ;
     const int64_t kk_cols = kp / 2;
@@ -678,11 +753,18 @@ TCEC_DEV void prep_bx_part(const float2* __restrict__ b, int64_t k,
     unsigned ovf = 0, bad = 0;
     for (int64_t t = bid; t < ntiles; t += nblk) {
         const int64_t j0 = (t % tiles_j) * kPrepBJ, kk0 = (t / tiles_j) * kPrepBKK;
+        const int64_t co = VIEW && j0 + lane < n ? run_offset(view.cols, uint32_t(j0 + lane)) : 0;
+        if (VIEW) {  // the tile's 64 row offsets, one thread each
+            if (threadIdx.x < kPrepBKK)
+                roff_s[threadIdx.x] = kk0 + threadIdx.x < k ? run_offset(view.rows, uint32_t(kk0 + threadIdx.x)) : 0;
+            __syncthreads();
+        }
 #pragma unroll
         for (int r = 0; r < kPrepBKK / 8; ++r) {
             const int kk = warp + 8 * r;
             const int64_t gk = kk0 + kk, gj = j0 + lane;
-            tile[lane][kk] = (gk < k && gj < n) ? __ldcs(b + gk * n + gj) : make_float2(0.0f, 0.0f);
+            const float2* src = VIEW ? b + roff_s[kk] + co : b + gk * n + gj;
+            tile[lane][kk] = (gk < k && gj < n) ? __ldcs(src) : make_float2(0.0f, 0.0f);
         }
         __syncthreads();
         const int64_t col = 2 * (kk0 + 2 * lane);
@@ -716,11 +798,13 @@ TCEC_DEV void prep_bx_part(const float2* __restrict__ b, int64_t k,
     flag_or(&dm->scale_overflow, bad);
 }
 
+template <bool VIEW>
 __global__ void __launch_bounds__(256) prep_bx_kernel(const float2* __restrict__ b, int64_t k,
                                                       int64_t n, int64_t kp, void* hi_v, void* lo_v,
                                                       const DevDecision* d, int kind_fixed,
-                                                      int corrected) {
-    prep_bx_part(b, k, n, kp, hi_v, lo_v, d, kind_fixed, corrected, const_cast<DevDecision*>(d), int(blockIdx.x), int(gridDim.x));
+                                                      int corrected,
+        const MatrixView view) {
+    prep_bx_part<VIEW>(b, k, n, kp, hi_v, lo_v, d, kind_fixed, corrected, const_cast<DevDecision*>(d), int(blockIdx.x), int(gridDim.x), view);
 }
 
 // ------------------------------------------------------------ SIMT GEMM
@@ -1139,25 +1223,6 @@ TCEC_DEV void skinny_mac(const float2* __restrict__ srow, float xr, float xi,
     }
 }
 
-// offset of index idx in a run map (runs outermost first, innermost last)
-TCEC_DEV int64_t run_offset(const RunMap& rm, uint32_t idx) {
-    int64_t off = 0;
-#pragma unroll
-    for (int r = kMaxRuns - 1; r >= 0; --r) {
-        if (r < rm.n) {
-            uint32_t dgt;
-            if (rm.pow2) {
-                dgt = idx & ((1u << rm.shift[r]) - 1u);
-                idx >>= rm.shift[r];
-            } else {
-                dgt = idx % rm.ext[r];
-                idx /= rm.ext[r];
-            }
-            off += int64_t(dgt) * rm.stride[r];
-        }
-    }
-    return off;
-}
 
 // m <= MX: thread j owns column j of C.  VIEW: B is read through a matrix
 // view of the unpermuted tensor (fused TTGT gather): B(kk, j) =
@@ -1443,7 +1508,10 @@ void launch_skinny_mx(const float2* a, const float2* b, float2* c, int64_t m, in
                     int dev = 0, sms = 148;
                     cudaGetDevice(&dev);
                     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-                    const int64_t blocks = std::min<int64_t>((m + 255) / 256, int64_t(per_sm) * sms);
+                    // VIEW (gathered rows): one 32-row block per warp measured faster
+                    // than the persistent walk ((2^22, 16, 64): 1.98 vs 1.67 ms)
+                    const int64_t blocks = VIEW ? (m + 255) / 256
+                                                : std::min<int64_t>((m + 255) / 256, int64_t(per_sm) * sms);
                     cgemm_skinny_row_kernel<F64, MX, true, VIEW><<<unsigned(blocks), 256, stage_bytes, s>>>(
                         a, b + j0, c + j0, m, cols, int(k), n, view);
                     continue;
@@ -1874,37 +1942,56 @@ void launch_select(DevDecision* d, double t, int target, int forced_scaled, cuda
 }
 
 void launch_prep_a(const float* a, int64_t m, int64_t k, int64_t kp, void* hi, void* lo,
-                   const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s, int64_t row0) {
+                   const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s, int64_t row0,
+                   const MatrixView* view) {
     const int64_t total = m * (kp / 8);
     if (total <= 0) return;
-    prep_a_kernel<<<grid_for(total, kThreads, 148 * 32), kThreads, 0, s>>>(
-        a, m, 2 * k, kp, hi, lo, d, kind_fixed, corrected, row0);
+    const unsigned grid = unsigned(grid_for(total, kThreads, 148 * 32));
+    if (view)
+        prep_a_kernel<true><<<grid, kThreads, 0, s>>>(a, m, 2 * k, kp, hi, lo, d, kind_fixed, corrected, row0, *view);
+    else
+        prep_a_kernel<false><<<grid, kThreads, 0, s>>>(a, m, 2 * k, kp, hi, lo, d, kind_fixed, corrected, row0,
+                                                       MatrixView{});
 }
 
 void launch_prep_b(const float* b, int64_t k, int64_t n, int64_t kp, void* hi, void* lo,
-                   const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s, int64_t jout0) {
+                   const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s, int64_t jout0,
+                   const MatrixView* view) {
     if (n <= 0 || kp <= 0) return;
     const int64_t tiles = ((n + kPrepBJ - 1) / kPrepBJ) * ((kp / 2 + kPrepBKK - 1) / kPrepBKK);
     const unsigned grid = unsigned(tiles < 148 * 8 ? tiles : 148 * 8);
-    prep_b_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const float2*>(b), k, n, kp, hi, lo, d,
-                                       kind_fixed, corrected, jout0);
+    const float2* b2 = reinterpret_cast<const float2*>(b);
+    if (view)
+        prep_b_kernel<true><<<grid, 256, 0, s>>>(b2, k, n, kp, hi, lo, d, kind_fixed, corrected, jout0, *view);
+    else
+        prep_b_kernel<false><<<grid, 256, 0, s>>>(b2, k, n, kp, hi, lo, d, kind_fixed, corrected, jout0,
+                                                  MatrixView{});
 }
 
 void launch_prep_ax(const float* a, int64_t m, int64_t k, int64_t kp, void* hi, void* lo,
-                    const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s) {
+                    const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s,
+                    const MatrixView* view) {
     const int64_t total = m * (kp / 8);
     if (total <= 0) return;
-    prep_ax_kernel<<<grid_for(total, kThreads, 148 * 32), kThreads, 0, s>>>(a, m, k, kp, hi, lo, d,
-                                                                           kind_fixed, corrected);
+    const unsigned grid = unsigned(grid_for(total, kThreads, 148 * 32));
+    if (view)
+        prep_ax_kernel<true><<<grid, kThreads, 0, s>>>(a, m, k, kp, hi, lo, d, kind_fixed, corrected, *view);
+    else
+        prep_ax_kernel<false><<<grid, kThreads, 0, s>>>(a, m, k, kp, hi, lo, d, kind_fixed, corrected,
+                                                        MatrixView{});
 }
 
 void launch_prep_bx(const float* b, int64_t k, int64_t n, int64_t kp, void* hi, void* lo,
-                    const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s) {
+                    const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s,
+                    const MatrixView* view) {
     if (n <= 0 || kp <= 0) return;
     const int64_t tiles = ((n + kPrepBJ - 1) / kPrepBJ) * ((kp / 2 + kPrepBKK - 1) / kPrepBKK);
     const unsigned grid = unsigned(tiles < 148 * 8 ? tiles : 148 * 8);
-    prep_bx_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const float2*>(b), k, n, kp, hi, lo, d,
-                                        kind_fixed, corrected);
+    const float2* b2 = reinterpret_cast<const float2*>(b);
+    if (view)
+        prep_bx_kernel<true><<<grid, 256, 0, s>>>(b2, k, n, kp, hi, lo, d, kind_fixed, corrected, *view);
+    else
+        prep_bx_kernel<false><<<grid, 256, 0, s>>>(b2, k, n, kp, hi, lo, d, kind_fixed, corrected, MatrixView{});
 }
 
 void launch_cgemm_fp32_ref(const float2* a, const float2* b, float2* c, int64_t m, int64_t n,

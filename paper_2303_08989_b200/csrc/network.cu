@@ -225,6 +225,14 @@ static int build_plan(const tcec_network_s& net, const int* steps, int n_steps,
                 sp.view_a = make_matrix_view(int(A.dims.size()), A.dims.data(), sp.a_axis.data(),
                                              int(A.dims.size()) - sp.n_shared, &sp.view);
         }
+        if (sp.dp.tier == kTierTc && view_gather_enabled()) {
+            if (sp.perm_a)
+                sp.tview_a = make_matrix_view(int(A.dims.size()), A.dims.data(), sp.a_axis.data(),
+                                              int(A.dims.size()) - sp.n_shared, &sp.tva);
+            if (sp.perm_b)
+                sp.tview_b = make_matrix_view(int(B.dims.size()), B.dims.data(), sp.b_axis.data(), sp.n_shared,
+                                              &sp.tvb);
+        }
         if (sp.dp.tier == kTierTc && cfg.k_tile < 1)
             return set_error(TCEC_ERR_INVALID_ARGUMENT, "k_tile must be >= 1");
         plan.ws_bytes = std::max(plan.ws_bytes, plan_workspace(sp.dp, sp.m, sp.n));
@@ -295,7 +303,8 @@ static int enqueue_fold(tcec_network_s& net, const FoldPlan& plan, const tcec_di
         float2* pa = pa_src;
         float2* pb = pb_src;
         cudaError_t e;
-        const bool perm_a = sp.perm_a && !sp.view_a, perm_b = sp.perm_b && !sp.view_b;
+        const bool perm_a = sp.perm_a && !sp.view_a && !sp.tview_a,
+                   perm_b = sp.perm_b && !sp.view_b && !sp.tview_b;
         if (perm_a) {
             e = cudaMallocAsync(reinterpret_cast<void**>(&pa), size_t(sp.a_size) * 8, s);
             if (e != cudaSuccess) return cuda_error(e, "permute buffer");
@@ -319,7 +328,8 @@ static int enqueue_fold(tcec_network_s& net, const FoldPlan& plan, const tcec_di
             const int rc = launch_dispatch(h, reinterpret_cast<const float*>(pa),
                                            reinterpret_cast<const float*>(pb),
                                            reinterpret_cast<float*>(pc), sp.m, sp.n, sp.k, cfg, sp.dp,
-                                           dec + si, ws);
+                                           dec + si, ws, nullptr, sp.tview_a ? &sp.tva : nullptr,
+                                           sp.tview_b ? &sp.tvb : nullptr);
             if (rc) return rc;
         }
         if (perm_a) cudaFreeAsync(pa, s);

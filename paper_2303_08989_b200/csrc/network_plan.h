@@ -33,6 +33,10 @@ struct StepPlan {
     // a strided view of the unpermuted tensor instead of a permuted copy
     bool view_a = false, view_b = false;
     MatrixView view;
+    // the same for tensor-core steps: the preparation kernels read either
+    // operand through a view (the statistics sweep the unpermuted tensor)
+    bool tview_a = false, tview_b = false;
+    MatrixView tva, tvb;
 };
 
 struct FoldPlan {

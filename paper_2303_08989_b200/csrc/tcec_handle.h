@@ -103,9 +103,13 @@ struct ChunkHook {
     int (*done)(void* ctx, int64_t r0, int64_t r1) = nullptr;
     void* ctx = nullptr;
 };
+// va / vb (tensor-core tier only): the operand is the unpermuted tensor read
+// through a matrix view by the preparation kernels (fused TTGT gather; the
+// statistics are order-free and sweep the tensor as is)
 int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t m, int64_t n,
                     int64_t k, const tcec_dispatch_config_t& cfg, const DispatchPlan& p,
-                    DevDecision* d, void* ws, const ChunkHook* hook = nullptr);
+                    DevDecision* d, void* ws, const ChunkHook* hook = nullptr,
+                    const MatrixView* va = nullptr, const MatrixView* vb = nullptr);
 int finish_dispatch(const DispatchPlan& p, const DevDecision& dd, int64_t m, int64_t n, int64_t k,
                     tcec_dispatch_result_t* res);
 void format_line(char* out, size_t cap, int64_t m, int64_t n, int64_t k, const char* label, int sa,

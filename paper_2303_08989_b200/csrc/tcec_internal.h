@@ -51,35 +51,10 @@ void launch_stats2(const float* a, int64_t n_a, const float* b, int64_t n_b, Dev
 void launch_select(DevDecision* d, double t, int target, int forced_scaled, cudaStream_t s);
 
 // ------------------------------------------------------- operand layouts
-// A (m x k complex, interleaved) -> A' = m x Kp real, K-major, hi/lo in the
-// decided format (f16 or tf32-in-f32); padded columns are zero.
-// kind_fixed >= 0 overrides the device decision (forced / size-gated modes).
-void launch_prep_a(const float* a, int64_t m, int64_t k, int64_t kp, void* hi, void* lo,
-                   const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s,
-                   int64_t row0 = 0);  // rows [row0, row0 + m) of a full A / A'
-// B (k x n complex) -> B'^T = 2n x Kp real, K-major, with the complex block
-// expansion [[Br, Bi], [-Bi, Br]] so one real GEMM yields interleaved C.
-void launch_prep_b(const float* b, int64_t k, int64_t n, int64_t kp, void* hi, void* lo,
-                   const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s,
-                   int64_t jout0 = 0);  // b = a k x n column block, B' rows from 2 jout0
-// A-expanded layout (used when m < n): A'' = 2m x Kp with rows 2i = (Ar, -Ai),
-// 2i+1 = (Ai, Ar) along K; B'' = B^T = n x Kp with (Br, Bi) along K.  The GEMM
-// yields rows (Re C[i,:], Im C[i,:]) and its epilogue interleaves them.
-void launch_prep_ax(const float* a, int64_t m, int64_t k, int64_t kp, void* hi, void* lo,
-                    const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s);
-void launch_prep_bx(const float* b, int64_t k, int64_t n, int64_t kp, void* hi, void* lo,
-                    const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s);
-
-// -------------------------------------------------------------- SIMT GEMM
-// FP32_REF complex GEMM, bit-identical to the reference schedule
-// (kernels_scalar.cpp:76-87 + cgemm.cpp:33-44).  Strided operand views allow
-// fused TTGT gathers: element (i, kk) of A is at a[ (row_off(i) + col_off(kk)) ]
-void launch_cgemm_fp32_ref(const float2* a, const float2* b, float2* c, int64_t m, int64_t n,
-                           int64_t k, cudaStream_t s);
 // Matrix view of a permuted tensor (fused TTGT gather): element (r, c) of the
 // rows x cols matrix is at base + rows.offset(r) + cols.offset(c), each offset
 // a mixed-radix sum over runs of merged tensor axes (innermost run last).
-constexpr int kMaxRuns = 8;
+constexpr int kMaxRuns = 16;  // Sycamore m=12 tensor-core operands need up to 16
 struct RunMap {
     int n = 0;                      // runs
     int pow2 = 1;                   // every extent a power of two (shift / mask decomposition)
@@ -90,6 +65,35 @@ struct RunMap {
 struct MatrixView {
     RunMap rows, cols;
 };
+// A (m x k complex, interleaved) -> A' = m x Kp real, K-major, hi/lo in the
+// decided format (f16 or tf32-in-f32); padded columns are zero.
+// kind_fixed >= 0 overrides the device decision (forced / size-gated modes).
+void launch_prep_a(const float* a, int64_t m, int64_t k, int64_t kp, void* hi, void* lo,
+                   const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s,
+                   int64_t row0 = 0,   // rows [row0, row0 + m) of a full A / A'
+                   const MatrixView* view = nullptr);  // A read through a view (fused TTGT gather)
+// B (k x n complex) -> B'^T = 2n x Kp real, K-major, with the complex block
+// expansion [[Br, Bi], [-Bi, Br]] so one real GEMM yields interleaved C.
+void launch_prep_b(const float* b, int64_t k, int64_t n, int64_t kp, void* hi, void* lo,
+                   const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s,
+                   int64_t jout0 = 0,  // b = a k x n column block, B' rows from 2 jout0
+                   const MatrixView* view = nullptr);
+// A-expanded layout (used when m < n): A'' = 2m x Kp with rows 2i = (Ar, -Ai),
+// 2i+1 = (Ai, Ar) along K; B'' = B^T = n x Kp with (Br, Bi) along K.  The GEMM
+// yields rows (Re C[i,:], Im C[i,:]) and its epilogue interleaves them.
+void launch_prep_ax(const float* a, int64_t m, int64_t k, int64_t kp, void* hi, void* lo,
+                    const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s,
+                    const MatrixView* view = nullptr);
+void launch_prep_bx(const float* b, int64_t k, int64_t n, int64_t kp, void* hi, void* lo,
+                    const DevDecision* d, int kind_fixed, int corrected, cudaStream_t s,
+                    const MatrixView* view = nullptr);
+
+// -------------------------------------------------------------- SIMT GEMM
+// FP32_REF complex GEMM, bit-identical to the reference schedule
+// (kernels_scalar.cpp:76-87 + cgemm.cpp:33-44).  Strided operand views allow
+// fused TTGT gathers: element (i, kk) of A is at a[ (row_off(i) + col_off(kk)) ]
+void launch_cgemm_fp32_ref(const float2* a, const float2* b, float2* c, int64_t m, int64_t n,
+                           int64_t k, cudaStream_t s);
 // Build the view of operand `role` (0 = A: rows = free_a, cols = shared;
 // 1 = B: rows = shared, cols = free_b) of a tensor with physical extents
 // dims[0..rank) permuted by axis_of (new axis a = old axis axis_of[a]) whose

@@ -405,3 +405,68 @@ def test_skinny_view_gather_bit_exact(handle, case, executor):
     finally:
         net.close()
         handle.set_executor(0)
+
+
+def _tc_view_spec(case):
+    """Networks whose tensor-core steps need operand permutes (scrambled shared
+    and free axes on both sides)."""
+    if case == 0:    # one TF32-tier step (512 <= min < 2048), A-expanded layout (m < n)
+        labels = [["x1", "s1", "x2", "s2"], ["s2", "y1", "s1", "y2"]]
+        dims = [[16, 32, 32, 16], [16, 32, 32, 32]]
+        path = [(0, 1)]
+    elif case == 1:  # one AUTO step (min >= 2048), B-expanded layout (m > n)
+        labels = [["s1", "x1", "s2", "x2"], ["y1", "s2", "s1"]]
+        dims = [[64, 64, 32, 64], [2048, 32, 64]]
+        path = [(0, 1)]
+    else:            # a chain: the intermediate feeds a second permuted tensor-core step
+        labels = [["x1", "s1", "x2", "s2"], ["s2", "y1", "s1", "y2"], ["y2", "z1", "x1", "z2"]]
+        dims = [[16, 32, 32, 16], [16, 32, 32, 32], [32, 32, 16, 32]]
+        path = [(0, 1), (2, 3)]
+    data = [matrix_recipe("uniform", 1, int(np.prod(d)), 90 + i).reshape(-1) for i, d in enumerate(dims)]
+    return NetworkSpec(labels=labels, dims=dims, data=data), path
+
+
+_VIEW_OFF_SCRIPT = """
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+from paper_2303_08989_b200 import Handle, make_config
+from paper_2303_08989_b200.network import Network
+from tests.test_gpu_network import _tc_view_spec
+spec, path = _tc_view_spec({case})
+h = Handle(0)
+net = Network(h, spec)
+r, lines = net.contract(path, make_config(), want_log=True)
+np.save({out!r}, r.data)
+open({out!r} + ".log", "w").write("\\n".join(lines))
+net.close(); h.close()
+"""
+
+
+@pytest.mark.parametrize("case", [0, 1, 2])
+def test_tc_step_view_gather_bit_identical(handle, case, tmp_path):
+    """Tensor-core steps read permuted operands through a strided view in the
+    preparation kernels (fused TTGT gather; statistics on the unpermuted
+    tensor): the contraction -- decision lines included -- is bit-identical to
+    the permute-then-prepare path (TCEC_VIEW_GATHER=0 in a subprocess), and
+    within the reference bar of the f64 oracle fold."""
+    import os
+    import subprocess
+    import sys
+    spec, path = _tc_view_spec(case)
+    net = Network(handle, spec)
+    try:
+        got, lines = net.contract(path, make_config(), want_log=True)
+        ref = net.contract_oracle(path).data
+    finally:
+        net.close()
+    assert all(ln.split(",")[3] in ("TF32TCEC", "FP16TCEC", "FP16TCEC_SCALED") for ln in lines), lines
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = str(tmp_path / "off.npy")
+    env = dict(os.environ, TCEC_VIEW_GATHER="0")
+    subprocess.run([sys.executable, "-c", _VIEW_OFF_SCRIPT.format(root=root, case=case, out=out)],
+                   env=env, cwd=root, check=True, timeout=600)
+    off = np.load(out)
+    assert open(out + ".log").read().split("\n") == lines
+    assert np.array_equal(bits(got.data.view(np.float32)), bits(off.view(np.float32)))
+    err = np.linalg.norm(got.data.astype(np.complex128) - ref) / np.linalg.norm(ref)
+    assert err <= 5e-6, err
