@@ -1224,6 +1224,50 @@ TCEC_DEV void skinny_mac(const float2* __restrict__ srow, float xr, float xi,
 }
 
 
+// Packed f32x2 chains: fma.rn.f32x2(a, b, -0) is RN(a*b) exactly (signed
+// zeros, subnormals and overflow included) and add.rn.f32x2 is two RN adds,
+// so two products of the reference's mul-then-add chains issue as one FFMA2 +
+// one FADD2 (tools/probes/f32x2_fmaz_probe.cu).  The -0 pair must arrive as a
+// kernel argument: a literal lets ptxas fold the addend and contract the
+// following add into an FMA.
+TCEC_DEV uint64_t mulz2(uint64_t a, uint64_t b, uint64_t mz) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(mz));
+    return r;
+}
+TCEC_DEV uint64_t add2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+TCEC_DEV uint64_t pack2(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+TCEC_DEV float2 unpack2(uint64_t v) {
+    float2 f;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(f.x), "=f"(f.y) : "l"(v));
+    return f;
+}
+
+// column kernel MACs, packed: q[i][0] = (P1, P2) += (ar, ai) * (xr, xi),
+// q[i][1] = (P3, P4) += (ar, ai) * (xi, xr) -- the four reference chains of
+// output i (kernels_scalar.cpp:76-87) in the same order
+template <int MX>
+TCEC_DEV void skinny_mac_x2(const float2* __restrict__ srow, float xr, float xi, uint64_t (&q)[MX][2],
+                            uint64_t mz) {
+    const uint64_t x01 = pack2(xr, xi), x10 = pack2(xi, xr);
+#pragma unroll
+    for (int h = 0; h < MX / 2; ++h) {
+        const ulonglong2 s2 = reinterpret_cast<const ulonglong2*>(srow)[h];  // (ar, ai) of rows 2h, 2h+1
+        q[2 * h][0] = add2(q[2 * h][0], mulz2(s2.x, x01, mz));
+        q[2 * h][1] = add2(q[2 * h][1], mulz2(s2.x, x10, mz));
+        q[2 * h + 1][0] = add2(q[2 * h + 1][0], mulz2(s2.y, x01, mz));
+        q[2 * h + 1][1] = add2(q[2 * h + 1][1], mulz2(s2.y, x10, mz));
+    }
+}
+
 // m <= MX: thread j owns column j of C.  VIEW: B is read through a matrix
 // view of the unpermuted tensor (fused TTGT gather): B(kk, j) =
 // b[view.rows(kk) + view.cols(j)], the same elements in the same order.
@@ -1231,8 +1275,12 @@ template <bool F64, int MX, bool GROUPED, bool VIEW = false>
 __global__ void __launch_bounds__(256, 2) cgemm_skinny_col_kernel(const float2* __restrict__ a,
                                                                const float2* __restrict__ b,
                                                                float2* __restrict__ c, int m,
-                                                               int64_t n, int k, const MatrixView view) {
+                                                               int64_t n, int k, const MatrixView view,
+                                                               uint64_t mz) {
     using acc_t = typename std::conditional<F64, double, float>::type;
+    // packed f32x2 chains where the kernel is issue-bound (MX >= 8: ncu 81 %
+    // issue slots busy, 1024 of ~1230 instructions per 8-k group FMUL/FADD)
+    constexpr bool X2 = !F64 && MX >= 8;
     __shared__ __align__(16) float2 as[kSkinnyMaxK * MX];  // [kk][i]
     __shared__ int64_t koff[VIEW ? kSkinnyMaxK : 1];
     for (int t = threadIdx.x; t < k * MX; t += blockDim.x) {
@@ -1268,9 +1316,21 @@ __global__ void __launch_bounds__(256, 2) cgemm_skinny_col_kernel(const float2* 
         const bool live = j < n;
         const int64_t jn = j + step;
         const float2* bjn = col_ptr(jn < n ? jn : 0);
-        acc_t p[MX][4];
+        acc_t p[X2 ? 1 : MX][4];
+        uint64_t q[X2 ? MX : 1][2];
+        if constexpr (X2) {
 #pragma unroll
-        for (int i = 0; i < MX; ++i) p[i][0] = p[i][1] = p[i][2] = p[i][3] = acc_t(0);
+            for (int i = 0; i < MX; ++i) q[i][0] = q[i][1] = 0;  // +0 pairs
+        } else {
+#pragma unroll
+            for (int i = 0; i < MX; ++i) p[i][0] = p[i][1] = p[i][2] = p[i][3] = acc_t(0);
+        }
+        auto mac = [&](const float2* srow, float xr, float xi) {
+            if constexpr (X2)
+                skinny_mac_x2<MX>(srow, xr, xi, q, mz);
+            else
+                skinny_mac<F64, MX>(srow, xr, xi, p, true);
+        };
         int k0 = 0;
         if (grouped) {  // A/B on B200: the plain loop wins for k <= 4, grouped loads from 8 up
 #pragma unroll 1
@@ -1285,8 +1345,7 @@ __global__ void __launch_bounds__(256, 2) cgemm_skinny_col_kernel(const float2* 
                 }
                 if (live) {
 #pragma unroll
-                    for (int u = 0; u < 8; ++u)
-                        skinny_mac<F64, MX>(as + (k0 + u) * MX, bcol[u].x, bcol[u].y, p, true);
+                    for (int u = 0; u < 8; ++u) mac(as + (k0 + u) * MX, bcol[u].x, bcol[u].y);
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u) bcol[u] = bnxt[u];
@@ -1296,11 +1355,19 @@ __global__ void __launch_bounds__(256, 2) cgemm_skinny_col_kernel(const float2* 
 #pragma unroll 1
             for (; k0 < k; ++k0) {
                 const float2 bv = bel(bj, k0);
-                skinny_mac<F64, MX>(as + k0 * MX, bv.x, bv.y, p, true);
+                mac(as + k0 * MX, bv.x, bv.y);
             }
 #pragma unroll
-            for (int i = 0; i < MX; ++i)
-                if (i < m) __stcs(c + int64_t(i) * n + j, assemble<F64>(p[i]));
+            for (int i = 0; i < MX; ++i) {
+                if (i >= m) continue;
+                if constexpr (X2) {
+                    const float2 p12 = unpack2(q[i][0]), p34 = unpack2(q[i][1]);
+                    __stcs(c + int64_t(i) * n + j,
+                           make_float2(__fsub_rn(p12.x, p12.y), __fadd_rn(p34.x, p34.y)));
+                } else {
+                    __stcs(c + int64_t(i) * n + j, assemble<F64>(p[i]));
+                }
+            }
         }
         if (grouped && !chain_next && jn < n) {
 #pragma unroll
@@ -1449,6 +1516,8 @@ __global__ void __launch_bounds__(256, (MX <= 8 ? 3 : 2)) cgemm_skinny_row_kerne
     }
 }
 
+constexpr uint64_t kNegZero2 = 0x8000000080000000ull;  // (-0.0f, -0.0f)
+
 // persistent grid of the column kernels: the co-resident blocks (queried once
 // per kernel), never more than the 256-column chunks
 template <bool F64, int MX, bool GROUPED, bool VIEW>
@@ -1480,11 +1549,11 @@ void launch_skinny_mx(const float2* a, const float2* b, float2* c, int64_t m, in
             if (k >= 8)
                 cgemm_skinny_col_kernel<F64, MX, true, VIEW>
                     <<<col_grid<F64, MX, true, VIEW>(n), 256, 0, s>>>(
-                        a + r0 * k, b, c + r0 * n, rows, n, int(k), view);
+                        a + r0 * k, b, c + r0 * n, rows, n, int(k), view, kNegZero2);
             else
                 cgemm_skinny_col_kernel<F64, MX, false, VIEW>
                     <<<col_grid<F64, MX, false, VIEW>(n), 256, 0, s>>>(
-                        a + r0 * k, b, c + r0 * n, rows, n, int(k), view);
+                        a + r0 * k, b, c + r0 * n, rows, n, int(k), view, kNegZero2);
         }
     } else {
         for (int64_t j0 = 0; j0 < n; j0 += MX) {
