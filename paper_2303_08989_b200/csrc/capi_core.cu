@@ -882,10 +882,16 @@ static HostPipe plan_host_pipe(int64_t m, int64_t n, int chunks, int parts) {
     hp.q = int(std::max<int64_t>(1, std::min<int64_t>(parts, n / 256)));  // parts of >= 256 columns
     hp.wq = round_up((n + hp.q - 1) / hp.q, 128);  // even column offsets keep C blocks 16-B aligned
     hp.q = int((n + hp.wq - 1) / hp.wq);
-    static const int front_num = [] {  // front parts in eighths of q (tuning: TCEC_HOST_BFRONT)
+    // front parts in eighths of q (tuning: TCEC_HOST_BFRONT).  A quarter of B
+    // ahead of A: the GEMM (not the H2D) bounds the TF32TCEC headline, so a
+    // shorter head wins (16384^3 on the reference inputs: e2e 207.6 / 216.4 /
+    // 218.0 TFLOP/s with 4 / 3 / 2 eighths, 0 reruns; profiles/r02_host_bfront_ab.log).
+    // The decision taken from fewer parts is checked against the exact one
+    // (rerun on disagreement), so only speed depends on it.
+    static const int front_num = [] {
         const char* e = std::getenv("TCEC_HOST_BFRONT");
         const int v = e ? std::atoi(e) : 0;
-        return v > 0 && v <= 8 ? v : 4;
+        return v > 0 && v <= 8 ? v : 2;
     }();
     hp.front = std::max(1, hp.q * front_num / 8);
     return hp;
