@@ -152,19 +152,6 @@ TCEC_DEV void tma_load_2d(void* smem_dst, const void* tmap, uint64_t* bar, int x
         : "memory");
 }
 
-// TMA store of a 2-D box from shared memory (bulk-group completion): the
-// issuing thread later waits with tma_store_wait_read before the staging smem
-// is rewritten, and with tma_store_wait_all before the kernel exits
-TCEC_DEV void tma_store_2d(const void* tmap, const void* smem_src, int x, int y) {
-    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                     reinterpret_cast<uint64_t>(tmap)),
-                 "r"(smem_u32(smem_src)), "r"(x), "r"(y)
-                 : "memory");
-}
-TCEC_DEV void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-TCEC_DEV void tma_store_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-TCEC_DEV void tma_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
 // ------------------------------------------------------------------ tcgen05
 TCEC_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 TCEC_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }

@@ -600,8 +600,6 @@ static_assert(kWideSmemBytes <= 232448, "exceeds the 227 KB dynamic shared memor
 struct WideMaps {
     CUtensorMap ahi, alo, bhi, blo;
     CUtensorMap bhi_h, blo_h;  // 64-row boxes: the halves a pair multicasts (clusters of 2 pairs)
-    CUtensorMap cmap;          // C (m x n2 f32), 32 x 32 boxes, 128-B swizzle: TMA-store epilogue
-    int tma_c;                 // cmap valid (persistent kernel, B-expanded layout)
 };
 
 template <int FMT>
@@ -823,39 +821,6 @@ __device__ __forceinline__ void widep_body(const WideMaps& mp, float* __restrict
             const int n0 = n_blk * kWideBN;
             const int ew = warp - 2;
             const bool full_cols = n0 + kWideBN <= n2 && (n2 & 3) == 0;
-            if (mp.tma_c && !xa) {
-                // TMA-store epilogue: the quadrant's rows go to eight 32 x 32
-                // 128-B-swizzled boxes (conflict-free float4 writes), one
-                // thread issues the bulk stores and waits only until they have
-                // read the stage -- the warps are back on the next tile's TMEM
-                // drains instead of stalling on 128 KB of global stores
-#pragma unroll 1
-                for (int qq = 0; qq < 4; ++qq) {
-                    if (q == qq) {
-#pragma unroll
-                        for (int hh = 0; hh < 2; ++hh)
-#pragma unroll
-                            for (int i = 0; i < 64; i += 4) {
-                                const int cc = (128 * hh + 64 * p + i) >> 2;  // 16-B chunk of the 256 columns
-                                float* dst = cstage + (cc >> 3) * 1024 + lane * 32 + (((cc & 7) ^ (lane & 7)) << 2);
-                                *reinterpret_cast<float4*>(dst) =
-                                    make_float4(acc[64 * hh + i], acc[64 * hh + i + 1], acc[64 * hh + i + 2],
-                                                acc[64 * hh + i + 3]);
-                            }
-                    }
-                    fence_proxy_async();
-                    epi_bar_sync();
-                    if (ew == 0 && lane == 0 && m0 + 32 * qq < m) {
-#pragma unroll 1
-                        for (int bx = 0; bx < 8; ++bx)
-                            if (n0 + 32 * bx < n2) tma_store_2d(&mp.cmap, cstage + bx * 1024, n0 + 32 * bx, m0 + 32 * qq);
-                        tma_store_commit();
-                        tma_store_wait_read();
-                    }
-                    epi_bar_sync();
-                }
-                continue;
-            }
 #pragma unroll 1
             for (int qq = 0; qq < 4; ++qq) {
                 if (q == qq) {
@@ -902,7 +867,6 @@ __device__ __forceinline__ void widep_body(const WideMaps& mp, float* __restrict
             }
         }
     }
-    if (mp.tma_c && warp == 2 && lane == 0) tma_store_wait_all();
     tc_fence_before();
     cluster_sync();
     if (warp == 1) {
@@ -1322,15 +1286,6 @@ bool make_map(CUtensorMap* map, const void* base, int fmt, int64_t rows, int64_t
     return r == CUDA_SUCCESS;
 }
 
-// TMA-store epilogue of the persistent kernel; TCEC_TMA_STORE = 0 disables (A/B)
-bool tma_store_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("TCEC_TMA_STORE");
-        return !e || std::atoi(e) != 0;
-    }();
-    return on;
-}
-
 bool make_wide_maps(WideMaps* w, const TcecGemmArgs& g, int fmt) {
     const void* alo = g.corrected ? g.a_lo : g.a_hi;
     const void* blo = g.corrected ? g.b_lo : g.b_hi;
@@ -1340,18 +1295,6 @@ bool make_wide_maps(WideMaps* w, const TcecGemmArgs& g, int fmt) {
     const size_t boff = size_t(g.b_row_off) * size_t(g.kp) * (fmt == kFp16 ? 2 : 4);
     const void* bhi = static_cast<const uint8_t*>(g.b_hi) + boff;
     blo = static_cast<const uint8_t*>(blo) + boff;
-    w->tma_c = 0;
-    if (g.pair == kVariantWidePersistent && !g.xa && tma_store_enabled() && g.ldc <= 0 &&
-        (reinterpret_cast<uintptr_t>(g.c) & 15u) == 0 && (g.n2 * 4) % 16 == 0) {
-        // C: n2 x m f32, row stride n2, 32 x 32 boxes (128 B inner), 128-B swizzle
-        cuuint64_t dims[2] = {cuuint64_t(g.n2), cuuint64_t(g.m)};
-        cuuint64_t strides[1] = {cuuint64_t(g.n2) * 4};
-        cuuint32_t box[2] = {32u, 32u};
-        cuuint32_t estr[2] = {1u, 1u};
-        w->tma_c = g_encode(&w->cmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, g.c, dims, strides, box, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-    }
     return make_map(&w->ahi, g.a_hi, fmt, arows, g.kp, 128u) && make_map(&w->alo, alo, fmt, arows, g.kp, 128u) &&
            make_map(&w->bhi, bhi, fmt, g.n2, g.kp, 128u) && make_map(&w->blo, blo, fmt, g.n2, g.kp, 128u) &&
            make_map(&w->bhi_h, bhi, fmt, g.n2, g.kp, 64u) && make_map(&w->blo_h, blo, fmt, g.n2, g.kp, 64u);
