@@ -1384,7 +1384,7 @@ __global__ void __launch_bounds__(256, 2) cgemm_skinny_col_kernel(const float2* 
 // VIEW: A is read through a matrix view of the unpermuted tensor, A(i, kk) =
 // a[view.rows(i) + view.cols(kk)].
 template <bool F64, int MX, bool GROUPED, bool VIEW = false>
-__global__ void __launch_bounds__(256, (MX <= 8 ? 3 : 2)) cgemm_skinny_row_kernel(const float2* __restrict__ a,
+__global__ void __launch_bounds__(256) cgemm_skinny_row_kernel(const float2* __restrict__ a,
                                                                const float2* __restrict__ b,
                                                                float2* __restrict__ c, int64_t m,
                                                                int n, int k, int64_t ldn,
@@ -1421,97 +1421,58 @@ __global__ void __launch_bounds__(256, (MX <= 8 ? 3 : 2)) cgemm_skinny_row_kerne
             if (j < n) __stcs(crow + j, assemble<F64>(p[j]));
         return;
     }
-    // persistent warps walk 32-row blocks; the next 32 x 8 slab's loads are
-    // issued before the current slab's MACs (across row blocks too when k is
-    // a multiple of 8)
     const int lane = threadIdx.x & 31;
-    const int64_t wstep = int64_t(gridDim.x) * blockDim.x;
-    int64_t w0 = int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31);
+    const int64_t w0 = int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31);
     if (w0 >= m) return;  // whole warp past the end
+    const int rows = int(min(int64_t(32), m - w0));
     float2* st = stage + (threadIdx.x >> 5) * 32 * SW;
-    auto row_off = [&](int64_t wb) -> int64_t {  // VIEW: offset of row wb + lane
-        return VIEW && wb + lane < m ? run_offset(view.rows, uint32_t(wb + lane)) : 0;
-    };
-    auto load_slab = [&](int64_t wb, int64_t roff, int kk0, float2 (&v)[8]) {
+    const float2* ablk = a + w0 * k;
+    // VIEW: row offsets of the warp's 32 rows, one per lane (shuffled to the loaders)
+    const int64_t my_roff = VIEW && lane < rows ? run_offset(view.rows, uint32_t(w0 + lane)) : 0;
+    int k0 = 0;
+#pragma unroll 1
+    for (; k0 + 8 <= k; k0 += 8) {
+        float2 v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {  // element e = lane + 32u of the 32 x 8 slab: row e / 8, column e % 8
             const int r = (lane >> 3) + 4 * u;
-            const bool ok = wb + r < m;
             if (VIEW) {
-                const int64_t ro = __shfl_sync(0xFFFFFFFFu, roff, r);
-                v[u] = ok ? __ldcs(a + ro + koff[kk0 + (lane & 7)]) : make_float2(0.0f, 0.0f);
+                const int64_t ro = __shfl_sync(0xFFFFFFFFu, my_roff, r);
+                v[u] = r < rows ? __ldcs(a + ro + koff[k0 + (lane & 7)]) : make_float2(0.0f, 0.0f);
             } else {
-                v[u] = ok ? __ldcs(a + (wb + r) * k + kk0 + (lane & 7)) : make_float2(0.0f, 0.0f);
+                v[u] = r < rows ? __ldcs(ablk + int64_t(r) * k + k0 + (lane & 7)) : make_float2(0.0f, 0.0f);
             }
         }
-    };
-    // prefetching the next slab (PF) needs 16 more registers; measured on
-    // B200 it costs more occupancy than it hides latency for every MX
-    // ((2^24, 8, 8) 0.594 -> 0.636 ms), so each slab loads right before its MACs
-    constexpr bool PF = false;
-    const bool chain_next = PF && (k % 8) == 0 && k >= 8;
-    float2 v[8], vn[8];
-    int64_t roff = row_off(w0);
-    if (PF && k >= 8) load_slab(w0, roff, 0, v);
-#pragma unroll 1
-    for (; w0 < m; w0 += wstep) {
-        const int rows = int(min(int64_t(32), m - w0));
-        const int64_t wn = w0 + wstep;
-        const int64_t roff_n = chain_next && wn < m ? row_off(wn) : 0;
-        acc_t p[MX][4];
 #pragma unroll
-        for (int j = 0; j < MX; ++j) p[j][0] = p[j][1] = p[j][2] = p[j][3] = acc_t(0);
-        int k0 = 0;
-#pragma unroll 1
-        for (; k0 + 8 <= k; k0 += 8) {
-            if (!PF)
-                load_slab(w0, roff, k0, v);
-            else if (k0 + 16 <= k)
-                load_slab(w0, roff, k0 + 8, vn);
-            else if (chain_next && wn < m)
-                load_slab(wn, roff_n, 0, vn);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) st[((lane >> 3) + 4 * u) * SW + (lane & 7)] = v[u];
-            __syncwarp();
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const float2 av = st[lane * SW + q];
-                skinny_mac<F64, MX>(bs + (k0 + q) * MX, av.x, av.y, p, false);
-            }
-            __syncwarp();
-            if (PF) {
-#pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = vn[u];
-            }
-        }
-#pragma unroll 1
-        for (; k0 < k; ++k0) {
-            const float2 av = lane < rows ? __ldcs(VIEW ? a + roff + koff[k0] : a + (w0 + lane) * k + k0)
-                                          : make_float2(0.0f, 0.0f);
-            skinny_mac<F64, MX>(bs + k0 * MX, av.x, av.y, p, false);
-        }
-#pragma unroll
-        for (int j = 0; j < MX; ++j) st[lane * SW + j] = assemble<F64>(p[j]);
+        for (int u = 0; u < 8; ++u) st[((lane >> 3) + 4 * u) * SW + (lane & 7)] = v[u];
         __syncwarp();
-        float2* cblk = c + w0 * ldn;
-        if (n == MX) {
 #pragma unroll
-            for (int u = 0; u < MX; ++u) {
-                const int e = lane + 32 * u, r = e / MX, j = e % MX;
-                if (r < rows) __stcs(cblk + int64_t(r) * ldn + j, st[r * SW + j]);
-            }
-        } else {
-            for (int e = lane; e < rows * n; e += 32) {
-                const int r = e / n, j = e - r * n;
-                __stcs(cblk + int64_t(r) * ldn + j, st[r * SW + j]);
-            }
+        for (int q = 0; q < 8; ++q) {
+            const float2 av = st[lane * SW + q];
+            skinny_mac<F64, MX>(bs + (k0 + q) * MX, av.x, av.y, p, false);
         }
         __syncwarp();
-        if (chain_next) {
-            roff = roff_n;
-        } else {
-            roff = row_off(wn);
-            if (PF && k >= 8 && wn < m) load_slab(wn, roff, 0, v);
+    }
+#pragma unroll 1
+    for (; k0 < k; ++k0) {
+        const float2 av = lane < rows ? __ldcs(VIEW ? a + my_roff + koff[k0] : ablk + int64_t(lane) * k + k0)
+                                      : make_float2(0.0f, 0.0f);
+        skinny_mac<F64, MX>(bs + k0 * MX, av.x, av.y, p, false);
+    }
+#pragma unroll
+    for (int j = 0; j < MX; ++j) st[lane * SW + j] = assemble<F64>(p[j]);
+    __syncwarp();
+    float2* cblk = c + w0 * ldn;
+    if (n == MX) {
+#pragma unroll
+        for (int u = 0; u < MX; ++u) {
+            const int e = lane + 32 * u, r = e / MX, j = e % MX;
+            if (r < rows) __stcs(cblk + int64_t(r) * ldn + j, st[r * SW + j]);
+        }
+    } else {
+        for (int e = lane; e < rows * n; e += 32) {
+            const int r = e / n, j = e - r * n;
+            __stcs(cblk + int64_t(r) * ldn + j, st[r * SW + j]);
         }
     }
 }
@@ -1566,22 +1527,7 @@ void launch_skinny_mx(const float2* a, const float2* b, float2* c, int64_t m, in
                         return cudaFuncSetAttribute(cgemm_skinny_row_kernel<F64, MX, true, VIEW>,
                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, stage_bytes);
                     }) == cudaSuccess) {
-                    static const int per_sm = [] {
-                        int nb = 0;
-                        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                                   &nb, cgemm_skinny_row_kernel<F64, MX, true, VIEW>, 256, stage_bytes) ==
-                                           cudaSuccess && nb > 0
-                                   ? nb
-                                   : 2;
-                    }();
-                    int dev = 0, sms = 148;
-                    cudaGetDevice(&dev);
-                    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-                    // VIEW (gathered rows): one 32-row block per warp measured faster
-                    // than the persistent walk ((2^22, 16, 64): 1.98 vs 1.67 ms)
-                    const int64_t blocks = VIEW ? (m + 255) / 256
-                                                : std::min<int64_t>((m + 255) / 256, int64_t(per_sm) * sms);
-                    cgemm_skinny_row_kernel<F64, MX, true, VIEW><<<unsigned(blocks), 256, stage_bytes, s>>>(
+                    cgemm_skinny_row_kernel<F64, MX, true, VIEW><<<unsigned((m + 255) / 256), 256, stage_bytes, s>>>(
                         a, b + j0, c + j0, m, cols, int(k), n, view);
                     continue;
                 }
