@@ -538,31 +538,54 @@ TCEC_DEV void prep_b_part(const float2* __restrict__ b, int64_t k,
     const double factor = ldexp(1.0, pm.scale);
     const float fs = (pm.scale >= -149 && pm.scale <= 127) ? ldexpf(1.0f, pm.scale) : 1.0f;
     __shared__ __align__(16) float2 tile[kPrepBJ][kPrepBStride];
-    __shared__ int64_t roff_s[VIEW ? kPrepBKK : 1];
+    __shared__ int64_t roff_s[2][VIEW ? kPrepBKK : 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;  // 8 warps
     const int64_t tiles_j = (n + kPrepBJ - 1) / kPrepBJ;
     const int64_t kk_cols = kp / 2;                               // complex K extent incl. padding
     const int64_t tiles_kk = (kk_cols + kPrepBKK - 1) / kPrepBKK;
     const int64_t ntiles = tiles_j * tiles_kk;
     unsigned ovf = 0, bad = 0;
-    for (int64_t t = bid; t < ntiles; t += nblk) {
-        const int64_t j0 = (t % tiles_j) * kPrepBJ, kk0 = (t / tiles_j) * kPrepBKK;
-        // load: warp w reads rows kk0 + w, w+8, ... (32 consecutive j each);
-        // VIEW: B is a view of the unpermuted tensor (fused TTGT gather)
-        const int64_t co = VIEW && j0 + lane < n ? run_offset(view.cols, uint32_t(j0 + lane)) : 0;
-        if (VIEW) {  // the tile's 64 row offsets, one thread each
-            if (threadIdx.x < kPrepBKK)
-                roff_s[threadIdx.x] = kk0 + threadIdx.x < k ? run_offset(view.rows, uint32_t(kk0 + threadIdx.x)) : 0;
-            __syncthreads();
+    // software-pipelined tiles: the next tile's loads are issued (into
+    // registers) before the current tile's conversion and stores, so every
+    // block keeps a tile of reads in flight (one tile at a time left the
+    // kernel latency-bound at ~4 TB/s).  Warp w loads rows kk0 + w, w+8, ...
+    // (32 consecutive j each); VIEW: B is a view of the unpermuted tensor
+    // (fused TTGT gather) whose 64 row offsets per tile are tabled, double
+    // buffered.
+    auto fill_roff = [&](int64_t t, int buf) {
+        if (VIEW && threadIdx.x < kPrepBKK) {
+            const int64_t kk0 = (t / tiles_j) * kPrepBKK;
+            roff_s[buf][threadIdx.x] =
+                kk0 + threadIdx.x < k ? run_offset(view.rows, uint32_t(kk0 + threadIdx.x)) : 0;
         }
+    };
+    auto load_tile = [&](int64_t t, int buf, float2 (&v)[kPrepBKK / 8]) {
+        const int64_t j0 = (t % tiles_j) * kPrepBJ, kk0 = (t / tiles_j) * kPrepBKK;
+        const int64_t gj = j0 + lane;
+        const int64_t co = VIEW && gj < n ? run_offset(view.cols, uint32_t(gj)) : 0;
 #pragma unroll
         for (int r = 0; r < kPrepBKK / 8; ++r) {
-            const int kk = warp + 8 * r;
-            const int64_t gk = kk0 + kk, gj = j0 + lane;
-            const float2* src = VIEW ? b + roff_s[kk] + co : b + gk * n + gj;
-            tile[lane][kk] = (gk < k && gj < n) ? __ldcs(src) : make_float2(0.0f, 0.0f);
+            const int64_t gk = kk0 + warp + 8 * r;
+            const float2* src = VIEW ? b + roff_s[buf][warp + 8 * r] + co : b + gk * n + gj;
+            v[r] = (gk < k && gj < n) ? __ldcs(src) : make_float2(0.0f, 0.0f);
         }
+    };
+    float2 vt[kPrepBKK / 8];
+    int buf = 0;
+    if (int64_t(bid) < ntiles) {
+        fill_roff(bid, 0);
+        if (VIEW) __syncthreads();
+        load_tile(bid, 0, vt);
+    }
+    for (int64_t t = bid; t < ntiles; t += nblk) {
+        const int64_t j0 = (t % tiles_j) * kPrepBJ, kk0 = (t / tiles_j) * kPrepBKK;
+#pragma unroll
+        for (int r = 0; r < kPrepBKK / 8; ++r) tile[lane][warp + 8 * r] = vt[r];
+        const int64_t tn = t + nblk;
+        if (tn < ntiles) fill_roff(tn, buf ^ 1);
         __syncthreads();
+        if (tn < ntiles) load_tile(tn, buf ^ 1, vt);
+        buf ^= 1;
         // write: warp w owns j = j0 + w, w+8, ...; lane owns kk0 + 2 lane, +1
         const int64_t col = 2 * (kk0 + 2 * lane);                 // K' column of (kk0 + 2 lane, re)
         if (col < kp) {
@@ -744,29 +767,54 @@ TCEC_DEV void prep_bx_part(const float2* __restrict__ b, int64_t k,
     const double factor = ldexp(1.0, pm.scale);
     const float fs = (pm.scale >= -149 && pm.scale <= 127) ? ldexpf(1.0f, pm.scale) : 1.0f;
     __shared__ __align__(16) float2 tile[kPrepBJ][kPrepBStride];
-    __shared__ int64_t roff_s[VIEW ? kPrepBKK : 1];
+    __shared__ int64_t roff_s[2][VIEW ? kPrepBKK : 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;  // 8 warps
     const int64_t tiles_j = (n + kPrepBJ - 1) / kPrepBJ;
     const int64_t kk_cols = kp / 2;
     const int64_t tiles_kk = (kk_cols + kPrepBKK - 1) / kPrepBKK;
     const int64_t ntiles = tiles_j * tiles_kk;
     unsigned ovf = 0, bad = 0;
-    for (int64_t t = bid; t < ntiles; t += nblk) {
-        const int64_t j0 = (t % tiles_j) * kPrepBJ, kk0 = (t / tiles_j) * kPrepBKK;
-        const int64_t co = VIEW && j0 + lane < n ? run_offset(view.cols, uint32_t(j0 + lane)) : 0;
-        if (VIEW) {  // the tile's 64 row offsets, one thread each
-            if (threadIdx.x < kPrepBKK)
-                roff_s[threadIdx.x] = kk0 + threadIdx.x < k ? run_offset(view.rows, uint32_t(kk0 + threadIdx.x)) : 0;
-            __syncthreads();
+    // software-pipelined tiles: the next tile's loads are issued (into
+    // registers) before the current tile's conversion and stores, so every
+    // block keeps a tile of reads in flight (one tile at a time left the
+    // kernel latency-bound at ~4 TB/s).  Warp w loads rows kk0 + w, w+8, ...
+    // (32 consecutive j each); VIEW: B is a view of the unpermuted tensor
+    // (fused TTGT gather) whose 64 row offsets per tile are tabled, double
+    // buffered.
+    auto fill_roff = [&](int64_t t, int buf) {
+        if (VIEW && threadIdx.x < kPrepBKK) {
+            const int64_t kk0 = (t / tiles_j) * kPrepBKK;
+            roff_s[buf][threadIdx.x] =
+                kk0 + threadIdx.x < k ? run_offset(view.rows, uint32_t(kk0 + threadIdx.x)) : 0;
         }
+    };
+    auto load_tile = [&](int64_t t, int buf, float2 (&v)[kPrepBKK / 8]) {
+        const int64_t j0 = (t % tiles_j) * kPrepBJ, kk0 = (t / tiles_j) * kPrepBKK;
+        const int64_t gj = j0 + lane;
+        const int64_t co = VIEW && gj < n ? run_offset(view.cols, uint32_t(gj)) : 0;
 #pragma unroll
         for (int r = 0; r < kPrepBKK / 8; ++r) {
-            const int kk = warp + 8 * r;
-            const int64_t gk = kk0 + kk, gj = j0 + lane;
-            const float2* src = VIEW ? b + roff_s[kk] + co : b + gk * n + gj;
-            tile[lane][kk] = (gk < k && gj < n) ? __ldcs(src) : make_float2(0.0f, 0.0f);
+            const int64_t gk = kk0 + warp + 8 * r;
+            const float2* src = VIEW ? b + roff_s[buf][warp + 8 * r] + co : b + gk * n + gj;
+            v[r] = (gk < k && gj < n) ? __ldcs(src) : make_float2(0.0f, 0.0f);
         }
+    };
+    float2 vt[kPrepBKK / 8];
+    int buf = 0;
+    if (int64_t(bid) < ntiles) {
+        fill_roff(bid, 0);
+        if (VIEW) __syncthreads();
+        load_tile(bid, 0, vt);
+    }
+    for (int64_t t = bid; t < ntiles; t += nblk) {
+        const int64_t j0 = (t % tiles_j) * kPrepBJ, kk0 = (t / tiles_j) * kPrepBKK;
+#pragma unroll
+        for (int r = 0; r < kPrepBKK / 8; ++r) tile[lane][warp + 8 * r] = vt[r];
+        const int64_t tn = t + nblk;
+        if (tn < ntiles) fill_roff(tn, buf ^ 1);
         __syncthreads();
+        if (tn < ntiles) load_tile(tn, buf ^ 1, vt);
+        buf ^= 1;
         const int64_t col = 2 * (kk0 + 2 * lane);
         if (col < kp) {
             for (int jj = warp; jj < kPrepBJ; jj += 8) {
