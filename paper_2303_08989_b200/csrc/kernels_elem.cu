@@ -2263,6 +2263,7 @@ static bool make_runs(int a0, int a1, const int64_t* dims, const int64_t* pstrid
 }
 
 bool make_matrix_view(int rank, const int64_t* dims, const int* axis_of, int n_row_axes, MatrixView* v) {
+    if (rank < 0 || rank > kMaxRank || n_row_axes < 0 || n_row_axes > rank) return false;
     int64_t pstride[kMaxRank];
     int64_t acc = 1;
     for (int i = rank - 1; i >= 0; --i) {

@@ -415,3 +415,26 @@ def test_operand_layout_host_buffers(handle):
     cd, res_d = handle.dispatch_cgemm(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev), cfg)
     assert res_h.line == res_d.line
     assert np.array_equal(ch.view(np.uint32), cd.cpu().numpy().view(np.uint32))
+
+
+@pytest.mark.parametrize("shape", [(64, 1000, 33), (300, 257, 200), (512, 2048, 512), (130, 600, 1100)])
+@pytest.mark.parametrize("mode", ["FP16TCEC", "TF32TCEC"])
+def test_operand_layouts_bit_identical(handle, dev, shape, mode):
+    """The two layouts hold the same products at the same K positions: A'(i, 2p)
+    = Ar, A'(i, 2p+1) = Ai against B'(2q, ·) = (Br, -Bi), versus A''(2i, ·) = (Ar,
+    -Ai) against B''(q, ·) = (Br, Bi) -- Ai*(-Bi) and (-Ai)*Bi are the same exact
+    product (the splits are sign-symmetric) -- so the tensor core sums identical
+    terms in identical order: C is bit-identical."""
+    m, n, k = shape
+    a = matrix_recipe("uniform", m, k, 31 + m)
+    b = matrix_recipe("uniform", k, n, 37 + n)
+    ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    outs = {}
+    try:
+        for layout in ("a", "b"):
+            handle.set_operand_layout(layout)
+            c, _ = handle.cgemm(ad, bd, mode)
+            outs[layout] = c.cpu().numpy()
+    finally:
+        handle.set_operand_layout("auto")
+    assert np.array_equal(outs["a"].view(np.uint32), outs["b"].view(np.uint32))
