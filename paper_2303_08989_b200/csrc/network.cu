@@ -226,12 +226,21 @@ static int build_plan(const tcec_network_s& net, const int* steps, int n_steps,
                                              int(A.dims.size()) - sp.n_shared, &sp.view);
         }
         if (sp.dp.tier == kTierTc && view_gather_enabled()) {
+            // only views the preparation kernels read efficiently: A rows along
+            // K in unit-stride runs of >= 4 complex (the 16-B fast path), B
+            // columns in unit-stride runs of >= 32 (a warp's coalesced row);
+            // otherwise the permute (4.4-5.9 TB/s) is cheaper than a scattered gather
+            auto inner_ok = [](const RunMap& r, uint32_t min_ext) {
+                return r.n == 0 || (r.stride[r.n - 1] == 1 && r.ext[r.n - 1] >= min_ext);
+            };
             if (sp.perm_a)
                 sp.tview_a = make_matrix_view(int(A.dims.size()), A.dims.data(), sp.a_axis.data(),
-                                              int(A.dims.size()) - sp.n_shared, &sp.tva);
+                                              int(A.dims.size()) - sp.n_shared, &sp.tva) &&
+                             inner_ok(sp.tva.cols, 4);
             if (sp.perm_b)
                 sp.tview_b = make_matrix_view(int(B.dims.size()), B.dims.data(), sp.b_axis.data(), sp.n_shared,
-                                              &sp.tvb);
+                                              &sp.tvb) &&
+                             inner_ok(sp.tvb.cols, 32);
         }
         if (sp.dp.tier == kTierTc && cfg.k_tile < 1)
             return set_error(TCEC_ERR_INVALID_ARGUMENT, "k_tile must be >= 1");
