@@ -162,9 +162,17 @@ class SlicePlan:
         return cls(spec, list(path), list(sliced), dims, n, var_nodes(spec, sliced), base)
 
     def run_data(self, slice_id: int):
-        """Data of the variable nodes for one slice."""
-        sub = slice_spec(self.spec, self.sliced, assignment(slice_id, self.dims))
-        return [sub.data[i] for i in self.var]
+        """Data of the variable nodes for one slice (the same arrays slice_spec
+        gives them; only the variable nodes are sliced -- fixing the labels of
+        all ~1000 nodes per slice cost 1.7 ms of host time per slice)."""
+        fix = dict(zip(self.sliced, assignment(slice_id, self.dims)))
+        out = []
+        for i in self.var:
+            ls, ds = self.spec.labels[i], self.spec.dims[i]
+            t = np.asarray(self.spec.data[i], dtype=np.complex64).reshape(ds)
+            t = t[tuple(fix[l] if l in fix else slice(None) for l in ls)]
+            out.append(np.ascontiguousarray(t).reshape(-1))
+        return out
 
 
 def ordered_sum(values_by_slice) -> complex:
