@@ -97,3 +97,24 @@ def test_two_rank_gloo_matches_single_rank_bitwise():
     for rank, amp, full in res:
         assert amp == amp1
         assert full == full1.tobytes()
+
+
+def test_run_data_equals_slice_spec_variable_nodes():
+    """SlicePlan.run_data slices only the variable nodes; its arrays equal the
+    variable nodes of the full slice_spec sub-network bit for bit, for every
+    slice, and the other nodes of every slice equal the plan's base."""
+    from paper_2303_08989_b200.slicing import assignment
+    spec, path = _spec(3, 3, 6, 5)
+    sliced = find_slices(spec, path, n_labels=3)
+    plan = SlicePlan.build(spec, path, sliced)
+    assert plan.n_slices > 1
+    var = set(plan.var)
+    for i in range(plan.n_slices):
+        sub = slice_spec(plan.spec, plan.sliced, assignment(i, plan.dims))
+        got = plan.run_data(i)
+        assert len(got) == len(plan.var)
+        for j, g in zip(plan.var, got):
+            assert np.array_equal(g.view(np.uint32), sub.data[j].view(np.uint32))
+        for j in range(len(sub.data)):
+            if j not in var:
+                assert np.array_equal(sub.data[j].view(np.uint32), plan.base.data[j].view(np.uint32))
