@@ -67,7 +67,9 @@ int tcec_get_flush_kblocks(tcec_handle h);
  * SMs, else single), 1 = CTA pair (cta_group::2, 256 x 128 tile), 2 = single
  * CTA (128 x 128 tile), 3 = wide CTA pair (cta_group::2, 256 x 256 tile),
  * 4 = the wide tile on persistent CTA pairs, 5 = the wide tile on clusters of
- * two CTA pairs that share each B' tile by TMA multicast */
+ * two CTA pairs that share each B' tile by TMA multicast, 6 = 256 x 128 tiles
+ * on persistent CTA pairs with two tiles' accumulators in TMEM (one tile's
+ * epilogue overlaps the next tile's MMAs) */
 int tcec_set_gemm_variant(tcec_handle h, int variant);
 /* operand layout of tensor-core dispatches: the complex GEMM runs as one real
  * GEMM in which one operand carries the 2x2 complex block expansion.

@@ -140,7 +140,8 @@ class Handle:
         3 per-step graph preceded by the fused subtree launch (hybrid)."""
         check(self.lib.tcec_set_executor(self.h, int(policy)))
 
-    GEMM_VARIANTS = {"auto": 0, "pair": 1, "single": 2, "wide": 3, "wide_persistent": 4, "wide_mc": 5}
+    GEMM_VARIANTS = {"auto": 0, "pair": 1, "single": 2, "wide": 3, "wide_persistent": 4, "wide_mc": 5,
+                     "pair_persistent": 6}
 
     def set_operand_layout(self, layout) -> None:
         """tcec_set_operand_layout: "auto" (expand the smaller operand), "b" (B' =

@@ -177,7 +177,9 @@ TcecGemmArgs tc_gemm_args(const Handle& h, const DispatchPlan& p, void* ws, floa
         return e ? std::max(0, std::min(64, std::atoi(e))) : 0;
     }();
     g.flush_kblocks = p.corrected ? (h.flush_kblocks | (h.flush_kblocks > 0 ? tf32_flush << 16 : 0)) : 0;
-    g.pair = resolve_gemm_variant(h.gemm_pair, rows_a, rows_b, p.kp, h.sm_count, !xa);  // no A-expanded pair kernel
+    // no A-expanded 256x128 pair kernel; the host-buffer pipeline (allow_xa =
+    // false) needs a kernel that takes row chunks and column blocks
+    g.pair = resolve_gemm_variant(h.gemm_pair, rows_a, rows_b, p.kp, h.sm_count, !xa && allow_xa, allow_xa);
     g.sms = h.sm_count;
     g.fmt = (p.kind < 0 && !p.forced_scaled) ? -1  // format chosen by the device decision
                                              : (p.kind == kKindTf32 ? kTf32 : kFp16);
@@ -500,7 +502,7 @@ int tcec_set_executor(tcec_handle h, int policy) {
 
 int tcec_set_gemm_variant(tcec_handle h, int variant) {
     CHECK_HANDLE(h);
-    if (variant < 0 || variant > 5) return set_error(TCEC_ERR_INVALID_ARGUMENT, "variant must be 0..5");
+    if (variant < 0 || variant > 6) return set_error(TCEC_ERR_INVALID_ARGUMENT, "variant must be 0..6");
     h->gemm_pair = variant;
     return TCEC_OK;
 }
@@ -1130,8 +1132,10 @@ int tcec_dispatch_cgemm_host(tcec_handle h, const void* a, const void* b, void* 
     }();
     const bool pipelined = pipe_chunks > 1 && p.tier == kTierTc && m >= 8192 && n > 0 && k > 0 &&
                            !(h->prof && h->ev[0]) &&
-                           (resolve_gemm_variant(h->gemm_pair, m, 2 * n, p.kp, h->sm_count) == kVariantWide ||
-                            resolve_gemm_variant(h->gemm_pair, m, 2 * n, p.kp, h->sm_count) == kVariantWideMc);
+                           (resolve_gemm_variant(h->gemm_pair, m, 2 * n, p.kp, h->sm_count, false, false) ==
+                                kVariantWide ||
+                            resolve_gemm_variant(h->gemm_pair, m, 2 * n, p.kp, h->sm_count, false, false) ==
+                                kVariantWideMc);
     DevDecision* d = pipelined ? h->decisions(3) : h->dec;
     if (!d) return set_error(TCEC_ERR_CUDA, "decision slots allocation failed");
     if (pipelined) {

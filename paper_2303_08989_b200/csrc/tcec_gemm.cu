@@ -1255,6 +1255,331 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kThreadsGemm, 1)
                             ldc, partial, kb_per, xa);
 }
 
+// ============================================ pair tiles, persistent, 2 buffers
+// Persistent cta_group::2 kernel on 256 x 128 tiles (variant 6) whose two
+// tiles in flight each own half of TMEM: buffer b = main partial (cols 256b +
+// [0,128)) + correction accumulator (256b + 128 + [0,128)).  The epilogue
+// warps form two sets, set b drains and stores the tiles of buffer b, so one
+// tile's correction drain and C store overlap the next tile's MMAs -- with the
+// 256 x 256 tile the whole of TMEM holds one tile and the next tile's main
+// products wait for the store (tensor pipe ~30 % busy at 4 k-blocks per tile,
+// ~77 % at 32).  The main term is drained (RN-added) every flush interval as
+// in the other kernels, while the tensor core runs the correction products of
+// the same k-block.  Each warp stores its 32 x 128 block through a private
+// 32 x 64 smem stage (two halves), no barrier across warps.
+constexpr int kP2Stages = 3;
+constexpr int kP2BN = 128;
+constexpr int kP2ATile = 128 * 128;  // 128 rows x 128 B
+constexpr int kP2BTile = 64 * 128;   // 64 rows x 128 B (this CTA's half of the pair's 128 B' rows)
+constexpr int kP2StageBytes = 2 * kP2ATile + 2 * kP2BTile;
+constexpr int kP2CStride = 68;       // padded staging row (floats): 64 columns
+constexpr size_t kP2WarpStage = size_t(32) * kP2CStride * 4;
+struct alignas(8) P2SmemTail {
+    uint64_t full[kP2Stages];
+    uint64_t empty[kP2Stages];
+    uint64_t tfull[2], tempty[2], cfull[2], cempty[2];
+    uint32_t tmem_base;
+};
+constexpr size_t kP2SmemBytes =
+    1024 + size_t(kP2Stages) * kP2StageBytes + size_t(kEpiWarps) * kP2WarpStage + sizeof(P2SmemTail);
+static_assert(kP2SmemBytes <= 232448, "exceeds the 227 KB dynamic shared memory of sm_100");
+
+template <int FMT>
+__device__ __forceinline__ void pairp_body(const WideMaps& mp, float* __restrict__ c, int m, int n2, int kp,
+                                           const DevDecision* __restrict__ dec, int kind, int corrected,
+                                           int flush_kblocks, int xa) {
+    using T = Traits<FMT>;
+    constexpr uint32_t kIdesc = umma_idesc<FMT, 2 * BM, kP2BN>();
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    float* cstage = reinterpret_cast<float*>(smem + size_t(kP2Stages) * kP2StageBytes);
+    P2SmemTail* tail = reinterpret_cast<P2SmemTail*>(smem + size_t(kP2Stages) * kP2StageBytes +
+                                                     size_t(kEpiWarps) * kP2WarpStage);
+    auto a_tile = [&](int st, int lo) -> uint8_t* {
+        return smem + size_t(st) * kP2StageBytes + size_t(lo) * kP2ATile;
+    };
+    auto b_tile = [&](int st, int lo) -> uint8_t* {
+        return smem + size_t(st) * kP2StageBytes + 2 * kP2ATile + size_t(lo) * kP2BTile;
+    };
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+
+    const int tiles_m = (m + 2 * BM - 1) / (2 * BM), tiles_n = (n2 + kP2BN - 1) / kP2BN;
+    const int ntiles = tiles_m * tiles_n;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int group = kWideGroupM * tiles_n;
+    auto tile_coords = [&](int t, int& m_blk, int& n_blk) {
+        const int first_m = (t / group) * kWideGroupM;
+        const int gsize = min(tiles_m - first_m, kWideGroupM);
+        m_blk = first_m + (t % group) % gsize;
+        n_blk = (t % group) / gsize;
+    };
+
+    const int nkb = kp / T::kBK;
+    const int F = flush_of(flush_kblocks, FMT) > 0 ? flush_of(flush_kblocks, FMT) : nkb;
+    const int nchunks = (nkb + F - 1) / F;
+    const uint32_t cta_bytes = corrected ? uint32_t(kP2StageBytes) : uint32_t(kP2ATile + kP2BTile);
+
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < kP2Stages; ++st) {
+            mbar_init(&tail->full[st], 1);
+            mbar_init(&tail->empty[st], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tail->tfull[b], 1);
+            mbar_init(&tail->tempty[b], 2 * (kEpiWarps / 2));  // one set: 4 warps in each CTA
+            mbar_init(&tail->cfull[b], 1);
+            mbar_init(&tail->cempty[b], 2 * (kEpiWarps / 2));
+        }
+        fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&mp.ahi);
+        tma_prefetch(&mp.bhi_h);
+        if (corrected) {
+            tma_prefetch(&mp.alo);
+            tma_prefetch(&mp.blo_h);
+        }
+    }
+    if (warp == 1) tmem_alloc_pair<kTmemCols>(&tail->tmem_base);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = tail->tmem_base;
+
+    if (warp == 0) {
+        // -------------------------------------------- TMA producer (both CTAs)
+        if (lane == 0) {
+            int it = 0;
+            for (int t = pair; t < ntiles; t += npairs) {
+                int m_blk, n_blk;
+                tile_coords(t, m_blk, n_blk);
+                const int m0 = m_blk * 2 * BM + int(rank) * BM;
+                const int nb0 = n_blk * kP2BN + 64 * int(rank);
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int st = it % kP2Stages;
+                    mbar_wait(&tail->empty[st], ((it / kP2Stages) & 1) ^ 1);
+                    if (leader) mbar_expect_tx(&tail->full[st], 2 * cta_bytes);
+                    const int kx = kb * T::kBK;
+                    tma_load_2d_pair(a_tile(st, 0), &mp.ahi, &tail->full[st], kx, m0);
+                    tma_load_2d_pair(b_tile(st, 0), &mp.bhi_h, &tail->full[st], kx, nb0);
+                    if (corrected) {
+                        tma_load_2d_pair(a_tile(st, 1), &mp.alo, &tail->full[st], kx, m0);
+                        tma_load_2d_pair(b_tile(st, 1), &mp.blo_h, &tail->full[st], kx, nb0);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------------------------------- MMA issuer (pair leader only)
+        if (leader) {
+            int it = 0, lt = 0;
+            int mcount[2] = {0, 0}, ccount[2] = {0, 0};  // main chunks / tiles issued per buffer
+            for (int t = pair; t < ntiles; t += npairs, ++lt) {
+                const int b = lt & 1;
+                const uint32_t d_main = tmem + uint32_t(256 * b);
+                const uint32_t d_corr = d_main + 128u;
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const bool chunk_start = (kb % F) == 0;
+                    const bool chunk_end = (kb % F) == F - 1 || kb == nkb - 1;
+                    const int st = it % kP2Stages;
+                    mbar_wait(&tail->full[st], (it / kP2Stages) & 1);
+                    tc_fence_after();
+                    if (chunk_start && mcount[b] > 0) {  // the previous partial of this buffer was drained
+                        mbar_wait(&tail->tempty[b], (mcount[b] - 1) & 1);
+                        tc_fence_after();
+                    }
+                    const uint64_t dah = umma_desc_k_sw128(a_tile(st, 0));
+                    const uint64_t dal = umma_desc_k_sw128(a_tile(st, 1));
+                    const uint64_t dbh = umma_desc_k_sw128(b_tile(st, 0));
+                    const uint64_t dbl = umma_desc_k_sw128(b_tile(st, 1));
+                    if (elect_one()) {
+#pragma unroll
+                        for (int ks = 0; ks < T::kKSteps; ++ks) {
+                            const uint64_t adv = uint64_t((ks * T::kUK * T::kElem) >> 4);
+                            const uint32_t acc = (!chunk_start || ks > 0) ? 1u : 0u;
+                            if (FMT == kFp16)
+                                mma2_f16(d_main, dah + adv, dbh + adv, kIdesc, acc);
+                            else
+                                mma2_tf32(d_main, dah + adv, dbh + adv, kIdesc, acc);
+                        }
+                        if (chunk_end) mma_commit_pair(&tail->tfull[b], 0x3);
+                    }
+                    __syncwarp();
+                    if (chunk_end) ++mcount[b];
+                    if (kb == 0 && ccount[b] > 0) {  // this buffer's previous correction was read
+                        mbar_wait(&tail->cempty[b], (ccount[b] - 1) & 1);
+                        tc_fence_after();
+                    }
+                    if (elect_one()) {
+                        if (corrected) {
+#pragma unroll
+                            for (int ks = 0; ks < T::kKSteps; ++ks) {
+                                const uint64_t adv = uint64_t((ks * T::kUK * T::kElem) >> 4);
+                                const uint32_t acc = (kb > 0 || ks > 0) ? 1u : 0u;
+                                if (FMT == kFp16) {
+                                    mma2_f16(d_corr, dal + adv, dbh + adv, kIdesc, acc);
+                                    mma2_f16(d_corr, dah + adv, dbl + adv, kIdesc, 1u);
+                                } else {
+                                    mma2_tf32(d_corr, dal + adv, dbh + adv, kIdesc, acc);
+                                    mma2_tf32(d_corr, dah + adv, dbl + adv, kIdesc, 1u);
+                                }
+                            }
+                        }
+                        mma_commit_pair(&tail->empty[st], 0x3);
+                        if (kb == nkb - 1) mma_commit_pair(&tail->cfull[b], 0x3);
+                    }
+                    __syncwarp();
+                }
+                ++ccount[b];
+            }
+        }
+    } else {
+        // -------------------------------- epilogue: set e = (warp - 2) / 4 (both CTAs)
+        const int q = warp & 3;
+        const int e = (warp - 2) >> 2;
+        const uint32_t lane_base = tmem + (uint32_t(32 * q) << 16) + uint32_t(256 * e);
+        const uint32_t tempty_leader = mapa_shared(smem_u32(&tail->tempty[e]), 0);
+        const uint32_t cempty_leader = mapa_shared(smem_u32(&tail->cempty[e]), 0);
+        const bool scaled = kind == kKindFp16Scaled && (dec->scale_a + dec->scale_b) != 0;
+        const double f = scaled ? ldexp(1.0, -(dec->scale_a + dec->scale_b)) : 1.0;
+        float* wst = cstage + size_t(warp - 2) * (kP2WarpStage / 4);  // this warp's private stage
+        int mc = 0, cc = 0, lt = e;
+        for (int t = pair + e * npairs; t < ntiles; t += 2 * npairs, lt += 2) {
+            int m_blk, n_blk;
+            tile_coords(t, m_blk, n_blk);
+            float acc[128];
+#pragma unroll
+            for (int i = 0; i < 128; ++i) acc[i] = -0.0f;  // RN identity
+            for (int ch = 0; ch < nchunks; ++ch, ++mc) {
+                mbar_wait(&tail->tfull[e], mc & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int cb = 0; cb < 8; ++cb) {
+                    float v[16];
+                    tmem_ld16(lane_base + uint32_t(16 * cb), v);
+                    if (cb == 7) {  // the partial is in registers: hand the buffer back
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_cluster(tempty_leader);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) acc[16 * cb + i] = __fadd_rn(acc[16 * cb + i], v[i]);
+                }
+            }
+            mbar_wait(&tail->cfull[e], cc & 1);
+            ++cc;
+            tc_fence_after();
+            if (corrected) {
+#pragma unroll
+                for (int cb = 0; cb < 8; ++cb) {
+                    float v[16];
+                    tmem_ld16(lane_base + 128u + uint32_t(16 * cb), v);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        float& a = acc[16 * cb + i];
+                        a = __fadd_rn(a, __fmul_rn(v[i], 0x1.0p-11f));
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(cempty_leader);
+            if (scaled) {
+#pragma unroll
+                for (int i = 0; i < 128; ++i) acc[i] = scale_pow2(acc[i], f);
+            }
+            // store this warp's 32 rows x 128 columns, 64 columns at a time
+            const int r0 = m_blk * 2 * BM + int(rank) * BM + 32 * q;  // first GEMM row of the warp
+            const int n0 = n_blk * kP2BN;
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                const int c0 = n0 + 64 * hh;
+                const bool full_cols = c0 + 64 <= n2 && (n2 & 3) == 0;
+#pragma unroll
+                for (int i = 0; i < 64; i += 4)
+                    *reinterpret_cast<float4*>(wst + size_t(lane) * kP2CStride + i) =
+                        make_float4(acc[64 * hh + i], acc[64 * hh + i + 1], acc[64 * hh + i + 2],
+                                    acc[64 * hh + i + 3]);
+                __syncwarp();
+                if (xa) {
+                    // A-expanded layout: stage rows 2i / 2i+1 = Re / Im of C row (r0 + 2i) / 2; two C rows
+                    // per instruction (lanes 0-15 / 16-31), each lane interleaves 4 columns into 32 B
+                    const int rsub = lane >> 4, cl = 4 * (lane & 15);
+                    for (int i = 0; i < 16; i += 2) {
+                        const int ii = i + rsub;
+                        if (r0 + 2 * ii >= m) continue;
+                        float* dst = c + size_t((r0 + 2 * ii) / 2) * (2 * size_t(n2)) + 2 * size_t(c0);
+                        const float* s0 = wst + size_t(2 * ii) * kP2CStride;
+                        const float* s1 = s0 + kP2CStride;
+                        if (full_cols) {
+                            const float4 re = *reinterpret_cast<const float4*>(s0 + cl);
+                            const float4 im = *reinterpret_cast<const float4*>(s1 + cl);
+                            float4* d4 = reinterpret_cast<float4*>(dst + 2 * cl);
+                            __stcs(d4, make_float4(re.x, im.x, re.y, im.y));
+                            __stcs(d4 + 1, make_float4(re.z, im.z, re.w, im.w));
+                        } else {
+                            for (int j = cl; j < cl + 4; ++j)
+                                if (c0 + j < n2) {
+                                    dst[2 * j] = s0[j];
+                                    dst[2 * j + 1] = s1[j];
+                                }
+                        }
+                    }
+                } else {
+                    // two rows per instruction: lanes 0-15 row 2i, 16-31 row 2i+1, 16 B each
+                    const int rsub = lane >> 4, cl = 4 * (lane & 15);
+                    for (int i = 0; i < 16; ++i) {
+                        const int r = 2 * i + rsub;
+                        if (r0 + r >= m) continue;
+                        float* dst = c + size_t(r0 + r) * n2 + c0;
+                        const float* srow = wst + size_t(r) * kP2CStride;
+                        if (full_cols) {
+                            __stcs(reinterpret_cast<float4*>(dst + cl), *reinterpret_cast<const float4*>(srow + cl));
+                        } else {
+                            for (int j = cl; j < cl + 4; ++j)
+                                if (c0 + j < n2) dst[j] = srow[j];
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_pair<kTmemCols>(tmem);
+    }
+}
+
+template <int FMT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
+    tcec_gemm_pairp_kernel(const __grid_constant__ WideMaps maps, float* __restrict__ c, int m, int n2, int kp,
+                           const DevDecision* __restrict__ dec, int kind_fixed, int corrected,
+                           int flush_kblocks, int xa) {
+    const int kind = kind_fixed >= 0 ? kind_fixed : dec->kind;
+    const bool mine = FMT == kTf32 ? kind == kKindTf32 : (kind == kKindFp16 || kind == kKindFp16Scaled);
+    if (!mine) return;
+    pairp_body<FMT>(maps, c, m, n2, kp, dec, kind, corrected, flush_kblocks, xa);
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsGemm, 1)
+    tcec_gemm_pairp_auto_kernel(const __grid_constant__ WideMaps maps16, const __grid_constant__ WideMaps maps32,
+                                float* __restrict__ c, int m, int n2, int kp, const DevDecision* __restrict__ dec,
+                                int corrected, int flush_kblocks, int xa) {
+    const int kind = dec->kind;
+    if (kind == kKindTf32)
+        pairp_body<kTf32>(maps32, c, m, n2, kp, dec, kind, corrected, flush_kblocks, xa);
+    else if (kind == kKindFp16 || kind == kKindFp16Scaled)
+        pairp_body<kFp16>(maps16, c, m, n2, kp, dec, kind, corrected, flush_kblocks, xa);
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
 
@@ -1326,6 +1651,13 @@ unsigned wide_grid(const TcecGemmArgs& g) {
     return unsigned(2 * pairs);
 }
 
+// persistent 256 x 128 pairs: one pair per two SMs, never more pairs than tiles
+unsigned pairp_grid(const TcecGemmArgs& g) {
+    const int64_t tiles = ((g.m + 2 * BM - 1) / (2 * BM)) * ((g.n2 + kP2BN - 1) / kP2BN);
+    const int64_t pairs = std::max<int64_t>(1, std::min<int64_t>(tiles, (g.sms > 1 ? g.sms : 148) / 2));
+    return unsigned(2 * pairs);
+}
+
 template <int FMT>
 int launch_fmt(const TcecGemmArgs& g, cudaStream_t s) {
     static std::atomic<uint64_t> attr_set{0};
@@ -1345,9 +1677,19 @@ int launch_fmt(const TcecGemmArgs& g, cudaStream_t s) {
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(tcec_gemm_widemc_kernel<FMT>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNpSmemBytes));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(tcec_gemm_pairp_kernel<FMT>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(kP2SmemBytes));
         return e;
     });
     if (ea != cudaSuccess) return int(ea);
+    if (g.pair == kVariantPairPersistent) {
+        WideMaps w;
+        if (!make_wide_maps(&w, g, FMT)) return int(cudaErrorInvalidValue);
+        tcec_gemm_pairp_kernel<FMT><<<pairp_grid(g), kThreadsGemm, kP2SmemBytes, s>>>(
+            w, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.kind_fixed, g.corrected, g.flush_kblocks, g.xa);
+        return int(cudaGetLastError());
+    }
     if (g.pair == kVariantWide || g.pair == kVariantWidePersistent || g.pair == kVariantWideMc) {
         WideMaps w;
         if (!make_wide_maps(&w, g, FMT)) return int(cudaErrorInvalidValue);
@@ -1401,13 +1743,19 @@ int launch_wide_auto(const TcecGemmArgs& g, cudaStream_t s) {
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(tcec_gemm_widemc_auto_kernel,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNpSmemBytes));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(tcec_gemm_pairp_auto_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(kP2SmemBytes));
         return e;
     });
     if (ea != cudaSuccess) return int(ea);
     WideMaps w16, w32;
     if (!make_wide_maps(&w16, g, kFp16) || !make_wide_maps(&w32, g, kTf32))
         return int(cudaErrorInvalidValue);
-    if (g.pair == kVariantWideMc)
+    if (g.pair == kVariantPairPersistent)
+        tcec_gemm_pairp_auto_kernel<<<pairp_grid(g), kThreadsGemm, kP2SmemBytes, s>>>(
+            w16, w32, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.corrected, g.flush_kblocks, g.xa);
+    else if (g.pair == kVariantWideMc)
         tcec_gemm_widemc_auto_kernel<<<dim3(wide_tiles_grid(g), unsigned(g.partial ? g.splits : 1)),
                                        kThreadsGemm, kNpSmemBytes, s>>>(
             w16, w32, g.c, int(g.m), int(g.n2), int(g.kp), g.d, g.corrected, g.flush_kblocks,
@@ -1425,17 +1773,24 @@ int launch_wide_auto(const TcecGemmArgs& g, cudaStream_t s) {
 
 }  // namespace
 
-int resolve_gemm_variant(int requested, int64_t m, int64_t n2, int64_t kp, int sm_count, bool allow_pair) {
+int resolve_gemm_variant(int requested, int64_t m, int64_t n2, int64_t kp, int sm_count, bool allow_pair,
+                         bool allow_pairp) {
     if (requested != kVariantAuto) return requested;
     const int64_t wide_ctas = 2 * ((m + 2 * BM - 1) / (2 * BM)) * ((n2 + kWideBN - 1) / kWideBN);
     // too few 256 x 256 tiles and a K too short to split: the 256 x 128 pair
     // tiles double the CTAs at ~0.9 of the wide tile's MMA efficiency --
     // 1024^3 TF32TCEC 58 (single) -> 42 us, 768^3 46 -> 34 us
     if (allow_pair && wide_ctas < sm_count && kp / 64 < 64) return kVariantPair;
-    // the 256 x 256 tiles fill the SMs, or K is long enough for split-K to fill
-    // them; with <= 8 k-blocks per tile the persistent pairs win (the next
-    // tile's loads and first MMAs overlap the epilogue: 2048x16384x64 TF32
-    // 0.176 -> 0.154 ms)
+    // the 256 x 256 tiles fill the SMs and K is short (<= 512 K' elements):
+    // persistent 256 x 128 pairs with two tiles' accumulators in TMEM, so one
+    // tile's epilogue overlaps the next tile's MMAs ((2048, 16384, 64) TF32
+    // 0.164 -> 0.126 ms, (2048, 4096, 32) 0.045 -> 0.035); also up to 1024 K'
+    // when the 256 x 256 tiles come in few waves ((512, 16384, 512) TF32 0.159
+    // -> 0.147, FP16 0.102 -> 0.085) -- with longer K or many tiles the wide
+    // tile's lower operand traffic per MAC wins (profiles/r02_pairp_ab.log)
+    const int64_t half_sms = std::max(1, sm_count / 2);
+    if (allow_pairp && wide_ctas >= sm_count && (kp / 64 <= 8 || (kp / 64 <= 16 && wide_ctas / 2 < 8 * half_sms)))
+        return kVariantPairPersistent;
     if (wide_ctas >= sm_count && kp / 64 <= 8) return kVariantWidePersistent;
     return (wide_ctas >= sm_count || kp / 64 >= 256) ? kVariantWide : kVariantSingle;
 }
@@ -1530,7 +1885,8 @@ static int launch_formats(const TcecGemmArgs& g, cudaStream_t s) {
     if (g.fmt < 0) {
         // device-decided format: the wide kernel branches on the decision; the
         // other variants launch both formats and the unselected one exits
-        if (g.pair == kVariantWide || g.pair == kVariantWidePersistent || g.pair == kVariantWideMc)
+        if (g.pair == kVariantWide || g.pair == kVariantWidePersistent || g.pair == kVariantWideMc ||
+            g.pair == kVariantPairPersistent)
             return launch_wide_auto(g, s);
         const int e = launch_fmt<kFp16>(g, s);
         return e ? e : launch_fmt<kTf32>(g, s);

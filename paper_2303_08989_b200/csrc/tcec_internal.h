@@ -149,9 +149,11 @@ struct TcecGemmArgs {
 // tcgen05 kernel variants (tcec_set_gemm_variant): auto picks wide when its
 // 256 x 256 pair tiles fill the SMs, else single
 enum GemmVariant : int { kVariantAuto = 0, kVariantPair = 1, kVariantSingle = 2, kVariantWide = 3, kVariantWidePersistent = 4,
-                         kVariantWideMc = 5 };
+                         kVariantWideMc = 5, kVariantPairPersistent = 6 };
+// allow_pair / allow_pairp = false: only the variants that take row chunks and
+// column blocks (the host-buffer pipeline) or the B-expanded layout
 int resolve_gemm_variant(int requested, int64_t m, int64_t n2, int64_t kp, int sm_count,
-                         bool allow_pair = true);
+                         bool allow_pair = true, bool allow_pairp = true);
 // returns a cudaError_t
 int launch_tcec_gemm(const TcecGemmArgs& args, cudaStream_t s);
 

@@ -87,7 +87,7 @@ def test_tcec_ragged_shapes(handle, orc, dev, shape):
         assert e <= max(TOL_FACTOR * err_ref, 2e-7), (mode, e, err_ref)
 
 
-@pytest.mark.parametrize("variant", ["single", "pair", "wide", "wide_persistent", "wide_mc"])
+@pytest.mark.parametrize("variant", ["single", "pair", "wide", "wide_persistent", "wide_mc", "pair_persistent"])
 @pytest.mark.parametrize("shape", [(3, 5, 7), (129, 65, 200), (300, 257, 31), (513, 385, 129),
                                    (130, 130, 1100), (600, 300, 2100)])
 def test_tcec_kernel_variants(handle, orc, dev, variant, shape):
@@ -114,7 +114,7 @@ def test_tcec_kernel_variants(handle, orc, dev, variant, shape):
         assert errs["FP16TC"] >= 10 * errs["FP16TCEC"], errs
 
 
-@pytest.mark.parametrize("variant", ["single", "wide", "wide_persistent", "wide_mc"])
+@pytest.mark.parametrize("variant", ["single", "wide", "wide_persistent", "wide_mc", "pair_persistent"])
 def test_tcec_all_positive_long_k(handle, orc, dev, variant):
     """All-positive operands make tensor-core truncation a systematic bias;
     the per-k-block RN flush keeps TCEC within the reference bar."""
@@ -351,7 +351,7 @@ def test_multicast_clusters_bit_identical_to_pairs(handle, dev, shape, mode):
     assert np.array_equal(outs["wide"].view(np.uint32), outs["wide_mc"].view(np.uint32)), lines["wide"]
 
 
-@pytest.mark.parametrize("variant", ["auto", "single", "wide", "wide_persistent", "wide_mc"])
+@pytest.mark.parametrize("variant", ["auto", "single", "wide", "wide_persistent", "wide_mc", "pair_persistent"])
 @pytest.mark.parametrize("shape", [(3, 5, 7), (64, 1000, 33), (129, 65, 200), (130, 600, 1100),
                                    (256, 4096, 64), (200, 150, 9000), (512, 2048, 512), (1, 300, 40)])
 def test_operand_layouts(handle, orc, dev, variant, shape):
@@ -438,3 +438,35 @@ def test_operand_layouts_bit_identical(handle, dev, shape, mode):
     finally:
         handle.set_operand_layout("auto")
     assert np.array_equal(outs["a"].view(np.uint32), outs["b"].view(np.uint32))
+
+
+@pytest.mark.parametrize("shape", [(512, 256, 64), (1024, 1000, 333), (2048, 512, 100), (768, 2048, 64),
+                                   (4096, 2048, 512), (300, 5000, 40)])
+@pytest.mark.parametrize("mode", ["FP16TCEC", "TF32TCEC", "AUTO", "SCALED"])
+def test_pair_persistent_bit_identical_to_wide(handle, dev, shape, mode):
+    """The persistent 256x128 pairs (two tiles' accumulators in TMEM) run the
+    same MMA sequence per output as the 256x256 kernels -- the same k-blocks,
+    the same RN flush per k-block, the same correction sum -- so C is
+    bit-identical (no split-K on these shapes), ragged edges, the
+    device-decided format and the descaled kind included."""
+    m, n, k = shape
+    a = matrix_recipe("uniform", m, k, 11 + m)
+    b = matrix_recipe("uniform", k, n, 13 + n)
+    if mode == "SCALED":
+        a = (a * np.float32(2.0 ** -20)).astype(np.complex64)
+    ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    if mode in ("AUTO", "SCALED"):
+        cfg = make_config(SelectionPolicy(size_auto=32, size_tf32=16))
+    else:
+        cfg = make_config(force=mode)
+    outs, lines = {}, {}
+    for variant in ("wide_persistent", "pair_persistent"):
+        handle.set_gemm_variant(variant)
+        try:
+            c, res = handle.dispatch_cgemm(ad, bd, cfg)
+            outs[variant] = c.cpu().numpy()
+            lines[variant] = res.line
+        finally:
+            handle.set_gemm_variant("auto")
+    assert lines["wide_persistent"] == lines["pair_persistent"]
+    assert np.array_equal(outs["wide_persistent"].view(np.uint32), outs["pair_persistent"].view(np.uint32))
