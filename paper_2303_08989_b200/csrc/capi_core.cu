@@ -223,8 +223,8 @@ int launch_dispatch(Handle& h, const float* a, const float* b, float* c, int64_t
     if (p.stats) {
         launch_stats1(a, 2 * m * k, b, 2 * k * n, d, s);
         const double t = p.forced_scaled ? 1.0 : cfg.threshold_t;
-        launch_stats2(a, 2 * m * k, b, 2 * k * n, d, t, cfg.target_max_exponent, 0, s);
-        launch_select(d, cfg.threshold_t, cfg.target_max_exponent, p.forced_scaled ? 1 : 0, s);
+        launch_stats2(a, 2 * m * k, b, 2 * k * n, d, t, cfg.target_max_exponent, 0, s, 1, cfg.threshold_t,
+                      p.forced_scaled ? 1 : 0);
     }
     if (prof) cudaEventRecord(h.ev[1], s);
     if (m == 0 || n == 0 || k == 0 || p.tier != kTierTc) {
@@ -976,8 +976,8 @@ static int host_pipeline(Handle& h, const uint8_t* a, const uint8_t* b, uint8_t*
     const int64_t bfront = k * std::min(n, j0_of(hp.front));  // the packed front parts
     if (p.stats) {
         launch_stats1(fa, 2 * rows0 * k, fb, 2 * bfront, ds, s);
-        launch_stats2(fa, 2 * rows0 * k, fb, 2 * bfront, ds, t, cfg.target_max_exponent, 0, s);
-        launch_select(ds, cfg.threshold_t, cfg.target_max_exponent, p.forced_scaled ? 1 : 0, s);
+        launch_stats2(fa, 2 * rows0 * k, fb, 2 * bfront, ds, t, cfg.target_max_exponent, 0, s, 1,
+                      cfg.threshold_t, p.forced_scaled ? 1 : 0);
         cudaMemcpyAsync(snap, ds, sizeof(DevDecision), cudaMemcpyDeviceToDevice, s);
     }
     TcecGemmArgs g = tc_gemm_args(h, p, ws, reinterpret_cast<float*>(dc), m, n, ds, false);
@@ -1033,8 +1033,8 @@ static int host_pipeline(Handle& h, const uint8_t* a, const uint8_t* b, uint8_t*
     if (p.stats) {
         cudaMemsetAsync(dr, 0, sizeof(DevDecision), s);
         launch_stats1(fa, 2 * m * k, fb, 2 * k * n, dr, s);
-        launch_stats2(fa, 2 * m * k, fb, 2 * k * n, dr, t, cfg.target_max_exponent, 0, s);
-        launch_select(dr, cfg.threshold_t, cfg.target_max_exponent, p.forced_scaled ? 1 : 0, s);
+        launch_stats2(fa, 2 * m * k, fb, 2 * k * n, dr, t, cfg.target_max_exponent, 0, s, 1, cfg.threshold_t,
+                      p.forced_scaled ? 1 : 0);
     }
     CUDA_TRY(cudaEventRecord(ev_sync, h.gemm_stream2));  // s covers the second GEMM stream
     CUDA_TRY(cudaStreamWaitEvent(s, ev_sync, 0));

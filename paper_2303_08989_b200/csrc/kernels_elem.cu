@@ -5,10 +5,11 @@
 // Reference mapping (KernelTable, proj/include/mpsgemm/kernels.hpp:20-63):
 //   quantize_buf / split_buf / scale_buf / add_buf / sub_buf -> *_kernel below
 //   abs_stats + count_abs_ge (stage1/stage2, precsel.cpp:23-45) -> stats1/stats2
-//   matrix_tolerance + select_mode (precsel.cpp:106-135)      -> select_kernel
+//   matrix_tolerance + select_mode (precsel.cpp:106-135)      -> select_body (stats2's last block)
 //   gemm_rows_rn (+ cgemm.cpp assembly)                        -> cgemm_fp32_ref_kernel
 //   gemm_rows_f64                                               -> cgemm_fp64_kernel
 //   permute (tensor.hpp:56-105)                                 -> permute_kernel
+#include <cstdlib>
 #include <type_traits>
 
 #include "tcec_common.cuh"
@@ -166,7 +167,10 @@ TCEC_DEV unsigned block_max(unsigned v, unsigned* red) {
 // no longer idles half the grid), and every thread keeps four independent
 // 16-B loads in flight (these sweeps were latency-bound at mid sizes).
 template <typename Visit>
-TCEC_DEV void sweep_operand(const float* __restrict__ x, int64_t n, int part, int nparts, Visit&& visit) {
+TCEC_DEV void sweep_operand(const float* __restrict__ x, int64_t n, int part, int nparts, bool keep, Visit&& visit) {
+    // keep: normal L2 policy (the next sweep / the preparation re-reads an
+    // operand that fits in L2); else evict-first streaming loads
+    auto ld = [keep](const float4* p) { return keep ? __ldg(p) : __ldcs(p); };
     const bool vec = (reinterpret_cast<uintptr_t>(x) & 15u) == 0;
     const int64_t n4 = vec ? n / 4 : 0;
     const int64_t per = (n4 + nparts - 1) / nparts;
@@ -175,15 +179,14 @@ TCEC_DEV void sweep_operand(const float* __restrict__ x, int64_t n, int part, in
     const int bd = int(blockDim.x);
     int64_t i = b0 + threadIdx.x;
     for (; i + 3 * bd < b1; i += 4 * bd) {
-        const float4 v0 = __ldcs(x4 + i), v1 = __ldcs(x4 + i + bd), v2 = __ldcs(x4 + i + 2 * bd),
-                     v3 = __ldcs(x4 + i + 3 * bd);
+        const float4 v0 = ld(x4 + i), v1 = ld(x4 + i + bd), v2 = ld(x4 + i + 2 * bd), v3 = ld(x4 + i + 3 * bd);
         visit(v0.x); visit(v0.y); visit(v0.z); visit(v0.w);
         visit(v1.x); visit(v1.y); visit(v1.z); visit(v1.w);
         visit(v2.x); visit(v2.y); visit(v2.z); visit(v2.w);
         visit(v3.x); visit(v3.y); visit(v3.z); visit(v3.w);
     }
     for (; i < b1; i += bd) {
-        const float4 v = __ldcs(x4 + i);
+        const float4 v = ld(x4 + i);
         visit(v.x); visit(v.y); visit(v.z); visit(v.w);
     }
     if (part == nparts - 1)  // scalar tail (and the whole operand when unaligned)
@@ -194,7 +197,7 @@ TCEC_DEV void sweep_operand(const float* __restrict__ x, int64_t n, int part, in
 // nonzero count, count of |x| >= 2^-14, max |x|
 // (block `bid` of `nblk`: blocks [0, nb_a) sweep A, the rest B)
 TCEC_DEV void stats1_part(const float* a, int64_t na, const float* b, int64_t nb, DevDecision* d,
-                          int nb_a, int bid, int nblk) {
+                          int nb_a, int bid, int nblk, bool keep) {
     const int op = bid < nb_a ? 0 : 1;
     const float* x = op ? b : a;
     const int64_t n = op ? nb : na;
@@ -202,7 +205,7 @@ TCEC_DEV void stats1_part(const float* a, int64_t na, const float* b, int64_t nb
     const int nparts = op ? nblk - nb_a : nb_a;
     if (x == nullptr || n == 0 || nparts <= 0) return;
     unsigned nz = 0, n1 = 0, mx = 0;
-    sweep_operand(x, n, part, nparts, [&](float v) {
+    sweep_operand(x, n, part, nparts, keep, [&](float v) {
         const uint32_t m = __float_as_uint(v) & 0x7FFFFFFFu;
         const bool ok = valid_mag(m);
         nz += ok;
@@ -224,8 +227,8 @@ TCEC_DEV void stats1_part(const float* a, int64_t na, const float* b, int64_t nb
 
 __global__ void __launch_bounds__(kThreads) stats1_kernel(const float* a, int64_t na,
                                                           const float* b, int64_t nb,
-                                                          DevDecision* d, int nb_a) {
-    stats1_part(a, na, b, nb, d, nb_a, int(blockIdx.x), int(gridDim.x));
+                                                          DevDecision* d, int nb_a, int keep) {
+    stats1_part(a, na, b, nb, d, nb_a, int(blockIdx.x), int(gridDim.x), keep != 0);
 }
 
 
@@ -240,7 +243,7 @@ TCEC_DEV bool stage1_passes(unsigned long long nz, unsigned long long n1, unsign
 
 // stage 2 (precsel.cpp:34-45 via count_abs_ge): count of |x| >= 2^(e_max - target - 14)
 TCEC_DEV void stats2_part(const float* a, int64_t na, const float* b, int64_t nb, DevDecision* d,
-                          double t, int target, int always, int nb_a, int bid, int nblk) {
+                          double t, int target, int always, int nb_a, int bid, int nblk, bool keep) {
     const int op = bid < nb_a ? 0 : 1;
     const float* x = op ? b : a;
     const int64_t n = op ? nb : na;
@@ -265,7 +268,7 @@ TCEC_DEV void stats2_part(const float* a, int64_t na, const float* b, int64_t nb
     const uint32_t thr = thr_s;
     if (thr == 0) return;
     unsigned cnt = 0;
-    sweep_operand(x, n, part, nparts, [&](float v) {
+    sweep_operand(x, n, part, nparts, keep, [&](float v) {
         const uint32_t m = __float_as_uint(v) & 0x7FFFFFFFu;
         cnt += valid_mag(m) && m >= thr;
     });
@@ -274,11 +277,38 @@ TCEC_DEV void stats2_part(const float* a, int64_t na, const float* b, int64_t nb
     if (threadIdx.x == 0 && s) atomicAdd(&d->st[op].n2, s);
 }
 
-__global__ void __launch_bounds__(kThreads) stats2_kernel(const float* a, int64_t na,
+TCEC_DEV void select_body(DevDecision* d, double t, int target, int forced_scaled, int stage2_always);
+
+// select = 1: the last block to finish also runs the selection (one launch
+// and one dependent kernel start less per dispatch); it reads the decision
+// slot past L1 (thread 0 of every block read its stage-1 line at the start)
+__global__ void __launch_bounds__(kThreads, 8) stats2_kernel(const float* a, int64_t na,
                                                           const float* b, int64_t nb,
                                                           DevDecision* d, double t, int target,
-                                                          int always, int nb_a) {
-    stats2_part(a, na, b, nb, d, t, target, always, nb_a, int(blockIdx.x), int(gridDim.x));
+                                                          int always, int nb_a, int keep, int select,
+                                                          double sel_t, int forced_scaled) {
+    stats2_part(a, na, b, nb, d, t, target, always, nb_a, int(blockIdx.x), int(gridDim.x), keep != 0);
+    if (!select) return;
+    constexpr int kWords = int(sizeof(DevDecision) / 4);
+    __shared__ int last_s;
+    __shared__ __align__(16) unsigned dec_s[kWords];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();  // this block's n2 before its ticket
+        last_s = atomicAdd(&d->pad_, 1) == int(gridDim.x) - 1;
+    }
+    __syncthreads();
+    if (!last_s) return;
+    __threadfence();
+    if (int(threadIdx.x) < kWords) dec_s[threadIdx.x] = __ldcg(reinterpret_cast<const unsigned*>(d) + threadIdx.x);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        DevDecision* dd = reinterpret_cast<DevDecision*>(dec_s);
+        select_body(dd, sel_t, target, forced_scaled, 0);
+        dd->pad_ = 0;
+    }
+    __syncthreads();
+    if (int(threadIdx.x) < kWords) reinterpret_cast<unsigned*>(d)[threadIdx.x] = dec_s[threadIdx.x];
 }
 
 // finalize ExpStats, tolerance levels and the pair rule (precsel.cpp:95-135)
@@ -333,11 +363,6 @@ TCEC_DEV void select_body(DevDecision* d, double t, int target, int forced_scale
     }
 }
 
-__global__ void select_kernel(DevDecision* d, double t, int target, int forced_scaled,
-                              int stage2_always) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    select_body(d, t, target, forced_scaled, stage2_always);
-}
 
 // --------------------------------------------------------- operand prep
 
@@ -1986,22 +2011,32 @@ static void stats_grid(int64_t na, int64_t nb, const float* a, const float* b, i
     *total = std::max(1, eb ? tot : ba);
 }
 
+// L2 policy of the statistics sweeps: operands that fit in L2 next to their
+// preparation's output stay resident for the second sweep and the preparation
+// (TCEC_STATS_KEEP = 0 / 1 forces streaming / keeping)
+static int stats_keep(int64_t na, int64_t nb) {
+    static const int mode = [] {
+        const char* e = std::getenv("TCEC_STATS_KEEP");
+        return e ? std::atoi(e) : -1;
+    }();
+    if (mode >= 0) return mode ? 1 : 0;
+    return (na + nb) * 4 <= (int64_t(96) << 20) ? 1 : 0;
+}
+
 void launch_stats1(const float* a, int64_t na, const float* b, int64_t nb, DevDecision* d,
                    cudaStream_t s) {
     int total = 0, nb_a = 0;
     stats_grid(na, nb, a, b, &total, &nb_a);
-    stats1_kernel<<<total, kThreads, 0, s>>>(a, na, b, nb, d, nb_a);
+    stats1_kernel<<<total, kThreads, 0, s>>>(a, na, b, nb, d, nb_a, stats_keep(na, nb));
 }
 
 void launch_stats2(const float* a, int64_t na, const float* b, int64_t nb, DevDecision* d,
-                   double t, int target, int always, cudaStream_t s) {
+                   double t, int target, int always, cudaStream_t s, int select, double sel_t,
+                   int forced_scaled) {
     int total = 0, nb_a = 0;
     stats_grid(na, nb, a, b, &total, &nb_a);
-    stats2_kernel<<<total, kThreads, 0, s>>>(a, na, b, nb, d, t, target, always, nb_a);
-}
-
-void launch_select(DevDecision* d, double t, int target, int forced_scaled, cudaStream_t s) {
-    select_kernel<<<1, 32, 0, s>>>(d, t, target, forced_scaled, 0);
+    stats2_kernel<<<total, kThreads, 0, s>>>(a, na, b, nb, d, t, target, always, nb_a, stats_keep(na, nb),
+                                             select, sel_t, forced_scaled);
 }
 
 void launch_prep_a(const float* a, int64_t m, int64_t k, int64_t kp, void* hi, void* lo,

@@ -26,7 +26,7 @@ struct DevDecision {
     int level_a, level_b;       // ToleranceLevel, -1 = logic_error
     unsigned int overflow;      // split/quantize saturation (DispatchResult::overflow)
     unsigned int scale_overflow;  // ScaleOverflow (precsel.cpp:54-57)
-    int pad_;
+    int pad_;                   // stats2_kernel's block counter (0 between dispatches)
 };
 
 enum Kind : int { kKindFp16 = 0, kKindFp16Scaled = 1, kKindTf32 = 2, kKindFp32 = 3 };
@@ -44,11 +44,13 @@ void launch_add_sub(const float* a, const float* b, float* dst, int64_t n, int s
 // stage 1 over both operands (n_a / n_b real components; a null operand is skipped)
 void launch_stats1(const float* a, int64_t n_a, const float* b, int64_t n_b, DevDecision* d,
                    cudaStream_t s);
-// stage 2; mode 0 = staged (skip when stage 1 passes for t), 1 = always
+// stage 2; mode 0 = staged (skip when stage 1 passes for t), 1 = always.
+// select = 1: the selection (precsel.cpp:106-135) with threshold sel_t follows
+// in the same launch (forced_scaled = 1 for ForcedMode::fp16_tcec_scaled); it
+// uses the decision slot's pad_ as its block counter (zeroed with the slot).
 void launch_stats2(const float* a, int64_t n_a, const float* b, int64_t n_b, DevDecision* d,
-                   double t, int target, int always, cudaStream_t s);
-// selection (precsel.cpp:106-135); forced_scaled = 1 for ForcedMode::fp16_tcec_scaled
-void launch_select(DevDecision* d, double t, int target, int forced_scaled, cudaStream_t s);
+                   double t, int target, int always, cudaStream_t s, int select = 0,
+                   double sel_t = 0.0, int forced_scaled = 0);
 
 // ------------------------------------------------------- operand layouts
 // Matrix view of a permuted tensor (fused TTGT gather): element (r, c) of the
