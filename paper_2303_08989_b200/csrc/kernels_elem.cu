@@ -1450,6 +1450,105 @@ __global__ void __launch_bounds__(256, 2) cgemm_skinny_col_kernel(const float2* 
     }
 }
 
+// Column kernel with the long operand staged through shared memory by
+// cp.async (X2 chains, k >= 8).  ncu on the register-prefetch kernel above
+// ((16, 2^22, 64), 1.94 GHz): FMA pipe 75 % busy, 3.4 warps per scheduler
+// (128 registers), long-scoreboard the top stall -- one group of 8 B values in
+// flight per thread is not enough to cover the DRAM latency.  Here every thread
+// copies ITS OWN column's next groups (8 x 8 B each) into a private
+// shared-memory slice kSkStages - 1 groups ahead, so nothing is shared between
+// threads (no barrier, a per-thread cp.async.wait_group), the prefetch
+// registers are gone and the walk over 256-column chunks is one continuous
+// pipeline.  Same values into the same chains in the same order: bit-identical.
+constexpr size_t kSkGroupBytes = size_t(8) * 256 * sizeof(float2);  // one stage: 8 k x 256 columns
+
+TCEC_DEV void cp_async8(void* smem_dst, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+TCEC_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+TCEC_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int MX, bool VIEW, int kSkStages>
+__global__ void __launch_bounds__(256, 2) cgemm_skinny_col_async_kernel(const float2* __restrict__ a,
+                                                                     const float2* __restrict__ b,
+                                                                     float2* __restrict__ c, int m,
+                                                                     int64_t n, int k, const MatrixView view,
+                                                                     uint64_t mz) {
+    __shared__ __align__(16) float2 as[kSkinnyMaxK * MX];  // [kk][i]
+    __shared__ int64_t koff[VIEW ? kSkinnyMaxK : 1];
+    extern __shared__ __align__(16) float2 bst[];            // [stage][u][thread]
+    for (int t = threadIdx.x; t < k * MX; t += blockDim.x) {
+        const int kk = t / MX, i = t % MX;
+        as[t] = i < m ? a[i * k + kk] : make_float2(0.0f, 0.0f);
+    }
+    if (VIEW)
+        for (int t = threadIdx.x; t < k; t += blockDim.x) koff[t] = run_offset(view.rows, uint32_t(t));
+    __syncthreads();
+    const int tid = int(threadIdx.x);
+    const int G = k >> 3;  // full groups of 8 k (k >= 8)
+    const int64_t step = int64_t(gridDim.x) * blockDim.x;
+    auto col_ptr = [&](int64_t jj) { return VIEW ? b + run_offset(view.cols, uint32_t(jj)) : b + jj; };
+    auto bel = [&](const float2* bj, int kk) { return VIEW ? bj + koff[kk] : bj + int64_t(kk) * n; };
+    // producer state: the next (chunk, group) tile this thread copies
+    int it_g = 0, it_s = 0;
+    int64_t it_j = int64_t(blockIdx.x) * blockDim.x + tid;
+    const float2* it_bj = col_ptr(it_j < n ? it_j : 0);
+    auto issue_next = [&]() {
+        if (it_j < n) {
+            float2* dst = bst + size_t(it_s) * 8 * 256 + tid;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) cp_async8(dst + u * 256, bel(it_bj, 8 * it_g + u));
+        }
+        cp_async_commit();  // empty groups too: the count stays uniform
+        it_s = it_s + 1 == kSkStages ? 0 : it_s + 1;
+        if (++it_g == G) {
+            it_g = 0;
+            it_j += step;
+            it_bj = col_ptr(it_j < n ? it_j : 0);
+        }
+    };
+#pragma unroll
+    for (int s = 0; s < kSkStages - 1; ++s) issue_next();
+    int cs = 0;  // consumer stage
+#pragma unroll 1
+    for (int64_t j = int64_t(blockIdx.x) * blockDim.x + tid; j - tid < n; j += step) {
+        const bool live = j < n;
+        uint64_t q[MX][2];
+#pragma unroll
+        for (int i = 0; i < MX; ++i) q[i][0] = q[i][1] = 0;  // +0 pairs
+#pragma unroll 1
+        for (int g = 0; g < G; ++g) {
+            issue_next();
+            cp_async_wait<kSkStages - 1>();  // this thread's copies of the tile landed
+            const float2* bs = bst + size_t(cs) * 8 * 256 + tid;
+            if (live) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const float2 bv = bs[u * 256];
+                    skinny_mac_x2<MX>(as + (8 * g + u) * MX, bv.x, bv.y, q, mz);
+                }
+            }
+            cs = cs + 1 == kSkStages ? 0 : cs + 1;
+        }
+        if (live) {
+            const float2* bj = 8 * G < k ? col_ptr(j) : b;
+#pragma unroll 1
+            for (int kk = 8 * G; kk < k; ++kk) {
+                const float2 bv = __ldcs(bel(bj, kk));
+                skinny_mac_x2<MX>(as + kk * MX, bv.x, bv.y, q, mz);
+            }
+#pragma unroll
+            for (int i = 0; i < MX; ++i) {
+                if (i >= m) continue;
+                const float2 p12 = unpack2(q[i][0]), p34 = unpack2(q[i][1]);
+                __stcs(c + int64_t(i) * n + j, make_float2(__fsub_rn(p12.x, p12.y), __fadd_rn(p34.x, p34.y)));
+            }
+        }
+    }
+    cp_async_wait<0>();
+}
+
 // n <= MX: thread i owns row i of C.  GROUPED (k >= 8, MX <= 8): each warp
 // stages its 32 rows of A through shared memory eight k at a time and writes
 // its 32 x n block of C back the same way, so global loads and stores are
@@ -1570,6 +1669,40 @@ unsigned col_grid(int64_t n) {
     return unsigned(std::max<int64_t>(1, std::min<int64_t>(chunks, int64_t(per_sm) * sms)));
 }
 
+int skinny_view_stages() {
+    static const int st = [] {
+        const char* e = std::getenv("TCEC_SKINNY_VSTAGES");
+        const int v = e ? std::atoi(e) : 0;
+        return v >= 2 && v <= 4 ? v : 2;
+    }();
+    return st;
+}
+
+// TCEC_SKINNY_ASYNC=0: the register-prefetch column kernel (A/B)
+bool skinny_async_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("TCEC_SKINNY_ASYNC");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <int MX, bool VIEW, int S>
+unsigned col_async_grid(int64_t n) {
+    static const int per_sm = [] {
+        int nb = 0;
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, cgemm_skinny_col_async_kernel<MX, VIEW, S>, 256,
+                                                             S * kSkGroupBytes) == cudaSuccess && nb > 0
+                   ? nb
+                   : 2;
+    }();
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t chunks = (n + 255) / 256;
+    return unsigned(std::max<int64_t>(1, std::min<int64_t>(chunks, int64_t(per_sm) * sms)));
+}
+
 template <bool F64, int MX, bool VIEW = false>
 void launch_skinny_mx(const float2* a, const float2* b, float2* c, int64_t m, int64_t n, int64_t k,
                       cudaStream_t s, const MatrixView& view = MatrixView{}) {
@@ -1580,6 +1713,38 @@ void launch_skinny_mx(const float2* a, const float2* b, float2* c, int64_t m, in
             const int rows = int(std::min<int64_t>(MX, m - r0));
             // separate instantiations: the grouped loop's registers must not
             // lower the occupancy of the short-k kernel
+            if constexpr (!F64 && MX >= 8) {
+                if (k >= 8 && skinny_async_enabled()) {
+                    static std::atomic<uint64_t> attr{0};
+                    if (ensure_smem_attr(attr, [] {
+                            cudaError_t e = cudaSuccess;
+                            for (auto f : {cgemm_skinny_col_async_kernel<MX, VIEW, 2>,
+                                           cgemm_skinny_col_async_kernel<MX, VIEW, 3>,
+                                           cgemm_skinny_col_async_kernel<MX, VIEW, 4>})
+                                if (e == cudaSuccess)
+                                    e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                             int(4 * kSkGroupBytes));
+                            return e;
+                        }) == cudaSuccess) {
+                        const int st = VIEW ? skinny_view_stages() : 4;
+                        const float2* ar = a + r0 * k;
+                        float2* cr = c + r0 * n;
+                        if (st == 2)
+                            cgemm_skinny_col_async_kernel<MX, VIEW, 2><<<col_async_grid<MX, VIEW, 2>(n), 256,
+                                                                        2 * kSkGroupBytes, s>>>(
+                                ar, b, cr, rows, n, int(k), view, kNegZero2);
+                        else if (st == 3)
+                            cgemm_skinny_col_async_kernel<MX, VIEW, 3><<<col_async_grid<MX, VIEW, 3>(n), 256,
+                                                                        3 * kSkGroupBytes, s>>>(
+                                ar, b, cr, rows, n, int(k), view, kNegZero2);
+                        else
+                            cgemm_skinny_col_async_kernel<MX, VIEW, 4><<<col_async_grid<MX, VIEW, 4>(n), 256,
+                                                                        4 * kSkGroupBytes, s>>>(
+                                ar, b, cr, rows, n, int(k), view, kNegZero2);
+                        continue;
+                    }
+                }
+            }
             if (k >= 8)
                 cgemm_skinny_col_kernel<F64, MX, true, VIEW>
                     <<<col_grid<F64, MX, true, VIEW>(n), 256, 0, s>>>(

@@ -35,7 +35,7 @@ _, lines = net.contract(path, cfg, want_log=True)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 reps = 10
-s = torch.cuda.ExternalStream(h.stream_ptr()) if h.stream_ptr() else torch.cuda.current_stream()
+s = torch.cuda.ExternalStream(h.stream_ptr) if h.stream_ptr else torch.cuda.current_stream()
 e0.record(s)
 for _ in range(reps):
     net.contract(path, cfg)
