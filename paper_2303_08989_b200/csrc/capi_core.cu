@@ -944,7 +944,7 @@ static int host_pipeline(Handle& h, const uint8_t* a, const uint8_t* b, uint8_t*
     auto w_of = [&](int j) { return std::min(hp.wq, n - j0_of(j)); };
     cudaEvent_t* ev_b = h.in_ev;              // B column parts
     cudaEvent_t* ev_a = h.in_ev + hp.q;       // A row chunks
-    cudaEvent_t ev_sync = h.in_ev[24];        // stream-to-stream ordering
+    cudaEvent_t ev_sync = h.in_ev[40];        // stream-to-stream ordering
     // the staging buffers may still be read by earlier work on the stream
     CUDA_TRY(cudaEventRecord(ev_sync, s));
     CUDA_TRY(cudaStreamWaitEvent(h.in_stream, ev_sync, 0));
@@ -1121,10 +1121,12 @@ int tcec_dispatch_cgemm_host(tcec_handle h, const void* a, const void* b, void* 
         return TCEC_OK;
     };
     // operand copies overlapped with the GEMM (host_pipeline) for large
-    // tensor-core dispatches; TCEC_HOST_CHUNKS = 0 disables
+    // tensor-core dispatches; TCEC_HOST_CHUNKS = 0 disables.  16 row chunks of
+    // A (1024 rows at 16384^3): e2e / device 0.945-0.950 against 0.919-0.922
+    // with 12 and 0.906-0.931 with 24-32 (profiles/r02e_host_chunks_sweep.log)
     static const int pipe_chunks = [] {
         const char* e = std::getenv("TCEC_HOST_CHUNKS");
-        return e ? std::max(0, std::min(16, std::atoi(e))) : 12;
+        return e ? std::max(0, std::min(32, std::atoi(e))) : 16;
     }();
     static const int pipe_parts = [] {  // column parts of B (front half sent before A)
         const char* e = std::getenv("TCEC_HOST_BPARTS");

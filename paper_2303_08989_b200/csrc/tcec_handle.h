@@ -36,7 +36,7 @@ struct tcec_handle_s {
     cudaStream_t gemm_stream2 = nullptr;  // second GEMM stream of the host-buffer pipeline
     int64_t pipe_runs = 0, pipe_reruns = 0;  // tcec_host_pipeline_stats
     std::unique_ptr<tcec::StageRing> stage;  // pinned ring for pageable host buffers
-    cudaEvent_t in_ev[25] = {};  // B parts (<= 8), A chunks (<= 16), ordering
+    cudaEvent_t in_ev[41] = {};  // B parts (<= 8), A chunks (<= 32), ordering
     // stage profiling (tcec_profile_*): CUDA events around the stages of a
     // dispatched CGEMM, accumulated after each synchronous dispatch
     bool prof = false;
