@@ -281,7 +281,11 @@ def test_long_k_kernels_bit_exact(handle, orc, dev, shape):
 @pytest.mark.parametrize("shape", [(2, 4096, 2), (3, 5000, 7), (16, 8192, 32), (9, 4100, 1),
                                    (5000, 9, 31), (8192, 16, 1), (4096, 2, 2), (4097, 5, 17),
                                    (32, 5000, 8), (20, 4200, 100), (5000, 32, 128), (17, 4096, 64),
-                                   (4100, 8, 8), (6000, 3, 24), (4133, 7, 9), (4096, 4, 16), (4111, 2, 40)])
+                                   (4100, 8, 8), (6000, 3, 24), (4133, 7, 9), (4096, 4, 16), (4111, 2, 40),
+                                   # cp.async-staged column kernel (MX 8 / 16, k >= 8): ragged n, k % 8 != 0,
+                                   # rows below MX, and a persistent walk over many 256-column chunks
+                                   (8, 4099, 13), (6, 10001, 64), (12, 4500, 128), (16, 300001, 72),
+                                   (5, 200000, 8), (31, 9000, 17)])
 def test_skinny_kernels_bit_exact(handle, orc, dev, shape):
     """Irregular skinny shapes (k <= 128, one outer dim <= 32: PAPER.md:346-352)
     take the thread-per-column / thread-per-row kernels; the chains keep the
