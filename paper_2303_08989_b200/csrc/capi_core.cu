@@ -826,10 +826,9 @@ int tcec_dispatch_cgemm(tcec_handle h, const void* a, const void* b, void* c, in
                 hit = &slot;
             }
             if (graph) cudaGraphDestroy(graph);
-            if (!hit) {
-                cudaGetLastError();
-                if (rc) return rc;
-            }
+            // a capture that failed for any reason falls through to direct
+            // launches, which report a genuine error themselves
+            if (!hit) cudaGetLastError();
         } else {
             cudaGetLastError();
         }
