@@ -447,19 +447,23 @@ static int run_fold(tcec_network_s& net, const int* steps, int n_steps,
             cudaGraphExecDestroy(net.graph);
             net.graph = nullptr;
         }
+        // a capture or instantiation that fails for any reason falls back to
+        // direct launches (which report a genuine error themselves)
         cudaGraph_t g = nullptr;
         cudaError_t e = cudaStreamBeginCapture(h.stream, cudaStreamCaptureModeThreadLocal);
-        if (e != cudaSuccess) return cuda_error(e, "graph capture");
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return enqueue_fold(net, plan, cfg, dec, ws, hyb);
+        }
         const int rc = enqueue_fold(net, plan, cfg, dec, ws, hyb);
         e = cudaStreamEndCapture(h.stream, &g);
-        if (rc) {
-            if (g) cudaGraphDestroy(g);
-            return rc;
+        if (rc == TCEC_OK && e == cudaSuccess && g) e = cudaGraphInstantiate(&net.graph, g, 0);
+        if (g) cudaGraphDestroy(g);
+        if (rc != TCEC_OK || e != cudaSuccess || !net.graph) {
+            net.graph = nullptr;
+            cudaGetLastError();
+            return enqueue_fold(net, plan, cfg, dec, ws, hyb);
         }
-        if (e != cudaSuccess) return cuda_error(e, "graph capture end");
-        e = cudaGraphInstantiate(&net.graph, g, 0);
-        cudaGraphDestroy(g);
-        if (e != cudaSuccess) return cuda_error(e, "graph instantiate");
         net.graph_key = key;
     }
     const cudaError_t e = cudaGraphLaunch(net.graph, h.stream);
