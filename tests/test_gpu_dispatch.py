@@ -337,3 +337,37 @@ def test_host_buffers_pinned_or_pageable(handle, dev, shape, pinned):
     c_dev, res_d = handle.dispatch_cgemm(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev), pol)
     assert res_h.line == res_d.line
     assert np.array_equal(c_host.view(np.uint32), c_dev.cpu().numpy().view(np.uint32))
+
+
+def test_dispatch_decision_randomized_vs_oracle(handle, orc, dev):
+    """Randomised selection parity (precsel.cpp:225-322): random shapes, input
+    families, thresholds, targets, size gates and forced modes -- the device
+    DecisionRecord line, kind and shifts equal the oracle's for every draw."""
+    rng = np.random.default_rng(2303)
+    recipes = ["uniform", "tiny20", "huge20", "banded", "type3", "subnormal", "mixed40", "ones", "zeros"]
+    forced = [None] * 6 + ["FP32_REF", "FP64_ORACLE", "TF32TC", "FP16TC", "TF32TCEC", "FP16TCEC",
+                           "FP16TCEC_SCALED"]
+    for i in range(40):
+        m, n, k = (int(x) for x in rng.integers(1, 97, 3))
+        ra, rb = rng.choice(recipes, 2)
+        a = matrix_recipe(str(ra), m, k, 1000 + i)
+        b = matrix_recipe(str(rb), k, n, 2000 + i)
+        t = float(rng.choice([0.0, 1e-6, 0.05, 0.3, 1.0]))
+        target = int(rng.choice([0, 7, 14, 15, 20]))
+        gate = int(rng.choice([1, 8, 32, 64, 4096]))
+        gate32 = int(rng.choice([1, gate]))
+        force = forced[int(rng.integers(0, len(forced)))]
+        kw = dict(threshold_t=t, size_auto=gate, size_tf32=min(gate32, gate), target=target, force=force)
+        gkw = dict(threshold_t=t, size_auto=gate, size_tf32=min(gate32, gate), target_max_exponent=target,
+                   force=force)
+        try:
+            _, res = handle.dispatch_cgemm(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev),
+                                           _gpu_cfg(gkw))
+            got = (0, res.line, res.kind, res.scale_a, res.scale_b)
+        except Exception as e:  # noqa: BLE001 -- the reference's exceptions map to error codes
+            got = (type(e).__name__,)
+        rc, want = orc.dispatch_decision(a, b, O.make_config(**kw))
+        if rc == 0:
+            assert got == (0, want.line.decode(), want.kind, want.scale_a, want.scale_b), (i, kw, ra, rb, got)
+        else:
+            assert got[0] != 0, (i, kw, ra, rb, rc, got)
