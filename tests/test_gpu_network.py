@@ -470,3 +470,73 @@ def test_tc_step_view_gather_bit_identical(handle, case, tmp_path):
     assert np.array_equal(bits(got.data.view(np.float32)), bits(off.view(np.float32)))
     err = np.linalg.norm(got.data.astype(np.complex128) - ref) / np.linalg.norm(ref)
     assert err <= 5e-6, err
+
+
+def _random_network(rng, seed):
+    """Random connected tensor network: 4-7 tensors of rank <= 5, bonds of
+    extent 1-5 (size-1 and repeated extents included), a few open legs."""
+    nt = int(rng.integers(4, 8))
+    labels = [[] for _ in range(nt)]
+    dims = [[] for _ in range(nt)]
+    nb = 0
+
+    def bond(i, j, d):
+        nonlocal nb
+        nm = f"b{nb}"
+        nb += 1
+        labels[i].append(nm)
+        dims[i].append(d)
+        labels[j].append(nm)
+        dims[j].append(d)
+
+    for i in range(1, nt):  # connected: a random tree, then extra bonds
+        bond(int(rng.integers(0, i)), i, int(rng.integers(1, 6)))
+    for _ in range(int(rng.integers(1, 5))):
+        i, j = (int(x) for x in rng.choice(nt, 2, replace=False))
+        if len(labels[i]) < 5 and len(labels[j]) < 5:
+            bond(i, j, int(rng.integers(1, 6)))
+    for o in range(int(rng.integers(0, 3))):
+        i = int(rng.integers(0, nt))
+        labels[i].append(f"o{o}")
+        dims[i].append(int(rng.integers(1, 4)))
+    for i in range(nt):  # random axis order per tensor
+        perm = rng.permutation(len(labels[i]))
+        labels[i] = [labels[i][p] for p in perm]
+        dims[i] = [dims[i][p] for p in perm]
+    data = [matrix_recipe("uniform", 1, int(np.prod(d)) if d else 1, seed * 31 + i).reshape(-1)
+            for i, d in enumerate(dims)]
+    return NetworkSpec(labels=labels, dims=dims, data=data)
+
+
+def _random_path(rng, n):
+    live, nxt, path = list(range(n)), n, []
+    while len(live) > 1:
+        a, b = (int(x) for x in rng.choice(len(live), 2, replace=False))
+        ia, ib = live[a], live[b]
+        path.append((ia, ib))
+        live = [x for x in live if x not in (ia, ib)] + [nxt]
+        nxt += 1
+    return path
+
+
+@pytest.mark.parametrize("executor", [0, 1, 3])
+def test_random_networks_fp32_tier_bit_exact_vs_oracle_fold(handle, executor):
+    """Random networks and random contraction orders (ragged extents, size-1
+    bonds, open legs, shuffled axes -> every TTGT permute / fused-gather case
+    of small tensors) through each executor: the FP32 tier is bit-identical to
+    the oracle fold (network.cpp:149-177) and the decision-log lines match."""
+    rng = np.random.default_rng(90 + executor)
+    handle.set_executor(executor)
+    try:
+        for case in range(12):
+            spec = _random_network(rng, 100 * executor + case)
+            path = _random_path(rng, len(spec.labels))
+            net = Network(handle, spec)
+            got, lines = net.contract(path, BASELINE, want_log=True)
+            net.close()
+            wl, wd, want, want_lines = oracle_fold(spec, path, O.make_config(force="FP32_REF"))
+            assert list(got.labels) == list(wl), (case, got.labels, wl)
+            assert np.array_equal(bits(got.data.view(np.float32)), bits(np.asarray(want).view(np.float32))), case
+            assert lines == want_lines, case
+    finally:
+        handle.set_executor(0)
