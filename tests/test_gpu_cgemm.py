@@ -474,3 +474,35 @@ def test_pair_persistent_bit_identical_to_wide(handle, dev, shape, mode):
             handle.set_gemm_variant("auto")
     assert lines["wide_persistent"] == lines["pair_persistent"]
     assert np.array_equal(outs["wide_persistent"].view(np.uint32), outs["pair_persistent"].view(np.uint32))
+
+
+def test_randomized_shapes_variants_layouts_within_bar(handle, orc, dev):
+    """Random ragged shapes (tile edges, k not a multiple of any k-block) on
+    every tcgen05 variant and both operand layouts, FP16TCEC and TF32TCEC:
+    relative error vs the f64 cgemm_oracle within the reference's bar
+    (<= 4x the FP32_REF error, test_cgemm.cpp:64-66; 2e-6 floor for tiny k
+    where FP32_REF is exact)."""
+    rng = np.random.default_rng(989)
+    variants = ["auto", "pair", "single", "wide", "wide_persistent", "pair_persistent"]
+    try:
+        for i in range(10):
+            m, n = (int(x) for x in rng.integers(1, 700, 2))
+            k = int(rng.integers(1, 600))
+            a = matrix_recipe("uniform", m, k, 500 + i)
+            b = matrix_recipe("uniform", k, n, 600 + i)
+            ref = orc.cgemm_oracle(a, b)
+            den = np.linalg.norm(ref)
+            ad, bd = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+            c32, _ = handle.cgemm(ad, bd, "FP32_REF")
+            bar = max(4 * np.linalg.norm(c32.cpu().numpy().astype(np.complex128) - ref) / den, 2e-6)
+            for mode in ("FP16TCEC", "TF32TCEC"):
+                for layout in ("b", "a"):
+                    handle.set_operand_layout(layout)
+                    v = variants[i % len(variants)]
+                    handle.set_gemm_variant(v)
+                    c, _ = handle.cgemm(ad, bd, mode)
+                    err = np.linalg.norm(c.cpu().numpy().astype(np.complex128) - ref) / den
+                    assert err <= bar, ((m, n, k), mode, layout, v, err, bar)
+    finally:
+        handle.set_gemm_variant("auto")
+        handle.set_operand_layout("auto")
