@@ -448,10 +448,11 @@ def cgemm_headline(args, world, rank, local):
                          "ratio_vs_fp32": round(err / err32, 3) if err32 else None,
                          "sample": "16 random rows vs complex128"},
             "e2e": e2e,
-            # per AUTO dispatch: stats1, stats2, select, prep_a, prep_b and ONE
-            # tcgen05 GEMM (the wide kernel branches on the device decision),
-            # plus a cudaMemsetAsync of the decision slot
-            "gpu_launches": 6 * args.steps,
+            # per AUTO dispatch: stats1, stats2 (whose last block runs the
+            # selection), prep_a, prep_b and ONE tcgen05 GEMM (the wide kernel
+            # branches on the device decision), plus a cudaMemsetAsync of the
+            # decision slot
+            "gpu_launches": 5 * args.steps,
             "clocks": clk.summary(),
         }
         if cpu:
