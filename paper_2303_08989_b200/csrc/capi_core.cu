@@ -876,9 +876,24 @@ struct HostPipe {
     int64_t rows_per = 0, wq = 0;
 };
 
+// TCEC_HOST_SPEC_TF32=0: take the sample's decision as is (A/B)
+static bool host_spec_tf32() {
+    static const bool on = [] {
+        const char* e = std::getenv("TCEC_HOST_SPEC_TF32");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 static HostPipe plan_host_pipe(int64_t m, int64_t n, int chunks, int parts) {
     HostPipe hp;
-    hp.rows_per = round_up((m + chunks - 1) / chunks, 256);
+    // >= 1024-row chunks: smaller GEMM blocks (at m < 16384) leave SMs idle
+    static const int64_t min_rows = [] {
+        const char* e = std::getenv("TCEC_HOST_MINROWS");
+        const int v = e ? std::atoi(e) : 0;
+        return v > 0 ? int64_t(v) : int64_t(1024);
+    }();
+    hp.rows_per = std::max(round_up((m + chunks - 1) / chunks, 256), round_up(std::min(m, min_rows), 256));
     hp.nch = int((m + hp.rows_per - 1) / hp.rows_per);
     hp.q = int(std::max<int64_t>(1, std::min<int64_t>(parts, n / 256)));  // parts of >= 256 columns
     hp.wq = round_up((n + hp.q - 1) / hp.q, 128);  // even column offsets keep C blocks 16-B aligned
@@ -975,8 +990,10 @@ static int host_pipeline(Handle& h, const uint8_t* a, const uint8_t* b, uint8_t*
     const int64_t bfront = k * std::min(n, j0_of(hp.front));  // the packed front parts
     if (p.stats) {
         launch_stats1(fa, 2 * rows0 * k, fb, 2 * bfront, ds, s);
+        const float fa_frac = host_spec_tf32() ? float(double(rows0) / double(m)) : 0.0f;
+        const float fb_frac = host_spec_tf32() ? float(double(bfront) / double(k * n)) : 0.0f;
         launch_stats2(fa, 2 * rows0 * k, fb, 2 * bfront, ds, t, cfg.target_max_exponent, 0, s, 1,
-                      cfg.threshold_t, p.forced_scaled ? 1 : 0);
+                      cfg.threshold_t, p.forced_scaled ? 1 : 0, fa_frac, fb_frac);
         cudaMemcpyAsync(snap, ds, sizeof(DevDecision), cudaMemcpyDeviceToDevice, s);
     }
     TcecGemmArgs g = tc_gemm_args(h, p, ws, reinterpret_cast<float*>(dc), m, n, ds, false);

@@ -286,7 +286,8 @@ __global__ void __launch_bounds__(kThreads, 8) stats2_kernel(const float* a, int
                                                           const float* b, int64_t nb,
                                                           DevDecision* d, double t, int target,
                                                           int always, int nb_a, int keep, int select,
-                                                          double sel_t, int forced_scaled) {
+                                                          double sel_t, int forced_scaled, float spec_fa,
+                                                          float spec_fb) {
     stats2_part(a, na, b, nb, d, t, target, always, nb_a, int(blockIdx.x), int(gridDim.x), keep != 0);
     if (!select) return;
     constexpr int kWords = int(sizeof(DevDecision) / 4);
@@ -305,6 +306,28 @@ __global__ void __launch_bounds__(kThreads, 8) stats2_kernel(const float* a, int
     if (threadIdx.x == 0) {
         DevDecision* dd = reinterpret_cast<DevDecision*>(dec_s);
         select_body(dd, sel_t, target, forced_scaled, 0);
+        // spec_fa / spec_fb > 0: the operands are SAMPLES (these fractions of
+        // A and B) and the decision is the host pipeline's speculation.  At
+        // t = 0 an FP16 kind after stage 2 only says the sample has no
+        // component below 2^(e_max - target - 14).  Extrapolating the sample's
+        // count below 2^-14 (stage 1) with a flat density near zero, the whole
+        // operands are expected to hold (nz - n1) / f * 2^(e_max - target)
+        // such components; from 0.5 on, the speculation takes TF32.  Either
+        // way it is checked against the exact decision (rerun on mismatch).
+        if (spec_fa > 0.0f && spec_fb > 0.0f && !forced_scaled && sel_t == 0.0 && dd->kind >= 0 &&
+            dd->kind != kKindTf32 && (dd->st[0].stage2_evaluated || dd->st[1].stage2_evaluated)) {
+            double expect = 0.0;
+            for (int op = 0; op < 2; ++op) {
+                const DevStats& st = dd->st[op];
+                if (!st.e_max_valid) continue;
+                const double f = op ? double(spec_fb) : double(spec_fa);
+                expect += double(st.n_nonzero - st.n1) / f * ldexp(1.0, st.e_max - target);
+            }
+            if (expect >= 0.5) {
+                dd->kind = kKindTf32;
+                dd->scale_a = dd->scale_b = 0;
+            }
+        }
         dd->pad_ = 0;
     }
     __syncthreads();
@@ -2197,11 +2220,11 @@ void launch_stats1(const float* a, int64_t na, const float* b, int64_t nb, DevDe
 
 void launch_stats2(const float* a, int64_t na, const float* b, int64_t nb, DevDecision* d,
                    double t, int target, int always, cudaStream_t s, int select, double sel_t,
-                   int forced_scaled) {
+                   int forced_scaled, float spec_fa, float spec_fb) {
     int total = 0, nb_a = 0;
     stats_grid(na, nb, a, b, &total, &nb_a);
     stats2_kernel<<<total, kThreads, 0, s>>>(a, na, b, nb, d, t, target, always, nb_a, stats_keep(na, nb),
-                                             select, sel_t, forced_scaled);
+                                             select, sel_t, forced_scaled, spec_fa, spec_fb);
 }
 
 void launch_prep_a(const float* a, int64_t m, int64_t k, int64_t kp, void* hi, void* lo,

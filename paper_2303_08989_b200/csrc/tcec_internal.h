@@ -48,9 +48,13 @@ void launch_stats1(const float* a, int64_t n_a, const float* b, int64_t n_b, Dev
 // select = 1: the selection (precsel.cpp:106-135) with threshold sel_t follows
 // in the same launch (forced_scaled = 1 for ForcedMode::fp16_tcec_scaled); it
 // uses the decision slot's pad_ as its block counter (zeroed with the slot).
+// spec_fa / spec_fb > 0: the operands are these fractions of larger ones
+// (the host pipeline's speculative decision); at t = 0 an FP16 kind reached
+// through stage 2 becomes TF32 when the whole operands are expected to hold a
+// component below the stage-2 threshold (see stats2_kernel).
 void launch_stats2(const float* a, int64_t n_a, const float* b, int64_t n_b, DevDecision* d,
                    double t, int target, int always, cudaStream_t s, int select = 0,
-                   double sel_t = 0.0, int forced_scaled = 0);
+                   double sel_t = 0.0, int forced_scaled = 0, float spec_fa = 0.0f, float spec_fb = 0.0f);
 
 // ------------------------------------------------------- operand layouts
 // Matrix view of a permuted tensor (fused TTGT gather): element (r, c) of the
