@@ -159,6 +159,7 @@ def test_host_buffer_row_chunks_match_the_device_path(handle, dev):
 
 @pytest.mark.parametrize("shape", [(16384, 768, 384), (8448, 2304, 640)])
 @pytest.mark.parametrize("case", ["uniform", "late_outlier", "late_tiny", "first_outlier", "late_b_outlier",
+                                  "sample_predicts_tiny",
                                   "FP16TCEC", "TF32TCEC", "FP16TCEC_SCALED", "fp16_overflow"])
 def test_host_pipeline_matches_the_device_path(handle, dev, case, shape):
     """Large host-buffer dispatches copy A in row chunks and start each chunk's
@@ -179,6 +180,14 @@ def test_host_pipeline_matches_the_device_path(handle, dev, case, shape):
         a[3, 2] = 1.0e6
     elif case == "late_b_outlier":
         b[k // 2, n - 3] = 2.0e9 - 1.0e9j
+    elif case == "sample_predicts_tiny":
+        # the first A chunk (the speculation's sample, 1024 rows) holds many
+        # components in [2^-20, 2^-14) but none below the stage-2 threshold;
+        # later rows hold some below it (exact: TF32).  The density
+        # extrapolation must predict TF32 -> no rerun.
+        sel = g.random((1024, k)) < 0.1
+        a[:1024][sel] = np.complex64(2.0 ** -17 + 2.0 ** -17 * 1j)
+        a[m - 7, 5] = np.complex64(2.0 ** -35)
     elif case == "fp16_overflow":
         a[m - 100, 3] = 9.0e4
         pol = make_config(force="FP16TCEC")
@@ -190,6 +199,8 @@ def test_host_pipeline_matches_the_device_path(handle, dev, case, shape):
     assert runs1 == runs0 + 1  # m >= 8192 on the tensor-core tier: pipelined
     if case in ("late_outlier", "late_b_outlier"):
         assert reruns1 == reruns0 + 1  # the first parts could not predict the scale
+    if case == "sample_predicts_tiny":
+        assert reruns1 == reruns0  # the density extrapolation predicted the exact decision
     c_dev, res_d = handle.dispatch_cgemm(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev), pol)
     if case in ("uniform", "late_outlier", "late_tiny", "late_b_outlier"):
         assert res_d.has_stats  # the AUTO tier: decided from statistics on the device
