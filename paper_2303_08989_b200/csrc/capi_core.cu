@@ -1178,6 +1178,15 @@ int tcec_dispatch_cgemm_host(tcec_handle h, const void* a, const void* b, void* 
             merged.scale_overflow = ds.scale_overflow;
             return finish_dispatch(p, merged, m, n, k, res);
         }
+        if (std::getenv("TCEC_DEBUG_RERUN"))
+            std::fprintf(stderr,
+                         "rerun: exact kind %d sa %d sb %d ovf %u sovf %u (e_max %d/%d n1 %llu/%llu nz %llu/%llu n2 %llu/%llu) | "
+                         "spec kind %d sa %d sb %d ovf %u sovf %u (e_max %d/%d n1 %llu/%llu nz %llu/%llu n2 %llu/%llu)\n",
+                         dr.kind, dr.scale_a, dr.scale_b, dr.overflow, dr.scale_overflow, dr.st[0].e_max,
+                         dr.st[1].e_max, dr.st[0].n1, dr.st[1].n1, dr.st[0].n_nonzero, dr.st[1].n_nonzero,
+                         dr.st[0].n2, dr.st[1].n2, snap.kind, snap.scale_a, snap.scale_b, snap.overflow,
+                         snap.scale_overflow, snap.st[0].e_max, snap.st[1].e_max, snap.st[0].n1, snap.st[1].n1,
+                         snap.st[0].n_nonzero, snap.st[1].n_nonzero, snap.st[0].n2, snap.st[1].n2);
         // the first chunks were not representative: plain path on the resident A
         // and a row-major copy of B (the staging holds it packed by column part)
         ctx.used = 0;

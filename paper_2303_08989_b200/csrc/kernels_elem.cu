@@ -241,9 +241,14 @@ TCEC_DEV bool stage1_passes(unsigned long long nz, unsigned long long n1, unsign
     return max_bits == 0 || exponent_of_bits(max_bits) <= target;
 }
 
+// binades above the stage-2 threshold whose sample count feeds the host
+// pipeline's speculation (5: above the 2^-24 grid of float32 uniforms in [-1, 1])
+constexpr int kSpecBinades = 5;
+
 // stage 2 (precsel.cpp:34-45 via count_abs_ge): count of |x| >= 2^(e_max - target - 14)
 TCEC_DEV void stats2_part(const float* a, int64_t na, const float* b, int64_t nb, DevDecision* d,
-                          double t, int target, int always, int nb_a, int bid, int nblk, bool keep) {
+                          double t, int target, int always, int nb_a, int bid, int nblk, bool keep,
+                          bool spec = false) {
     const int op = bid < nb_a ? 0 : 1;
     const float* x = op ? b : a;
     const int64_t n = op ? nb : na;
@@ -253,28 +258,41 @@ TCEC_DEV void stats2_part(const float* a, int64_t na, const float* b, int64_t nb
     // one thread reads the stage-1 statistics and derives the threshold
     // (every thread reading them put ~2.4 M same-address loads per 66 MB
     // sweep in front of the data stream: 2x the stage-1 time at 2^24 elements)
-    __shared__ uint32_t thr_s;
+    __shared__ uint32_t thr_s, thr_hi_s;
     if (threadIdx.x == 0) {
         const DevStats st = d->st[op];
-        uint32_t th = 0;  // 0: this operand needs no stage 2 (stage 1 passed, or no e_max: n2 = 0)
+        uint32_t th = 0, th_hi = 0;  // 0: this operand needs no stage 2 (stage 1 passed, or no e_max: n2 = 0)
         if ((always || !stage1_passes(st.n_nonzero, st.n1, st.max_bits, t, target)) && st.max_bits != 0) {
             const int w = exponent_of_bits(st.max_bits) - (target + 14);
             // ldexp(1.0f, w): a normal, a subnormal power of two, or 0 (all nonzero pass)
-            th = w >= -126 ? uint32_t(w + 127) << 23 : (w >= -149 ? 1u << (w + 149) : 1u);
+            auto pow2_bits = [](int e) -> uint32_t {
+                return e >= -126 ? (e > 127 ? 0x7F800000u : uint32_t(e + 127) << 23)
+                                 : (e >= -149 ? 1u << (e + 149) : 1u);
+            };
+            th = pow2_bits(w);
+            th_hi = pow2_bits(w + kSpecBinades);
         }
         thr_s = th;
+        thr_hi_s = th_hi;
     }
     __syncthreads();
-    const uint32_t thr = thr_s;
+    const uint32_t thr = thr_s, thr_hi = thr_hi_s;
     if (thr == 0) return;
-    unsigned cnt = 0;
+    unsigned cnt = 0, lo = 0;
     sweep_operand(x, n, part, nparts, keep, [&](float v) {
         const uint32_t m = __float_as_uint(v) & 0x7FFFFFFFu;
         cnt += valid_mag(m) && m >= thr;
+        if (spec) lo += valid_mag(m) && m < thr_hi;
     });
     __shared__ unsigned long long red64[kThreads / 32];
     const unsigned long long s = block_sum<unsigned long long>(cnt, red64);
     if (threadIdx.x == 0 && s) atomicAdd(&d->st[op].n2, s);
+    if (spec) {
+        // speculation only: components below 2^(w + kSpecBinades), kept in the
+        // slot's otherwise unused n_total (the host reports n_total itself)
+        const unsigned long long sl = block_sum<unsigned long long>(lo, red64);
+        if (threadIdx.x == 0 && sl) atomicAdd(&d->st[op].n_total, sl);
+    }
 }
 
 TCEC_DEV void select_body(DevDecision* d, double t, int target, int forced_scaled, int stage2_always);
@@ -288,7 +306,8 @@ __global__ void __launch_bounds__(kThreads, 8) stats2_kernel(const float* a, int
                                                           int always, int nb_a, int keep, int select,
                                                           double sel_t, int forced_scaled, float spec_fa,
                                                           float spec_fb) {
-    stats2_part(a, na, b, nb, d, t, target, always, nb_a, int(blockIdx.x), int(gridDim.x), keep != 0);
+    stats2_part(a, na, b, nb, d, t, target, always, nb_a, int(blockIdx.x), int(gridDim.x), keep != 0,
+                spec_fa > 0.0f && spec_fb > 0.0f);
     if (!select) return;
     constexpr int kWords = int(sizeof(DevDecision) / 4);
     __shared__ int last_s;
@@ -309,23 +328,39 @@ __global__ void __launch_bounds__(kThreads, 8) stats2_kernel(const float* a, int
         // spec_fa / spec_fb > 0: the operands are SAMPLES (these fractions of
         // A and B) and the decision is the host pipeline's speculation.  At
         // t = 0 an FP16 kind after stage 2 only says the sample has no
-        // component below 2^(e_max - target - 14).  Extrapolating the sample's
-        // count below 2^-14 (stage 1) with a flat density near zero, the whole
-        // operands are expected to hold (nz - n1) / f * 2^(e_max - target)
-        // such components; from 0.5 on, the speculation takes TF32.  Either
-        // way it is checked against the exact decision (rerun on mismatch).
+        // component below the threshold 2^w, w = e_max - target - 14.  The
+        // sample's count below 2^(w + kSpecBinades), extrapolated with a flat
+        // density near zero, expects count / f / 2^kSpecBinades such
+        // components in the whole operands; from 0.5 on, the speculation takes
+        // TF32.  (Data on a coarse grid -- float32 uniforms have no magnitude
+        // below 2^-23 -- shows no count there and keeps FP16.)  Either way the
+        // speculation is checked against the exact decision (rerun on mismatch).
         if (spec_fa > 0.0f && spec_fb > 0.0f && !forced_scaled && sel_t == 0.0 && dd->kind >= 0 &&
             dd->kind != kKindTf32 && (dd->st[0].stage2_evaluated || dd->st[1].stage2_evaluated)) {
             double expect = 0.0;
             for (int op = 0; op < 2; ++op) {
                 const DevStats& st = dd->st[op];
-                if (!st.e_max_valid) continue;
                 const double f = op ? double(spec_fb) : double(spec_fa);
-                expect += double(st.n_nonzero - st.n1) / f * ldexp(1.0, st.e_max - target);
+                expect += double(st.n_total) / f / double(1 << kSpecBinades);
             }
             if (expect >= 0.5) {
                 dd->kind = kKindTf32;
                 dd->scale_a = dd->scale_b = 0;
+            }
+        }
+        // the scaled kind's shifts come from e_max, a maximum: a sample whose
+        // largest magnitude sits at the very top of its binade (uniform data in
+        // [-1, 1], whose whole operand holds exact 1.0s) predicts the next
+        // binade for the whole operand
+        if (spec_fa > 0.0f && spec_fb > 0.0f && dd->kind == kKindFp16Scaled) {
+            for (int op = 0; op < 2; ++op) {
+                const DevStats& st = dd->st[op];
+                const float f = op ? spec_fb : spec_fa;
+                if (st.e_max_valid && f <= 0.5f && (st.max_bits & 0x7FFFFFu) >= 0x7FF800u &&
+                    st.max_bits < 0x7F000000u) {
+                    if (op) dd->scale_b -= 1;
+                    else dd->scale_a -= 1;
+                }
             }
         }
         dd->pad_ = 0;

@@ -182,11 +182,11 @@ def test_host_pipeline_matches_the_device_path(handle, dev, case, shape):
         b[k // 2, n - 3] = 2.0e9 - 1.0e9j
     elif case == "sample_predicts_tiny":
         # the first A chunk (the speculation's sample, 1024 rows) holds many
-        # components in [2^-20, 2^-14) but none below the stage-2 threshold;
-        # later rows hold some below it (exact: TF32).  The density
-        # extrapolation must predict TF32 -> no rerun.
+        # components just above the stage-2 threshold 2^-29 (2^-26 < 2^(-29 + 5))
+        # but none below it; later rows hold some below it (exact: TF32).  The
+        # density extrapolation must predict TF32 -> no rerun.
         sel = g.random((1024, k)) < 0.1
-        a[:1024][sel] = np.complex64(2.0 ** -17 + 2.0 ** -17 * 1j)
+        a[:1024][sel] = np.complex64(2.0 ** -26 + 2.0 ** -26 * 1j)
         a[m - 7, 5] = np.complex64(2.0 ** -35)
     elif case == "fp16_overflow":
         a[m - 100, 3] = 9.0e4
